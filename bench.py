@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark of the spliced-KV attention hot path (BASELINE.json).
+
+Default workload = BASELINE config 2 (configs[1]): 7B-shaped attention —
+32 q-heads, 8 kv-heads (GQA), d_head 128, bf16 KV — over a spliced cache of
+4096 cloud-prompt + 512 edge-private + 1 generated (self) token per request,
+private pages per request, batch 32, one decode query row per request.
+A "step" = one spliced-attention pass of the whole batch through one layer
+(all heads) = 32 tokens. Synthetic SplitMix64 U(-1,1) inputs (seeds q 21,
+K 22, V 23), no checkpoint.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun: every rank serves its own batch of 32
+requests (replicas, weak scaling — config 2 does not shard). Prints one JSON
+line on rank 0. `--impl reference` times the reference's own CPU
+implementation (oracle/_ref: the unmodified reference sources) of the same
+workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spliced-KV attention tokens/s & HBM GB/s vs roofline; verify-step p50 latency"
+
+# Config 2 shape.
+B, HQ, HKV, D, P = 32, 32, 8, 128, 64
+CLOUD, EDGE, SELF = 4096, 512, 1
+SEQ = CLOUD + EDGE + SELF
+PAGES_PER_REQ = CLOUD // P + EDGE // P + 1
+ALG_BYTES = B * SEQ * 2 * HKV * D * 2  # every unique K/V byte once = 603,979,776
+SEED_Q, SEED_K, SEED_V = 21, 22, 23
+
+WORKLOAD = ("cfg2: 7B-shaped spliced decode, Hq=32 Hkv=8 d=128 bf16, 4096 cloud + 512 edge "
+            "+ 1 self KV per request (private pages), batch 32, n_q=1")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _poll(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._poll, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_requests_table(SpliceTable, pool, batch):
+    table = SpliceTable(batch, P)
+    for b in range(batch):
+        base = b * PAGES_PER_REQ
+        pages = list(range(base, base + PAGES_PER_REQ))
+        table.append(b, 0, 0, CLOUD, pages[:CLOUD // P])
+        table.append(b, 1, CLOUD, EDGE, pages[CLOUD // P:CLOUD // P + EDGE // P])
+        table.append(b, 2, CLOUD + EDGE, SELF, pages[-1:])
+        table.q_pos[b] = SEQ - 1
+    return table
+
+
+def host_batch_for(requests, k_host, v_host, q_host):
+    """oracle.HostSpliceBatch of the given request subset (for the CPU legs)."""
+    import numpy as np
+    from oracle import oracle as O
+    n = len(requests)
+    segs, pt, indptr = [], [], [0]
+    for i, b in enumerate(requests):
+        base = i * PAGES_PER_REQ
+        segs += [(0, CLOUD, 0, len(pt)), (1, EDGE, CLOUD, len(pt) + CLOUD // P),
+                 (2, SELF, CLOUD + EDGE, len(pt) + CLOUD // P + EDGE // P)]
+        pt += list(range(base, base + PAGES_PER_REQ))
+        indptr.append(len(segs))
+    return O.HostSpliceBatch(
+        O.DT_BF16, HKV, HQ, D, P, np.ascontiguousarray(k_host), np.ascontiguousarray(v_host),
+        np.array(indptr, np.int64), np.array(segs, dtype=O.SEGMENT_DTYPE),
+        np.array(pt, np.int32), np.full(n, SEQ - 1, np.int64), O.DT_BF16,
+        np.ascontiguousarray(q_host), 1)
+
+
+def cpu_reference_rate(sb, threads, min_seconds=10.0, max_seconds=30.0):
+    """Times the reference attention block (oracle/_ref) over all units of sb
+    on `threads` host threads; returns (tokens/s, seconds, units)."""
+    from oracle import oracle as O
+    cache = O.RefBatchCache(sb)
+    units_per_pass = sb.batch * sb.n_q_heads
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        cache.attention(n_threads=threads)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= min_seconds or el * (passes + 1) / passes > max_seconds:
+            break
+    tokens = passes * units_per_pass / sb.n_q_heads
+    return tokens / el, el, passes * units_per_pass
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the same
+    workload on the host cores (rank 0 only)."""
+    import numpy as np
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    n_req = max(1, min(B, threads // 4))  # bounded sample per step
+    per_pool = n_req * PAGES_PER_REQ * HKV * P * D
+    k_host = O.fill_uniform(O.DT_BF16, per_pool, SEED_K).reshape(-1, HKV, P, D)
+    v_host = O.fill_uniform(O.DT_BF16, per_pool, SEED_V).reshape(-1, HKV, P, D)
+    q_host = O.fill_uniform(O.DT_BF16, n_req * HQ * D, SEED_Q).reshape(n_req, 1, HQ, D)
+    sb = host_batch_for(list(range(n_req)), k_host, v_host, q_host)
+    cache = O.RefBatchCache(sb)
+    for _ in range(args.warmup):
+        cache.attention(n_threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cache.attention(n_threads=threads)
+        times.append(time.perf_counter() - t0)
+    step_s = sum(times) / len(times)
+    value = n_req / step_s  # one token per request per step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample_requests_per_step": n_req},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+                         "kind": "reference",
+                         "sample": f"{n_req} of 32 requests x 32 heads per step (all segments), "
+                                   "reference attention block (partial_attention per segment + "
+                                   "merge) in fp64 from oracle/_ref"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2504_11729_b200 import _capi
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splice import KVPool, SpliceTable, SplicedAttention
+
+    h = Handle(local_rank)
+    stream = torch.cuda.current_stream()
+    num_pages = B * PAGES_PER_REQ
+    pool = KVPool(num_pages, HKV, D, P, dtype="bf16", device=local_rank)
+    lib = _capi.lib()
+    sp = stream.cuda_stream
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, pool.k.data_ptr(), pool.k.numel(),
+                                    SEED_K, -1.0, 1.0, sp))
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, pool.v.data_ptr(), pool.v.numel(),
+                                    SEED_V, -1.0, 1.0, sp))
+    q = torch.empty((B, 1, HQ, D), dtype=torch.bfloat16, device="cuda")
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, q.data_ptr(), q.numel(), SEED_Q,
+                                    -1.0, 1.0, sp))
+    table = build_requests_table(SpliceTable, pool, B)
+    attn = SplicedAttention(pool, table, HQ, 1, handle=h)
+    o = torch.empty_like(q)
+    lse = torch.empty((B, 1, HQ), dtype=torch.float32, device="cuda")
+
+    def step():
+        attn(q, o=o, lse=lse, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ------------------------------------------------------ device timing --
+    with ClockSampler(local_rank) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = h.launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        launches = h.launch_count() - l0
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ----------------------------------------------------- end-to-end (host) --
+    # Per step, through the public C-ABI: H2D of the step's query rows and the
+    # new (self) token's K/V rows from pinned host memory, ep_kv_append into
+    # the generated page slot, ep_spliced_attention, D2H of the output rows.
+    q_host = q.cpu().pin_memory()
+    kv_rows = torch.empty((2, B, HKV, D), dtype=torch.bfloat16)
+    kv_rows[0] = pool.k[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
+    kv_rows[1] = pool.v[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
+    kv_host = kv_rows.pin_memory()
+    o_host = torch.empty_like(o, device="cpu").pin_memory()
+    q_dev = torch.empty_like(q)
+    kv_dev = torch.empty_like(kv_host, device="cuda")
+    dst_page = torch.tensor([b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)],
+                            dtype=torch.int32, device="cuda")
+    dst_slot = torch.zeros(B, dtype=torch.int32, device="cuda")
+    pd = pool.desc()
+    import ctypes as C
+
+    def e2e_step():
+        q_dev.copy_(q_host, non_blocking=True)
+        kv_dev.copy_(kv_host, non_blocking=True)
+        _capi.check(lib.ep_kv_append(h.ptr, C.byref(pd), B, dst_page.data_ptr(),
+                                     dst_slot.data_ptr(), kv_dev[0].data_ptr(),
+                                     kv_dev[1].data_ptr(), sp))
+        attn(q_dev, o=o, lse=lse, stream=stream)
+        o_host.copy_(o, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    ok = bool(torch.equal(o_host.to("cuda"), o))
+
+    tokens_per_step = B * world
+    value = tokens_per_step / (ms / 1e3)
+    peak, peak_kind = peaks()
+    achieved = ALG_BYTES / (ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("cfg2_decode_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    n_ctas, n_items, n_pages = attn.info()
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": SEQ,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (604 MB of KV per step > 126 MB), no flush",
+                   "plan": {"ctas": n_ctas, "work_items": n_items, "pages": n_pages}},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "peak_kind": peak_kind,
+                     "note": "algorithmic bytes = 2*Hkv*d*2 B x 4609 keys x 32 requests per "
+                             "step; time = K1 decode + K2 merge per step (CUDA events)",
+                     "frac_of_8tbs_nominal": achieved / 8000.0},
+        "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": q.numel() * 2 + kv_host.numel() * 2,
+                "d2h_bytes_per_step": o.numel() * 2, "ms_per_step": ms_e2e,
+                "result_check": ok},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_req = 4
+        pg = n_req * PAGES_PER_REQ
+        sb = host_batch_for(list(range(n_req)),
+                            pool.k[:pg].view(torch.int16).cpu().numpy().view(np.uint16),
+                            pool.v[:pg].view(torch.int16).cpu().numpy().view(np.uint16),
+                            q[:n_req].view(torch.int16).cpu().numpy().view(np.uint16))
+        rate, secs, units = cpu_reference_rate(sb, threads)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"requests 0-3 of the same workload (128 (request, head) units per pass, "
+                      f"{units} units in {secs:.1f} s), reference attention block in fp64 "
+                      "(oracle/_ref, unmodified reference sources)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

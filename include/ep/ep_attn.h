@@ -1,0 +1,187 @@
+/*
+ * ep_attn.h — C-ABI of the B200 spliced-KV attention library (libep_b200.so).
+ *
+ * This is the drop-in boundary for EdgePrompt's attention/splice path. The
+ * reference exposes it as C++ (namespace edgeprompt) in
+ *   /root/reference/proj/core/include/edgeprompt/attention.hpp:13-52
+ *   /root/reference/proj/core/include/edgeprompt/cache.hpp:11-61
+ * and the reference's link-level swap point is attention.cpp in
+ * proj/core/CMakeLists.txt:1-14. Every entry point below names the reference
+ * interface it replaces. Plain pointers and sizes only; no CUDA or torch types
+ * (streams are passed as void* = cudaStream_t). No exceptions cross the ABI:
+ * every call returns an ep_status and sets a thread-local message readable with
+ * ep_last_error().
+ *
+ * Ownership: the caller owns every host and device buffer passed in. The
+ * library allocates only inside objects it creates (ep_handle, ep_plan,
+ * ep_cache) and frees them in the matching destroy call.
+ *
+ * Threading: an ep_handle may be used by one host thread at a time; separate
+ * handles are independent. Device entry points (*_dev, ep_spliced_*) are
+ * stream-ordered and asynchronous; host-buffer entry points (*_f64) are
+ * synchronous, like the reference functions they replace.
+ */
+#ifndef EP_ATTN_H
+#define EP_ATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EP_ABI_VERSION 1
+
+typedef enum ep_status {
+    EP_OK = 0,
+    EP_EINVAL = 1,       /* std::invalid_argument in the reference (attention.cpp:14-25, :117) */
+    EP_EMASKED = 2,      /* std::domain_error: a row sees no key (attention.cpp:52-56, :150-153) */
+    EP_ECUDA = 3,        /* CUDA runtime / launch failure */
+    EP_ENCCL = 4,        /* NCCL failure (split-KV combine) */
+    EP_ENOMEM = 5,       /* device or host allocation failed */
+    EP_EUNSUPPORTED = 6  /* shape/dtype combination without a kernel instance */
+} ep_status;
+
+/* Numbering matches oracle/ep_oracle.h (EPO_DT_*). bf16 is raw uint16 storage. */
+typedef enum ep_dtype { EP_F32 = 0, EP_BF16 = 1, EP_F64 = 2 } ep_dtype;
+
+typedef struct ep_context* ep_handle;
+typedef struct ep_plan_s* ep_plan;
+typedef void* ep_stream; /* cudaStream_t; NULL = legacy default stream */
+
+int ep_abi_version(void);
+const char* ep_last_error(void);
+
+/* Binds to a CUDA device and creates the per-handle workspace. */
+int ep_create(int device, ep_handle* out);
+int ep_destroy(ep_handle h);
+
+/* ==================================================================== */
+/* 1. Drop-in, host buffers, fp64 (synchronous). Replaces attention.cpp. */
+/*    Row-major, leading dimension = d. q [n_q x d], k/v [n_keys x d],  */
+/*    out [n_q x d], lse [n_q] (natural log; -inf for masked rows).     */
+/* ==================================================================== */
+
+/* edgeprompt::partial_attention (attention.hpp:39-40, attention.cpp:80-114) */
+int ep_partial_attention_f64(ep_handle h, const double* q, size_t n_q, const double* k,
+                             const double* v, size_t n_keys, size_t d, size_t query_offset,
+                             size_t key_offset, double* out, double* lse);
+
+/* edgeprompt::full_attention (attention.hpp:35, attention.cpp:45-78).
+ * EP_EMASKED if any row has no visible key. */
+int ep_full_attention_f64(ep_handle h, const double* q, size_t n_q, const double* k,
+                          const double* v, size_t n_keys, size_t d, size_t query_offset,
+                          size_t key_offset, double* out);
+
+/* edgeprompt::merge_partials (attention.hpp:52, attention.cpp:116-145).
+ * outs[p] -> [n_q x d], lses[p] -> [n_q]. EP_EINVAL when n_parts == 0. */
+int ep_merge_partials_f64(ep_handle h, size_t n_parts, const double* const* outs,
+                          const double* const* lses, size_t n_q, size_t d, double* out,
+                          double* lse);
+
+/* edgeprompt::fuse_partials (attention.hpp:47, attention.cpp:147-156).
+ * EP_EMASKED when some row is masked in every part. */
+int ep_fuse_partials_f64(ep_handle h, size_t n_parts, const double* const* outs,
+                         const double* const* lses, size_t n_q, size_t d, double* out);
+
+/* ==================================================================== */
+/* 2. Device buffers, stream-ordered. Same math as section 1 on device  */
+/*    pointers; dt = EP_F64 or EP_F32 (q, k, v, out and lse share dt).   */
+/* ==================================================================== */
+
+int ep_partial_attention_dev(ep_handle h, ep_dtype dt, const void* q, size_t ldq, size_t n_q,
+                             const void* k, size_t ldk, const void* v, size_t ldv,
+                             size_t n_keys, size_t d, size_t query_offset, size_t key_offset,
+                             void* out, size_t ldo, void* lse, ep_stream stream);
+
+/* K2: LSE merge of n_parts partials in part order. outs: [n_parts][rows][d],
+ * lses: [n_parts][rows]; out [rows][d], lse [rows]. dt = EP_F64 or EP_F32. */
+int ep_merge_partials_dev(ep_handle h, ep_dtype dt, size_t n_parts, const void* outs,
+                          const void* lses, size_t rows, size_t d, void* out, void* lse,
+                          ep_stream stream);
+
+/* ==================================================================== */
+/* 3. Paged splice table (cache.hpp:11-61 made device-resident).        */
+/* ==================================================================== */
+
+/* One KV segment of one request (KVSegment, cache.hpp:18-28): `len` tokens
+ * at absolute positions [pos_offset, pos_offset+len), stored in pages
+ * page_table[page_off ...], filling each page from slot 0. Pages may be
+ * shared between requests (a cloud prompt is stored once). */
+typedef struct ep_segment {
+    int32_t origin;     /* 0 cloud, 1 edge, 2 generated (SegmentOrigin, cache.hpp:11) */
+    int32_t len;
+    int64_t pos_offset;
+    int64_t page_off;
+} ep_segment;
+
+/* Device page pool: K and V as [num_pages][n_kv_heads][page_tokens][d_head]
+ * (one contiguous page_tokens x d_head tile per (page, head)). */
+typedef struct ep_kv_pool {
+    int32_t dtype;      /* EP_F32 or EP_BF16 */
+    int32_t n_kv_heads;
+    int32_t d_head;     /* 64 or 128 */
+    int32_t page_tokens;/* multiple of 64 */
+    int64_t num_pages;
+    void* k_pages;
+    void* v_pages;
+} ep_kv_pool;
+
+/* Builds the launch plan for one batch from a HOST copy of the splice table
+ * (seg_indptr [batch+1], segs, page_table, q_pos [batch] = absolute position
+ * of each request's first query row). n_q query rows per request, n_q_heads
+ * query heads (GQA group = n_q_heads / n_kv_heads). The plan owns its device
+ * descriptors and fp32 partial workspace. ctas_per_sm = 0 picks the default. */
+int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,
+                   int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, int32_t ctas_per_sm,
+                   ep_plan* out);
+/* Re-plans in place (e.g. after appending generated tokens); device buffers are
+ * reused when large enough, so captured CUDA graphs stay valid. */
+int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, ep_stream stream);
+int ep_plan_destroy(ep_plan p);
+/* Introspection: number of CTAs, work items and pages in the plan. */
+int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages);
+
+/* K1 + K2: spliced attention for every (request, query row, q-head) of the
+ * plan. q [batch][n_q][n_q_heads][d] (q_dtype EP_F32/EP_BF16); o same layout
+ * (o_dtype EP_F32/EP_BF16); lse [batch][n_q][n_q_heads] fp32 natural log
+ * (may be NULL). Reproduces transformer_layer's attention block
+ * (model.cpp:161-182): a per-segment partial with CausalSpan{q_pos,
+ * seg.pos_offset} merged in segment order — here as one online-softmax pass
+ * over the pages, so no spliced copy of the cache is materialised. */
+int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype,
+                         const void* q, int32_t o_dtype, void* o, float* lse, ep_stream stream);
+
+/* For cross-GPU split-KV each rank calls ep_spliced_attention on its own KV
+ * shard with o_dtype = EP_F32 and a non-NULL lse: (o, lse) of that shard's keys
+ * only, which ep_merge_partials_dev (or ep_splitkv_combine in the NCCL build)
+ * recombines in rank = segment order. */
+
+/* Appends n_tok token rows per request into the pool (the device form of
+ * SegmentedCache::append_generated_token, cache.cpp:55-80, without its
+ * whole-segment copy). k_new/v_new: [n_rows][n_kv_heads][d_head] in the pool
+ * dtype; row i goes to page dst_page[i], slot dst_slot[i] (device int32). */
+int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int32_t* dst_page,
+                 const int32_t* dst_slot, const void* k_new, const void* v_new,
+                 ep_stream stream);
+
+/* ==================================================================== */
+/* 4. Utilities                                                         */
+/* ==================================================================== */
+
+/* dst[i] = uniform(lo, hi) of the i-th SplitMix64(seed) draw (rng.hpp:10-29),
+ * rounded f64 -> f32 (RN) -> bf16 (RN) for EP_BF16. Device pointer. */
+int ep_fill_uniform(ep_handle h, ep_dtype dt, void* dst, size_t n, uint64_t seed, double lo,
+                    double hi, ep_stream stream);
+
+/* Number of kernel launches issued by this handle since creation (evidence for
+ * bench.py's gpu_launches). */
+int64_t ep_launch_count(ep_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EP_ATTN_H */

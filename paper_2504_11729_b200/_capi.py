@@ -1,0 +1,137 @@
+"""ctypes binding of include/ep/ep_attn.h (libep_b200.so).
+
+Loading fails loudly when the library is missing — there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "_lib", "libep_b200.so")
+HEADER = os.path.join(os.path.dirname(PKG), "include", "ep", "ep_attn.h")
+
+EP_OK, EP_EINVAL, EP_EMASKED, EP_ECUDA, EP_ENCCL, EP_ENOMEM, EP_EUNSUPPORTED = range(7)
+EP_F32, EP_BF16, EP_F64 = 0, 1, 2
+
+
+class EPError(RuntimeError):
+    status = -1
+
+
+class InvalidArgument(EPError, ValueError):
+    """std::invalid_argument in the reference (attention.cpp:14-25, :117)."""
+    status = EP_EINVAL
+
+
+class DomainError(EPError, ArithmeticError):
+    """std::domain_error in the reference (attention.cpp:52-56, :150-153)."""
+    status = EP_EMASKED
+
+
+class CudaError(EPError):
+    status = EP_ECUDA
+
+
+class NcclError(EPError):
+    status = EP_ENCCL
+
+
+class OutOfMemory(EPError, MemoryError):
+    status = EP_ENOMEM
+
+
+class Unsupported(EPError, NotImplementedError):
+    status = EP_EUNSUPPORTED
+
+
+_ERRORS = {cls.status: cls for cls in (InvalidArgument, DomainError, CudaError, NcclError,
+                                       OutOfMemory, Unsupported)}
+
+
+class Segment(C.Structure):
+    """ep_segment (KVSegment, cache.hpp:18-28)."""
+    _fields_ = [("origin", C.c_int32), ("len", C.c_int32), ("pos_offset", C.c_int64),
+                ("page_off", C.c_int64)]
+
+
+class KVPoolDesc(C.Structure):
+    """ep_kv_pool."""
+    _fields_ = [("dtype", C.c_int32), ("n_kv_heads", C.c_int32), ("d_head", C.c_int32),
+                ("page_tokens", C.c_int32), ("num_pages", C.c_int64), ("k_pages", C.c_void_p),
+                ("v_pages", C.c_void_p)]
+
+
+_lib: C.CDLL | None = None
+
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_sz = C.c_size_t
+
+_SIGS = {
+    "ep_abi_version": (C.c_int, []),
+    "ep_last_error": (C.c_char_p, []),
+    "ep_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "ep_destroy": (C.c_int, [_vp]),
+    "ep_partial_attention_f64": (C.c_int, [_vp, _dp, _sz, _dp, _dp, _sz, _sz, _sz, _sz, _dp, _dp]),
+    "ep_full_attention_f64": (C.c_int, [_vp, _dp, _sz, _dp, _dp, _sz, _sz, _sz, _sz, _dp]),
+    "ep_merge_partials_f64": (C.c_int, [_vp, _sz, C.POINTER(_dp), C.POINTER(_dp), _sz, _sz, _dp,
+                                        _dp]),
+    "ep_fuse_partials_f64": (C.c_int, [_vp, _sz, C.POINTER(_dp), C.POINTER(_dp), _sz, _sz, _dp]),
+    "ep_partial_attention_dev": (C.c_int, [_vp, C.c_int, _vp, _sz, _sz, _vp, _sz, _vp, _sz, _sz,
+                                           _sz, _sz, _sz, _vp, _sz, _vp, _vp]),
+    "ep_merge_partials_dev": (C.c_int, [_vp, C.c_int, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "ep_plan_create": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, C.c_int32, C.c_int32, _vp,
+                                 _vp, _vp, _vp, C.c_int32, C.POINTER(_vp)]),
+    "ep_plan_update": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "ep_plan_destroy": (C.c_int, [_vp]),
+    "ep_plan_info": (C.c_int, [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                               C.POINTER(C.c_int64)]),
+    "ep_spliced_attention": (C.c_int, [_vp, _vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, C.c_int32,
+                                       _vp, _vp, _vp]),
+    "ep_fill_uniform": (C.c_int, [_vp, C.c_int, _vp, _sz, C.c_uint64, C.c_double, C.c_double,
+                                  _vp]),
+    "ep_launch_count": (C.c_int64, [_vp]),
+    "ep_kv_append": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp, _vp, _vp, _vp]),
+}
+
+# Optional entry points (present when the corresponding kernels are built).
+_OPTIONAL_SIGS = {
+    "ep_verify_greedy": (C.c_int, [_vp, _vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp,
+                                   C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp]),
+}
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -m paper_2504_11729_b200.build` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        for name, (res, args) in _OPTIONAL_SIGS.items():
+            if hasattr(L, name):
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int, where: str = "") -> None:
+    if rc == EP_OK:
+        return
+    msg = lib().ep_last_error().decode(errors="replace")
+    raise _ERRORS.get(rc, EPError)(f"{where}: {msg}" if where else msg)
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/ep/ep_attn.h."""
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ep_[a-z0-9_]+)\s*\(", text)))

@@ -1,0 +1,532 @@
+// capi.cpp — implementation of include/ep/ep_attn.h (host side of libep_b200.so).
+//
+// Sections mirror the header: (1) the synchronous host-buffer drop-in entry
+// points that replace attention.cpp's functions, (2) device-pointer variants,
+// (3) the paged splice-table plan + K1/K2 launch, (4) utilities.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ep_internal.h"
+
+namespace ep {
+
+namespace {
+thread_local std::string g_err;
+}
+
+int fail(int rc, const std::string& msg) {
+    g_err = msg;
+    return rc;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(EP_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr) cudaFree(ptr);
+}
+
+cudaError_t DeviceBuffer::reserve(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+}
+
+}  // namespace ep
+
+using namespace ep;
+
+#define EP_CUDA_TRY(expr, where)                          \
+    do {                                                  \
+        cudaError_t _e = (expr);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+// ------------------------------------------------------------- plan object --
+
+struct ep_plan_s {
+    ep_handle h = nullptr;
+    int32_t kv_dtype = 0, n_kv_heads = 0, d_head = 0, page_tokens = 0;
+    int64_t num_pages = 0;
+    int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
+    int64_t n_ctas = 0, n_items = 0, n_pages = 0;
+    bool need_merge = false;
+    // host mirrors
+    std::vector<PageDesc> pdesc;
+    std::vector<int64_t> req_page_off;
+    std::vector<WorkItem> items;
+    std::vector<int32_t> cta_item_ptr, unit_item_ptr;
+    std::vector<int64_t> q_pos;
+    // device copies
+    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_qpos, d_opart, d_lsepart;
+    void* h_stage = nullptr;  // pinned staging for async updates
+    size_t h_stage_bytes = 0;
+    cudaEvent_t staged = nullptr;
+    ~ep_plan_s() {
+        if (h_stage) cudaFreeHost(h_stage);
+        if (staged) cudaEventDestroy(staged);
+    }
+};
+
+namespace {
+
+constexpr int kBlockTokens = 64;
+
+int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
+                    const int32_t* page_table, const int64_t* q_pos) {
+    const int B = p.batch, Hkv = p.n_kv_heads, P = p.page_tokens;
+    p.pdesc.clear();
+    p.req_page_off.assign(B + 1, 0);
+    p.q_pos.assign(q_pos, q_pos + B);
+    std::vector<int64_t> req_blocks(B, 0);
+    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
+    for (int b = 0; b < B; ++b) {
+        if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
+        if (q_pos[b] < 0) return fail(EP_EINVAL, "ep_plan: negative query position");
+        int64_t expect_pos = -1;
+        int last_origin = -1;
+        for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
+            const ep_segment& s = segs[si];
+            if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
+                return fail(EP_EINVAL, "ep_plan: negative segment field");
+            // SegmentedCache invariants (cache.cpp:25-53): gapless, origin order.
+            if (expect_pos >= 0 && s.pos_offset != expect_pos)
+                return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
+                                           std::to_string(s.pos_offset) + ", previous ends at " +
+                                           std::to_string(expect_pos));
+            if (s.origin < last_origin)
+                return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
+            expect_pos = s.pos_offset + s.len;
+            last_origin = s.origin;
+            const int64_t npg = (int64_t(s.len) + P - 1) / P;
+            for (int64_t i = 0; i < npg; ++i) {
+                const int32_t page = page_table[s.page_off + i];
+                if (page < 0 || page >= p.num_pages)
+                    return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
+                PageDesc d;
+                d.page = page;
+                d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
+                d.pos = s.pos_offset + i * P;
+                p.pdesc.push_back(d);
+                req_blocks[b] += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+            }
+        }
+        p.req_page_off[b + 1] = int64_t(p.pdesc.size());
+    }
+    p.n_pages = int64_t(p.pdesc.size());
+
+    // Work split: every CTA streams the same number of 64-token blocks. Walk
+    // the (request, kv-head) units in order and cut at page boundaries.
+    int64_t total = 0;
+    for (int b = 0; b < B; ++b) total += req_blocks[b] * Hkv;
+    const int64_t cap = int64_t(p.h->n_sms) * std::max(1, decode_ctas_per_sm(p.kv_dtype, p.d_head, p.rows));
+    p.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap, total));
+    p.items.clear();
+    p.cta_item_ptr.assign(p.n_ctas + 1, 0);
+    p.unit_item_ptr.assign(int64_t(B) * Hkv + 1, 0);
+    std::vector<int32_t> item_cta;
+    int64_t acc = 0;
+    int64_t cta = 0;
+    auto boundary = [&](int64_t c) { return (total * (c + 1) + p.n_ctas - 1) / p.n_ctas; };
+    for (int b = 0; b < B; ++b) {
+        const int64_t npg = p.req_page_off[b + 1] - p.req_page_off[b];
+        for (int g = 0; g < Hkv; ++g) {
+            const int64_t unit = int64_t(b) * Hkv + g;
+            bool open = false;
+            for (int64_t lp = 0; lp < npg; ++lp) {
+                while (cta < p.n_ctas - 1 && acc >= boundary(cta)) {
+                    ++cta;
+                    open = false;
+                }
+                if (!open) {
+                    p.items.push_back(WorkItem{b, g, int32_t(lp), int32_t(lp)});
+                    item_cta.push_back(int32_t(cta));
+                    p.unit_item_ptr[unit + 1]++;
+                    open = true;
+                }
+                p.items.back().lp1 = int32_t(lp + 1);
+                const PageDesc& d = p.pdesc[p.req_page_off[b] + lp];
+                acc += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+            }
+        }
+    }
+    p.n_items = int64_t(p.items.size());
+    for (int32_t c : item_cta) p.cta_item_ptr[c + 1]++;
+    for (int64_t c = 0; c < p.n_ctas; ++c) p.cta_item_ptr[c + 1] += p.cta_item_ptr[c];
+    p.need_merge = false;
+    for (int64_t u = 0; u < int64_t(B) * Hkv; ++u) {
+        if (p.unit_item_ptr[u + 1] != 1) p.need_merge = true;
+        p.unit_item_ptr[u + 1] += p.unit_item_ptr[u];
+    }
+    return EP_OK;
+}
+
+template <typename T>
+size_t bytes_of(const std::vector<T>& v) {
+    return v.size() * sizeof(T);
+}
+
+int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
+    struct Part {
+        DeviceBuffer* dst;
+        const void* src;
+        size_t n;
+    };
+    const Part parts[] = {
+        {&p.d_pdesc, p.pdesc.data(), bytes_of(p.pdesc)},
+        {&p.d_req_off, p.req_page_off.data(), bytes_of(p.req_page_off)},
+        {&p.d_items, p.items.data(), bytes_of(p.items)},
+        {&p.d_cta_ptr, p.cta_item_ptr.data(), bytes_of(p.cta_item_ptr)},
+        {&p.d_unit_ptr, p.unit_item_ptr.data(), bytes_of(p.unit_item_ptr)},
+        {&p.d_qpos, p.q_pos.data(), bytes_of(p.q_pos)},
+    };
+    size_t total = 0;
+    for (const Part& x : parts) total += (x.n + 255) & ~size_t(255);
+    for (const Part& x : parts) EP_CUDA_TRY(x.dst->reserve(std::max<size_t>(x.n, 16)), "ep_plan alloc");
+    const size_t ws = size_t(std::max<int64_t>(p.n_items, 1)) * p.rows;
+    EP_CUDA_TRY(p.d_opart.reserve(ws * p.d_head * sizeof(float)), "ep_plan workspace");
+    EP_CUDA_TRY(p.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
+    if (!async) {
+        for (const Part& x : parts)
+            if (x.n) EP_CUDA_TRY(cudaMemcpy(x.dst->ptr, x.src, x.n, cudaMemcpyHostToDevice), "ep_plan upload");
+        return EP_OK;
+    }
+    if (p.staged) EP_CUDA_TRY(cudaEventSynchronize(p.staged), "ep_plan_update wait");
+    if (total > p.h_stage_bytes) {
+        if (p.h_stage) cudaFreeHost(p.h_stage);
+        p.h_stage = nullptr;
+        EP_CUDA_TRY(cudaMallocHost(&p.h_stage, total), "ep_plan_update pinned");
+        p.h_stage_bytes = total;
+    }
+    if (!p.staged) EP_CUDA_TRY(cudaEventCreateWithFlags(&p.staged, cudaEventDisableTiming), "event");
+    size_t off = 0;
+    for (const Part& x : parts) {
+        if (x.n) {
+            std::memcpy(static_cast<char*>(p.h_stage) + off, x.src, x.n);
+            EP_CUDA_TRY(cudaMemcpyAsync(x.dst->ptr, static_cast<char*>(p.h_stage) + off, x.n,
+                                        cudaMemcpyHostToDevice, s),
+                        "ep_plan_update copy");
+        }
+        off += (x.n + 255) & ~size_t(255);
+    }
+    EP_CUDA_TRY(cudaEventRecord(p.staged, s), "ep_plan_update event");
+    return EP_OK;
+}
+
+bool valid_dt(int dt) { return dt == EP_F32 || dt == EP_BF16; }
+
+}  // namespace
+
+extern "C" {
+
+int ep_abi_version(void) { return EP_ABI_VERSION; }
+
+const char* ep_last_error(void) { return ep::g_err.c_str(); }
+
+int ep_create(int device, ep_handle* out) {
+    if (!out) return fail(EP_EINVAL, "ep_create: null out");
+    *out = nullptr;
+    int n = 0;
+    EP_CUDA_TRY(cudaGetDeviceCount(&n), "ep_create");
+    if (device < 0 || device >= n) return fail(EP_EINVAL, "ep_create: no CUDA device " + std::to_string(device));
+    EP_CUDA_TRY(cudaSetDevice(device), "ep_create");
+    cudaDeviceProp prop;
+    EP_CUDA_TRY(cudaGetDeviceProperties(&prop, device), "ep_create");
+    if (prop.major != 10)
+        return fail(EP_EUNSUPPORTED, std::string("ep_create: built for sm_100a (B200), device is ") + prop.name);
+    auto* h = new (std::nothrow) ep_context();
+    if (!h) return fail(EP_ENOMEM, "ep_create: host alloc");
+    h->device = device;
+    h->n_sms = prop.multiProcessorCount;
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete h;
+        return cuda_fail(e, "ep_create stream");
+    }
+    *out = h;
+    return EP_OK;
+}
+
+int ep_destroy(ep_handle h) {
+    if (!h) return EP_OK;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return EP_OK;
+}
+
+int64_t ep_launch_count(ep_handle h) { return h ? h->launches.load() : 0; }
+
+// ------------------------------------------------ (1) host-buffer drop-in --
+
+namespace {
+
+int check_head(size_t d, const char* where) {
+    if (d == 0) return fail(EP_EINVAL, std::string(where) + ": zero head width");
+    if (d > 256) return fail(EP_EUNSUPPORTED, std::string(where) + ": head width > 256");
+    return EP_OK;
+}
+
+size_t visible(size_t q_off, size_t k_off, size_t n_keys, size_t i) {
+    const size_t qpos = q_off + i;
+    if (qpos < k_off) return 0;
+    return std::min(n_keys, qpos - k_off + 1);
+}
+
+}  // namespace
+
+int ep_partial_attention_f64(ep_handle h, const double* q, size_t n_q, const double* k,
+                             const double* v, size_t n_keys, size_t d, size_t query_offset,
+                             size_t key_offset, double* out, double* lse) {
+    if (!h) return fail(EP_EINVAL, "partial_attention: null handle");
+    if (int rc = check_head(d, "partial_attention")) return rc;
+    if (n_q == 0) return EP_OK;
+    const size_t nq = n_q * d, nk = n_keys * d;
+    const size_t total = (2 * nq + 2 * nk + n_q) * sizeof(double);
+    EP_CUDA_TRY(cudaSetDevice(h->device), "partial_attention");
+    EP_CUDA_TRY(h->scratch.reserve(total), "partial_attention scratch");
+    double* dq = static_cast<double*>(h->scratch.ptr);
+    double* dk = dq + nq;
+    double* dv = dk + nk;
+    double* dout = dv + nk;
+    double* dlse = dout + nq;
+    cudaStream_t s = h->stream;
+    EP_CUDA_TRY(cudaMemcpyAsync(dq, q, nq * sizeof(double), cudaMemcpyHostToDevice, s), "H2D q");
+    if (nk) {
+        EP_CUDA_TRY(cudaMemcpyAsync(dk, k, nk * sizeof(double), cudaMemcpyHostToDevice, s), "H2D k");
+        EP_CUDA_TRY(cudaMemcpyAsync(dv, v, nk * sizeof(double), cudaMemcpyHostToDevice, s), "H2D v");
+    }
+    EP_CUDA_TRY(launch_partial_generic(EP_F64, dq, d, n_q, dk, d, dv, d, n_keys, d, query_offset,
+                                       key_offset, dout, d, dlse, s),
+                "partial_attention launch");
+    h->launches++;
+    EP_CUDA_TRY(cudaMemcpyAsync(out, dout, nq * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H out");
+    EP_CUDA_TRY(cudaMemcpyAsync(lse, dlse, n_q * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lse");
+    EP_CUDA_TRY(cudaStreamSynchronize(s), "partial_attention sync");
+    return EP_OK;
+}
+
+int ep_full_attention_f64(ep_handle h, const double* q, size_t n_q, const double* k,
+                          const double* v, size_t n_keys, size_t d, size_t query_offset,
+                          size_t key_offset, double* out) {
+    if (!h) return fail(EP_EINVAL, "full_attention: null handle");
+    if (int rc = check_head(d, "full_attention")) return rc;
+    for (size_t i = 0; i < n_q; ++i)
+        if (visible(query_offset, key_offset, n_keys, i) == 0)
+            return fail(EP_EMASKED, "full_attention: query at position " +
+                                        std::to_string(query_offset + i) + " has no visible key");
+    std::vector<double> lse(n_q);
+    return ep_partial_attention_f64(h, q, n_q, k, v, n_keys, d, query_offset, key_offset, out,
+                                    lse.data());
+}
+
+int ep_merge_partials_f64(ep_handle h, size_t n_parts, const double* const* outs,
+                          const double* const* lses, size_t n_q, size_t d, double* out,
+                          double* lse) {
+    if (!h) return fail(EP_EINVAL, "merge_partials: null handle");
+    if (n_parts == 0) return fail(EP_EINVAL, "merge_partials: no partials");
+    if (n_q == 0 || d == 0) return EP_OK;
+    const size_t per = n_q * d;
+    const size_t total = (n_parts * (per + n_q) + per + n_q) * sizeof(double);
+    EP_CUDA_TRY(cudaSetDevice(h->device), "merge_partials");
+    EP_CUDA_TRY(h->scratch.reserve(total), "merge_partials scratch");
+    double* d_outs = static_cast<double*>(h->scratch.ptr);
+    double* d_lses = d_outs + n_parts * per;
+    double* d_out = d_lses + n_parts * n_q;
+    double* d_lse = d_out + per;
+    cudaStream_t s = h->stream;
+    for (size_t p = 0; p < n_parts; ++p) {
+        EP_CUDA_TRY(cudaMemcpyAsync(d_outs + p * per, outs[p], per * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        EP_CUDA_TRY(cudaMemcpyAsync(d_lses + p * n_q, lses[p], n_q * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    }
+    EP_CUDA_TRY(launch_merge_generic(EP_F64, n_parts, d_outs, d_lses, n_q, d, d_out, d_lse, s),
+                "merge_partials launch");
+    h->launches++;
+    EP_CUDA_TRY(cudaMemcpyAsync(out, d_out, per * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    EP_CUDA_TRY(cudaMemcpyAsync(lse, d_lse, n_q * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    EP_CUDA_TRY(cudaStreamSynchronize(s), "merge_partials sync");
+    return EP_OK;
+}
+
+int ep_fuse_partials_f64(ep_handle h, size_t n_parts, const double* const* outs,
+                         const double* const* lses, size_t n_q, size_t d, double* out) {
+    std::vector<double> lse(n_q);
+    int rc = ep_merge_partials_f64(h, n_parts, outs, lses, n_q, d, out, lse.data());
+    if (rc) return rc;
+    for (size_t i = 0; i < n_q; ++i)
+        if (std::isinf(lse[i]) && lse[i] < 0)
+            return fail(EP_EMASKED, "fuse_partials: query row " + std::to_string(i) +
+                                        " is masked in every partial");
+    return EP_OK;
+}
+
+// -------------------------------------------------- (2) device pointers --
+
+int ep_partial_attention_dev(ep_handle h, ep_dtype dt, const void* q, size_t ldq, size_t n_q,
+                             const void* k, size_t ldk, const void* v, size_t ldv,
+                             size_t n_keys, size_t d, size_t query_offset, size_t key_offset,
+                             void* out, size_t ldo, void* lse, ep_stream stream) {
+    if (!h) return fail(EP_EINVAL, "partial_attention_dev: null handle");
+    if (dt != EP_F64 && dt != EP_F32) return fail(EP_EUNSUPPORTED, "partial_attention_dev: dtype");
+    if (int rc = check_head(d, "partial_attention_dev")) return rc;
+    if (ldq < d || ldk < d || ldv < d || ldo < d)
+        return fail(EP_EINVAL, "partial_attention_dev: leading dimension < d");
+    EP_CUDA_TRY(launch_partial_generic(dt, q, ldq, n_q, k, ldk, v, ldv, n_keys, d, query_offset,
+                                       key_offset, out, ldo, lse, static_cast<cudaStream_t>(stream)),
+                "partial_attention_dev launch");
+    if (n_q) h->launches++;
+    return EP_OK;
+}
+
+int ep_merge_partials_dev(ep_handle h, ep_dtype dt, size_t n_parts, const void* outs,
+                          const void* lses, size_t rows, size_t d, void* out, void* lse,
+                          ep_stream stream) {
+    if (!h) return fail(EP_EINVAL, "merge_partials_dev: null handle");
+    if (dt != EP_F64 && dt != EP_F32) return fail(EP_EUNSUPPORTED, "merge_partials_dev: dtype");
+    if (n_parts == 0) return fail(EP_EINVAL, "merge_partials: no partials");
+    EP_CUDA_TRY(launch_merge_generic(dt, n_parts, outs, lses, rows, d, out, lse,
+                                     static_cast<cudaStream_t>(stream)),
+                "merge_partials_dev launch");
+    if (rows) h->launches++;
+    return EP_OK;
+}
+
+// ------------------------------------------------------------ (3) plans --
+
+int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,
+                   int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, int32_t ctas_per_sm,
+                   ep_plan* out) {
+    if (!h || !pool || !out || !seg_indptr || !q_pos) return fail(EP_EINVAL, "ep_plan_create: null argument");
+    *out = nullptr;
+    if (!valid_dt(pool->dtype)) return fail(EP_EUNSUPPORTED, "ep_plan_create: kv dtype must be f32 or bf16");
+    if (pool->n_kv_heads <= 0 || n_q_heads <= 0 || n_q_heads % pool->n_kv_heads)
+        return fail(EP_EINVAL, "ep_plan_create: n_q_heads must be a multiple of n_kv_heads");
+    if (pool->page_tokens <= 0 || pool->page_tokens % kBlockTokens)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create: page_tokens must be a multiple of 64");
+    if (batch < 0 || n_q <= 0) return fail(EP_EINVAL, "ep_plan_create: batch/n_q");
+    const int rows = (n_q_heads / pool->n_kv_heads) * n_q;
+    if (!decode_supported(pool->dtype, pool->d_head, rows))
+        return fail(EP_EUNSUPPORTED, "ep_plan_create: no decode kernel for d_head=" +
+                                         std::to_string(pool->d_head) + " rows=" + std::to_string(rows) +
+                                         " (group*n_q must be 1, 2, 4 or 8)");
+    std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
+    if (!p) return fail(EP_ENOMEM, "ep_plan_create");
+    p->h = h;
+    p->kv_dtype = pool->dtype;
+    p->n_kv_heads = pool->n_kv_heads;
+    p->d_head = pool->d_head;
+    p->page_tokens = pool->page_tokens;
+    p->num_pages = pool->num_pages;
+    p->n_q_heads = n_q_heads;
+    p->n_q = n_q;
+    p->batch = batch;
+    p->rows = rows;
+    (void)ctas_per_sm;
+    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create");
+    if (int rc = upload_plan(*p, nullptr, false)) return rc;
+    *out = p.release();
+    return EP_OK;
+}
+
+int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, ep_stream stream) {
+    if (!p) return fail(EP_EINVAL, "ep_plan_update: null plan");
+    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
+    return upload_plan(*p, static_cast<cudaStream_t>(stream), true);
+}
+
+int ep_plan_destroy(ep_plan p) {
+    delete p;
+    return EP_OK;
+}
+
+int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages) {
+    if (!p) return fail(EP_EINVAL, "ep_plan_info: null plan");
+    if (n_ctas) *n_ctas = p->n_ctas;
+    if (n_items) *n_items = p->n_items;
+    if (n_pages) *n_pages = p->n_pages;
+    return EP_OK;
+}
+
+int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype,
+                         const void* q, int32_t o_dtype, void* o, float* lse, ep_stream stream) {
+    if (!h || !p || !pool || !q || !o) return fail(EP_EINVAL, "ep_spliced_attention: null argument");
+    if (pool->dtype != p->kv_dtype || pool->n_kv_heads != p->n_kv_heads ||
+        pool->d_head != p->d_head || pool->page_tokens != p->page_tokens ||
+        pool->num_pages < p->num_pages)
+        return fail(EP_EINVAL, "ep_spliced_attention: pool does not match the plan");
+    if (!valid_dt(q_dtype) || !valid_dt(o_dtype))
+        return fail(EP_EUNSUPPORTED, "ep_spliced_attention: q/o dtype must be f32 or bf16");
+    DecodeArgs a{};
+    a.k_pages = pool->k_pages;
+    a.v_pages = pool->v_pages;
+    a.n_kv_heads = p->n_kv_heads;
+    a.n_q_heads = p->n_q_heads;
+    a.page_tokens = p->page_tokens;
+    a.n_q = p->n_q;
+    a.pdesc = static_cast<const PageDesc*>(p->d_pdesc.ptr);
+    a.req_page_off = static_cast<const int64_t*>(p->d_req_off.ptr);
+    a.items = static_cast<const WorkItem*>(p->d_items.ptr);
+    a.cta_item_ptr = static_cast<const int32_t*>(p->d_cta_ptr.ptr);
+    a.unit_item_ptr = static_cast<const int32_t*>(p->d_unit_ptr.ptr);
+    a.q_pos = static_cast<const int64_t*>(p->d_qpos.ptr);
+    a.q = q;
+    a.q_dtype = q_dtype;
+    a.o_part = static_cast<float*>(p->d_opart.ptr);
+    a.lse_part = static_cast<float*>(p->d_lsepart.ptr);
+    a.o = o;
+    a.o_dtype = o_dtype;
+    a.lse = lse;
+    a.batch = p->batch;
+    a.q_scale = float(1.4426950408889634 / std::sqrt(double(p->d_head)));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
+                "spliced decode launch");
+    h->launches++;
+    if (p->need_merge) {
+        EP_CUDA_TRY(launch_split_merge(p->d_head, p->rows, a, s), "split merge launch");
+        h->launches++;
+    }
+    return EP_OK;
+}
+
+int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int32_t* dst_page,
+                 const int32_t* dst_slot, const void* k_new, const void* v_new,
+                 ep_stream stream) {
+    if (!h || !pool) return fail(EP_EINVAL, "ep_kv_append: null argument");
+    if (!valid_dt(pool->dtype)) return fail(EP_EUNSUPPORTED, "ep_kv_append: kv dtype");
+    const int row_bytes = pool->d_head * (pool->dtype == EP_BF16 ? 2 : 4);
+    if (row_bytes % 16) return fail(EP_EUNSUPPORTED, "ep_kv_append: row must be a multiple of 16 bytes");
+    EP_CUDA_TRY(launch_kv_append(row_bytes, pool->n_kv_heads, pool->page_tokens, n_rows, dst_page,
+                                 dst_slot, k_new, v_new, pool->k_pages, pool->v_pages,
+                                 static_cast<cudaStream_t>(stream)),
+                "ep_kv_append launch");
+    if (n_rows > 0) h->launches++;
+    return EP_OK;
+}
+
+// --------------------------------------------------------- (4) utilities --
+
+int ep_fill_uniform(ep_handle h, ep_dtype dt, void* dst, size_t n, uint64_t seed, double lo,
+                    double hi, ep_stream stream) {
+    if (!h) return fail(EP_EINVAL, "ep_fill_uniform: null handle");
+    if (dt != EP_F32 && dt != EP_BF16 && dt != EP_F64) return fail(EP_EINVAL, "ep_fill_uniform: dtype");
+    EP_CUDA_TRY(launch_fill_uniform(dt, dst, n, seed, lo, hi, static_cast<cudaStream_t>(stream)),
+                "ep_fill_uniform launch");
+    if (n) h->launches++;
+    return EP_OK;
+}
+
+}  // extern "C"

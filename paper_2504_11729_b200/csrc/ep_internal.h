@@ -1,0 +1,99 @@
+// ep_internal.h — host-side internals of libep_b200.so (not part of the ABI).
+#pragma once
+
+#include <atomic>
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ep/ep_attn.h"
+
+namespace ep {
+
+// Sets the thread-local message returned by ep_last_error() and returns rc.
+int fail(int rc, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ~DeviceBuffer();
+    cudaError_t reserve(size_t n);
+};
+
+}  // namespace ep
+
+struct ep_context {
+    int device = 0;
+    int n_sms = 0;
+    cudaStream_t stream = nullptr;  // used by the synchronous host-buffer entry points
+    ep::DeviceBuffer scratch;       // staging for host-buffer calls
+    std::atomic<int64_t> launches{0};
+};
+
+namespace ep {
+
+// ---------------------------------------------------------- launchers --
+// Each returns the launch status and counts launches into *counter.
+
+cudaError_t launch_partial_generic(int dt, const void* q, size_t ldq, size_t n_q, const void* k,
+                                   size_t ldk, const void* v, size_t ldv, size_t n_keys, size_t d,
+                                   size_t q_off, size_t k_off, void* out, size_t ldo, void* lse,
+                                   cudaStream_t s);
+
+cudaError_t launch_merge_generic(int dt, size_t n_parts, const void* outs, const void* lses,
+                                 size_t rows, size_t d, void* out, void* lse, cudaStream_t s);
+
+cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int n_rows,
+                             const int32_t* dst_page, const int32_t* dst_slot, const void* k_new,
+                             const void* v_new, void* k_pages, void* v_pages, cudaStream_t s);
+
+cudaError_t launch_fill_uniform(int dt, void* dst, size_t n, uint64_t seed, double lo, double hi,
+                                cudaStream_t s);
+
+// Device-side descriptors of a spliced-decode plan (see plan.cpp).
+struct PageDesc {
+    int32_t page;   // page id in the pool
+    int32_t n_tok;  // valid tokens (1..page_tokens)
+    int64_t pos;    // absolute position of slot 0
+};
+
+struct WorkItem {
+    int32_t b;    // request
+    int32_t g;    // kv head
+    int32_t lp0;  // logical page range [lp0, lp1) of request b
+    int32_t lp1;
+};
+
+struct DecodeArgs {
+    const void* k_pages;
+    const void* v_pages;
+    int32_t n_kv_heads, n_q_heads, page_tokens, n_q;
+    const PageDesc* pdesc;
+    const int64_t* req_page_off;   // [batch+1]
+    const WorkItem* items;
+    const int32_t* cta_item_ptr;   // [n_ctas+1]
+    const int32_t* unit_item_ptr;  // [batch*Hkv+1]
+    const int64_t* q_pos;          // [batch]
+    const void* q;
+    int32_t q_dtype;
+    float* o_part;    // [n_items][R][D]
+    float* lse_part;  // [n_items][R] (log2 units)
+    void* o;
+    int32_t o_dtype;
+    float* lse;       // natural log, may be null
+    int32_t batch;
+    float q_scale;    // log2(e) / sqrt(d)
+};
+
+// R = rows per (request, kv-head) = group * n_q.
+bool decode_supported(int kv_dtype, int d_head, int rows);
+int decode_ctas_per_sm(int kv_dtype, int d_head, int rows);
+cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas,
+                                  const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_split_merge(int d_head, int rows, const DecodeArgs& a, cudaStream_t s);
+
+}  // namespace ep

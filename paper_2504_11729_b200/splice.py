@@ -1,0 +1,288 @@
+"""Device-resident paged KV store and splice tables.
+
+The reference keeps, per session and per layer, an ordered list of fp64
+``KVSegment`` s (cloud -> edge -> generated, gapless positions;
+/root/reference/proj/core/include/edgeprompt/cache.hpp:11-61,
+src/cache.cpp:25-103) and copies the whole generated segment on every decoded
+token (cache.cpp:55-80). Here:
+
+* ``KVPool``      — one HBM page pool per layer: K and V as
+  ``[num_pages][n_kv_heads][page_tokens][d_head]`` (bf16 or fp32). A page is
+  one contiguous ``page_tokens x d_head`` tile per kv-head, so the decode
+  kernel streams it with a single bulk-async copy. Pages are refcounted, so a
+  cloud-prompt segment is written once and referenced by every request's
+  splice table (config 5).
+* ``SpliceTable`` — per-request ordered segment descriptors (``ep_segment``)
+  over pool pages, with the reference's append invariants (gapless positions,
+  origin order, atomic validation) and O(1) token append into the trailing
+  generated segment's last page.
+* ``SplicedAttention`` — an ``ep_plan`` over (pool, table): the K1+K2 launch.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from ._capi import InvalidArgument, KVPoolDesc, check, lib
+from .attention import Handle, default_handle
+
+ORIGIN_CLOUD, ORIGIN_EDGE, ORIGIN_GENERATED = 0, 1, 2  # SegmentOrigin (cache.hpp:11)
+_ORIGIN_NAMES = {0: "cloud", 1: "edge", 2: "generated"}
+
+SEGMENT_DTYPE = np.dtype([("origin", "<i4"), ("len", "<i4"), ("pos_offset", "<i8"),
+                          ("page_off", "<i8")])
+assert SEGMENT_DTYPE.itemsize == C.sizeof(_capi.Segment)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def dtype_code(dtype) -> int:
+    torch = _torch()
+    if dtype in ("bf16", torch.bfloat16):
+        return _capi.EP_BF16
+    if dtype in ("f32", "fp32", torch.float32):
+        return _capi.EP_F32
+    raise _capi.Unsupported(f"KV dtype {dtype!r}: expected bf16 or fp32")
+
+
+class KVPool:
+    """Paged K/V pool in HBM for one layer (ep_kv_pool)."""
+
+    def __init__(self, num_pages: int, n_kv_heads: int, d_head: int, page_tokens: int = 64,
+                 dtype="bf16", device: int = 0, k=None, v=None):
+        torch = _torch()
+        self.code = dtype_code(dtype)
+        self.tdtype = torch.bfloat16 if self.code == _capi.EP_BF16 else torch.float32
+        self.num_pages, self.n_kv_heads, self.d_head = num_pages, n_kv_heads, d_head
+        self.page_tokens = page_tokens
+        shape = (num_pages, n_kv_heads, page_tokens, d_head)
+        dev = torch.device("cuda", device)
+        self.k = k if k is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
+        self.v = v if v is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
+        assert tuple(self.k.shape) == shape and tuple(self.v.shape) == shape
+        self._free = list(range(num_pages - 1, -1, -1))
+        self._ref = np.zeros(num_pages, dtype=np.int32)
+
+    # --------------------------------------------------------- allocator --
+    def alloc(self, n: int) -> np.ndarray:
+        if n > len(self._free):
+            raise _capi.OutOfMemory(f"KVPool: {n} pages requested, {len(self._free)} free")
+        pages = np.array([self._free.pop() for _ in range(n)], dtype=np.int32)
+        self._ref[pages] = 1
+        return pages
+
+    def retain(self, pages) -> None:
+        self._ref[np.asarray(pages)] += 1
+
+    def release(self, pages) -> None:
+        for p in np.asarray(pages).tolist():
+            self._ref[p] -= 1
+            if self._ref[p] == 0:
+                self._free.append(p)
+
+    @property
+    def free_pages(self) -> int:
+        return len(self._free)
+
+    # ------------------------------------------------------------ writes --
+    def write(self, pages, k, v, start: int = 0) -> None:
+        """Scatter token rows k/v [len][n_kv_heads][d_head] into ``pages``,
+        starting at token slot ``start`` of the first page."""
+        torch = _torch()
+        n = int(k.shape[0])
+        if n == 0:
+            return
+        t = torch.arange(start, start + n, device=self.k.device)
+        pg = torch.as_tensor(np.asarray(pages, dtype=np.int64), device=self.k.device)
+        pidx = pg[t // self.page_tokens]
+        sidx = t % self.page_tokens
+        self.k[pidx, :, sidx, :] = k.to(self.tdtype)
+        self.v[pidx, :, sidx, :] = v.to(self.tdtype)
+
+    def desc(self) -> KVPoolDesc:
+        return KVPoolDesc(self.code, self.n_kv_heads, self.d_head, self.page_tokens,
+                          self.num_pages, self.k.data_ptr(), self.v.data_ptr())
+
+    def host_raw(self):
+        """(k, v) as numpy (fp32 or raw-bf16 uint16) for the CPU oracle."""
+        torch = _torch()
+        if self.code == _capi.EP_BF16:
+            return (self.k.view(torch.int16).cpu().numpy().view(np.uint16),
+                    self.v.view(torch.int16).cpu().numpy().view(np.uint16))
+        return self.k.cpu().numpy(), self.v.cpu().numpy()
+
+
+@dataclass
+class SegmentRef:
+    origin: int
+    pos_offset: int
+    length: int
+    pages: np.ndarray  # int32 page ids
+
+    @property
+    def end_position(self) -> int:
+        return self.pos_offset + self.length
+
+
+class SpliceTable:
+    """Ordered segment lists for a batch of requests (SegmentedCache analogue)."""
+
+    def __init__(self, batch: int, page_tokens: int = 64):
+        self.page_tokens = page_tokens
+        self.requests: list[list[SegmentRef]] = [[] for _ in range(batch)]
+        self.q_pos = np.zeros(batch, dtype=np.int64)
+
+    @property
+    def batch(self) -> int:
+        return len(self.requests)
+
+    def end_position(self, b: int) -> int:
+        segs = self.requests[b]
+        return segs[-1].end_position if segs else 0
+
+    def append(self, b: int, origin: int, pos_offset: int, length: int, pages) -> None:
+        """SegmentedCache::append invariants (cache.cpp:25-53), validated
+        before any mutation."""
+        pages = np.asarray(pages, dtype=np.int32)
+        end = self.end_position(b)
+        if pos_offset != end:
+            raise InvalidArgument(f"SpliceTable.append: segment starts at {pos_offset}, "
+                                  f"cache ends at {end}")
+        if length <= 0:
+            raise InvalidArgument("SpliceTable.append: empty segment")
+        need = -(-length // self.page_tokens)
+        if pages.size < need:
+            raise InvalidArgument(f"SpliceTable.append: {length} tokens need {need} pages, "
+                                  f"got {pages.size}")
+        segs = self.requests[b]
+        if segs and origin < segs[-1].origin:
+            raise InvalidArgument("SpliceTable.append: origin order must be (cloud, edge, "
+                                  "generated)")
+        segs.append(SegmentRef(origin, pos_offset, length, pages[:need].copy()))
+
+    def append_generated_tokens(self, b: int, n: int, pool: KVPool | None = None):
+        """Grows the trailing generated segment by n tokens (cache.cpp:55-80)
+        without copying: new tokens go to the last page's free slots or a fresh
+        page. Returns (pages, start_slot) where the caller writes the K/V rows."""
+        segs = self.requests[b]
+        pos = self.end_position(b)
+        P = self.page_tokens
+        if not segs or segs[-1].origin != ORIGIN_GENERATED:
+            if pool is None:
+                raise InvalidArgument("append_generated_tokens: pool needed for a new page")
+            pages = pool.alloc(-(-n // P))
+            segs.append(SegmentRef(ORIGIN_GENERATED, pos, n, pages))
+            return pages, 0
+        g = segs[-1]
+        start = g.length % P
+        have = g.pages.size * P - g.length
+        if n > have:
+            if pool is None:
+                raise InvalidArgument("append_generated_tokens: pool needed for a new page")
+            extra = pool.alloc(-(-(n - have) // P))
+            g.pages = np.concatenate([g.pages, extra])
+        first = g.length // P
+        g.length += n
+        return g.pages[first:], start
+
+    def check_consistent(self) -> str:
+        """cache.cpp:82-103 restricted to one layer: gapless, origin order."""
+        for b, segs in enumerate(self.requests):
+            pos, last = None, -1
+            for s in segs:
+                if pos is not None and s.pos_offset != pos:
+                    return f"request {b}: gap in position coverage"
+                if s.origin < last:
+                    return f"request {b}: origin order violated"
+                pos, last = s.end_position, s.origin
+        return ""
+
+    def arrays(self):
+        """(seg_indptr int64 [B+1], segs SEGMENT_DTYPE, page_table int32)."""
+        indptr = np.zeros(self.batch + 1, dtype=np.int64)
+        recs = []
+        pages = []
+        off = 0
+        for b, segs in enumerate(self.requests):
+            for s in segs:
+                recs.append((s.origin, s.length, s.pos_offset, off))
+                pages.append(s.pages)
+                off += s.pages.size
+            indptr[b + 1] = len(recs)
+        segs_arr = np.array(recs, dtype=SEGMENT_DTYPE) if recs else np.zeros(0, SEGMENT_DTYPE)
+        pt = np.concatenate(pages).astype(np.int32) if pages else np.zeros(1, np.int32)
+        return indptr, segs_arr, np.ascontiguousarray(pt)
+
+
+class SplicedAttention:
+    """ep_plan over (pool, table): spliced attention for every request."""
+
+    def __init__(self, pool: KVPool, table: SpliceTable, n_q_heads: int, n_q: int = 1,
+                 handle: Handle | None = None):
+        self.pool, self.table = pool, table
+        self.n_q_heads, self.n_q = n_q_heads, n_q
+        self.handle = handle or default_handle(pool.k.device.index or 0)
+        self._keep = None
+        indptr, segs, pt = table.arrays()
+        self._keep = (indptr, segs, pt, np.ascontiguousarray(table.q_pos, dtype=np.int64))
+        plan = C.c_void_p()
+        pd = pool.desc()
+        check(lib().ep_plan_create(self.handle.ptr, C.byref(pd), n_q_heads, n_q, table.batch,
+                                   indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
+                                   self._keep[3].ctypes.data, 0, C.byref(plan)),
+              "ep_plan_create")
+        self.plan = plan
+
+    def update(self, stream=None) -> None:
+        """Re-plan after the table changed (ep_plan_update, stream-ordered)."""
+        indptr, segs, pt = self.table.arrays()
+        self._keep = (indptr, segs, pt, np.ascontiguousarray(self.table.q_pos, dtype=np.int64))
+        check(lib().ep_plan_update(self.plan, indptr.ctypes.data, segs.ctypes.data,
+                                   pt.ctypes.data, self._keep[3].ctypes.data,
+                                   _stream(stream)), "ep_plan_update")
+
+    def info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ep_plan_info(self.plan, C.byref(a), C.byref(b), C.byref(c)), "ep_plan_info")
+        return a.value, b.value, c.value
+
+    def __call__(self, q, o=None, lse=None, o_dtype=None, stream=None):
+        """q [B][n_q][Hq][d] (bf16/fp32 CUDA tensor) -> (o, lse)."""
+        torch = _torch()
+        B, d = self.table.batch, self.pool.d_head
+        if tuple(q.shape) != (B, self.n_q, self.n_q_heads, d) or not q.is_contiguous():
+            raise InvalidArgument(f"SplicedAttention: q must be contiguous "
+                                  f"[{B}][{self.n_q}][{self.n_q_heads}][{d}]")
+        if o is None:
+            o = torch.empty(q.shape, dtype=o_dtype or q.dtype, device=q.device)
+        if lse is None:
+            lse = torch.empty((B, self.n_q, self.n_q_heads), dtype=torch.float32, device=q.device)
+        pd = self.pool.desc()
+        check(lib().ep_spliced_attention(self.handle.ptr, self.plan, C.byref(pd),
+                                         dtype_code(q.dtype), q.data_ptr(), dtype_code(o.dtype),
+                                         o.data_ptr(), lse.data_ptr() if lse is not False else None,
+                                         _stream(stream)), "ep_spliced_attention")
+        return o, lse
+
+    def close(self):
+        if getattr(self, "plan", None):
+            lib().ep_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _stream(stream):
+    if stream is None:
+        return _torch().cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)

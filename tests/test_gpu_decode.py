@@ -1,0 +1,184 @@
+"""GPU parity of K1/K2 (spliced flash-decode over the paged splice table)
+against the fp64 oracle on identical rounded inputs. Tolerances are the
+north_star's: 1e-3 relative (fp32 KV) and 2e-2 (bf16 KV), metric
+|got - want| / max(1, |want|) (acceptance_test.cpp:107-109)."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import cases as CS
+from tests import splice_cases as SC
+from tests.gpu_util import to_device, tol_for, torch_from_raw
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _check(o, lse, want_o, want_l, kv_dtype, units=None, Hq=None):
+    o = o.float().cpu().numpy().astype(np.float64)
+    lse = lse.cpu().numpy().astype(np.float64)
+    if units is not None:
+        sel = [(int(u) // Hq, int(u) % Hq) for u in units]
+        o = np.stack([o[b, :, h] for b, h in sel])
+        lse = np.stack([lse[b, :, h] for b, h in sel])
+        want_o = np.stack([want_o[b, :, h] for b, h in sel])
+        want_l = np.stack([want_l[b, :, h] for b, h in sel])
+    err_o = CS.rel_err(o, want_o)
+    fin = np.isfinite(want_l)
+    assert np.array_equal(np.isfinite(lse), fin)
+    err_l = CS.rel_err(lse[fin], want_l[fin])
+    tol = tol_for(kv_dtype)
+    assert err_o <= tol, f"out rel err {err_o:.3e} > {tol}"
+    assert err_l <= 1e-4, f"lse rel err {err_l:.3e}"
+    return err_o, err_l
+
+
+@pytest.mark.parametrize("name", list(SC.SMALL_CASES))
+def test_small_cases_vs_reference_golden(cuda_handle, name):
+    gold = np.load(os.path.join(GOLD, "splice_golden.npz"))
+    sb = SC.small_case(name)
+    pool, table, attn, q = to_device(sb, cuda_handle)
+    o, lse = attn(q, o_dtype=q.dtype)
+    e1 = _check(o, lse, gold[f"{name}/out"], gold[f"{name}/lse"], sb.kv_dtype)
+    # fp32 output path as well
+    import torch
+    o32, lse32 = attn(q, o_dtype=torch.float32)
+    e2 = _check(o32, lse32, gold[f"{name}/out"], gold[f"{name}/lse"], sb.kv_dtype)
+    print(name, "rel err (o, lse):", e1, e2)
+
+
+def test_deterministic(cuda_handle):
+    sb = SC.small_case("gqa4_bf16_decode")
+    _, _, attn, q = to_device(sb, cuda_handle)
+    o1, l1 = attn(q)
+    o2, l2 = attn(q)
+    assert bool((o1 == o2).all()) and bool((l1 == l2).all())
+
+
+def _big_case(kv_dtype, Hq, Hkv, d, requests, n_q=1, seed=3):
+    return SC.make_case(kv_dtype, Hq, Hkv, d, requests, n_q=n_q, seed=seed)
+
+
+def test_config2_shape_full_size(cuda_handle):
+    """BASELINE config 2: Hq=32, Hkv=8, d=128, bf16, private 4096 cloud + 512
+    edge + self token per request, B=32. Checked on 96 random units."""
+    reqs = [[(SC.CLOUD, 4096, None), (SC.EDGE, 512, None), (SC.GEN, 1, None)]] * 32
+    sb = _big_case(O.DT_BF16, 32, 8, 128, reqs)
+    _, _, attn, q = to_device(sb, cuda_handle)
+    o, lse = attn(q)
+    units = np.random.default_rng(0).choice(32 * 32, 96, replace=False)
+    want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4, units=units)
+    print("cfg2 rel err:", _check(o, lse, want_o, want_l, sb.kv_dtype, units, 32))
+    print("plan (ctas, items, pages):", attn.info())
+
+
+def test_config5_shared_prefix_ragged(cuda_handle):
+    """BASELINE config 5 structure at reduced batch: requests share one 8192-token
+    cloud segment (same pages) with ragged U{32..2048} edge segments."""
+    r = O.SplitMix64(5)
+    reqs = [[(SC.CLOUD, 8192, "cloud"), (SC.EDGE, 32 + r.next_u64() % 2017, None),
+             (SC.GEN, 1, None)] for _ in range(24)]
+    sb = _big_case(O.DT_BF16, 32, 8, 128, reqs, seed=4)
+    _, _, attn, q = to_device(sb, cuda_handle)
+    o, lse = attn(q)
+    units = np.random.default_rng(1).choice(24 * 32, 64, replace=False)
+    want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4, units=units)
+    print("cfg5 rel err:", _check(o, lse, want_o, want_l, sb.kv_dtype, units, 32))
+
+
+def test_config1_real_model_kv(cuda_handle):
+    """Config 1 KV produced by the reference model itself (L=2, H=4, D=256,
+    cloud 512 + edge 64), fp32 pages, MHA d=64; synthetic decode queries."""
+    import json
+    from tests.conftest import require_ref
+    require_ref()
+    g = json.load(open(os.path.join(GOLD, "model_golden.json")))
+    m = O.RefModel(2, 4, 256, 256, 1024, 42)
+    sess = m.session(g["cfg1_cloud"], g["cfg1_edge"])
+    H, d, P = 4, 64, 64
+    for layer in range(2):
+        ks, vs, segs = [], [], []
+        for s in range(sess.n_segments):
+            k, v, pos, org = sess.segment(layer, s)
+            segs.append((org, k.shape[0], pos))
+            ks.append(k)
+            vs.append(v)
+        # one page-aligned pool: segment s occupies its own pages
+        n_pages = sum(-(-n // P) for _, n, _ in segs) + 1
+        kp = np.zeros((n_pages, H, P, d), np.float32)
+        vp = np.zeros((n_pages, H, P, d), np.float32)
+        recs, pt, page = [], [], 0
+        for (org, n, pos), k, v in zip(segs, ks, vs):
+            recs.append((org, n, pos, len(pt)))
+            for t in range(n):
+                kp[page + t // P, :, t % P] = k[t].reshape(H, d)
+                vp[page + t // P, :, t % P] = v[t].reshape(H, d)
+            npg = -(-n // P)
+            pt.extend(range(page, page + npg))
+            page += npg
+        end = segs[-1][2] + segs[-1][1]
+        q = O.fill_uniform(O.DT_F32, H * d, 77 + layer).reshape(1, 1, H, d)
+        sb = O.HostSpliceBatch(O.DT_F32, H, H, d, P, kp, vp, np.array([0, len(recs)], np.int64),
+                               np.array(recs, dtype=O.SEGMENT_DTYPE), np.array(pt, np.int32),
+                               np.array([end - 1], np.int64), O.DT_F32, q, 1)
+        want_o, want_l = O.spliced_attention(sb, n_threads=4)
+        _, _, attn, qd = to_device(sb, cuda_handle)
+        o, lse = attn(qd)
+        print("cfg1 layer", layer, "rel err:", _check(o, lse, want_o, want_l, O.DT_F32))
+
+
+def test_decode_loop_with_plan_update(cuda_handle):
+    """Generated tokens appended page-slot by page-slot (no segment copy,
+    cf. cache.cpp:55-80); the plan is updated in place each step."""
+    import torch
+    sb = SC.make_case(O.DT_BF16, 8, 2, 128, [[(SC.CLOUD, 190, None), (SC.EDGE, 40, None)],
+                                              [(SC.EDGE, 63, None)]], seed=9, spare_pages=8)
+    pool, table, attn, q = to_device(sb, cuda_handle)
+    pool._free = [p for p in range(pool.num_pages - 1, -1, -1)
+                  if p not in set(sb.page_table.tolist())]
+    host_k, host_v = sb.k_pages.copy(), sb.v_pages.copy()
+    for step in range(70):
+        for b in range(table.batch):
+            pages, start = table.append_generated_tokens(b, 1, pool)
+            kv = O.fill_uniform(O.DT_BF16, 2 * 2 * 128, 1000 + step * 7 + b).reshape(2, 2, 128)
+            pool.write(pages, torch_from_raw(kv[0:1].copy(), O.DT_BF16),
+                       torch_from_raw(kv[1:2].copy(), O.DT_BF16), start=start)
+            host_k[pages[0], :, start] = kv[0]
+            host_v[pages[0], :, start] = kv[1]
+            table.q_pos[b] = table.end_position(b) - 1
+        attn.update()
+        o, lse = attn(q)
+        if step % 23 == 0 or step == 69:
+            indptr, segs, pt = table.arrays()
+            hb = O.HostSpliceBatch(sb.kv_dtype, 2, 8, 128, 64, host_k, host_v, indptr, segs, pt,
+                                   table.q_pos.copy(), sb.q_dtype, sb.q, 1)
+            want_o, want_l = O.spliced_attention(hb, n_threads=4)
+            _check(o, lse, want_o, want_l, sb.kv_dtype)
+
+
+def test_plan_rejects_bad_tables(cuda_handle):
+    import ctypes as C
+    from paper_2504_11729_b200 import _capi
+    sb = SC.small_case("gqa4_bf16_decode")
+    pool, table, attn, q = to_device(sb, cuda_handle)
+    indptr, segs, pt = table.arrays()
+    segs_bad = segs.copy()
+    segs_bad[1]["pos_offset"] += 1  # gap (cache.cpp:37-41)
+    plan = C.c_void_p()
+    pd = pool.desc()
+    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 1, table.batch,
+                                    indptr.ctypes.data, segs_bad.ctypes.data, pt.ctypes.data,
+                                    table.q_pos.ctypes.data, 0, C.byref(plan))
+    assert rc == _capi.EP_EINVAL and b"segment starts" in _capi.lib().ep_last_error()
+    pt_bad = pt.copy()
+    pt_bad[0] = pool.num_pages + 5
+    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 1, table.batch,
+                                    indptr.ctypes.data, segs.ctypes.data, pt_bad.ctypes.data,
+                                    table.q_pos.ctypes.data, 0, C.byref(plan))
+    assert rc == _capi.EP_EINVAL
+    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 3, table.batch,
+                                    indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
+                                    table.q_pos.ctypes.data, 0, C.byref(plan))
+    assert rc == _capi.EP_EUNSUPPORTED  # rows = 4*3 = 12 has no CUDA-core instance
