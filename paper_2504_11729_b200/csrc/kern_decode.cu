@@ -410,12 +410,19 @@ __global__ void __launch_bounds__(128) split_merge_kernel(const DecodeArgs a) {
     }
 }
 
-constexpr int kStages = 4;
+// Pipeline depth: ~128 KB of K+V blocks in flight per SM (4 stages of a
+// 64-token bf16 d=128 block; 2 for fp32 d=128 whose blocks are twice as big).
+template <typename KV, int D>
+constexpr int stages_for() {
+    return (2 * 64 * D * int(sizeof(KV))) >= 65536 ? 2 : 4;
+}
 
 template <typename KV, int D, int R>
 cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
-    using C = DecodeCfg<KV, D, R, kStages>;
-    auto kern = spliced_decode_kernel<KV, D, R, kStages>;
+    constexpr int S = stages_for<KV, D>();
+    using C = DecodeCfg<KV, D, R, S>;
+    static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
+    auto kern = spliced_decode_kernel<KV, D, R, S>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
