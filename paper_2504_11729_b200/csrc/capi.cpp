@@ -60,7 +60,7 @@ struct ep_plan_s {
     int64_t num_pages = 0;
     int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
     int64_t n_ctas = 0, n_items = 0, n_pages = 0;
-    bool need_merge = false;
+    bool has_empty_unit = false;
     // host mirrors
     std::vector<PageDesc> pdesc;
     std::vector<int64_t> req_page_off;
@@ -69,6 +69,8 @@ struct ep_plan_s {
     std::vector<int64_t> q_pos;
     // device copies
     DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_qpos, d_opart, d_lsepart;
+    DeviceBuffer d_counter;  // per-unit arrival counters of the fused merge (zero between launches)
+    size_t counter_units = 0;
     void* h_stage = nullptr;  // pinned staging for async updates
     size_t h_stage_bytes = 0;
     cudaEvent_t staged = nullptr;
@@ -149,23 +151,25 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
                     open = false;
                 }
                 if (!open) {
-                    p.items.push_back(WorkItem{b, g, int32_t(lp), int32_t(lp)});
+                    p.items.push_back(WorkItem{b, g, int32_t(lp), int32_t(lp), 0, {0, 0, 0}});
                     item_cta.push_back(int32_t(cta));
                     p.unit_item_ptr[unit + 1]++;
                     open = true;
                 }
                 p.items.back().lp1 = int32_t(lp + 1);
                 const PageDesc& d = p.pdesc[p.req_page_off[b] + lp];
-                acc += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+                const int nb = (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+                p.items.back().nblk += nb;
+                acc += nb;
             }
         }
     }
     p.n_items = int64_t(p.items.size());
     for (int32_t c : item_cta) p.cta_item_ptr[c + 1]++;
     for (int64_t c = 0; c < p.n_ctas; ++c) p.cta_item_ptr[c + 1] += p.cta_item_ptr[c];
-    p.need_merge = false;
+    p.has_empty_unit = false;
     for (int64_t u = 0; u < int64_t(B) * Hkv; ++u) {
-        if (p.unit_item_ptr[u + 1] != 1) p.need_merge = true;
+        if (p.unit_item_ptr[u + 1] == 0) p.has_empty_unit = true;
         p.unit_item_ptr[u + 1] += p.unit_item_ptr[u];
     }
     return EP_OK;
@@ -196,6 +200,12 @@ int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
     const size_t ws = size_t(std::max<int64_t>(p.n_items, 1)) * p.rows;
     EP_CUDA_TRY(p.d_opart.reserve(ws * p.d_head * sizeof(float)), "ep_plan workspace");
     EP_CUDA_TRY(p.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
+    const size_t units = size_t(std::max(1, p.batch * p.n_kv_heads));
+    if (units > p.counter_units) {
+        EP_CUDA_TRY(p.d_counter.reserve(units * sizeof(int32_t)), "ep_plan counters");
+        EP_CUDA_TRY(cudaMemset(p.d_counter.ptr, 0, units * sizeof(int32_t)), "ep_plan counters");
+        p.counter_units = units;
+    }
     if (!async) {
         for (const Part& x : parts)
             if (x.n) EP_CUDA_TRY(cudaMemcpy(x.dst->ptr, x.src, x.n, cudaMemcpyHostToDevice), "ep_plan upload");
@@ -249,9 +259,12 @@ int ep_create(int device, ep_handle* out) {
     h->device = device;
     h->n_sms = prop.multiProcessorCount;
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = h->zero_rows.reserve(64 * 128 * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemset(h->zero_rows.ptr, 0, h->zero_rows.bytes);
     if (e != cudaSuccess) {
+        if (h->stream) cudaStreamDestroy(h->stream);
         delete h;
-        return cuda_fail(e, "ep_create stream");
+        return cuda_fail(e, "ep_create");
     }
     *out = h;
     return EP_OK;
@@ -491,12 +504,16 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
     a.lse = lse;
     a.batch = p->batch;
     a.q_scale = float(1.4426950408889634 / std::sqrt(double(p->d_head)));
+    a.zero_rows = h->zero_rows.ptr;
+    a.unit_counter = static_cast<int32_t*>(p->d_counter.ptr);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
-                "spliced decode launch");
-    h->launches++;
-    if (p->need_merge) {
-        EP_CUDA_TRY(launch_split_merge(p->d_head, p->rows, a, s), "split merge launch");
+    if (p->n_items > 0) {
+        EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
+                    "spliced decode launch");
+        h->launches++;
+    }
+    if (p->has_empty_unit) {
+        EP_CUDA_TRY(launch_empty_units(p->d_head, p->rows, a, s), "empty units launch");
         h->launches++;
     }
     return EP_OK;

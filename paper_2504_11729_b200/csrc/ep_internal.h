@@ -31,6 +31,7 @@ struct ep_context {
     int n_sms = 0;
     cudaStream_t stream = nullptr;  // used by the synchronous host-buffer entry points
     ep::DeviceBuffer scratch;       // staging for host-buffer calls
+    ep::DeviceBuffer zero_rows;     // 64 zero rows of the widest KV row (page-tail fill)
     std::atomic<int64_t> launches{0};
 };
 
@@ -62,10 +63,12 @@ struct PageDesc {
 };
 
 struct WorkItem {
-    int32_t b;    // request
-    int32_t g;    // kv head
-    int32_t lp0;  // logical page range [lp0, lp1) of request b
+    int32_t b;     // request
+    int32_t g;     // kv head
+    int32_t lp0;   // logical page range [lp0, lp1) of request b
     int32_t lp1;
+    int32_t nblk;  // 64-token pipeline blocks in the range
+    int32_t pad[3];
 };
 
 struct DecodeArgs {
@@ -86,7 +89,9 @@ struct DecodeArgs {
     int32_t o_dtype;
     float* lse;       // natural log, may be null
     int32_t batch;
-    float q_scale;    // log2(e) / sqrt(d)
+    float q_scale;            // log2(e) / sqrt(d)
+    const void* zero_rows;    // >= 64 zero K/V rows (page-tail fill)
+    int32_t* unit_counter;    // [batch*Hkv], zero between launches (fused K2)
 };
 
 // R = rows per (request, kv-head) = group * n_q.
@@ -94,6 +99,6 @@ bool decode_supported(int kv_dtype, int d_head, int rows);
 int decode_ctas_per_sm(int kv_dtype, int d_head, int rows);
 cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas,
                                   const DecodeArgs& a, cudaStream_t s);
-cudaError_t launch_split_merge(int d_head, int rows, const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_empty_units(int d_head, int rows, const DecodeArgs& a, cudaStream_t s);
 
 }  // namespace ep

@@ -1,4 +1,4 @@
-// kern_decode.cu — K1 spliced flash-decode and K2 split merge (sm_100a).
+// kern_decode.cu — K1 spliced flash-decode with the K2 split merge fused in (sm_100a).
 //
 // Replaces, for a whole batch at once, the per-head loop of transformer_layer's
 // attention block (/root/reference/proj/core/src/model.cpp:161-182): one
@@ -8,21 +8,26 @@
 // online-softmax state per (request, kv-head) — the same log-sum-exp algebra —
 // so no spliced copy of the cache is ever materialised.
 //
-// CTA anatomy (persistent, one CTA per SM, work = contiguous page ranges from
-// plan.cpp so every SM streams the same number of bytes):
-//   * warp NCW, one elected lane: producer. Streams each 64-token block of K
-//     and V for the CTA's kv-head into an S-stage shared-memory ring with 1-D
-//     bulk-async copies (TMA, SASS UBLKCP), completion on `full` mbarriers.
-//   * warps 0..NCW-1: consumers. Each warp owns KPW keys of every block; each
-//     half-warp owns J = 16/R keys; lane l16 of a half owns E = D/16 contiguous
-//     elements of d. Per block: QK^T as packed-fp32 FFMA2 partial dots, a
-//     16-lane butterfly reduce-scatter (every lane ends with exactly one
-//     (row, key) score), warp-shuffle row max, exp2 online softmax, PV with
-//     FFMA2. The R = group * n_q query rows of one kv-head share every K/V
-//     element loaded (GQA reuse).
-//   * end of a work item: halves, then warps combine in shared memory by
-//     LSE; the result goes straight to the output when the item covers the
-//     whole (request, kv-head), else to an fp32 partial slot for K2.
+// CTA anatomy (persistent, one CTA per SM; work = contiguous page ranges from
+// capi.cpp's planner, so every SM streams the same number of bytes):
+//   * warp NCW, one lane: producer. Streams each 64-token block of K and V of
+//     the CTA's kv-head into an S-stage shared-memory ring with 1-D bulk-async
+//     copies (TMA, SASS UBLKCP) completing on `full` mbarriers, and writes a
+//     16-byte stage header {position, valid rows}. A block shorter than 64
+//     rows (segment tail) gets its V tail filled from a zero page by one more
+//     bulk copy, so the consumers' PV loop is branch-free.
+//   * warps 0..NCW-1: consumers. Warp w owns keys [w*2J, w*2J+2J) of every
+//     block; each half-warp J keys; lane l16 of a half owns E = D/16 contiguous
+//     elements of d. Per block: QK^T as packed-fp32 FFMA2 partial dots (K
+//     bf16 pairs unpacked with one shift/and each), a 16-lane butterfly
+//     reduce-scatter (each lane ends with one (row, key) score), warp-shuffle
+//     row max, exp2 online softmax, rescale + PV with FMUL2/FFMA2. The
+//     R = group * n_q rows of one kv-head share every K/V element (GQA reuse).
+//   * end of a work item: the warps' states combine by LSE in shared memory.
+//     An item that covers its whole (request, kv-head) writes the output
+//     directly; otherwise it writes an fp32 partial, and the LAST CTA to
+//     finish a unit (per-unit arrival counter) merges the unit's partials in
+//     page = segment order (attention.cpp:116-145) — no second launch.
 #include <cmath>
 #include <cstdint>
 
@@ -32,37 +37,49 @@
 namespace ep {
 namespace {
 
-template <typename KV, int D, int R, int S>
+constexpr int kLog2(int x) { return x <= 1 ? 0 : 1 + kLog2(x / 2); }
+
+template <typename KV, int D, int R, int J, int S>
 struct DecodeCfg {
     static constexpr int BT = 64;          // tokens per pipeline block
     static constexpr int E = D / 16;       // d-elements per lane
-    static constexpr int J = 16 / R;       // keys per half-warp per block
     static constexpr int KPW = 2 * J;      // keys per warp per block
     static constexpr int NCW = BT / KPW;   // consumer warps
     static constexpr int THREADS = (NCW + 1) * 32;
+    static constexpr int NV = R * J;       // partial scores per half-warp
+    static constexpr int LOGN = kLog2(NV);
+    static constexpr int DUP = 4 - LOGN;   // low lane bits holding duplicate slots
     static constexpr int ROW_BYTES = D * int(sizeof(KV));
     static constexpr int BLK_BYTES = BT * ROW_BYTES;
     static constexpr int PW_FLOATS = 2 * J * R + R;  // per-warp p and corr slots
     static constexpr int OFF_V = S * BLK_BYTES;
     static constexpr int OFF_BAR = 2 * S * BLK_BYTES;
-    static constexpr int OFF_P = OFF_BAR + 2 * S * 8;
+    static constexpr int OFF_HDR = OFF_BAR + 2 * S * 8;
+    static constexpr int OFF_P = OFF_HDR + S * 16;
     static constexpr int OFF_CO = OFF_P + NCW * PW_FLOATS * 4;
     static constexpr int OFF_CM = OFF_CO + NCW * R * D * 4;
     static constexpr int OFF_CL = OFF_CM + NCW * R * 4;
-    static constexpr int SMEM = OFF_CL + NCW * R * 4;
-    static_assert(R * J == 16, "one score per lane after the reduce-scatter");
+    static constexpr int OFF_FLAG = OFF_CL + NCW * R * 4;
+    static constexpr int SMEM = OFF_FLAG + 16;
+    static_assert((1 << LOGN) == NV && NV <= 16, "R*J must be a power of two <= 16");
     static_assert(E % 4 == 0, "vector width");
+    static_assert(NCW * 32 <= 1024 - 32, "block size");
 };
 
-// Loads the E elements lane l16 owns of one K/V row as E/2 float2 pairs.
+struct StageHdr {
+    int64_t pos;  // absolute position of row 0
+    int32_t nv;   // valid rows
+    int32_t pad;
+};
+
+// Loads the E elements lane l16 owns of one K/V row; pair(i) is elements 2i, 2i+1.
 template <typename KV, int E>
 struct RowLoader;
 
 template <int E>
 struct RowLoader<__nv_bfloat16, E> {
-    static_assert(E % 4 == 0, "bf16 rows are read 8 or 16 bytes at a time");
-    // E/2 packed bf16 pairs, loaded as 8- or 16-byte vectors.
-    __device__ __forceinline__ static void load(const uint8_t* row, int l16, uint32_t (&raw)[E / 2]) {
+    using Raw = uint32_t[E / 2];
+    __device__ __forceinline__ static void load(const uint8_t* row, int l16, Raw& raw) {
         if constexpr (E % 8 == 0) {
             const uint4* p = reinterpret_cast<const uint4*>(row) + l16 * (E / 8);
 #pragma unroll
@@ -83,37 +100,43 @@ struct RowLoader<__nv_bfloat16, E> {
             }
         }
     }
-    __device__ __forceinline__ static float2 pair(const uint32_t (&raw)[E / 2], int i) {
+    __device__ __forceinline__ static float2 pair(const Raw& raw, int i) {
         return bf16x2_to_float2(raw[i]);
     }
-    using Raw = uint32_t[E / 2];
 };
 
 template <int E>
 struct RowLoader<float, E> {
-    static_assert(E % 4 == 0, "fp32 rows are read 16 bytes at a time");
-    __device__ __forceinline__ static void load(const uint8_t* row, int l16, float4 (&raw)[E / 4]) {
+    using Raw = float4[E / 4];
+    __device__ __forceinline__ static void load(const uint8_t* row, int l16, Raw& raw) {
         const float4* p = reinterpret_cast<const float4*>(row) + l16 * (E / 4);
 #pragma unroll
         for (int i = 0; i < E / 4; ++i) raw[i] = p[i];
     }
-    __device__ __forceinline__ static float2 pair(const float4 (&raw)[E / 4], int i) {
+    __device__ __forceinline__ static float2 pair(const Raw& raw, int i) {
         const float4 w = raw[i / 2];
         return (i % 2 == 0) ? make_float2(w.x, w.y) : make_float2(w.z, w.w);
     }
-    using Raw = float4[E / 4];
 };
 
-template <typename T>
-__device__ __forceinline__ float load_q(const void* q, size_t idx) {
-    return to_f32<T>(static_cast<const T*>(q)[idx]);
+__device__ __forceinline__ float load_q(const void* q, int dtype, size_t idx) {
+    return dtype == EP_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(q)[idx])
+                            : static_cast<const float*>(q)[idx];
 }
 
-template <typename KV, int D, int R, int S>
-__global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
+__device__ __forceinline__ void store_o(void* o, int dtype, size_t idx, float v) {
+    if (dtype == EP_BF16)
+        static_cast<__nv_bfloat16*>(o)[idx] = __float2bfloat16_rn(v);
+    else
+        static_cast<float*>(o)[idx] = v;
+}
+
+template <typename KV, int D, int R, int J, int S>
+__global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     spliced_decode_kernel(const DecodeArgs a) {
-    using C = DecodeCfg<KV, D, R, S>;
-    constexpr int BT = C::BT, E = C::E, J = C::J, KPW = C::KPW, NCW = C::NCW;
+    using C = DecodeCfg<KV, D, R, J, S>;
+    constexpr int BT = C::BT, E = C::E, KPW = C::KPW, NCW = C::NCW, NV = C::NV;
+    constexpr int LOGN = C::LOGN, DUP = C::DUP;
     using L = RowLoader<KV, E>;
 
     extern __shared__ __align__(128) uint8_t smem[];
@@ -121,10 +144,12 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
     uint8_t* sV = smem + C::OFF_V;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint64_t* empty = full + S;
+    StageHdr* hdr = reinterpret_cast<StageHdr*>(smem + C::OFF_HDR);
     float* s_pw = reinterpret_cast<float*>(smem + C::OFF_P);
     float* c_o = reinterpret_cast<float*>(smem + C::OFF_CO);
     float* c_m = reinterpret_cast<float*>(smem + C::OFF_CM);
     float* c_l = reinterpret_cast<float*>(smem + C::OFF_CL);
+    int* s_flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
@@ -144,6 +169,9 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint8_t* kp = static_cast<const uint8_t*>(a.k_pages);
+            const uint8_t* vp = static_cast<const uint8_t*>(a.v_pages);
+            const uint8_t* zp = static_cast<const uint8_t*>(a.zero_rows);
             for (int it = it0; it < it1; ++it) {
                 const WorkItem w = a.items[it];
                 const PageDesc* pd = a.pdesc + a.req_page_off[w.b];
@@ -153,13 +181,17 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
                     for (int t0 = 0; t0 < d.n_tok; t0 += BT) {
                         const int nv = min(BT, d.n_tok - t0);
                         const uint32_t bytes = uint32_t(nv) * C::ROW_BYTES;
+                        const uint32_t tail = uint32_t(BT - nv) * C::ROW_BYTES;
                         mbar_wait(&empty[stage], phase ^ 1);
-                        mbar_arrive_expect_tx(&full[stage], 2 * bytes);
+                        hdr[stage].pos = d.pos + t0;
+                        hdr[stage].nv = nv;
+                        mbar_arrive_expect_tx(&full[stage], 2 * bytes + tail);
                         const size_t off = (tile + t0) * C::ROW_BYTES;
-                        bulk_g2s(sK + stage * C::BLK_BYTES,
-                                 static_cast<const uint8_t*>(a.k_pages) + off, bytes, &full[stage]);
-                        bulk_g2s(sV + stage * C::BLK_BYTES,
-                                 static_cast<const uint8_t*>(a.v_pages) + off, bytes, &full[stage]);
+                        uint8_t* dk = sK + stage * C::BLK_BYTES;
+                        uint8_t* dv = sV + stage * C::BLK_BYTES;
+                        bulk_g2s(dk, kp + off, bytes, &full[stage]);
+                        bulk_g2s(dv, vp + off, bytes, &full[stage]);
+                        if (tail) bulk_g2s(dv + bytes, zp, tail, &full[stage]);
                         if (++stage == S) {
                             stage = 0;
                             phase ^= 1;
@@ -173,15 +205,16 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
 
     // ============================== consumers ==============================
     const int hh = lane >> 4, l16 = lane & 15;
-    const int my_r = l16 / J, my_j = l16 % J;  // (row, key) slot after reduce-scatter
+    const int my_idx = l16 >> DUP;           // (row, key) slot after the reduce-scatter
+    const int my_r = my_idx / J, my_j = my_idx % J;
     const int G = a.n_q_heads / Hkv;
     float* pw = s_pw + warp * C::PW_FLOATS;  // [2][J][R] p, then [R] corr
+    const int key0 = warp * KPW + hh * J;
     int stage = 0;
     uint32_t phase = 0;
 
     for (int it = it0; it < it1; ++it) {
         const WorkItem w = a.items[it];
-        const PageDesc* pd = a.pdesc + a.req_page_off[w.b];
         const int64_t q0 = a.q_pos[w.b];
 
         // q rows of this kv-head, pre-scaled by log2(e)/sqrt(d): row r is
@@ -192,17 +225,9 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
             const int qi = r / G, h = w.g * G + r % G;
             const size_t base = ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * D + l16 * E;
 #pragma unroll
-            for (int e = 0; e < E / 2; ++e) {
-                float x0, x1;
-                if (a.q_dtype == EP_BF16) {
-                    x0 = load_q<__nv_bfloat16>(a.q, base + 2 * e);
-                    x1 = load_q<__nv_bfloat16>(a.q, base + 2 * e + 1);
-                } else {
-                    x0 = load_q<float>(a.q, base + 2 * e);
-                    x1 = load_q<float>(a.q, base + 2 * e + 1);
-                }
-                q2[r][e] = make_float2(x0 * a.q_scale, x1 * a.q_scale);
-            }
+            for (int e = 0; e < E / 2; ++e)
+                q2[r][e] = make_float2(load_q(a.q, a.q_dtype, base + 2 * e) * a.q_scale,
+                                       load_q(a.q, a.q_dtype, base + 2 * e + 1) * a.q_scale);
         }
         const int64_t my_qpos = q0 + my_r / G;
 
@@ -213,101 +238,94 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
 #pragma unroll
             for (int e = 0; e < E / 2; ++e) o2[r][e] = make_float2(0.f, 0.f);
 
-        for (int lp = w.lp0; lp < w.lp1; ++lp) {
-            const PageDesc d = pd[lp];
-            for (int t0 = 0; t0 < d.n_tok; t0 += BT) {
-                const int nv = min(BT, d.n_tok - t0);
-                const int64_t blk_pos = d.pos + t0;
-                const bool fast = (nv == BT) && (blk_pos + BT - 1 <= q0);
-                mbar_wait(&full[stage], phase);
-                const uint8_t* kb = sK + stage * C::BLK_BYTES;
-                const uint8_t* vb = sV + stage * C::BLK_BYTES;
-                const int key0 = warp * KPW + hh * J;
+        for (int blk = 0; blk < w.nblk; ++blk) {
+            mbar_wait(&full[stage], phase);
+            const StageHdr hd = hdr[stage];
+            const bool fast = (hd.nv == BT) && (hd.pos + BT - 1 <= q0);
+            const uint8_t* kb = sK + stage * C::BLK_BYTES;
+            const uint8_t* vb = sV + stage * C::BLK_BYTES;
 
-                // ---- S = Q K^T (partial dots over this lane's E elements) ----
-                float sc[16];
-                {
-                    typename L::Raw kr[J];
+            // ---- S = Q K^T: partial dots over this lane's E elements ----
+            float sc[NV];
+            {
+                typename L::Raw kr[J];
 #pragma unroll
-                    for (int j = 0; j < J; ++j) L::load(kb + (key0 + j) * C::ROW_BYTES, l16, kr[j]);
+                for (int j = 0; j < J; ++j) L::load(kb + (key0 + j) * C::ROW_BYTES, l16, kr[j]);
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-#pragma unroll
-                        for (int j = 0; j < J; ++j) {
-                            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                            for (int e = 0; e < E / 2; ++e) acc = ffma2(q2[r][e], L::pair(kr[j], e), acc);
-                            sc[r * J + j] = acc.x + acc.y;
-                        }
-                    }
-                }
-                // ---- 16-lane butterfly reduce-scatter: lane l16 keeps sc index l16 ----
-#pragma unroll
-                for (int step = 0; step < 4; ++step) {
-                    const int half = 8 >> step;  // 8,4,2,1 values exchanged
-                    const bool upper = (l16 & half) != 0;
-#pragma unroll
-                    for (int i = 0; i < half; ++i) {
-                        const float send = upper ? sc[i] : sc[i + half];
-                        const float keep = upper ? sc[i + half] : sc[i];
-                        sc[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
-                    }
-                }
-                float s = sc[0];
-                if (!fast) {
-                    const int kk = key0 + my_j;
-                    const bool ok = kk < nv && blk_pos + kk <= my_qpos;
-                    s = ok ? s : -INFINITY;
-                }
-                // ---- online softmax (rows are lane groups: j bits and the half bit) ----
-                float bm = s;
-#pragma unroll
-                for (int msk = 1; msk < J; msk <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, msk));
-                bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-                const float m_new = fmaxf(m_run, bm);
-                const float m_use = m_new == -INFINITY ? 0.f : m_new;
-                const float p = fast_exp2(s - m_use);
-                const float corr = fast_exp2(m_run - m_use);
-                m_run = m_new;
-                l_run = l_run * corr + p;
-                pw[(hh * J + my_j) * R + my_r] = p;
-                if (lane < 16 && my_j == 0) pw[2 * J * R + my_r] = corr;
-                __syncwarp();
-
-                // ---- rescale and O += P V ----
-                float cr[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) cr[r] = pw[2 * J * R + r];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const float2 c2 = make_float2(cr[r], cr[r]);
-#pragma unroll
-                    for (int e = 0; e < E / 2; ++e) o2[r][e] = fmul2(o2[r][e], c2);
-                }
-                {
-                    typename L::Raw vr[J];
-#pragma unroll
-                    for (int j = 0; j < J; ++j) L::load(vb + (key0 + j) * C::ROW_BYTES, l16, vr[j]);
+                for (int r = 0; r < R; ++r)
 #pragma unroll
                     for (int j = 0; j < J; ++j) {
-                        if (!fast && key0 + j >= nv) continue;  // stale smem beyond the page tail
-                        float pj[R];
+                        float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-                        for (int r = 0; r < R; ++r) pj[r] = pw[(hh * J + j) * R + r];
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const float2 p2 = make_float2(pj[r], pj[r]);
-#pragma unroll
-                            for (int e = 0; e < E / 2; ++e) o2[r][e] = ffma2(p2, L::pair(vr[j], e), o2[r][e]);
-                        }
+                        for (int e = 0; e < E / 2; ++e) acc = ffma2(q2[r][e], L::pair(kr[j], e), acc);
+                        sc[r * J + j] = acc.x + acc.y;
                     }
+            }
+            // ---- butterfly reduce-scatter over the 16 lanes of a half ----
+#pragma unroll
+            for (int st = 0; st < LOGN; ++st) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int half = NV >> (st + 1);
+                const int mask = 8 >> st;
+                const bool upper = (l16 & mask) != 0;
+#pragma unroll
+                for (int i = 0; i < half; ++i) {
+                    const float send = upper ? sc[i] : sc[i + half];
+                    const float keep = upper ? sc[i + half] : sc[i];
+                    sc[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stage]);
-                if (++stage == S) {
-                    stage = 0;
-                    phase ^= 1;
+            }
+            float s = sc[0];
+#pragma unroll
+            for (int st = LOGN; st < 4; ++st) s += __shfl_xor_sync(0xffffffffu, s, 8 >> st);
+            if (!fast) {
+                const int kk = key0 + my_j;
+                const bool ok = kk < hd.nv && hd.pos + kk <= my_qpos;
+                s = ok ? s : -INFINITY;
+            }
+            // ---- online softmax: a row's slots span the j bits, dup bits and the half ----
+            float bm = s;
+#pragma unroll
+            for (int msk = 1; msk < (J << DUP); msk <<= 1)
+                bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, msk));
+            bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+            const float m_new = fmaxf(m_run, bm);
+            const float m_use = m_new == -INFINITY ? 0.f : m_new;
+            const float p = fast_exp2(s - m_use);
+            const float corr = fast_exp2(m_run - m_use);
+            m_run = m_new;
+            l_run = l_run * corr + p;
+            pw[(hh * J + my_j) * R + my_r] = p;
+            if (lane < 16 && my_j == 0) pw[2 * J * R + my_r] = corr;
+            __syncwarp();
+
+            // ---- rescale, then O += P V (V tails are zero-filled: no branches) ----
+            typename L::Raw vr[J];
+#pragma unroll
+            for (int j = 0; j < J; ++j) L::load(vb + (key0 + j) * C::ROW_BYTES, l16, vr[j]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float cr = pw[2 * J * R + r];
+                const float2 c2 = make_float2(cr, cr);
+#pragma unroll
+                for (int e = 0; e < E / 2; ++e) o2[r][e] = fmul2(o2[r][e], c2);
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float pj = pw[(hh * J + j) * R + r];
+                    const float2 p2 = make_float2(pj, pj);
+#pragma unroll
+                    for (int e = 0; e < E / 2; ++e) o2[r][e] = ffma2(p2, L::pair(vr[j], e), o2[r][e]);
                 }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == S) {
+                stage = 0;
+                phase ^= 1;
             }
         }
 
@@ -319,20 +337,18 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
                 o2[r][e].x += __shfl_xor_sync(0xffffffffu, o2[r][e].x, 16);
                 o2[r][e].y += __shfl_xor_sync(0xffffffffu, o2[r][e].y, 16);
             }
-        float l_row = l_run;
+        float l_row = l_run;  // sum over distinct slots of the row (skip duplicate lanes)
 #pragma unroll
-        for (int msk = 1; msk < J; msk <<= 1) l_row += __shfl_xor_sync(0xffffffffu, l_row, msk);
+        for (int msk = 1 << DUP; msk < (J << DUP); msk <<= 1)
+            l_row += __shfl_xor_sync(0xffffffffu, l_row, msk);
         l_row += __shfl_xor_sync(0xffffffffu, l_row, 16);
         if (lane < 16) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int e = 0; e < E / 2; ++e) {
-                    float* dst = c_o + (warp * R + r) * D + l16 * E + 2 * e;
-                    dst[0] = o2[r][e].x;
-                    dst[1] = o2[r][e].y;
-                }
-            if (my_j == 0) {
+                for (int e = 0; e < E / 2; ++e)
+                    *reinterpret_cast<float2*>(c_o + (warp * R + r) * D + l16 * E + 2 * e) = o2[r][e];
+            if (my_j == 0 && (l16 & ((1 << DUP) - 1)) == 0) {
                 c_m[warp * R + my_r] = m_run;
                 c_l[warp * R + my_r] = l_row;
             }
@@ -340,7 +356,8 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
         named_bar_sync(1, NCW * 32);
 
         const int unit = w.b * Hkv + w.g;
-        const bool direct = (a.unit_item_ptr[unit + 1] - a.unit_item_ptr[unit]) == 1;
+        const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
+        const bool direct = n_items == 1;
         for (int idx = threadIdx.x; idx < R * D; idx += NCW * 32) {
             const int r = idx / D, c = idx % D;
             float M = -INFINITY;
@@ -361,57 +378,75 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, S>::THREADS, 1)
             if (direct) {
                 const int qi = r / G, h = w.g * G + r % G;
                 const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
-                if (a.o_dtype == EP_BF16)
-                    static_cast<__nv_bfloat16*>(a.o)[orow * D + c] = __float2bfloat16_rn(val);
-                else
-                    static_cast<float*>(a.o)[orow * D + c] = val;
+                store_o(a.o, a.o_dtype, orow * D + c, val);
                 if (c == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
             } else {
                 a.o_part[(size_t(it) * R + r) * D + c] = val;
                 if (c == 0) a.lse_part[size_t(it) * R + r] = lse2;
             }
         }
+        if (!direct) {
+            // Fused K2: the last CTA to finish one of this unit's items merges
+            // them all, in page (= segment) order (attention.cpp:128-144).
+            __threadfence();
+            named_bar_sync(1, NCW * 32);
+            if (threadIdx.x == 0) *s_flag = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
+            named_bar_sync(1, NCW * 32);
+            if (*s_flag) {
+                __threadfence();
+                const int b = w.b;
+                for (int idx = threadIdx.x; idx < R * D; idx += NCW * 32) {
+                    const int r = idx / D, c = idx % D;
+                    float M = -INFINITY;
+                    for (int i = u0; i < u0 + n_items; ++i) M = fmaxf(M, __ldcg(&a.lse_part[size_t(i) * R + r]));
+                    float Lsum = 0.f, acc = 0.f;
+                    if (M != -INFINITY) {
+                        for (int i = u0; i < u0 + n_items; ++i) {
+                            const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i) * R + r]) - M);
+                            Lsum += wt;
+                            acc += wt * __ldcg(&a.o_part[(size_t(i) * R + r) * D + c]);
+                        }
+                    }
+                    const bool empty_row = !(Lsum > 0.f);
+                    const int qi = r / G, h = w.g * G + r % G;
+                    const size_t orow = (size_t(b) * a.n_q + qi) * a.n_q_heads + h;
+                    store_o(a.o, a.o_dtype, orow * D + c, empty_row ? 0.f : acc / Lsum);
+                    if (c == 0 && a.lse)
+                        a.lse[orow] = empty_row ? -INFINITY : (M + fast_log2(Lsum)) * kLn2;
+                }
+                if (threadIdx.x == 0) a.unit_counter[unit] = 0;  // ready for the next launch
+            }
+        }
         named_bar_sync(1, NCW * 32);
     }
 }
 
-// K2 for split (request, kv-head) units: LSE-merge the unit's partials in
-// page (= segment) order, attention.cpp:116-145 in fp32/log2. Units with one
-// item were written directly by K1; units with none are identity rows.
+// Units with no pages at all (empty requests) are identity rows: o = 0,
+// lse = -inf (attention.cpp:37-43). Launched only when the plan has any.
 template <int D, int R>
-__global__ void __launch_bounds__(128) split_merge_kernel(const DecodeArgs a) {
+__global__ void empty_units_kernel(const DecodeArgs a) {
     const int unit = blockIdx.x;
-    const int i0 = a.unit_item_ptr[unit], i1 = a.unit_item_ptr[unit + 1];
-    if (i1 - i0 == 1) return;
+    if (a.unit_item_ptr[unit + 1] != a.unit_item_ptr[unit]) return;
     const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv;
     const int b = unit / Hkv, g = unit % Hkv;
     for (int idx = threadIdx.x; idx < R * D; idx += blockDim.x) {
         const int r = idx / D, c = idx % D;
-        float M = -INFINITY;
-        for (int i = i0; i < i1; ++i) M = fmaxf(M, a.lse_part[size_t(i) * R + r]);
-        float Lsum = 0.f, acc = 0.f;
-        if (M != -INFINITY) {
-            for (int i = i0; i < i1; ++i) {
-                const float wt = exp2f(a.lse_part[size_t(i) * R + r] - M);
-                if (wt == 0.f) continue;
-                Lsum += wt;
-                acc += wt * a.o_part[(size_t(i) * R + r) * D + c];
-            }
-        }
-        const bool empty_row = !(Lsum > 0.f);
-        const float val = empty_row ? 0.f : acc / Lsum;
         const int qi = r / G, h = g * G + r % G;
         const size_t orow = (size_t(b) * a.n_q + qi) * a.n_q_heads + h;
-        if (a.o_dtype == EP_BF16)
-            static_cast<__nv_bfloat16*>(a.o)[orow * D + c] = __float2bfloat16_rn(val);
-        else
-            static_cast<float*>(a.o)[orow * D + c] = val;
-        if (c == 0 && a.lse) a.lse[orow] = empty_row ? -INFINITY : (M + log2f(Lsum)) * kLn2;
+        store_o(a.o, a.o_dtype, orow * D + c, 0.f);
+        if (c == 0 && a.lse) a.lse[orow] = -INFINITY;
     }
 }
 
-// Pipeline depth: ~128 KB of K+V blocks in flight per SM (4 stages of a
-// 64-token bf16 d=128 block; 2 for fp32 d=128 whose blocks are twice as big).
+// Keys per half-warp: R*J = 16 partial scores per 16 lanes, except R = 8
+// where J = 2 keeps the warp count at 16.
+template <int R>
+constexpr int keys_per_half() {
+    return R >= 8 ? 2 : 16 / R / 2 > 0 ? 16 / R / 2 : 1;
+}
+
+// Pipeline depth: 128 KB of K+V blocks per SM (4 stages of a 64-token bf16
+// d=128 block; 2 for fp32 d=128 whose blocks are twice as big).
 template <typename KV, int D>
 constexpr int stages_for() {
     return (2 * 64 * D * int(sizeof(KV))) >= 65536 ? 2 : 4;
@@ -420,9 +455,10 @@ constexpr int stages_for() {
 template <typename KV, int D, int R>
 cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
     constexpr int S = stages_for<KV, D>();
-    using C = DecodeCfg<KV, D, R, S>;
+    constexpr int J = keys_per_half<R>();
+    using C = DecodeCfg<KV, D, R, J, S>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
-    auto kern = spliced_decode_kernel<KV, D, R, S>;
+    auto kern = spliced_decode_kernel<KV, D, R, J, S>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e =
@@ -464,14 +500,14 @@ cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas
                          : dispatch_rows<float, 64>(rows, n_ctas, a, s);
 }
 
-cudaError_t launch_split_merge(int d_head, int rows, const DecodeArgs& a, cudaStream_t s) {
+cudaError_t launch_empty_units(int d_head, int rows, const DecodeArgs& a, cudaStream_t s) {
     const int units = a.batch * a.n_kv_heads;
     if (units == 0) return cudaSuccess;
-#define EP_MERGE_CASE(DD, RR) \
-    if (d_head == DD && rows == RR) { split_merge_kernel<DD, RR><<<units, 128, 0, s>>>(a); return cudaGetLastError(); }
-    EP_MERGE_CASE(64, 1) EP_MERGE_CASE(64, 2) EP_MERGE_CASE(64, 4) EP_MERGE_CASE(64, 8)
-    EP_MERGE_CASE(128, 1) EP_MERGE_CASE(128, 2) EP_MERGE_CASE(128, 4) EP_MERGE_CASE(128, 8)
-#undef EP_MERGE_CASE
+#define EP_EMPTY_CASE(DD, RR) \
+    if (d_head == DD && rows == RR) { empty_units_kernel<DD, RR><<<units, 128, 0, s>>>(a); return cudaGetLastError(); }
+    EP_EMPTY_CASE(64, 1) EP_EMPTY_CASE(64, 2) EP_EMPTY_CASE(64, 4) EP_EMPTY_CASE(64, 8)
+    EP_EMPTY_CASE(128, 1) EP_EMPTY_CASE(128, 2) EP_EMPTY_CASE(128, 4) EP_EMPTY_CASE(128, 8)
+#undef EP_EMPTY_CASE
     return cudaErrorInvalidValue;
 }
 
