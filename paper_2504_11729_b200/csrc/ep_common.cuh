@@ -118,8 +118,12 @@ __device__ __forceinline__ float fast_log2(float x) {
 // Two packed bf16 (low half = element 2i) -> float2 without cvt: a bf16 is the
 // high 16 bits of the fp32 with the same value.
 __device__ __forceinline__ float2 bf16x2_to_float2(uint32_t w) {
+    // PRMT and LOP3 both issue on the ALU pipe, leaving the FMA pipe (which
+    // an IMAD.SHL would use) to the FFMA2s.
+    uint32_t lo;
+    asm("prmt.b32 %0, %1, 0, 0x1044;" : "=r"(lo) : "r"(w));
     float2 r;
-    r.x = __uint_as_float(w << 16);
+    r.x = __uint_as_float(lo);
     r.y = __uint_as_float(w & 0xffff0000u);
     return r;
 }

@@ -217,16 +217,18 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
         const WorkItem w = a.items[it];
         const int64_t q0 = a.q_pos[w.b];
 
-        // q rows of this kv-head, pre-scaled by log2(e)/sqrt(d): row r is
-        // (query row r / G, head g*G + r % G).
+        // q rows of this kv-head, pre-scaled by log2(e)/sqrt(d): logical row r
+        // is (query row r / G, head g*G + r % G). Physical slot rp holds
+        // logical row rp ^ my_r (see the reduce-scatter below).
         float2 q2[R][E / 2];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int rp = 0; rp < R; ++rp) {
+            const int r = rp ^ my_r;
             const int qi = r / G, h = w.g * G + r % G;
             const size_t base = ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * D + l16 * E;
 #pragma unroll
             for (int e = 0; e < E / 2; ++e)
-                q2[r][e] = make_float2(load_q(a.q, a.q_dtype, base + 2 * e) * a.q_scale,
+                q2[rp][e] = make_float2(load_q(a.q, a.q_dtype, base + 2 * e) * a.q_scale,
                                        load_q(a.q, a.q_dtype, base + 2 * e + 1) * a.q_scale);
         }
         const int64_t my_qpos = q0 + my_r / G;
@@ -246,35 +248,35 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const uint8_t* vb = sV + stage * C::BLK_BYTES;
 
             // ---- S = Q K^T: partial dots over this lane's E elements ----
+            // Physical score slot p = rp*J + jp holds logical (row, key) index
+            // p ^ my_idx: rows via the q2 permutation, keys by loading key
+            // jp ^ my_j into kr[jp]. Then at every reduce-scatter step the
+            // values a lane keeps are its low half and the ones it sends its
+            // high half, for every lane — no per-lane selects.
             float sc[NV];
             {
                 typename L::Raw kr[J];
 #pragma unroll
-                for (int j = 0; j < J; ++j) L::load(kb + (key0 + j) * C::ROW_BYTES, l16, kr[j]);
+                for (int jp = 0; jp < J; ++jp)
+                    L::load(kb + (key0 + (jp ^ my_j)) * C::ROW_BYTES, l16, kr[jp]);
 #pragma unroll
-                for (int r = 0; r < R; ++r)
+                for (int rp = 0; rp < R; ++rp)
 #pragma unroll
-                    for (int j = 0; j < J; ++j) {
+                    for (int jp = 0; jp < J; ++jp) {
                         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-                        for (int e = 0; e < E / 2; ++e) acc = ffma2(q2[r][e], L::pair(kr[j], e), acc);
-                        sc[r * J + j] = acc.x + acc.y;
+                        for (int e = 0; e < E / 2; ++e) acc = ffma2(q2[rp][e], L::pair(kr[jp], e), acc);
+                        sc[rp * J + jp] = acc.x + acc.y;
                     }
             }
             // ---- butterfly reduce-scatter over the 16 lanes of a half ----
 #pragma unroll
             for (int st = 0; st < LOGN; ++st) {
-                constexpr int dummy = 0;
-                (void)dummy;
                 const int half = NV >> (st + 1);
                 const int mask = 8 >> st;
-                const bool upper = (l16 & mask) != 0;
 #pragma unroll
-                for (int i = 0; i < half; ++i) {
-                    const float send = upper ? sc[i] : sc[i + half];
-                    const float keep = upper ? sc[i + half] : sc[i];
-                    sc[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-                }
+                for (int i = 0; i < half; ++i)
+                    sc[i] += __shfl_xor_sync(0xffffffffu, sc[i + half], mask);
             }
             float s = sc[0];
 #pragma unroll
@@ -304,12 +306,14 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             typename L::Raw vr[J];
 #pragma unroll
             for (int j = 0; j < J; ++j) L::load(vb + (key0 + j) * C::ROW_BYTES, l16, vr[j]);
+            if (!__all_sync(0xffffffffu, corr == 1.f)) {  // some row's max moved
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const float cr = pw[2 * J * R + r];
-                const float2 c2 = make_float2(cr, cr);
+                for (int r = 0; r < R; ++r) {
+                    const float cr = pw[2 * J * R + r];
+                    const float2 c2 = make_float2(cr, cr);
 #pragma unroll
-                for (int e = 0; e < E / 2; ++e) o2[r][e] = fmul2(o2[r][e], c2);
+                    for (int e = 0; e < E / 2; ++e) o2[r][e] = fmul2(o2[r][e], c2);
+                }
             }
 #pragma unroll
             for (int j = 0; j < J; ++j) {
@@ -438,11 +442,14 @@ __global__ void empty_units_kernel(const DecodeArgs a) {
     }
 }
 
-// Keys per half-warp: R*J = 16 partial scores per 16 lanes, except R = 8
-// where J = 2 keeps the warp count at 16.
+// Keys per half-warp. R*J = 16 partial scores per 16 lanes (one per lane
+// after the reduce-scatter) with 2R consumer warps: measured on cfg2 (R = 4),
+// 8 warps with J = 4 and ~150 registers beat 16 warps with J = 2 squeezed into
+// 96 registers (5.71 vs 5.01 TB/s). R = 1 uses J = 8 (4 warps); R = 8 uses
+// J = 2 (16 warps).
 template <int R>
 constexpr int keys_per_half() {
-    return R >= 8 ? 2 : 16 / R / 2 > 0 ? 16 / R / 2 : 1;
+    return R == 1 ? 8 : 16 / R;
 }
 
 // Pipeline depth: 128 KB of K+V blocks per SM (4 stages of a 64-token bf16
@@ -452,10 +459,9 @@ constexpr int stages_for() {
     return (2 * 64 * D * int(sizeof(KV))) >= 65536 ? 2 : 4;
 }
 
-template <typename KV, int D, int R>
+template <typename KV, int D, int R, int J = keys_per_half<R>()>
 cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
     constexpr int S = stages_for<KV, D>();
-    constexpr int J = keys_per_half<R>();
     using C = DecodeCfg<KV, D, R, J, S>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     auto kern = spliced_decode_kernel<KV, D, R, J, S>;
