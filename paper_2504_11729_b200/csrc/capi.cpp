@@ -5,6 +5,7 @@
 // (3) the paged splice-table plan + K1/K2 launch, (4) utilities.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -61,6 +62,11 @@ struct ep_plan_s {
     int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
     int64_t n_ctas = 0, n_items = 0, n_pages = 0;
     bool has_empty_unit = false;
+    bool use_tc = false;  // K3 tcgen05 path (rows > 8 or EP_FORCE_TC)
+    CUtensorMap tmap_k{}, tmap_v{};
+    const void* tm_k = nullptr;
+    const void* tm_v = nullptr;
+    int64_t tm_pages = -1;
     // host mirrors
     std::vector<PageDesc> pdesc;
     std::vector<int64_t> req_page_off;
@@ -83,6 +89,44 @@ struct ep_plan_s {
 namespace {
 
 constexpr int kBlockTokens = 64;
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f)
+            return fail(EP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    // The pool as a 2-D tensor of 128-element bf16 rows (one row per
+    // (page, head, slot)); 64 x 64 boxes, 128B swizzle = the UMMA K-major
+    // (K tiles) / MN-major (V tiles) canonical layouts.
+    const cuuint64_t dims[2] = {128, cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {64, 64};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(EP_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return EP_OK;
+}
+
+bool force_tc() {
+    static const bool f = [] {
+        const char* e = std::getenv("EP_FORCE_TC");
+        return e && e[0] == '1';
+    }();
+    return f;
+}
 
 int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
                     const int32_t* page_table, const int64_t* q_pos) {
@@ -429,10 +473,13 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
         return fail(EP_EUNSUPPORTED, "ep_plan_create: page_tokens must be a multiple of 64");
     if (batch < 0 || n_q <= 0) return fail(EP_EINVAL, "ep_plan_create: batch/n_q");
     const int rows = (n_q_heads / pool->n_kv_heads) * n_q;
-    if (!decode_supported(pool->dtype, pool->d_head, rows))
-        return fail(EP_EUNSUPPORTED, "ep_plan_create: no decode kernel for d_head=" +
-                                         std::to_string(pool->d_head) + " rows=" + std::to_string(rows) +
-                                         " (group*n_q must be 1, 2, 4 or 8)");
+    const bool k1 = decode_supported(pool->dtype, pool->d_head, rows);
+    const bool k3 = verify_supported(pool->dtype, pool->d_head, rows);
+    if (!k1 && !k3)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create: no kernel for kv dtype " + std::to_string(pool->dtype) +
+                                         ", d_head=" + std::to_string(pool->d_head) + ", rows=group*n_q=" +
+                                         std::to_string(rows) +
+                                         " (CUDA-core decode: rows 1/2/4/8; tcgen05 verify: bf16, d 128, rows <= 64)");
     std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
     if (!p) return fail(EP_ENOMEM, "ep_plan_create");
     p->h = h;
@@ -445,6 +492,7 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
     p->n_q = n_q;
     p->batch = batch;
     p->rows = rows;
+    p->use_tc = k3 && (!k1 || force_tc());
     (void)ctas_per_sm;
     if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create");
@@ -507,7 +555,19 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
     a.zero_rows = h->zero_rows.ptr;
     a.unit_counter = static_cast<int32_t*>(p->d_counter.ptr);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (p->n_items > 0) {
+    if (p->n_items > 0 && p->use_tc) {
+        if (p->tm_k != pool->k_pages || p->tm_v != pool->v_pages || p->tm_pages != pool->num_pages) {
+            const int64_t rows_total = pool->num_pages * pool->n_kv_heads * pool->page_tokens;
+            if (int rc = encode_kv_map(&p->tmap_k, pool->k_pages, rows_total)) return rc;
+            if (int rc = encode_kv_map(&p->tmap_v, pool->v_pages, rows_total)) return rc;
+            p->tm_k = pool->k_pages;
+            p->tm_v = pool->v_pages;
+            p->tm_pages = pool->num_pages;
+        }
+        EP_CUDA_TRY(launch_verify_attention(int(p->n_ctas), a, p->tmap_k, p->tmap_v, p->rows, s),
+                    "verify attention launch");
+        h->launches++;
+    } else if (p->n_items > 0) {
         EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
                     "spliced decode launch");
         h->launches++;

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "ep/ep_attn.h"
@@ -100,5 +101,10 @@ int decode_ctas_per_sm(int kv_dtype, int d_head, int rows);
 cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas,
                                   const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_empty_units(int d_head, int rows, const DecodeArgs& a, cudaStream_t s);
+
+// K3: tcgen05 multi-row (verify) attention; bf16 KV, d_head 128, rows <= 64.
+bool verify_supported(int kv_dtype, int d_head, int rows);
+cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUtensorMap& tk,
+                                    const CUtensorMap& tv, int rows, cudaStream_t s);
 
 }  // namespace ep

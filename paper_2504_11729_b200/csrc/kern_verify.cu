@@ -1,0 +1,459 @@
+// kern_verify.cu — K3: multi-row (speculative-verify) spliced attention on
+// the sm_100a tensor cores.
+//
+// Reference: the verify construction of SURVEY §8a a16 — prefill of
+// [last, d1..dk] against the cache (model.cpp:211-236), i.e. transformer_layer's
+// attention block (model.cpp:161-182) with n_q = k+1 causal rows: cached
+// segments fully visible, the draft segment causal (attention.cpp:29-33).
+// With GQA the R = group * n_q rows of one kv-head (20 for k=4, 36 for k=8)
+// share every K/V byte; at 20-36 FLOP/B that is beyond the CUDA cores, so:
+//
+//   QK^T : S[128 x 64]  (TMEM, fp32) = Q[128 x 128] (smem) . K[64 keys x 128]^T
+//   PV   : O[128 x 128] (TMEM, fp32) += P[128 x 64] (smem, bf16) . V[64 x 128]
+//
+// tcgen05.mma M=128 (rows >= R are padding; the M=128 issue rate equals
+// M=64's), operands staged by TMA with 128B swizzle straight from the paged
+// pool (the [page][head][token][d] tile is a 2-D tensor of 128-element rows).
+// Warp roles (128 threads, one CTA per SM, persistent over the planner's page
+// ranges like K1):
+//   warp 2 lane 0 : TMA producer (K and V boxes, S-stage ring)
+//   warp 3 lane 0 : MMA issuer; warp 3 owns the TMEM allocation
+//   warps 0-1     : softmax + epilogue, one thread per query row: tcgen05.ld
+//                   of the S row, causal/tail mask, exp2, bf16 P row written
+//                   swizzled to smem. Rescaling is lazy (FA4-style): the row
+//                   max is only moved when it grows by > 2^8, then the O row
+//                   is rescaled in TMEM (tcgen05.ld/st); otherwise P <= 256.
+// QK of block i+1 is issued before PV of block i so the tensor core overlaps
+// the softmax. Items that split a (request, kv-head) merge by LSE through the
+// same per-unit counter protocol as K1.
+#include <cmath>
+#include <cstdint>
+
+#include "ep_common.cuh"
+#include "ep_internal.h"
+#include "umma.cuh"
+
+namespace ep {
+namespace {
+
+constexpr int kBT = 64;        // keys per block
+constexpr int kD = 128;        // head dim
+constexpr int kM = 128;        // UMMA M (rows, padded)
+constexpr int kStages = 4;
+constexpr int kThreads = 128;
+constexpr int kSoftThreads = 64;  // rows 0..63
+constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
+
+constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
+constexpr int kKVHalf = kBT * 128;         // 8 KB: 64 rows x 64 bf16
+constexpr int kStageBytes = 4 * kKVHalf;   // K0 K1 V0 V1
+constexpr int kPBytes = kM * 128;          // 16 KB: 128 rows x 64 keys bf16
+constexpr int OFF_Q = 0;
+constexpr int OFF_STAGE = 2 * kQHalf;
+constexpr int OFF_P = OFF_STAGE + kStages * kStageBytes;
+constexpr int OFF_BAR = OFF_P + 2 * kPBytes;
+constexpr int kNumBars = 2 * kStages + 2 + 2 + 2 + 2 + 2;
+constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
+constexpr int kSmem = OFF_MISC + 32 + 1024;  // + alignment slack
+
+constexpr uint32_t kIdescQK = umma::idesc_bf16_f32(kM, kBT, false, false);
+constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
+
+struct Bars {
+    uint64_t* full;     // [S] TMA landed
+    uint64_t* empty;    // [S] K/V stage consumed (commit after PV)
+    uint64_t* s_full;   // [2] QK result in TMEM
+    uint64_t* s_free;   // [2] softmax done reading S
+    uint64_t* p_full;   // [2] P written (+ O rescaled)
+    uint64_t* pv_done;  // [2] PV finished (P buffer free, O updated)
+    uint64_t* q_ready;  // Q tile of the item in smem
+    uint64_t* o_free;   // epilogue read O
+};
+
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+    return row * 128 + ((chunk ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Walks the 64-token blocks of a work item in order: page by page.
+struct BlockWalker {
+    const PageDesc* pd;
+    int lp, lp1, t0;
+    PageDesc cur;
+    __device__ void init(const PageDesc* p, int lp0, int lp1_) {
+        pd = p;
+        lp = lp0;
+        lp1 = lp1_;
+        t0 = 0;
+        if (lp < lp1) cur = pd[lp];
+    }
+    // current block: page, token offset in page, valid rows, absolute position
+    __device__ int nv() const { return min(kBT, cur.n_tok - t0); }
+    __device__ int64_t pos() const { return cur.pos + t0; }
+    __device__ void next() {
+        t0 += kBT;
+        if (t0 >= cur.n_tok) {
+            t0 = 0;
+            if (++lp < lp1) cur = pd[lp];
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
+                            const __grid_constant__ CUtensorMap tmap_v, int rows) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sQ = smem + OFF_Q;
+    uint8_t* sStage = smem + OFF_STAGE;
+    uint8_t* sP = smem + OFF_P;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    Bars B{bar, bar + kStages, bar + 2 * kStages, bar + 2 * kStages + 2, bar + 2 * kStages + 4,
+           bar + 2 * kStages + 6, bar + 2 * kStages + 8, bar + 2 * kStages + 9};
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_MISC);
+    int* s_flag = reinterpret_cast<int*>(smem + OFF_MISC + 16);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
+    const int Hkv = a.n_kv_heads, P = a.page_tokens;
+    const int G = a.n_q_heads / Hkv;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&B.full[s], 1);
+            mbar_init(&B.empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&B.s_full[i], 1);
+            mbar_init(&B.s_free[i], 2);
+            mbar_init(&B.p_full[i], 2);
+            mbar_init(&B.pv_done[i], 1);
+        }
+        mbar_init(B.q_ready, 2);
+        mbar_init(B.o_free, 2);
+        fence_mbar_init();
+    }
+    if (warp == 3) umma::tmem_alloc(tmem_slot, 256);
+    if (warp == 2 && lane == 0) {
+        umma::tma_prefetch_desc(&tmap_k);
+        umma::tma_prefetch_desc(&tmap_v);
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tO = tmem, tS0 = tmem + 128;
+
+    if (warp == 2) {
+        // ============================== producer ==============================
+        if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
+            uint32_t gi = 0;
+            for (int it = it0; it < it1; ++it) {
+                const WorkItem w = a.items[it];
+                BlockWalker wk;
+                wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
+                for (int i = 0; i < w.nblk; ++i, ++gi, wk.next()) {
+                    const int st = gi % kStages;
+                    mbar_wait(&B.empty[st], ((gi / kStages) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&B.full[st], kStageBytes);
+                    const int row = int((int64_t(wk.cur.page) * Hkv + w.g) * P + wk.t0);
+                    uint8_t* dst = sStage + st * kStageBytes;
+                    umma::tma_load_2d(dst, &tmap_k, 0, row, &B.full[st], pol);
+                    umma::tma_load_2d(dst + kKVHalf, &tmap_k, 64, row, &B.full[st], pol);
+                    umma::tma_load_2d(dst + 2 * kKVHalf, &tmap_v, 0, row, &B.full[st], pol);
+                    umma::tma_load_2d(dst + 3 * kKVHalf, &tmap_v, 64, row, &B.full[st], pol);
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ================================ MMA =================================
+        if (lane == 0) {
+            const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
+            const uint32_t st_addr = smem_u32(sStage);
+            uint32_t gi = 0, n = 0;
+            auto issue_pv = [&](uint32_t g, bool first) {
+                const uint32_t pb = g & 1;
+                mbar_wait(&B.p_full[pb], (g >> 1) & 1);
+                if (first) mbar_wait(B.o_free, (n & 1) ^ 1);
+                umma::fence_after_sync();
+                const uint32_t v_addr = st_addr + (g % kStages) * kStageBytes + 2 * kKVHalf;
+#pragma unroll
+                for (int kk = 0; kk < kBT / 16; ++kk) {
+                    const uint64_t ad = umma::smem_desc_sw128(p_addr + pb * kPBytes + kk * 32, 16, 1024);
+                    const uint64_t bd = umma::smem_desc_sw128(v_addr + kk * 2048, kKVHalf, 1024);
+                    umma::mma_bf16_ss(tO, ad, bd, kIdescPV, (first && kk == 0) ? 0u : 1u);
+                }
+                umma::mma_commit(&B.pv_done[pb]);
+                umma::mma_commit(&B.empty[g % kStages]);
+            };
+            for (int it = it0; it < it1; ++it, ++n) {
+                const WorkItem w = a.items[it];
+                mbar_wait(B.q_ready, n & 1);
+                for (int i = 0; i < w.nblk; ++i, ++gi) {
+                    const int st = gi % kStages;
+                    const uint32_t sb = gi & 1;
+                    mbar_wait(&B.full[st], (gi / kStages) & 1);
+                    mbar_wait(&B.s_free[sb], ((gi >> 1) & 1) ^ 1);
+                    umma::fence_after_sync();
+                    const uint32_t k_addr = st_addr + st * kStageBytes;
+#pragma unroll
+                    for (int kk = 0; kk < kD / 16; ++kk) {
+                        const uint32_t half = kk >> 2, off = (kk & 3) * 32;
+                        const uint64_t ad = umma::smem_desc_sw128(q_addr + half * kQHalf + off, 16, 1024);
+                        const uint64_t bd = umma::smem_desc_sw128(k_addr + half * kKVHalf + off, 16, 1024);
+                        umma::mma_bf16_ss(tS0 + sb * 64, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+                    }
+                    umma::mma_commit(&B.s_full[sb]);
+                    if (i > 0) issue_pv(gi - 1, i == 1);
+                }
+                if (w.nblk > 0) issue_pv(gi - 1, w.nblk == 1);
+            }
+        }
+    } else {
+        // ========================= softmax + epilogue =========================
+        const int row = threadIdx.x;  // 0..63 ; TMEM lane = row
+        const uint32_t lane_off = uint32_t(warp * 32) << 16;
+        const float scale = a.q_scale;  // log2(e)/sqrt(d)
+        uint32_t gi = 0, n = 0;
+        for (int it = it0; it < it1; ++it, ++n) {
+            const WorkItem w = a.items[it];
+            const int64_t q0 = a.q_pos[w.b];
+            const bool valid_row = row < rows;
+            const int qi = row / G, h = w.g * G + row % G;
+            const int64_t my_qpos = q0 + qi;
+
+            // ---- Q tile: this row, swizzled K-major, two 64-element halves ----
+            {
+                const uint8_t* src = static_cast<const uint8_t*>(a.q) +
+                                     ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD * 2;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (valid_row) v = *reinterpret_cast<const uint4*>(src + c * 16);
+                    *reinterpret_cast<uint4*>(sQ + (c >> 3) * kQHalf + swz(row, c & 7)) = v;
+                }
+                umma::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(B.q_ready);
+            }
+
+            float m_used = -INFINITY, l = 0.f;
+            BlockWalker wk;
+            wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
+            for (int i = 0; i < w.nblk; ++i, ++gi, wk.next()) {
+                const uint32_t sb = gi & 1, pb = gi & 1;
+                const int nv = wk.nv();
+                const int64_t pos = wk.pos();
+
+                // ---- S row from TMEM ----
+                mbar_wait(&B.s_full[sb], (gi >> 1) & 1);
+                umma::fence_after_sync();
+                uint32_t s0[32], s1[32];
+                umma::tmem_ld32(tS0 + sb * 64 + lane_off, s0);
+                umma::tmem_ld32(tS0 + sb * 64 + 32 + lane_off, s1);
+                umma::tmem_wait_ld();
+                umma::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&B.s_free[sb]);
+
+                float sc[64];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    sc[j] = __uint_as_float(s0[j]) * scale;
+                    sc[32 + j] = __uint_as_float(s1[j]) * scale;
+                }
+                const bool full_vis = nv == kBT && pos + kBT - 1 <= q0;
+                if (!full_vis) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j)
+                        if (!(j < nv && pos + j <= my_qpos)) sc[j] = -INFINITY;
+                }
+                float bmax = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) bmax = fmaxf(bmax, sc[j]);
+                if (!valid_row) bmax = -INFINITY;
+                // lazy max: move it only when the block exceeds it by > 2^kLazy
+                float corr = 1.f;
+                bool move = bmax > m_used + kLazy;
+                if (move) {
+                    corr = m_used == -INFINITY ? 0.f : fast_exp2(m_used - bmax);
+                    m_used = bmax;
+                }
+                const float mu = m_used == -INFINITY ? 0.f : m_used;
+                float rs = 0.f;
+                uint32_t pk[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float p0 = fast_exp2(sc[2 * j] - mu), p1 = fast_exp2(sc[2 * j + 1] - mu);
+                    rs += p0 + p1;
+                    pk[j] = pack_bf16(p0, p1);
+                }
+                l = l * corr + rs;
+
+                // P buffer pb is free once PV(gi-2) completed.
+                mbar_wait(&B.pv_done[pb], ((gi >> 1) & 1) ^ 1);
+                // O rescale (warp-uniform: tcgen05.ld/st are warp-collective);
+                // needs PV(gi-1) complete. Block 0 of an item needs none: its PV
+                // overwrites O.
+                if (i > 0 && __any_sync(0xffffffffu, move)) {
+                    const uint32_t pg = gi - 1;
+                    mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
+                    umma::fence_after_sync();
+#pragma unroll
+                    for (int cblk = 0; cblk < 4; ++cblk) {
+                        uint32_t o[32];
+                        umma::tmem_ld32(tO + cblk * 32 + lane_off, o);
+                        umma::tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * corr);
+                        umma::tmem_st32(tO + cblk * 32 + lane_off, o);
+                    }
+                    umma::tmem_wait_st();
+                }
+                uint8_t* prow = sP + pb * kPBytes;
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    *reinterpret_cast<uint4*>(prow + swz(row, c)) =
+                        make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                if (nv < kBT) {
+                    // Tail rows of V in the stage are stale page slots: zero them
+                    // so 0 * garbage cannot reach the PV accumulator.
+                    const int st = gi % kStages;
+                    mbar_wait(&B.full[st], (gi / kStages) & 1);
+                    uint8_t* vs = sStage + st * kStageBytes + 2 * kKVHalf;
+                    const int n_chunks = (kBT - nv) * 8;
+                    for (int c = row; c < 2 * n_chunks; c += kSoftThreads) {
+                        const int hsel = c / n_chunks, cc = c % n_chunks;
+                        *reinterpret_cast<uint4*>(vs + hsel * kKVHalf + nv * 128 + cc * 16) =
+                            make_uint4(0, 0, 0, 0);
+                    }
+                }
+                umma::fence_proxy_async_smem();
+                umma::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&B.p_full[pb]);
+            }
+
+            // ---- epilogue: O row / l, direct or partial + fused merge ----
+            float o[128];
+            if (w.nblk > 0) {
+                const uint32_t pg = gi - 1;
+                mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
+                umma::fence_after_sync();
+#pragma unroll
+                for (int cblk = 0; cblk < 4; ++cblk) {
+                    uint32_t r32[32];
+                    umma::tmem_ld32(tO + cblk * 32 + lane_off, r32);
+                    umma::tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) o[cblk * 32 + j] = __uint_as_float(r32[j]);
+                }
+            }
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(B.o_free);
+
+            const int unit = w.b * Hkv + w.g;
+            const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
+            const bool empty_row = !(l > 0.f);
+            const float inv = empty_row ? 0.f : 1.f / l;
+            const float lse2 = empty_row ? -INFINITY : m_used + fast_log2(l);
+            if (valid_row) {
+                if (n_items == 1) {
+                    const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
+                    if (a.o_dtype == EP_BF16) {
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD);
+#pragma unroll
+                        for (int c = 0; c < 16; ++c)
+                            dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
+                                                pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
+                                                pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
+                                                pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+                    } else {
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow * kD);
+#pragma unroll
+                        for (int c = 0; c < 32; ++c)
+                            dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
+                                                 o[4 * c + 3] * inv);
+                    }
+                    if (a.lse) a.lse[orow] = lse2 * kLn2;
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(a.o_part + (size_t(it) * rows + row) * kD);
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
+                                             o[4 * c + 3] * inv);
+                    a.lse_part[size_t(it) * rows + row] = lse2;
+                }
+            }
+            if (n_items > 1) {
+                __threadfence();
+                named_bar_sync(1, kSoftThreads);
+                if (threadIdx.x == 0) *s_flag = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
+                named_bar_sync(1, kSoftThreads);
+                if (*s_flag) {
+                    __threadfence();
+                    for (int idx = threadIdx.x; idx < rows * kD; idx += kSoftThreads) {
+                        const int r = idx / kD, c = idx % kD;
+                        float M = -INFINITY;
+                        for (int i2 = u0; i2 < u0 + n_items; ++i2)
+                            M = fmaxf(M, __ldcg(&a.lse_part[size_t(i2) * rows + r]));
+                        float Ls = 0.f, acc = 0.f;
+                        if (M != -INFINITY) {
+                            for (int i2 = u0; i2 < u0 + n_items; ++i2) {
+                                const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i2) * rows + r]) - M);
+                                Ls += wt;
+                                acc += wt * __ldcg(&a.o_part[(size_t(i2) * rows + r) * kD + c]);
+                            }
+                        }
+                        const bool er = !(Ls > 0.f);
+                        const int qi2 = r / G, h2 = w.g * G + r % G;
+                        const size_t orow = (size_t(w.b) * a.n_q + qi2) * a.n_q_heads + h2;
+                        const float val = er ? 0.f : acc / Ls;
+                        if (a.o_dtype == EP_BF16)
+                            static_cast<__nv_bfloat16*>(a.o)[orow * kD + c] = __float2bfloat16_rn(val);
+                        else
+                            static_cast<float*>(a.o)[orow * kD + c] = val;
+                        if (c == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (M + fast_log2(Ls)) * kLn2;
+                    }
+                    if (threadIdx.x == 0) a.unit_counter[unit] = 0;
+                }
+                named_bar_sync(1, kSoftThreads);
+            }
+        }
+    }
+
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == 3) {
+        umma::fence_after_sync();
+        umma::tmem_dealloc(tmem, 256);
+    }
+}
+
+}  // namespace
+
+bool verify_supported(int kv_dtype, int d_head, int rows) {
+    return kv_dtype == EP_BF16 && d_head == kD && rows >= 1 && rows <= kSoftThreads;
+}
+
+cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUtensorMap& tk,
+                                    const CUtensorMap& tv, int rows, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(verify_attention_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows);
+    return cudaGetLastError();
+}
+
+}  // namespace ep

@@ -69,6 +69,16 @@ SMALL_CASES = {
     "gqa2_f32_d128_nq2": dict(kv_dtype=O.DT_F32, n_q_heads=4, n_kv_heads=2, d=128, n_q=2,
                               requests=[[(CLOUD, 200, None), (EDGE, 70, None), (GEN, 2, None)],
                                         [(EDGE, 3, None)]]),
+    # speculative verify (n_q = k+1 causal rows over the last n_q keys):
+    # the tcgen05 path (rows = 4*5 = 20 and 4*9 = 36)
+    "gqa4_bf16_verify_k4": dict(kv_dtype=O.DT_BF16, n_q_heads=8, n_kv_heads=2, d=128, n_q=5,
+                                requests=[[(CLOUD, 300, "c"), (EDGE, 37, None), (GEN, 12, None)],
+                                          [(CLOUD, 300, "c"), (EDGE, 130, None), (GEN, 5, None)],
+                                          [(EDGE, 5, None)],
+                                          [(CLOUD, 64, None), (EDGE, 64, None), (GEN, 64, None)]]),
+    "gqa4_bf16_verify_k8": dict(kv_dtype=O.DT_BF16, n_q_heads=8, n_kv_heads=2, d=128, n_q=9,
+                                requests=[[(CLOUD, 700, None), (EDGE, 90, None), (GEN, 20, None)],
+                                          [(EDGE, 9, None)]]),
     "gqa4_bf16_d64_nq2": dict(kv_dtype=O.DT_BF16, n_q_heads=8, n_kv_heads=2, d=64, n_q=2,
                               requests=[[(CLOUD, 129, "c"), (EDGE, 65, None), (GEN, 9, None)],
                                         [(CLOUD, 129, "c"), (EDGE, 2, None)]]),

@@ -178,7 +178,7 @@ def test_plan_rejects_bad_tables(cuda_handle):
                                     indptr.ctypes.data, segs.ctypes.data, pt_bad.ctypes.data,
                                     table.q_pos.ctypes.data, 0, C.byref(plan))
     assert rc == _capi.EP_EINVAL
-    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 3, table.batch,
+    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 17, table.batch,
                                     indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
                                     table.q_pos.ctypes.data, 0, C.byref(plan))
-    assert rc == _capi.EP_EUNSUPPORTED  # rows = 4*3 = 12 has no CUDA-core instance
+    assert rc == _capi.EP_EUNSUPPORTED  # rows = 4*17 = 68 > 64: no kernel instance
