@@ -160,6 +160,30 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
  * only, which ep_merge_partials_dev (or ep_splitkv_combine in the NCCL build)
  * recombines in rank = segment order. */
 
+/* ---- Speculative verify: fused score + greedy accept (K4) ----------- */
+/* Constructed from prefill + unembed_logits + argmax_token (model.cpp:211-255,
+ * SURVEY a16): for verify row j of a request (the last accepted token, then
+ * drafts d1..dk), g_j = argmax(LayerNorm(attn_row_j) @ W_score), ties to the
+ * lowest id; accepted n = largest n <= k with d_i == g_{i-1} for all i <= n
+ * (emit d1..dn, then g_n). */
+typedef struct ep_verifier_s* ep_verifier;
+
+/* w_score_t: device bf16 [vocab][width] (W_score transposed, K-major), kept
+ * by reference; width % 64 == 0, vocab % 256 == 0. */
+int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_score_t,
+                       ep_verifier* out);
+int ep_verifier_destroy(ep_verifier v);
+
+/* attn_out: device [batch * n_q][width] in attn_dtype (the ep_spliced_attention
+ * output [batch][n_q][n_q_heads][d], width = n_q_heads * d). EP_F32 (preferred)
+ * is scored as a bf16 hi+lo pair at ~fp32 accuracy; EP_BF16 in one pass.
+ * drafts [batch][n_q-1], target_ids [batch][n_q], n_accepted [batch] (device
+ * int32). logits: NULL, or a device fp32 [batch * n_q][vocab] buffer receiving
+ * LayerNorm(row) @ W_score (diagnostics). */
+int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int32_t attn_dtype,
+                     const void* attn_out, const int32_t* drafts, int32_t* target_ids,
+                     int32_t* n_accepted, float* logits, ep_stream stream);
+
 /* Appends n_tok token rows per request into the pool (the device form of
  * SegmentedCache::append_generated_token, cache.cpp:55-80, without its
  * whole-segment copy). k_new/v_new: [n_rows][n_kv_heads][d_head] in the pool

@@ -96,11 +96,15 @@ _SIGS = {
     "ep_kv_append": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp, _vp, _vp, _vp]),
 }
 
+_SIGS.update({
+    "ep_verifier_create": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
+    "ep_verifier_destroy": (C.c_int, [_vp]),
+    "ep_verify_greedy": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, C.c_int32, _vp, _vp, _vp,
+                                   _vp, _vp, _vp]),
+})
+
 # Optional entry points (present when the corresponding kernels are built).
-_OPTIONAL_SIGS = {
-    "ep_verify_greedy": (C.c_int, [_vp, _vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp,
-                                   C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp]),
-}
+_OPTIONAL_SIGS: dict = {}
 
 
 def lib() -> C.CDLL:

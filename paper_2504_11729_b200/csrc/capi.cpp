@@ -96,7 +96,10 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
+// A row-major bf16 matrix [outer][inner] with box [box_outer][box_inner],
+// 128B swizzle (box_inner * 2 == 128).
+int encode_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint32_t box_inner, uint32_t box_outer) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -106,18 +109,22 @@ int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
             return fail(EP_ECUDA, "cuTensorMapEncodeTiled unavailable");
         fn = reinterpret_cast<EncodeTiledFn>(f);
     }
-    // The pool as a 2-D tensor of 128-element bf16 rows (one row per
-    // (page, head, slot)); 64 x 64 boxes, 128B swizzle = the UMMA K-major
-    // (K tiles) / MN-major (V tiles) canonical layouts.
-    const cuuint64_t dims[2] = {128, cuuint64_t(rows)};
-    const cuuint64_t strides[1] = {256};
-    const cuuint32_t box[2] = {64, 64};
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {inner * 2};
+    const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(EP_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     return EP_OK;
+}
+
+// The KV pool as a 2-D tensor of 128-element bf16 rows (one row per (page,
+// head, slot)); 64 x 64 boxes with 128B swizzle are exactly the UMMA K-major
+// (K tiles) / MN-major (V tiles) canonical layouts.
+int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
+    return encode_bf16_2d(map, base, 128, uint64_t(rows), 64, 64);
 }
 
 bool force_tc() {
@@ -591,6 +598,84 @@ int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int3
                                  static_cast<cudaStream_t>(stream)),
                 "ep_kv_append launch");
     if (n_rows > 0) h->launches++;
+    return EP_OK;
+}
+
+// ------------------------------------------------------- verify (K4) --
+
+struct ep_verifier_s {
+    ep_handle h = nullptr;
+    int32_t width = 0, vocab = 0;
+    const void* w_t = nullptr;
+    CUtensorMap tmap_w{};
+    DeviceBuffer colsum, mean, rstd, best, split;
+    CUtensorMap tmap_a{};
+    const void* a_ptr = nullptr;
+    int32_t a_rows = -1, a_dtype = -1;
+};
+
+int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_score_t,
+                       ep_verifier* out) {
+    if (!h || !out || !w_score_t) return fail(EP_EINVAL, "ep_verifier_create: null argument");
+    *out = nullptr;
+    if (width <= 0 || width % 64 || vocab <= 0 || vocab % 256)
+        return fail(EP_EUNSUPPORTED, "ep_verifier_create: width must be a multiple of 64 and vocab of 256");
+    std::unique_ptr<ep_verifier_s> v(new (std::nothrow) ep_verifier_s());
+    if (!v) return fail(EP_ENOMEM, "ep_verifier_create");
+    v->h = h;
+    v->width = width;
+    v->vocab = vocab;
+    v->w_t = w_score_t;
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_verifier_create");
+    if (int rc = encode_bf16_2d(&v->tmap_w, w_score_t, uint64_t(width), uint64_t(vocab), 64, 256)) return rc;
+    EP_CUDA_TRY(v->colsum.reserve(size_t(vocab) * sizeof(float)), "ep_verifier_create colsum");
+    EP_CUDA_TRY(launch_colsum(w_score_t, width, vocab, static_cast<float*>(v->colsum.ptr), h->stream),
+                "colsum launch");
+    h->launches++;
+    EP_CUDA_TRY(cudaStreamSynchronize(h->stream), "ep_verifier_create sync");
+    *out = v.release();
+    return EP_OK;
+}
+
+int ep_verifier_destroy(ep_verifier v) {
+    delete v;
+    return EP_OK;
+}
+
+int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int32_t attn_dtype,
+                     const void* attn_out, const int32_t* drafts, int32_t* target_ids,
+                     int32_t* n_accepted, float* logits, ep_stream stream) {
+    if (!h || !v || !attn_out || !target_ids || !n_accepted || (n_q > 1 && !drafts))
+        return fail(EP_EINVAL, "ep_verify_greedy: null argument");
+    if (batch <= 0 || n_q <= 0) return fail(EP_EINVAL, "ep_verify_greedy: batch/n_q");
+    if (attn_dtype != EP_F32 && attn_dtype != EP_BF16)
+        return fail(EP_EUNSUPPORTED, "ep_verify_greedy: attn_out must be f32 or bf16");
+    const int32_t rows = batch * n_q;
+    EP_CUDA_TRY(v->mean.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
+    EP_CUDA_TRY(v->rstd.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
+    EP_CUDA_TRY(v->best.reserve(size_t(rows) * sizeof(unsigned long long)), "ep_verify_greedy ws");
+    void* split = nullptr;
+    const void* a_src = attn_out;
+    uint64_t a_inner = uint64_t(v->width);
+    if (attn_dtype == EP_F32) {
+        EP_CUDA_TRY(v->split.reserve(size_t(rows) * 2 * v->width * 2), "ep_verify_greedy ws");
+        split = v->split.ptr;
+        a_src = split;
+        a_inner = 2 * uint64_t(v->width);
+    }
+    if (v->a_ptr != a_src || v->a_rows != rows || v->a_dtype != attn_dtype) {
+        if (int rc = encode_bf16_2d(&v->tmap_a, a_src, a_inner, uint64_t(rows), 64, 128)) return rc;
+        v->a_ptr = a_src;
+        v->a_rows = rows;
+        v->a_dtype = attn_dtype;
+    }
+    EP_CUDA_TRY(launch_score_accept(rows, v->width, v->vocab, attn_out, split, v->tmap_a, v->tmap_w,
+                                    static_cast<const float*>(v->colsum.ptr),
+                                    static_cast<float*>(v->mean.ptr), static_cast<float*>(v->rstd.ptr),
+                                    static_cast<unsigned long long*>(v->best.ptr), logits, batch, n_q,
+                                    drafts, target_ids, n_accepted, static_cast<cudaStream_t>(stream)),
+                "score/accept launch");
+    h->launches += 3;
     return EP_OK;
 }
 

@@ -107,4 +107,13 @@ bool verify_supported(int kv_dtype, int d_head, int rows);
 cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUtensorMap& tk,
                                     const CUtensorMap& tv, int rows, cudaStream_t s);
 
+// K4: score GEMM (tcgen05) + LN-folded argmax + greedy accept.
+cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, cudaStream_t s);
+cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn_out, void* split,
+                                const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
+                                const float* colsum, float* mean, float* rstd,
+                                unsigned long long* best, float* logits, int batch, int n_q,
+                                const int32_t* drafts, int32_t* target, int32_t* n_accepted,
+                                cudaStream_t s);
+
 }  // namespace ep

@@ -9,7 +9,7 @@
 // share every K/V byte; at 20-36 FLOP/B that is beyond the CUDA cores, so:
 //
 //   QK^T : S[128 x 64]  (TMEM, fp32) = Q[128 x 128] (smem) . K[64 keys x 128]^T
-//   PV   : O[128 x 128] (TMEM, fp32) += P[128 x 64] (smem, bf16) . V[64 x 128]
+//   PV   : O[128 x 128] (TMEM, fp32) += (P_hi + P_lo)[128 x 64] (smem, 2 x bf16) . V[64 x 128]
 //
 // tcgen05.mma M=128 (rows >= R are padding; the M=128 issue rate equals
 // M=64's), operands staged by TMA with 128B swizzle straight from the paged
@@ -39,7 +39,7 @@ namespace {
 constexpr int kBT = 64;        // keys per block
 constexpr int kD = 128;        // head dim
 constexpr int kM = 128;        // UMMA M (rows, padded)
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kThreads = 128;
 constexpr int kSoftThreads = 64;  // rows 0..63
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
@@ -48,10 +48,11 @@ constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
 constexpr int kKVHalf = kBT * 128;         // 8 KB: 64 rows x 64 bf16
 constexpr int kStageBytes = 4 * kKVHalf;   // K0 K1 V0 V1
 constexpr int kPBytes = kM * 128;          // 16 KB: 128 rows x 64 keys bf16
+constexpr int kPBuf = 2 * kPBytes;         // hi and lo halves of one P tile
 constexpr int OFF_Q = 0;
 constexpr int OFF_STAGE = 2 * kQHalf;
 constexpr int OFF_P = OFF_STAGE + kStages * kStageBytes;
-constexpr int OFF_BAR = OFF_P + 2 * kPBytes;
+constexpr int OFF_BAR = OFF_P + 2 * kPBuf;
 constexpr int kNumBars = 2 * kStages + 2 + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
 constexpr int kSmem = OFF_MISC + 32 + 1024;  // + alignment slack
@@ -183,12 +184,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (first) mbar_wait(B.o_free, (n & 1) ^ 1);
                 umma::fence_after_sync();
                 const uint32_t v_addr = st_addr + (g % kStages) * kStageBytes + 2 * kKVHalf;
+                // P = hi + lo (two bf16 tiles): O += P_hi V + P_lo V keeps the
+                // probabilities at ~2^-17 relative instead of bf16's 2^-9.
 #pragma unroll
-                for (int kk = 0; kk < kBT / 16; ++kk) {
-                    const uint64_t ad = umma::smem_desc_sw128(p_addr + pb * kPBytes + kk * 32, 16, 1024);
-                    const uint64_t bd = umma::smem_desc_sw128(v_addr + kk * 2048, kKVHalf, 1024);
-                    umma::mma_bf16_ss(tO, ad, bd, kIdescPV, (first && kk == 0) ? 0u : 1u);
-                }
+                for (int part = 0; part < 2; ++part)
+#pragma unroll
+                    for (int kk = 0; kk < kBT / 16; ++kk) {
+                        const uint64_t ad = umma::smem_desc_sw128(
+                            p_addr + pb * kPBuf + part * kPBytes + kk * 32, 16, 1024);
+                        const uint64_t bd = umma::smem_desc_sw128(v_addr + kk * 2048, kKVHalf, 1024);
+                        umma::mma_bf16_ss(tO, ad, bd, kIdescPV, (first && part == 0 && kk == 0) ? 0u : 1u);
+                    }
                 umma::mma_commit(&B.pv_done[pb]);
                 umma::mma_commit(&B.empty[g % kStages]);
             };
@@ -287,12 +293,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const float mu = m_used == -INFINITY ? 0.f : m_used;
                 float rs = 0.f;
-                uint32_t pk[32];
+                uint32_t pk[32], pl[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
                     const float p0 = fast_exp2(sc[2 * j] - mu), p1 = fast_exp2(sc[2 * j + 1] - mu);
                     rs += p0 + p1;
                     pk[j] = pack_bf16(p0, p1);
+                    const float2 hi = bf16x2_to_float2(pk[j]);
+                    pl[j] = pack_bf16(p0 - hi.x, p1 - hi.y);
                 }
                 l = l * corr + rs;
 
@@ -316,11 +324,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     umma::tmem_wait_st();
                 }
-                uint8_t* prow = sP + pb * kPBytes;
+                uint8_t* prow = sP + pb * kPBuf;
 #pragma unroll
-                for (int c = 0; c < 8; ++c)
+                for (int c = 0; c < 8; ++c) {
                     *reinterpret_cast<uint4*>(prow + swz(row, c)) =
                         make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                    *reinterpret_cast<uint4*>(prow + kPBytes + swz(row, c)) =
+                        make_uint4(pl[4 * c], pl[4 * c + 1], pl[4 * c + 2], pl[4 * c + 3]);
+                }
                 if (nv < kBT) {
                     // Tail rows of V in the stage are stale page slots: zero them
                     // so 0 * garbage cannot reach the PV accumulator.

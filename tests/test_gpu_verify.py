@@ -53,3 +53,62 @@ def test_tc_path_on_decode_rows_matches_golden():
                        timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     print(r.stdout)
+
+
+@pytest.mark.parametrize("k", [4, 8])
+def test_verify_greedy_accept_bit_exact(cuda_handle, k):
+    """Full verify step (K3 attention + K4 score/argmax/accept) against the
+    fp64 oracle (spliced attention -> LN -> @W_score -> argmax -> accept rule).
+    Drafts follow the oracle's own targets with a seeded forced mismatch per
+    request, so every acceptance length 0..k occurs. Rows whose oracle top-2
+    logit gap is below 8x the measured max |logit error| are margin-guarded
+    (SURVEY §8a); all other target ids and every accepted count must be
+    bit-exact."""
+    import torch
+    from paper_2504_11729_b200.verify import VerifyGreedy
+    from tests.gpu_util import torch_from_raw
+    B, Hq, Hkv, d, V = 8, 32, 8, 128, 4096
+    n_q = k + 1
+    reqs = [[(SC.CLOUD, 1024 + 64 * b, None), (SC.EDGE, 200 + b, None), (SC.GEN, 64, None)]
+            for b in range(B)]
+    sb = SC.make_case(O.DT_BF16, Hq, Hkv, d, reqs, n_q=n_q, seed=33 + k)
+    _, _, attn, q = to_device(sb, cuda_handle)
+    o, _ = attn(q, o_dtype=torch.float32)  # [B][n_q][Hq][d], scored as bf16 hi+lo
+
+    W = O.fill_uniform(O.DT_BF16, Hq * d * V, 33).reshape(Hq * d, V)   # [width][vocab]
+    w_t = torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16)         # [vocab][width]
+    ver = VerifyGreedy(w_t, handle=cuda_handle)
+
+    want_o, _ = O.spliced_attention(sb, n_threads=os.cpu_count() or 4)
+    attn64 = want_o.reshape(B, n_q, Hq * d)
+    W64 = O.bf16_to_f64(W)
+    g_ref, _, gap = O.verify_greedy(attn64, W64, np.zeros((B, k), np.int32))
+    drafts = g_ref[:, :k].copy()
+    for b in range(B):
+        a = b % (k + 1)              # force acceptance length a
+        if a < k:
+            drafts[b, a] = (g_ref[b, a] + 1) % V
+            drafts[b, a + 1:] = (g_ref[b, a + 1:k] + 7) % V
+    g_ref, nacc_ref, gap = O.verify_greedy(attn64, W64, drafts)
+
+    tgt, nacc, logits = ver(o, torch.from_numpy(drafts).cuda(), logits=True)
+    torch.cuda.synchronize()
+    tgt, nacc = tgt.cpu().numpy(), nacc.cpu().numpy()
+    # oracle logits for the margin guard
+    ref_logits = np.zeros((B, n_q, V))
+    for b in range(B):
+        for j in range(n_q):
+            x = attn64[b, j]
+            xn = (x - x.mean()) / np.sqrt(x.var() + 1e-5)
+            ref_logits[b, j] = xn @ W64
+    err = float(np.max(np.abs(logits.cpu().numpy() - ref_logits)))
+    guarded = gap < 8 * err
+    print(f"k={k}: max |logit err| {err:.3e}, guarded rows {int(guarded.sum())}/{B * n_q}")
+    assert guarded.mean() < 0.1
+    ok_rows = ~guarded
+    assert np.array_equal(tgt[ok_rows], g_ref[ok_rows])
+    # accepted counts: bit-exact wherever no guarded row decides them
+    for b in range(B):
+        if not guarded[b, :min(nacc_ref[b] + 1, k)].any():
+            assert nacc[b] == nacc_ref[b], (b, nacc[b], nacc_ref[b])
+    assert sorted(set(nacc_ref.tolist())) == list(range(min(B, k + 1)))
