@@ -16,13 +16,15 @@
 // pool (the [page][head][token][d] tile is a 2-D tensor of 128-element rows).
 // Warp roles (128 threads, one CTA per SM, persistent over the planner's page
 // ranges like K1):
-//   warp 2 lane 0 : TMA producer (K and V boxes, S-stage ring)
-//   warp 3 lane 0 : MMA issuer; warp 3 owns the TMEM allocation
-//   warps 0-1     : softmax + epilogue, one thread per query row: tcgen05.ld
-//                   of the S row, causal/tail mask, exp2, bf16 P row written
-//                   swizzled to smem. Rescaling is lazy (FA4-style): the row
-//                   max is only moved when it grows by > 2^8, then the O row
-//                   is rescaled in TMEM (tcgen05.ld/st); otherwise P <= 256.
+//   warp 8 lane 0 : TMA producer (K and V boxes, S-stage ring)
+//   warp 9 lane 0 : MMA issuer; warp 9 owns the TMEM allocation
+//   warps 0-7     : softmax + epilogue. Query rows are spread over the four
+//                   TMEM lane quarters (row v -> M row 32*(v%4) + v/4) so all
+//                   four SMSPs work, and each row's 64 keys are split between
+//                   warps q and q+4: tcgen05.ld of 32 scores, causal/tail mask,
+//                   exp2, P written as bf16 hi+lo, swizzled. Rescaling is lazy
+//                   (FA4-style): the row max only moves when it grows by > 2^8,
+//                   then O is rescaled in TMEM (tcgen05.ld/st); else P <= 256.
 // QK of block i+1 is issued before PV of block i so the tensor core overlaps
 // the softmax. Items that split a (request, kv-head) merge by LSE through the
 // same per-unit counter protocol as K1.
@@ -40,8 +42,11 @@ constexpr int kBT = 64;        // keys per block
 constexpr int kD = 128;        // head dim
 constexpr int kM = 128;        // UMMA M (rows, padded)
 constexpr int kStages = 3;
-constexpr int kThreads = 128;
-constexpr int kSoftThreads = 64;  // rows 0..63
+constexpr int kSoftWarps = 8;  // 4 TMEM lane quarters x 2 column halves
+constexpr int kSoftThreads = kSoftWarps * 32;
+constexpr int kProdWarp = 8, kMmaWarp = 9;
+constexpr int kThreads = 320;
+constexpr int kMaxRows = 64;      // valid query rows per (request, kv-head)
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
 
 constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
@@ -52,7 +57,9 @@ constexpr int kPBuf = 2 * kPBytes;         // hi and lo halves of one P tile
 constexpr int OFF_Q = 0;
 constexpr int OFF_STAGE = 2 * kQHalf;
 constexpr int OFF_P = OFF_STAGE + kStages * kStageBytes;
-constexpr int OFF_BAR = OFF_P + 2 * kPBuf;
+constexpr int OFF_XCH = OFF_P + 2 * kPBuf;           // [2 parity][2 halves][128] row-max exchange
+constexpr int OFF_LX = OFF_XCH + 2 * 2 * kM * 4;      // [2 halves][128] row-sum exchange
+constexpr int OFF_BAR = OFF_LX + 2 * kM * 4;
 constexpr int kNumBars = 2 * kStages + 2 + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
 constexpr int kSmem = OFF_MISC + 32 + 1024;  // + alignment slack
@@ -92,7 +99,7 @@ struct BlockWalker {
         t0 = 0;
         if (lp < lp1) cur = pd[lp];
     }
-    // current block: page, token offset in page, valid rows, absolute position
+    // current block: valid rows and absolute position of its first key
     __device__ int nv() const { return min(kBT, cur.n_tok - t0); }
     __device__ int64_t pos() const { return cur.pos + t0; }
     __device__ void next() {
@@ -104,6 +111,10 @@ struct BlockWalker {
     }
 };
 
+// Query row v of a (request, kv-head) lives in M row 32*(v%4) + v/4, so the
+// R valid rows spread over all four TMEM lane quarters (= all four SMSPs:
+// a warp reads only the quarter warp%4); each row's 64 keys are split between
+// warps q and q+4 (32 columns each).
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v, int rows) {
@@ -113,6 +124,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sQ = smem + OFF_Q;
     uint8_t* sStage = smem + OFF_STAGE;
     uint8_t* sP = smem + OFF_P;
+    float* xch = reinterpret_cast<float*>(smem + OFF_XCH);
+    float* lx = reinterpret_cast<float*>(smem + OFF_LX);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     Bars B{bar, bar + kStages, bar + 2 * kStages, bar + 2 * kStages + 2, bar + 2 * kStages + 4,
            bar + 2 * kStages + 6, bar + 2 * kStages + 8, bar + 2 * kStages + 9};
@@ -131,16 +144,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&B.s_full[i], 1);
-            mbar_init(&B.s_free[i], 2);
-            mbar_init(&B.p_full[i], 2);
+            mbar_init(&B.s_free[i], kSoftWarps);
+            mbar_init(&B.p_full[i], kSoftWarps);
             mbar_init(&B.pv_done[i], 1);
         }
-        mbar_init(B.q_ready, 2);
-        mbar_init(B.o_free, 2);
+        mbar_init(B.q_ready, kSoftWarps);
+        mbar_init(B.o_free, kSoftWarps);
         fence_mbar_init();
     }
-    if (warp == 3) umma::tmem_alloc(tmem_slot, 256);
-    if (warp == 2 && lane == 0) {
+    if (warp == kMmaWarp) umma::tmem_alloc(tmem_slot, 256);
+    if (warp == kProdWarp && lane == 0) {
         umma::tma_prefetch_desc(&tmap_k);
         umma::tma_prefetch_desc(&tmap_v);
     }
@@ -150,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = *tmem_slot;
     const uint32_t tO = tmem, tS0 = tmem + 128;
 
-    if (warp == 2) {
+    if (warp == kProdWarp) {
         // ============================== producer ==============================
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_first();
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 3) {
+    } else if (warp == kMmaWarp) {
         // ================================ MMA =================================
         if (lane == 0) {
             const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
@@ -223,26 +236,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ========================= softmax + epilogue =========================
-        const int row = threadIdx.x;  // 0..63 ; TMEM lane = row
-        const uint32_t lane_off = uint32_t(warp * 32) << 16;
+        const int quarter = warp & 3, ch = warp >> 2;  // TMEM lane quarter, column half
+        const int m = quarter * 32 + lane;              // M row = TMEM lane
+        const int v = lane * 4 + quarter;               // query row index of this M row
+        const bool valid_row = v < rows;
+        const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         const float scale = a.q_scale;  // log2(e)/sqrt(d)
+        const uint32_t pair_bar = 1 + quarter;  // named barrier of warps q and q+4
         uint32_t gi = 0, n = 0;
         for (int it = it0; it < it1; ++it, ++n) {
             const WorkItem w = a.items[it];
             const int64_t q0 = a.q_pos[w.b];
-            const bool valid_row = row < rows;
-            const int qi = row / G, h = w.g * G + row % G;
+            const int qi = v / G, h = w.g * G + v % G;
             const int64_t my_qpos = q0 + qi;
 
-            // ---- Q tile: this row, swizzled K-major, two 64-element halves ----
+            // ---- Q tile: this row's half, swizzled K-major ----
             {
                 const uint8_t* src = static_cast<const uint8_t*>(a.q) +
-                                     ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD * 2;
+                                     (((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD + ch * 64) * 2;
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    uint4 v = make_uint4(0, 0, 0, 0);
-                    if (valid_row) v = *reinterpret_cast<const uint4*>(src + c * 16);
-                    *reinterpret_cast<uint4*>(sQ + (c >> 3) * kQHalf + swz(row, c & 7)) = v;
+                for (int c = 0; c < 8; ++c) {
+                    uint4 val = make_uint4(0, 0, 0, 0);
+                    if (valid_row) val = *reinterpret_cast<const uint4*>(src + c * 16);
+                    *reinterpret_cast<uint4*>(sQ + ch * kQHalf + swz(m, c)) = val;
                 }
                 umma::fence_proxy_async_smem();
                 __syncwarp();
@@ -257,46 +273,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int nv = wk.nv();
                 const int64_t pos = wk.pos();
 
-                // ---- S row from TMEM ----
+                // ---- this thread's 32 scores of the S row ----
                 mbar_wait(&B.s_full[sb], (gi >> 1) & 1);
                 umma::fence_after_sync();
-                uint32_t s0[32], s1[32];
-                umma::tmem_ld32(tS0 + sb * 64 + lane_off, s0);
-                umma::tmem_ld32(tS0 + sb * 64 + 32 + lane_off, s1);
+                uint32_t sr[32];
+                umma::tmem_ld32(tS0 + sb * 64 + ch * 32 + lane_off, sr);
                 umma::tmem_wait_ld();
                 umma::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&B.s_free[sb]);
 
-                float sc[64];
+                float sc[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    sc[j] = __uint_as_float(s0[j]) * scale;
-                    sc[32 + j] = __uint_as_float(s1[j]) * scale;
+                for (int j = 0; j < 32; ++j) sc[j] = __uint_as_float(sr[j]);
+                if (!(nv == kBT && pos + kBT - 1 <= q0)) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int key = ch * 32 + j;
+                        if (!(key < nv && pos + key <= my_qpos)) sc[j] = -INFINITY;
+                    }
                 }
-                const bool full_vis = nv == kBT && pos + kBT - 1 <= q0;
-                if (!full_vis) {
+                float hmax = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j)
-                        if (!(j < nv && pos + j <= my_qpos)) sc[j] = -INFINITY;
-                }
-                float bmax = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 64; ++j) bmax = fmaxf(bmax, sc[j]);
-                if (!valid_row) bmax = -INFINITY;
+                for (int j = 0; j < 32; ++j) hmax = fmaxf(hmax, sc[j]);
+                if (!valid_row) hmax = -INFINITY;
+                float* xb = xch + (gi & 1) * 2 * kM;
+                xb[ch * kM + m] = hmax;
+                named_bar_sync(pair_bar, 64);
+                const float bmax = fmaxf(hmax, xb[(1 - ch) * kM + m]) * scale;
                 // lazy max: move it only when the block exceeds it by > 2^kLazy
+                // (both halves of the row take the same decision)
                 float corr = 1.f;
-                bool move = bmax > m_used + kLazy;
+                const bool move = bmax > m_used + kLazy;
                 if (move) {
                     corr = m_used == -INFINITY ? 0.f : fast_exp2(m_used - bmax);
                     m_used = bmax;
                 }
                 const float mu = m_used == -INFINITY ? 0.f : m_used;
                 float rs = 0.f;
-                uint32_t pk[32], pl[32];
+                uint32_t pk[16], pl[16];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float p0 = fast_exp2(sc[2 * j] - mu), p1 = fast_exp2(sc[2 * j + 1] - mu);
+                for (int j = 0; j < 16; ++j) {
+                    const float p0 = fast_exp2(fmaf(sc[2 * j], scale, -mu));
+                    const float p1 = fast_exp2(fmaf(sc[2 * j + 1], scale, -mu));
                     rs += p0 + p1;
                     pk[j] = pack_bf16(p0, p1);
                     const float2 hi = bf16x2_to_float2(pk[j]);
@@ -306,30 +325,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
                 // P buffer pb is free once PV(gi-2) completed.
                 mbar_wait(&B.pv_done[pb], ((gi >> 1) & 1) ^ 1);
-                // O rescale (warp-uniform: tcgen05.ld/st are warp-collective);
-                // needs PV(gi-1) complete. Block 0 of an item needs none: its PV
-                // overwrites O.
+                // O rescale of this thread's 64 O columns (warp-uniform:
+                // tcgen05.ld/st are warp-collective); needs PV(gi-1) complete.
+                // Block 0 of an item needs none: its PV overwrites O.
                 if (i > 0 && __any_sync(0xffffffffu, move)) {
                     const uint32_t pg = gi - 1;
                     mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
                     umma::fence_after_sync();
 #pragma unroll
-                    for (int cblk = 0; cblk < 4; ++cblk) {
+                    for (int cblk = 0; cblk < 2; ++cblk) {
                         uint32_t o[32];
-                        umma::tmem_ld32(tO + cblk * 32 + lane_off, o);
+                        const uint32_t ta = tO + ch * 64 + cblk * 32 + lane_off;
+                        umma::tmem_ld32(ta, o);
                         umma::tmem_wait_ld();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * corr);
-                        umma::tmem_st32(tO + cblk * 32 + lane_off, o);
+                        umma::tmem_st32(ta, o);
                     }
                     umma::tmem_wait_st();
                 }
                 uint8_t* prow = sP + pb * kPBuf;
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    *reinterpret_cast<uint4*>(prow + swz(row, c)) =
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t off = swz(m, ch * 4 + c);
+                    *reinterpret_cast<uint4*>(prow + off) =
                         make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-                    *reinterpret_cast<uint4*>(prow + kPBytes + swz(row, c)) =
+                    *reinterpret_cast<uint4*>(prow + kPBytes + off) =
                         make_uint4(pl[4 * c], pl[4 * c + 1], pl[4 * c + 2], pl[4 * c + 3]);
                 }
                 if (nv < kBT) {
@@ -339,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&B.full[st], (gi / kStages) & 1);
                     uint8_t* vs = sStage + st * kStageBytes + 2 * kKVHalf;
                     const int n_chunks = (kBT - nv) * 8;
-                    for (int c = row; c < 2 * n_chunks; c += kSoftThreads) {
+                    for (int c = threadIdx.x; c < 2 * n_chunks; c += kSoftThreads) {
                         const int hsel = c / n_chunks, cc = c % n_chunks;
                         *reinterpret_cast<uint4*>(vs + hsel * kKVHalf + nv * 128 + cc * 16) =
                             make_uint4(0, 0, 0, 0);
@@ -351,16 +372,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&B.p_full[pb]);
             }
 
-            // ---- epilogue: O row / l, direct or partial + fused merge ----
-            float o[128];
-            if (w.nblk > 0) {
+            // ---- epilogue: this thread's 64 O columns / l ----
+            float o[64];
+            {
                 const uint32_t pg = gi - 1;
                 mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
                 umma::fence_after_sync();
 #pragma unroll
-                for (int cblk = 0; cblk < 4; ++cblk) {
+                for (int cblk = 0; cblk < 2; ++cblk) {
                     uint32_t r32[32];
-                    umma::tmem_ld32(tO + cblk * 32 + lane_off, r32);
+                    umma::tmem_ld32(tO + ch * 64 + cblk * 32 + lane_off, r32);
                     umma::tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) o[cblk * 32 + j] = __uint_as_float(r32[j]);
@@ -369,45 +390,50 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(B.o_free);
+            lx[ch * kM + m] = l;
+            named_bar_sync(pair_bar, 64);
+            const float L = l + lx[(1 - ch) * kM + m];
 
             const int unit = w.b * Hkv + w.g;
             const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
-            const bool empty_row = !(l > 0.f);
-            const float inv = empty_row ? 0.f : 1.f / l;
-            const float lse2 = empty_row ? -INFINITY : m_used + fast_log2(l);
+            const bool empty_row = !(L > 0.f);
+            const float inv = empty_row ? 0.f : 1.f / L;
+            const float lse2 = empty_row ? -INFINITY : m_used + fast_log2(L);
             if (valid_row) {
                 if (n_items == 1) {
                     const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
                     if (a.o_dtype == EP_BF16) {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD);
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD + ch * 64);
 #pragma unroll
-                        for (int c = 0; c < 16; ++c)
+                        for (int c = 0; c < 8; ++c)
                             dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
                                                 pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
                                                 pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
                                                 pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
                     } else {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow * kD);
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow * kD + ch * 64);
 #pragma unroll
-                        for (int c = 0; c < 32; ++c)
+                        for (int c = 0; c < 16; ++c)
                             dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
                                                  o[4 * c + 3] * inv);
                     }
-                    if (a.lse) a.lse[orow] = lse2 * kLn2;
+                    if (ch == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
                 } else {
-                    float4* dst = reinterpret_cast<float4*>(a.o_part + (size_t(it) * rows + row) * kD);
+                    float4* dst = reinterpret_cast<float4*>(a.o_part + (size_t(it) * rows + v) * kD + ch * 64);
 #pragma unroll
-                    for (int c = 0; c < 32; ++c)
+                    for (int c = 0; c < 16; ++c)
                         dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
                                              o[4 * c + 3] * inv);
-                    a.lse_part[size_t(it) * rows + row] = lse2;
+                    if (ch == 0) a.lse_part[size_t(it) * rows + v] = lse2;
                 }
             }
             if (n_items > 1) {
+                // Fused K2: the last CTA to finish one of this unit's items merges
+                // them in page (= segment) order (attention.cpp:128-144).
                 __threadfence();
-                named_bar_sync(1, kSoftThreads);
+                named_bar_sync(5, kSoftThreads);
                 if (threadIdx.x == 0) *s_flag = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
-                named_bar_sync(1, kSoftThreads);
+                named_bar_sync(5, kSoftThreads);
                 if (*s_flag) {
                     __threadfence();
                     for (int idx = threadIdx.x; idx < rows * kD; idx += kSoftThreads) {
@@ -435,14 +461,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if (threadIdx.x == 0) a.unit_counter[unit] = 0;
                 }
-                named_bar_sync(1, kSoftThreads);
+                named_bar_sync(5, kSoftThreads);
             }
         }
     }
 
     umma::fence_before_sync();
     __syncthreads();
-    if (warp == 3) {
+    if (warp == kMmaWarp) {
         umma::fence_after_sync();
         umma::tmem_dealloc(tmem, 256);
     }
@@ -451,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 bool verify_supported(int kv_dtype, int d_head, int rows) {
-    return kv_dtype == EP_BF16 && d_head == kD && rows >= 1 && rows <= kSoftThreads;
+    return kv_dtype == EP_BF16 && d_head == kD && rows >= 1 && rows <= kMaxRows;
 }
 
 cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUtensorMap& tk,
