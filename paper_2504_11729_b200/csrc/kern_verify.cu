@@ -41,8 +41,8 @@ namespace {
 constexpr int kBT = 64;        // keys per block
 constexpr int kD = 128;        // head dim
 constexpr int kM = 128;        // UMMA M (rows, padded)
-constexpr int kStages = 3;
-constexpr int kSoftWarps = 8;  // 4 TMEM lane quarters x 2 column halves
+constexpr int kStages = 4;
+constexpr int kSoftWarps = 8;  // 2 ping-pong groups x 4 TMEM lane quarters
 constexpr int kSoftThreads = kSoftWarps * 32;
 constexpr int kProdWarp = 8, kMmaWarp = 9;
 constexpr int kThreads = 320;
@@ -57,12 +57,15 @@ constexpr int kPBuf = 2 * kPBytes;         // hi and lo halves of one P tile
 constexpr int OFF_Q = 0;
 constexpr int OFF_STAGE = 2 * kQHalf;
 constexpr int OFF_P = OFF_STAGE + kStages * kStageBytes;
-constexpr int OFF_XCH = OFF_P + 2 * kPBuf;           // [2 parity][2 halves][128] row-max exchange
-constexpr int OFF_LX = OFF_XCH + 2 * 2 * kM * 4;      // [2 halves][128] row-sum exchange
-constexpr int OFF_BAR = OFF_LX + 2 * kM * 4;
+constexpr int OFF_XM = OFF_P + 2 * kPBuf;   // [2 groups][128] row max of each group
+constexpr int OFF_XL = OFF_XM + 2 * kM * 4; // [2 groups][128] row sum of each group
+constexpr int OFF_BAR = OFF_XL + 2 * kM * 4;
 constexpr int kNumBars = 2 * kStages + 2 + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
-constexpr int kSmem = OFF_MISC + 32 + 1024;  // + alignment slack
+constexpr int kSmem = OFF_MISC + 32;  // dynamic smem base must be 1024-aligned (checked)
+// TMEM columns: O of group 0 / 1, then S of group 0 / 1.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kColO = 0, kColS = 256;
 
 constexpr uint32_t kIdescQK = umma::idesc_bf16_f32(kM, kBT, false, false);
 constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
@@ -70,7 +73,7 @@ constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
 struct Bars {
     uint64_t* full;     // [S] TMA landed
     uint64_t* empty;    // [S] K/V stage consumed (commit after PV)
-    uint64_t* s_full;   // [2] QK result in TMEM
+    uint64_t* s_full;   // [2 groups] QK result in TMEM
     uint64_t* s_free;   // [2] softmax done reading S
     uint64_t* p_full;   // [2] P written (+ O rescaled)
     uint64_t* pv_done;  // [2] PV finished (P buffer free, O updated)
@@ -111,21 +114,25 @@ struct BlockWalker {
     }
 };
 
-// Query row v of a (request, kv-head) lives in M row 32*(v%4) + v/4, so the
-// R valid rows spread over all four TMEM lane quarters (= all four SMSPs:
-// a warp reads only the quarter warp%4); each row's 64 keys are split between
-// warps q and q+4 (32 columns each).
+// Softmax layout: query row v of a (request, kv-head) lives in M row
+// 32*(v%4) + v/4, so the valid rows spread over all four TMEM lane quarters
+// (a warp reads only quarter warp%4, i.e. its own SMSP). Ping-pong: warps
+// 0-3 (group 0) take the even key blocks of an item, warps 4-7 (group 1) the
+// odd ones, each group with its own online-softmax state, S and P buffers and
+// O accumulator in TMEM; the two states merge by LSE in the epilogue. While
+// one group waits on TMEM loads / barriers the other computes, and the tensor
+// core always has the other group's QK or PV to run.
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v, int rows) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1 KB alignment
     uint8_t* sQ = smem + OFF_Q;
     uint8_t* sStage = smem + OFF_STAGE;
     uint8_t* sP = smem + OFF_P;
-    float* xch = reinterpret_cast<float*>(smem + OFF_XCH);
-    float* lx = reinterpret_cast<float*>(smem + OFF_LX);
+    float* xm = reinterpret_cast<float*>(smem + OFF_XM);
+    float* xl = reinterpret_cast<float*>(smem + OFF_XL);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     Bars B{bar, bar + kStages, bar + 2 * kStages, bar + 2 * kStages + 2, bar + 2 * kStages + 4,
            bar + 2 * kStages + 6, bar + 2 * kStages + 8, bar + 2 * kStages + 9};
@@ -144,15 +151,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&B.s_full[i], 1);
-            mbar_init(&B.s_free[i], kSoftWarps);
-            mbar_init(&B.p_full[i], kSoftWarps);
+            mbar_init(&B.s_free[i], 4);
+            mbar_init(&B.p_full[i], 4);
             mbar_init(&B.pv_done[i], 1);
         }
         mbar_init(B.q_ready, kSoftWarps);
         mbar_init(B.o_free, kSoftWarps);
         fence_mbar_init();
     }
-    if (warp == kMmaWarp) umma::tmem_alloc(tmem_slot, 256);
+    if (warp == kMmaWarp) umma::tmem_alloc(tmem_slot, kTmemCols);
     if (warp == kProdWarp && lane == 0) {
         umma::tma_prefetch_desc(&tmap_k);
         umma::tma_prefetch_desc(&tmap_v);
@@ -161,7 +168,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tO = tmem, tS0 = tmem + 128;
 
     if (warp == kProdWarp) {
         // ============================== producer ==============================
@@ -191,12 +197,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
             const uint32_t st_addr = smem_u32(sStage);
             uint32_t gi = 0, n = 0;
-            auto issue_pv = [&](uint32_t g, bool first) {
-                const uint32_t pb = g & 1;
-                mbar_wait(&B.p_full[pb], (g >> 1) & 1);
-                if (first) mbar_wait(B.o_free, (n & 1) ^ 1);
+            uint32_t cqk[2] = {0, 0}, cpv[2] = {0, 0};  // per-group block counters
+            // PV of local block i (global gi) into O[i & 1].
+            auto issue_pv = [&](int i, uint32_t g_i) {
+                const int grp = i & 1;
+                mbar_wait(&B.p_full[grp], cpv[grp] & 1);
+                if (i == 0) mbar_wait(B.o_free, (n & 1) ^ 1);  // previous item's epilogue read O
                 umma::fence_after_sync();
-                const uint32_t v_addr = st_addr + (g % kStages) * kStageBytes + 2 * kKVHalf;
+                const uint32_t v_addr = st_addr + (g_i % kStages) * kStageBytes + 2 * kKVHalf;
                 // P = hi + lo (two bf16 tiles): O += P_hi V + P_lo V keeps the
                 // probabilities at ~2^-17 relative instead of bf16's 2^-9.
 #pragma unroll
@@ -204,61 +212,75 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int kk = 0; kk < kBT / 16; ++kk) {
                         const uint64_t ad = umma::smem_desc_sw128(
-                            p_addr + pb * kPBuf + part * kPBytes + kk * 32, 16, 1024);
+                            p_addr + grp * kPBuf + part * kPBytes + kk * 32, 16, 1024);
                         const uint64_t bd = umma::smem_desc_sw128(v_addr + kk * 2048, kKVHalf, 1024);
-                        umma::mma_bf16_ss(tO, ad, bd, kIdescPV, (first && part == 0 && kk == 0) ? 0u : 1u);
+                        umma::mma_bf16_ss(tmem + kColO + grp * kD, ad, bd, kIdescPV,
+                                          (i < 2 && part == 0 && kk == 0) ? 0u : 1u);
                     }
-                umma::mma_commit(&B.pv_done[pb]);
-                umma::mma_commit(&B.empty[g % kStages]);
+                umma::mma_commit(&B.pv_done[grp]);
+                umma::mma_commit(&B.empty[g_i % kStages]);
+                ++cpv[grp];
             };
+            // QK of local block i (global g_i) into S[i & 1].
+            auto issue_qk = [&](int i, uint32_t g_i) {
+                const int st = g_i % kStages;
+                const int grp = i & 1;
+                mbar_wait(&B.full[st], (g_i / kStages) & 1);
+                mbar_wait(&B.s_free[grp], (cqk[grp] & 1) ^ 1);
+                umma::fence_after_sync();
+                const uint32_t k_addr = st_addr + st * kStageBytes;
+#pragma unroll
+                for (int kk = 0; kk < kD / 16; ++kk) {
+                    const uint32_t half = kk >> 2, off = (kk & 3) * 32;
+                    const uint64_t ad = umma::smem_desc_sw128(q_addr + half * kQHalf + off, 16, 1024);
+                    const uint64_t bd = umma::smem_desc_sw128(k_addr + half * kKVHalf + off, 16, 1024);
+                    umma::mma_bf16_ss(tmem + kColS + grp * kBT, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+                }
+                umma::mma_commit(&B.s_full[grp]);
+                ++cqk[grp];
+            };
+            // Issue order QK(0) QK(1) | QK(i+2) PV(i) ...: a group's next S is
+            // computed as soon as it has read its current S, so the softmax of
+            // block i+2 can start the moment block i's is done.
             for (int it = it0; it < it1; ++it, ++n) {
                 const WorkItem w = a.items[it];
                 mbar_wait(B.q_ready, n & 1);
-                for (int i = 0; i < w.nblk; ++i, ++gi) {
-                    const int st = gi % kStages;
-                    const uint32_t sb = gi & 1;
-                    mbar_wait(&B.full[st], (gi / kStages) & 1);
-                    mbar_wait(&B.s_free[sb], ((gi >> 1) & 1) ^ 1);
-                    umma::fence_after_sync();
-                    const uint32_t k_addr = st_addr + st * kStageBytes;
-#pragma unroll
-                    for (int kk = 0; kk < kD / 16; ++kk) {
-                        const uint32_t half = kk >> 2, off = (kk & 3) * 32;
-                        const uint64_t ad = umma::smem_desc_sw128(q_addr + half * kQHalf + off, 16, 1024);
-                        const uint64_t bd = umma::smem_desc_sw128(k_addr + half * kKVHalf + off, 16, 1024);
-                        umma::mma_bf16_ss(tS0 + sb * 64, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
-                    }
-                    umma::mma_commit(&B.s_full[sb]);
-                    if (i > 0) issue_pv(gi - 1, i == 1);
+                for (int i = 0; i < 2 && i < w.nblk; ++i) issue_qk(i, gi + i);
+                for (int i = 0; i < w.nblk; ++i) {
+                    if (i + 2 < w.nblk) issue_qk(i + 2, gi + i + 2);
+                    issue_pv(i, gi + i);
                 }
-                if (w.nblk > 0) issue_pv(gi - 1, w.nblk == 1);
+                gi += uint32_t(w.nblk);
             }
         }
     } else {
         // ========================= softmax + epilogue =========================
-        const int quarter = warp & 3, ch = warp >> 2;  // TMEM lane quarter, column half
-        const int m = quarter * 32 + lane;              // M row = TMEM lane
-        const int v = lane * 4 + quarter;               // query row index of this M row
+        const int quarter = warp & 3, grp = warp >> 2;  // TMEM lane quarter, ping-pong group
+        const int m = quarter * 32 + lane;               // M row = TMEM lane
+        const int v = lane * 4 + quarter;                // query row index of this M row
         const bool valid_row = v < rows;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+        const uint32_t tS = tmem + kColS + grp * kBT + lane_off;
+        const uint32_t tOg = tmem + kColO + grp * kD + lane_off;
         const float scale = a.q_scale;  // log2(e)/sqrt(d)
         const uint32_t pair_bar = 1 + quarter;  // named barrier of warps q and q+4
-        uint32_t gi = 0, n = 0;
+        uint32_t cnt = 0, n = 0;  // blocks processed by this group (all items)
+        uint32_t gi0 = 0;         // global index of the item's first block
         for (int it = it0; it < it1; ++it, ++n) {
             const WorkItem w = a.items[it];
             const int64_t q0 = a.q_pos[w.b];
             const int qi = v / G, h = w.g * G + v % G;
             const int64_t my_qpos = q0 + qi;
 
-            // ---- Q tile: this row's half, swizzled K-major ----
+            // ---- Q tile: group g writes K-half g of this row, swizzled ----
             {
                 const uint8_t* src = static_cast<const uint8_t*>(a.q) +
-                                     (((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD + ch * 64) * 2;
+                                     (((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint4 val = make_uint4(0, 0, 0, 0);
                     if (valid_row) val = *reinterpret_cast<const uint4*>(src + c * 16);
-                    *reinterpret_cast<uint4*>(sQ + ch * kQHalf + swz(m, c)) = val;
+                    *reinterpret_cast<uint4*>(sQ + grp * kQHalf + swz(m, c)) = val;
                 }
                 umma::fence_proxy_async_smem();
                 __syncwarp();
@@ -268,41 +290,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m_used = -INFINITY, l = 0.f;
             BlockWalker wk;
             wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
-            for (int i = 0; i < w.nblk; ++i, ++gi, wk.next()) {
-                const uint32_t sb = gi & 1, pb = gi & 1;
+            if (grp == 1) wk.next();
+            for (int i = grp; i < w.nblk; i += 2) {
                 const int nv = wk.nv();
                 const int64_t pos = wk.pos();
+                const uint32_t gi = gi0 + i;
 
-                // ---- this thread's 32 scores of the S row ----
-                mbar_wait(&B.s_full[sb], (gi >> 1) & 1);
+                // ---- the 64 scores of this row ----
+                mbar_wait(&B.s_full[grp], cnt & 1);
                 umma::fence_after_sync();
-                uint32_t sr[32];
-                umma::tmem_ld32(tS0 + sb * 64 + ch * 32 + lane_off, sr);
+                uint32_t sr[64];
+                umma::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(sr));
+                umma::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
                 umma::tmem_wait_ld();
                 umma::fence_before_sync();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&B.s_free[sb]);
+                if (lane == 0) mbar_arrive(&B.s_free[grp]);
 
-                float sc[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) sc[j] = __uint_as_float(sr[j]);
                 if (!(nv == kBT && pos + kBT - 1 <= q0)) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int key = ch * 32 + j;
-                        if (!(key < nv && pos + key <= my_qpos)) sc[j] = -INFINITY;
-                    }
+                    for (int j = 0; j < 64; ++j)
+                        if (!(j < nv && pos + j <= my_qpos)) sr[j] = __float_as_uint(-INFINITY);
                 }
                 float hmax = -INFINITY;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) hmax = fmaxf(hmax, sc[j]);
-                if (!valid_row) hmax = -INFINITY;
-                float* xb = xch + (gi & 1) * 2 * kM;
-                xb[ch * kM + m] = hmax;
-                named_bar_sync(pair_bar, 64);
-                const float bmax = fmaxf(hmax, xb[(1 - ch) * kM + m]) * scale;
+                for (int j = 0; j < 64; ++j) hmax = fmaxf(hmax, __uint_as_float(sr[j]));
+                const float bmax = valid_row ? hmax * scale : -INFINITY;
                 // lazy max: move it only when the block exceeds it by > 2^kLazy
-                // (both halves of the row take the same decision)
                 float corr = 1.f;
                 const bool move = bmax > m_used + kLazy;
                 if (move) {
@@ -310,44 +324,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m_used = bmax;
                 }
                 const float mu = m_used == -INFINITY ? 0.f : m_used;
-                float rs = 0.f;
-                uint32_t pk[16], pl[16];
+                float2 rs2 = make_float2(0.f, 0.f);
+                uint32_t pk[32], pl[32];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const float p0 = fast_exp2(fmaf(sc[2 * j], scale, -mu));
-                    const float p1 = fast_exp2(fmaf(sc[2 * j + 1], scale, -mu));
-                    rs += p0 + p1;
+                for (int j = 0; j < 32; ++j) {
+                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
+                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
+                    const float2 p2 = make_float2(p0, p1);
+                    rs2 = __fadd2_rn(rs2, p2);
                     pk[j] = pack_bf16(p0, p1);
                     const float2 hi = bf16x2_to_float2(pk[j]);
-                    pl[j] = pack_bf16(p0 - hi.x, p1 - hi.y);
+                    const float2 lo = __fadd2_rn(p2, make_float2(-hi.x, -hi.y));
+                    pl[j] = pack_bf16(lo.x, lo.y);
                 }
-                l = l * corr + rs;
+                l = l * corr + (rs2.x + rs2.y);
 
-                // P buffer pb is free once PV(gi-2) completed.
-                mbar_wait(&B.pv_done[pb], ((gi >> 1) & 1) ^ 1);
-                // O rescale of this thread's 64 O columns (warp-uniform:
-                // tcgen05.ld/st are warp-collective); needs PV(gi-1) complete.
-                // Block 0 of an item needs none: its PV overwrites O.
-                if (i > 0 && __any_sync(0xffffffffu, move)) {
-                    const uint32_t pg = gi - 1;
-                    mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
+                // P/O of this group are free once its previous PV completed.
+                mbar_wait(&B.pv_done[grp], (cnt & 1) ^ 1);
+                if (i >= 2 && __any_sync(0xffffffffu, move)) {
                     umma::fence_after_sync();
 #pragma unroll
-                    for (int cblk = 0; cblk < 2; ++cblk) {
+                    for (int cblk = 0; cblk < 4; ++cblk) {
                         uint32_t o[32];
-                        const uint32_t ta = tO + ch * 64 + cblk * 32 + lane_off;
-                        umma::tmem_ld32(ta, o);
+                        umma::tmem_ld32(tOg + cblk * 32, o);
                         umma::tmem_wait_ld();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * corr);
-                        umma::tmem_st32(ta, o);
+                        umma::tmem_st32(tOg + cblk * 32, o);
                     }
                     umma::tmem_wait_st();
                 }
-                uint8_t* prow = sP + pb * kPBuf;
+                uint8_t* prow = sP + grp * kPBuf;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const uint32_t off = swz(m, ch * 4 + c);
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t off = swz(m, c);
                     *reinterpret_cast<uint4*>(prow + off) =
                         make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
                     *reinterpret_cast<uint4*>(prow + kPBytes + off) =
@@ -360,7 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&B.full[st], (gi / kStages) & 1);
                     uint8_t* vs = sStage + st * kStageBytes + 2 * kKVHalf;
                     const int n_chunks = (kBT - nv) * 8;
-                    for (int c = threadIdx.x; c < 2 * n_chunks; c += kSoftThreads) {
+                    for (int c = (threadIdx.x & 127); c < 2 * n_chunks; c += 128) {
                         const int hsel = c / n_chunks, cc = c % n_chunks;
                         *reinterpret_cast<uint4*>(vs + hsel * kKVHalf + nv * 128 + cc * 16) =
                             make_uint4(0, 0, 0, 0);
@@ -369,62 +379,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::fence_proxy_async_smem();
                 umma::fence_before_sync();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&B.p_full[pb]);
+                if (lane == 0) mbar_arrive(&B.p_full[grp]);
+                ++cnt;
+                wk.next();
+                if (i + 1 < w.nblk) wk.next();
             }
+            gi0 += uint32_t(w.nblk);
 
-            // ---- epilogue: this thread's 64 O columns / l ----
-            float o[64];
-            {
-                const uint32_t pg = gi - 1;
-                mbar_wait(&B.pv_done[pg & 1], (pg >> 1) & 1);
-                umma::fence_after_sync();
+            // ---- epilogue: merge the two groups' (m, l, O) by LSE ----
+            if (grp < w.nblk) {  // this group ran at least one block: wait its last PV
+                mbar_wait(&B.pv_done[grp], (cnt & 1) ^ 1);
+            }
+            xm[grp * kM + m] = m_used;
+            xl[grp * kM + m] = l;
+            named_bar_sync(pair_bar, 64);
+            // Past the pair barrier the partner warp (same lane quarter, other
+            // group) has also waited for its last PV: both O tiles are final.
+            const float m0v = xm[m], m1v = xm[kM + m], l0v = xl[m], l1v = xl[kM + m];
+            const float M = fmaxf(m0v, m1v);
+            const float w0 = (l0v > 0.f) ? fast_exp2(m0v - M) : 0.f;
+            const float w1 = (l1v > 0.f) ? fast_exp2(m1v - M) : 0.f;
+            const float L = w0 * l0v + w1 * l1v;
+            const bool empty_row = !(L > 0.f);
+            const float inv = empty_row ? 0.f : 1.f / L;
+            const float lse2 = empty_row ? -INFINITY : M + fast_log2(L);
+            const float a0 = w0 * inv, a1 = w1 * inv;
+            umma::fence_after_sync();
+            float o[64];  // this thread's columns [64 grp, 64 grp + 64) of the merged row
 #pragma unroll
-                for (int cblk = 0; cblk < 2; ++cblk) {
-                    uint32_t r32[32];
-                    umma::tmem_ld32(tO + ch * 64 + cblk * 32 + lane_off, r32);
-                    umma::tmem_wait_ld();
+            for (int cblk = 0; cblk < 2; ++cblk) {
+                uint32_t r0[32], r1[32];
+                umma::tmem_ld32(tmem + kColO + grp * 64 + cblk * 32 + lane_off, r0);
+                umma::tmem_ld32(tmem + kColO + kD + grp * 64 + cblk * 32 + lane_off, r1);
+                umma::tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) o[cblk * 32 + j] = __uint_as_float(r32[j]);
+                for (int j = 0; j < 32; ++j) {
+                    const float x0 = a0 > 0.f ? __uint_as_float(r0[j]) * a0 : 0.f;
+                    const float x1 = a1 > 0.f ? __uint_as_float(r1[j]) * a1 : 0.f;
+                    o[cblk * 32 + j] = x0 + x1;
                 }
             }
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(B.o_free);
-            lx[ch * kM + m] = l;
-            named_bar_sync(pair_bar, 64);
-            const float L = l + lx[(1 - ch) * kM + m];
 
             const int unit = w.b * Hkv + w.g;
             const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
-            const bool empty_row = !(L > 0.f);
-            const float inv = empty_row ? 0.f : 1.f / L;
-            const float lse2 = empty_row ? -INFINITY : m_used + fast_log2(L);
             if (valid_row) {
                 if (n_items == 1) {
                     const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
                     if (a.o_dtype == EP_BF16) {
-                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD + ch * 64);
+                        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD + grp * 64);
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
-                            dst[c] = make_uint4(pack_bf16(o[8 * c] * inv, o[8 * c + 1] * inv),
-                                                pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv),
-                                                pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv),
-                                                pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv));
+                            dst[c] = make_uint4(pack_bf16(o[8 * c], o[8 * c + 1]), pack_bf16(o[8 * c + 2], o[8 * c + 3]),
+                                                pack_bf16(o[8 * c + 4], o[8 * c + 5]), pack_bf16(o[8 * c + 6], o[8 * c + 7]));
                     } else {
-                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow * kD + ch * 64);
+                        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.o) + orow * kD + grp * 64);
 #pragma unroll
                         for (int c = 0; c < 16; ++c)
-                            dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
-                                                 o[4 * c + 3] * inv);
+                            dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
                     }
-                    if (ch == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+                    if (grp == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
                 } else {
-                    float4* dst = reinterpret_cast<float4*>(a.o_part + (size_t(it) * rows + v) * kD + ch * 64);
+                    float4* dst = reinterpret_cast<float4*>(a.o_part + (size_t(it) * rows + v) * kD + grp * 64);
 #pragma unroll
                     for (int c = 0; c < 16; ++c)
-                        dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv,
-                                             o[4 * c + 3] * inv);
-                    if (ch == 0) a.lse_part[size_t(it) * rows + v] = lse2;
+                        dst[c] = make_float4(o[4 * c], o[4 * c + 1], o[4 * c + 2], o[4 * c + 3]);
+                    if (grp == 0) a.lse_part[size_t(it) * rows + v] = lse2;
                 }
             }
             if (n_items > 1) {
@@ -438,13 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                     for (int idx = threadIdx.x; idx < rows * kD; idx += kSoftThreads) {
                         const int r = idx / kD, c = idx % kD;
-                        float M = -INFINITY;
+                        float Mx = -INFINITY;
                         for (int i2 = u0; i2 < u0 + n_items; ++i2)
-                            M = fmaxf(M, __ldcg(&a.lse_part[size_t(i2) * rows + r]));
+                            Mx = fmaxf(Mx, __ldcg(&a.lse_part[size_t(i2) * rows + r]));
                         float Ls = 0.f, acc = 0.f;
-                        if (M != -INFINITY) {
+                        if (Mx != -INFINITY) {
                             for (int i2 = u0; i2 < u0 + n_items; ++i2) {
-                                const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i2) * rows + r]) - M);
+                                const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i2) * rows + r]) - Mx);
                                 Ls += wt;
                                 acc += wt * __ldcg(&a.o_part[(size_t(i2) * rows + r) * kD + c]);
                             }
@@ -457,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             static_cast<__nv_bfloat16*>(a.o)[orow * kD + c] = __float2bfloat16_rn(val);
                         else
                             static_cast<float*>(a.o)[orow * kD + c] = val;
-                        if (c == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (M + fast_log2(Ls)) * kLn2;
+                        if (c == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (Mx + fast_log2(Ls)) * kLn2;
                     }
                     if (threadIdx.x == 0) a.unit_counter[unit] = 0;
                 }
@@ -470,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == kMmaWarp) {
         umma::fence_after_sync();
-        umma::tmem_dealloc(tmem, 256);
+        umma::tmem_dealloc(tmem, kTmemCols);
     }
 }
 
