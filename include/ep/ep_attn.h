@@ -101,6 +101,16 @@ int ep_merge_partials_dev(ep_handle h, ep_dtype dt, size_t n_parts, const void* 
                           const void* lses, size_t rows, size_t d, void* out, void* lse,
                           ep_stream stream);
 
+/* K5, cross-GPU split-KV combine: n_parts rank partials packed as
+ * [part][rows*d fp32 o | rows fp32 lse (natural log)] — exactly what one
+ * all-gather of every rank's ep_spliced_attention(o_dtype EP_F32, lse) output
+ * yields — merged in part (= rank = KV segment) order like merge_partials
+ * (attention.cpp:116-145). out [rows][d] in out_dtype (EP_F32/EP_BF16), lse
+ * [rows] natural log (may be NULL). d <= 256. */
+int ep_merge_partials_packed_dev(ep_handle h, int32_t n_parts, const float* packed, int32_t rows,
+                                 int32_t d, int32_t out_dtype, void* out, float* lse,
+                                 ep_stream stream);
+
 /* ==================================================================== */
 /* 3. Paged splice table (cache.hpp:11-61 made device-resident).        */
 /* ==================================================================== */

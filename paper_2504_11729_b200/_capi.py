@@ -82,6 +82,8 @@ _SIGS = {
     "ep_partial_attention_dev": (C.c_int, [_vp, C.c_int, _vp, _sz, _sz, _vp, _sz, _vp, _sz, _sz,
                                            _sz, _sz, _sz, _vp, _sz, _vp, _vp]),
     "ep_merge_partials_dev": (C.c_int, [_vp, C.c_int, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "ep_merge_partials_packed_dev": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, C.c_int32,
+                                               C.c_int32, _vp, _vp, _vp]),
     "ep_plan_create": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, C.c_int32, C.c_int32, _vp,
                                  _vp, _vp, _vp, C.c_int32, C.POINTER(_vp)]),
     "ep_plan_update": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),

@@ -465,6 +465,20 @@ int ep_merge_partials_dev(ep_handle h, ep_dtype dt, size_t n_parts, const void* 
     return EP_OK;
 }
 
+int ep_merge_partials_packed_dev(ep_handle h, int32_t n_parts, const float* packed, int32_t rows,
+                                 int32_t d, int32_t out_dtype, void* out, float* lse,
+                                 ep_stream stream) {
+    if (!h || !packed || !out) return fail(EP_EINVAL, "merge_partials_packed: null argument");
+    if (n_parts <= 0) return fail(EP_EINVAL, "merge_partials: no partials");
+    if (d <= 0 || d > 256) return fail(EP_EUNSUPPORTED, "merge_partials_packed: d must be 1..256");
+    if (out_dtype != EP_F32 && out_dtype != EP_BF16) return fail(EP_EUNSUPPORTED, "merge_partials_packed: out dtype");
+    EP_CUDA_TRY(launch_merge_packed(n_parts, packed, rows, d, out, out_dtype, lse,
+                                    static_cast<cudaStream_t>(stream)),
+                "merge_partials_packed launch");
+    if (rows > 0) h->launches++;
+    return EP_OK;
+}
+
 // ------------------------------------------------------------ (3) plans --
 
 int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,

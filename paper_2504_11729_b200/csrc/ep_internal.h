@@ -53,6 +53,9 @@ cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int
                              const int32_t* dst_page, const int32_t* dst_slot, const void* k_new,
                              const void* v_new, void* k_pages, void* v_pages, cudaStream_t s);
 
+cudaError_t launch_merge_packed(int n_parts, const float* packed, int rows, int d, void* out,
+                                int out_dtype, float* lse, cudaStream_t s);
+
 cudaError_t launch_fill_uniform(int dt, void* dst, size_t n, uint64_t seed, double lo, double hi,
                                 cudaStream_t s);
 

@@ -281,3 +281,60 @@ cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int
 }
 
 }  // namespace ep
+
+namespace ep {
+namespace {
+
+// K5 merge: n_parts rank partials packed as [part][rows * d (o) | rows (lse,
+// natural log)] — the layout one all-gather of each rank's (o, lse) produces.
+// Folds in part (= rank = segment) order like merge_partials
+// (attention.cpp:116-145): one warp per row, lanes over d.
+__global__ void merge_packed_kernel(int n_parts, const float* __restrict__ packed, int rows, int d,
+                                    void* out, int out_dtype, float* __restrict__ lse_out) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const size_t part_stride = size_t(rows) * (d + 1);
+    float M = -INFINITY;
+    for (int p = 0; p < n_parts; ++p)
+        M = fmaxf(M, packed[p * part_stride + size_t(rows) * d + row]);
+    float L = 0.f;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    if (M != -INFINITY) {
+        for (int p = 0; p < n_parts; ++p) {
+            const float wt = expf(packed[p * part_stride + size_t(rows) * d + row] - M);
+            if (wt == 0.f) continue;
+            L += wt;
+            const float* o = packed + p * part_stride + size_t(row) * d;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int c = lane + 32 * i;
+                if (c < d) acc[i] += wt * o[c];
+            }
+        }
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int c = lane + 32 * i;
+        if (c >= d) continue;
+        if (out_dtype == EP_BF16)
+            static_cast<__nv_bfloat16*>(out)[size_t(row) * d + c] = __float2bfloat16_rn(acc[i] * inv);
+        else
+            static_cast<float*>(out)[size_t(row) * d + c] = acc[i] * inv;
+    }
+    if (lane == 0 && lse_out) lse_out[row] = L > 0.f ? M + logf(L) : -INFINITY;
+}
+
+}  // namespace
+
+cudaError_t launch_merge_packed(int n_parts, const float* packed, int rows, int d, void* out,
+                                int out_dtype, float* lse, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    merge_packed_kernel<<<(rows + 3) / 4, 128, 0, s>>>(n_parts, packed, rows, d, out, out_dtype, lse);
+    return cudaGetLastError();
+}
+
+}  // namespace ep

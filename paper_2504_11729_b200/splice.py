@@ -55,14 +55,14 @@ class KVPool:
     """Paged K/V pool in HBM for one layer (ep_kv_pool)."""
 
     def __init__(self, num_pages: int, n_kv_heads: int, d_head: int, page_tokens: int = 64,
-                 dtype="bf16", device: int = 0, k=None, v=None):
+                 dtype="bf16", device: int | None = None, k=None, v=None):
         torch = _torch()
         self.code = dtype_code(dtype)
         self.tdtype = torch.bfloat16 if self.code == _capi.EP_BF16 else torch.float32
         self.num_pages, self.n_kv_heads, self.d_head = num_pages, n_kv_heads, d_head
         self.page_tokens = page_tokens
         shape = (num_pages, n_kv_heads, page_tokens, d_head)
-        dev = torch.device("cuda", device)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.k = k if k is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
         self.v = v if v is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
         assert tuple(self.k.shape) == shape and tuple(self.v.shape) == shape
@@ -151,7 +151,9 @@ class SpliceTable:
         before any mutation."""
         pages = np.asarray(pages, dtype=np.int32)
         end = self.end_position(b)
-        if pos_offset != end:
+        # A request's first segment may start past 0: a rank of the split-KV
+        # path holds a contiguous window of the global cache (splitkv.py).
+        if self.requests[b] and pos_offset != end:
             raise InvalidArgument(f"SpliceTable.append: segment starts at {pos_offset}, "
                                   f"cache ends at {end}")
         if length <= 0:

@@ -1,0 +1,170 @@
+"""BASELINE config 4: long-context split-KV. A 131072-token cloud prompt per
+request is sharded contiguously across the P GPUs of one box (edge 512 on the
+last rank); every rank runs the spliced decode kernel over its shard (fp32
+o + lse), then one NCCL all-gather of the packed partials and the K5 LSE merge
+in rank order.
+
+    torchrun --nproc-per-node P tools/splitkv_bench.py [--batch 32] [--check]
+
+Times (CUDA events, max over ranks): the local attention, and the whole step
+(local attention + all-gather + merge). --check compares rank 0's merged
+output with an unsharded single-GPU run of the same batch.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+HQ, HKV, D, P = 32, 8, 128, 64
+CLOUD, EDGE = 131072, 512
+
+
+def build_local(batch, world, rank, h, cloud=CLOUD, edge=EDGE, seed=41):
+    """This rank's pool/table/plan for `batch` requests; KV of global token t of
+    request b is row t of a seeded token-major tensor (identical on all ranks)."""
+    import numpy as np
+    import torch
+    from paper_2504_11729_b200 import _capi
+    from paper_2504_11729_b200.splice import KVPool, SpliceTable, SplicedAttention
+    from paper_2504_11729_b200.splitkv import shard_segments
+    lib = _capi.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    segments = [(0, cloud), (1, edge)]
+    shards = shard_segments(segments, world, rank)
+    n_loc = sum(x.length for x in shards)
+    pages_per_req = sum(-(-x.length // P) for x in shards)
+    pool = KVPool(max(1, batch * pages_per_req), HKV, D, P, dtype="bf16")
+    table = SpliceTable(batch, P)
+    n_total = cloud + edge
+    tok = torch.empty((n_total, HKV, D), dtype=torch.bfloat16, device="cuda")
+    for b in range(batch):
+        pg = b * pages_per_req
+        page_lists = []
+        for x in shards:
+            npg = -(-x.length // P)
+            page_lists.append(np.arange(pg, pg + npg, dtype=np.int32))
+            pg += npg
+        for kv, off in (("k", 0), ("v", 1)):
+            # the request's whole token-major K (or V), identical on every rank;
+            # this rank keeps its shards' rows
+            _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, tok.data_ptr(), tok.numel(),
+                                            seed * 1000003 + b * 7919 + off * 104729, -1.0, 1.0, s))
+            target = pool.k if kv == "k" else pool.v
+            for x, pages in zip(shards, page_lists):
+                t = torch.arange(x.length, device="cuda")
+                pidx = torch.as_tensor(pages.astype(np.int64), device="cuda")[t // P]
+                target[pidx, :, t % P, :] = tok[x.pos_offset:x.pos_offset + x.length]
+        for x, pages in zip(shards, page_lists):
+            table.append(b, x.origin, x.pos_offset, x.length, pages)
+        table.q_pos[b] = cloud + edge - 1
+    attn = SplicedAttention(pool, table, HQ, 1, handle=h)
+    q = torch.empty((batch, 1, HQ, D), dtype=torch.bfloat16, device="cuda")
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, q.data_ptr(), q.numel(), seed + 5, -1.0,
+                                    1.0, s))
+    return pool, table, attn, q, n_loc
+
+
+def run(batch, steps, warmup, check=False):
+    import torch
+    import torch.distributed as dist
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splitkv import SplitKVCombine
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    h = Handle(torch.cuda.current_device())
+    pool, table, attn, q, n_loc = build_local(batch, world, rank, h)
+    rows = batch * HQ
+    comb = SplitKVCombine(world, rows, D, handle=h, device="cuda") if world > 1 else None
+    o_part = torch.empty((batch, 1, HQ, D), dtype=torch.float32, device="cuda")
+    lse_part = torch.empty((batch, 1, HQ), dtype=torch.float32, device="cuda")
+    out = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
+    out_lse = torch.empty((rows,), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        attn(q, o=o_part, lse=lse_part, stream=stream)
+        if comb is not None:
+            comb(o_part, lse_part, out=out, out_lse=out_lse, stream=stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    e[0].record(stream)
+    for _ in range(steps):
+        attn(q, o=o_part, lse=lse_part, stream=stream)
+    e[1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e[2].record(stream)
+    for _ in range(steps):
+        step()
+    e[3].record(stream)
+    torch.cuda.synchronize()
+    t_attn = e[0].elapsed_time(e[1]) / steps
+    t_step = e[2].elapsed_time(e[3]) / steps
+    t = torch.tensor([t_attn, t_step], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_attn, t_step = float(t[0]), float(t[1])
+    loc_bytes = batch * n_loc * 2 * HKV * D * 2
+    gather_bytes = (world - 1) * rows * (D + 1) * 4  # received per rank
+    res = {
+        "workload": f"cfg4 split-KV: {CLOUD} cloud + {EDGE} edge keys, Hq=32 Hkv=8 d=128 bf16, "
+                    f"batch {batch}, {world} GPU(s)",
+        "batch": batch, "gpus": world, "step_ms": t_step, "local_attention_ms": t_attn,
+        "combine_ms": t_step - t_attn if world > 1 else 0.0,
+        "tokens_per_s": batch / (t_step / 1e3),
+        "local_hbm_gbs": loc_bytes / (t_attn / 1e3) / 1e9,
+        "allgather_bytes_per_rank": gather_bytes,
+    }
+    if check:
+        ok = True
+        if world > 1:
+            # rank 0 recomputes the unsharded batch on its own GPU
+            if rank == 0:
+                _, _, attn1, q1, _ = build_local(batch, 1, 0, h)
+                o1, l1 = attn1(q1, o_dtype=torch.float32)
+                torch.cuda.synchronize()
+                err = (out.float() - o1.reshape(rows, D)).abs().max().item()
+                lerr = (out_lse - l1.reshape(rows)).abs().max().item()
+                res["check_max_abs_err"] = err
+                res["check_lse_max_abs_err"] = lerr
+                ok = err < 2e-2 and lerr < 1e-3
+        res["check_ok"] = ok
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, nargs="+", default=[1, 32])
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--check", action="store_true")
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    for b in args.batch:
+        r = run(b, args.steps, args.warmup, check=args.check)
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps(r), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
