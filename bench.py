@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config 3/4/5 measurements (verify, split-KV, multi-tenant)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -366,10 +368,48 @@ def main():
             "sample": f"requests 0-3 of the same workload (128 (request, head) units per pass, "
                       f"{units} units in {secs:.1f} s), reference attention block in fp64 "
                       "(oracle/_ref, unmodified reference sources)"}
+    if not args.no_extras:
+        line.update(run_extras(args, world, rank, h))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_extras(args, world, rank, h):
+    """The other BASELINE configs, measured in the same run: config 3
+    (speculative verify p50 latency, k = 4 / 8) and config 5 (multi-tenant
+    shared prefix) on rank 0 at N = 1; config 4 (128K split-KV, NCCL
+    all-gather + LSE merge) at every N."""
+    import gc
+
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import splitkv_bench
+    extras = {}
+    steps = max(5, min(args.steps, 30))
+    if world == 1:
+        import multitenant_bench
+        import verify_bench
+        gc.collect()
+        torch.cuda.empty_cache()
+        ver = {}
+        for k in (4, 8):
+            ver[f"k{k}"] = verify_bench.run(k, steps, 3, h)
+            gc.collect()
+            torch.cuda.empty_cache()
+        extras["verify"] = ver
+        extras["verify_p50_ms"] = {k: v["step_p50_ms"] for k, v in ver.items()}
+        extras["multitenant"] = multitenant_bench.run(steps, 3, h)
+        gc.collect()
+        torch.cuda.empty_cache()
+    skv = {}
+    for b in (1, 32):
+        skv[f"batch{b}"] = splitkv_bench.run(b, steps, 3)
+        gc.collect()
+        torch.cuda.empty_cache()
+    extras["splitkv"] = skv
+    return extras
 
 
 if __name__ == "__main__":
