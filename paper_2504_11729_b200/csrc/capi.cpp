@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -575,6 +576,15 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
     a.q_scale = float(1.4426950408889634 / std::sqrt(double(p->d_head)));
     a.zero_rows = h->zero_rows.ptr;
     a.unit_counter = static_cast<int32_t*>(p->d_counter.ptr);
+    a.trace = nullptr;
+    static unsigned long long* trace_buf = [] {
+        unsigned long long* t = nullptr;
+        const char* e = std::getenv("EP_TRACE");
+        if (e && e[0] == '1' && cudaMalloc(&t, 12 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(t, 0, 12 * 1024 * sizeof(unsigned long long));
+        return t;
+    }();
+    a.trace = trace_buf;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (p->n_items > 0 && p->use_tc) {
         if (p->tm_k != pool->k_pages || p->tm_v != pool->v_pages || p->tm_pages != pool->num_pages) {
@@ -588,6 +598,16 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
         EP_CUDA_TRY(launch_verify_attention(int(p->n_ctas), a, p->tmap_k, p->tmap_v, p->rows, s),
                     "verify attention launch");
         h->launches++;
+        if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
+            std::vector<unsigned long long> host(12 * 1024);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+            const char* f = std::getenv("EP_TRACE_FILE");
+            if (FILE* fp = std::fopen(f ? f : "ep_trace.bin", "wb")) {
+                std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
+                std::fclose(fp);
+            }
+        }
     } else if (p->n_items > 0) {
         EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
                     "spliced decode launch");

@@ -96,6 +96,7 @@ struct DecodeArgs {
     float q_scale;            // log2(e) / sqrt(d)
     const void* zero_rows;    // >= 64 zero K/V rows (page-tail fill)
     int32_t* unit_counter;    // [batch*Hkv], zero between launches (fused K2)
+    unsigned long long* trace;  // optional clock64 event trace of CTA 0 (debug, may be null)
 };
 
 // R = rows per (request, kv-head) = group * n_q.

@@ -9,14 +9,15 @@
 // share every K/V byte; at 20-36 FLOP/B that is beyond the CUDA cores, so:
 //
 //   QK^T : S[128 x 64]  (TMEM, fp32) = Q[128 x 128] (smem) . K[64 keys x 128]^T
-//   PV   : O[128 x 128] (TMEM, fp32) += (P_hi + P_lo)[128 x 64] (smem, 2 x bf16) . V[64 x 128]
+//   PV   : O[128 x 128] (TMEM, fp32) += (P_hi + P_lo)[128 x 64] (TMEM, 2 x bf16) . V[64 x 128]
 //
 // tcgen05.mma M=128 (rows >= R are padding; the M=128 issue rate equals
 // M=64's), operands staged by TMA with 128B swizzle straight from the paged
 // pool (the [page][head][token][d] tile is a 2-D tensor of 128-element rows).
 // Warp roles (128 threads, one CTA per SM, persistent over the planner's page
 // ranges like K1):
-//   warp 8 lane 0 : TMA producer (K and V boxes, S-stage ring)
+//   warp 8 lane 0 : TMA producer of the K ring (5 stages, freed after QK)
+//   warp 10 lane 0: TMA producer of the V ring (3 stages, freed after PV)
 //   warp 9 lane 0 : MMA issuer; warp 9 owns the TMEM allocation
 //   warps 0-7     : softmax + epilogue. Query rows are spread over the four
 //                   TMEM lane quarters (row v -> M row 32*(v%4) + v/4) so all
@@ -30,6 +31,7 @@
 // same per-unit counter protocol as K1.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ep_common.cuh"
 #include "ep_internal.h"
@@ -41,45 +43,60 @@ namespace {
 constexpr int kBT = 64;        // keys per block
 constexpr int kD = 128;        // head dim
 constexpr int kM = 128;        // UMMA M (rows, padded)
-constexpr int kStages = 4;
+constexpr int kKStages = 7;  // K ring: a K block is free right after its QK
+constexpr int kVStages = 7;  // V ring: a V block is free after its PV
 constexpr int kSoftWarps = 8;  // 2 ping-pong groups x 4 TMEM lane quarters
 constexpr int kSoftThreads = kSoftWarps * 32;
-constexpr int kProdWarp = 8, kMmaWarp = 9;
-constexpr int kThreads = 320;
+constexpr int kProdWarp = 8, kMmaWarp = 9, kProdVWarp = 10;
+constexpr int kThreads = 352;
 constexpr int kMaxRows = 64;      // valid query rows per (request, kv-head)
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
 
 constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
 constexpr int kKVHalf = kBT * 128;         // 8 KB: 64 rows x 64 bf16
-constexpr int kStageBytes = 4 * kKVHalf;   // K0 K1 V0 V1
-constexpr int kPBytes = kM * 128;          // 16 KB: 128 rows x 64 keys bf16
-constexpr int kPBuf = 2 * kPBytes;         // hi and lo halves of one P tile
-constexpr int OFF_Q = 0;
-constexpr int OFF_STAGE = 2 * kQHalf;
-constexpr int OFF_P = OFF_STAGE + kStages * kStageBytes;
-constexpr int OFF_XM = OFF_P + 2 * kPBuf;   // [2 groups][128] row max of each group
+constexpr int kBlkBytes = 2 * kKVHalf;     // one K (or V) block: two 64-column halves
+constexpr int OFF_STAGE = 0;
+constexpr int OFF_VST = OFF_STAGE + kKStages * kBlkBytes;
+constexpr int OFF_XM = OFF_VST + kVStages * kBlkBytes;  // [2 groups][128] row max of each group
 constexpr int OFF_XL = OFF_XM + 2 * kM * 4; // [2 groups][128] row sum of each group
 constexpr int OFF_BAR = OFF_XL + 2 * kM * 4;
-constexpr int kNumBars = 2 * kStages + 2 + 2 + 2 + 2 + 2;
+constexpr int kNumBars = 2 * kKStages + 2 * kVStages + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
 constexpr int kSmem = OFF_MISC + 32;  // dynamic smem base must be 1024-aligned (checked)
-// TMEM columns: O of group 0 / 1, then S of group 0 / 1.
+// TMEM columns (512): O of group 0 / 1 (128 each, fp32), S of group 0 / 1
+// (64 each, fp32) whose columns are overwritten by that group's P as bf16 hi
+// (32 columns: two bf16 per 32-bit column) and lo (32), then the item's Q
+// tile (64 columns, bf16). Q and P are the A operands of the MMAs, so the
+// tensor core reads only K and V from shared memory.
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColO = 0, kColS = 256;
+constexpr uint32_t kColO = 0, kColS = 256, kColQ = 384;
 
 constexpr uint32_t kIdescQK = umma::idesc_bf16_f32(kM, kBT, false, false);
 constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
 
 struct Bars {
-    uint64_t* full;     // [S] TMA landed
-    uint64_t* empty;    // [S] K/V stage consumed (commit after PV)
+    uint64_t* full_k;   // [KS] K block landed
+    uint64_t* empty_k;  // [KS] K block consumed (commit after its QK)
+    uint64_t* full_v;   // [VS] V block landed
+    uint64_t* empty_v;  // [VS] V block consumed (commit after its PV)
     uint64_t* s_full;   // [2 groups] QK result in TMEM
-    uint64_t* s_free;   // [2] softmax done reading S
     uint64_t* p_full;   // [2] P written (+ O rescaled)
     uint64_t* pv_done;  // [2] PV finished (P buffer free, O updated)
     uint64_t* q_ready;  // Q tile of the item in smem
     uint64_t* o_free;   // epilogue read O
 };
+
+// Debug trace (a.trace != null, CTA 0 only): clock64 per event and block.
+constexpr int kTraceBlocks = 1024;
+enum TraceEv { TR_KISSUE = 0, TR_VISSUE, TR_QK, TR_PV, TR_S_SEEN, TR_P_DONE,
+              TR_QK_START, TR_QK_FULLK, TR_QK_DONE, TR_PV_START, TR_PV_PFULL, TR_PV_DONE, TR_N };
+__device__ __forceinline__ void trace(const DecodeArgs& a, int ev, uint32_t gi) {
+    if (a.trace && blockIdx.x == 0 && gi < kTraceBlocks && (threadIdx.x & 31) == 0) {
+        long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+        a.trace[ev * kTraceBlocks + gi] = (unsigned long long)t;
+    }
+}
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
     return row * 128 + ((chunk ^ (row & 7)) << 4);
@@ -124,18 +141,17 @@ struct BlockWalker {
 // core always has the other group's QK or PV to run.
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
-                            const __grid_constant__ CUtensorMap tmap_v, int rows) {
+                            const __grid_constant__ CUtensorMap tmap_v, int rows, int pv_parts) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1 KB alignment
-    uint8_t* sQ = smem + OFF_Q;
     uint8_t* sStage = smem + OFF_STAGE;
-    uint8_t* sP = smem + OFF_P;
     float* xm = reinterpret_cast<float*>(smem + OFF_XM);
     float* xl = reinterpret_cast<float*>(smem + OFF_XL);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-    Bars B{bar, bar + kStages, bar + 2 * kStages, bar + 2 * kStages + 2, bar + 2 * kStages + 4,
-           bar + 2 * kStages + 6, bar + 2 * kStages + 8, bar + 2 * kStages + 9};
+    constexpr int kRB = 2 * kKStages + 2 * kVStages;
+    Bars B{bar, bar + kKStages, bar + 2 * kKStages, bar + 2 * kKStages + kVStages,
+           bar + kRB, bar + kRB + 2, bar + kRB + 4, bar + kRB + 6, bar + kRB + 7};
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_MISC);
     int* s_flag = reinterpret_cast<int*>(smem + OFF_MISC + 16);
 
@@ -145,13 +161,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int G = a.n_q_heads / Hkv;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&B.full[s], 1);
-            mbar_init(&B.empty[s], 1);
+        for (int s = 0; s < kKStages; ++s) {
+            mbar_init(&B.full_k[s], 1);
+            mbar_init(&B.empty_k[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
+            mbar_init(&B.full_v[s], 1);
+            mbar_init(&B.empty_v[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&B.s_full[i], 1);
-            mbar_init(&B.s_free[i], 4);
             mbar_init(&B.p_full[i], 4);
             mbar_init(&B.pv_done[i], 1);
         }
@@ -160,18 +179,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_mbar_init();
     }
     if (warp == kMmaWarp) umma::tmem_alloc(tmem_slot, kTmemCols);
-    if (warp == kProdWarp && lane == 0) {
-        umma::tma_prefetch_desc(&tmap_k);
-        umma::tma_prefetch_desc(&tmap_v);
-    }
+    if (warp == kProdWarp && lane == 0) umma::tma_prefetch_desc(&tmap_k);
+    if (warp == kProdVWarp && lane == 0) umma::tma_prefetch_desc(&tmap_v);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == kProdWarp) {
-        // ============================== producer ==============================
+    if (warp == kProdWarp || warp == kProdVWarp) {
+        // ========================= producers (K ring, V ring) =========================
         if (lane == 0) {
+            const bool is_k = warp == kProdWarp;
+            const int ns = is_k ? kKStages : kVStages;
+            uint64_t* fullb = is_k ? B.full_k : B.full_v;
+            uint64_t* emptyb = is_k ? B.empty_k : B.empty_v;
+            uint8_t* ring = smem + (is_k ? OFF_STAGE : OFF_VST);
+            const CUtensorMap* tm = is_k ? &tmap_k : &tmap_v;
             const uint64_t pol = l2_policy_evict_first();
             uint32_t gi = 0;
             for (int it = it0; it < it1; ++it) {
@@ -179,64 +202,78 @@ __global__ void __launch_bounds__(kThreads, 1)
                 BlockWalker wk;
                 wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
                 for (int i = 0; i < w.nblk; ++i, ++gi, wk.next()) {
-                    const int st = gi % kStages;
-                    mbar_wait(&B.empty[st], ((gi / kStages) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&B.full[st], kStageBytes);
+                    const int st = gi % ns;
+                    mbar_wait(&emptyb[st], ((gi / ns) & 1) ^ 1);
+                    trace(a, is_k ? TR_KISSUE : TR_VISSUE, gi);
+                    mbar_arrive_expect_tx(&fullb[st], kBlkBytes);
                     const int row = int((int64_t(wk.cur.page) * Hkv + w.g) * P + wk.t0);
-                    uint8_t* dst = sStage + st * kStageBytes;
-                    umma::tma_load_2d(dst, &tmap_k, 0, row, &B.full[st], pol);
-                    umma::tma_load_2d(dst + kKVHalf, &tmap_k, 64, row, &B.full[st], pol);
-                    umma::tma_load_2d(dst + 2 * kKVHalf, &tmap_v, 0, row, &B.full[st], pol);
-                    umma::tma_load_2d(dst + 3 * kKVHalf, &tmap_v, 64, row, &B.full[st], pol);
+                    uint8_t* dst = ring + st * kBlkBytes;
+                    umma::tma_load_2d(dst, tm, 0, row, &fullb[st], pol);
+                    umma::tma_load_2d(dst + kKVHalf, tm, 64, row, &fullb[st], pol);
                 }
             }
         }
     } else if (warp == kMmaWarp) {
         // ================================ MMA =================================
-        if (lane == 0) {
-            const uint32_t q_addr = smem_u32(sQ), p_addr = smem_u32(sP);
-            const uint32_t st_addr = smem_u32(sStage);
+        // The whole warp runs the loop (operands stay warp-uniform); one
+        // elected lane issues each MMA / commit.
+        {
+            // Descriptors are built once; per MMA only the 14-bit start-address
+            // field moves (byte offset >> 4, no carry for smem < 256 KB), so the
+            // single issuing thread spends a couple of instructions per MMA.
+            const uint64_t dk = umma::smem_desc_sw128(smem_u32(sStage), 16, 1024);
+            const uint64_t dv = umma::smem_desc_sw128(smem_u32(smem + OFF_VST), kKVHalf, 1024);
             uint32_t gi = 0, n = 0;
             uint32_t cqk[2] = {0, 0}, cpv[2] = {0, 0};  // per-group block counters
-            // PV of local block i (global gi) into O[i & 1].
+            // PV of local block i (global g_i) into O[i & 1].
             auto issue_pv = [&](int i, uint32_t g_i) {
                 const int grp = i & 1;
+                trace(a, TR_PV_START, g_i);
                 mbar_wait(&B.p_full[grp], cpv[grp] & 1);
+                trace(a, TR_PV_PFULL, g_i);
                 if (i == 0) mbar_wait(B.o_free, (n & 1) ^ 1);  // previous item's epilogue read O
+                const uint32_t vs = g_i % kVStages;
+                mbar_wait(&B.full_v[vs], (g_i / kVStages) & 1);
+                trace(a, TR_PV, g_i);
                 umma::fence_after_sync();
-                const uint32_t v_addr = st_addr + (g_i % kStages) * kStageBytes + 2 * kKVHalf;
-                // P = hi + lo (two bf16 tiles): O += P_hi V + P_lo V keeps the
-                // probabilities at ~2^-17 relative instead of bf16's 2^-9.
-#pragma unroll
-                for (int part = 0; part < 2; ++part)
-#pragma unroll
-                    for (int kk = 0; kk < kBT / 16; ++kk) {
-                        const uint64_t ad = umma::smem_desc_sw128(
-                            p_addr + grp * kPBuf + part * kPBytes + kk * 32, 16, 1024);
-                        const uint64_t bd = umma::smem_desc_sw128(v_addr + kk * 2048, kKVHalf, 1024);
-                        umma::mma_bf16_ss(tmem + kColO + grp * kD, ad, bd, kIdescPV,
-                                          (i < 2 && part == 0 && kk == 0) ? 0u : 1u);
-                    }
-                umma::mma_commit(&B.pv_done[grp]);
-                umma::mma_commit(&B.empty[g_i % kStages]);
+                const uint64_t bd0 = dv + ((vs * kBlkBytes) >> 4);
+                const uint32_t ta0 = tmem + kColS + grp * kBT, td = tmem + kColO + grp * kD;
+                // P = hi + lo (two bf16 tiles in TMEM): O += P_hi V + P_lo V keeps
+                // the probabilities at ~2^-17 relative instead of bf16's 2^-9.
+                if (umma::elect_one()) {
+                    umma::mma_chain_pv4(td, ta0, bd0, kIdescPV, i < 2 ? 1u : 0u);
+                    if (pv_parts > 1) umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
+                }
+                if (umma::elect_one()) {
+                    umma::mma_commit(&B.pv_done[grp]);
+                    umma::mma_commit(&B.empty_v[vs]);
+                }
+                __syncwarp();
+                trace(a, TR_PV_DONE, g_i);
                 ++cpv[grp];
             };
             // QK of local block i (global g_i) into S[i & 1].
             auto issue_qk = [&](int i, uint32_t g_i) {
-                const int st = g_i % kStages;
+                const int st = g_i % kKStages;
                 const int grp = i & 1;
-                mbar_wait(&B.full[st], (g_i / kStages) & 1);
-                mbar_wait(&B.s_free[grp], (cqk[grp] & 1) ^ 1);
+                trace(a, TR_QK_START, g_i);
+                mbar_wait(&B.full_k[st], (g_i / kKStages) & 1);
+                trace(a, TR_QK_FULLK, g_i);
+                // S[grp] holds P of this group's previous block until its PV has
+                // read it; that PV was issued before this QK and the tensor pipe
+                // executes in issue order, so no wait is needed here.
+                trace(a, TR_QK, g_i);
                 umma::fence_after_sync();
-                const uint32_t k_addr = st_addr + st * kStageBytes;
-#pragma unroll
-                for (int kk = 0; kk < kD / 16; ++kk) {
-                    const uint32_t half = kk >> 2, off = (kk & 3) * 32;
-                    const uint64_t ad = umma::smem_desc_sw128(q_addr + half * kQHalf + off, 16, 1024);
-                    const uint64_t bd = umma::smem_desc_sw128(k_addr + half * kKVHalf + off, 16, 1024);
-                    umma::mma_bf16_ss(tmem + kColS + grp * kBT, ad, bd, kIdescQK, kk > 0 ? 1u : 0u);
+                const uint64_t kd0 = dk + ((st * kBlkBytes) >> 4);
+                const uint32_t ts = tmem + kColS + grp * kBT;
+                static_assert(kKVHalf == 8192, "offsets baked into mma_chain_qk8_ts");
+                if (umma::elect_one()) umma::mma_chain_qk8_ts(ts, tmem + kColQ, kd0, kIdescQK);
+                if (umma::elect_one()) {
+                    umma::mma_commit(&B.s_full[grp]);
+                    umma::mma_commit(&B.empty_k[st]);
                 }
-                umma::mma_commit(&B.s_full[grp]);
+                __syncwarp();
+                trace(a, TR_QK_DONE, g_i);
                 ++cqk[grp];
             };
             // Issue order QK(0) QK(1) | QK(i+2) PV(i) ...: a group's next S is
@@ -247,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(B.q_ready, n & 1);
                 for (int i = 0; i < 2 && i < w.nblk; ++i) issue_qk(i, gi + i);
                 for (int i = 0; i < w.nblk; ++i) {
-                    if (i + 2 < w.nblk) issue_qk(i + 2, gi + i + 2);
-                    issue_pv(i, gi + i);
+                    issue_pv(i, gi + i);  // reads P(i) from S[i & 1] ...
+                    if (i + 2 < w.nblk) issue_qk(i + 2, gi + i + 2);  // ... before QK(i+2) overwrites it
                 }
                 gi += uint32_t(w.nblk);
             }
@@ -272,17 +309,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int qi = v / G, h = w.g * G + v % G;
             const int64_t my_qpos = q0 + qi;
 
-            // ---- Q tile: group g writes K-half g of this row, swizzled ----
+            // ---- Q tile -> TMEM (A operand of QK): group g writes d-half g ----
             {
                 const uint8_t* src = static_cast<const uint8_t*>(a.q) +
                                      (((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
+                uint32_t qv[32];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     uint4 val = make_uint4(0, 0, 0, 0);
                     if (valid_row) val = *reinterpret_cast<const uint4*>(src + c * 16);
-                    *reinterpret_cast<uint4*>(sQ + grp * kQHalf + swz(m, c)) = val;
+                    qv[4 * c] = val.x;
+                    qv[4 * c + 1] = val.y;
+                    qv[4 * c + 2] = val.z;
+                    qv[4 * c + 3] = val.w;
                 }
-                umma::fence_proxy_async_smem();
+                umma::tmem_st32(tmem + kColQ + grp * 32 + lane_off, qv);
+                umma::tmem_wait_st();
+                umma::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(B.q_ready);
             }
@@ -298,14 +341,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
                 // ---- the 64 scores of this row ----
                 mbar_wait(&B.s_full[grp], cnt & 1);
+                if (threadIdx.x == grp * 128) trace(a, TR_S_SEEN, gi);
                 umma::fence_after_sync();
                 uint32_t sr[64];
                 umma::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(sr));
                 umma::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
                 umma::tmem_wait_ld();
-                umma::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&B.s_free[grp]);
 
                 if (!(nv == kBT && pos + kBT - 1 <= q0)) {
 #pragma unroll
@@ -354,21 +395,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     umma::tmem_wait_st();
                 }
-                uint8_t* prow = sP + grp * kPBuf;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint32_t off = swz(m, c);
-                    *reinterpret_cast<uint4*>(prow + off) =
-                        make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-                    *reinterpret_cast<uint4*>(prow + kPBytes + off) =
-                        make_uint4(pl[4 * c], pl[4 * c + 1], pl[4 * c + 2], pl[4 * c + 3]);
-                }
+                // P row -> TMEM over this group's S columns (A operand of the PV
+                // MMAs): hi tile then lo tile.
+                umma::tmem_st32(tS, pk);
+                umma::tmem_st32(tS + 32, pl);
+                umma::tmem_wait_st();
                 if (nv < kBT) {
                     // Tail rows of V in the stage are stale page slots: zero them
                     // so 0 * garbage cannot reach the PV accumulator.
-                    const int st = gi % kStages;
-                    mbar_wait(&B.full[st], (gi / kStages) & 1);
-                    uint8_t* vs = sStage + st * kStageBytes + 2 * kKVHalf;
+                    const int st = gi % kVStages;
+                    mbar_wait(&B.full_v[st], (gi / kVStages) & 1);
+                    uint8_t* vs = smem + OFF_VST + st * kBlkBytes;
                     const int n_chunks = (kBT - nv) * 8;
                     for (int c = (threadIdx.x & 127); c < 2 * n_chunks; c += 128) {
                         const int hsel = c / n_chunks, cc = c % n_chunks;
@@ -380,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&B.p_full[grp]);
+                if (threadIdx.x == grp * 128) trace(a, TR_P_DONE, gi);
                 ++cnt;
                 wk.next();
                 if (i + 1 < w.nblk) wk.next();
@@ -511,7 +549,12 @@ cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUten
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows);
+    // EP_PV_PARTS=1 drops the P_lo pass (bf16 P, timing experiments only).
+    static const int pv_parts = [] {
+        const char* e = getenv("EP_PV_PARTS");
+        return (e && e[0] == '1') ? 1 : 2;
+    }();
+    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows, pv_parts);
     return cudaGetLastError();
 }
 

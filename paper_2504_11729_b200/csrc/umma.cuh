@@ -68,6 +68,17 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// One lane of the (converged) warp returns true (elect.sync). Used so a whole
+// warp runs an MMA-issue loop with warp-uniform operands (uniform registers,
+// no R2UR waterfall) while exactly one lane issues.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ----------------------------------------------------------- descriptors --
 
 // Shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), sm100
@@ -101,6 +112,73 @@ __device__ __forceinline__ void mma_bf16_ss(uint32_t tmem_d, uint64_t adesc, uin
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// D[tmem] (+)= A[tmem] * B[smem] (A in TMEM: lane = row, two 16-bit K
+// elements per 32-bit column); issued by ONE thread.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Batched issue: one asm block per MMA chain so the descriptor bases are moved
+// to uniform registers once and each MMA only adds an immediate offset
+// (the start-address field of a smem descriptor is bits [0,14) in 16-byte
+// units; offsets never carry out of it for smem addresses < 256 KB).
+//
+// QK^T chain of kverify: 8 x (M128 N64 K16), A = Q tile (two 64-column SW128
+// halves 16 KB apart), B = K block (two halves 8 KB apart), k-step 32 bytes.
+__device__ __forceinline__ void mma_chain_qk8(uint32_t tmem_d, uint64_t dq, uint64_t dk,
+                                              uint32_t idesc) {
+#define EP_QK_STEP(OA, OB) \
+    "add.s64 a, %1, " #OA ";\n\tadd.s64 b, %2, " #OB ";\n\t" \
+    "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+    asm volatile(
+        "{\n\t.reg .b64 a, b;\n\t.reg .pred f, t;\n\t"
+        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, f;\n\t"
+        EP_QK_STEP(2, 2) EP_QK_STEP(4, 4) EP_QK_STEP(6, 6)
+        EP_QK_STEP(1024, 512) EP_QK_STEP(1026, 514) EP_QK_STEP(1028, 516) EP_QK_STEP(1030, 518)
+        "}" ::"r"(tmem_d), "l"(dq), "l"(dk), "r"(idesc));
+#undef EP_QK_STEP
+}
+
+// QK^T chain with A = Q from TMEM (64 columns: two bf16 per column, +8
+// columns per 16-element k-step) and B = K block (two SW128 halves 8 KB apart).
+__device__ __forceinline__ void mma_chain_qk8_ts(uint32_t tmem_d, uint32_t tq, uint64_t dk,
+                                                 uint32_t idesc) {
+#define EP_QKT_STEP(OA, OB) \
+    "add.u32 x, %1, " #OA ";\n\tadd.s64 b, %2, " #OB ";\n\t" \
+    "tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %3, t;\n\t"
+    asm volatile(
+        "{\n\t.reg .b64 b;\n\t.reg .b32 x;\n\t.reg .pred f, t;\n\t"
+        "setp.ne.b32 f, 0, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n\t"
+        EP_QKT_STEP(8, 2) EP_QKT_STEP(16, 4) EP_QKT_STEP(24, 6)
+        EP_QKT_STEP(32, 512) EP_QKT_STEP(40, 514) EP_QKT_STEP(48, 516) EP_QKT_STEP(56, 518)
+        "}" ::"r"(tmem_d), "r"(tq), "l"(dk), "r"(idesc));
+#undef EP_QKT_STEP
+}
+
+// PV chain: 4 x (M128 N128 K16) with A from TMEM (ta: +8 columns per k-step)
+// and B = V block MN-major (+2048 bytes = +128 units per k-step). `first`
+// clears the accumulator on the first MMA.
+__device__ __forceinline__ void mma_chain_pv4(uint32_t tmem_d, uint32_t ta, uint64_t dv,
+                                              uint32_t idesc, uint32_t first) {
+#define EP_PV_STEP(OA, OB) \
+    "add.u32 x, %1, " #OA ";\n\tadd.s64 b, %2, " #OB ";\n\t" \
+    "tcgen05.mma.cta_group::1.kind::f16 [%0], [x], b, %3, t;\n\t"
+    asm volatile(
+        "{\n\t.reg .b64 b;\n\t.reg .b32 x;\n\t.reg .pred f, t;\n\t"
+        "setp.eq.b32 f, %4, 0;\n\tsetp.eq.b32 t, 0, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n\t"
+        EP_PV_STEP(8, 128) EP_PV_STEP(16, 256) EP_PV_STEP(24, 384)
+        "}" ::"r"(tmem_d), "r"(ta), "l"(dv), "r"(idesc), "r"(first));
+#undef EP_PV_STEP
 }
 
 // Arrive once on `bar` when all previously issued tcgen05 ops of this thread
