@@ -48,49 +48,7 @@ cudaError_t DeviceBuffer::reserve(size_t n) {
 
 using namespace ep;
 
-#define EP_CUDA_TRY(expr, where)                          \
-    do {                                                  \
-        cudaError_t _e = (expr);                          \
-        if (_e != cudaSuccess) return cuda_fail(_e, where); \
-    } while (0)
-
-// ------------------------------------------------------------- plan object --
-
-struct ep_plan_s {
-    ep_handle h = nullptr;
-    int32_t kv_dtype = 0, n_kv_heads = 0, d_head = 0, page_tokens = 0;
-    int64_t num_pages = 0;
-    int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
-    int64_t n_ctas = 0, n_items = 0, n_pages = 0;
-    bool has_empty_unit = false;
-    bool use_tc = false;  // K3 tcgen05 path (rows > 8 or EP_FORCE_TC)
-    CUtensorMap tmap_k{}, tmap_v{};
-    const void* tm_k = nullptr;
-    const void* tm_v = nullptr;
-    int64_t tm_pages = -1;
-    // host mirrors
-    std::vector<PageDesc> pdesc;
-    std::vector<int64_t> req_page_off;
-    std::vector<WorkItem> items;
-    std::vector<int32_t> cta_item_ptr, unit_item_ptr;
-    std::vector<int64_t> q_pos;
-    // device copies
-    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_qpos, d_opart, d_lsepart;
-    DeviceBuffer d_counter;  // per-unit arrival counters of the fused merge (zero between launches)
-    size_t counter_units = 0;
-    void* h_stage = nullptr;  // pinned staging for async updates
-    size_t h_stage_bytes = 0;
-    cudaEvent_t staged = nullptr;
-    ~ep_plan_s() {
-        if (h_stage) cudaFreeHost(h_stage);
-        if (staged) cudaEventDestroy(staged);
-    }
-};
-
-namespace {
-
-constexpr int kBlockTokens = 64;
-
+namespace ep {
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -136,154 +94,9 @@ bool force_tc() {
     return f;
 }
 
-int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
-                    const int32_t* page_table, const int64_t* q_pos) {
-    const int B = p.batch, Hkv = p.n_kv_heads, P = p.page_tokens;
-    p.pdesc.clear();
-    p.req_page_off.assign(B + 1, 0);
-    p.q_pos.assign(q_pos, q_pos + B);
-    std::vector<int64_t> req_blocks(B, 0);
-    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
-    for (int b = 0; b < B; ++b) {
-        if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
-        if (q_pos[b] < 0) return fail(EP_EINVAL, "ep_plan: negative query position");
-        int64_t expect_pos = -1;
-        int last_origin = -1;
-        for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
-            const ep_segment& s = segs[si];
-            if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
-                return fail(EP_EINVAL, "ep_plan: negative segment field");
-            // SegmentedCache invariants (cache.cpp:25-53): gapless, origin order.
-            if (expect_pos >= 0 && s.pos_offset != expect_pos)
-                return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
-                                           std::to_string(s.pos_offset) + ", previous ends at " +
-                                           std::to_string(expect_pos));
-            if (s.origin < last_origin)
-                return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
-            expect_pos = s.pos_offset + s.len;
-            last_origin = s.origin;
-            const int64_t npg = (int64_t(s.len) + P - 1) / P;
-            for (int64_t i = 0; i < npg; ++i) {
-                const int32_t page = page_table[s.page_off + i];
-                if (page < 0 || page >= p.num_pages)
-                    return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
-                PageDesc d;
-                d.page = page;
-                d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
-                d.pos = s.pos_offset + i * P;
-                p.pdesc.push_back(d);
-                req_blocks[b] += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
-            }
-        }
-        p.req_page_off[b + 1] = int64_t(p.pdesc.size());
-    }
-    p.n_pages = int64_t(p.pdesc.size());
+}  // namespace ep
 
-    // Work split: every CTA streams the same number of 64-token blocks. Walk
-    // the (request, kv-head) units in order and cut at page boundaries.
-    int64_t total = 0;
-    for (int b = 0; b < B; ++b) total += req_blocks[b] * Hkv;
-    const int64_t cap = int64_t(p.h->n_sms) * std::max(1, decode_ctas_per_sm(p.kv_dtype, p.d_head, p.rows));
-    p.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap, total));
-    p.items.clear();
-    p.cta_item_ptr.assign(p.n_ctas + 1, 0);
-    p.unit_item_ptr.assign(int64_t(B) * Hkv + 1, 0);
-    std::vector<int32_t> item_cta;
-    int64_t acc = 0;
-    int64_t cta = 0;
-    auto boundary = [&](int64_t c) { return (total * (c + 1) + p.n_ctas - 1) / p.n_ctas; };
-    for (int b = 0; b < B; ++b) {
-        const int64_t npg = p.req_page_off[b + 1] - p.req_page_off[b];
-        for (int g = 0; g < Hkv; ++g) {
-            const int64_t unit = int64_t(b) * Hkv + g;
-            bool open = false;
-            for (int64_t lp = 0; lp < npg; ++lp) {
-                while (cta < p.n_ctas - 1 && acc >= boundary(cta)) {
-                    ++cta;
-                    open = false;
-                }
-                if (!open) {
-                    p.items.push_back(WorkItem{b, g, int32_t(lp), int32_t(lp), 0, {0, 0, 0}});
-                    item_cta.push_back(int32_t(cta));
-                    p.unit_item_ptr[unit + 1]++;
-                    open = true;
-                }
-                p.items.back().lp1 = int32_t(lp + 1);
-                const PageDesc& d = p.pdesc[p.req_page_off[b] + lp];
-                const int nb = (d.n_tok + kBlockTokens - 1) / kBlockTokens;
-                p.items.back().nblk += nb;
-                acc += nb;
-            }
-        }
-    }
-    p.n_items = int64_t(p.items.size());
-    for (int32_t c : item_cta) p.cta_item_ptr[c + 1]++;
-    for (int64_t c = 0; c < p.n_ctas; ++c) p.cta_item_ptr[c + 1] += p.cta_item_ptr[c];
-    p.has_empty_unit = false;
-    for (int64_t u = 0; u < int64_t(B) * Hkv; ++u) {
-        if (p.unit_item_ptr[u + 1] == 0) p.has_empty_unit = true;
-        p.unit_item_ptr[u + 1] += p.unit_item_ptr[u];
-    }
-    return EP_OK;
-}
-
-template <typename T>
-size_t bytes_of(const std::vector<T>& v) {
-    return v.size() * sizeof(T);
-}
-
-int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
-    struct Part {
-        DeviceBuffer* dst;
-        const void* src;
-        size_t n;
-    };
-    const Part parts[] = {
-        {&p.d_pdesc, p.pdesc.data(), bytes_of(p.pdesc)},
-        {&p.d_req_off, p.req_page_off.data(), bytes_of(p.req_page_off)},
-        {&p.d_items, p.items.data(), bytes_of(p.items)},
-        {&p.d_cta_ptr, p.cta_item_ptr.data(), bytes_of(p.cta_item_ptr)},
-        {&p.d_unit_ptr, p.unit_item_ptr.data(), bytes_of(p.unit_item_ptr)},
-        {&p.d_qpos, p.q_pos.data(), bytes_of(p.q_pos)},
-    };
-    size_t total = 0;
-    for (const Part& x : parts) total += (x.n + 255) & ~size_t(255);
-    for (const Part& x : parts) EP_CUDA_TRY(x.dst->reserve(std::max<size_t>(x.n, 16)), "ep_plan alloc");
-    const size_t ws = size_t(std::max<int64_t>(p.n_items, 1)) * p.rows;
-    EP_CUDA_TRY(p.d_opart.reserve(ws * p.d_head * sizeof(float)), "ep_plan workspace");
-    EP_CUDA_TRY(p.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
-    const size_t units = size_t(std::max(1, p.batch * p.n_kv_heads));
-    if (units > p.counter_units) {
-        EP_CUDA_TRY(p.d_counter.reserve(units * sizeof(int32_t)), "ep_plan counters");
-        EP_CUDA_TRY(cudaMemset(p.d_counter.ptr, 0, units * sizeof(int32_t)), "ep_plan counters");
-        p.counter_units = units;
-    }
-    if (!async) {
-        for (const Part& x : parts)
-            if (x.n) EP_CUDA_TRY(cudaMemcpy(x.dst->ptr, x.src, x.n, cudaMemcpyHostToDevice), "ep_plan upload");
-        return EP_OK;
-    }
-    if (p.staged) EP_CUDA_TRY(cudaEventSynchronize(p.staged), "ep_plan_update wait");
-    if (total > p.h_stage_bytes) {
-        if (p.h_stage) cudaFreeHost(p.h_stage);
-        p.h_stage = nullptr;
-        EP_CUDA_TRY(cudaMallocHost(&p.h_stage, total), "ep_plan_update pinned");
-        p.h_stage_bytes = total;
-    }
-    if (!p.staged) EP_CUDA_TRY(cudaEventCreateWithFlags(&p.staged, cudaEventDisableTiming), "event");
-    size_t off = 0;
-    for (const Part& x : parts) {
-        if (x.n) {
-            std::memcpy(static_cast<char*>(p.h_stage) + off, x.src, x.n);
-            EP_CUDA_TRY(cudaMemcpyAsync(x.dst->ptr, static_cast<char*>(p.h_stage) + off, x.n,
-                                        cudaMemcpyHostToDevice, s),
-                        "ep_plan_update copy");
-        }
-        off += (x.n + 255) & ~size_t(255);
-    }
-    EP_CUDA_TRY(cudaEventRecord(p.staged, s), "ep_plan_update event");
-    return EP_OK;
-}
+namespace {
 
 bool valid_dt(int dt) { return dt == EP_F32 || dt == EP_BF16; }
 
@@ -477,146 +290,6 @@ int ep_merge_partials_packed_dev(ep_handle h, int32_t n_parts, const float* pack
                                     static_cast<cudaStream_t>(stream)),
                 "merge_partials_packed launch");
     if (rows > 0) h->launches++;
-    return EP_OK;
-}
-
-// ------------------------------------------------------------ (3) plans --
-
-int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,
-                   int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
-                   const int32_t* page_table, const int64_t* q_pos, int32_t ctas_per_sm,
-                   ep_plan* out) {
-    if (!h || !pool || !out || !seg_indptr || !q_pos) return fail(EP_EINVAL, "ep_plan_create: null argument");
-    *out = nullptr;
-    if (!valid_dt(pool->dtype)) return fail(EP_EUNSUPPORTED, "ep_plan_create: kv dtype must be f32 or bf16");
-    if (pool->n_kv_heads <= 0 || n_q_heads <= 0 || n_q_heads % pool->n_kv_heads)
-        return fail(EP_EINVAL, "ep_plan_create: n_q_heads must be a multiple of n_kv_heads");
-    if (pool->page_tokens <= 0 || pool->page_tokens % kBlockTokens)
-        return fail(EP_EUNSUPPORTED, "ep_plan_create: page_tokens must be a multiple of 64");
-    if (batch < 0 || n_q <= 0) return fail(EP_EINVAL, "ep_plan_create: batch/n_q");
-    const int rows = (n_q_heads / pool->n_kv_heads) * n_q;
-    const bool k1 = decode_supported(pool->dtype, pool->d_head, rows);
-    const bool k3 = verify_supported(pool->dtype, pool->d_head, rows);
-    if (!k1 && !k3)
-        return fail(EP_EUNSUPPORTED, "ep_plan_create: no kernel for kv dtype " + std::to_string(pool->dtype) +
-                                         ", d_head=" + std::to_string(pool->d_head) + ", rows=group*n_q=" +
-                                         std::to_string(rows) +
-                                         " (CUDA-core decode: rows 1/2/4/8; tcgen05 verify: bf16, d 128, rows <= 64)");
-    std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
-    if (!p) return fail(EP_ENOMEM, "ep_plan_create");
-    p->h = h;
-    p->kv_dtype = pool->dtype;
-    p->n_kv_heads = pool->n_kv_heads;
-    p->d_head = pool->d_head;
-    p->page_tokens = pool->page_tokens;
-    p->num_pages = pool->num_pages;
-    p->n_q_heads = n_q_heads;
-    p->n_q = n_q;
-    p->batch = batch;
-    p->rows = rows;
-    p->use_tc = k3 && (!k1 || force_tc());
-    (void)ctas_per_sm;
-    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
-    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create");
-    if (int rc = upload_plan(*p, nullptr, false)) return rc;
-    *out = p.release();
-    return EP_OK;
-}
-
-int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
-                   const int32_t* page_table, const int64_t* q_pos, ep_stream stream) {
-    if (!p) return fail(EP_EINVAL, "ep_plan_update: null plan");
-    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
-    return upload_plan(*p, static_cast<cudaStream_t>(stream), true);
-}
-
-int ep_plan_destroy(ep_plan p) {
-    delete p;
-    return EP_OK;
-}
-
-int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages) {
-    if (!p) return fail(EP_EINVAL, "ep_plan_info: null plan");
-    if (n_ctas) *n_ctas = p->n_ctas;
-    if (n_items) *n_items = p->n_items;
-    if (n_pages) *n_pages = p->n_pages;
-    return EP_OK;
-}
-
-int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype,
-                         const void* q, int32_t o_dtype, void* o, float* lse, ep_stream stream) {
-    if (!h || !p || !pool || !q || !o) return fail(EP_EINVAL, "ep_spliced_attention: null argument");
-    if (pool->dtype != p->kv_dtype || pool->n_kv_heads != p->n_kv_heads ||
-        pool->d_head != p->d_head || pool->page_tokens != p->page_tokens ||
-        pool->num_pages < p->num_pages)
-        return fail(EP_EINVAL, "ep_spliced_attention: pool does not match the plan");
-    if (!valid_dt(q_dtype) || !valid_dt(o_dtype))
-        return fail(EP_EUNSUPPORTED, "ep_spliced_attention: q/o dtype must be f32 or bf16");
-    DecodeArgs a{};
-    a.k_pages = pool->k_pages;
-    a.v_pages = pool->v_pages;
-    a.n_kv_heads = p->n_kv_heads;
-    a.n_q_heads = p->n_q_heads;
-    a.page_tokens = p->page_tokens;
-    a.n_q = p->n_q;
-    a.pdesc = static_cast<const PageDesc*>(p->d_pdesc.ptr);
-    a.req_page_off = static_cast<const int64_t*>(p->d_req_off.ptr);
-    a.items = static_cast<const WorkItem*>(p->d_items.ptr);
-    a.cta_item_ptr = static_cast<const int32_t*>(p->d_cta_ptr.ptr);
-    a.unit_item_ptr = static_cast<const int32_t*>(p->d_unit_ptr.ptr);
-    a.q_pos = static_cast<const int64_t*>(p->d_qpos.ptr);
-    a.q = q;
-    a.q_dtype = q_dtype;
-    a.o_part = static_cast<float*>(p->d_opart.ptr);
-    a.lse_part = static_cast<float*>(p->d_lsepart.ptr);
-    a.o = o;
-    a.o_dtype = o_dtype;
-    a.lse = lse;
-    a.batch = p->batch;
-    a.q_scale = float(1.4426950408889634 / std::sqrt(double(p->d_head)));
-    a.zero_rows = h->zero_rows.ptr;
-    a.unit_counter = static_cast<int32_t*>(p->d_counter.ptr);
-    a.trace = nullptr;
-    static unsigned long long* trace_buf = [] {
-        unsigned long long* t = nullptr;
-        const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&t, 12 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(t, 0, 12 * 1024 * sizeof(unsigned long long));
-        return t;
-    }();
-    a.trace = trace_buf;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (p->n_items > 0 && p->use_tc) {
-        if (p->tm_k != pool->k_pages || p->tm_v != pool->v_pages || p->tm_pages != pool->num_pages) {
-            const int64_t rows_total = pool->num_pages * pool->n_kv_heads * pool->page_tokens;
-            if (int rc = encode_kv_map(&p->tmap_k, pool->k_pages, rows_total)) return rc;
-            if (int rc = encode_kv_map(&p->tmap_v, pool->v_pages, rows_total)) return rc;
-            p->tm_k = pool->k_pages;
-            p->tm_v = pool->v_pages;
-            p->tm_pages = pool->num_pages;
-        }
-        EP_CUDA_TRY(launch_verify_attention(int(p->n_ctas), a, p->tmap_k, p->tmap_v, p->rows, s),
-                    "verify attention launch");
-        h->launches++;
-        if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
-            std::vector<unsigned long long> host(12 * 1024);
-            cudaStreamSynchronize(s);
-            cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            const char* f = std::getenv("EP_TRACE_FILE");
-            if (FILE* fp = std::fopen(f ? f : "ep_trace.bin", "wb")) {
-                std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
-                std::fclose(fp);
-            }
-        }
-    } else if (p->n_items > 0) {
-        EP_CUDA_TRY(launch_spliced_decode(p->kv_dtype, p->d_head, p->rows, int(p->n_ctas), a, s),
-                    "spliced decode launch");
-        h->launches++;
-    }
-    if (p->has_empty_unit) {
-        EP_CUDA_TRY(launch_empty_units(p->d_head, p->rows, a, s), "empty units launch");
-        h->launches++;
-    }
     return EP_OK;
 }
 

@@ -12,6 +12,12 @@
 
 #include "ep/ep_attn.h"
 
+#define EP_CUDA_TRY(expr, where)                               \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return ep::cuda_fail(_e, where); \
+    } while (0)
+
 namespace ep {
 
 // Sets the thread-local message returned by ep_last_error() and returns rc.
@@ -67,12 +73,14 @@ struct PageDesc {
 };
 
 struct WorkItem {
-    int32_t b;     // request
+    int32_t b;     // (virtual) request whose page list the item walks
     int32_t g;     // kv head
     int32_t lp0;   // logical page range [lp0, lp1) of request b
     int32_t lp1;
     int32_t nblk;  // 64-token pipeline blocks in the range
-    int32_t pad[3];
+    int32_t rq0;   // first real request of the item's query rows (K3 row groups)
+    int32_t q0min; // smallest query position of those rows (all-visible fast path)
+    int32_t pad;
 };
 
 struct DecodeArgs {
@@ -97,7 +105,20 @@ struct DecodeArgs {
     const void* zero_rows;    // >= 64 zero K/V rows (page-tail fill)
     int32_t* unit_counter;    // [batch*Hkv], zero between launches (fused K2)
     unsigned long long* trace;  // optional clock64 event trace of CTA 0 (debug, may be null)
+    int32_t reqs_per_unit;    // K3: consecutive requests whose rows share one tile (cascade), else 1
 };
+
+// TMA tensor maps over bf16 row-major matrices (capi.cpp).
+int encode_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                   uint32_t box_inner, uint32_t box_outer);
+int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows);
+bool force_tc();
+
+// Cascade (shared-prefix) merge: per row, LSE-merge the shared-pass partial
+// (part 0, only where has_shared[request]) with the private-pass partial.
+cudaError_t launch_cascade_merge(int rows, int d, int row_per_req, const float* o_parts,
+                                 const float* lse_parts, const uint8_t* has_shared, void* o,
+                                 int o_dtype, float* lse, cudaStream_t s);
 
 // R = rows per (request, kv-head) = group * n_q.
 bool decode_supported(int kv_dtype, int d_head, int rows);

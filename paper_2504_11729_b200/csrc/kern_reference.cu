@@ -338,3 +338,48 @@ cudaError_t launch_merge_packed(int n_parts, const float* packed, int rows, int 
 }
 
 }  // namespace ep
+
+namespace ep {
+namespace {
+
+// Cascade merge (config 5): per output row, the shared-prefix partial (part 0,
+// keys at the lowest positions — only for requests that have one) and the
+// private-remainder partial (part 1), folded in that (segment) order by LSE as
+// merge_partials does (attention.cpp:116-145). One warp per row.
+__global__ void cascade_merge_kernel(int rows, int d, int row_per_req, const float* __restrict__ po,
+                                     const float* __restrict__ pl, const uint8_t* __restrict__ has_shared,
+                                     void* o, int o_dtype, float* __restrict__ lse) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    const bool sh = has_shared[row / row_per_req] != 0;
+    const float l0 = sh ? pl[row] : -INFINITY, l1 = pl[rows + row];
+    const float M = fmaxf(l0, l1);
+    const float w0 = (M == -INFINITY || l0 == -INFINITY) ? 0.f : expf(l0 - M);
+    const float w1 = (M == -INFINITY || l1 == -INFINITY) ? 0.f : expf(l1 - M);
+    const float L = w0 + w1;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    for (int c = lane; c < d; c += 32) {
+        const float x0 = w0 > 0.f ? po[size_t(row) * d + c] * w0 : 0.f;
+        const float x1 = w1 > 0.f ? po[(size_t(rows) + row) * d + c] * w1 : 0.f;
+        const float val = (x0 + x1) * inv;
+        if (o_dtype == EP_BF16)
+            static_cast<__nv_bfloat16*>(o)[size_t(row) * d + c] = __float2bfloat16_rn(val);
+        else
+            static_cast<float*>(o)[size_t(row) * d + c] = val;
+    }
+    if (lane == 0 && lse) lse[row] = L > 0.f ? M + logf(L) : -INFINITY;
+}
+
+}  // namespace
+
+cudaError_t launch_cascade_merge(int rows, int d, int row_per_req, const float* o_parts,
+                                 const float* lse_parts, const uint8_t* has_shared, void* o,
+                                 int o_dtype, float* lse, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    cascade_merge_kernel<<<(rows + 7) / 8, 256, 0, s>>>(rows, d, row_per_req, o_parts, lse_parts,
+                                                        has_shared, o, o_dtype, lse);
+    return cudaGetLastError();
+}
+
+}  // namespace ep

@@ -49,7 +49,7 @@ constexpr int kSoftWarps = 8;  // 2 ping-pong groups x 4 TMEM lane quarters
 constexpr int kSoftThreads = kSoftWarps * 32;
 constexpr int kProdWarp = 8, kMmaWarp = 9, kProdVWarp = 10;
 constexpr int kThreads = 352;
-constexpr int kMaxRows = 64;      // valid query rows per (request, kv-head)
+constexpr int kMaxRows = 128;     // valid query rows per tile (one M = 128 MMA tile)
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
 
 constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
@@ -295,7 +295,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quarter = warp & 3, grp = warp >> 2;  // TMEM lane quarter, ping-pong group
         const int m = quarter * 32 + lane;               // M row = TMEM lane
         const int v = lane * 4 + quarter;                // query row index of this M row
-        const bool valid_row = v < rows;
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         const uint32_t tS = tmem + kColS + grp * kBT + lane_off;
         const uint32_t tOg = tmem + kColO + grp * kD + lane_off;
@@ -305,14 +304,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t gi0 = 0;         // global index of the item's first block
         for (int it = it0; it < it1; ++it, ++n) {
             const WorkItem w = a.items[it];
-            const int64_t q0 = a.q_pos[w.b];
-            const int qi = v / G, h = w.g * G + v % G;
-            const int64_t my_qpos = q0 + qi;
+            const int nrows = w.pad > 0 ? w.pad : rows;  // valid rows of this item's tile
+            const bool valid_row = v < nrows;
+            // Row v of the tile: request rq0 + v / (G n_q), query row qi, head h.
+            // A tile spans several requests in the shared-prefix (cascade) pass.
+            const int rpr = G * a.n_q;
+            const int rq = w.rq0 + v / rpr, qi = (v % rpr) / G, h = w.g * G + v % G;
+            const int64_t q0 = w.q0min;
+            const int64_t my_qpos = (valid_row ? a.q_pos[rq] : q0) + qi;
 
             // ---- Q tile -> TMEM (A operand of QK): group g writes d-half g ----
             {
                 const uint8_t* src = static_cast<const uint8_t*>(a.q) +
-                                     (((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
+                                     (((size_t(rq) * a.n_q + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
                 uint32_t qv[32];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -465,7 +469,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
             if (valid_row) {
                 if (n_items == 1) {
-                    const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
+                    const size_t orow = (size_t(rq) * a.n_q + qi) * a.n_q_heads + h;
                     if (a.o_dtype == EP_BF16) {
                         uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD + grp * 64);
 #pragma unroll
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 named_bar_sync(5, kSoftThreads);
                 if (*s_flag) {
                     __threadfence();
-                    for (int idx = threadIdx.x; idx < rows * kD; idx += kSoftThreads) {
+                    for (int idx = threadIdx.x; idx < nrows * kD; idx += kSoftThreads) {
                         const int r = idx / kD, c = idx % kD;
                         float Mx = -INFINITY;
                         for (int i2 = u0; i2 < u0 + n_items; ++i2)
@@ -510,8 +514,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                         const bool er = !(Ls > 0.f);
-                        const int qi2 = r / G, h2 = w.g * G + r % G;
-                        const size_t orow = (size_t(w.b) * a.n_q + qi2) * a.n_q_heads + h2;
+                        const int rq2 = w.rq0 + r / rpr, qi2 = (r % rpr) / G, h2 = w.g * G + r % G;
+                        const size_t orow = (size_t(rq2) * a.n_q + qi2) * a.n_q_heads + h2;
                         const float val = er ? 0.f : acc / Ls;
                         if (a.o_dtype == EP_BF16)
                             static_cast<__nv_bfloat16*>(a.o)[orow * kD + c] = __float2bfloat16_rn(val);

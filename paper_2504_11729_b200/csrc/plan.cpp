@@ -1,0 +1,503 @@
+// plan.cpp — the device-resident splice-table plan (ep_plan_*) and the
+// spliced-attention launch (ep_spliced_attention).
+//
+// The reference walks, per session, per layer and per head, an ordered list
+// of KVSegments and calls partial_attention per segment (model.cpp:161-182,
+// cache.cpp:25-103). Here the host turns the whole batch's splice table into
+// device work lists once (and again only when it changes):
+//
+//   * every request's segments become a list of page descriptors
+//     {page, valid tokens, absolute position} (validated with the reference's
+//     invariants: gapless positions, origin order — cache.cpp:25-53);
+//   * "virtual requests" (a page list + the query rows that attend to it) are
+//     cut into work items so every CTA (one per SM) streams the same number of
+//     64-token blocks ("stream-K" over pages, crossing (request, kv-head)
+//     boundaries; split units merge by LSE inside the kernels);
+//   * cascade: when consecutive requests share an identical first segment
+//     (the same cloud-prompt pages, config 5), that prefix is attended ONCE per
+//     kv-head for tiles of up to 128 query rows spanning 128/(G n_q) requests
+//     on the tensor cores (K3), the private remainder per request by K1/K3,
+//     and a 2-way LSE merge combines them.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "ep_internal.h"
+
+using namespace ep;
+
+namespace {
+
+constexpr int kBlockTokens = 64;
+
+// One query-row set attending to one page list.
+struct VReq {
+    std::vector<PageDesc> pages;
+    int32_t rq0;     // first real request of the rows
+    int64_t q0min;   // smallest query position among the rows
+    int32_t n_rows;  // valid rows (<= the sub-plan's row stride)
+};
+
+struct SubPlan {
+    int rows = 0;  // row stride per unit
+    bool tc = false;
+    int64_t n_ctas = 0, n_items = 0, n_pages = 0, n_units = 0;
+    bool has_empty_unit = false;
+    std::vector<PageDesc> pdesc;
+    std::vector<int64_t> req_page_off;
+    std::vector<WorkItem> items;
+    std::vector<int32_t> cta_item_ptr, unit_item_ptr;
+    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_opart, d_lsepart, d_counter;
+    size_t counter_units = 0;
+};
+
+void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t cap_ctas) {
+    sp.pdesc.clear();
+    sp.req_page_off.assign(vr.size() + 1, 0);
+    std::vector<int64_t> blocks(vr.size(), 0);
+    for (size_t b = 0; b < vr.size(); ++b) {
+        for (const PageDesc& d : vr[b].pages) {
+            sp.pdesc.push_back(d);
+            blocks[b] += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+        }
+        sp.req_page_off[b + 1] = int64_t(sp.pdesc.size());
+    }
+    sp.n_pages = int64_t(sp.pdesc.size());
+    sp.n_units = int64_t(vr.size()) * Hkv;
+    int64_t total = 0;
+    for (int64_t x : blocks) total += x * Hkv;
+    sp.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap_ctas, total));
+    sp.items.clear();
+    sp.cta_item_ptr.assign(sp.n_ctas + 1, 0);
+    sp.unit_item_ptr.assign(sp.n_units + 1, 0);
+    std::vector<int32_t> item_cta;
+    int64_t acc = 0, cta = 0;
+    auto boundary = [&](int64_t c) { return (total * (c + 1) + sp.n_ctas - 1) / sp.n_ctas; };
+    for (size_t b = 0; b < vr.size(); ++b) {
+        const int64_t npg = sp.req_page_off[b + 1] - sp.req_page_off[b];
+        for (int g = 0; g < Hkv; ++g) {
+            const int64_t unit = int64_t(b) * Hkv + g;
+            bool open = false;
+            for (int64_t lp = 0; lp < npg; ++lp) {
+                while (cta < sp.n_ctas - 1 && acc >= boundary(cta)) {
+                    ++cta;
+                    open = false;
+                }
+                if (!open) {
+                    WorkItem w{};
+                    w.b = int32_t(b);
+                    w.g = g;
+                    w.lp0 = w.lp1 = int32_t(lp);
+                    w.nblk = 0;
+                    w.rq0 = vr[b].rq0;
+                    w.q0min = int32_t(vr[b].q0min);
+                    w.pad = vr[b].n_rows;
+                    sp.items.push_back(w);
+                    item_cta.push_back(int32_t(cta));
+                    sp.unit_item_ptr[unit + 1]++;
+                    open = true;
+                }
+                sp.items.back().lp1 = int32_t(lp + 1);
+                const PageDesc& d = sp.pdesc[sp.req_page_off[b] + lp];
+                const int nb = (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+                sp.items.back().nblk += nb;
+                acc += nb;
+            }
+        }
+    }
+    sp.n_items = int64_t(sp.items.size());
+    for (int32_t c : item_cta) sp.cta_item_ptr[c + 1]++;
+    for (int64_t c = 0; c < sp.n_ctas; ++c) sp.cta_item_ptr[c + 1] += sp.cta_item_ptr[c];
+    sp.has_empty_unit = false;
+    for (int64_t u = 0; u < sp.n_units; ++u) {
+        if (sp.unit_item_ptr[u + 1] == 0) sp.has_empty_unit = true;
+        sp.unit_item_ptr[u + 1] += sp.unit_item_ptr[u];
+    }
+}
+
+template <typename T>
+size_t bytes_of(const std::vector<T>& v) {
+    return v.size() * sizeof(T);
+}
+
+}  // namespace
+
+struct ep_plan_s {
+    ep_handle h = nullptr;
+    int32_t kv_dtype = 0, n_kv_heads = 0, d_head = 0, page_tokens = 0;
+    int64_t num_pages = 0;
+    int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
+    bool cascade = false;
+    SubPlan main;    // whole table (non-cascade) or the private remainders (cascade)
+    SubPlan shared;  // cascade: shared prefixes, row-group tiles on K3
+    std::vector<int64_t> q_pos;
+    std::vector<uint8_t> has_shared;  // per request (cascade)
+    DeviceBuffer d_qpos, d_has_shared, d_parts_o, d_parts_lse;
+    // staging for stream-ordered updates
+    void* h_stage = nullptr;
+    size_t h_stage_bytes = 0;
+    cudaEvent_t staged = nullptr;
+    CUtensorMap tmap_k{}, tmap_v{};
+    const void* tm_k = nullptr;
+    const void* tm_v = nullptr;
+    int64_t tm_pages = -1;
+    ~ep_plan_s() {
+        if (h_stage) cudaFreeHost(h_stage);
+        if (staged) cudaEventDestroy(staged);
+    }
+};
+
+namespace {
+
+bool cascade_allowed(const ep_plan_s& p) {
+    static const bool off = [] {
+        const char* e = std::getenv("EP_NO_CASCADE");
+        return e && e[0] == '1';
+    }();
+    const int rpr = (p.n_q_heads / p.n_kv_heads) * p.n_q;
+    return !off && verify_supported(p.kv_dtype, p.d_head, rpr) && rpr <= 128 && 128 / rpr >= 2;
+}
+
+int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
+                    const int32_t* page_table, const int64_t* q_pos) {
+    const int B = p.batch, Hkv = p.n_kv_heads, P = p.page_tokens;
+    const int rpr = (p.n_q_heads / Hkv) * p.n_q;
+    p.q_pos.assign(q_pos, q_pos + B);
+    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
+    // per request: page descriptors, and where its first segment's pages end
+    std::vector<std::vector<PageDesc>> req_pages(B);
+    std::vector<int64_t> first_seg_pages(B, 0);
+    for (int b = 0; b < B; ++b) {
+        if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
+        if (q_pos[b] < 0 || q_pos[b] > INT32_MAX) return fail(EP_EINVAL, "ep_plan: query position out of range");
+        int64_t expect_pos = -1;
+        int last_origin = -1;
+        for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
+            const ep_segment& s = segs[si];
+            if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
+                return fail(EP_EINVAL, "ep_plan: negative segment field");
+            // SegmentedCache invariants (cache.cpp:25-53): gapless, origin order.
+            if (expect_pos >= 0 && s.pos_offset != expect_pos)
+                return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
+                                           std::to_string(s.pos_offset) + ", previous ends at " +
+                                           std::to_string(expect_pos));
+            if (s.origin < last_origin)
+                return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
+            expect_pos = s.pos_offset + s.len;
+            last_origin = s.origin;
+            const int64_t npg = (int64_t(s.len) + P - 1) / P;
+            for (int64_t i = 0; i < npg; ++i) {
+                const int32_t page = page_table[s.page_off + i];
+                if (page < 0 || page >= p.num_pages)
+                    return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
+                PageDesc d;
+                d.page = page;
+                d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
+                d.pos = s.pos_offset + i * P;
+                req_pages[b].push_back(d);
+            }
+            if (si == seg_indptr[b]) first_seg_pages[b] = int64_t(req_pages[b].size());
+        }
+    }
+    const int64_t cap = int64_t(p.h->n_sms);
+
+    // ---- cascade detection: runs of consecutive requests whose first segment
+    // is the same page list (a shared cloud prompt) ----
+    p.cascade = false;
+    p.has_shared.assign(B, 0);
+    std::vector<VReq> shared_vr;
+    const int group_cap = cascade_allowed(p) ? 128 / rpr : 0;
+    if (group_cap >= 2) {
+        auto same_first = [&](int a, int b) {
+            if (first_seg_pages[a] != first_seg_pages[b] || first_seg_pages[a] < 2) return false;
+            for (int64_t i = 0; i < first_seg_pages[a]; ++i) {
+                const PageDesc &x = req_pages[a][i], &y = req_pages[b][i];
+                if (x.page != y.page || x.n_tok != y.n_tok || x.pos != y.pos) return false;
+            }
+            return true;
+        };
+        int b = 0;
+        while (b < B) {
+            int e = b + 1;
+            while (e < B && same_first(b, e)) ++e;
+            if (e - b >= 2) {
+                for (int r0 = b; r0 < e; r0 += group_cap) {
+                    const int r1 = std::min(e, r0 + group_cap);
+                    VReq v;
+                    v.pages.assign(req_pages[r0].begin(), req_pages[r0].begin() + first_seg_pages[r0]);
+                    v.rq0 = r0;
+                    v.q0min = q_pos[r0];
+                    for (int r = r0; r < r1; ++r) {
+                        v.q0min = std::min<int64_t>(v.q0min, q_pos[r]);
+                        p.has_shared[r] = 1;
+                    }
+                    v.n_rows = (r1 - r0) * rpr;
+                    shared_vr.push_back(std::move(v));
+                }
+            }
+            b = e;
+        }
+        p.cascade = !shared_vr.empty();
+    }
+    std::vector<VReq> main_vr(B);
+    for (int b = 0; b < B; ++b) {
+        const int64_t skip = p.has_shared[b] ? first_seg_pages[b] : 0;
+        main_vr[b].pages.assign(req_pages[b].begin() + skip, req_pages[b].end());
+        main_vr[b].rq0 = b;
+        main_vr[b].q0min = q_pos[b];
+        main_vr[b].n_rows = rpr;
+    }
+    build_subplan(p.main, main_vr, Hkv, cap);
+    p.main.rows = rpr;
+    p.main.tc = !decode_supported(p.kv_dtype, p.d_head, rpr) || force_tc();
+    if (p.cascade) {
+        build_subplan(p.shared, shared_vr, Hkv, cap);
+        p.shared.rows = group_cap * rpr;
+        p.shared.tc = true;
+    }
+    return EP_OK;
+}
+
+int upload_subplan(SubPlan& sp, int d_head, std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>>& parts) {
+    parts.push_back({&sp.d_pdesc, {sp.pdesc.data(), bytes_of(sp.pdesc)}});
+    parts.push_back({&sp.d_req_off, {sp.req_page_off.data(), bytes_of(sp.req_page_off)}});
+    parts.push_back({&sp.d_items, {sp.items.data(), bytes_of(sp.items)}});
+    parts.push_back({&sp.d_cta_ptr, {sp.cta_item_ptr.data(), bytes_of(sp.cta_item_ptr)}});
+    parts.push_back({&sp.d_unit_ptr, {sp.unit_item_ptr.data(), bytes_of(sp.unit_item_ptr)}});
+    const size_t ws = size_t(std::max<int64_t>(sp.n_items, 1)) * sp.rows;
+    EP_CUDA_TRY(sp.d_opart.reserve(ws * d_head * sizeof(float)), "ep_plan workspace");
+    EP_CUDA_TRY(sp.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
+    const size_t units = size_t(std::max<int64_t>(1, sp.n_units));
+    if (units > sp.counter_units) {
+        EP_CUDA_TRY(sp.d_counter.reserve(units * sizeof(int32_t)), "ep_plan counters");
+        EP_CUDA_TRY(cudaMemset(sp.d_counter.ptr, 0, units * sizeof(int32_t)), "ep_plan counters");
+        sp.counter_units = units;
+    }
+    return EP_OK;
+}
+
+int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
+    std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>> parts;
+    parts.push_back({&p.d_qpos, {p.q_pos.data(), bytes_of(p.q_pos)}});
+    parts.push_back({&p.d_has_shared, {p.has_shared.data(), bytes_of(p.has_shared)}});
+    if (int rc = upload_subplan(p.main, p.d_head, parts)) return rc;
+    if (p.cascade) {
+        if (int rc = upload_subplan(p.shared, p.d_head, parts)) return rc;
+        const size_t rows = size_t(p.batch) * p.n_q * p.n_q_heads;
+        EP_CUDA_TRY(p.d_parts_o.reserve(2 * rows * p.d_head * sizeof(float)), "ep_plan cascade ws");
+        EP_CUDA_TRY(p.d_parts_lse.reserve(2 * rows * sizeof(float)), "ep_plan cascade ws");
+    }
+    size_t total = 0;
+    for (auto& x : parts) total += (x.second.second + 255) & ~size_t(255);
+    for (auto& x : parts) EP_CUDA_TRY(x.first->reserve(std::max<size_t>(x.second.second, 16)), "ep_plan alloc");
+    if (!async) {
+        for (auto& x : parts)
+            if (x.second.second)
+                EP_CUDA_TRY(cudaMemcpy(x.first->ptr, x.second.first, x.second.second, cudaMemcpyHostToDevice),
+                            "ep_plan upload");
+        return EP_OK;
+    }
+    if (p.staged) EP_CUDA_TRY(cudaEventSynchronize(p.staged), "ep_plan_update wait");
+    if (total > p.h_stage_bytes) {
+        if (p.h_stage) cudaFreeHost(p.h_stage);
+        p.h_stage = nullptr;
+        EP_CUDA_TRY(cudaMallocHost(&p.h_stage, total), "ep_plan_update pinned");
+        p.h_stage_bytes = total;
+    }
+    if (!p.staged) EP_CUDA_TRY(cudaEventCreateWithFlags(&p.staged, cudaEventDisableTiming), "event");
+    size_t off = 0;
+    for (auto& x : parts) {
+        if (x.second.second) {
+            std::memcpy(static_cast<char*>(p.h_stage) + off, x.second.first, x.second.second);
+            EP_CUDA_TRY(cudaMemcpyAsync(x.first->ptr, static_cast<char*>(p.h_stage) + off, x.second.second,
+                                        cudaMemcpyHostToDevice, s),
+                        "ep_plan_update copy");
+        }
+        off += (x.second.second + 255) & ~size_t(255);
+    }
+    EP_CUDA_TRY(cudaEventRecord(p.staged, s), "ep_plan_update event");
+    return EP_OK;
+}
+
+bool valid_dt(int dt) { return dt == EP_F32 || dt == EP_BF16; }
+
+DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* pool, int32_t q_dtype,
+                     const void* q, int32_t o_dtype, void* o, float* lse) {
+    DecodeArgs a{};
+    a.k_pages = pool->k_pages;
+    a.v_pages = pool->v_pages;
+    a.n_kv_heads = p.n_kv_heads;
+    a.n_q_heads = p.n_q_heads;
+    a.page_tokens = p.page_tokens;
+    a.n_q = p.n_q;
+    a.pdesc = static_cast<const PageDesc*>(sp.d_pdesc.ptr);
+    a.req_page_off = static_cast<const int64_t*>(sp.d_req_off.ptr);
+    a.items = static_cast<const WorkItem*>(sp.d_items.ptr);
+    a.cta_item_ptr = static_cast<const int32_t*>(sp.d_cta_ptr.ptr);
+    a.unit_item_ptr = static_cast<const int32_t*>(sp.d_unit_ptr.ptr);
+    a.q_pos = static_cast<const int64_t*>(p.d_qpos.ptr);
+    a.q = q;
+    a.q_dtype = q_dtype;
+    a.o_part = static_cast<float*>(sp.d_opart.ptr);
+    a.lse_part = static_cast<float*>(sp.d_lsepart.ptr);
+    a.o = o;
+    a.o_dtype = o_dtype;
+    a.lse = lse;
+    a.batch = int32_t(sp.n_units / std::max(1, p.n_kv_heads));
+    a.q_scale = float(1.4426950408889634 / std::sqrt(double(p.d_head)));
+    a.zero_rows = p.h->zero_rows.ptr;
+    a.unit_counter = static_cast<int32_t*>(sp.d_counter.ptr);
+    a.trace = nullptr;
+    a.reqs_per_unit = 1;
+    return a;
+}
+
+unsigned long long* trace_buffer() {
+    static unsigned long long* t = [] {
+        unsigned long long* b = nullptr;
+        const char* e = std::getenv("EP_TRACE");
+        if (e && e[0] == '1' && cudaMalloc(&b, 12 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 12 * 1024 * sizeof(unsigned long long));
+        return b;
+    }();
+    return t;
+}
+
+int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs a, cudaStream_t s) {
+    ep_handle h = p.h;
+    if (sp.n_items > 0 && sp.tc) {
+        if (p.tm_k != pool->k_pages || p.tm_v != pool->v_pages || p.tm_pages != pool->num_pages) {
+            const int64_t rows_total = pool->num_pages * pool->n_kv_heads * pool->page_tokens;
+            if (int rc = encode_kv_map(&p.tmap_k, pool->k_pages, rows_total)) return rc;
+            if (int rc = encode_kv_map(&p.tmap_v, pool->v_pages, rows_total)) return rc;
+            p.tm_k = pool->k_pages;
+            p.tm_v = pool->v_pages;
+            p.tm_pages = pool->num_pages;
+        }
+        a.trace = trace_buffer();
+        EP_CUDA_TRY(launch_verify_attention(int(sp.n_ctas), a, p.tmap_k, p.tmap_v, sp.rows, s),
+                    "verify attention launch");
+        h->launches++;
+        if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
+            std::vector<unsigned long long> host(12 * 1024);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+            const char* f = std::getenv("EP_TRACE_FILE");
+            if (FILE* fp = std::fopen(f ? f : "ep_trace.bin", "wb")) {
+                std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
+                std::fclose(fp);
+            }
+        }
+    } else if (sp.n_items > 0) {
+        EP_CUDA_TRY(launch_spliced_decode(p.kv_dtype, p.d_head, sp.rows, int(sp.n_ctas), a, s),
+                    "spliced decode launch");
+        h->launches++;
+    }
+    if (sp.has_empty_unit) {
+        EP_CUDA_TRY(launch_empty_units(p.d_head, sp.rows, a, s), "empty units launch");
+        h->launches++;
+    }
+    return EP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,
+                   int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, int32_t ctas_per_sm,
+                   ep_plan* out) {
+    if (!h || !pool || !out || !seg_indptr || !q_pos) return fail(EP_EINVAL, "ep_plan_create: null argument");
+    *out = nullptr;
+    if (!valid_dt(pool->dtype)) return fail(EP_EUNSUPPORTED, "ep_plan_create: kv dtype must be f32 or bf16");
+    if (pool->n_kv_heads <= 0 || n_q_heads <= 0 || n_q_heads % pool->n_kv_heads)
+        return fail(EP_EINVAL, "ep_plan_create: n_q_heads must be a multiple of n_kv_heads");
+    if (pool->page_tokens <= 0 || pool->page_tokens % kBlockTokens)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create: page_tokens must be a multiple of 64");
+    if (batch < 0 || n_q <= 0) return fail(EP_EINVAL, "ep_plan_create: batch/n_q");
+    const int rows = (n_q_heads / pool->n_kv_heads) * n_q;
+    const bool k1 = decode_supported(pool->dtype, pool->d_head, rows);
+    const bool k3 = verify_supported(pool->dtype, pool->d_head, rows) && rows <= 64;
+    if (!k1 && !k3)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create: no kernel for kv dtype " + std::to_string(pool->dtype) +
+                                         ", d_head=" + std::to_string(pool->d_head) + ", rows=group*n_q=" +
+                                         std::to_string(rows) +
+                                         " (CUDA-core decode: rows 1/2/4/8; tcgen05 verify: bf16, d 128, rows <= 64)");
+    std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
+    if (!p) return fail(EP_ENOMEM, "ep_plan_create");
+    p->h = h;
+    p->kv_dtype = pool->dtype;
+    p->n_kv_heads = pool->n_kv_heads;
+    p->d_head = pool->d_head;
+    p->page_tokens = pool->page_tokens;
+    p->num_pages = pool->num_pages;
+    p->n_q_heads = n_q_heads;
+    p->n_q = n_q;
+    p->batch = batch;
+    p->rows = rows;
+    (void)ctas_per_sm;
+    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create");
+    if (int rc = upload_plan(*p, nullptr, false)) return rc;
+    *out = p.release();
+    return EP_OK;
+}
+
+int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
+                   const int32_t* page_table, const int64_t* q_pos, ep_stream stream) {
+    if (!p) return fail(EP_EINVAL, "ep_plan_update: null plan");
+    if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
+    return upload_plan(*p, static_cast<cudaStream_t>(stream), true);
+}
+
+int ep_plan_destroy(ep_plan p) {
+    delete p;
+    return EP_OK;
+}
+
+int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages) {
+    if (!p) return fail(EP_EINVAL, "ep_plan_info: null plan");
+    if (n_ctas) *n_ctas = p->main.n_ctas + (p->cascade ? p->shared.n_ctas : 0);
+    if (n_items) *n_items = p->main.n_items + (p->cascade ? p->shared.n_items : 0);
+    if (n_pages) *n_pages = p->main.n_pages + (p->cascade ? p->shared.n_pages : 0);
+    return EP_OK;
+}
+
+int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype,
+                         const void* q, int32_t o_dtype, void* o, float* lse, ep_stream stream) {
+    if (!h || !p || !pool || !q || !o) return fail(EP_EINVAL, "ep_spliced_attention: null argument");
+    if (pool->dtype != p->kv_dtype || pool->n_kv_heads != p->n_kv_heads ||
+        pool->d_head != p->d_head || pool->page_tokens != p->page_tokens ||
+        pool->num_pages < p->num_pages)
+        return fail(EP_EINVAL, "ep_spliced_attention: pool does not match the plan");
+    if (!valid_dt(q_dtype) || !valid_dt(o_dtype))
+        return fail(EP_EUNSUPPORTED, "ep_spliced_attention: q/o dtype must be f32 or bf16");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!p->cascade) {
+        DecodeArgs a = make_args(*p, p->main, pool, q_dtype, q, o_dtype, o, lse);
+        return launch_subplan(*p, p->main, pool, a, s);
+    }
+    // cascade: shared prefixes (K3 row-group tiles) -> part 0, private
+    // remainders (K1/K3) -> part 1, then the 2-way LSE merge into o / lse.
+    const size_t rows = size_t(p->batch) * p->n_q * p->n_q_heads;
+    float* po = static_cast<float*>(p->d_parts_o.ptr);
+    float* pl = static_cast<float*>(p->d_parts_lse.ptr);
+    DecodeArgs as = make_args(*p, p->shared, pool, q_dtype, q, EP_F32, po, pl);
+    if (int rc = launch_subplan(*p, p->shared, pool, as, s)) return rc;
+    DecodeArgs am = make_args(*p, p->main, pool, q_dtype, q, EP_F32, po + rows * p->d_head, pl + rows);
+    if (int rc = launch_subplan(*p, p->main, pool, am, s)) return rc;
+    EP_CUDA_TRY(launch_cascade_merge(int(rows), p->d_head, p->n_q * p->n_q_heads, po, pl,
+                                     static_cast<const uint8_t*>(p->d_has_shared.ptr), o, o_dtype, lse, s),
+                "cascade merge launch");
+    h->launches++;
+    return EP_OK;
+}
+
+}  // extern "C"
