@@ -33,6 +33,7 @@
 
 #include "ep_common.cuh"
 #include "ep_internal.h"
+#include "merge.cuh"
 
 namespace ep {
 namespace {
@@ -398,26 +399,10 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             named_bar_sync(1, NCW * 32);
             if (*s_flag) {
                 __threadfence();
-                const int b = w.b;
-                for (int idx = threadIdx.x; idx < R * D; idx += NCW * 32) {
-                    const int r = idx / D, c = idx % D;
-                    float M = -INFINITY;
-                    for (int i = u0; i < u0 + n_items; ++i) M = fmaxf(M, __ldcg(&a.lse_part[size_t(i) * R + r]));
-                    float Lsum = 0.f, acc = 0.f;
-                    if (M != -INFINITY) {
-                        for (int i = u0; i < u0 + n_items; ++i) {
-                            const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i) * R + r]) - M);
-                            Lsum += wt;
-                            acc += wt * __ldcg(&a.o_part[(size_t(i) * R + r) * D + c]);
-                        }
-                    }
-                    const bool empty_row = !(Lsum > 0.f);
+                merge_unit_rows<D>(a, u0, n_items, R, R, warp, NCW, [&](int r) {
                     const int qi = r / G, h = w.g * G + r % G;
-                    const size_t orow = (size_t(b) * a.n_q + qi) * a.n_q_heads + h;
-                    store_o(a.o, a.o_dtype, orow * D + c, empty_row ? 0.f : acc / Lsum);
-                    if (c == 0 && a.lse)
-                        a.lse[orow] = empty_row ? -INFINITY : (M + fast_log2(Lsum)) * kLn2;
-                }
+                    return (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
+                });
                 if (threadIdx.x == 0) a.unit_counter[unit] = 0;  // ready for the next launch
             }
         }

@@ -35,6 +35,7 @@
 
 #include "ep_common.cuh"
 #include "ep_internal.h"
+#include "merge.cuh"
 #include "umma.cuh"
 
 namespace ep {
@@ -500,29 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 named_bar_sync(5, kSoftThreads);
                 if (*s_flag) {
                     __threadfence();
-                    for (int idx = threadIdx.x; idx < nrows * kD; idx += kSoftThreads) {
-                        const int r = idx / kD, c = idx % kD;
-                        float Mx = -INFINITY;
-                        for (int i2 = u0; i2 < u0 + n_items; ++i2)
-                            Mx = fmaxf(Mx, __ldcg(&a.lse_part[size_t(i2) * rows + r]));
-                        float Ls = 0.f, acc = 0.f;
-                        if (Mx != -INFINITY) {
-                            for (int i2 = u0; i2 < u0 + n_items; ++i2) {
-                                const float wt = fast_exp2(__ldcg(&a.lse_part[size_t(i2) * rows + r]) - Mx);
-                                Ls += wt;
-                                acc += wt * __ldcg(&a.o_part[(size_t(i2) * rows + r) * kD + c]);
-                            }
-                        }
-                        const bool er = !(Ls > 0.f);
+                    merge_unit_rows<kD>(a, u0, n_items, rows, nrows, warp, kSoftWarps, [&](int r) {
                         const int rq2 = w.rq0 + r / rpr, qi2 = (r % rpr) / G, h2 = w.g * G + r % G;
-                        const size_t orow = (size_t(rq2) * a.n_q + qi2) * a.n_q_heads + h2;
-                        const float val = er ? 0.f : acc / Ls;
-                        if (a.o_dtype == EP_BF16)
-                            static_cast<__nv_bfloat16*>(a.o)[orow * kD + c] = __float2bfloat16_rn(val);
-                        else
-                            static_cast<float*>(a.o)[orow * kD + c] = val;
-                        if (c == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (Mx + fast_log2(Ls)) * kLn2;
-                    }
+                        return (size_t(rq2) * a.n_q + qi2) * a.n_q_heads + h2;
+                    });
                     if (threadIdx.x == 0) a.unit_counter[unit] = 0;
                 }
                 named_bar_sync(5, kSoftThreads);
