@@ -61,7 +61,10 @@ struct DecodeCfg {
     static constexpr int OFF_CM = OFF_CO + NCW * R * D * 4;
     static constexpr int OFF_CL = OFF_CM + NCW * R * 4;
     static constexpr int OFF_FLAG = OFF_CL + NCW * R * 4;
-    static constexpr int SMEM = OFF_FLAG + 16;
+    static constexpr int Q_BYTES = R * D * 4;               // one item's q rows (fp32 worst case)
+    static constexpr int OFF_Q = (OFF_FLAG + 16 + 127) / 128 * 128;  // [2] q slots (bulk-prefetched)
+    static constexpr int OFF_QBAR = OFF_Q + 2 * Q_BYTES;      // q_full[2], q_empty[2]
+    static constexpr int SMEM = OFF_QBAR + 4 * 8;
     static_assert((1 << LOGN) == NV && NV <= 16, "R*J must be a power of two <= 16");
     static_assert(E % 4 == 0, "vector width");
     static_assert(NCW * 32 <= 1024 - 32, "block size");
@@ -156,10 +159,18 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
     const int P = a.page_tokens, Hkv = a.n_kv_heads;
 
+    uint8_t* sq = smem + C::OFF_Q;
+    uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + C::OFF_QBAR);
+    uint64_t* q_empty = q_full + 2;
+    const int qsz = a.q_dtype == EP_BF16 ? 2 : 4;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], NCW);
         }
         fence_mbar_init();
     }
@@ -173,9 +184,22 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const uint8_t* kp = static_cast<const uint8_t*>(a.k_pages);
             const uint8_t* vp = static_cast<const uint8_t*>(a.v_pages);
             const uint8_t* zp = static_cast<const uint8_t*>(a.zero_rows);
+            const int G = a.n_q_heads / Hkv;
             for (int it = it0; it < it1; ++it) {
                 const WorkItem w = a.items[it];
                 const PageDesc* pd = a.pdesc + a.req_page_off[w.b];
+                {
+                    // the item's R query rows: n_q runs of G consecutive heads
+                    const int n = it - it0, slot = n & 1;
+                    const uint32_t run = uint32_t(G) * D * qsz;
+                    mbar_wait(&q_empty[slot], ((n >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&q_full[slot], run * a.n_q);
+                    for (int qi = 0; qi < a.n_q; ++qi)
+                        bulk_g2s(sq + slot * C::Q_BYTES + qi * run,
+                                 static_cast<const uint8_t*>(a.q) +
+                                     ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + size_t(w.g) * G) * D * qsz,
+                                 run, &q_full[slot]);
+                }
                 for (int lp = w.lp0; lp < w.lp1; ++lp) {
                     const PageDesc d = pd[lp];
                     const size_t tile = (size_t(d.page) * Hkv + w.g) * size_t(P);
@@ -221,16 +245,23 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
         // q rows of this kv-head, pre-scaled by log2(e)/sqrt(d): logical row r
         // is (query row r / G, head g*G + r % G). Physical slot rp holds
         // logical row rp ^ my_r (see the reduce-scatter below).
+        // (prefetched by the producer into q slot (it - it0) & 1; row r sits at r * D)
         float2 q2[R][E / 2];
+        {
+            const int n = it - it0, slot = n & 1;
+            mbar_wait(&q_full[slot], (n >> 1) & 1);
+            const uint8_t* qs = sq + slot * C::Q_BYTES;
 #pragma unroll
-        for (int rp = 0; rp < R; ++rp) {
-            const int r = rp ^ my_r;
-            const int qi = r / G, h = w.g * G + r % G;
-            const size_t base = ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + h) * D + l16 * E;
+            for (int rp = 0; rp < R; ++rp) {
+                const int r = rp ^ my_r;
+                const size_t base = size_t(r) * D + l16 * E;
 #pragma unroll
-            for (int e = 0; e < E / 2; ++e)
-                q2[rp][e] = make_float2(load_q(a.q, a.q_dtype, base + 2 * e) * a.q_scale,
-                                       load_q(a.q, a.q_dtype, base + 2 * e + 1) * a.q_scale);
+                for (int e = 0; e < E / 2; ++e)
+                    q2[rp][e] = make_float2(load_q(qs, a.q_dtype, base + 2 * e) * a.q_scale,
+                                           load_q(qs, a.q_dtype, base + 2 * e + 1) * a.q_scale);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&q_empty[slot]);
         }
         const int64_t my_qpos = q0 + my_r / G;
 
