@@ -379,8 +379,9 @@ def main():
 def run_extras(args, world, rank, h):
     """The other BASELINE configs, measured in the same run: config 3
     (speculative verify p50 latency, k = 4 / 8) and config 5 (multi-tenant
-    shared prefix) on rank 0 at N = 1; config 4 (128K split-KV, NCCL
-    all-gather + LSE merge) at every N."""
+    shared prefix) on rank 0 at N = 1; config 4 (128K split-KV: local K1 +
+    the peer-memory combine kernel; at N > 1 also NCCL all-gather + K5 merge
+    for comparison) at every N."""
     import gc
 
     import torch
@@ -405,9 +406,13 @@ def run_extras(args, world, rank, h):
         torch.cuda.empty_cache()
     skv = {}
     for b in (1, 32):
-        skv[f"batch{b}"] = splitkv_bench.run(b, steps, 3)
+        skv[f"batch{b}"] = splitkv_bench.run(b, steps, 3, combine="peer")
         gc.collect()
         torch.cuda.empty_cache()
+        if world > 1:
+            skv[f"batch{b}_nccl"] = splitkv_bench.run(b, steps, 3, combine="nccl")
+            gc.collect()
+            torch.cuda.empty_cache()
     extras["splitkv"] = skv
     return extras
 

@@ -203,6 +203,43 @@ int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int3
                  ep_stream stream);
 
 /* ==================================================================== */
+/* 3b. Cross-GPU split-KV combine over NVLink peer memory (config 4).   */
+/* ==================================================================== */
+
+/* The reference fuses any ordered partition of a row's keys with
+ * merge_partials (attention.cpp:116-156). When the partition is across the
+ * GPUs of one box, each rank's fp32 (o, lse) partial is pushed straight into
+ * every peer's receive buffer over NVLink (remote stores of {value, flag}
+ * words) and merged there in rank order by the same kernel — no NCCL on the
+ * data path, one launch, graph-capturable. Collective: every rank creates,
+ * connects, combines and destroys in the same order (barrier before
+ * destroy). The group owns one device allocation: receive words
+ * [2][world][rows_max][d/2 + 1] x 16 B + per-CTA epochs. d even, <= 256. */
+typedef struct ep_peer_group_s* ep_peer_group;
+#define EP_IPC_HANDLE_BYTES 64
+
+int ep_peer_group_create(ep_handle h, int32_t world, int32_t rank, int32_t rows_max, int32_t d,
+                         ep_peer_group* out);
+/* cudaIpcMemHandle_t of the group's allocation (EP_IPC_HANDLE_BYTES bytes) for
+ * a cross-process exchange (e.g. torch.distributed.all_gather_object). */
+int ep_peer_group_export(ep_peer_group g, void* ipc_handle);
+/* Device base pointer of the allocation, for ranks that share one process. */
+int ep_peer_group_base(ep_peer_group g, void** base);
+/* handles: world * EP_IPC_HANDLE_BYTES bytes in rank order (own entry ignored). */
+int ep_peer_group_connect_ipc(ep_peer_group g, const void* handles);
+/* bases: world device pointers in rank order (own entry ignored); enables peer
+ * access when the peer lives on another device of this process. */
+int ep_peer_group_connect_ptrs(ep_peer_group g, void* const* bases);
+/* o_part [rows][d] fp32 and lse_part [rows] (natural log) = this rank's
+ * ep_spliced_attention output over its KV shard -> out [rows][d] (out_dtype
+ * EP_F32/EP_BF16) and out_lse [rows] (may be NULL), identical on every rank.
+ * rows <= rows_max. */
+int ep_splitkv_combine_dev(ep_handle h, ep_peer_group g, int32_t rows, const float* o_part,
+                           const float* lse_part, int32_t out_dtype, void* out, float* out_lse,
+                           ep_stream stream);
+int ep_peer_group_destroy(ep_peer_group g);
+
+/* ==================================================================== */
 /* 4. Utilities                                                         */
 /* ==================================================================== */
 

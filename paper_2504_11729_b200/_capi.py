@@ -84,6 +84,14 @@ _SIGS = {
     "ep_merge_partials_dev": (C.c_int, [_vp, C.c_int, _sz, _vp, _vp, _sz, _sz, _vp, _vp, _vp]),
     "ep_merge_partials_packed_dev": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, C.c_int32,
                                                C.c_int32, _vp, _vp, _vp]),
+    "ep_peer_group_create": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(_vp)]),
+    "ep_peer_group_export": (C.c_int, [_vp, _vp]),
+    "ep_peer_group_base": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ep_peer_group_connect_ipc": (C.c_int, [_vp, _vp]),
+    "ep_peer_group_connect_ptrs": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "ep_splitkv_combine_dev": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp, _vp]),
+    "ep_peer_group_destroy": (C.c_int, [_vp]),
     "ep_plan_create": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, C.c_int32, C.c_int32, _vp,
                                  _vp, _vp, _vp, C.c_int32, C.POINTER(_vp)]),
     "ep_plan_update": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),

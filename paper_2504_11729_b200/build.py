@@ -28,7 +28,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", f"-I{INCLUDE}", f"-I{CSRC}"]
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
-SOURCES = ["kern_reference.cu", "kern_decode.cu", "kern_verify.cu", "kern_score.cu", "capi.cpp", "plan.cpp"]
+SOURCES = ["kern_reference.cu", "kern_decode.cu", "kern_verify.cu", "kern_score.cu", "kern_peer.cu",
+           "capi.cpp", "plan.cpp"]
 HEADERS = ["ep_common.cuh", "ep_internal.h", "umma.cuh", "merge.cuh"]
 
 

@@ -53,6 +53,91 @@ def shard_segments(segments, world: int, rank: int):
     return out
 
 
+class PeerSplitKVCombine:
+    """The combine as ONE kernel over NVLink peer memory
+    (ep_splitkv_combine_dev): every rank pushes its fp32 (o, lse) rows into
+    the peers' receive buffers and merges what it received in rank order — no
+    NCCL on the data path. The group's buffers are exchanged once:
+
+    * across processes (one per GPU): ``PeerSplitKVCombine(world, rank, rows,
+      d, handle)`` exchanges CUDA IPC handles with
+      torch.distributed.all_gather_object (``exchange`` is injectable);
+    * inside one process (tests: P emulated ranks on one GPU, or a thread per
+      GPU): ``PeerSplitKVCombine.local_group(world, rows, d, handles)``.
+    """
+
+    def __init__(self, world: int, rank: int, rows: int, d: int, handle, exchange=None,
+                 _connect=True):
+        self.world, self.rank, self.rows, self.d = world, rank, rows, d
+        self.handle = handle
+        self._lib = lib()
+        g = C.c_void_p()
+        check(self._lib.ep_peer_group_create(handle.ptr, world, rank, rows, d, C.byref(g)),
+              "ep_peer_group_create")
+        self._g = g
+        if _connect and world > 1:
+            buf = (C.c_ubyte * 64)()
+            check(self._lib.ep_peer_group_export(g, buf), "ep_peer_group_export")
+            mine = bytes(buf)
+            if exchange is None:
+                import torch.distributed as dist
+                handles = [None] * world
+                dist.all_gather_object(handles, mine)
+            else:
+                handles = exchange(mine)
+            assert len(handles) == world and all(len(x) == 64 for x in handles)
+            blob = b"".join(handles)
+            check(self._lib.ep_peer_group_connect_ipc(g, blob), "ep_peer_group_connect_ipc")
+            if exchange is None:
+                import torch.distributed as dist
+                dist.barrier()
+
+    @classmethod
+    def local_group(cls, world: int, rows: int, d: int, handles):
+        """world groups in this process (handles[r] = rank r's Handle; may share a device)."""
+        groups = [cls(world, r, rows, d, handles[r], _connect=False) for r in range(world)]
+        bases = (C.c_void_p * world)()
+        for r, g in enumerate(groups):
+            b = C.c_void_p()
+            check(g._lib.ep_peer_group_base(g._g, C.byref(b)), "ep_peer_group_base")
+            bases[r] = b
+        if world > 1:
+            for g in groups:
+                check(g._lib.ep_peer_group_connect_ptrs(g._g, bases), "ep_peer_group_connect_ptrs")
+        return groups
+
+    def __call__(self, o_part, lse_part, out=None, out_lse=None, stream=None):
+        """o_part [rows][d] fp32, lse_part [rows] fp32 (natural log) of this rank's
+        keys -> merged (out [rows][d] fp32/bf16, out_lse [rows])."""
+        import torch
+        assert o_part.dtype == torch.float32 and lse_part.dtype == torch.float32
+        assert o_part.is_contiguous() and lse_part.is_contiguous()
+        dev = o_part.device
+        if out is None:
+            out = torch.empty((self.rows, self.d), dtype=torch.float32, device=dev)
+        if out_lse is None:
+            out_lse = torch.empty((self.rows,), dtype=torch.float32, device=dev)
+        odt = {torch.float32: 0, torch.bfloat16: 1}[out.dtype]
+        s = torch.cuda.current_stream(dev).cuda_stream if stream is None else getattr(
+            stream, "cuda_stream", stream)
+        check(self._lib.ep_splitkv_combine_dev(self.handle.ptr, self._g, self.rows,
+                                               o_part.data_ptr(), lse_part.data_ptr(), odt,
+                                               out.data_ptr(), out_lse.data_ptr(), s),
+              "ep_splitkv_combine_dev")
+        return out, out_lse
+
+    def close(self):
+        if self._g is not None and self._g.value:
+            self._lib.ep_peer_group_destroy(self._g)
+        self._g = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class SplitKVCombine:
     """All-gather of every rank's fp32 (o, lse) + the K5 LSE merge.
 

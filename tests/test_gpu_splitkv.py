@@ -4,9 +4,11 @@
   their fp32 (o, lse) partials are packed exactly as the NCCL all-gather packs
   them and merged by the K5 kernel — compared with the unsharded spliced
   attention and with the fp64 oracle.
-* With >= 2 GPUs: tools/splitkv_bench.py --check under torchrun (NCCL
-  all-gather across real ranks, merged result checked against an unsharded
-  single-GPU run)."""
+* The peer-memory combine kernel with P ranks emulated in one process (own
+  stream each) against the K5 merge.
+* With >= 2 GPUs: tools/splitkv_bench.py --check under torchrun (peer-memory
+  combine over NVLink and NCCL all-gather + K5, each checked against an
+  unsharded single-GPU run)."""
 import os
 import subprocess
 import sys
@@ -55,6 +57,52 @@ def test_emulated_ranks_merge(cuda_handle, world):
     assert np.max(np.abs(ml.cpu().numpy() - want_l)) < 1e-5
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_combine_emulated_ranks(cuda_handle, world):
+    """ep_splitkv_combine_dev with `world` ranks in one process on one GPU
+    (each rank's kernel on its own stream, buffers connected by pointer):
+    every rank's result equals the K5 merge of the same partials (which the
+    test above pins to the oracle), over several steps so the epoch/ack
+    protocol and buffer reuse are exercised."""
+    import torch
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splitkv import PeerSplitKVCombine, SplitKVCombine
+    rows, D = 96, 128
+    handles = [Handle(torch.cuda.current_device()) for _ in range(world)]
+    groups = PeerSplitKVCombine.local_group(world, rows, D, handles)
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    for step in range(4):
+        o = torch.randn((world, rows, D), device="cuda", generator=gen)
+        lse = torch.randn((world, rows), device="cuda", generator=gen) * 3
+        if step == 1:
+            lse[0, :5] = float("-inf")  # a rank with no visible keys for some rows
+        if step == 2:
+            lse[:, 7] = float("-inf")   # a fully masked row
+        packed = torch.cat([torch.cat([o[p].reshape(-1), lse[p]]) for p in range(world)])
+        want_o, want_l = SplitKVCombine(world, rows, D, handle=cuda_handle, device="cuda",
+                                        gather=lambda out, inp: out.copy_(packed))(o[0], lse[0])
+        outs = []
+        torch.cuda.synchronize()
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                oo = torch.empty((rows, D), dtype=torch.bfloat16 if step == 3 else torch.float32,
+                                 device="cuda")
+                ol = torch.empty((rows,), device="cuda")
+                groups[r](o[r].contiguous(), lse[r].contiguous(), out=oo, out_lse=ol,
+                          stream=streams[r])
+                outs.append((oo, ol))
+        torch.cuda.synchronize()
+        for r, (oo, ol) in enumerate(outs):
+            tol = 1e-2 if step == 3 else 1e-5
+            assert torch.allclose(oo.float(), want_o, atol=tol, rtol=tol), (step, r)
+            fin = torch.isfinite(want_l)
+            assert torch.equal(fin, torch.isfinite(ol)), (step, r)
+            assert torch.allclose(ol[fin], want_l[fin], atol=1e-5), (step, r)
+    for g in groups:
+        g.close()
+
+
 def test_torchrun_nccl_two_ranks():
     import torch
     if torch.cuda.device_count() < 2:
@@ -62,7 +110,7 @@ def test_torchrun_nccl_two_ranks():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533",
            os.path.join(ROOT, "tools", "splitkv_bench.py"), "--batch", "2", "--steps", "3",
-           "--check"]
+           "--check", "--combine", "peer", "nccl"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
-    assert '"check_ok": true' in r.stdout, r.stdout
+    assert r.stdout.count('"check_ok": true') == 2, r.stdout

@@ -1,13 +1,13 @@
 """BASELINE config 4: long-context split-KV. A 131072-token cloud prompt per
 request is sharded contiguously across the P GPUs of one box (edge 512 on the
 last rank); every rank runs the spliced decode kernel over its shard (fp32
-o + lse), then one NCCL all-gather of the packed partials and the K5 LSE merge
-in rank order.
+o + lse), then the combine in rank order — either ONE peer-memory combine kernel over NVLink
+(ep_splitkv_combine_dev, default) or NCCL all-gather + the K5 merge.
 
     torchrun --nproc-per-node P tools/splitkv_bench.py [--batch 32] [--check]
 
 Times (CUDA events, max over ranks): the local attention, and the whole step
-(local attention + all-gather + merge). --check compares rank 0's merged
+(local attention + combine). --check compares rank 0's merged
 output with an unsharded single-GPU run of the same batch.
 """
 from __future__ import annotations
@@ -69,27 +69,33 @@ def build_local(batch, world, rank, h, cloud=CLOUD, edge=EDGE, seed=41):
     return pool, table, attn, q, n_loc
 
 
-def run(batch, steps, warmup, check=False):
+def run(batch, steps, warmup, check=False, combine="peer", graph=False):
+    """combine: "peer" = one ep_splitkv_combine_dev kernel over NVLink peer
+    memory; "nccl" = NCCL all-gather + K5 merge. graph: replay the step
+    (attention + combine) as one CUDA graph (removes host launch overhead)."""
     import torch
     import torch.distributed as dist
     from paper_2504_11729_b200.attention import Handle
-    from paper_2504_11729_b200.splitkv import SplitKVCombine
+    from paper_2504_11729_b200.splitkv import PeerSplitKVCombine, SplitKVCombine
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     h = Handle(torch.cuda.current_device())
     pool, table, attn, q, n_loc = build_local(batch, world, rank, h)
     rows = batch * HQ
-    comb = SplitKVCombine(world, rows, D, handle=h, device="cuda") if world > 1 else None
+    comb = None
+    if world > 1:
+        comb = (PeerSplitKVCombine(world, rank, rows, D, h) if combine == "peer" else
+                SplitKVCombine(world, rows, D, handle=h, device="cuda"))
     o_part = torch.empty((batch, 1, HQ, D), dtype=torch.float32, device="cuda")
     lse_part = torch.empty((batch, 1, HQ), dtype=torch.float32, device="cuda")
     out = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
     out_lse = torch.empty((rows,), dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
-    def step():
-        attn(q, o=o_part, lse=lse_part, stream=stream)
+    def step(st=stream):
+        attn(q, o=o_part, lse=lse_part, stream=st)
         if comb is not None:
-            comb(o_part, lse_part, out=out, out_lse=out_lse, stream=stream)
+            comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=st)
 
     for _ in range(warmup):
         step()
@@ -104,9 +110,26 @@ def run(batch, steps, warmup, check=False):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    run_step = step
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step(side)  # warm the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g):
+            step(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        run_step = g.replay
+    import time
     e[2].record(stream)
+    h0 = time.perf_counter()
     for _ in range(steps):
-        step()
+        run_step()
+    host_us = (time.perf_counter() - h0) / steps * 1e6
     e[3].record(stream)
     torch.cuda.synchronize()
     t_attn = e[0].elapsed_time(e[1]) / steps
@@ -115,17 +138,39 @@ def run(batch, steps, warmup, check=False):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_attn, t_step = float(t[0]), float(t[1])
+    per_rank = None
+    if world > 1:
+        # where the step goes on each rank: attention vs combine (incl. waiting for peers)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev[0].record(stream)
+        for i in range(steps):
+            attn(q, o=o_part, lse=lse_part, stream=stream)
+            ev[2 * i + 1].record(stream)
+            comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=stream)
+            ev[2 * i + 2].record(stream)
+        torch.cuda.synchronize()
+        a_ms = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(steps)) / steps
+        c_ms = sum(ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(steps)) / steps
+        mine = torch.tensor([a_ms, c_ms], device="cuda")
+        allr = torch.empty((world, 2), device="cuda")
+        dist.all_gather_into_tensor(allr, mine)
+        per_rank = [[round(float(x), 4) for x in r] for r in allr.cpu()]
     loc_bytes = batch * n_loc * 2 * HKV * D * 2
     gather_bytes = (world - 1) * rows * (D + 1) * 4  # received per rank
     res = {
         "workload": f"cfg4 split-KV: {CLOUD} cloud + {EDGE} edge keys, Hq=32 Hkv=8 d=128 bf16, "
                     f"batch {batch}, {world} GPU(s)",
-        "batch": batch, "gpus": world, "step_ms": t_step, "local_attention_ms": t_attn,
+        "batch": batch, "gpus": world, "combine": combine if world > 1 else None, "step_ms": t_step, "local_attention_ms": t_attn,
         "combine_ms": t_step - t_attn if world > 1 else 0.0,
         "tokens_per_s": batch / (t_step / 1e3),
         "local_hbm_gbs": loc_bytes / (t_attn / 1e3) / 1e9,
         "allgather_bytes_per_rank": gather_bytes,
+        "graph": graph, "host_launch_us_per_step": host_us,
     }
+    if per_rank is not None:
+        res["per_rank_attention_combine_ms"] = per_rank
     if check:
         ok = True
         if world > 1:
@@ -140,6 +185,11 @@ def run(batch, steps, warmup, check=False):
                 res["check_lse_max_abs_err"] = lerr
                 ok = err < 2e-2 and lerr < 1e-3
         res["check_ok"] = ok
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()  # no peer still writes into our buffers
+        if hasattr(comb, "close"):
+            comb.close()
     return res
 
 
@@ -149,6 +199,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--combine", choices=["peer", "nccl"], nargs="+", default=["peer"])
+    ap.add_argument("--graph", action="store_true")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -158,10 +210,11 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    for b in args.batch:
-        r = run(b, args.steps, args.warmup, check=args.check)
-        if int(os.environ.get("RANK", "0")) == 0:
-            print(json.dumps(r), flush=True)
+    for cmb in args.combine:
+        for b in args.batch:
+            r = run(b, args.steps, args.warmup, check=args.check, combine=cmb, graph=args.graph)
+            if int(os.environ.get("RANK", "0")) == 0:
+                print(json.dumps(r), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
