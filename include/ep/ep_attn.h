@@ -151,6 +151,18 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
  * reused when large enough, so captured CUDA graphs stay valid. */
 int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
                    const int32_t* page_table, const int64_t* q_pos, ep_stream stream);
+/* Prefill plan — the cloud-prompt / edge prefill attention tiles (prefill,
+ * model.cpp:211-236 -> transformer_layer's attention block, model.cpp:161-182;
+ * CloudServer::serve_stream, cloud.cpp:160-172). The LAST n_new[b] tokens of
+ * request b's spliced sequence are queries; query t attends to every key at a
+ * position <= its own (CausalSpan rule, attention.cpp:29-33). Their K/V must
+ * already be in the pool as part of the segments. q / o are token-major
+ * [sum n_new][n_q_heads][d_head], lse [sum n_new][n_q_heads]; run with
+ * ep_spliced_attention. tcgen05 tiles of 128/G query tokens x G heads: bf16
+ * KV, d_head 128. o_dtype EP_BF16 uses a bf16 P operand, EP_F32 a hi+lo split. */
+int ep_plan_create_prefill(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t batch,
+                           const int64_t* seg_indptr, const ep_segment* segs,
+                           const int32_t* page_table, const int32_t* n_new, ep_plan* out);
 int ep_plan_destroy(ep_plan p);
 /* Introspection: number of CTAs, work items and pages in the plan. */
 int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages);

@@ -106,7 +106,15 @@ struct DecodeArgs {
     int32_t* unit_counter;    // [batch*Hkv], zero between launches (fused K2)
     unsigned long long* trace;  // optional clock64 event trace of CTA 0 (debug, may be null)
     int32_t reqs_per_unit;    // K3: consecutive requests whose rows share one tile (cascade), else 1
+    const int32_t* q_row0;    // per (virtual) request: first q/o token row; null = b * n_q
+    int32_t pv_parts;         // K3: P as bf16 hi+lo (2) or bf16 (1)
 };
+
+// First q/o token row of (virtual) request b: prefill plans cut one request's
+// queries into chunks that are separate virtual requests.
+__host__ __device__ inline size_t q_row_base(const DecodeArgs& a, int b) {
+    return a.q_row0 ? size_t(a.q_row0[b]) : size_t(b) * a.n_q;
+}
 
 // TMA tensor maps over bf16 row-major matrices (capi.cpp).
 int encode_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,

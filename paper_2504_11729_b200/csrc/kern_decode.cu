@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                     for (int qi = 0; qi < a.n_q; ++qi)
                         bulk_g2s(sq + slot * C::Q_BYTES + qi * run,
                                  static_cast<const uint8_t*>(a.q) +
-                                     ((size_t(w.b) * a.n_q + qi) * a.n_q_heads + size_t(w.g) * G) * D * qsz,
+                                     ((q_row_base(a, w.b) + qi) * a.n_q_heads + size_t(w.g) * G) * D * qsz,
                                  run, &q_full[slot]);
                 }
                 for (int lp = w.lp0; lp < w.lp1; ++lp) {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const float lse2 = empty_row ? -INFINITY : M + fast_log2(Lsum);
             if (direct) {
                 const int qi = r / G, h = w.g * G + r % G;
-                const size_t orow = (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
+                const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
                 store_o(a.o, a.o_dtype, orow * D + c, val);
                 if (c == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
             } else {
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                 __threadfence();
                 merge_unit_rows<D>(a, u0, n_items, R, R, warp, NCW, [&](int r) {
                     const int qi = r / G, h = w.g * G + r % G;
-                    return (size_t(w.b) * a.n_q + qi) * a.n_q_heads + h;
+                    return (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
                 });
                 if (threadIdx.x == 0) a.unit_counter[unit] = 0;  // ready for the next launch
             }
@@ -443,8 +443,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
 
 // Units with no pages at all (empty requests) are identity rows: o = 0,
 // lse = -inf (attention.cpp:37-43). Launched only when the plan has any.
-template <int D, int R>
-__global__ void empty_units_kernel(const DecodeArgs a) {
+__global__ void empty_units_kernel(const DecodeArgs a, int D, int R) {
     const int unit = blockIdx.x;
     if (a.unit_item_ptr[unit + 1] != a.unit_item_ptr[unit]) return;
     const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv;
@@ -452,7 +451,7 @@ __global__ void empty_units_kernel(const DecodeArgs a) {
     for (int idx = threadIdx.x; idx < R * D; idx += blockDim.x) {
         const int r = idx / D, c = idx % D;
         const int qi = r / G, h = g * G + r % G;
-        const size_t orow = (size_t(b) * a.n_q + qi) * a.n_q_heads + h;
+        const size_t orow = (q_row_base(a, b) + qi) * a.n_q_heads + h;
         store_o(a.o, a.o_dtype, orow * D + c, 0.f);
         if (c == 0 && a.lse) a.lse[orow] = -INFINITY;
     }
@@ -525,12 +524,9 @@ cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas
 cudaError_t launch_empty_units(int d_head, int rows, const DecodeArgs& a, cudaStream_t s) {
     const int units = a.batch * a.n_kv_heads;
     if (units == 0) return cudaSuccess;
-#define EP_EMPTY_CASE(DD, RR) \
-    if (d_head == DD && rows == RR) { empty_units_kernel<DD, RR><<<units, 128, 0, s>>>(a); return cudaGetLastError(); }
-    EP_EMPTY_CASE(64, 1) EP_EMPTY_CASE(64, 2) EP_EMPTY_CASE(64, 4) EP_EMPTY_CASE(64, 8)
-    EP_EMPTY_CASE(128, 1) EP_EMPTY_CASE(128, 2) EP_EMPTY_CASE(128, 4) EP_EMPTY_CASE(128, 8)
-#undef EP_EMPTY_CASE
-    return cudaErrorInvalidValue;
+    // rows = G * n_q rows of one (request, kv-head) unit
+    empty_units_kernel<<<units, 128, 0, s>>>(a, d_head, rows);
+    return cudaGetLastError();
 }
 
 }  // namespace ep

@@ -10,6 +10,7 @@
 //
 //   QK^T : S[128 x 64]  (TMEM, fp32) = Q[128 x 128] (smem) . K[64 keys x 128]^T
 //   PV   : O[128 x 128] (TMEM, fp32) += (P_hi + P_lo)[128 x 64] (TMEM, 2 x bf16) . V[64 x 128]
+//          (P_hi alone when the caller asked for bf16 output: prefill tiles)
 //
 // tcgen05.mma M=128 (rows >= R are padding; the M=128 issue rate equals
 // M=64's), operands staged by TMA with 128B swizzle straight from the paged
@@ -142,7 +143,7 @@ struct BlockWalker {
 // core always has the other group's QK or PV to run.
 __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
-                            const __grid_constant__ CUtensorMap tmap_v, int rows, int pv_parts) {
+                            const __grid_constant__ CUtensorMap tmap_v, int rows) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1 KB alignment
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // the probabilities at ~2^-17 relative instead of bf16's 2^-9.
                 if (umma::elect_one()) {
                     umma::mma_chain_pv4(td, ta0, bd0, kIdescPV, i < 2 ? 1u : 0u);
-                    if (pv_parts > 1) umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
+                    if (a.pv_parts > 1) umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
                 }
                 if (umma::elect_one()) {
                     umma::mma_commit(&B.pv_done[grp]);
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tS = tmem + kColS + grp * kBT + lane_off;
         const uint32_t tOg = tmem + kColO + grp * kD + lane_off;
         const float scale = a.q_scale;  // log2(e)/sqrt(d)
+        const bool two_part = a.pv_parts > 1;
         const uint32_t pair_bar = 1 + quarter;  // named barrier of warps q and q+4
         uint32_t cnt = 0, n = 0;  // blocks processed by this group (all items)
         uint32_t gi0 = 0;         // global index of the item's first block
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ---- Q tile -> TMEM (A operand of QK): group g writes d-half g ----
             {
                 const uint8_t* src = static_cast<const uint8_t*>(a.q) +
-                                     (((size_t(rq) * a.n_q + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
+                                     (((q_row_base(a, rq) + qi) * a.n_q_heads + h) * kD + grp * 64) * 2;
                 uint32_t qv[32];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -372,16 +374,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float mu = m_used == -INFINITY ? 0.f : m_used;
                 float2 rs2 = make_float2(0.f, 0.f);
                 uint32_t pk[32], pl[32];
+                if (two_part) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
-                    const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
-                    const float2 p2 = make_float2(p0, p1);
-                    rs2 = __fadd2_rn(rs2, p2);
-                    pk[j] = pack_bf16(p0, p1);
-                    const float2 hi = bf16x2_to_float2(pk[j]);
-                    const float2 lo = __fadd2_rn(p2, make_float2(-hi.x, -hi.y));
-                    pl[j] = pack_bf16(lo.x, lo.y);
+                    for (int j = 0; j < 32; ++j) {
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
+                        const float2 p2 = make_float2(p0, p1);
+                        rs2 = __fadd2_rn(rs2, p2);
+                        pk[j] = pack_bf16(p0, p1);
+                        const float2 hi = bf16x2_to_float2(pk[j]);
+                        const float2 lo = __fadd2_rn(p2, make_float2(-hi.x, -hi.y));
+                        pl[j] = pack_bf16(lo.x, lo.y);
+                    }
+                } else {
+                    // single bf16 P (bf16 output): the row sum keeps the fp32
+                    // probabilities, so the lse stays fp32-accurate; RN rounding
+                    // of P is unbiased, so the output scale error averages out
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
+                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
+                        pk[j] = pack_bf16(p0, p1);
+                        rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
+                    }
                 }
                 l = l * corr + (rs2.x + rs2.y);
 
@@ -403,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // P row -> TMEM over this group's S columns (A operand of the PV
                 // MMAs): hi tile then lo tile.
                 umma::tmem_st32(tS, pk);
-                umma::tmem_st32(tS + 32, pl);
+                if (two_part) umma::tmem_st32(tS + 32, pl);
                 umma::tmem_wait_st();
                 if (nv < kBT) {
                     // Tail rows of V in the stage are stale page slots: zero them
@@ -470,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
             if (valid_row) {
                 if (n_items == 1) {
-                    const size_t orow = (size_t(rq) * a.n_q + qi) * a.n_q_heads + h;
+                    const size_t orow = (q_row_base(a, rq) + qi) * a.n_q_heads + h;
                     if (a.o_dtype == EP_BF16) {
                         uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.o) + orow * kD + grp * 64);
 #pragma unroll
@@ -503,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __threadfence();
                     merge_unit_rows<kD>(a, u0, n_items, rows, nrows, warp, kSoftWarps, [&](int r) {
                         const int rq2 = w.rq0 + r / rpr, qi2 = (r % rpr) / G, h2 = w.g * G + r % G;
-                        return (size_t(rq2) * a.n_q + qi2) * a.n_q_heads + h2;
+                        return (q_row_base(a, rq2) + qi2) * a.n_q_heads + h2;
                     });
                     if (threadIdx.x == 0) a.unit_counter[unit] = 0;
                 }
@@ -535,12 +550,7 @@ cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUten
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    // EP_PV_PARTS=1 drops the P_lo pass (bf16 P, timing experiments only).
-    static const int pv_parts = [] {
-        const char* e = getenv("EP_PV_PARTS");
-        return (e && e[0] == '1') ? 1 : 2;
-    }();
-    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows, pv_parts);
+    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows);
     return cudaGetLastError();
 }
 

@@ -134,11 +134,13 @@ struct ep_plan_s {
     int64_t num_pages = 0;
     int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
     bool cascade = false;
+    bool prefill = false;             // prefill plan: virtual requests = query chunks
+    std::vector<int32_t> q_row0;      // prefill: first q/o token row per virtual request
     SubPlan main;    // whole table (non-cascade) or the private remainders (cascade)
     SubPlan shared;  // cascade: shared prefixes, row-group tiles on K3
     std::vector<int64_t> q_pos;
     std::vector<uint8_t> has_shared;  // per request (cascade)
-    DeviceBuffer d_qpos, d_has_shared, d_parts_o, d_parts_lse;
+    DeviceBuffer d_qpos, d_has_shared, d_parts_o, d_parts_lse, d_qrow0;
     // staging for stream-ordered updates
     void* h_stage = nullptr;
     size_t h_stage_bytes = 0;
@@ -164,9 +166,47 @@ bool cascade_allowed(const ep_plan_s& p) {
     return !off && verify_supported(p.kv_dtype, p.d_head, rpr) && rpr <= 128 && 128 / rpr >= 2;
 }
 
+// Validates request b's segments with the SegmentedCache invariants
+// (cache.cpp:25-53: gapless positions, origin order, pages in the pool) and
+// appends its page descriptors; *first_pages = pages of its first segment.
+int collect_pages(const ep_plan_s& p, int b, const int64_t* seg_indptr, const ep_segment* segs,
+                  const int32_t* page_table, std::vector<PageDesc>& out, int64_t* first_pages) {
+    const int P = p.page_tokens;
+    if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
+    int64_t expect_pos = -1;
+    int last_origin = -1;
+    *first_pages = 0;
+    for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
+        const ep_segment& s = segs[si];
+        if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
+            return fail(EP_EINVAL, "ep_plan: negative segment field");
+        if (expect_pos >= 0 && s.pos_offset != expect_pos)
+            return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
+                                       std::to_string(s.pos_offset) + ", previous ends at " +
+                                       std::to_string(expect_pos));
+        if (s.origin < last_origin)
+            return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
+        expect_pos = s.pos_offset + s.len;
+        last_origin = s.origin;
+        const int64_t npg = (int64_t(s.len) + P - 1) / P;
+        for (int64_t i = 0; i < npg; ++i) {
+            const int32_t page = page_table[s.page_off + i];
+            if (page < 0 || page >= p.num_pages)
+                return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
+            PageDesc d;
+            d.page = page;
+            d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
+            d.pos = s.pos_offset + i * P;
+            out.push_back(d);
+        }
+        if (si == seg_indptr[b]) *first_pages = int64_t(out.size());
+    }
+    return EP_OK;
+}
+
 int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
                     const int32_t* page_table, const int64_t* q_pos) {
-    const int B = p.batch, Hkv = p.n_kv_heads, P = p.page_tokens;
+    const int B = p.batch, Hkv = p.n_kv_heads;
     const int rpr = (p.n_q_heads / Hkv) * p.n_q;
     p.q_pos.assign(q_pos, q_pos + B);
     if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
@@ -174,36 +214,9 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
     std::vector<std::vector<PageDesc>> req_pages(B);
     std::vector<int64_t> first_seg_pages(B, 0);
     for (int b = 0; b < B; ++b) {
-        if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
         if (q_pos[b] < 0 || q_pos[b] > INT32_MAX) return fail(EP_EINVAL, "ep_plan: query position out of range");
-        int64_t expect_pos = -1;
-        int last_origin = -1;
-        for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
-            const ep_segment& s = segs[si];
-            if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
-                return fail(EP_EINVAL, "ep_plan: negative segment field");
-            // SegmentedCache invariants (cache.cpp:25-53): gapless, origin order.
-            if (expect_pos >= 0 && s.pos_offset != expect_pos)
-                return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
-                                           std::to_string(s.pos_offset) + ", previous ends at " +
-                                           std::to_string(expect_pos));
-            if (s.origin < last_origin)
-                return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
-            expect_pos = s.pos_offset + s.len;
-            last_origin = s.origin;
-            const int64_t npg = (int64_t(s.len) + P - 1) / P;
-            for (int64_t i = 0; i < npg; ++i) {
-                const int32_t page = page_table[s.page_off + i];
-                if (page < 0 || page >= p.num_pages)
-                    return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
-                PageDesc d;
-                d.page = page;
-                d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
-                d.pos = s.pos_offset + i * P;
-                req_pages[b].push_back(d);
-            }
-            if (si == seg_indptr[b]) first_seg_pages[b] = int64_t(req_pages[b].size());
-        }
+        if (int rc = collect_pages(p, b, seg_indptr, segs, page_table, req_pages[b], &first_seg_pages[b]))
+            return rc;
     }
     const int64_t cap = int64_t(p.h->n_sms);
 
@@ -264,6 +277,61 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
     return EP_OK;
 }
 
+// Prefill plan (cloud-prompt / edge prefill, model.cpp:211-236 ->
+// transformer_layer's attention block): the last n_new[b] tokens of request b
+// are queries; query t attends to every key at a position <= its own
+// (attention.cpp:29-33). The queries are cut into chunks of C = 128 / G
+// tokens, so one chunk x G heads fills the M = 128 rows of a K3 tile; each
+// chunk is a virtual request whose page list stops at its last query (the
+// diagonal blocks are masked per row inside K3).
+int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const ep_segment* segs,
+                       const int32_t* page_table, const int32_t* n_new) {
+    const int Hkv = p.n_kv_heads, G = p.n_q_heads / Hkv;
+    const int C = p.n_q;  // query tokens per chunk
+    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
+    std::vector<VReq> vr;
+    p.q_pos.clear();
+    p.q_row0.clear();
+    int64_t tok_base = 0;
+    for (int b = 0; b < n_req; ++b) {
+        std::vector<PageDesc> pages;
+        int64_t first = 0;
+        if (int rc = collect_pages(p, b, seg_indptr, segs, page_table, pages, &first)) return rc;
+        const int64_t end = pages.empty() ? 0 : pages.back().pos + pages.back().n_tok;
+        const int64_t start = pages.empty() ? 0 : pages.front().pos;
+        if (n_new[b] < 0 || n_new[b] > end - start)
+            return fail(EP_EINVAL, "ep_plan_create_prefill: request " + std::to_string(b) + " has " +
+                                       std::to_string(end - start) + " tokens, n_new = " +
+                                       std::to_string(n_new[b]));
+        if (end > INT32_MAX) return fail(EP_EINVAL, "ep_plan_create_prefill: position out of range");
+        for (int64_t q0 = end - n_new[b]; q0 < end; q0 += C) {
+            const int64_t nq = std::min<int64_t>(C, end - q0), vis = q0 + nq;  // keys < vis
+            VReq v;
+            for (const PageDesc& d : pages) {
+                if (d.pos >= vis) break;
+                PageDesc t = d;
+                t.n_tok = int32_t(std::min<int64_t>(d.n_tok, vis - d.pos));
+                v.pages.push_back(t);
+            }
+            v.rq0 = int32_t(vr.size());
+            v.q0min = q0;
+            v.n_rows = int32_t(nq) * G;
+            p.q_pos.push_back(q0);
+            p.q_row0.push_back(int32_t(tok_base + (q0 - (end - n_new[b]))));
+            vr.push_back(std::move(v));
+        }
+        tok_base += n_new[b];
+        if (tok_base > INT32_MAX) return fail(EP_EINVAL, "ep_plan_create_prefill: too many query tokens");
+    }
+    p.batch = int32_t(vr.size());
+    p.cascade = false;
+    p.has_shared.assign(vr.size(), 0);
+    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms));
+    p.main.rows = G * C;
+    p.main.tc = true;
+    return EP_OK;
+}
+
 int upload_subplan(SubPlan& sp, int d_head, std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>>& parts) {
     parts.push_back({&sp.d_pdesc, {sp.pdesc.data(), bytes_of(sp.pdesc)}});
     parts.push_back({&sp.d_req_off, {sp.req_page_off.data(), bytes_of(sp.req_page_off)}});
@@ -286,6 +354,7 @@ int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
     std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>> parts;
     parts.push_back({&p.d_qpos, {p.q_pos.data(), bytes_of(p.q_pos)}});
     parts.push_back({&p.d_has_shared, {p.has_shared.data(), bytes_of(p.has_shared)}});
+    if (p.prefill) parts.push_back({&p.d_qrow0, {p.q_row0.data(), bytes_of(p.q_row0)}});
     if (int rc = upload_subplan(p.main, p.d_head, parts)) return rc;
     if (p.cascade) {
         if (int rc = upload_subplan(p.shared, p.d_head, parts)) return rc;
@@ -327,8 +396,10 @@ int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
 
 bool valid_dt(int dt) { return dt == EP_F32 || dt == EP_BF16; }
 
+// final_dtype: the dtype the caller asked for (fp32 output keeps P as bf16
+// hi+lo in K3; bf16 output uses a single bf16 P).
 DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* pool, int32_t q_dtype,
-                     const void* q, int32_t o_dtype, void* o, float* lse) {
+                     const void* q, int32_t o_dtype, void* o, float* lse, int32_t final_dtype) {
     DecodeArgs a{};
     a.k_pages = pool->k_pages;
     a.v_pages = pool->v_pages;
@@ -355,6 +426,8 @@ DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* po
     a.unit_counter = static_cast<int32_t*>(sp.d_counter.ptr);
     a.trace = nullptr;
     a.reqs_per_unit = 1;
+    a.q_row0 = p.prefill ? static_cast<const int32_t*>(p.d_qrow0.ptr) : nullptr;
+    a.pv_parts = final_dtype == EP_F32 ? 2 : 1;
     return a;
 }
 
@@ -450,9 +523,44 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
     return EP_OK;
 }
 
+int ep_plan_create_prefill(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t batch,
+                           const int64_t* seg_indptr, const ep_segment* segs, const int32_t* page_table,
+                           const int32_t* n_new, ep_plan* out) {
+    if (!h || !pool || !out || !seg_indptr || !n_new) return fail(EP_EINVAL, "ep_plan_create_prefill: null argument");
+    *out = nullptr;
+    if (pool->n_kv_heads <= 0 || n_q_heads <= 0 || n_q_heads % pool->n_kv_heads)
+        return fail(EP_EINVAL, "ep_plan_create_prefill: n_q_heads must be a multiple of n_kv_heads");
+    if (pool->page_tokens <= 0 || pool->page_tokens % kBlockTokens)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create_prefill: page_tokens must be a multiple of 64");
+    if (batch < 0) return fail(EP_EINVAL, "ep_plan_create_prefill: batch");
+    const int G = n_q_heads / pool->n_kv_heads;
+    const int C = 128 / G;
+    if (C < 1 || !verify_supported(pool->dtype, pool->d_head, G * C))
+        return fail(EP_EUNSUPPORTED, "ep_plan_create_prefill: tcgen05 prefill tiles need bf16 KV, d_head 128, "
+                                     "group <= 128");
+    std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
+    if (!p) return fail(EP_ENOMEM, "ep_plan_create_prefill");
+    p->h = h;
+    p->kv_dtype = pool->dtype;
+    p->n_kv_heads = pool->n_kv_heads;
+    p->d_head = pool->d_head;
+    p->page_tokens = pool->page_tokens;
+    p->num_pages = pool->num_pages;
+    p->n_q_heads = n_q_heads;
+    p->n_q = C;
+    p->rows = G * C;
+    p->prefill = true;
+    if (int rc = build_prefill_host(*p, batch, seg_indptr, segs, page_table, n_new)) return rc;
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create_prefill");
+    if (int rc = upload_plan(*p, nullptr, false)) return rc;
+    *out = p.release();
+    return EP_OK;
+}
+
 int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
                    const int32_t* page_table, const int64_t* q_pos, ep_stream stream) {
     if (!p) return fail(EP_EINVAL, "ep_plan_update: null plan");
+    if (p->prefill) return fail(EP_EINVAL, "ep_plan_update: prefill plans are rebuilt with ep_plan_create_prefill");
     if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
     return upload_plan(*p, static_cast<cudaStream_t>(stream), true);
 }
@@ -481,7 +589,7 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
         return fail(EP_EUNSUPPORTED, "ep_spliced_attention: q/o dtype must be f32 or bf16");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (!p->cascade) {
-        DecodeArgs a = make_args(*p, p->main, pool, q_dtype, q, o_dtype, o, lse);
+        DecodeArgs a = make_args(*p, p->main, pool, q_dtype, q, o_dtype, o, lse, o_dtype);
         return launch_subplan(*p, p->main, pool, a, s);
     }
     // cascade: shared prefixes (K3 row-group tiles) -> part 0, private
@@ -489,9 +597,9 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
     const size_t rows = size_t(p->batch) * p->n_q * p->n_q_heads;
     float* po = static_cast<float*>(p->d_parts_o.ptr);
     float* pl = static_cast<float*>(p->d_parts_lse.ptr);
-    DecodeArgs as = make_args(*p, p->shared, pool, q_dtype, q, EP_F32, po, pl);
+    DecodeArgs as = make_args(*p, p->shared, pool, q_dtype, q, EP_F32, po, pl, o_dtype);
     if (int rc = launch_subplan(*p, p->shared, pool, as, s)) return rc;
-    DecodeArgs am = make_args(*p, p->main, pool, q_dtype, q, EP_F32, po + rows * p->d_head, pl + rows);
+    DecodeArgs am = make_args(*p, p->main, pool, q_dtype, q, EP_F32, po + rows * p->d_head, pl + rows, o_dtype);
     if (int rc = launch_subplan(*p, p->main, pool, am, s)) return rc;
     EP_CUDA_TRY(launch_cascade_merge(int(rows), p->d_head, p->n_q * p->n_q_heads, po, pl,
                                      static_cast<const uint8_t*>(p->d_has_shared.ptr), o, o_dtype, lse, s),

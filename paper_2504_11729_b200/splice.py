@@ -284,6 +284,65 @@ class SplicedAttention:
             pass
 
 
+class SplicedPrefill:
+    """Prefill attention over (pool, table) on the tensor cores
+    (ep_plan_create_prefill): the last n_new[b] tokens of request b attend
+    causally to everything up to themselves — the cloud-prompt prefill
+    (n_new = whole prompt) and the edge prefill against a cloud segment
+    (edge.cpp:148-164) alike. The new tokens' K/V must already be written into
+    the table's pages. q / o: [sum n_new][n_q_heads][d] token-major."""
+
+    def __init__(self, pool: KVPool, table: SpliceTable, n_q_heads: int, n_new,
+                 handle: Handle | None = None):
+        self.pool, self.table, self.n_q_heads = pool, table, n_q_heads
+        self.handle = handle or default_handle(pool.k.device.index or 0)
+        self.n_new = np.ascontiguousarray(np.asarray(n_new, dtype=np.int32).reshape(table.batch))
+        self.n_tokens = int(self.n_new.sum())
+        indptr, segs, pt = table.arrays()
+        self._keep = (indptr, segs, pt, self.n_new)
+        plan = C.c_void_p()
+        pd = pool.desc()
+        check(lib().ep_plan_create_prefill(self.handle.ptr, C.byref(pd), n_q_heads, table.batch,
+                                           indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
+                                           self.n_new.ctypes.data, C.byref(plan)),
+              "ep_plan_create_prefill")
+        self.plan = plan
+
+    def __call__(self, q, o=None, lse=None, o_dtype=None, stream=None):
+        """q [sum n_new][Hq][d] (bf16/fp32 CUDA tensor) -> (o, lse)."""
+        torch = _torch()
+        d = self.pool.d_head
+        if tuple(q.shape) != (self.n_tokens, self.n_q_heads, d) or not q.is_contiguous():
+            raise InvalidArgument(f"SplicedPrefill: q must be contiguous "
+                                  f"[{self.n_tokens}][{self.n_q_heads}][{d}]")
+        if o is None:
+            o = torch.empty(q.shape, dtype=o_dtype or q.dtype, device=q.device)
+        if lse is None:
+            lse = torch.empty((self.n_tokens, self.n_q_heads), dtype=torch.float32, device=q.device)
+        pd = self.pool.desc()
+        check(lib().ep_spliced_attention(self.handle.ptr, self.plan, C.byref(pd),
+                                         dtype_code(q.dtype), q.data_ptr(), dtype_code(o.dtype),
+                                         o.data_ptr(), lse.data_ptr() if lse is not False else None,
+                                         _stream(stream)), "ep_spliced_attention")
+        return o, lse
+
+    def info(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().ep_plan_info(self.plan, C.byref(a), C.byref(b), C.byref(c)), "ep_plan_info")
+        return a.value, b.value, c.value
+
+    def close(self):
+        if getattr(self, "plan", None):
+            lib().ep_plan_destroy(self.plan)
+            self.plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _stream(stream):
     if stream is None:
         return _torch().cuda.current_stream().cuda_stream
