@@ -92,6 +92,8 @@ struct Bars {
 constexpr int kTraceBlocks = 1024;
 enum TraceEv { TR_KISSUE = 0, TR_VISSUE, TR_QK, TR_PV, TR_S_SEEN, TR_P_DONE,
               TR_QK_START, TR_QK_FULLK, TR_QK_DONE, TR_PV_START, TR_PV_PFULL, TR_PV_DONE, TR_N };
+// Per-item events (indexed by the CTA's item number), softmax warp 0.
+enum ItemEv { IT_START = TR_N, IT_QDONE, IT_LASTPV, IT_EPI, IT_OUT, IT_END };  // 18 rows in total
 __device__ __forceinline__ void trace(const DecodeArgs& a, int ev, uint32_t gi) {
     if (a.trace && blockIdx.x == 0 && gi < kTraceBlocks && (threadIdx.x & 31) == 0) {
         long long t;
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t cnt = 0, n = 0;  // blocks processed by this group (all items)
         uint32_t gi0 = 0;         // global index of the item's first block
         for (int it = it0; it < it1; ++it, ++n) {
+            if (threadIdx.x == 0) trace(a, IT_START, n);
             const WorkItem w = a.items[it];
             const int nrows = w.pad > 0 ? w.pad : rows;  // valid rows of this item's tile
             const bool valid_row = v < nrows;
@@ -335,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(B.q_ready);
+                if (threadIdx.x == 0) trace(a, IT_QDONE, n);
             }
 
             float m_used = -INFINITY, l = 0.f;
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (grp < w.nblk) {  // this group ran at least one block: wait its last PV
                 mbar_wait(&B.pv_done[grp], (cnt & 1) ^ 1);
             }
+            if (threadIdx.x == 0) trace(a, IT_LASTPV, n);
             xm[grp * kM + m] = m_used;
             xl[grp * kM + m] = l;
             named_bar_sync(pair_bar, 64);
@@ -480,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(B.o_free);
+            if (threadIdx.x == 0) trace(a, IT_EPI, n);
 
             const int unit = w.b * Hkv + w.g;
             const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
@@ -507,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (grp == 0) a.lse_part[size_t(it) * rows + v] = lse2;
                 }
             }
+            if (threadIdx.x == 0) trace(a, IT_OUT, n);
             if (n_items > 1) {
                 // Fused K2: the last CTA to finish one of this unit's items merges
                 // them in page (= segment) order (attention.cpp:128-144).
@@ -524,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 named_bar_sync(5, kSoftThreads);
             }
+            if (threadIdx.x == 0) trace(a, IT_END, n);
         }
     }
 

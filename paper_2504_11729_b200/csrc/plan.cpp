@@ -35,6 +35,7 @@ using namespace ep;
 namespace {
 
 constexpr int kBlockTokens = 64;
+constexpr int64_t kTcItemWeight = 10;  // K3 work-item overhead in blocks (see build_subplan)
 
 // One query-row set attending to one page list.
 struct VReq {
@@ -57,7 +58,12 @@ struct SubPlan {
     size_t counter_units = 0;
 };
 
-void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t cap_ctas) {
+// item_weight: fixed cost of one work item (Q load, epilogue, output) in
+// 64-token-block units, so CTAs that get many short units (prefill chunks near
+// the start of a prompt) are not overloaded. Measured for K3 (clock64 item
+// trace): ~12-13K cycles per item vs ~1.0-1.4K per block -> 10.
+void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t cap_ctas,
+                   int64_t item_weight = 0) {
     sp.pdesc.clear();
     sp.req_page_off.assign(vr.size() + 1, 0);
     std::vector<int64_t> blocks(vr.size(), 0);
@@ -70,9 +76,12 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
     }
     sp.n_pages = int64_t(sp.pdesc.size());
     sp.n_units = int64_t(vr.size()) * Hkv;
-    int64_t total = 0;
-    for (int64_t x : blocks) total += x * Hkv;
-    sp.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap_ctas, total));
+    int64_t total = 0, total_blocks = 0;
+    for (int64_t x : blocks) {
+        total += (x + (x > 0 ? item_weight : 0)) * Hkv;
+        total_blocks += x * Hkv;
+    }
+    sp.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap_ctas, total_blocks));
     sp.items.clear();
     sp.cta_item_ptr.assign(sp.n_ctas + 1, 0);
     sp.unit_item_ptr.assign(sp.n_units + 1, 0);
@@ -84,6 +93,7 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
         for (int g = 0; g < Hkv; ++g) {
             const int64_t unit = int64_t(b) * Hkv + g;
             bool open = false;
+            if (npg > 0) acc += item_weight;
             for (int64_t lp = 0; lp < npg; ++lp) {
                 while (cta < sp.n_ctas - 1 && acc >= boundary(cta)) {
                     ++cta;
@@ -266,11 +276,11 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         main_vr[b].q0min = q_pos[b];
         main_vr[b].n_rows = rpr;
     }
-    build_subplan(p.main, main_vr, Hkv, cap);
-    p.main.rows = rpr;
     p.main.tc = !decode_supported(p.kv_dtype, p.d_head, rpr) || force_tc();
+    build_subplan(p.main, main_vr, Hkv, cap, p.main.tc ? kTcItemWeight : 0);
+    p.main.rows = rpr;
     if (p.cascade) {
-        build_subplan(p.shared, shared_vr, Hkv, cap);
+        build_subplan(p.shared, shared_vr, Hkv, cap, kTcItemWeight);
         p.shared.rows = group_cap * rpr;
         p.shared.tc = true;
     }
@@ -326,7 +336,7 @@ int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const
     p.batch = int32_t(vr.size());
     p.cascade = false;
     p.has_shared.assign(vr.size(), 0);
-    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms));
+    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), kTcItemWeight);
     p.main.rows = G * C;
     p.main.tc = true;
     return EP_OK;
@@ -435,8 +445,8 @@ unsigned long long* trace_buffer() {
     static unsigned long long* t = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&b, 12 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(b, 0, 12 * 1024 * sizeof(unsigned long long));
+        if (e && e[0] == '1' && cudaMalloc(&b, 18 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 18 * 1024 * sizeof(unsigned long long));
         return b;
     }();
     return t;
@@ -458,7 +468,7 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
                     "verify attention launch");
         h->launches++;
         if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
-            std::vector<unsigned long long> host(12 * 1024);
+            std::vector<unsigned long long> host(18 * 1024);
             cudaStreamSynchronize(s);
             cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
             const char* f = std::getenv("EP_TRACE_FILE");
