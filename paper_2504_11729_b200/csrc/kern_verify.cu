@@ -19,7 +19,8 @@
 // ranges like K1):
 //   warp 8 lane 0 : TMA producer of the K ring (5 stages, freed after QK)
 //   warp 10 lane 0: TMA producer of the V ring (3 stages, freed after PV)
-//   warp 9 lane 0 : MMA issuer; warp 9 owns the TMEM allocation
+//   warp 9        : QK MMA issuer (one elected lane); owns the TMEM allocation
+//   warp 11       : PV MMA issuer
 //   warps 0-7     : softmax + epilogue. Query rows are spread over the four
 //                   TMEM lane quarters (row v -> M row 32*(v%4) + v/4) so all
 //                   four SMSPs work, and each row's 64 keys are split between
@@ -49,8 +50,8 @@ constexpr int kKStages = 7;  // K ring: a K block is free right after its QK
 constexpr int kVStages = 7;  // V ring: a V block is free after its PV
 constexpr int kSoftWarps = 8;  // 2 ping-pong groups x 4 TMEM lane quarters
 constexpr int kSoftThreads = kSoftWarps * 32;
-constexpr int kProdWarp = 8, kMmaWarp = 9, kProdVWarp = 10;
-constexpr int kThreads = 352;
+constexpr int kProdWarp = 8, kMmaWarp = 9, kProdVWarp = 10, kPvWarp = 11;
+constexpr int kThreads = 384;
 constexpr int kMaxRows = 128;     // valid query rows per tile (one M = 128 MMA tile)
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
 
@@ -62,16 +63,19 @@ constexpr int OFF_VST = OFF_STAGE + kKStages * kBlkBytes;
 constexpr int OFF_XM = OFF_VST + kVStages * kBlkBytes;  // [2 groups][128] row max of each group
 constexpr int OFF_XL = OFF_XM + 2 * kM * 4; // [2 groups][128] row sum of each group
 constexpr int OFF_BAR = OFF_XL + 2 * kM * 4;
-constexpr int kNumBars = 2 * kKStages + 2 * kVStages + 2 + 2 + 2 + 2;
+constexpr int kNumBars = 2 * kKStages + 2 * kVStages + 2 + 2 + 2 + 2 + 2;
 constexpr int OFF_MISC = OFF_BAR + kNumBars * 8;
 constexpr int kSmem = OFF_MISC + 32;  // dynamic smem base must be 1024-aligned (checked)
 // TMEM columns (512): O of group 0 / 1 (128 each, fp32), S of group 0 / 1
 // (64 each, fp32) whose columns are overwritten by that group's P as bf16 hi
 // (32 columns: two bf16 per 32-bit column) and lo (32), then the item's Q
 // tile (64 columns, bf16). Q and P are the A operands of the MMAs, so the
-// tensor core reads only K and V from shared memory.
+// tensor core reads only K and V from shared memory. With a single bf16 P
+// (bf16 output) P gets its own 32 columns per group (kColP), so the QK of a
+// group's next block can overwrite S as soon as the softmax has read it,
+// instead of after the PV that consumes P.
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColO = 0, kColS = 256, kColQ = 384;
+constexpr uint32_t kColO = 0, kColS = 256, kColQ = 384, kColP = 448;
 
 constexpr uint32_t kIdescQK = umma::idesc_bf16_f32(kM, kBT, false, false);
 constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
@@ -86,6 +90,7 @@ struct Bars {
     uint64_t* pv_done;  // [2] PV finished (P buffer free, O updated)
     uint64_t* q_ready;  // Q tile of the item in smem
     uint64_t* o_free;   // epilogue read O
+    uint64_t* s_free;   // [2] softmax read S (single-P mode: S may be overwritten)
 };
 
 // Debug trace (a.trace != null, CTA 0 only): clock64 per event and block.
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
     constexpr int kRB = 2 * kKStages + 2 * kVStages;
     Bars B{bar, bar + kKStages, bar + 2 * kKStages, bar + 2 * kKStages + kVStages,
-           bar + kRB, bar + kRB + 2, bar + kRB + 4, bar + kRB + 6, bar + kRB + 7};
+           bar + kRB, bar + kRB + 2, bar + kRB + 4, bar + kRB + 6, bar + kRB + 7, bar + kRB + 8};
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_MISC);
     int* s_flag = reinterpret_cast<int*>(smem + OFF_MISC + 16);
 
@@ -177,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&B.s_full[i], 1);
             mbar_init(&B.p_full[i], 4);
             mbar_init(&B.pv_done[i], 1);
+            mbar_init(&B.s_free[i], 4);
         }
         mbar_init(B.q_ready, kSoftWarps);
         mbar_init(B.o_free, kSoftWarps);
@@ -218,35 +224,57 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kMmaWarp) {
-        // ================================ MMA =================================
+        // ============================== QK issuer ===============================
         // The whole warp runs the loop (operands stay warp-uniform); one
-        // elected lane issues each MMA / commit.
-        {
-            // Descriptors are built once; per MMA only the 14-bit start-address
-            // field moves (byte offset >> 4, no carry for smem < 256 KB), so the
-            // single issuing thread spends a couple of instructions per MMA.
-            const uint64_t dk = umma::smem_desc_sw128(smem_u32(sStage), 16, 1024);
+        // elected lane issues each MMA / commit. QK and PV have separate issuing
+        // warps, so neither's barrier waits stall the other's MMAs (a UTCHMMA
+        // blocks its issuer while the tensor queue is full). Descriptors are
+        // built once; per MMA only the 14-bit start-address field moves.
+        const uint64_t dk = umma::smem_desc_sw128(smem_u32(sStage), 16, 1024);
+        const bool two_part = a.pv_parts > 1;
+        // S[grp] may be overwritten once the previous block of the group has
+        // been read by the softmax (single P: s_free) or, when P aliases S
+        // (hi+lo), once its PV completed (pv_done). Every phase is waited in
+        // order, so the parities never alias.
+        uint64_t* sbar = two_part ? B.pv_done : B.s_free;
+        uint32_t gi = 0, n = 0;
+        uint32_t nqk[2] = {0, 0};
+        if (two_part) {
+            // hi+lo P aliases S: QK(i+2) must follow PV(i). One warp issues both
+            // in the order QK(0) QK(1) | PV(i) QK(i+2) ...; the tensor pipe runs
+            // in issue order, so QK(i+2) needs no wait for PV(i)'s completion.
             const uint64_t dv = umma::smem_desc_sw128(smem_u32(smem + OFF_VST), kKVHalf, 1024);
-            uint32_t gi = 0, n = 0;
-            uint32_t cqk[2] = {0, 0}, cpv[2] = {0, 0};  // per-group block counters
-            // PV of local block i (global g_i) into O[i & 1].
+            uint32_t cpv[2] = {0, 0};
+            auto issue_qk = [&](int i, uint32_t g_i) {
+                const int st = g_i % kKStages, grp = i & 1;
+                trace(a, TR_QK_START, g_i);
+                mbar_wait(&B.full_k[st], (g_i / kKStages) & 1);
+                trace(a, TR_QK, g_i);
+                umma::fence_after_sync();
+                const uint64_t kd0 = dk + ((st * kBlkBytes) >> 4);
+                if (umma::elect_one())
+                    umma::mma_chain_qk8_ts(tmem + kColS + grp * kBT, tmem + kColQ, kd0, kIdescQK);
+                if (umma::elect_one()) {
+                    umma::mma_commit(&B.s_full[grp]);
+                    umma::mma_commit(&B.empty_k[st]);
+                }
+                __syncwarp();
+                trace(a, TR_QK_DONE, g_i);
+            };
             auto issue_pv = [&](int i, uint32_t g_i) {
                 const int grp = i & 1;
                 trace(a, TR_PV_START, g_i);
                 mbar_wait(&B.p_full[grp], cpv[grp] & 1);
-                trace(a, TR_PV_PFULL, g_i);
-                if (i == 0) mbar_wait(B.o_free, (n & 1) ^ 1);  // previous item's epilogue read O
+                if (i == 0) mbar_wait(B.o_free, (n & 1) ^ 1);
                 const uint32_t vs = g_i % kVStages;
                 mbar_wait(&B.full_v[vs], (g_i / kVStages) & 1);
                 trace(a, TR_PV, g_i);
                 umma::fence_after_sync();
                 const uint64_t bd0 = dv + ((vs * kBlkBytes) >> 4);
                 const uint32_t ta0 = tmem + kColS + grp * kBT, td = tmem + kColO + grp * kD;
-                // P = hi + lo (two bf16 tiles in TMEM): O += P_hi V + P_lo V keeps
-                // the probabilities at ~2^-17 relative instead of bf16's 2^-9.
                 if (umma::elect_one()) {
                     umma::mma_chain_pv4(td, ta0, bd0, kIdescPV, i < 2 ? 1u : 0u);
-                    if (a.pv_parts > 1) umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
+                    umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
                 }
                 if (umma::elect_one()) {
                     umma::mma_commit(&B.pv_done[grp]);
@@ -256,16 +284,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                 trace(a, TR_PV_DONE, g_i);
                 ++cpv[grp];
             };
-            // QK of local block i (global g_i) into S[i & 1].
-            auto issue_qk = [&](int i, uint32_t g_i) {
-                const int st = g_i % kKStages;
+            for (int it = it0; it < it1; ++it, ++n) {
+                const WorkItem w = a.items[it];
+                mbar_wait(B.q_ready, n & 1);
+                for (int i = 0; i < 2 && i < w.nblk; ++i) issue_qk(i, gi + i);
+                for (int i = 0; i < w.nblk; ++i) {
+                    issue_pv(i, gi + i);
+                    if (i + 2 < w.nblk) issue_qk(i + 2, gi + i + 2);
+                }
+                gi += uint32_t(w.nblk);
+            }
+        } else
+        for (int it = it0; it < it1; ++it, ++n) {
+            const WorkItem w = a.items[it];
+            mbar_wait(B.q_ready, n & 1);
+            for (int i = 0; i < w.nblk; ++i) {
                 const int grp = i & 1;
+                const uint32_t g_i = gi + i;
+                const int st = g_i % kKStages;
                 trace(a, TR_QK_START, g_i);
+                if (nqk[grp] > 0) mbar_wait(&sbar[grp], (nqk[grp] - 1) & 1);
                 mbar_wait(&B.full_k[st], (g_i / kKStages) & 1);
-                trace(a, TR_QK_FULLK, g_i);
-                // S[grp] holds P of this group's previous block until its PV has
-                // read it; that PV was issued before this QK and the tensor pipe
-                // executes in issue order, so no wait is needed here.
                 trace(a, TR_QK, g_i);
                 umma::fence_after_sync();
                 const uint64_t kd0 = dk + ((st * kBlkBytes) >> 4);
@@ -278,21 +317,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
                 trace(a, TR_QK_DONE, g_i);
-                ++cqk[grp];
-            };
-            // Issue order QK(0) QK(1) | QK(i+2) PV(i) ...: a group's next S is
-            // computed as soon as it has read its current S, so the softmax of
-            // block i+2 can start the moment block i's is done.
-            for (int it = it0; it < it1; ++it, ++n) {
-                const WorkItem w = a.items[it];
-                mbar_wait(B.q_ready, n & 1);
-                for (int i = 0; i < 2 && i < w.nblk; ++i) issue_qk(i, gi + i);
-                for (int i = 0; i < w.nblk; ++i) {
-                    issue_pv(i, gi + i);  // reads P(i) from S[i & 1] ...
-                    if (i + 2 < w.nblk) issue_qk(i + 2, gi + i + 2);  // ... before QK(i+2) overwrites it
-                }
-                gi += uint32_t(w.nblk);
+                ++nqk[grp];
             }
+            gi += uint32_t(w.nblk);
+        }
+    } else if (warp == kPvWarp) {
+        // ======================= PV issuer (single-P mode) =======================
+        const uint64_t dv = umma::smem_desc_sw128(smem_u32(smem + OFF_VST), kKVHalf, 1024);
+        const bool two_part = a.pv_parts > 1;
+        uint32_t gi = 0, n = 0;
+        uint32_t cpv[2] = {0, 0};
+        for (int it = two_part ? it1 : it0; it < it1; ++it, ++n) {
+            const WorkItem w = a.items[it];
+            for (int i = 0; i < w.nblk; ++i) {
+                const int grp = i & 1;
+                const uint32_t g_i = gi + i;
+                trace(a, TR_PV_START, g_i);
+                mbar_wait(&B.p_full[grp], cpv[grp] & 1);
+                trace(a, TR_PV_PFULL, g_i);
+                if (i == 0) mbar_wait(B.o_free, (n & 1) ^ 1);  // previous item's epilogue read O
+                const uint32_t vs = g_i % kVStages;
+                mbar_wait(&B.full_v[vs], (g_i / kVStages) & 1);
+                trace(a, TR_PV, g_i);
+                umma::fence_after_sync();
+                const uint64_t bd0 = dv + ((vs * kBlkBytes) >> 4);
+                const uint32_t ta0 = two_part ? tmem + kColS + grp * kBT : tmem + kColP + grp * 32;
+                const uint32_t td = tmem + kColO + grp * kD;
+                // P = hi + lo (two bf16 tiles in TMEM): O += P_hi V + P_lo V keeps
+                // the probabilities at ~2^-17 relative instead of bf16's 2^-9.
+                if (umma::elect_one()) {
+                    umma::mma_chain_pv4(td, ta0, bd0, kIdescPV, i < 2 ? 1u : 0u);
+                    if (two_part) umma::mma_chain_pv4(td, ta0 + 32, bd0, kIdescPV, 0u);
+                }
+                if (umma::elect_one()) {
+                    umma::mma_commit(&B.pv_done[grp]);
+                    umma::mma_commit(&B.empty_v[vs]);
+                }
+                __syncwarp();
+                trace(a, TR_PV_DONE, g_i);
+                ++cpv[grp];
+            }
+            gi += uint32_t(w.nblk);
         }
     } else {
         // ========================= softmax + epilogue =========================
@@ -301,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int v = lane * 4 + quarter;                // query row index of this M row
         const uint32_t lane_off = uint32_t(quarter * 32) << 16;
         const uint32_t tS = tmem + kColS + grp * kBT + lane_off;
+        const uint32_t tP = tmem + kColP + grp * 32 + lane_off;  // single-P mode
         const uint32_t tOg = tmem + kColO + grp * kD + lane_off;
         const float scale = a.q_scale;  // log2(e)/sqrt(d)
         const bool two_part = a.pv_parts > 1;
@@ -358,15 +424,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(sr));
                 umma::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
                 umma::tmem_wait_ld();
+                if (!two_part) {  // S is in registers: the next QK may overwrite it
+                    umma::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&B.s_free[grp]);
+                }
 
                 if (!(nv == kBT && pos + kBT - 1 <= q0)) {
 #pragma unroll
                     for (int j = 0; j < 64; ++j)
                         if (!(j < nv && pos + j <= my_qpos)) sr[j] = __float_as_uint(-INFINITY);
                 }
-                float hmax = -INFINITY;
+                // row max as a tree (8 independent chains, then 3 levels)
+                float mx[8];
 #pragma unroll
-                for (int j = 0; j < 64; ++j) hmax = fmaxf(hmax, __uint_as_float(sr[j]));
+                for (int c = 0; c < 8; ++c) mx[c] = __uint_as_float(sr[c]);
+#pragma unroll
+                for (int j = 8; j < 64; ++j) mx[j & 7] = fmaxf(mx[j & 7], __uint_as_float(sr[j]));
+                const float hmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
                 const float bmax = valid_row ? hmax * scale : -INFINITY;
                 // lazy max: move it only when the block exceeds it by > 2^kLazy
                 float corr = 1.f;
@@ -376,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m_used = bmax;
                 }
                 const float mu = m_used == -INFINITY ? 0.f : m_used;
-                float2 rs2 = make_float2(0.f, 0.f);
+                float2 rsa[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f)};  // 4 independent row-sum chains
                 uint32_t pk[32], pl[32];
                 if (two_part) {
 #pragma unroll
@@ -384,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
                         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
                         const float2 p2 = make_float2(p0, p1);
-                        rs2 = __fadd2_rn(rs2, p2);
+                        rsa[j & 3] = __fadd2_rn(rsa[j & 3], p2);
                         pk[j] = pack_bf16(p0, p1);
                         const float2 hi = bf16x2_to_float2(pk[j]);
                         const float2 lo = __fadd2_rn(p2, make_float2(-hi.x, -hi.y));
@@ -399,9 +476,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
                         const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
                         pk[j] = pack_bf16(p0, p1);
-                        rs2 = __fadd2_rn(rs2, make_float2(p0, p1));
+                        rsa[j & 3] = __fadd2_rn(rsa[j & 3], make_float2(p0, p1));
                     }
                 }
+                const float2 rs2 = __fadd2_rn(__fadd2_rn(rsa[0], rsa[1]), __fadd2_rn(rsa[2], rsa[3]));
                 l = l * corr + (rs2.x + rs2.y);
 
                 // P/O of this group are free once its previous PV completed.
@@ -421,8 +499,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 // P row -> TMEM over this group's S columns (A operand of the PV
                 // MMAs): hi tile then lo tile.
-                umma::tmem_st32(tS, pk);
-                if (two_part) umma::tmem_st32(tS + 32, pl);
+                if (two_part) {
+                    umma::tmem_st32(tS, pk);
+                    umma::tmem_st32(tS + 32, pl);
+                } else {
+                    umma::tmem_st32(tP, pk);
+                }
                 umma::tmem_wait_st();
                 if (nv < kBT) {
                     // Tail rows of V in the stage are stale page slots: zero them
