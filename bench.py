@@ -378,8 +378,8 @@ def main():
 
 def run_extras(args, world, rank, h):
     """The other BASELINE configs, measured in the same run: config 3
-    (speculative verify p50 latency, k = 4 / 8) and config 5 (multi-tenant
-    shared prefix) on rank 0 at N = 1; config 4 (128K split-KV: local K1 +
+    (speculative verify p50 latency, k = 4 / 8), config 5 (multi-tenant
+    shared prefix), the prefill tiles and the KV ingest on rank 0 at N = 1; config 4 (128K split-KV: local K1 +
     the peer-memory combine kernel; at N > 1 also NCCL all-gather + K5 merge
     for comparison) at every N."""
     import gc
@@ -402,6 +402,17 @@ def run_extras(args, world, rank, h):
         extras["verify"] = ver
         extras["verify_p50_ms"] = {k: v["step_p50_ms"] for k, v in ver.items()}
         extras["multitenant"] = multitenant_bench.run(steps, 3, h)
+        gc.collect()
+        torch.cuda.empty_cache()
+        # prefill tiles on tcgen05, KV ingest from EPKV frames
+        import ingest_bench
+        import prefill_bench
+        extras["prefill"] = {kind: prefill_bench.run(kind, 4 if kind == "cloud" else 32,
+                                                     max(5, steps // 2), 3, h)
+                             for kind in ("cloud", "edge")}
+        gc.collect()
+        torch.cuda.empty_cache()
+        extras["ingest"] = ingest_bench.run(max(5, steps // 2), 3, h)
         gc.collect()
         torch.cuda.empty_cache()
     skv = {}

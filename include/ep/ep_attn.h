@@ -40,7 +40,8 @@ typedef enum ep_status {
     EP_ECUDA = 3,        /* CUDA runtime / launch failure */
     EP_ENCCL = 4,        /* NCCL failure (split-KV combine) */
     EP_ENOMEM = 5,       /* device or host allocation failed */
-    EP_EUNSUPPORTED = 6  /* shape/dtype combination without a kernel instance */
+    EP_EUNSUPPORTED = 6, /* shape/dtype combination without a kernel instance */
+    EP_EWIRE = 7         /* malformed EPKV frame (wire::WireError, wire.hpp:94-104) */
 } ep_status;
 
 /* Numbering matches oracle/ep_oracle.h (EPO_DT_*). bf16 is raw uint16 storage. */
@@ -213,6 +214,36 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
 int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int32_t* dst_page,
                  const int32_t* dst_slot, const void* k_new, const void* v_new,
                  ep_stream stream);
+
+/* KV ingest: one EPKV kv_frame as the reference's
+ * encode_frame writes it (wire.hpp:59-75, wire.cpp:70-136: 10-byte header,
+ * 14-byte body header, then K and V as seq_len x (n_heads*d_head) row-major
+ * little-endian doubles) decoded straight into the page pool: frame token t
+ * -> page page_table[t / page_tokens], slot t % page_tokens; frame head h
+ * (columns [h*d, (h+1)*d), segment_from_frame, edge.cpp:61-67) -> kv head h;
+ * values rounded to the pool dtype (f64 -> bf16 / f32, round to nearest even).
+ * frame may be device memory, pinned host memory (read in place by the
+ * kernel: decode + convert + scatter in one pass) or pageable host memory
+ * (staged). Validation mirrors decode_frame (wire.cpp:138-221): EP_EWIRE
+ * with info->wire_error = WireError::Kind + 1 (1 bad_magic, 2 bad_version,
+ * 3 truncated, 4 length_overflow, 5 malformed) or 6 for a valid frame that
+ * is not a kv frame. EP_EINVAL when n_heads / d_head do not match the pool,
+ * seq_len is 0 (expect_kv_frame, edge.cpp:41-60) or n_pages is too small.
+ * page_table: device int32 [n_pages]. Stream-ordered; a pinned or device
+ * frame must stay valid until the stream reaches this point. */
+typedef struct ep_kv_frame_info {
+    uint32_t session_id;
+    uint32_t seq_len;
+    uint16_t layer;
+    uint16_t n_heads;
+    uint16_t d_head;
+    uint16_t pad;
+    int32_t wire_error;
+} ep_kv_frame_info;
+
+int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const void* frame, size_t frame_bytes,
+                       const int32_t* page_table, int32_t n_pages, ep_kv_frame_info* info,
+                       ep_stream stream);
 
 /* ==================================================================== */
 /* 3b. Cross-GPU split-KV combine over NVLink peer memory (config 4).   */

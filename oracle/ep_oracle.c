@@ -361,3 +361,103 @@ int epo_verify_greedy(const double* attn_out, int batch, int n_q, int width,
     free(logits);
     return EPO_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* KV ingest (wire.cpp:119-221, edge.cpp:61-67)                              */
+/* ------------------------------------------------------------------------ */
+
+static uint32_t rd_u32(const uint8_t* b) {
+    return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+}
+static uint16_t rd_u16(const uint8_t* b) { return (uint16_t)(b[0] | (b[1] << 8)); }
+static double rd_f64(const uint8_t* b) {
+    uint64_t bits = 0;
+    double d;
+    for (int i = 0; i < 8; ++i) bits |= (uint64_t)b[i] << (8 * i);
+    memcpy(&d, &bits, 8);
+    return d;
+}
+
+int epo_kv_frame_decode(const uint8_t* frame, size_t n, epo_kv_frame_info* info, double* k,
+                        double* v) {
+    /* decode_header (wire.cpp:138-162) */
+    if (n < 10) return EPO_WIRE_TRUNCATED;
+    if (frame[0] != 'E' || frame[1] != 'P' || frame[2] != 'K' || frame[3] != 'V') return EPO_WIRE_BAD_MAGIC;
+    if (frame[4] != 0x01) return EPO_WIRE_BAD_VERSION;
+    if (frame[5] > 4) return EPO_WIRE_MALFORMED;
+    const uint32_t len = rd_u32(frame + 6);
+    if (len > (1u << 30)) return EPO_WIRE_LENGTH_OVERFLOW;
+    /* decode_frame (wire.cpp:209-219): exactly one frame */
+    if (n != 10 + (size_t)len) return EPO_WIRE_TRUNCATED;
+    /* decode_payload of the other message types (wire.cpp:165-184, :202-208):
+     * short payloads are truncated reads, trailing bytes are malformed */
+    switch (frame[5]) {
+    case 0: return len < 20 ? EPO_WIRE_TRUNCATED : len > 20 ? EPO_WIRE_MALFORMED : EPO_WIRE_NOT_KV;
+    case 1: return len < 6 ? EPO_WIRE_TRUNCATED : len > 6 ? EPO_WIRE_MALFORMED : EPO_WIRE_NOT_KV;
+    case 3: return len != 0 ? EPO_WIRE_MALFORMED : EPO_WIRE_NOT_KV;
+    case 4: return len < 4 ? EPO_WIRE_TRUNCATED : EPO_WIRE_NOT_KV;
+    default: break;
+    }
+    /* decode_payload, kv_frame (wire.cpp:185-201) */
+    const uint8_t* p = frame + 10;
+    if (len < 14) return EPO_WIRE_TRUNCATED;
+    epo_kv_frame_info f;
+    f.session_id = rd_u32(p);
+    f.layer = rd_u16(p + 4);
+    f.seq_len = rd_u32(p + 6);
+    f.n_heads = rd_u16(p + 10);
+    f.d_head = rd_u16(p + 12);
+    f.pad = 0;
+    const uint64_t vals = (uint64_t)f.seq_len * f.n_heads * f.d_head;
+    if ((uint64_t)(len - 14) != 16 * vals) return EPO_WIRE_MALFORMED;
+    if (info) *info = f;
+    if (k)
+        for (uint64_t i = 0; i < vals; ++i) k[i] = rd_f64(p + 14 + 8 * i);
+    if (v)
+        for (uint64_t i = 0; i < vals; ++i) v[i] = rd_f64(p + 14 + 8 * (vals + i));
+    return EPO_WIRE_OK;
+}
+
+float epo_f64_to_f32(double x) { return (float)x; }
+
+/* Correct RNE f64 -> bf16: f64 -> f32 rounded to ODD, then f32 -> bf16 RNE
+ * (round-to-odd keeps 16 > 2 guard bits, so the double rounding is exact). */
+uint16_t epo_f64_to_bf16(double x) {
+    if (x != x) return 0x7FC0;
+    float f = (float)x; /* RN */
+    if (fabs((double)f) > fabs(x)) f = nextafterf(f, 0.0f); /* -> toward zero */
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((double)f != x) u |= 1u; /* inexact: set the sticky (odd) bit */
+    if ((u & 0x7F800000u) == 0x7F800000u) return (uint16_t)(u >> 16); /* inf */
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+int epo_kv_ingest(const uint8_t* frame, size_t n, int kv_dtype, int page_tokens,
+                  const int32_t* page_table, void* k_pages, void* v_pages, epo_kv_frame_info* info) {
+    epo_kv_frame_info f;
+    int rc = epo_kv_frame_decode(frame, n, &f, NULL, NULL);
+    if (rc) return rc;
+    if (info) *info = f;
+    const size_t H = f.n_heads, d = f.d_head, row = H * d;
+    const uint8_t* kd = frame + 24;
+    const uint8_t* vd = kd + 8 * (size_t)f.seq_len * row;
+    for (size_t t = 0; t < f.seq_len; ++t) {
+        const size_t page = (size_t)page_table[t / (size_t)page_tokens], slot = t % (size_t)page_tokens;
+        for (size_t h = 0; h < H; ++h)
+            for (size_t c = 0; c < d; ++c) {
+                const size_t src = t * row + h * d + c;
+                const size_t dst = ((page * H + h) * (size_t)page_tokens + slot) * d + c;
+                const double a = rd_f64(kd + 8 * src), b = rd_f64(vd + 8 * src);
+                if (kv_dtype == EPO_DT_BF16) {
+                    ((uint16_t*)k_pages)[dst] = epo_f64_to_bf16(a);
+                    ((uint16_t*)v_pages)[dst] = epo_f64_to_bf16(b);
+                } else {
+                    ((float*)k_pages)[dst] = epo_f64_to_f32(a);
+                    ((float*)v_pages)[dst] = epo_f64_to_f32(b);
+                }
+            }
+    }
+    return EPO_WIRE_OK;
+}

@@ -104,6 +104,43 @@ int epo_verify_greedy(const double* attn_out, int batch, int n_q, int width,
  * i-th draw of SplitMix64(seed), rounded to dtype (f64 -> f32 RN -> bf16 RN). */
 void epo_fill_uniform(int dtype, void* dst, size_t n, uint64_t seed, double lo, double hi);
 
+/* ------------------------------------------------------------------------ */
+/* KV ingest: an EPKV kv_frame (wire.hpp:59-75) decoded into device-layout   */
+/* pages.                                                */
+/* ------------------------------------------------------------------------ */
+
+/* WireError::Kind (wire.hpp:94-104) + 1; EPO_WIRE_NOT_KV: a valid frame of
+ * another message type. */
+enum { EPO_WIRE_OK = 0, EPO_WIRE_BAD_MAGIC = 1, EPO_WIRE_BAD_VERSION = 2, EPO_WIRE_TRUNCATED = 3,
+       EPO_WIRE_LENGTH_OVERFLOW = 4, EPO_WIRE_MALFORMED = 5, EPO_WIRE_NOT_KV = 6 };
+
+typedef struct {
+    uint32_t session_id;
+    uint32_t seq_len;
+    uint16_t layer;
+    uint16_t n_heads;
+    uint16_t d_head;
+    uint16_t pad;
+} epo_kv_frame_info;
+
+/* decode_frame restricted to kv frames (wire.cpp:138-221): validates the
+ * 10-byte header and the 14-byte body header, fills *info and, when k / v are
+ * non-NULL, the seq_len x (n_heads*d_head) row-major doubles. Returns an
+ * EPO_WIRE_* code. */
+int epo_kv_frame_decode(const uint8_t* frame, size_t n, epo_kv_frame_info* info, double* k,
+                        double* v);
+
+/* f64 -> bf16 (raw) and f64 -> f32, round to nearest even, correctly rounded. */
+uint16_t epo_f64_to_bf16(double x);
+float epo_f64_to_f32(double x);
+
+/* The ingest: token t of the frame -> page page_table[t / page_tokens], slot
+ * t % page_tokens; frame head h (columns [h*d, (h+1)*d), segment_from_frame,
+ * edge.cpp:61-67) -> kv head h of the page. Pages [num][n_heads][page_tokens][d]
+ * in kv_dtype (EPO_DT_F32 / EPO_DT_BF16). Returns an EPO_WIRE_* code. */
+int epo_kv_ingest(const uint8_t* frame, size_t n, int kv_dtype, int page_tokens,
+                  const int32_t* page_table, void* k_pages, void* v_pages, epo_kv_frame_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,12 @@ def _load(impl: str) -> C.CDLL:
                                           C.c_void_p, C.c_void_p, C.c_void_p, _dp]
         lib.epo_fill_uniform.argtypes = [C.c_int, C.c_void_p, C.c_size_t, C.c_uint64,
                                          C.c_double, C.c_double]
+        lib.epo_kv_frame_decode.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                            C.c_void_p]
+        lib.epo_f64_to_bf16.restype = C.c_uint16
+        lib.epo_f64_to_bf16.argtypes = [C.c_double]
+        lib.epo_kv_ingest.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]
     else:
         lib.epref_last_error.restype = C.c_char_p
         lib.epref_log_add_exp.restype = C.c_double
@@ -140,6 +146,14 @@ def _load(impl: str) -> C.CDLL:
         lib.epref_session_first_token.argtypes = [C.c_void_p, C.POINTER(C.c_uint32)]
         lib.epref_session_decode_step.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p,
                                                   C.POINTER(C.c_uint32)]
+        if hasattr(lib, "epref_kv_frame_encode"):
+            lib.epref_kv_frame_encode.restype = C.c_size_t
+            lib.epref_kv_frame_encode.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                                  C.c_size_t]
+            lib.epref_end_of_prefill_frame.restype = C.c_size_t
+            lib.epref_end_of_prefill_frame.argtypes = [C.c_void_p, C.c_size_t]
+            lib.epref_kv_frame_decode.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                                  C.c_void_p]
     _libs[impl] = lib
     return lib
 
@@ -508,3 +522,79 @@ class RefSession:
         rc = self.lib.epref_session_decode_step(self.h, last, logits.ctypes.data, C.byref(nxt))
         _raise(rc, "decode_step", self.lib)
         return nxt.value, logits
+
+
+# -------------------------------------------------------------- KV ingest --
+# EPKV kv frames (wire.hpp:59-75; wire.cpp:70-221) and their decode into
+# device-layout pages.
+
+WIRE_OK, WIRE_BAD_MAGIC, WIRE_BAD_VERSION, WIRE_TRUNCATED, WIRE_LENGTH_OVERFLOW, \
+    WIRE_MALFORMED, WIRE_NOT_KV = range(7)
+
+
+class KVFrameInfo(C.Structure):
+    """epo_kv_frame_info."""
+    _fields_ = [("session_id", C.c_uint32), ("seq_len", C.c_uint32), ("layer", C.c_uint16),
+                ("n_heads", C.c_uint16), ("d_head", C.c_uint16), ("pad", C.c_uint16)]
+
+
+def kv_frame_encode(session_id, layer, k, v):
+    """The reference's own encode_frame of a KVFrame (oracle/_ref). k, v:
+    [seq_len][n_heads][d_head] float64 -> frame bytes."""
+    k = _f64(k)
+    v = _f64(v)
+    seq, H, d = k.shape
+    info = KVFrameInfo(session_id, seq, layer, H, d, 0)
+    lib = _load("ref")
+    n = lib.epref_kv_frame_encode(C.byref(info), k.ctypes.data, v.ctypes.data, None, 0)
+    out = np.empty(n, dtype=np.uint8)
+    lib.epref_kv_frame_encode(C.byref(info), k.ctypes.data, v.ctypes.data, out.ctypes.data, n)
+    return out
+
+
+def end_of_prefill_frame():
+    lib = _load("ref")
+    out = np.empty(16, dtype=np.uint8)
+    n = lib.epref_end_of_prefill_frame(out.ctypes.data, 16)
+    return out[:n].copy()
+
+
+def kv_frame_decode(frame, impl: str = "port"):
+    """(code, info, k, v): code is WIRE_*; k, v [seq][H][d] float64 when OK."""
+    frame = np.ascontiguousarray(frame, dtype=np.uint8)
+    lib = _load(impl)
+    f = lib.epo_kv_frame_decode if impl == "port" else lib.epref_kv_frame_decode
+    info = KVFrameInfo()
+    rc = f(frame.ctypes.data, frame.size, C.byref(info), None, None)
+    if rc != WIRE_OK:
+        return rc, None, None, None
+    n = info.seq_len * info.n_heads * info.d_head
+    k = np.empty(n)
+    v = np.empty(n)
+    rc = f(frame.ctypes.data, frame.size, C.byref(info), k.ctypes.data, v.ctypes.data)
+    shape = (info.seq_len, info.n_heads, info.d_head)
+    return rc, info, k.reshape(shape), v.reshape(shape)
+
+
+def f64_to_bf16(x) -> np.ndarray:
+    lib = _load("port")
+    x = _f64(x)
+    return np.array([lib.epo_f64_to_bf16(float(a)) for a in x.reshape(-1)], dtype=np.uint16)
+
+
+def kv_ingest(frame, kv_dtype: int, page_tokens: int, page_table, num_pages: int):
+    """Port of the device ingest: (code, info, k_pages, v_pages) with pages
+    [num_pages][n_heads][page_tokens][d] (bf16 raw uint16 or float32)."""
+    frame = np.ascontiguousarray(frame, dtype=np.uint8)
+    code, info, _, _ = kv_frame_decode(frame)
+    if code != WIRE_OK:
+        return code, None, None, None
+    dt = np.uint16 if kv_dtype == DT_BF16 else np.float32
+    shape = (num_pages, info.n_heads, page_tokens, info.d_head)
+    kp = np.zeros(shape, dtype=dt)
+    vp = np.zeros(shape, dtype=dt)
+    pt = np.ascontiguousarray(page_table, dtype=np.int32)
+    lib = _load("port")
+    rc = lib.epo_kv_ingest(frame.ctypes.data, frame.size, kv_dtype, page_tokens, pt.ctypes.data,
+                           kp.ctypes.data, vp.ctypes.data, C.byref(info))
+    return rc, info, kp, vp

@@ -27,6 +27,7 @@
 #include "edgeprompt/cache.hpp"
 #include "edgeprompt/matrix.hpp"
 #include "edgeprompt/model.hpp"
+#include "edgeprompt/wire.hpp"
 #include "ep_oracle.h"
 
 using namespace edgeprompt;
@@ -387,6 +388,57 @@ int epref_session_decode_step(void* s, std::uint32_t last, double* logits, std::
         if (logits) std::copy(r.logits.begin(), r.logits.end(), logits);
         *next = r.next_token;
     });
+}
+
+
+// ---------------------------------------------------------------- wire --
+// The reference's own EPKV codec (wire.cpp): encode a kv frame, decode any
+// frame and report its WireError kind (wire.hpp:94-104) + 1, or 6 when the
+// frame is valid but not a kv frame.
+
+std::size_t epref_kv_frame_encode(const epo_kv_frame_info* info, const double* k, const double* v,
+                                  std::uint8_t* out, std::size_t cap) {
+    wire::KVFrame f;
+    f.session_id = info->session_id;
+    f.layer = info->layer;
+    f.seq_len = info->seq_len;
+    f.n_heads = info->n_heads;
+    f.d_head = info->d_head;
+    const std::size_t n = f.values_per_matrix();
+    f.k_data.assign(k, k + n);
+    f.v_data.assign(v, v + n);
+    const std::vector<std::uint8_t> bytes = wire::encode_frame(f);
+    if (out && bytes.size() <= cap) std::memcpy(out, bytes.data(), bytes.size());
+    return bytes.size();
+}
+
+std::size_t epref_end_of_prefill_frame(std::uint8_t* out, std::size_t cap) {
+    const std::vector<std::uint8_t> bytes = wire::encode_frame(wire::EndOfPrefill{});
+    if (out && bytes.size() <= cap) std::memcpy(out, bytes.data(), bytes.size());
+    return bytes.size();
+}
+
+int epref_kv_frame_decode(const std::uint8_t* frame, std::size_t n, epo_kv_frame_info* info,
+                          double* k, double* v) {
+    try {
+        const wire::Message m = wire::decode_frame(std::span<const std::uint8_t>(frame, n));
+        const auto* f = std::get_if<wire::KVFrame>(&m);
+        if (!f) return 6;
+        if (info) {
+            info->session_id = f->session_id;
+            info->layer = f->layer;
+            info->seq_len = f->seq_len;
+            info->n_heads = f->n_heads;
+            info->d_head = f->d_head;
+            info->pad = 0;
+        }
+        if (k) std::copy(f->k_data.begin(), f->k_data.end(), k);
+        if (v) std::copy(f->v_data.begin(), f->v_data.end(), v);
+        return 0;
+    } catch (const wire::WireError& e) {
+        std::snprintf(g_err, sizeof g_err, "%s", e.what());
+        return 1 + static_cast<int>(e.kind());
+    }
 }
 
 } // extern "C"

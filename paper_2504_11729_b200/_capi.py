@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "_lib", "libep_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "ep", "ep_attn.h")
 
-EP_OK, EP_EINVAL, EP_EMASKED, EP_ECUDA, EP_ENCCL, EP_ENOMEM, EP_EUNSUPPORTED = range(7)
+EP_OK, EP_EINVAL, EP_EMASKED, EP_ECUDA, EP_ENCCL, EP_ENOMEM, EP_EUNSUPPORTED, EP_EWIRE = range(8)
 EP_F32, EP_BF16, EP_F64 = 0, 1, 2
 
 
@@ -46,14 +46,31 @@ class Unsupported(EPError, NotImplementedError):
     status = EP_EUNSUPPORTED
 
 
+class WireError(EPError, ValueError):
+    """edgeprompt::wire::WireError (wire.hpp:94-104): a malformed EPKV frame;
+    ``kind`` = WireError::Kind + 1 (see KV_FRAME_KINDS), 6 = not a kv frame."""
+    status = EP_EWIRE
+    kind = 0
+
+
+KV_FRAME_KINDS = ("ok", "bad_magic", "bad_version", "truncated", "length_overflow", "malformed",
+                  "not_kv_frame")
+
 _ERRORS = {cls.status: cls for cls in (InvalidArgument, DomainError, CudaError, NcclError,
-                                       OutOfMemory, Unsupported)}
+                                       OutOfMemory, Unsupported, WireError)}
 
 
 class Segment(C.Structure):
     """ep_segment (KVSegment, cache.hpp:18-28)."""
     _fields_ = [("origin", C.c_int32), ("len", C.c_int32), ("pos_offset", C.c_int64),
                 ("page_off", C.c_int64)]
+
+
+class KVFrameInfo(C.Structure):
+    """ep_kv_frame_info."""
+    _fields_ = [("session_id", C.c_uint32), ("seq_len", C.c_uint32), ("layer", C.c_uint16),
+                ("n_heads", C.c_uint16), ("d_head", C.c_uint16), ("pad", C.c_uint16),
+                ("wire_error", C.c_int32)]
 
 
 class KVPoolDesc(C.Structure):
@@ -106,6 +123,8 @@ _SIGS = {
                                   _vp]),
     "ep_launch_count": (C.c_int64, [_vp]),
     "ep_kv_append": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp, _vp, _vp, _vp]),
+    "ep_kv_ingest_frame": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, _sz, _vp, C.c_int32,
+                                     C.POINTER(KVFrameInfo), _vp]),
 }
 
 _SIGS.update({

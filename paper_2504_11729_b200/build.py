@@ -29,7 +29,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", f"-I{INCL
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
 SOURCES = ["kern_reference.cu", "kern_decode.cu", "kern_verify.cu", "kern_score.cu", "kern_peer.cu",
-           "capi.cpp", "plan.cpp"]
+           "kern_ingest.cu", "capi.cpp", "plan.cpp"]
 HEADERS = ["ep_common.cuh", "ep_internal.h", "umma.cuh", "merge.cuh"]
 
 

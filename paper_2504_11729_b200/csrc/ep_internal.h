@@ -1,6 +1,7 @@
 // ep_internal.h — host-side internals of libep_b200.so (not part of the ABI).
 #pragma once
 
+#include <algorithm>
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
@@ -39,6 +40,7 @@ struct ep_context {
     cudaStream_t stream = nullptr;  // used by the synchronous host-buffer entry points
     ep::DeviceBuffer scratch;       // staging for host-buffer calls
     ep::DeviceBuffer zero_rows;     // 64 zero rows of the widest KV row (page-tail fill)
+    ep::DeviceBuffer ingest_stage;  // pageable kv frames staged for ep_kv_ingest_frame
     std::atomic<int64_t> launches{0};
 };
 

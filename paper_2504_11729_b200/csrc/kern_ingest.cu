@@ -1,0 +1,201 @@
+// kern_ingest.cu — KV ingest: one EPKV kv_frame straight into the page pool
+// (SURVEY §8f rank 2).
+//
+// The reference's edge receives each layer's cloud-prompt KV as a kv frame
+// (wire.hpp:59-75; encode_frame / decode_frame, wire.cpp:70-221), decodes
+// it into two fp64 Matrices and copies them into a KVSegment
+// (segment_from_frame, edge.cpp:61-67). Here the frame's little-endian
+// doubles are read where they lie — device memory, or pinned host memory
+// read in place over the host link — and a single pass decodes, rounds to the
+// pool dtype (f64 -> bf16 / f32, round to nearest even) and scatters token t,
+// head h into page page_table[t / page_tokens], slot t % page_tokens: no fp64
+// staging copy, no separate convert pass. Pageable frames are staged into a
+// per-handle device buffer first.
+//
+// Byte work, bound by the host link (pinned frames) or HBM (device frames):
+// per value 8 B read, 2 B (bf16) or 4 B (fp32) written.
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "ep_common.cuh"
+#include "ep_internal.h"
+
+namespace ep {
+namespace {
+
+// Correctly rounded f64 -> bf16 (RNE): f64 -> f32 rounded to odd (toward
+// zero, sticky bit on inexact), then f32 -> bf16 RNE; the 16 guard bits make
+// the double rounding exact. Same rule as oracle/ep_oracle.c epo_f64_to_bf16.
+__device__ __forceinline__ uint16_t f64_to_bf16(double x) {
+    if (x != x) return 0x7FC0;
+    float f = __double2float_rz(x);
+    if (double(f) != x) f = __uint_as_float(__float_as_uint(f) | 1u);
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+template <bool BF16, bool A16>
+__global__ void __launch_bounds__(256) kv_ingest_kernel(const uint8_t* __restrict__ src,
+                                                        uint32_t n_pairs, uint32_t row_pairs,
+                                                        uint32_t d_pairs, uint32_t P, uint32_t H,
+                                                        const int32_t* __restrict__ page_table,
+                                                        void* __restrict__ kp, void* __restrict__ vp) {
+    constexpr int U = 4;  // pairs in flight per thread
+    const uint32_t total = 2 * n_pairs;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+        double2 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = base + u * stride;
+            if (q < total) {
+                const uint8_t* p = src + size_t(q) * 16;  // K pairs, then V pairs
+                if (A16) {
+                    x[u] = __ldg(reinterpret_cast<const double2*>(p));
+                } else {
+                    x[u].x = __ldg(reinterpret_cast<const double*>(p));
+                    x[u].y = __ldg(reinterpret_cast<const double*>(p + 8));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t q = base + u * stride;
+            if (q >= total) continue;
+            const bool is_v = q >= n_pairs;
+            const uint32_t qq = is_v ? q - n_pairs : q;
+            const uint32_t t = qq / row_pairs, r = qq - t * row_pairs;
+            const uint32_t h = r / d_pairs, cp = r - h * d_pairs;
+            const uint32_t page = uint32_t(page_table[t / P]), slot = t % P;
+            const size_t dst = ((size_t(page) * H + h) * P + slot) * d_pairs + cp;
+            if (BF16) {
+                const uint32_t w = uint32_t(f64_to_bf16(x[u].x)) | (uint32_t(f64_to_bf16(x[u].y)) << 16);
+                static_cast<uint32_t*>(is_v ? vp : kp)[dst] = w;
+            } else {
+                static_cast<float2*>(is_v ? vp : kp)[dst] =
+                    make_float2(__double2float_rn(x[u].x), __double2float_rn(x[u].y));
+            }
+        }
+    }
+}
+
+uint32_t rd_u32(const uint8_t* b) {
+    return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+}
+uint16_t rd_u16(const uint8_t* b) { return uint16_t(b[0] | (b[1] << 8)); }
+
+const char* kWireKind[] = {"ok", "bad_magic", "bad_version", "truncated", "length_overflow", "malformed",
+                           "not a kv frame"};
+
+// decode_header + decode_frame + the kv_frame payload header (wire.cpp:138-221).
+// hdr holds min(24, n) leading bytes of the frame.
+int parse_kv_header(const uint8_t* hdr, size_t n, ep_kv_frame_info* f, std::string* why) {
+    if (n < 10) { *why = "frame header shorter than 10 bytes"; return 3; }
+    if (hdr[0] != 'E' || hdr[1] != 'P' || hdr[2] != 'K' || hdr[3] != 'V') { *why = "frame magic is not EPKV"; return 1; }
+    if (hdr[4] != 0x01) { *why = "unsupported protocol version " + std::to_string(hdr[4]); return 2; }
+    if (hdr[5] > 4) { *why = "unknown message type " + std::to_string(hdr[5]); return 5; }
+    const uint32_t len = rd_u32(hdr + 6);
+    if (len > (1u << 30)) { *why = "declared payload length " + std::to_string(len) + " exceeds limit"; return 4; }
+    if (n != 10 + size_t(len)) {
+        *why = "frame buffer holds " + std::to_string(n) + " bytes, header declares " + std::to_string(10 + size_t(len));
+        return 3;
+    }
+    // the other message types decode (or fail) as decode_payload would
+    // (wire.cpp:165-184, :202-208); a valid one is "not a kv frame"
+    switch (hdr[5]) {
+    case 0: if (len != 20) { *why = len < 20 ? "frame payload truncated" : "session init payload has trailing bytes"; return len < 20 ? 3 : 5; } break;
+    case 1: if (len != 6) { *why = len < 6 ? "frame payload truncated" : "ack payload has trailing bytes"; return len < 6 ? 3 : 5; } break;
+    case 3: if (len != 0) { *why = "end-of-prefill payload must be empty"; return 5; } break;
+    case 4: if (len < 4) { *why = "frame payload truncated"; return 3; } break;
+    default: break;
+    }
+    if (hdr[5] != 2) { *why = "message type " + std::to_string(hdr[5]) + " is not a kv frame"; return 6; }
+    if (len < 14) { *why = "frame payload truncated"; return 3; }
+    const uint8_t* p = hdr + 10;
+    f->session_id = rd_u32(p);
+    f->layer = rd_u16(p + 4);
+    f->seq_len = rd_u32(p + 6);
+    f->n_heads = rd_u16(p + 10);
+    f->d_head = rd_u16(p + 12);
+    const uint64_t vals = uint64_t(f->seq_len) * f->n_heads * f->d_head;
+    if (uint64_t(len) - 14 != 16 * vals) {
+        *why = "kv frame payload length " + std::to_string(len) + " does not match shape (expected " +
+               std::to_string(14 + 16 * vals) + ")";
+        return 5;
+    }
+    return 0;
+}
+
+}  // namespace
+}  // namespace ep
+
+using ep::fail;
+
+extern "C" int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const void* frame,
+                                  size_t frame_bytes, const int32_t* page_table, int32_t n_pages,
+                                  ep_kv_frame_info* info, ep_stream stream) {
+    if (!h || !pool || !frame || !page_table) return fail(EP_EINVAL, "ep_kv_ingest_frame: null argument");
+    if (pool->dtype != EP_F32 && pool->dtype != EP_BF16)
+        return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: pool dtype must be f32 or bf16");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ep_kv_frame_info f{};
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_kv_ingest_frame");
+    cudaPointerAttributes at{};
+    EP_CUDA_TRY(cudaPointerGetAttributes(&at, frame), "ep_kv_ingest_frame pointer attributes");
+    const bool on_device = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+    const bool pinned = at.type == cudaMemoryTypeHost;
+    uint8_t hdr[24] = {};
+    const size_t nh = frame_bytes < 24 ? frame_bytes : 24;
+    if (on_device) {
+        EP_CUDA_TRY(cudaMemcpyAsync(hdr, frame, nh, cudaMemcpyDeviceToHost, s), "ep_kv_ingest_frame header");
+        EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_kv_ingest_frame header");
+    } else {
+        std::memcpy(hdr, frame, nh);
+    }
+    std::string why;
+    const int kind = ep::parse_kv_header(hdr, frame_bytes, &f, &why);
+    f.wire_error = kind;
+    if (info) *info = f;
+    if (kind) return fail(EP_EWIRE, std::string("wire: ") + ep::kWireKind[kind] + ": " + why);
+    if (f.n_heads != pool->n_kv_heads || f.d_head != pool->d_head)
+        return fail(EP_EINVAL, "ep_kv_ingest_frame: kv frame head shape (" + std::to_string(f.n_heads) + " x " +
+                                   std::to_string(f.d_head) + ") does not match the pool");
+    if (f.seq_len == 0) return fail(EP_EINVAL, "ep_kv_ingest_frame: kv frame with empty sequence");
+    const int64_t need = (int64_t(f.seq_len) + pool->page_tokens - 1) / pool->page_tokens;
+    if (n_pages < need)
+        return fail(EP_EINVAL, "ep_kv_ingest_frame: " + std::to_string(f.seq_len) + " tokens need " +
+                                   std::to_string(need) + " pages, got " + std::to_string(n_pages));
+    if (f.d_head % 2) return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: odd d_head");
+    const uint64_t vals = uint64_t(f.seq_len) * f.n_heads * f.d_head;
+    if (vals / 2 > 0x7FFFFFFFull) return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: frame too large");
+    const uint8_t* src;
+    if (on_device) {
+        src = static_cast<const uint8_t*>(frame) + 24;
+    } else if (pinned) {
+        src = static_cast<const uint8_t*>(at.devicePointer ? at.devicePointer : frame) + 24;
+    } else {
+        EP_CUDA_TRY(h->ingest_stage.reserve(16 * vals), "ep_kv_ingest_frame staging");
+        EP_CUDA_TRY(cudaMemcpyAsync(h->ingest_stage.ptr, static_cast<const uint8_t*>(frame) + 24, 16 * vals,
+                                    cudaMemcpyHostToDevice, s),
+                    "ep_kv_ingest_frame staging copy");
+        src = static_cast<const uint8_t*>(h->ingest_stage.ptr);
+    }
+    const uint32_t n_pairs = uint32_t(vals / 2), d_pairs = uint32_t(f.d_head / 2);
+    const uint32_t row_pairs = uint32_t(f.n_heads) * d_pairs;
+    const bool a16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const uint32_t total = 2 * n_pairs;
+    const uint32_t blocks = std::min<uint32_t>((total + 1023) / 1024, uint32_t(h->n_sms) * 8);
+    const uint32_t P = uint32_t(pool->page_tokens), H = uint32_t(f.n_heads);
+#define EP_INGEST(BF, AL)                                                                              \
+    ep::kv_ingest_kernel<BF, AL><<<blocks, 256, 0, s>>>(src, n_pairs, row_pairs, d_pairs, P, H, page_table, \
+                                                       pool->k_pages, pool->v_pages)
+    if (pool->dtype == EP_BF16) {
+        if (a16) EP_INGEST(true, true); else EP_INGEST(true, false);
+    } else {
+        if (a16) EP_INGEST(false, true); else EP_INGEST(false, false);
+    }
+#undef EP_INGEST
+    EP_CUDA_TRY(cudaGetLastError(), "ep_kv_ingest_frame launch");
+    h->launches++;
+    return EP_OK;
+}

@@ -105,6 +105,40 @@ class KVPool:
         self.k[pidx, :, sidx, :] = k.to(self.tdtype)
         self.v[pidx, :, sidx, :] = v.to(self.tdtype)
 
+    def ingest_frame(self, frame, pages, handle: Handle | None = None, stream=None):
+        """Decodes one EPKV kv frame (the reference's encode_frame bytes,
+        wire.cpp:70-136) straight into ``pages`` (ep_kv_ingest_frame): frame
+        token t -> pages[t // page_tokens], slot t % page_tokens, values rounded
+        to the pool dtype. ``frame``: bytes / uint8 numpy (pageable, staged),
+        a pinned uint8 CPU tensor (read in place by the kernel) or a uint8
+        CUDA tensor. Returns the frame info (session_id, layer, seq_len, ...).
+        Raises WireError (``.kind``) for malformed frames like decode_frame."""
+        torch = _torch()
+        handle = handle or default_handle(self.k.device.index or 0)
+        if isinstance(frame, (bytes, bytearray)):
+            frame = np.frombuffer(frame, dtype=np.uint8)
+        if isinstance(frame, np.ndarray):
+            frame = np.ascontiguousarray(frame, dtype=np.uint8)
+            ptr, nbytes = frame.ctypes.data, frame.size
+        else:
+            assert frame.dtype == torch.uint8 and frame.is_contiguous()
+            ptr, nbytes = frame.data_ptr(), frame.numel()
+        if isinstance(pages, torch.Tensor) and pages.is_cuda:
+            pt = pages.to(torch.int32).contiguous()
+        else:
+            pt = torch.as_tensor(np.asarray(pages, dtype=np.int32), device=self.k.device)
+        self._ingest_keep = (frame, pt)
+        info = _capi.KVFrameInfo()
+        pd = self.desc()
+        rc = lib().ep_kv_ingest_frame(handle.ptr, C.byref(pd), ptr, nbytes, pt.data_ptr(),
+                                      int(pt.numel()), C.byref(info), _stream(stream))
+        if rc == _capi.EP_EWIRE:
+            err = _capi.WireError("ep_kv_ingest_frame: " + lib().ep_last_error().decode())
+            err.kind = int(info.wire_error)
+            raise err
+        check(rc, "ep_kv_ingest_frame")
+        return info
+
     def desc(self) -> KVPoolDesc:
         return KVPoolDesc(self.code, self.n_kv_heads, self.d_head, self.page_tokens,
                           self.num_pages, self.k.data_ptr(), self.v.data_ptr())

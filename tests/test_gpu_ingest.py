@@ -1,0 +1,122 @@
+"""GPU parity of the KV ingest (ep_kv_ingest_frame):
+frames written by the reference's own encode_frame (oracle/_ref) are decoded
+into the page pool from pinned host, pageable host and device memory, and
+the pages must equal the C oracle's decode + round + scatter BIT-EXACTLY;
+malformed frames fail with the reference's WireError kind."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not O.available("ref"), reason="oracle/_ref not built")]
+
+
+def _frame(seq, H, d, seed, specials=False):
+    rng = np.random.default_rng(seed)
+    k = rng.uniform(-2, 2, (seq, H, d))
+    v = rng.standard_normal((seq, H, d)) * 3
+    if specials:
+        k[0, 0, :8] = [np.inf, -np.inf, np.nan, 1e300, -1e-300, 2 ** -140 * 1.5, 1 + 2 ** -8, 0.0]
+    return O.kv_frame_encode(17, 2, k, v)
+
+
+def _pool(H, d, dtype, num_pages):
+    from paper_2504_11729_b200.splice import KVPool
+    return KVPool(num_pages, H, d, 64, dtype=dtype)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("where", ["pinned", "pageable", "device"])
+def test_ingest_bit_exact(cuda_handle, dtype, where):
+    import torch
+    seq, H, d = 200, 8, 128
+    fr = _frame(seq, H, d, seed=3, specials=True)
+    num_pages = 7
+    pages = np.array([6, 2, 0, 4], dtype=np.int32)  # scattered, last page partial (200 = 3*64 + 8)
+    pool = _pool(H, d, dtype, num_pages)
+    if where == "pinned":
+        src = torch.from_numpy(fr).pin_memory()
+    elif where == "device":
+        src = torch.from_numpy(fr).cuda()
+    else:
+        src = fr
+    info = pool.ingest_frame(src, pages, handle=cuda_handle)
+    torch.cuda.synchronize()
+    assert (info.seq_len, info.n_heads, info.d_head, info.layer, info.session_id) == (seq, H, d, 2, 17)
+    kv_dt = O.DT_BF16 if dtype == "bf16" else O.DT_F32
+    code, _, want_k, want_v = O.kv_ingest(fr, kv_dt, 64, pages, num_pages)
+    assert code == O.WIRE_OK
+    if dtype == "bf16":
+        got_k = pool.k.view(torch.int16).cpu().numpy().view(np.uint16)
+        got_v = pool.v.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        got_k, got_v = pool.k.cpu().numpy(), pool.v.cpu().numpy()
+    for p in pages:
+        assert np.array_equal(got_k[p].view(np.uint8), want_k[p].view(np.uint8)), p
+        assert np.array_equal(got_v[p].view(np.uint8), want_v[p].view(np.uint8)), p
+
+
+def test_ingest_unaligned_device_frame(cuda_handle):
+    """A device frame at an odd 8-byte offset takes the 8-byte-load path."""
+    import torch
+    fr = _frame(64, 4, 64, seed=4)
+    buf = torch.zeros(fr.size + 8, dtype=torch.uint8, device="cuda")
+    buf[8:].copy_(torch.from_numpy(fr))
+    pool = _pool(4, 64, "bf16", 2)
+    pool.ingest_frame(buf[8:], [1], handle=cuda_handle)
+    _, _, want_k, _ = O.kv_ingest(fr, O.DT_BF16, 64, [1], 2)
+    got = pool.k.view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got[1], want_k[1])
+
+
+def test_ingest_errors_match_reference(cuda_handle):
+    import torch
+    from paper_2504_11729_b200._capi import InvalidArgument, WireError
+    fr = _frame(70, 4, 64, seed=5)
+    pool = _pool(4, 64, "bf16", 2)
+    cases = {}
+    b = fr.copy(); b[0] = ord("Q"); cases["bad_magic"] = b
+    b = fr.copy(); b[4] = 7; cases["bad_version"] = b
+    cases["truncated"] = fr[:-1].copy()
+    b = fr.copy(); b[6:10] = np.frombuffer(np.uint32(0xFFFFFFF0).tobytes(), np.uint8); cases["overflow"] = b
+    b = fr.copy(); b[16] ^= 2; cases["shape"] = b
+    cases["end_of_prefill"] = O.end_of_prefill_frame()
+    for name, b in cases.items():
+        want = O.kv_frame_decode(b, "ref")[0]
+        for src in (b, torch.from_numpy(b).cuda()):
+            with pytest.raises(WireError) as ei:
+                pool.ingest_frame(src, [0, 1], handle=cuda_handle)
+            assert ei.value.kind == want, (name, ei.value.kind, want)
+    with pytest.raises(InvalidArgument):   # head shape does not match the pool (edge.cpp:53-55)
+        _pool(8, 64, "bf16", 2).ingest_frame(fr, [0, 1], handle=cuda_handle)
+    with pytest.raises(InvalidArgument):   # not enough pages
+        pool.ingest_frame(fr, [0], handle=cuda_handle)
+
+
+def test_ingested_kv_attends_like_oracle(cuda_handle):
+    """Cloud KV arriving as a frame, then spliced decode over it (the edge's
+    per-layer flow, edge.cpp:148-164) equals the oracle on the same pages."""
+    import torch
+    from paper_2504_11729_b200.splice import SpliceTable, SplicedAttention
+    from tests.cases import rel_err
+    from tests.gpu_util import torch_from_raw
+    seq, H, Hq, d = 300, 2, 8, 128
+    fr = _frame(seq, H, d, seed=6)
+    pages = np.array([3, 1, 4, 0, 2], dtype=np.int32)
+    pool = _pool(H, d, "bf16", 5)
+    pool.ingest_frame(fr, pages, handle=cuda_handle)
+    table = SpliceTable(1, 64)
+    table.append(0, 0, 0, seq, pages)
+    table.q_pos[0] = seq - 1
+    attn = SplicedAttention(pool, table, Hq, 1, handle=cuda_handle)
+    q_raw = O.fill_uniform(O.DT_BF16, Hq * d, 99).reshape(1, 1, Hq, d)
+    o, lse = attn(torch_from_raw(np.ascontiguousarray(q_raw), O.DT_BF16), o_dtype=torch.float32)
+    _, _, kp, vp = O.kv_ingest(fr, O.DT_BF16, 64, pages, 5)
+    sb = O.HostSpliceBatch(kv_dtype=O.DT_BF16, n_kv_heads=H, n_q_heads=Hq, d_head=d, page_tokens=64,
+                           k_pages=kp, v_pages=vp, seg_indptr=np.array([0, 1], np.int64),
+                           segs=np.array([(0, seq, 0, 0)], dtype=O.SEGMENT_DTYPE), page_table=pages,
+                           q_pos=np.array([seq - 1], np.int64), q_dtype=O.DT_BF16,
+                           q=np.ascontiguousarray(q_raw), n_q=1)
+    want_o, _ = O.spliced_attention(sb)
+    assert rel_err(o.cpu().numpy(), want_o) < 1e-4

@@ -1,0 +1,93 @@
+"""KV ingest: one layer's cloud-prompt KV as an EPKV
+kv frame (the reference's wire format: fp64 LE, K then V) decoded into bf16
+pages, 7B shape: 4096 tokens x 8 KV heads x 128 = 67 MB per frame.
+
+    python tools/ingest_bench.py [--steps 20]
+
+Modes: frame in pinned host memory (read in place by the kernel over the
+host link), in device memory (HBM -> HBM), pageable host memory (staged).
+Reported next to the link roofline measured in the same run (a plain
+pinned -> device copy of the same bytes) and the HBM copy peak."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+SEQ, H, D, P = 4096, 8, 128, 64
+HBM_PEAK_GBS = 6549.1
+
+
+def make_frame(seq=SEQ):
+    import numpy as np
+    vals = seq * H * D
+    hdr = bytearray(b"EPKV\x01\x02")
+    hdr += (14 + 16 * vals).to_bytes(4, "little")
+    hdr += (1).to_bytes(4, "little") + (0).to_bytes(2, "little") + seq.to_bytes(4, "little")
+    hdr += H.to_bytes(2, "little") + D.to_bytes(2, "little")
+    rng = np.random.default_rng(0)
+    body = rng.uniform(-1, 1, 2 * vals).astype("<f8").tobytes()
+    return np.frombuffer(bytes(hdr) + body, dtype=np.uint8)
+
+
+def run(steps=20, warmup=3, h=None):
+    import numpy as np
+    import torch
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splice import KVPool
+    h = h or Handle(0)
+    fr = make_frame()
+    pool = KVPool(SEQ // P, H, D, P, dtype="bf16")
+    pages = torch.arange(SEQ // P, dtype=torch.int32, device="cuda")
+    fr_w = fr.copy()  # writable copy for torch
+    srcs = {"pinned": torch.from_numpy(fr_w).pin_memory(), "device": torch.from_numpy(fr_w).cuda(),
+            "pageable": fr}
+    st = torch.cuda.current_stream()
+    res = {"workload": f"kv frame {SEQ} tokens x {H} kv heads x {D} (fp64 wire, {fr.size / 1e6:.1f} MB) "
+                       "-> bf16 pages", "frame_bytes": int(fr.size)}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for mode, src in srcs.items():
+        for _ in range(warmup):
+            pool.ingest_frame(src, pages, handle=h, stream=st)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(steps):
+            pool.ingest_frame(src, pages, handle=h, stream=st)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        res[mode] = {"ms": ms, "wire_gbs": fr.size / (ms / 1e3) / 1e9}
+    # the host-link roofline of this box: pinned -> device copy of the same bytes
+    dst = torch.empty(fr.size, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        dst.copy_(srcs["pinned"], non_blocking=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(steps):
+        dst.copy_(srcs["pinned"], non_blocking=True)
+    e1.record(st)
+    torch.cuda.synchronize()
+    link = fr.size / (e0.elapsed_time(e1) / steps / 1e3) / 1e9
+    res["h2d_copy_gbs"] = link
+    res["pinned"]["frac_of_h2d_copy"] = res["pinned"]["wire_gbs"] / link
+    dev_bytes = fr.size + fr.size // 4  # read fp64, write bf16
+    res["device"]["hbm_gbs"] = dev_bytes / (res["device"]["ms"] / 1e3) / 1e9
+    res["device"]["frac_of_hbm"] = res["device"]["hbm_gbs"] / HBM_PEAK_GBS
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    torch.cuda.set_device(0)
+    print(json.dumps(run(args.steps)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
