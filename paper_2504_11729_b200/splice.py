@@ -51,25 +51,15 @@ def dtype_code(dtype) -> int:
     raise _capi.Unsupported(f"KV dtype {dtype!r}: expected bf16 or fp32")
 
 
-class KVPool:
-    """Paged K/V pool in HBM for one layer (ep_kv_pool)."""
+class PageAllocator:
+    """Refcounted page ids of a pool (or of several per-layer pools that share
+    one page numbering: a page id then names the same slot in every layer)."""
 
-    def __init__(self, num_pages: int, n_kv_heads: int, d_head: int, page_tokens: int = 64,
-                 dtype="bf16", device: int | None = None, k=None, v=None):
-        torch = _torch()
-        self.code = dtype_code(dtype)
-        self.tdtype = torch.bfloat16 if self.code == _capi.EP_BF16 else torch.float32
-        self.num_pages, self.n_kv_heads, self.d_head = num_pages, n_kv_heads, d_head
-        self.page_tokens = page_tokens
-        shape = (num_pages, n_kv_heads, page_tokens, d_head)
-        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        self.k = k if k is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
-        self.v = v if v is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
-        assert tuple(self.k.shape) == shape and tuple(self.v.shape) == shape
+    def __init__(self, num_pages: int):
+        self.num_pages = num_pages
         self._free = list(range(num_pages - 1, -1, -1))
         self._ref = np.zeros(num_pages, dtype=np.int32)
 
-    # --------------------------------------------------------- allocator --
     def alloc(self, n: int) -> np.ndarray:
         if n > len(self._free):
             raise _capi.OutOfMemory(f"KVPool: {n} pages requested, {len(self._free)} free")
@@ -82,13 +72,53 @@ class KVPool:
 
     def release(self, pages) -> None:
         for p in np.asarray(pages).tolist():
+            if self._ref[p] <= 0:
+                raise InvalidArgument(f"PageAllocator: page {p} released more often than retained")
             self._ref[p] -= 1
             if self._ref[p] == 0:
                 self._free.append(p)
 
+    def refcount(self, page: int) -> int:
+        return int(self._ref[page])
+
     @property
     def free_pages(self) -> int:
         return len(self._free)
+
+
+class KVPool:
+    """Paged K/V pool in HBM for one layer (ep_kv_pool)."""
+
+    def __init__(self, num_pages: int, n_kv_heads: int, d_head: int, page_tokens: int = 64,
+                 dtype="bf16", device: int | None = None, k=None, v=None,
+                 allocator: PageAllocator | None = None):
+        torch = _torch()
+        self.code = dtype_code(dtype)
+        self.tdtype = torch.bfloat16 if self.code == _capi.EP_BF16 else torch.float32
+        self.num_pages, self.n_kv_heads, self.d_head = num_pages, n_kv_heads, d_head
+        self.page_tokens = page_tokens
+        shape = (num_pages, n_kv_heads, page_tokens, d_head)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.k = k if k is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
+        self.v = v if v is not None else torch.zeros(shape, dtype=self.tdtype, device=dev)
+        assert tuple(self.k.shape) == shape and tuple(self.v.shape) == shape
+        if allocator is not None and allocator.num_pages != num_pages:
+            raise InvalidArgument("KVPool: shared allocator has a different page count")
+        self.allocator = allocator or PageAllocator(num_pages)
+
+    # --------------------------------------------------------- allocator --
+    def alloc(self, n: int) -> np.ndarray:
+        return self.allocator.alloc(n)
+
+    def retain(self, pages) -> None:
+        self.allocator.retain(pages)
+
+    def release(self, pages) -> None:
+        self.allocator.release(pages)
+
+    @property
+    def free_pages(self) -> int:
+        return self.allocator.free_pages
 
     # ------------------------------------------------------------ writes --
     def write(self, pages, k, v, start: int = 0) -> None:
