@@ -159,8 +159,10 @@ int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
  * position <= its own (CausalSpan rule, attention.cpp:29-33). Their K/V must
  * already be in the pool as part of the segments. q / o are token-major
  * [sum n_new][n_q_heads][d_head], lse [sum n_new][n_q_heads]; run with
- * ep_spliced_attention. tcgen05 tiles of 128/G query tokens x G heads: bf16
- * KV, d_head 128. o_dtype EP_BF16 uses a bf16 P operand, EP_F32 a hi+lo split. */
+ * ep_spliced_attention. bf16 KV with d_head 128: tcgen05 tiles of 128/G query
+ * tokens x G heads (o_dtype EP_BF16 uses a bf16 P operand, EP_F32 a hi+lo
+ * split). Otherwise (f32 or bf16 KV, d_head 64/128, G <= 8): CUDA-core chunks
+ * of 8/G query tokens on the decode kernel. */
 int ep_plan_create_prefill(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t batch,
                            const int64_t* seg_indptr, const ep_segment* segs,
                            const int32_t* page_table, const int32_t* n_new, ep_plan* out);

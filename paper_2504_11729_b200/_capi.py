@@ -11,6 +11,7 @@ import re
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "_lib", "libep_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "ep", "ep_attn.h")
+HEADERS = [HEADER, os.path.join(os.path.dirname(PKG), "include", "ep", "ep_model.h")]
 
 EP_OK, EP_EINVAL, EP_EMASKED, EP_ECUDA, EP_ENCCL, EP_ENOMEM, EP_EUNSUPPORTED, EP_EWIRE = range(8)
 EP_F32, EP_BF16, EP_F64 = 0, 1, 2
@@ -80,6 +81,13 @@ class KVPoolDesc(C.Structure):
                 ("v_pages", C.c_void_p)]
 
 
+class ModelConfigDesc(C.Structure):
+    """ep_model_config (ModelConfig, model.hpp:15-25, + storage dtype)."""
+    _fields_ = [("n_layers", C.c_int32), ("n_heads", C.c_int32), ("d_model", C.c_int32),
+                ("vocab_size", C.c_int32), ("max_positions", C.c_int32), ("dtype", C.c_int32),
+                ("init_seed", C.c_uint64)]
+
+
 _lib: C.CDLL | None = None
 
 _dp = C.POINTER(C.c_double)
@@ -134,6 +142,19 @@ _SIGS.update({
                                    _vp, _vp, _vp]),
 })
 
+_SIGS.update({
+    "ep_model_create": (C.c_int, [_vp, C.POINTER(ModelConfigDesc), C.c_int32, C.c_int32,
+                                  C.c_int64, C.POINTER(_vp)]),
+    "ep_model_destroy": (C.c_int, [_vp]),
+    "ep_model_weight_sum": (C.c_int, [_vp, C.POINTER(C.c_double)]),
+    "ep_model_kv_pool": (C.c_int, [_vp, C.c_int32, C.POINTER(KVPoolDesc)]),
+    "ep_model_weight": (C.c_int, [_vp, C.c_char_p, C.c_int32, C.POINTER(_vp),
+                                  C.POINTER(C.c_size_t)]),
+    "ep_model_forward": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                   _vp]),
+    "ep_model_last_attention_path": (C.c_int, [_vp]),
+})
+
 # Optional entry points (present when the corresponding kernels are built).
 _OPTIONAL_SIGS: dict = {}
 
@@ -166,7 +187,7 @@ def check(rc: int, where: str = "") -> None:
 
 
 def header_symbols() -> list[str]:
-    """Function names declared in include/ep/ep_attn.h."""
-    text = open(HEADER).read()
+    """Function names declared in include/ep/*.h."""
+    text = "\n".join(open(h).read() for h in HEADERS)
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(ep_[a-z0-9_]+)\s*\(", text)))

@@ -29,13 +29,14 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", f"-I{INCL
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
 SOURCES = ["kern_reference.cu", "kern_decode.cu", "kern_verify.cu", "kern_score.cu", "kern_peer.cu",
-           "kern_ingest.cu", "capi.cpp", "plan.cpp"]
-HEADERS = ["ep_common.cuh", "ep_internal.h", "umma.cuh", "merge.cuh"]
+           "kern_ingest.cu", "kern_model.cu", "capi.cpp", "plan.cpp", "model.cpp"]
+HEADERS = ["ep_common.cuh", "ep_internal.h", "umma.cuh", "merge.cuh", "model_internal.h"]
+PUBLIC_HEADERS = ["ep_attn.h", "ep_model.h"]
 
 
 def _deps(src: str) -> list[str]:
     hdrs = [os.path.join(CSRC, h) for h in HEADERS if os.path.exists(os.path.join(CSRC, h))]
-    return [os.path.join(CSRC, src), os.path.join(INCLUDE, "ep", "ep_attn.h")] + hdrs
+    return [os.path.join(CSRC, src)] + [os.path.join(INCLUDE, "ep", h) for h in PUBLIC_HEADERS] + hdrs
 
 
 def _stale(target: str, deps: list[str]) -> bool:

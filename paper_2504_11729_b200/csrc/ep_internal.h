@@ -112,6 +112,14 @@ struct DecodeArgs {
     int32_t pv_parts;         // K3: P as bf16 hi+lo (2) or bf16 (1)
 };
 
+// Validates request b's segments of a host splice table with the
+// SegmentedCache invariants (cache.cpp:25-53: gapless positions, origin
+// order, pages inside the pool) and appends its page descriptors to out;
+// *first_pages = descriptors of its first segment (plan.cpp).
+int collect_request_pages(int page_tokens, int64_t num_pages, int b, const int64_t* seg_indptr,
+                          const ep_segment* segs, const int32_t* page_table, std::vector<PageDesc>& out,
+                          int64_t* first_pages);
+
 // First q/o token row of (virtual) request b: prefill plans cut one request's
 // queries into chunks that are separate virtual requests.
 __host__ __device__ inline size_t q_row_base(const DecodeArgs& a, int b) {

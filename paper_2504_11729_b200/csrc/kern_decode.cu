@@ -191,10 +191,13 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                 {
                     // the item's R query rows: n_q runs of G consecutive heads
                     const int n = it - it0, slot = n & 1;
+                    // (a prefill chunk's last item may hold fewer than n_q query tokens:
+                    // w.pad = its valid rows; only those are loaded and stored)
                     const uint32_t run = uint32_t(G) * D * qsz;
+                    const int nq = min(a.n_q, (w.pad + G - 1) / G);
                     mbar_wait(&q_empty[slot], ((n >> 1) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&q_full[slot], run * a.n_q);
-                    for (int qi = 0; qi < a.n_q; ++qi)
+                    mbar_arrive_expect_tx(&q_full[slot], run * nq);
+                    for (int qi = 0; qi < nq; ++qi)
                         bulk_g2s(sq + slot * C::Q_BYTES + qi * run,
                                  static_cast<const uint8_t*>(a.q) +
                                      ((q_row_base(a, w.b) + qi) * a.n_q_heads + size_t(w.g) * G) * D * qsz,
@@ -255,10 +258,12 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             for (int rp = 0; rp < R; ++rp) {
                 const int r = rp ^ my_r;
                 const size_t base = size_t(r) * D + l16 * E;
+                const bool live = r < w.pad;  // rows past a short prefill chunk: zero q
 #pragma unroll
                 for (int e = 0; e < E / 2; ++e)
-                    q2[rp][e] = make_float2(load_q(qs, a.q_dtype, base + 2 * e) * a.q_scale,
-                                           load_q(qs, a.q_dtype, base + 2 * e + 1) * a.q_scale);
+                    q2[rp][e] = live ? make_float2(load_q(qs, a.q_dtype, base + 2 * e) * a.q_scale,
+                                                   load_q(qs, a.q_dtype, base + 2 * e + 1) * a.q_scale)
+                                     : make_float2(0.f, 0.f);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&q_empty[slot]);
@@ -412,10 +417,12 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const float val = empty_row ? 0.f : acc / Lsum;
             const float lse2 = empty_row ? -INFINITY : M + fast_log2(Lsum);
             if (direct) {
-                const int qi = r / G, h = w.g * G + r % G;
-                const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
-                store_o(a.o, a.o_dtype, orow * D + c, val);
-                if (c == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+                if (r < w.pad) {
+                    const int qi = r / G, h = w.g * G + r % G;
+                    const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
+                    store_o(a.o, a.o_dtype, orow * D + c, val);
+                    if (c == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+                }
             } else {
                 a.o_part[(size_t(it) * R + r) * D + c] = val;
                 if (c == 0) a.lse_part[size_t(it) * R + r] = lse2;
@@ -430,7 +437,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             named_bar_sync(1, NCW * 32);
             if (*s_flag) {
                 __threadfence();
-                merge_unit_rows<D>(a, u0, n_items, R, R, warp, NCW, [&](int r) {
+                merge_unit_rows<D>(a, u0, n_items, R, w.pad, warp, NCW, [&](int r) {
                     const int qi = r / G, h = w.g * G + r % G;
                     return (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
                 });

@@ -1,0 +1,69 @@
+// model_internal.h — launchers of kern_model.cu (the decoder layer around the
+// spliced attention). Not part of the ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "ep_internal.h"
+
+namespace ep {
+
+// Epilogues of the dense kernel (transformer_layer, model.cpp:161-205).
+enum DenseEpi : int {
+    kEpiStore = 0,  // out = acc                        (unembed_logits)
+    kEpiQKV = 1,    // q -> q_out, k/v -> page slots    (Q/K/V projections + append)
+    kEpiResid = 2,  // out = (resid + acc) [+ bias]     (Wo, W2 + b2)
+    kEpiRelu = 3,   // out = max(acc + bias, 0)         (W1 + b1, ReLU)
+};
+
+// out[r][c] = epi( LN?(x[row_map ? row_map[r] : r]) @ W )[c]; W is n_wblk
+// row-major [K][N / n_wblk] column blocks (wq | wk | wv for kEpiQKV).
+struct DenseArgs {
+    const void* x;
+    const int32_t* row_map;  // gathered input rows (unembedding of the last rows), may be null
+    int32_t n, K, N;
+    const void* w[3];
+    int32_t n_wblk;
+    const void* bias;
+    const void* resid;  // [n][N]
+    void* out;          // [n][N]
+    // kEpiQKV: q rows [n][N/3]; k/v into pages [page][H][P][dh] at (dst_page[r], dst_slot[r])
+    void* q_out;
+    void* k_pages;
+    void* v_pages;
+    int32_t kv_dtype, H, P, dh;
+    const int32_t* dst_page;
+    const int32_t* dst_slot;
+};
+
+// dt: EP_F64 or EP_F32 (x, W, bias, resid, out, q_out share it).
+cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStream_t s);
+
+// embed (model.cpp:104-129): out[r] = embedding[tokens[r]] + sinusoid(pos[r]).
+cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* pos, int n,
+                         int D, void* out, cudaStream_t s);
+
+// Generic paged causal attention: one CTA per (query row, head); row r of
+// request row_req[r] at position row_pos[r] attends to every key of that
+// request's pages (pdesc[req_page_off[b]..]) at a position <= row_pos[r].
+// q/out [n][H][dh] in dt (EP_F64/EP_F32); pages in kv_dtype.
+cudaError_t launch_attention_generic(int dt, int kv_dtype, const void* q, int n, int H, int dh,
+                                     const PageDesc* pdesc, const int64_t* req_page_off,
+                                     const int32_t* row_req, const int32_t* row_pos,
+                                     const void* k_pages, const void* v_pages, int P, void* out,
+                                     cudaStream_t s);
+
+// argmax_token (model.cpp:248-255) per row of logits [rows][V]: the first
+// index of the maximum.
+cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, int32_t* next,
+                               cudaStream_t s);
+
+// dst[i] = uniform(lo, hi) of SplitMix64(seed) draw first + i (fp64 draw,
+// stored in dt = EP_F64 / EP_F32 / EP_BF16).
+cudaError_t launch_fill_uniform_at(int dt, void* dst, size_t n, uint64_t seed, uint64_t first,
+                                   double lo, double hi, cudaStream_t s);
+
+}  // namespace ep

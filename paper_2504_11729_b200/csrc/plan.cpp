@@ -32,6 +32,49 @@
 
 using namespace ep;
 
+namespace ep {
+
+// Validates request b's segments with the SegmentedCache invariants
+// (cache.cpp:25-53: gapless positions, origin order, pages in the pool) and
+// appends its page descriptors; *first_pages = pages of its first segment.
+int collect_request_pages(int page_tokens, int64_t num_pages, int b, const int64_t* seg_indptr,
+                          const ep_segment* segs, const int32_t* page_table, std::vector<PageDesc>& out,
+                          int64_t* first_pages) {
+    const int P = page_tokens;
+    if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
+    int64_t expect_pos = -1;
+    int last_origin = -1;
+    *first_pages = 0;
+    for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
+        const ep_segment& s = segs[si];
+        if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
+            return fail(EP_EINVAL, "ep_plan: negative segment field");
+        if (expect_pos >= 0 && s.pos_offset != expect_pos)
+            return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
+                                       std::to_string(s.pos_offset) + ", previous ends at " +
+                                       std::to_string(expect_pos));
+        if (s.origin < last_origin)
+            return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
+        expect_pos = s.pos_offset + s.len;
+        last_origin = s.origin;
+        const int64_t npg = (int64_t(s.len) + P - 1) / P;
+        for (int64_t i = 0; i < npg; ++i) {
+            const int32_t page = page_table[s.page_off + i];
+            if (page < 0 || page >= num_pages)
+                return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
+            PageDesc d;
+            d.page = page;
+            d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
+            d.pos = s.pos_offset + i * P;
+            out.push_back(d);
+        }
+        if (si == seg_indptr[b]) *first_pages = int64_t(out.size());
+    }
+    return EP_OK;
+}
+
+}  // namespace ep
+
 namespace {
 
 constexpr int kBlockTokens = 64;
@@ -176,42 +219,12 @@ bool cascade_allowed(const ep_plan_s& p) {
     return !off && verify_supported(p.kv_dtype, p.d_head, rpr) && rpr <= 128 && 128 / rpr >= 2;
 }
 
-// Validates request b's segments with the SegmentedCache invariants
-// (cache.cpp:25-53: gapless positions, origin order, pages in the pool) and
-// appends its page descriptors; *first_pages = pages of its first segment.
+// Validates request b's segments with the SegmentedCache invariants and
+// appends its page descriptors (see ep::collect_request_pages).
 int collect_pages(const ep_plan_s& p, int b, const int64_t* seg_indptr, const ep_segment* segs,
                   const int32_t* page_table, std::vector<PageDesc>& out, int64_t* first_pages) {
-    const int P = p.page_tokens;
-    if (seg_indptr[b + 1] < seg_indptr[b]) return fail(EP_EINVAL, "ep_plan: seg_indptr not monotone");
-    int64_t expect_pos = -1;
-    int last_origin = -1;
-    *first_pages = 0;
-    for (int64_t si = seg_indptr[b]; si < seg_indptr[b + 1]; ++si) {
-        const ep_segment& s = segs[si];
-        if (s.len < 0 || s.pos_offset < 0 || s.page_off < 0)
-            return fail(EP_EINVAL, "ep_plan: negative segment field");
-        if (expect_pos >= 0 && s.pos_offset != expect_pos)
-            return fail(EP_EINVAL, "ep_plan: request " + std::to_string(b) + " segment starts at " +
-                                       std::to_string(s.pos_offset) + ", previous ends at " +
-                                       std::to_string(expect_pos));
-        if (s.origin < last_origin)
-            return fail(EP_EINVAL, "ep_plan: origin order must be (cloud, edge, generated)");
-        expect_pos = s.pos_offset + s.len;
-        last_origin = s.origin;
-        const int64_t npg = (int64_t(s.len) + P - 1) / P;
-        for (int64_t i = 0; i < npg; ++i) {
-            const int32_t page = page_table[s.page_off + i];
-            if (page < 0 || page >= p.num_pages)
-                return fail(EP_EINVAL, "ep_plan: page id " + std::to_string(page) + " outside pool");
-            PageDesc d;
-            d.page = page;
-            d.n_tok = int32_t(std::min<int64_t>(P, s.len - i * P));
-            d.pos = s.pos_offset + i * P;
-            out.push_back(d);
-        }
-        if (si == seg_indptr[b]) *first_pages = int64_t(out.size());
-    }
-    return EP_OK;
+    return collect_request_pages(p.page_tokens, p.num_pages, b, seg_indptr, segs, page_table, out,
+                                 first_pages);
 }
 
 int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
@@ -336,9 +349,8 @@ int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const
     p.batch = int32_t(vr.size());
     p.cascade = false;
     p.has_shared.assign(vr.size(), 0);
-    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), kTcItemWeight);
+    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), p.main.tc ? kTcItemWeight : 1);
     p.main.rows = G * C;
-    p.main.tc = true;
     return EP_OK;
 }
 
@@ -543,11 +555,19 @@ int ep_plan_create_prefill(ep_handle h, const ep_kv_pool* pool, int32_t n_q_head
     if (pool->page_tokens <= 0 || pool->page_tokens % kBlockTokens)
         return fail(EP_EUNSUPPORTED, "ep_plan_create_prefill: page_tokens must be a multiple of 64");
     if (batch < 0) return fail(EP_EINVAL, "ep_plan_create_prefill: batch");
+    // tcgen05 tiles (K3) of C = 128/G query tokens x G heads where K3 has an
+    // instance (bf16 KV, d_head 128); otherwise CUDA-core chunks (K1) of
+    // C = 8/G tokens (fp32 / bf16 KV, d_head 64 or 128, G <= 8) — the
+    // reference's own MHA shapes (config 1: fp32, d_head 64).
     const int G = n_q_heads / pool->n_kv_heads;
-    const int C = 128 / G;
-    if (C < 1 || !verify_supported(pool->dtype, pool->d_head, G * C))
-        return fail(EP_EUNSUPPORTED, "ep_plan_create_prefill: tcgen05 prefill tiles need bf16 KV, d_head 128, "
-                                     "group <= 128");
+    const bool tc = G <= 128 && verify_supported(pool->dtype, pool->d_head, 128 / G * G);
+    const bool k1 = !tc && G <= 8 && decode_supported(pool->dtype, pool->d_head, 8 / G * G);
+    if (!tc && !k1)
+        return fail(EP_EUNSUPPORTED, "ep_plan_create_prefill: no prefill kernel for kv dtype " +
+                                         std::to_string(pool->dtype) + ", d_head " + std::to_string(pool->d_head) +
+                                         ", group " + std::to_string(G) +
+                                         " (tcgen05: bf16, d_head 128; CUDA cores: f32/bf16, d_head 64/128, group <= 8)");
+    const int C = tc ? 128 / G : 8 / G;
     std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
     if (!p) return fail(EP_ENOMEM, "ep_plan_create_prefill");
     p->h = h;
@@ -560,6 +580,7 @@ int ep_plan_create_prefill(ep_handle h, const ep_kv_pool* pool, int32_t n_q_head
     p->n_q = C;
     p->rows = G * C;
     p->prefill = true;
+    p->main.tc = tc;
     if (int rc = build_prefill_host(*p, batch, seg_indptr, segs, page_table, n_new)) return rc;
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_plan_create_prefill");
     if (int rc = upload_plan(*p, nullptr, false)) return rc;
