@@ -83,7 +83,22 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
                      const int32_t* page_table, const int32_t* n_new, const int32_t* tokens,
                      void* hidden, void* logits, int32_t* next, ep_stream stream);
 
-/* Which attention kernel the last ep_model_forward used: 1 = spliced decode /
+/* decode_greedy (model.cpp:285-297) resident on the device: for every request
+ * b, the LAST n_steps positions of its splice table (a trailing generated
+ * segment the caller has reserved) are decoded autoregressively — the first
+ * embeds first_tokens[b] (host), each later one the greedy argmax of the
+ * step before (decode_step, model.cpp:257-283). out_tokens (host, [batch]
+ * [n_steps]) receives the argmax after every step; the K/V of every step is
+ * written into its reserved slot. One step (all layers + argmax + a position
+ * advance) is captured into a CUDA graph once and replayed n_steps times:
+ * no host work and no host round trip between steps. Synchronous on return.
+ * EP_EINVAL as ep_model_forward, and for a request with no cached token
+ * before the reserved positions (decode_step's empty-cache error). */
+int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                      const int32_t* page_table, int32_t n_steps, const int32_t* first_tokens,
+                      int32_t* out_tokens, ep_stream stream);
+
+/* Which attention kernel the last ep_model_forward / ep_model_generate used: 1 = spliced decode /
  * prefill plans (K1/K3 of ep_attn.h), 2 = the generic paged kernel (fp64, or
  * d_head outside {64, 128}). */
 int ep_model_last_attention_path(ep_model m);

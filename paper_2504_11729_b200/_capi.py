@@ -152,6 +152,7 @@ _SIGS.update({
                                   C.POINTER(C.c_size_t)]),
     "ep_model_forward": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp]),
+    "ep_model_generate": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, C.c_int32, _vp, _vp, _vp]),
     "ep_model_last_attention_path": (C.c_int, [_vp]),
 })
 

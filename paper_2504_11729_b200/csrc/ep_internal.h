@@ -120,6 +120,10 @@ int collect_request_pages(int page_tokens, int64_t num_pages, int b, const int64
                           const ep_segment* segs, const int32_t* page_table, std::vector<PageDesc>& out,
                           int64_t* first_pages);
 
+// Device copy of a plan's per-request query positions (a device-resident
+// rollout advances them in place, one token per step).
+int64_t* plan_qpos_dev(ep_plan p);
+
 // First q/o token row of (virtual) request b: prefill plans cut one request's
 // queries into chunks that are separate virtual requests.
 __host__ __device__ inline size_t q_row_base(const DecodeArgs& a, int b) {

@@ -11,14 +11,23 @@
 //
 // The tiny reference models (d_model 8..256) are launch- and L2-latency
 // bound, not HBM or tensor bound: weights of config 1 are 6.6 MB (fp32) and
-// stay in L2 across steps. The dense kernel therefore favours few launches and
-// coalesced weight streaming over tensor cores: a CTA owns 64 output columns
-// of MR rows, its 256 threads split K four ways, every weight element read
-// once per CTA is used for MR FMAs, and the LayerNorm of the input rows is
-// computed in the prologue (the reference's two-pass mean / variance).
+// stay in L2 across steps. Two dense kernels, both with the LayerNorm of the
+// input rows in the prologue (the reference's two-pass mean / variance) and
+// the layer's elementwise work in the epilogue:
+//   * widths % 4 == 0 (every reference shape of interest): a split-K GEMV on
+//     a thread-block cluster per 8-row block — CS CTAs of one cluster take
+//     K/CS rows each, every thread keeps 8+ independent 16-byte weight loads
+//     in flight, and the cluster's partial tiles are summed in rank order
+//     through distributed shared memory by rank 0 (deterministic, no
+//     atomics, no second launch); weights are re-read from L2 per row block;
+//   * other shapes: a CTA owns 64 output columns of MR rows, its 256 threads
+//     split K four ways, every weight element read once per CTA is used for
+//     MR FMAs.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "ep_common.cuh"
@@ -33,6 +42,9 @@ constexpr int kBN = 64;                      // output columns per CTA
 constexpr int kKS = kDenseThreads / kBN;     // K slices
 constexpr int kKC = 128;                     // K chunk staged in smem
 constexpr double kLayerNormEps = 1e-5;       // model.cpp:14
+constexpr int kGvCols = 64;                  // output columns per CTA (16 threads x 4)
+constexpr int kGvKS = kDenseThreads / 16;    // k-slices per CTA
+constexpr int kGvRows = 8;                   // rows (decode batch) per CTA
 
 template <typename T>
 __device__ __forceinline__ T ld(const void* p, size_t i) {
@@ -68,8 +80,8 @@ __device__ __forceinline__ void dense_epilogue(const DenseArgs& a, int row, int 
             static_cast<T*>(a.q_out)[size_t(row) * D + cc] = v;
         } else {
             const int h = cc / a.dh, e = cc - h * a.dh;
-            const size_t idx =
-                ((size_t(a.dst_page[row]) * a.H + h) * a.P + a.dst_slot[row]) * a.dh + e;
+            const size_t r = (a.step ? size_t(*a.step) * a.n : 0) + row;  // rollout step rows
+            const size_t idx = ((size_t(a.dst_page[r]) * a.H + h) * a.P + a.dst_slot[r]) * a.dh + e;
             store_kv<T>(which == 1 ? a.k_pages : a.v_pages, a.kv_dtype, idx, v);
         }
     }
@@ -194,9 +206,18 @@ cudaError_t launch_dense_t(const DenseArgs& a, cudaStream_t s) {
 }
 
 template <typename T, int EPI, bool LN>
+cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s);
+
+template <typename T, int EPI, bool LN>
 cudaError_t dispatch_rows(const DenseArgs& a, cudaStream_t s) {
-    // decode (a few rows): every CTA streams its weight columns once for up
-    // to 8 rows; prefill: 32 rows per weight element read.
+    // the cluster split-K GEMV (8-row blocks) wherever 16-byte weight loads
+    // are aligned (every column block a multiple of 4 wide, 16-byte bases);
+    // else the scalar kernel: every CTA streams its weight columns once for up
+    // to 8 rows (decode) or 32 rows (prefill).
+    const int nb = a.N / a.n_wblk;
+    bool aligned = nb % 4 == 0;
+    for (int i = 0; i < a.n_wblk; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(a.w[i]) % 16 == 0;
+    if (aligned) return launch_gemv_t<T, EPI, LN>(a, s);
     if (a.n <= 8) return launch_dense_t<T, 8, EPI, LN>(a, s);
     return launch_dense_t<T, 32, EPI, LN>(a, s);
 }
@@ -212,13 +233,167 @@ cudaError_t dispatch_epi(int epi, bool ln, const DenseArgs& a, cudaStream_t s) {
     }
 }
 
-// ------------------------------------------------------------------ embed --
+// ------------------------------------------------------ cluster split-K GEMV --
+
 
 template <typename T>
-__global__ void embed_kernel(const T* emb, const int32_t* tokens, const int32_t* pos, int D, T* out) {
-    const int r = blockIdx.x;
-    const T* e = emb + size_t(tokens[r]) * D;
-    const double p = double(pos[r]);
+struct Vec4 {
+    T x, y, z, w;
+};
+
+template <typename T>
+__device__ __forceinline__ Vec4<T> ld4(const T* p) {
+    if constexpr (sizeof(T) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        return {v.x, v.y, v.z, v.w};
+    } else {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        return {a.x, a.y, b.x, b.y};
+    }
+}
+
+// smem: A slice [kGvRows][KR] | k-slice partials [kGvKS][kGvRows][kGvCols]
+//       | cluster partial [kGvRows][kGvCols]
+template <typename T, int EPI, bool LN>
+__global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const DenseArgs a, int KR) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int crank = int(cluster.block_rank()), csize = int(cluster.num_blocks());
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* As = reinterpret_cast<T*>(smem_raw);
+    T* red = As + kGvRows * KR;
+    T* part = red + kGvKS * kGvRows * kGvCols;
+    __shared__ T s_mean[kGvRows], s_inv[kGvRows];
+    __shared__ int s_row[kGvRows];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row0 = blockIdx.z * kGvRows;
+    const int nr = min(kGvRows, a.n - row0);
+    const int k0 = crank * KR, kr = max(0, min(KR, a.K - k0));
+    const T* X = static_cast<const T*>(a.x);
+    if (tid < kGvRows)
+        s_row[tid] = tid < nr ? (a.row_map ? a.row_map[row0 + tid] : row0 + tid) : 0;
+    __syncthreads();
+    if constexpr (LN) {
+        for (int r = warp; r < nr; r += kDenseThreads / 32) {
+            const T* xr = X + size_t(s_row[r]) * a.K;
+            T sm = 0;
+            for (int c = lane; c < a.K; c += 32) sm += xr[c];
+            sm = warp_sum(sm);
+            const T mean = sm / T(a.K);
+            T q = 0;
+            for (int c = lane; c < a.K; c += 32) {
+                const T dx = xr[c] - mean;
+                q += dx * dx;
+            }
+            q = warp_sum(q);
+            if (lane == 0) {
+                s_mean[r] = mean;
+                s_inv[r] = T(1) / sqrt(q / T(a.K) + T(kLayerNormEps));
+            }
+        }
+        __syncthreads();
+    }
+    for (int i = tid; i < kGvRows * KR; i += kDenseThreads) {
+        const int r = i / KR, kk = i - r * KR;
+        T v = T(0);
+        if (r < nr && kk < kr) {
+            v = X[size_t(s_row[r]) * a.K + k0 + kk];
+            if constexpr (LN) v = (v - s_mean[r]) * s_inv[r];
+        }
+        As[i] = v;
+    }
+    __syncthreads();
+
+    const int cg4 = tid % 16, ks = tid / 16;
+    const int col0 = blockIdx.x * kGvCols + cg4 * 4;
+    const bool cvalid = col0 < a.N;  // N % 4 == 0 and block width % 4 == 0
+    T acc[kGvRows][4];
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = T(0);
+    if (cvalid) {
+        const int nb = a.N / a.n_wblk, blk = col0 / nb;
+        const T* wp = static_cast<const T*>(a.w[blk]) + (col0 - blk * nb) + size_t(k0) * nb;
+        const int per = (kr + kGvKS - 1) / kGvKS;
+        const int kb = ks * per, ke = min(kr, kb + per);
+#pragma unroll 8
+        for (int kk = kb; kk < ke; ++kk) {
+            const Vec4<T> w = ld4(wp + size_t(kk) * nb);
+#pragma unroll
+            for (int r = 0; r < kGvRows; ++r) {
+                const T x = As[r * KR + kk];
+                acc[r][0] += x * w.x;
+                acc[r][1] += x * w.y;
+                acc[r][2] += x * w.z;
+                acc[r][3] += x * w.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kGvRows; ++r)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) red[(ks * kGvRows + r) * kGvCols + cg4 * 4 + e] = acc[r][e];
+    __syncthreads();
+    // k-slices summed in order -> this CTA's partial tile
+    for (int i = tid; i < kGvRows * kGvCols; i += kDenseThreads) {
+        T v = T(0);
+#pragma unroll 4
+        for (int k = 0; k < kGvKS; ++k) v += red[k * kGvRows * kGvCols + i];
+        part[i] = v;
+    }
+    cluster.sync();
+    if (crank == 0) {
+        for (int i = tid; i < nr * kGvCols; i += kDenseThreads) {
+            const int r = i / kGvCols, c = blockIdx.x * kGvCols + (i % kGvCols);
+            if (c >= a.N) continue;
+            T v = part[i];
+            for (int q = 1; q < csize; ++q) v += cluster.map_shared_rank(part, q)[i];
+            dense_epilogue<T, EPI>(a, row0 + r, c, v);
+        }
+    }
+    cluster.sync();  // peers' partials stay mapped until rank 0 has read them
+}
+
+template <typename T, int EPI, bool LN>
+cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s) {
+    // ~128 K-rows per CTA, at most 8 CTAs (the portable cluster size)
+    int cs = std::min(8, std::max(1, (a.K + 127) / 128));
+    const int KR = (((a.K + cs - 1) / cs) + 15) / 16 * 16;
+    cs = (a.K + KR - 1) / KR;
+    const size_t smem = sizeof(T) * (size_t(kGvRows) * KR + size_t(kGvKS + 1) * kGvRows * kGvCols);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(gemv_cluster_kernel<T, EPI, LN>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((a.N + kGvCols - 1) / kGvCols, cs, (a.n + kGvRows - 1) / kGvRows);
+    cfg.blockDim = dim3(kDenseThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = cs;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemv_cluster_kernel<T, EPI, LN>, a, KR);
+}
+
+// ------------------------------------------------------------------ embed --
+
+// With a rollout step counter, step 0 embeds tokens[r] and step s > 0 the
+// previous step's greedy token prev[(s - 1) * n + r]; positions are pos[s * n + r].
+template <typename T>
+__global__ void embed_kernel(const T* emb, const int32_t* tokens, const int32_t* prev,
+                             const int32_t* step, const int32_t* pos, int D, T* out) {
+    const int r = blockIdx.x, n = gridDim.x;
+    const int st = step ? *step : 0;
+    const int tok = st == 0 ? tokens[r] : prev[size_t(st - 1) * n + r];
+    const T* e = emb + size_t(tok) * D;
+    const double p = double(pos[size_t(st) * n + r]);
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
         // model.cpp:121-126: pair = c - c % 2, freq = 10000^(-pair / d)
         const int pair = c - (c % 2);
@@ -258,7 +433,8 @@ template <typename T, typename KV>
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attention_generic_kernel(const T* q, int H, int dh, const PageDesc* pdesc,
                              const int64_t* req_page_off, const int32_t* row_req,
-                             const int32_t* row_pos, const KV* kp, const KV* vp, int P, T* out) {
+                             const int32_t* row_pos, const int32_t* step, const KV* kp,
+                             const KV* vp, int P, T* out) {
     const int r = blockIdx.x, h = blockIdx.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -271,7 +447,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     __syncthreads();
 
     const T scale = T(1) / sqrt(T(dh));
-    const int64_t qpos = row_pos[r];
+    const int64_t qpos = row_pos[(step ? size_t(*step) * gridDim.x : 0) + r];
     const int b = row_req[r];
     const int64_t p0 = req_page_off[b], np = req_page_off[b + 1] - p0;
 
@@ -346,11 +522,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 template <typename T, typename KV>
 cudaError_t launch_attn_t(const void* q, int n, int H, int dh, const PageDesc* pdesc,
                           const int64_t* req_page_off, const int32_t* row_req,
-                          const int32_t* row_pos, const void* kp, const void* vp, int P,
-                          void* out, cudaStream_t s) {
+                          const int32_t* row_pos, const int32_t* step, const void* kp,
+                          const void* vp, int P, void* out, cudaStream_t s) {
     const size_t smem = sizeof(T) * size_t(dh) * (1 + kAttnWarps);
     attention_generic_kernel<T, KV><<<dim3(n, H), kAttnWarps * 32, smem, s>>>(
-        static_cast<const T*>(q), H, dh, pdesc, req_page_off, row_req, row_pos,
+        static_cast<const T*>(q), H, dh, pdesc, req_page_off, row_req, row_pos, step,
         static_cast<const KV*>(kp), static_cast<const KV*>(vp), P, static_cast<T*>(out));
     return cudaGetLastError();
 }
@@ -359,8 +535,9 @@ cudaError_t launch_attn_t(const void* q, int n, int H, int dh, const PageDesc* p
 
 // argmax_token (model.cpp:248-255): first index of the maximum (strict >).
 template <typename T>
-__global__ void argmax_rows_kernel(const T* logits, int V, int32_t* next) {
+__global__ void argmax_rows_kernel(const T* logits, int V, const int32_t* step, int32_t* next) {
     const int r = blockIdx.x, tid = threadIdx.x;
+    if (step) next += size_t(*step) * gridDim.x;  // rollout: row block of this step
     const T* x = logits + size_t(r) * V;
     T bv = T(-INFINITY);
     int bi = V;
@@ -422,47 +599,65 @@ cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStrea
     return dt == EP_F64 ? dispatch_epi<double>(epi, ln, a, s) : dispatch_epi<float>(epi, ln, a, s);
 }
 
-cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* pos, int n,
-                         int D, void* out, cudaStream_t s) {
+cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* prev,
+                         const int32_t* step, const int32_t* pos, int n, int D, void* out,
+                         cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int threads = D >= 256 ? 256 : ((D + 31) / 32) * 32;
     if (dt == EP_F64)
-        embed_kernel<double><<<n, threads, 0, s>>>(static_cast<const double*>(emb), tokens, pos, D,
-                                                   static_cast<double*>(out));
+        embed_kernel<double><<<n, threads, 0, s>>>(static_cast<const double*>(emb), tokens, prev,
+                                                   step, pos, D, static_cast<double*>(out));
     else
-        embed_kernel<float><<<n, threads, 0, s>>>(static_cast<const float*>(emb), tokens, pos, D,
-                                                  static_cast<float*>(out));
+        embed_kernel<float><<<n, threads, 0, s>>>(static_cast<const float*>(emb), tokens, prev,
+                                                  step, pos, D, static_cast<float*>(out));
     return cudaGetLastError();
 }
 
 cudaError_t launch_attention_generic(int dt, int kv_dtype, const void* q, int n, int H, int dh,
                                      const PageDesc* pdesc, const int64_t* req_page_off,
                                      const int32_t* row_req, const int32_t* row_pos,
-                                     const void* k_pages, const void* v_pages, int P, void* out,
-                                     cudaStream_t s) {
+                                     const int32_t* step, const void* k_pages,
+                                     const void* v_pages, int P, void* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     if (dh > 32 * kMaxDhPerLane) return cudaErrorInvalidValue;
     if (dt == EP_F64) {
         if (kv_dtype != EP_F64) return cudaErrorInvalidValue;
         return launch_attn_t<double, double>(q, n, H, dh, pdesc, req_page_off, row_req, row_pos,
-                                             k_pages, v_pages, P, out, s);
+                                             step, k_pages, v_pages, P, out, s);
     }
     if (kv_dtype == EP_F32)
         return launch_attn_t<float, float>(q, n, H, dh, pdesc, req_page_off, row_req, row_pos,
-                                           k_pages, v_pages, P, out, s);
+                                           step, k_pages, v_pages, P, out, s);
     if (kv_dtype == EP_BF16)
         return launch_attn_t<float, __nv_bfloat16>(q, n, H, dh, pdesc, req_page_off, row_req,
-                                                   row_pos, k_pages, v_pages, P, out, s);
+                                                   row_pos, step, k_pages, v_pages, P, out, s);
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, int32_t* next,
-                               cudaStream_t s) {
+cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, const int32_t* step,
+                               int32_t* next, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
     if (dt == EP_F64)
-        argmax_rows_kernel<double><<<rows, 256, 0, s>>>(static_cast<const double*>(logits), V, next);
+        argmax_rows_kernel<double><<<rows, 256, 0, s>>>(static_cast<const double*>(logits), V, step,
+                                                        next);
     else
-        argmax_rows_kernel<float><<<rows, 256, 0, s>>>(static_cast<const float*>(logits), V, next);
+        argmax_rows_kernel<float><<<rows, 256, 0, s>>>(static_cast<const float*>(logits), V, step,
+                                                       next);
+    return cudaGetLastError();
+}
+
+namespace {
+// End of one rollout step: step += 1 and every request's query position
+// (the decode plan's q_pos, read by K1/K3) moves to the next token.
+__global__ void advance_kernel(int32_t* step, int64_t* q_pos, int batch) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) *step += 1;
+    if (q_pos && i < batch) q_pos[i] += 1;
+}
+}  // namespace
+
+cudaError_t launch_advance(int32_t* step, int64_t* q_pos, int batch, cudaStream_t s) {
+    advance_kernel<<<(batch + 255) / 256, 256, 0, s>>>(step, q_pos, batch);
     return cudaGetLastError();
 }
 

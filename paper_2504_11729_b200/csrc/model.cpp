@@ -6,8 +6,9 @@
 // transformer_layer -> unembed_logits -> argmax_token, with the attention of
 // each layer as one partial_attention per cached segment (+ the new tokens)
 // fused by merge_partials. Here:
-//   * weights live in one device allocation in generation order, so
-//     init_model is a single SplitMix64 fill (draw i -> element i);
+//   * weights live in one device allocation in generation order, each tensor
+//     256-byte aligned and filled from its own range of the one SplitMix64
+//     stream (init_model's draw order);
 //   * every layer has a KV page pool with the same page numbering, so one
 //     host splice table addresses all layers;
 //   * a forward pass is a fixed launch sequence per layer — QKV (LN fused,
@@ -81,11 +82,20 @@ namespace {
 
 size_t kv_elem_bytes(int kv) { return kv == EP_F64 ? 8 : kv == EP_F32 ? 4 : 2; }
 
-// Host-side row metadata of one forward, uploaded in one copy.
+// Host-side row metadata of one forward (or rollout), uploaded in one copy.
 struct Meta {
-    std::vector<int32_t> tokens, pos, dst_page, dst_slot, row_req, last_row;
+    std::vector<int32_t> tokens, pos, dst_page, dst_slot, row_req, last_row, step;
     std::vector<int64_t> req_page_off, q_pos;
     std::vector<PageDesc> pdesc;
+};
+
+// One request of a forward: its validated page descriptors and the page
+// slots of its last nn positions (the new tokens).
+struct Req {
+    std::vector<PageDesc> pages;
+    int64_t start = 0, end = 0;
+    int nn = 0;
+    std::vector<std::pair<int32_t, int32_t>> slots;
 };
 
 template <typename T>
@@ -94,6 +104,211 @@ size_t append_bytes(std::vector<char>& blob, const std::vector<T>& v) {
     blob.resize(off + v.size() * sizeof(T));
     if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
     return off;
+}
+
+}  // namespace
+
+namespace {
+
+bool uses_plans(ep_model m) {
+    return m->dt == EP_F32 && (m->dh == 64 || m->dh == 128) && m->P % 64 == 0;
+}
+
+// Validates every request's splice table (SegmentedCache invariants via
+// collect_request_pages) and locates the page slot of each new position.
+int collect_requests(ep_model m, int batch, const int64_t* seg_indptr, const ep_segment* segs,
+                     const int32_t* page_table, const int32_t* n_new, std::vector<Req>& reqs, bool* all_decode) {
+    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_model: seg_indptr[0] must be 0");
+    reqs.assign(batch, Req{});
+    *all_decode = true;
+    for (int b = 0; b < batch; ++b) {
+        Req& r = reqs[b];
+        int64_t first = 0;
+        if (int rc = collect_request_pages(m->P, m->num_pages, b, seg_indptr, segs, page_table, r.pages, &first))
+            return rc;
+        r.start = r.pages.empty() ? 0 : r.pages.front().pos;
+        r.end = r.pages.empty() ? 0 : r.pages.back().pos + r.pages.back().n_tok;
+        r.nn = n_new[b];
+        if (r.nn <= 0 || r.nn > r.end - r.start)
+            return fail(EP_EINVAL, "ep_model: request " + std::to_string(b) + " has " +
+                                       std::to_string(r.end - r.start) + " tokens, n_new = " + std::to_string(r.nn));
+        if (r.end > m->cfg.max_positions)  // embed's std::out_of_range (model.cpp:107-112)
+            return fail(EP_EINVAL, "embed: positions " + std::to_string(r.end - r.nn) + ".." +
+                                       std::to_string(r.end) + " overflow max_positions " +
+                                       std::to_string(m->cfg.max_positions));
+        *all_decode = *all_decode && r.nn == 1;
+        // new positions [end - nn, end): walk the descriptors from the back
+        r.slots.resize(r.nn);
+        size_t di = r.pages.size();
+        for (int64_t p = r.end - 1; p >= r.end - r.nn; --p) {
+            while (di > 0 && r.pages[di - 1].pos > p) --di;
+            const PageDesc& d = r.pages[di - 1];
+            r.slots[p - (r.end - r.nn)] = {d.page, int32_t(p - d.pos)};
+        }
+    }
+    return EP_OK;
+}
+
+int reserve_ws(ep_model m, int n, int batch) {
+    const size_t es = m->esz();
+    EP_CUDA_TRY(m->hid.reserve(size_t(n) * m->D * es), "ep_model ws");
+    EP_CUDA_TRY(m->xbuf.reserve(size_t(n) * m->D * es), "ep_model ws");
+    EP_CUDA_TRY(m->qbuf.reserve(size_t(n) * m->D * es), "ep_model ws");
+    EP_CUDA_TRY(m->attn.reserve(size_t(n) * m->D * es), "ep_model ws");
+    EP_CUDA_TRY(m->h1.reserve(size_t(n) * m->F * es), "ep_model ws");
+    EP_CUDA_TRY(m->logits_ws.reserve(size_t(batch) * m->V * es), "ep_model ws");
+    EP_CUDA_TRY(m->next_ws.reserve(size_t(batch) * sizeof(int32_t)), "ep_model ws");
+    return EP_OK;
+}
+
+// forward declaration (defined below)
+struct Pass;
+int upload_meta(ep_model m, const Meta& md, Pass& ps, cudaStream_t s);
+
+// One forward pass over n token rows of `batch` requests (device metadata
+// already uploaded). step != null: a rollout step — row metadata is indexed
+// by the device step counter and the step's tokens come from the previous
+// step's argmax (see ep_model_generate).
+struct Pass {
+    int n = 0, batch = 0;
+    const int32_t *tok = nullptr, *prev = nullptr, *step = nullptr, *pos = nullptr;
+    const int32_t *dst_page = nullptr, *dst_slot = nullptr, *row_req = nullptr, *last_row = nullptr;
+    const int64_t* req_page_off = nullptr;
+    const PageDesc* pdesc = nullptr;
+    ep_plan plan = nullptr;
+    void* logits = nullptr;
+    int32_t* next = nullptr;
+};
+
+// Metadata upload: one pinned staging buffer, one async copy; fills the
+// device pointers of ps.
+int upload_meta(ep_model m, const Meta& md, Pass& ps, cudaStream_t s) {
+    std::vector<char> blob;
+    const size_t o_tok = append_bytes(blob, md.tokens), o_pos = append_bytes(blob, md.pos),
+                 o_pg = append_bytes(blob, md.dst_page), o_sl = append_bytes(blob, md.dst_slot),
+                 o_rq = append_bytes(blob, md.row_req), o_last = append_bytes(blob, md.last_row),
+                 o_rpo = append_bytes(blob, md.req_page_off), o_pd = append_bytes(blob, md.pdesc),
+                 o_st = append_bytes(blob, md.step);
+    EP_CUDA_TRY(m->meta.reserve(blob.size()), "ep_model meta");
+    EP_CUDA_TRY(cudaEventSynchronize(m->staged), "ep_model staging");
+    if (blob.size() > m->stage_bytes) {
+        if (m->stage) cudaFreeHost(m->stage);
+        m->stage = nullptr;
+        EP_CUDA_TRY(cudaMallocHost(&m->stage, blob.size()), "ep_model pinned");
+        m->stage_bytes = blob.size();
+    }
+    std::memcpy(m->stage, blob.data(), blob.size());
+    EP_CUDA_TRY(cudaMemcpyAsync(m->meta.ptr, m->stage, blob.size(), cudaMemcpyHostToDevice, s), "ep_model meta copy");
+    EP_CUDA_TRY(cudaEventRecord(m->staged, s), "ep_model event");
+    char* mb = static_cast<char*>(m->meta.ptr);
+    ps.tok = reinterpret_cast<const int32_t*>(mb + o_tok);
+    ps.pos = reinterpret_cast<const int32_t*>(mb + o_pos);
+    ps.dst_page = reinterpret_cast<const int32_t*>(mb + o_pg);
+    ps.dst_slot = reinterpret_cast<const int32_t*>(mb + o_sl);
+    ps.row_req = reinterpret_cast<const int32_t*>(mb + o_rq);
+    ps.last_row = reinterpret_cast<const int32_t*>(mb + o_last);
+    ps.req_page_off = reinterpret_cast<const int64_t*>(mb + o_rpo);
+    ps.pdesc = reinterpret_cast<const PageDesc*>(mb + o_pd);
+    ps.step = md.step.empty() ? nullptr : reinterpret_cast<const int32_t*>(mb + o_st);
+    return EP_OK;
+}
+
+int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
+    ep_handle h = m->h;
+    const int dt = m->dt, n = ps.n;
+    EP_CUDA_TRY(launch_embed(dt, m->wptr(0), ps.tok, ps.prev, ps.step, ps.pos, n, m->D, m->hid.ptr, s),
+                "embed launch");
+    h->launches++;
+    for (int l = 0; l < m->L; ++l) {
+        const LayerOffsets& o = m->lw[l];
+        const ep_kv_pool pool = m->pool(l);
+        // LN -> Q | K | V; K/V rows scattered into their page slots
+        DenseArgs a{};
+        a.x = m->hid.ptr;
+        a.n = n;
+        a.K = m->D;
+        a.N = 3 * m->D;
+        a.w[0] = m->wptr(o.wq);
+        a.w[1] = m->wptr(o.wk);
+        a.w[2] = m->wptr(o.wv);
+        a.n_wblk = 3;
+        a.q_out = m->qbuf.ptr;
+        a.k_pages = pool.k_pages;
+        a.v_pages = pool.v_pages;
+        a.kv_dtype = m->kv_dtype;
+        a.H = m->H;
+        a.P = m->P;
+        a.dh = m->dh;
+        a.dst_page = ps.dst_page;
+        a.dst_slot = ps.dst_slot;
+        a.step = ps.step;
+        EP_CUDA_TRY(launch_dense(dt, kEpiQKV, true, a, s), "qkv launch");
+        h->launches++;
+        // spliced causal attention over the request's pages
+        if (ps.plan) {
+            if (int rc = ep_spliced_attention(h, ps.plan, &pool, EP_F32, m->qbuf.ptr, EP_F32, m->attn.ptr,
+                                              nullptr, s))
+                return rc;
+        } else {
+            EP_CUDA_TRY(launch_attention_generic(dt, m->kv_dtype, m->qbuf.ptr, n, m->H, m->dh, ps.pdesc,
+                                                 ps.req_page_off, ps.row_req, ps.pos, ps.step, pool.k_pages,
+                                                 pool.v_pages, m->P, m->attn.ptr, s),
+                        "attention launch");
+            h->launches++;
+        }
+        // x = hidden + attn @ Wo
+        DenseArgs b{};
+        b.x = m->attn.ptr;
+        b.n = n;
+        b.K = m->D;
+        b.N = m->D;
+        b.w[0] = m->wptr(o.wo);
+        b.n_wblk = 1;
+        b.resid = m->hid.ptr;
+        b.out = m->xbuf.ptr;
+        EP_CUDA_TRY(launch_dense(dt, kEpiResid, false, b, s), "wo launch");
+        h->launches++;
+        // h1 = relu(LN(x) @ W1 + b1)
+        DenseArgs c{};
+        c.x = m->xbuf.ptr;
+        c.n = n;
+        c.K = m->D;
+        c.N = m->F;
+        c.w[0] = m->wptr(o.w1);
+        c.n_wblk = 1;
+        c.bias = m->wptr(o.b1);
+        c.out = m->h1.ptr;
+        EP_CUDA_TRY(launch_dense(dt, kEpiRelu, true, c, s), "w1 launch");
+        h->launches++;
+        // hidden = x + h1 @ W2 + b2
+        DenseArgs d{};
+        d.x = m->h1.ptr;
+        d.n = n;
+        d.K = m->F;
+        d.N = m->D;
+        d.w[0] = m->wptr(o.w2);
+        d.n_wblk = 1;
+        d.bias = m->wptr(o.b2);
+        d.resid = m->xbuf.ptr;
+        d.out = m->hid.ptr;
+        EP_CUDA_TRY(launch_dense(dt, kEpiResid, false, d, s), "w2 launch");
+        h->launches++;
+    }
+    // unembed_logits of each request's last row (model.cpp:238-246) + argmax
+    DenseArgs u{};
+    u.x = m->hid.ptr;
+    u.row_map = ps.last_row;
+    u.n = ps.batch;
+    u.K = m->D;
+    u.N = m->V;
+    u.w[0] = m->wptr(m->off_unembed);
+    u.n_wblk = 1;
+    u.out = ps.logits;
+    EP_CUDA_TRY(launch_dense(dt, kEpiStore, true, u, s), "unembed launch");
+    h->launches++;
+    EP_CUDA_TRY(launch_argmax_rows(dt, ps.logits, ps.batch, m->V, ps.step, ps.next, s), "argmax launch");
+    h->launches++;
+    return EP_OK;
 }
 
 }  // namespace
@@ -134,29 +349,45 @@ int ep_model_create(ep_handle h, const ep_model_config* cfg, int32_t kv_dtype, i
     m->V = c.vocab_size;
     m->L = c.n_layers;
     m->F = 4 * c.d_model;
-    // generation order of init_model (model.cpp:82-102) = storage order
+    // Tensors in generation order of init_model (model.cpp:82-102); each
+    // starts 256-byte aligned (16-byte vector loads) and is filled with its
+    // own range of the single SplitMix64 stream (draw index != storage index).
     const size_t D = size_t(m->D), V = size_t(m->V), F = size_t(m->F);
-    size_t off = D * V;  // embedding [V][D]
+    struct Fill {
+        size_t store, draw, count;
+    };
+    std::vector<Fill> fills;
+    size_t store = 0, draw = 0;
+    auto place = [&](size_t count) {
+        const size_t at = store;
+        fills.push_back({at, draw, count});
+        draw += count;
+        store = (store + count + 31) & ~size_t(31);
+        return at;
+    };
+    place(V * D);  // embedding [V][D] at 0
     m->lw.resize(m->L);
     for (LayerOffsets& o : m->lw) {
-        o.wq = off; off += D * D;
-        o.wk = off; off += D * D;
-        o.wv = off; off += D * D;
-        o.wo = off; off += D * D;
-        o.w1 = off; off += D * F;
-        o.b1 = off; off += F;
-        o.w2 = off; off += F * D;
-        o.b2 = off; off += D;
+        o.wq = place(D * D);
+        o.wk = place(D * D);
+        o.wv = place(D * D);
+        o.wo = place(D * D);
+        o.w1 = place(D * F);
+        o.b1 = place(F);
+        o.w2 = place(F * D);
+        o.b2 = place(D);
     }
-    m->off_unembed = off;
-    off += D * V;
-    m->n_weights = off;
+    m->off_unembed = place(D * V);
+    m->n_weights = draw;
 
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_model_create");
-    EP_CUDA_TRY(m->weights.reserve(m->n_weights * m->esz()), "ep_model_create weights");
-    EP_CUDA_TRY(launch_fill_uniform_at(m->dt, m->weights.ptr, m->n_weights, c.init_seed, 0, -0.1, 0.1, nullptr),
-                "ep_model_create init");
-    h->launches++;
+    EP_CUDA_TRY(m->weights.reserve(store * m->esz()), "ep_model_create weights");
+    for (const Fill& f : fills) {
+        EP_CUDA_TRY(launch_fill_uniform_at(m->dt, m->wptr(f.store), f.count, c.init_seed, f.draw, -0.1, 0.1,
+                                           nullptr),
+                    "ep_model_create init");
+        h->launches++;
+    }
     const size_t pool_bytes = size_t(num_pages) * m->H * size_t(page_tokens) * m->dh * kv_elem_bytes(kv_dtype);
     for (int l = 0; l < m->L; ++l) {
         m->kpages.emplace_back(new DeviceBuffer());
@@ -184,18 +415,14 @@ int ep_model_destroy(ep_model m) {
 int ep_model_weight_sum(ep_model m, double* out) {
     if (!m || !out) return fail(EP_EINVAL, "ep_model_weight_sum: null argument");
     EP_CUDA_TRY(cudaSetDevice(m->h->device), "ep_model_weight_sum");
-    // the fp64 draws (re-drawn when the weights are stored in fp32)
+    // the fp64 draws of the whole stream, contiguous in generation order
     DeviceBuffer tmp;
-    const void* src = m->weights.ptr;
-    if (m->dt != EP_F64) {
-        EP_CUDA_TRY(tmp.reserve(m->n_weights * sizeof(double)), "ep_model_weight_sum");
-        EP_CUDA_TRY(launch_fill_uniform_at(EP_F64, tmp.ptr, m->n_weights, m->cfg.init_seed, 0, -0.1, 0.1, nullptr),
-                    "ep_model_weight_sum");
-        m->h->launches++;
-        src = tmp.ptr;
-    }
+    EP_CUDA_TRY(tmp.reserve(m->n_weights * sizeof(double)), "ep_model_weight_sum");
+    EP_CUDA_TRY(launch_fill_uniform_at(EP_F64, tmp.ptr, m->n_weights, m->cfg.init_seed, 0, -0.1, 0.1, nullptr),
+                "ep_model_weight_sum");
+    m->h->launches++;
     std::vector<double> w(m->n_weights);
-    EP_CUDA_TRY(cudaMemcpy(w.data(), src, w.size() * sizeof(double), cudaMemcpyDeviceToHost),
+    EP_CUDA_TRY(cudaMemcpy(w.data(), tmp.ptr, w.size() * sizeof(double), cudaMemcpyDeviceToHost),
                 "ep_model_weight_sum copy");
     // Model::weight_sum (model.cpp:52-67) adds in generation order
     double sum = 0.0;
@@ -251,98 +478,41 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
         return fail(EP_EINVAL, "ep_model_forward: null argument");
     if (batch < 0) return fail(EP_EINVAL, "ep_model_forward: batch");
     if (batch == 0) return EP_OK;
-    if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_model_forward: seg_indptr[0] must be 0");
-    ep_handle h = m->h;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_model_forward");
+    EP_CUDA_TRY(cudaSetDevice(m->h->device), "ep_model_forward");
 
-    // ---- host: validate, locate every new token's page slot ----
+    std::vector<Req> reqs;
+    bool all_decode = true;
+    if (int rc = collect_requests(m, batch, seg_indptr, segs, page_table, n_new, reqs, &all_decode)) return rc;
+    // request-major rows: request b's new tokens are consecutive
     Meta md;
     md.req_page_off.push_back(0);
-    bool all_decode = true;
     for (int b = 0; b < batch; ++b) {
-        std::vector<PageDesc> pages;
-        int64_t first = 0;
-        if (int rc = collect_request_pages(m->P, m->num_pages, b, seg_indptr, segs, page_table, pages, &first))
-            return rc;
-        const int64_t start = pages.empty() ? 0 : pages.front().pos;
-        const int64_t end = pages.empty() ? 0 : pages.back().pos + pages.back().n_tok;
-        const int nn = n_new[b];
-        if (nn <= 0 || nn > end - start)
-            return fail(EP_EINVAL, "ep_model_forward: request " + std::to_string(b) + " has " +
-                                       std::to_string(end - start) + " tokens, n_new = " + std::to_string(nn));
-        if (end > m->cfg.max_positions)
-            return fail(EP_EINVAL, "embed: positions " + std::to_string(end - nn) + ".." + std::to_string(end) +
-                                       " overflow max_positions " + std::to_string(m->cfg.max_positions));
-        all_decode = all_decode && nn == 1;
-        // new positions [end - nn, end): walk the descriptors from the back
-        size_t di = pages.size();
-        std::vector<std::pair<int32_t, int32_t>> slots(nn);
-        for (int64_t p = end - 1; p >= end - nn; --p) {
-            while (di > 0 && pages[di - 1].pos > p) --di;
-            const PageDesc& d = pages[di - 1];
-            slots[p - (end - nn)] = {d.page, int32_t(p - d.pos)};
-        }
-        for (int i = 0; i < nn; ++i) {
+        const Req& r = reqs[b];
+        for (int i = 0; i < r.nn; ++i) {
             const int32_t tok = tokens[md.tokens.size()];
-            if (tok < 0 || tok >= m->V)
-                return fail(EP_EINVAL, "embed: unknown token id " + std::to_string(tok));
+            if (tok < 0 || tok >= m->V) return fail(EP_EINVAL, "embed: unknown token id " + std::to_string(tok));
             md.tokens.push_back(tok);
-            md.pos.push_back(int32_t(end - nn + i));
-            md.dst_page.push_back(slots[i].first);
-            md.dst_slot.push_back(slots[i].second);
+            md.pos.push_back(int32_t(r.end - r.nn + i));
+            md.dst_page.push_back(r.slots[i].first);
+            md.dst_slot.push_back(r.slots[i].second);
             md.row_req.push_back(b);
         }
         md.last_row.push_back(int32_t(md.tokens.size() - 1));
-        md.q_pos.push_back(end - 1);
-        md.pdesc.insert(md.pdesc.end(), pages.begin(), pages.end());
+        md.q_pos.push_back(r.end - 1);
+        md.pdesc.insert(md.pdesc.end(), r.pages.begin(), r.pages.end());
         md.req_page_off.push_back(int64_t(md.pdesc.size()));
     }
     const int n = int(md.tokens.size());
+    if (int rc = reserve_ws(m, n, batch)) return rc;
+    Pass ps{};
+    if (int rc = upload_meta(m, md, ps, s)) return rc;
+    ps.n = n;
+    ps.batch = batch;
 
-    // ---- workspace ----
-    const size_t es = m->esz();
-    EP_CUDA_TRY(m->hid.reserve(size_t(n) * m->D * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->xbuf.reserve(size_t(n) * m->D * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->qbuf.reserve(size_t(n) * m->D * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->attn.reserve(size_t(n) * m->D * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->h1.reserve(size_t(n) * m->F * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->logits_ws.reserve(size_t(batch) * m->V * es), "ep_model_forward ws");
-    EP_CUDA_TRY(m->next_ws.reserve(size_t(batch) * sizeof(int32_t)), "ep_model_forward ws");
-
-    // ---- metadata upload (pinned staging, one copy) ----
-    std::vector<char> blob;
-    const size_t o_tok = append_bytes(blob, md.tokens), o_pos = append_bytes(blob, md.pos),
-                 o_pg = append_bytes(blob, md.dst_page), o_sl = append_bytes(blob, md.dst_slot),
-                 o_rq = append_bytes(blob, md.row_req), o_last = append_bytes(blob, md.last_row),
-                 o_rpo = append_bytes(blob, md.req_page_off), o_pd = append_bytes(blob, md.pdesc);
-    EP_CUDA_TRY(m->meta.reserve(blob.size()), "ep_model_forward meta");
-    EP_CUDA_TRY(cudaEventSynchronize(m->staged), "ep_model_forward staging");
-    if (blob.size() > m->stage_bytes) {
-        if (m->stage) cudaFreeHost(m->stage);
-        m->stage = nullptr;
-        EP_CUDA_TRY(cudaMallocHost(&m->stage, blob.size()), "ep_model_forward pinned");
-        m->stage_bytes = blob.size();
-    }
-    std::memcpy(m->stage, blob.data(), blob.size());
-    EP_CUDA_TRY(cudaMemcpyAsync(m->meta.ptr, m->stage, blob.size(), cudaMemcpyHostToDevice, s),
-                "ep_model_forward meta copy");
-    EP_CUDA_TRY(cudaEventRecord(m->staged, s), "ep_model_forward event");
-    char* mb = static_cast<char*>(m->meta.ptr);
-    const int32_t* d_tok = reinterpret_cast<const int32_t*>(mb + o_tok);
-    const int32_t* d_pos = reinterpret_cast<const int32_t*>(mb + o_pos);
-    const int32_t* d_pg = reinterpret_cast<const int32_t*>(mb + o_pg);
-    const int32_t* d_sl = reinterpret_cast<const int32_t*>(mb + o_sl);
-    const int32_t* d_rq = reinterpret_cast<const int32_t*>(mb + o_rq);
-    const int32_t* d_last = reinterpret_cast<const int32_t*>(mb + o_last);
-    const int64_t* d_rpo = reinterpret_cast<const int64_t*>(mb + o_rpo);
-    const PageDesc* d_pd = reinterpret_cast<const PageDesc*>(mb + o_pd);
-
-    // ---- attention path: the spliced decode / prefill plans where a kernel
-    // instance exists, otherwise the generic paged kernel ----
-    const bool fast = m->dt == EP_F32 && (m->dh == 64 || m->dh == 128) && m->P % 64 == 0;
-    ep_plan plan = nullptr;
-    if (fast) {
+    // attention: the spliced decode / prefill plans where a kernel instance
+    // exists, otherwise the generic paged kernel
+    if (uses_plans(m)) {
         const ep_kv_pool pool0 = m->pool(0);
         if (all_decode) {
             if (m->decode_plan && m->decode_plan_batch == batch) {
@@ -354,122 +524,131 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
                     ep_plan_destroy(m->decode_plan);
                     m->decode_plan = nullptr;
                 }
-                if (int rc = ep_plan_create(h, &pool0, m->H, 1, batch, seg_indptr, segs, page_table,
+                if (int rc = ep_plan_create(m->h, &pool0, m->H, 1, batch, seg_indptr, segs, page_table,
                                             md.q_pos.data(), 0, &m->decode_plan))
                     return rc;
                 m->decode_plan_batch = batch;
             }
-            plan = m->decode_plan;
+            ps.plan = m->decode_plan;
         } else {
             if (m->prefill_plan) {
                 EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_model_forward");
                 ep_plan_destroy(m->prefill_plan);
                 m->prefill_plan = nullptr;
             }
-            if (int rc = ep_plan_create_prefill(h, &pool0, m->H, batch, seg_indptr, segs, page_table, n_new,
+            if (int rc = ep_plan_create_prefill(m->h, &pool0, m->H, batch, seg_indptr, segs, page_table, n_new,
                                                 &m->prefill_plan))
                 return rc;
-            plan = m->prefill_plan;
+            ps.plan = m->prefill_plan;
         }
     }
+    m->last_path = ps.plan ? 1 : 2;
+    ps.logits = logits ? logits : m->logits_ws.ptr;
+    ps.next = next ? next : static_cast<int32_t*>(m->next_ws.ptr);
+    if (int rc = enqueue_pass(m, ps, s)) return rc;
+    if (hidden)
+        EP_CUDA_TRY(cudaMemcpyAsync(hidden, m->hid.ptr, size_t(n) * m->D * m->esz(), cudaMemcpyDeviceToDevice, s),
+                    "ep_model_forward hidden copy");
+    return EP_OK;
+}
+
+int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                      const int32_t* page_table, int32_t n_steps, const int32_t* first_tokens,
+                      int32_t* out_tokens, ep_stream stream) {
+    if (!m || !seg_indptr || !first_tokens || !out_tokens || (batch > 0 && (!segs || !page_table)))
+        return fail(EP_EINVAL, "ep_model_generate: null argument");
+    if (batch < 0 || n_steps < 0) return fail(EP_EINVAL, "ep_model_generate: batch / n_steps");
+    if (batch == 0 || n_steps == 0) return EP_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EP_CUDA_TRY(cudaSetDevice(m->h->device), "ep_model_generate");
+
+    std::vector<int32_t> nn(batch, n_steps);
+    std::vector<Req> reqs;
+    bool all_decode = true;
+    if (int rc = collect_requests(m, batch, seg_indptr, segs, page_table, nn.data(), reqs, &all_decode)) return rc;
+    Meta md;
+    md.req_page_off.push_back(0);
+    for (int b = 0; b < batch; ++b) {
+        const Req& r = reqs[b];
+        if (r.end - r.nn <= r.start)  // decode_step on an empty cache (model.cpp:258)
+            return fail(EP_EINVAL, "decode_step: empty cache");
+        const int32_t tok = first_tokens[b];
+        if (tok < 0 || tok >= m->V) return fail(EP_EINVAL, "embed: unknown token id " + std::to_string(tok));
+        md.tokens.push_back(tok);
+        md.row_req.push_back(b);
+        md.last_row.push_back(b);
+        md.q_pos.push_back(r.end - r.nn);  // advanced on the device after every step
+        md.pdesc.insert(md.pdesc.end(), r.pages.begin(), r.pages.end());
+        md.req_page_off.push_back(int64_t(md.pdesc.size()));
+    }
+    // step-major rows: entry t * batch + b
+    for (int t = 0; t < n_steps; ++t)
+        for (int b = 0; b < batch; ++b) {
+            const Req& r = reqs[b];
+            md.pos.push_back(int32_t(r.end - r.nn + t));
+            md.dst_page.push_back(r.slots[t].first);
+            md.dst_slot.push_back(r.slots[t].second);
+        }
+    md.step.assign(1, 0);
+    if (int rc = reserve_ws(m, batch, batch)) return rc;
+    DeviceBuffer out_dev;
+    EP_CUDA_TRY(out_dev.reserve(size_t(n_steps) * batch * sizeof(int32_t)), "ep_model_generate out");
+    Pass ps{};
+    if (int rc = upload_meta(m, md, ps, s)) return rc;
+    ps.n = batch;
+    ps.batch = batch;
+    ps.prev = static_cast<const int32_t*>(out_dev.ptr);
+    ps.next = static_cast<int32_t*>(out_dev.ptr);
+    ps.logits = m->logits_ws.ptr;
+
+    // the decode plan is built once for the FINAL table; the causal rule
+    // masks the keys past each step's query position, which advances on the
+    // device (launch_advance), so every step replays the same launches
+    ep_plan plan = nullptr;
+    int64_t* qpos_dev = nullptr;
+    if (uses_plans(m)) {
+        const ep_kv_pool pool0 = m->pool(0);
+        if (int rc = ep_plan_create(m->h, &pool0, m->H, 1, batch, seg_indptr, segs, page_table, md.q_pos.data(), 0,
+                                    &plan))
+            return rc;
+        qpos_dev = plan_qpos_dev(plan);
+    }
+    std::unique_ptr<ep_plan_s, int (*)(ep_plan)> plan_guard(plan, ep_plan_destroy);
+    ps.plan = plan;
     m->last_path = plan ? 1 : 2;
 
-    // ---- launches ----
-    const int dt = m->dt;
-    EP_CUDA_TRY(launch_embed(dt, m->wptr(0), d_tok, d_pos, n, m->D, m->hid.ptr, s), "embed launch");
-    h->launches++;
-    for (int l = 0; l < m->L; ++l) {
-        const LayerOffsets& o = m->lw[l];
-        const ep_kv_pool pool = m->pool(l);
-        DenseArgs a{};
-        a.x = m->hid.ptr;
-        a.n = n;
-        a.K = m->D;
-        a.N = 3 * m->D;
-        a.w[0] = m->wptr(o.wq);
-        a.w[1] = m->wptr(o.wk);
-        a.w[2] = m->wptr(o.wv);
-        a.n_wblk = 3;
-        a.q_out = m->qbuf.ptr;
-        a.k_pages = pool.k_pages;
-        a.v_pages = pool.v_pages;
-        a.kv_dtype = m->kv_dtype;
-        a.H = m->H;
-        a.P = m->P;
-        a.dh = m->dh;
-        a.dst_page = d_pg;
-        a.dst_slot = d_sl;
-        EP_CUDA_TRY(launch_dense(dt, kEpiQKV, true, a, s), "qkv launch");
-        h->launches++;
-
-        if (plan) {
-            if (int rc = ep_spliced_attention(h, plan, &pool, EP_F32, m->qbuf.ptr, EP_F32, m->attn.ptr, nullptr,
-                                              stream))
-                return rc;
-        } else {
-            EP_CUDA_TRY(launch_attention_generic(dt, m->kv_dtype, m->qbuf.ptr, n, m->H, m->dh, d_pd, d_rpo, d_rq,
-                                                 d_pos, pool.k_pages, pool.v_pages, m->P, m->attn.ptr, s),
-                        "attention launch");
-            h->launches++;
-        }
-
-        DenseArgs b{};
-        b.x = m->attn.ptr;
-        b.n = n;
-        b.K = m->D;
-        b.N = m->D;
-        b.w[0] = m->wptr(o.wo);
-        b.n_wblk = 1;
-        b.resid = m->hid.ptr;
-        b.out = m->xbuf.ptr;
-        EP_CUDA_TRY(launch_dense(dt, kEpiResid, false, b, s), "wo launch");
-        h->launches++;
-
-        DenseArgs c{};
-        c.x = m->xbuf.ptr;
-        c.n = n;
-        c.K = m->D;
-        c.N = m->F;
-        c.w[0] = m->wptr(o.w1);
-        c.n_wblk = 1;
-        c.bias = m->wptr(o.b1);
-        c.out = m->h1.ptr;
-        EP_CUDA_TRY(launch_dense(dt, kEpiRelu, true, c, s), "w1 launch");
-        h->launches++;
-
-        DenseArgs d{};
-        d.x = m->h1.ptr;
-        d.n = n;
-        d.K = m->F;
-        d.N = m->D;
-        d.w[0] = m->wptr(o.w2);
-        d.n_wblk = 1;
-        d.bias = m->wptr(o.b2);
-        d.resid = m->xbuf.ptr;
-        d.out = m->hid.ptr;
-        EP_CUDA_TRY(launch_dense(dt, kEpiResid, false, d, s), "w2 launch");
-        h->launches++;
+    // capture one step into a CUDA graph, replay it n_steps times
+    cudaStream_t cap = nullptr;
+    EP_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "ep_model_generate stream");
+    std::unique_ptr<CUstream_st, cudaError_t (*)(cudaStream_t)> cap_guard(cap, cudaStreamDestroy);
+    EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_model_generate");  // metadata + plan uploads landed
+    const int64_t launches0 = m->h->launches.load();
+    EP_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "ep_model_generate capture");
+    int rc = enqueue_pass(m, ps, cap);
+    cudaError_t e = rc ? cudaSuccess : launch_advance(const_cast<int32_t*>(ps.step), qpos_dev, batch, cap);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
     }
-
-    // unembed_logits of each request's last row (model.cpp:238-246) + argmax
-    void* lg = logits ? logits : m->logits_ws.ptr;
-    int32_t* nx = next ? next : static_cast<int32_t*>(m->next_ws.ptr);
-    DenseArgs u{};
-    u.x = m->hid.ptr;
-    u.row_map = d_last;
-    u.n = batch;
-    u.K = m->D;
-    u.N = m->V;
-    u.w[0] = m->wptr(m->off_unembed);
-    u.n_wblk = 1;
-    u.out = lg;
-    EP_CUDA_TRY(launch_dense(dt, kEpiStore, true, u, s), "unembed launch");
-    h->launches++;
-    EP_CUDA_TRY(launch_argmax_rows(dt, lg, batch, m->V, nx, s), "argmax launch");
-    h->launches++;
-    if (hidden)
-        EP_CUDA_TRY(cudaMemcpyAsync(hidden, m->hid.ptr, size_t(n) * m->D * es, cudaMemcpyDeviceToDevice, s),
-                    "ep_model_forward hidden copy");
+    EP_CUDA_TRY(e, "ep_model_generate advance");
+    EP_CUDA_TRY(e2, "ep_model_generate end capture");
+    const int64_t per_step = m->h->launches.load() - launches0 + 1;
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    EP_CUDA_TRY(e, "ep_model_generate instantiate");
+    for (int t = 0; t < n_steps && e == cudaSuccess; ++t) e = cudaGraphLaunch(exec, s);
+    std::vector<int32_t> host(size_t(n_steps) * batch);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(host.data(), out_dev.ptr, host.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaGraphExecDestroy(exec);
+    EP_CUDA_TRY(e, "ep_model_generate replay");
+    m->h->launches += per_step * n_steps - (per_step - 1);  // replays run; the capture counted per_step - 1
+    for (int b = 0; b < batch; ++b)
+        for (int t = 0; t < n_steps; ++t) out_tokens[size_t(b) * n_steps + t] = host[size_t(t) * batch + b];
     return EP_OK;
 }
 

@@ -37,29 +37,39 @@ struct DenseArgs {
     int32_t kv_dtype, H, P, dh;
     const int32_t* dst_page;
     const int32_t* dst_slot;
+    // rollout: device step counter; dst_page / dst_slot are [steps][n] and
+    // row r of step s is entry s * n + r (null = a single forward)
+    const int32_t* step;
 };
 
 // dt: EP_F64 or EP_F32 (x, W, bias, resid, out, q_out share it).
 cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStream_t s);
 
-// embed (model.cpp:104-129): out[r] = embedding[tokens[r]] + sinusoid(pos[r]).
-cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* pos, int n,
-                         int D, void* out, cudaStream_t s);
+// embed (model.cpp:104-129): out[r] = embedding[token] + sinusoid(pos). With
+// a rollout step counter (step != null): token = tokens[r] at step 0, else
+// prev[(step - 1) * n + r]; position pos[step * n + r].
+cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* prev,
+                         const int32_t* step, const int32_t* pos, int n, int D, void* out,
+                         cudaStream_t s);
 
 // Generic paged causal attention: one CTA per (query row, head); row r of
-// request row_req[r] at position row_pos[r] attends to every key of that
-// request's pages (pdesc[req_page_off[b]..]) at a position <= row_pos[r].
+// request row_req[r] at position row_pos[r] (row_pos[step * n + r] in a
+// rollout) attends to every key of that request's pages
+// (pdesc[req_page_off[b]..]) at a position <= its own.
 // q/out [n][H][dh] in dt (EP_F64/EP_F32); pages in kv_dtype.
 cudaError_t launch_attention_generic(int dt, int kv_dtype, const void* q, int n, int H, int dh,
                                      const PageDesc* pdesc, const int64_t* req_page_off,
                                      const int32_t* row_req, const int32_t* row_pos,
-                                     const void* k_pages, const void* v_pages, int P, void* out,
-                                     cudaStream_t s);
+                                     const int32_t* step, const void* k_pages,
+                                     const void* v_pages, int P, void* out, cudaStream_t s);
 
 // argmax_token (model.cpp:248-255) per row of logits [rows][V]: the first
-// index of the maximum.
-cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, int32_t* next,
-                               cudaStream_t s);
+// index of the maximum, into next[rows] (next[step * rows + r] in a rollout).
+cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, const int32_t* step,
+                               int32_t* next, cudaStream_t s);
+
+// Rollout step end: *step += 1, q_pos[0..batch) += 1 (q_pos may be null).
+cudaError_t launch_advance(int32_t* step, int64_t* q_pos, int batch, cudaStream_t s);
 
 // dst[i] = uniform(lo, hi) of SplitMix64(seed) draw first + i (fp64 draw,
 // stored in dt = EP_F64 / EP_F32 / EP_BF16).

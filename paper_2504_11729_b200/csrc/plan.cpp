@@ -503,6 +503,10 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
 
 }  // namespace
 
+namespace ep {
+int64_t* plan_qpos_dev(ep_plan p) { return p ? static_cast<int64_t*>(p->d_qpos.ptr) : nullptr; }
+}  // namespace ep
+
 extern "C" {
 
 int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32_t n_q,

@@ -32,7 +32,7 @@ from .splice import (ORIGIN_CLOUD, ORIGIN_EDGE, ORIGIN_GENERATED, SEGMENT_DTYPE,
                      SegmentRef)
 
 __all__ = ["ModelConfig", "Model", "init_model", "SegmentedCache", "PrefillResult",
-           "DecodeResult", "prefill", "decode_step", "decode_batch", "decode_greedy",
+           "DecodeResult", "prefill", "decode_step", "decode_batch", "decode_greedy", "generate_batch",
            "generate_monolithic", "generate_split", "ORIGIN_CLOUD", "ORIGIN_EDGE",
            "ORIGIN_GENERATED"]
 
@@ -150,6 +150,21 @@ class Model:
                                      logits.data_ptr() if logits is not None else None,
                                      nxt.data_ptr(), s.cuda_stream), "forward")
         return nxt, logits, hidden
+
+    def generate(self, tables, n_steps: int, first_tokens, *, stream=None):
+        """ep_model_generate: the last n_steps positions of every table are
+        decoded on the device (one CUDA graph per step, replayed). Returns
+        [B][n_steps] greedy tokens."""
+        torch = _torch()
+        B = len(tables)
+        indptr, segs, pt = _batch_arrays(tables)
+        first = np.ascontiguousarray(first_tokens, dtype=np.int32)
+        out = np.zeros((B, n_steps), dtype=np.int32)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().ep_model_generate(self._m, B, indptr.ctypes.data, segs.ctypes.data,
+                                      pt.ctypes.data, n_steps, first.ctypes.data, out.ctypes.data,
+                                      s.cuda_stream), "generate")
+        return out.tolist()
 
     def close(self) -> None:
         if getattr(self, "_m", None):
@@ -350,32 +365,59 @@ def decode_batch(model: Model, caches, last_tokens, *, want_logits: bool = False
     return nxt.cpu().numpy(), (logits.cpu().numpy() if logits is not None else None)
 
 
+def generate_batch(model: Model, caches, first_tokens, n_steps: int):
+    """n_steps greedy decode steps for every session, resident on the device
+    (ep_model_generate): the generated segments grow by n_steps and the
+    tokens come back once at the end. Returns [B][n_steps]."""
+    if n_steps <= 0:
+        return [[] for _ in caches]
+    for c in caches:
+        if c.empty():
+            raise InvalidArgument("decode_step: empty cache")
+        if c.end_position() + n_steps > model.config.max_positions:
+            raise InvalidArgument("embed: positions overflow max_positions")
+    _check_tokens(model, first_tokens)
+    for c in caches:
+        c._grow_generated(n_steps)
+    try:
+        return model.generate([c.segments for c in caches], n_steps, list(first_tokens))
+    except Exception:
+        for c in caches:
+            c._shrink_generated(n_steps)
+        raise
+
+
 def decode_greedy(model: Model, cache: SegmentedCache, prefill_result: PrefillResult,
-                  n_steps: int):
+                  n_steps: int, *, device_loop: bool = True):
     """decode_greedy (model.cpp:285-297), starting from the greedy token of
-    the last prefilled row."""
+    the last prefilled row. device_loop: the n_steps - 1 decode steps run as
+    one device-resident rollout (generate_batch); otherwise one decode_step
+    (host round trip) per token."""
     out = []
     if n_steps == 0:
         return out
     out.append(prefill_result.next_token)
+    if device_loop:
+        return out + generate_batch(model, [cache], [out[0]], n_steps - 1)[0]
     while len(out) < n_steps:
         nxt, _ = decode_batch(model, [cache], [out[-1]])
         out.append(int(nxt[0]))
     return out
 
 
-def generate_monolithic(model: Model, prompt, n_steps: int):
+def generate_monolithic(model: Model, prompt, n_steps: int, *, device_loop: bool = True):
     """model.cpp:299-305."""
     cache = SegmentedCache(model)
     try:
         pf = prefill(model, prompt, ORIGIN_EDGE, 0, cache, want_hidden=False)
         cache.append(pf.segments)
-        return decode_greedy(model, cache, pf, n_steps)
+        return decode_greedy(model, cache, pf, n_steps, device_loop=device_loop)
     finally:
         cache.release()
 
 
-def generate_split(model: Model, cloud_prompt, edge_prompt, n_steps: int):
+def generate_split(model: Model, cloud_prompt, edge_prompt, n_steps: int, *,
+                   device_loop: bool = True):
     """model.cpp:307-316: cloud prefill, edge prefill against the cloud KV,
     decode on the edge-side cache."""
     cache = SegmentedCache(model)
@@ -385,6 +427,6 @@ def generate_split(model: Model, cloud_prompt, edge_prompt, n_steps: int):
         edge = prefill(model, edge_prompt, ORIGIN_EDGE, len(cloud_prompt), cache,
                        want_hidden=False)
         cache.append(edge.segments)
-        return decode_greedy(model, cache, edge, n_steps)
+        return decode_greedy(model, cache, edge, n_steps, device_loop=device_loop)
     finally:
         cache.release()

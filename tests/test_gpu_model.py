@@ -88,8 +88,9 @@ def test_tiny_rollout_golden(cuda_handle, dtype):
     M = _mod()
     m = make(TINY, dtype)
     cloud, edge = tiny_prompts()
-    assert M.generate_split(m, cloud, edge, 8) == GOLD["tiny_rollout"]
-    assert M.generate_monolithic(m, cloud + edge, 8) == GOLD["tiny_rollout"]
+    for loop in (True, False):  # device-resident rollout (CUDA graph) / one decode_step per token
+        assert M.generate_split(m, cloud, edge, 8, device_loop=loop) == GOLD["tiny_rollout"]
+        assert M.generate_monolithic(m, cloud + edge, 8, device_loop=loop) == GOLD["tiny_rollout"]
     assert m.last_attention_path() == "generic"  # d_head 4
     assert m.pages.free_pages == m.num_pages  # caches released their pages
 
@@ -253,3 +254,48 @@ def test_errors_mirror_the_reference(cuda_handle):
     assert cache.end_position() == 512
     with pytest.raises(ValueError):
         M.ModelConfig(2, 3, 8, 32).validate()
+
+
+@pytest.mark.parametrize("dtype,kv", [("f64", "f64"), ("f32", "f32"), ("f32", "bf16")])
+def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv):
+    """generate_batch (one CUDA graph per step, positions advanced on the
+    device, K1 plan built for the final length) = decode_step per token, for
+    3 sessions sharing a cloud prompt; the cached K/V are the same too."""
+    import torch
+    M = _mod()
+    rng = O.SplitMix64(5)
+    cloud = [rng.next_u64() % 256 for _ in range(100)]
+    edges = [[rng.next_u64() % 256 for _ in range(n)] for n in (3, 40, 70)]
+    n_steps = 70  # crosses a page boundary for every session
+
+    def sessions(m):
+        pf = M.prefill(m, cloud, M.ORIGIN_CLOUD, 0, M.SegmentedCache(m))
+        out = []
+        for edge in edges:
+            c = M.SegmentedCache(m)
+            m.pages.retain(pf.segment.pages)
+            c.append(pf.segments)
+            e = M.prefill(m, edge, M.ORIGIN_EDGE, len(cloud), c)
+            c.append(e.segments)
+            out.append((c, e.next_token))
+        return out
+
+    m1 = make(CFG1, dtype, kv, num_pages=64)
+    s1 = sessions(m1)
+    got = M.generate_batch(m1, [c for c, _ in s1], [t for _, t in s1], n_steps)
+    m2 = make(CFG1, dtype, kv, num_pages=64)
+    s2 = sessions(m2)
+    for b, (c, t) in enumerate(s2):
+        toks = []
+        for _ in range(n_steps):
+            t = M.decode_step(m2, c, t).next_token
+            toks.append(t)
+        assert got[b] == toks, b
+        assert s1[b][0].end_position() == c.end_position()
+    for layer in range(CFG1[0]):
+        p1, p2 = m1.kv_pool(layer), m2.kv_pool(layer)
+        esz = {"f64": 8, "f32": 4, "bf16": 2}[kv]
+        n = p1.num_pages * p1.n_kv_heads * p1.page_tokens * p1.d_head * esz // 8
+        a = _read_device(p1.k_pages, n, torch.float64)
+        b2 = _read_device(p2.k_pages, n, torch.float64)
+        np.testing.assert_array_equal(a, b2)
