@@ -442,6 +442,12 @@ def run_extras(args, world, rank, h):
         extras["ingest"] = ingest_bench.run(max(5, steps // 2), 3, h)
         gc.collect()
         torch.cuda.empty_cache()
+        # the whole decoder on the GPU at config 1 (tiny
+        # reference model, fp32), next to the reference's own decode_step
+        import model_bench
+        extras["model_cfg1"] = model_bench.run(64, 5, h, batch=64, cpu=not args.no_cpu_baseline)
+        gc.collect()
+        torch.cuda.empty_cache()
     skv = {}
     for b in (1, 32):
         skv[f"batch{b}"] = splitkv_bench.run(b, steps, 3, combine="peer")

@@ -45,6 +45,8 @@ constexpr double kLayerNormEps = 1e-5;       // model.cpp:14
 constexpr int kGvCols = 64;                  // output columns per CTA (16 threads x 4)
 constexpr int kGvKS = kDenseThreads / 16;    // k-slices per CTA
 constexpr int kGvRows = 8;                   // rows (decode batch) per CTA
+constexpr int kGvPre = 8;        // weight rows per thread held in registers before the wait
+constexpr int kGvMaxK = 32 * 32; // LN rows kept in registers (K <= 1024 with LN)
 
 template <typename T>
 __device__ __forceinline__ T ld(const void* p, size_t i) {
@@ -215,7 +217,7 @@ cudaError_t dispatch_rows(const DenseArgs& a, cudaStream_t s) {
     // else the scalar kernel: every CTA streams its weight columns once for up
     // to 8 rows (decode) or 32 rows (prefill).
     const int nb = a.N / a.n_wblk;
-    bool aligned = nb % 4 == 0;
+    bool aligned = nb % 4 == 0 && (!LN || a.K <= kGvMaxK);
     for (int i = 0; i < a.n_wblk; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(a.w[i]) % 16 == 0;
     if (aligned) return launch_gemv_t<T, EPI, LN>(a, s);
     if (a.n <= 8) return launch_dense_t<T, 8, EPI, LN>(a, s);
@@ -253,6 +255,13 @@ __device__ __forceinline__ Vec4<T> ld4(const T* p) {
     }
 }
 
+// Programmatic dependent launch: the weights do not depend on the previous
+// kernel, so their loads are issued before griddepcontrol.wait and overlap
+// the predecessor's tail; inputs are read only after it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+
 // smem: A slice [kGvRows][KR] | k-slice partials [kGvKS][kGvRows][kGvCols]
 //       | cluster partial [kGvRows][kGvCols]
 template <typename T, int EPI, bool LN>
@@ -264,61 +273,93 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
     T* As = reinterpret_cast<T*>(smem_raw);
     T* red = As + kGvRows * KR;
     T* part = red + kGvKS * kGvRows * kGvCols;
-    __shared__ T s_mean[kGvRows], s_inv[kGvRows];
-    __shared__ int s_row[kGvRows];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int row0 = blockIdx.z * kGvRows;
     const int nr = min(kGvRows, a.n - row0);
     const int k0 = crank * KR, kr = max(0, min(KR, a.K - k0));
     const T* X = static_cast<const T*>(a.x);
-    if (tid < kGvRows)
-        s_row[tid] = tid < nr ? (a.row_map ? a.row_map[row0 + tid] : row0 + tid) : 0;
-    __syncthreads();
-    if constexpr (LN) {
-        for (int r = warp; r < nr; r += kDenseThreads / 32) {
-            const T* xr = X + size_t(s_row[r]) * a.K;
-            T sm = 0;
-            for (int c = lane; c < a.K; c += 32) sm += xr[c];
-            sm = warp_sum(sm);
-            const T mean = sm / T(a.K);
-            T q = 0;
-            for (int c = lane; c < a.K; c += 32) {
-                const T dx = xr[c] - mean;
-                q += dx * dx;
-            }
-            q = warp_sum(q);
-            if (lane == 0) {
-                s_mean[r] = mean;
-                s_inv[r] = T(1) / sqrt(q / T(a.K) + T(kLayerNormEps));
-            }
-        }
-        __syncthreads();
-    }
-    for (int i = tid; i < kGvRows * KR; i += kDenseThreads) {
-        const int r = i / KR, kk = i - r * KR;
-        T v = T(0);
-        if (r < nr && kk < kr) {
-            v = X[size_t(s_row[r]) * a.K + k0 + kk];
-            if constexpr (LN) v = (v - s_mean[r]) * s_inv[r];
-        }
-        As[i] = v;
-    }
-    __syncthreads();
 
+    // ---- 1. this thread's weight rows (independent of the predecessor) ----
     const int cg4 = tid % 16, ks = tid / 16;
     const int col0 = blockIdx.x * kGvCols + cg4 * 4;
     const bool cvalid = col0 < a.N;  // N % 4 == 0 and block width % 4 == 0
+    const int per = (kr + kGvKS - 1) / kGvKS;
+    const int kb = ks * per, ke = min(kr, kb + per);
+    const T* wp = nullptr;
+    int nb = 1;
+    Vec4<T> wpre[kGvPre];
+    if (cvalid) {
+        nb = a.N / a.n_wblk;
+        const int blk = col0 / nb;
+        wp = static_cast<const T*>(a.w[blk]) + (col0 - blk * nb) + size_t(k0) * nb;
+#pragma unroll
+        for (int i = 0; i < kGvPre; ++i)
+            if (kb + i < ke) wpre[i] = ld4(wp + size_t(kb + i) * nb);
+    }
+
+    // ---- 2. inputs: wait for the producer of x, LayerNorm from registers ----
+    pdl_wait();
+    for (int r = warp; r < kGvRows; r += kDenseThreads / 32) {
+        T* dst = As + r * KR;
+        if (r >= nr) {
+            for (int kk = lane; kk < KR; kk += 32) dst[kk] = T(0);
+            continue;
+        }
+        const int grow = a.row_map ? a.row_map[row0 + r] : row0 + r;
+        const T* xr = X + size_t(grow) * a.K;
+        if constexpr (LN) {
+            // layer_norm (model.cpp:131-150): mean, mean squared deviation,
+            // inv = 1 / sqrt(var + eps) — the row is read once into registers
+            constexpr int NV = kGvMaxK / 32;
+            T v[NV];
+            T sm = 0;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int c = lane + 32 * i;
+                v[i] = c < a.K ? xr[c] : T(0);
+                sm += v[i];
+            }
+            const T mean = warp_sum(sm) / T(a.K);
+            T q = 0;
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int c = lane + 32 * i;
+                const T dx = v[i] - mean;
+                q += c < a.K ? dx * dx : T(0);
+            }
+            const T inv = T(1) / sqrt(warp_sum(q) / T(a.K) + T(kLayerNormEps));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+                const int c = lane + 32 * i;
+                if (c >= k0 && c < k0 + KR) dst[c - k0] = c < a.K ? (v[i] - mean) * inv : T(0);
+            }
+        } else {
+            for (int kk = lane; kk < KR; kk += 32) dst[kk] = kk < kr ? xr[k0 + kk] : T(0);
+        }
+    }
+    __syncthreads();
+
     T acc[kGvRows][4];
 #pragma unroll
     for (int r = 0; r < kGvRows; ++r) acc[r][0] = acc[r][1] = acc[r][2] = acc[r][3] = T(0);
     if (cvalid) {
-        const int nb = a.N / a.n_wblk, blk = col0 / nb;
-        const T* wp = static_cast<const T*>(a.w[blk]) + (col0 - blk * nb) + size_t(k0) * nb;
-        const int per = (kr + kGvKS - 1) / kGvKS;
-        const int kb = ks * per, ke = min(kr, kb + per);
-#pragma unroll 8
-        for (int kk = kb; kk < ke; ++kk) {
+#pragma unroll
+        for (int i = 0; i < kGvPre; ++i) {
+            if (kb + i >= ke) break;
+            const Vec4<T> w = wpre[i];
+            const int kk = kb + i;
+#pragma unroll
+            for (int r = 0; r < kGvRows; ++r) {
+                const T x = As[r * KR + kk];
+                acc[r][0] += x * w.x;
+                acc[r][1] += x * w.y;
+                acc[r][2] += x * w.z;
+                acc[r][3] += x * w.w;
+            }
+        }
+#pragma unroll 4
+        for (int kk = kb + kGvPre; kk < ke; ++kk) {
             const Vec4<T> w = ld4(wp + size_t(kk) * nb);
 #pragma unroll
             for (int r = 0; r < kGvRows; ++r) {
@@ -330,6 +371,7 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
             }
         }
     }
+    pdl_trigger();  // the successor may start prefetching its weights
 #pragma unroll
     for (int r = 0; r < kGvRows; ++r)
 #pragma unroll
@@ -372,13 +414,15 @@ cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s) {
     cfg.blockDim = dim3(kDenseThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = cs;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, gemv_cluster_kernel<T, EPI, LN>, a, KR);
 }
 
