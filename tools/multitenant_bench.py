@@ -93,8 +93,9 @@ def run(steps=50, warmup=5, h=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     args = ap.parse_args()
-    print(json.dumps(run(args.steps)))
+    print(json.dumps(run(args.steps, args.warmup)))
 
 
 if __name__ == "__main__":
