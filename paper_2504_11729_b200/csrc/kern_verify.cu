@@ -77,8 +77,15 @@ constexpr int kSmem = OFF_MISC + 32;  // dynamic smem base must be 1024-aligned 
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColO = 0, kColS = 256, kColQ = 384, kColP = 448;
 
-constexpr uint32_t kIdescQK = umma::idesc_bf16_f32(kM, kBT, false, false);
-constexpr uint32_t kIdescPV = umma::idesc_bf16_f32(kM, kD, false, true);
+// Tiles of <= 64 rows (verify: 20 / 36 rows per kv-head) issue M = 64 MMAs —
+// half the tensor work of M = 128. With cta_group::1 an M = 64 operand / result
+// row m lives in TMEM lane 32 * (m / 16) + m % 16, i.e. lanes 0-15 of each
+// lane quarter, where the softmax threads of lanes 0-15 already keep rows
+// v = 4 * lane + quarter < 64 — the thread <-> row mapping does not change.
+constexpr uint32_t kIdescQK128 = umma::idesc_bf16_f32(kM, kBT, false, false);
+constexpr uint32_t kIdescPV128 = umma::idesc_bf16_f32(kM, kD, false, true);
+constexpr uint32_t kIdescQK64 = umma::idesc_bf16_f32(64, kBT, false, false);
+constexpr uint32_t kIdescPV64 = umma::idesc_bf16_f32(64, kD, false, true);
 
 struct Bars {
     uint64_t* full_k;   // [KS] K block landed
@@ -105,6 +112,12 @@ __device__ __forceinline__ void trace(const DecodeArgs& a, int ev, uint32_t gi) 
         asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
         a.trace[ev * kTraceBlocks + gi] = (unsigned long long)t;
     }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
@@ -167,6 +180,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
     const int Hkv = a.n_kv_heads, P = a.page_tokens;
+    const bool m64 = rows <= 64;
+    const uint32_t kIdescQK = m64 ? kIdescQK64 : kIdescQK128;
+    const uint32_t kIdescPV = m64 ? kIdescPV64 : kIdescPV128;
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks)  // debug: per-CTA start (ns)
+        a.trace[18 * kTraceBlocks + 2 * blockIdx.x] = globaltimer_ns();
     const int G = a.n_q_heads / Hkv;
 
     if (threadIdx.x == 0) {
@@ -623,6 +641,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::fence_after_sync();
         umma::tmem_dealloc(tmem, kTmemCols);
     }
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks)  // debug: per-CTA end (ns)
+        a.trace[18 * kTraceBlocks + 2 * blockIdx.x + 1] = globaltimer_ns();
 }
 
 }  // namespace

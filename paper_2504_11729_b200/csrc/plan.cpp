@@ -457,8 +457,8 @@ unsigned long long* trace_buffer() {
     static unsigned long long* t = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&b, 18 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(b, 0, 18 * 1024 * sizeof(unsigned long long));
+        if (e && e[0] == '1' && cudaMalloc(&b, 20 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 20 * 1024 * sizeof(unsigned long long));
         return b;
     }();
     return t;
@@ -480,7 +480,7 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
                     "verify attention launch");
         h->launches++;
         if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
-            std::vector<unsigned long long> host(18 * 1024);
+            std::vector<unsigned long long> host(20 * 1024);
             cudaStreamSynchronize(s);
             cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
             const char* f = std::getenv("EP_TRACE_FILE");

@@ -1,0 +1,63 @@
+"""Debug: clock64 trace of CTA 0 of the last K3 launch, for one of the K3
+workloads, and a per-block breakdown of the steady state.
+
+    EP_TRACE=1 EP_TRACE_FILE=gpurun_out/trace_k3.bin python tools/trace_k3.py {verify4|verify8|shared|prefill}
+    python tools/trace_k3.py --analyse gpurun_out/trace_k3.bin
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+EV = ["KISSUE", "VISSUE", "QK", "PV", "S_SEEN", "P_DONE", "QK_START", "QK_FULLK", "QK_DONE",
+      "PV_START", "PV_PFULL", "PV_DONE"]
+NB = 1024
+
+
+def analyse(path):
+    raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
+    t = raw[:18 * NB].reshape(18, NB)
+    if raw.size >= 20 * NB:  # per-CTA globaltimer start / end (ns)
+        se = raw[18 * NB:20 * NB].reshape(NB, 2)
+        se = se[se[:, 0] > 0]
+        t0 = se[:, 0].min()
+        dur = (se[:, 1] - se[:, 0]) / 1e3
+        end = (se[:, 1] - t0) / 1e3
+        print(f"CTAs {len(se)}: start spread {(se[:, 0].max() - t0) / 1e3:.1f} us, "
+              f"duration us min {dur.min():.1f} p50 {np.median(dur):.1f} max {dur.max():.1f}; "
+              f"last end {end.max():.1f} us; slowest CTAs {np.argsort(-end)[:6].tolist()}")
+    base = t[t > 0].min()
+    n = int((t[4] > 0).sum())  # blocks with an S_SEEN event
+    print(f"blocks traced: {n}")
+    lo, hi = n // 4, 3 * n // 4  # steady state
+    s_seen, p_done = t[4, lo:hi], t[5, lo:hi]
+    per = np.diff(s_seen)
+    print(f"S_SEEN period p50 {np.median(per):.0f} cycles (mean {per.mean():.0f})")
+    for name, a, b in (("softmax S_SEEN->P_DONE", 4, 5), ("QK issue->done", 6, 8), ("QK wait K", 6, 7),
+                       ("PV start->done", 9, 11), ("PV wait P", 9, 10), ("P_DONE->PV_START", 5, 9),
+                       ("QK_DONE->S_SEEN", 8, 4), ("KISSUE->QK_FULLK", 0, 7)):
+        d = t[b, lo:hi] - t[a, lo:hi]
+        d = d[(t[a, lo:hi] > 0) & (t[b, lo:hi] > 0)]
+        if d.size:
+            print(f"  {name:26s} p50 {np.median(d):7.0f}  mean {d.mean():7.0f}")
+    print("total span", (t[t > 0].max() - base))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--analyse":
+        analyse(sys.argv[2])
+        sys.exit(0)
+    kind = sys.argv[1]
+    if kind.startswith("verify"):
+        import verify_bench
+        print(verify_bench.run(int(kind[6:]), 1, 1))
+    elif kind == "shared":
+        import multitenant_bench
+        print(multitenant_bench.run(1, 1))
+    else:
+        import prefill_bench
+        print(prefill_bench.run("cloud", 4, 1, 1))
