@@ -641,8 +641,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::fence_after_sync();
         umma::tmem_dealloc(tmem, kTmemCols);
     }
-    if (a.trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks)  // debug: per-CTA end (ns)
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) {  // debug: per-CTA end (ns), work
         a.trace[18 * kTraceBlocks + 2 * blockIdx.x + 1] = globaltimer_ns();
+        unsigned long long nb = 0;
+        for (int it = it0; it < it1; ++it) nb += a.items[it].nblk;
+        a.trace[20 * kTraceBlocks + 2 * blockIdx.x] = it1 - it0;
+        a.trace[20 * kTraceBlocks + 2 * blockIdx.x + 1] = nb;
+    }
 }
 
 }  // namespace

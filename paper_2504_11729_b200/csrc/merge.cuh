@@ -15,63 +15,106 @@ namespace ep {
 
 // o_part[(item * stride + r) * D + c], lse_part[item * stride + r] (log2);
 // rows r = r0, r0 + r_step, ... < nrows; orow(r) = output row index.
+// Latency-bound by construction (a few rows x a few items of L2 reads), so a
+// warp works on kRB rows at once: their lse loads, then their partial rows of
+// two items at a time, all in flight together (a K3 shared-prefix tile merges
+// 128 rows x 2-3 items; serial per-row loads made that the CTA's tail).
 template <int D, typename RowMap>
 __device__ __forceinline__ void merge_unit_rows(const DecodeArgs& a, int u0, int n, int stride,
                                                 int nrows, int r0, int r_step, RowMap orow_of) {
     constexpr int E = D / 32;
+    constexpr int kRB = 4;
     static_assert(E == 2 || E == 4, "D must be 64 or 128");
     const int lane = threadIdx.x & 31;
-    for (int r = r0; r < nrows; r += r_step) {
-        float M = -INFINITY;
-        for (int base = 0; base < n; base += 32) {
-            const float ls = base + lane < n ? __ldcg(&a.lse_part[size_t(u0 + base + lane) * stride + r])
-                                             : -INFINITY;
-            M = fmaxf(M, ls);
-        }
-        M = warp_max(M);
-        float L = 0.f;
-        float acc[E];
+    for (int rb = r0; rb < nrows; rb += kRB * r_step) {
+        int rr[kRB];
+        bool ok[kRB];
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc[e] = 0.f;
-        if (M != -INFINITY) {
-            for (int base = 0; base < n; base += 32) {
-                const float ls = base + lane < n ? __ldcg(&a.lse_part[size_t(u0 + base + lane) * stride + r])
-                                                 : -INFINITY;
-                const float wt = ls == -INFINITY ? 0.f : fast_exp2(ls - M);
-                L += wt;
-                const int cnt = min(32, n - base);
-#pragma unroll 4
-                for (int j = 0; j < cnt; ++j) {
-                    const float wj = __shfl_sync(0xffffffffu, wt, j);
-                    const float* src = a.o_part + (size_t(u0 + base + j) * stride + r) * D + lane * E;
+        for (int k = 0; k < kRB; ++k) {
+            rr[k] = rb + k * r_step;
+            ok[k] = rr[k] < nrows;
+        }
+        // row max / weights over the items' lse (lane = item within a chunk of 32)
+        float M[kRB], L[kRB], inv[kRB], acc[kRB][E];
+#pragma unroll
+        for (int k = 0; k < kRB; ++k) {
+            M[k] = -INFINITY;
+            L[k] = 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[k][e] = 0.f;
+        }
+        for (int base = 0; base < n; base += 32) {
+            float ls[kRB];
+#pragma unroll
+            for (int k = 0; k < kRB; ++k)
+                ls[k] = (ok[k] && base + lane < n) ? __ldcg(&a.lse_part[size_t(u0 + base + lane) * stride + rr[k]])
+                                                   : -INFINITY;
+#pragma unroll
+            for (int k = 0; k < kRB; ++k) M[k] = fmaxf(M[k], warp_max(ls[k]));
+        }
+        for (int base = 0; base < n; base += 32) {
+            float wt[kRB];
+#pragma unroll
+            for (int k = 0; k < kRB; ++k) {
+                const float ls = (ok[k] && base + lane < n)
+                                     ? __ldcg(&a.lse_part[size_t(u0 + base + lane) * stride + rr[k]])
+                                     : -INFINITY;
+                wt[k] = (ls == -INFINITY || M[k] == -INFINITY) ? 0.f : fast_exp2(ls - M[k]);
+                L[k] += wt[k];
+            }
+            const int cnt = min(32, n - base);
+            for (int j = 0; j < cnt; j += 2) {
+                const bool two = j + 1 < cnt;
+                float x0[kRB][E], x1[kRB][E];
+#pragma unroll
+                for (int k = 0; k < kRB; ++k) {
+                    const float* s0 = a.o_part + (size_t(u0 + base + j) * stride + (ok[k] ? rr[k] : 0)) * D + lane * E;
+                    const float* s1 = s0 + size_t(stride) * D;
                     if constexpr (E == 4) {
-                        const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
-                        acc[0] += wj * x.x;
-                        acc[1] += wj * x.y;
-                        acc[2] += wj * x.z;
-                        acc[3] += wj * x.w;
+                        const float4 v0 = __ldcg(reinterpret_cast<const float4*>(s0));
+                        const float4 v1 = two ? __ldcg(reinterpret_cast<const float4*>(s1)) : make_float4(0, 0, 0, 0);
+                        x0[k][0] = v0.x; x0[k][1] = v0.y; x0[k][2] = v0.z; x0[k][3] = v0.w;
+                        x1[k][0] = v1.x; x1[k][1] = v1.y; x1[k][2] = v1.z; x1[k][3] = v1.w;
                     } else {
-                        const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
-                        acc[0] += wj * x.x;
-                        acc[1] += wj * x.y;
+                        const float2 v0 = __ldcg(reinterpret_cast<const float2*>(s0));
+                        const float2 v1 = two ? __ldcg(reinterpret_cast<const float2*>(s1)) : make_float2(0, 0);
+                        x0[k][0] = v0.x; x0[k][1] = v0.y;
+                        x1[k][0] = v1.x; x1[k][1] = v1.y;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kRB; ++k) {
+                    const float w0 = __shfl_sync(0xffffffffu, wt[k], j);
+                    const float w1 = __shfl_sync(0xffffffffu, wt[k], two ? j + 1 : j);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        acc[k][e] += w0 * x0[k][e];
+                        if (two) acc[k][e] += w1 * x1[k][e];
                     }
                 }
             }
-            L = warp_sum(L);
         }
-        const bool er = !(L > 0.f);
-        const float inv = er ? 0.f : 1.f / L;
-        const size_t orow = orow_of(r);
-        if (a.o_dtype == EP_BF16) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(a.o) + orow * D + lane * E;
 #pragma unroll
-            for (int e = 0; e < E; ++e) dst[e] = __float2bfloat16_rn(acc[e] * inv);
-        } else {
-            float* dst = static_cast<float*>(a.o) + orow * D + lane * E;
-#pragma unroll
-            for (int e = 0; e < E; ++e) dst[e] = acc[e] * inv;
+        for (int k = 0; k < kRB; ++k) {
+            L[k] = warp_sum(L[k]);
+            inv[k] = L[k] > 0.f ? 1.f / L[k] : 0.f;
         }
-        if (lane == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (M + fast_log2(L)) * kLn2;
+#pragma unroll
+        for (int k = 0; k < kRB; ++k) {
+            if (!ok[k]) continue;
+            const bool er = !(L[k] > 0.f);
+            const size_t orow = orow_of(rr[k]);
+            if (a.o_dtype == EP_BF16) {
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(a.o) + orow * D + lane * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e] = __float2bfloat16_rn(acc[k][e] * inv[k]);
+            } else {
+                float* dst = static_cast<float*>(a.o) + orow * D + lane * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e] = acc[k][e] * inv[k];
+            }
+            if (lane == 0 && a.lse) a.lse[orow] = er ? -INFINITY : (M[k] + fast_log2(L[k])) * kLn2;
+        }
     }
 }
 

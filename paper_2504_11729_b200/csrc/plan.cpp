@@ -79,6 +79,17 @@ namespace {
 
 constexpr int kBlockTokens = 64;
 constexpr int64_t kTcItemWeight = 10;  // K3 work-item overhead in blocks (see build_subplan)
+// Overhead of a full 128-row K3 tile item (shared-prefix / prefill): the Q
+// load, the two-group epilogue over 128 rows and, when the unit is split,
+// the partial store + merge — measured by the per-CTA trace (tools/trace_k3.py).
+int64_t tc_item_weight(int rows) {
+    static const int64_t env = [] {
+        const char* e = std::getenv("EP_TC_ITEM_WEIGHT");
+        return e ? std::atoll(e) : -1;
+    }();
+    if (env >= 0) return env;
+    return rows > 64 ? 14 : kTcItemWeight;
+}
 
 // One query-row set attending to one page list.
 struct VReq {
@@ -293,7 +304,7 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
     build_subplan(p.main, main_vr, Hkv, cap, p.main.tc ? kTcItemWeight : 0);
     p.main.rows = rpr;
     if (p.cascade) {
-        build_subplan(p.shared, shared_vr, Hkv, cap, kTcItemWeight);
+        build_subplan(p.shared, shared_vr, Hkv, cap, tc_item_weight(group_cap * rpr));
         p.shared.rows = group_cap * rpr;
         p.shared.tc = true;
     }
@@ -349,7 +360,7 @@ int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const
     p.batch = int32_t(vr.size());
     p.cascade = false;
     p.has_shared.assign(vr.size(), 0);
-    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), p.main.tc ? kTcItemWeight : 1);
+    build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), p.main.tc ? tc_item_weight(G * C) : 1);
     p.main.rows = G * C;
     return EP_OK;
 }
@@ -457,8 +468,8 @@ unsigned long long* trace_buffer() {
     static unsigned long long* t = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&b, 20 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(b, 0, 20 * 1024 * sizeof(unsigned long long));
+        if (e && e[0] == '1' && cudaMalloc(&b, 22 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 22 * 1024 * sizeof(unsigned long long));
         return b;
     }();
     return t;
@@ -480,7 +491,7 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
                     "verify attention launch");
         h->launches++;
         if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
-            std::vector<unsigned long long> host(20 * 1024);
+            std::vector<unsigned long long> host(22 * 1024);
             cudaStreamSynchronize(s);
             cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
             const char* f = std::getenv("EP_TRACE_FILE");

@@ -30,6 +30,15 @@ def analyse(path):
         print(f"CTAs {len(se)}: start spread {(se[:, 0].max() - t0) / 1e3:.1f} us, "
               f"duration us min {dur.min():.1f} p50 {np.median(dur):.1f} max {dur.max():.1f}; "
               f"last end {end.max():.1f} us; slowest CTAs {np.argsort(-end)[:6].tolist()}")
+        if raw.size >= 22 * NB:
+            wk = raw[20 * NB:22 * NB].reshape(NB, 2)[:len(se)]
+            order = np.argsort(-dur)
+            print("  slowest (cta, us, items, blocks):",
+                  [(int(c), round(float(dur[c]), 1), int(wk[c, 0]), int(wk[c, 1])) for c in order[:8]])
+            print("  fastest (cta, us, items, blocks):",
+                  [(int(c), round(float(dur[c]), 1), int(wk[c, 0]), int(wk[c, 1])) for c in order[-5:]])
+            us_per_blk = dur / np.maximum(wk[:, 1], 1)
+            print(f"  us per block p50 {np.median(us_per_blk):.3f}; items/CTA max {wk[:, 0].max()}")
     base = t[t > 0].min()
     n = int((t[4] > 0).sum())  # blocks with an S_SEEN event
     print(f"blocks traced: {n}")
