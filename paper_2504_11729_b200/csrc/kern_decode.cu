@@ -30,6 +30,7 @@
 //     page = segment order (attention.cpp:116-145) — no second launch.
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ep_common.cuh"
 #include "ep_internal.h"
@@ -158,6 +159,14 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
     const int P = a.page_tokens, Hkv = a.n_kv_heads;
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // debug: per-CTA start (ns), work
+        unsigned long long t, nb = 0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[18 * 1024 + 2 * blockIdx.x] = t;
+        for (int it = it0; it < it1; ++it) nb += a.items[it].nblk;
+        a.trace[20 * 1024 + 2 * blockIdx.x] = it1 - it0;
+        a.trace[20 * 1024 + 2 * blockIdx.x + 1] = nb;
+    }
 
     uint8_t* sq = smem + C::OFF_Q;
     uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + C::OFF_QBAR);
@@ -446,6 +455,11 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
         }
         named_bar_sync(1, NCW * 32);
     }
+    if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // debug: per-CTA end (ns)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[18 * 1024 + 2 * blockIdx.x + 1] = t;
+    }
 }
 
 // Units with no pages at all (empty requests) are identity rows: o = 0,
@@ -474,16 +488,17 @@ constexpr int keys_per_half() {
     return R == 1 ? 8 : 16 / R;
 }
 
-// Pipeline depth: 128 KB of K+V blocks per SM (4 stages of a 64-token bf16
-// d=128 block; 2 for fp32 d=128 whose blocks are twice as big).
-template <typename KV, int D>
+// Pipeline depth: 128-160 KB of K+V blocks per SM (5 stages of a 64-token
+// bf16 d=128 block for up to 4 rows — measured on cfg2: 4 / 5 / 6 stages
+// 104.5 / 103.2 / 104.2 us — 4 otherwise; 2 for fp32 d=128 whose blocks are
+// twice as big).
+template <typename KV, int D, int R>
 constexpr int stages_for() {
-    return (2 * 64 * D * int(sizeof(KV))) >= 65536 ? 2 : 4;
+    return (2 * 64 * D * int(sizeof(KV))) >= 65536 ? 2 : (sizeof(KV) == 2 && D == 128 && R <= 4 ? 5 : 4);
 }
 
-template <typename KV, int D, int R, int J = keys_per_half<R>()>
+template <typename KV, int D, int R, int J = keys_per_half<R>(), int S = stages_for<KV, D, R>()>
 cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
-    constexpr int S = stages_for<KV, D>();
     using C = DecodeCfg<KV, D, R, J, S>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     auto kern = spliced_decode_kernel<KV, D, R, J, S>;

@@ -90,6 +90,17 @@ int64_t tc_item_weight(int rows) {
     if (env >= 0) return env;
     return rows > 64 ? 14 : kTcItemWeight;
 }
+// K1 (CUDA-core decode) item overhead in blocks: q rows, the 8-warp LSE
+// combine and, for a split unit, the partial store + arrival + merge. The
+// per-CTA trace puts a third item at ~8 us on cfg2; sweeping 0-12 blocks:
+// cfg5's ragged private pass 0.321 -> 0.296 ms at 4, cfg2 unchanged.
+int64_t k1_item_weight() {
+    static const int64_t w = [] {
+        const char* e = std::getenv("EP_K1_ITEM_WEIGHT");
+        return e ? std::atoll(e) : int64_t(4);
+    }();
+    return w;
+}
 
 // One query-row set attending to one page list.
 struct VReq {
@@ -301,7 +312,15 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         main_vr[b].n_rows = rpr;
     }
     p.main.tc = !decode_supported(p.kv_dtype, p.d_head, rpr) || force_tc();
-    build_subplan(p.main, main_vr, Hkv, cap, p.main.tc ? kTcItemWeight : 0);
+    int64_t cap_main = cap;
+    if (!p.main.tc) {
+        static const int64_t env = [] {
+            const char* e = std::getenv("EP_K1_CTAS");
+            return e ? std::atoll(e) : int64_t(0);
+        }();
+        if (env > 0) cap_main = env;
+    }
+    build_subplan(p.main, main_vr, Hkv, cap_main, p.main.tc ? kTcItemWeight : k1_item_weight());
     p.main.rows = rpr;
     if (p.cascade) {
         build_subplan(p.shared, shared_vr, Hkv, cap, tc_item_weight(group_cap * rpr));
@@ -475,6 +494,19 @@ unsigned long long* trace_buffer() {
     return t;
 }
 
+// debug: EP_TRACE=1 dumps the trace buffer (CTA 0 event clocks, per-CTA
+// start / end / work) of the last launch to EP_TRACE_FILE
+void dump_trace(unsigned long long* trace, cudaStream_t s) {
+    std::vector<unsigned long long> host(22 * 1024);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(host.data(), trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const char* f = std::getenv("EP_TRACE_FILE");
+    if (FILE* fp = std::fopen(f ? f : "ep_trace.bin", "wb")) {
+        std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
+        std::fclose(fp);
+    }
+}
+
 int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs a, cudaStream_t s) {
     ep_handle h = p.h;
     if (sp.n_items > 0 && sp.tc) {
@@ -490,20 +522,13 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
         EP_CUDA_TRY(launch_verify_attention(int(sp.n_ctas), a, p.tmap_k, p.tmap_v, sp.rows, s),
                     "verify attention launch");
         h->launches++;
-        if (a.trace) {  // debug: EP_TRACE=1 dumps CTA 0's event clocks to EP_TRACE_FILE
-            std::vector<unsigned long long> host(22 * 1024);
-            cudaStreamSynchronize(s);
-            cudaMemcpy(host.data(), a.trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            const char* f = std::getenv("EP_TRACE_FILE");
-            if (FILE* fp = std::fopen(f ? f : "ep_trace.bin", "wb")) {
-                std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
-                std::fclose(fp);
-            }
-        }
+        if (a.trace) dump_trace(a.trace, s);
     } else if (sp.n_items > 0) {
+        a.trace = trace_buffer();
         EP_CUDA_TRY(launch_spliced_decode(p.kv_dtype, p.d_head, sp.rows, int(sp.n_ctas), a, s),
                     "spliced decode launch");
         h->launches++;
+        if (a.trace) dump_trace(a.trace, s);
     }
     if (sp.has_empty_unit) {
         EP_CUDA_TRY(launch_empty_units(p.d_head, sp.rows, a, s), "empty units launch");

@@ -64,7 +64,7 @@ def _read_device(ptr, n, tdtype):
     (err,) = rt.cudaMemcpy(out.data_ptr(), ptr, n * out.element_size(),
                            rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
     assert err == rt.cudaError_t.cudaSuccess
-    return out.cpu().numpy().astype(np.float64)
+    return out.cpu().to(torch.float64).numpy()
 
 
 def test_weights_are_the_reference_draws(cuda_handle):
@@ -292,10 +292,17 @@ def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv):
             toks.append(t)
         assert got[b] == toks, b
         assert s1[b][0].end_position() == c.end_position()
+    # cached K: bit-identical in fp64 (same kernels, same order); in fp32 /
+    # bf16 the spliced-decode plan of the rollout (built once for the final
+    # length) splits the keys differently from the per-step plans, so the fp32
+    # summation order differs in the last bits
+    tdt = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}[kv]
     for layer in range(CFG1[0]):
         p1, p2 = m1.kv_pool(layer), m2.kv_pool(layer)
-        esz = {"f64": 8, "f32": 4, "bf16": 2}[kv]
-        n = p1.num_pages * p1.n_kv_heads * p1.page_tokens * p1.d_head * esz // 8
-        a = _read_device(p1.k_pages, n, torch.float64)
-        b2 = _read_device(p2.k_pages, n, torch.float64)
-        np.testing.assert_array_equal(a, b2)
+        n = p1.num_pages * p1.n_kv_heads * p1.page_tokens * p1.d_head
+        a = _read_device(p1.k_pages, n, tdt)
+        b2 = _read_device(p2.k_pages, n, tdt)
+        if kv == "f64":
+            np.testing.assert_array_equal(a, b2)
+        else:
+            assert rel_err(a, b2) <= (1e-5 if kv == "f32" else 1e-2)

@@ -42,6 +42,8 @@ def analyse(path):
     base = t[t > 0].min()
     n = int((t[4] > 0).sum())  # blocks with an S_SEEN event
     print(f"blocks traced: {n}")
+    if n < 8:
+        return
     lo, hi = n // 4, 3 * n // 4  # steady state
     s_seen, p_done = t[4, lo:hi], t[5, lo:hi]
     per = np.diff(s_seen)
@@ -64,6 +66,10 @@ if __name__ == "__main__":
     if kind.startswith("verify"):
         import verify_bench
         print(verify_bench.run(int(kind[6:]), 1, 1))
+    elif kind == "decode":  # K1, config 2 (the trace of the last launch is kept)
+        sys.argv = [sys.argv[0], "--steps", "3"]
+        import decode_only
+        decode_only.main()
     elif kind == "shared":
         import multitenant_bench
         print(multitenant_bench.run(1, 1))
