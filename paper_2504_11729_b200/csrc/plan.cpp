@@ -209,6 +209,9 @@ struct ep_plan_s {
     int64_t num_pages = 0;
     int32_t n_q_heads = 0, n_q = 0, batch = 0, rows = 0;
     bool cascade = false;
+    bool concurrent = false;          // cascade passes on disjoint SM sets, side by side
+    cudaStream_t side = nullptr;      // the shared-prefix pass's stream (concurrent cascade)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool prefill = false;             // prefill plan: virtual requests = query chunks
     std::vector<int32_t> q_row0;      // prefill: first q/o token row per virtual request
     SubPlan main;    // whole table (non-cascade) or the private remainders (cascade)
@@ -227,10 +230,23 @@ struct ep_plan_s {
     ~ep_plan_s() {
         if (h_stage) cudaFreeHost(h_stage);
         if (staged) cudaEventDestroy(staged);
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
     }
 };
 
 namespace {
+
+// EP_CASCADE_SERIAL=1 runs the two cascade passes one after the other on
+// all SMs (the pre-overlap schedule, kept for comparison).
+bool concurrent_cascade() {
+    static const bool serial = [] {
+        const char* e = std::getenv("EP_CASCADE_SERIAL");
+        return e && e[0] == '1';
+    }();
+    return !serial;
+}
 
 bool cascade_allowed(const ep_plan_s& p) {
     static const bool off = [] {
@@ -312,7 +328,31 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         main_vr[b].n_rows = rpr;
     }
     p.main.tc = !decode_supported(p.kv_dtype, p.d_head, rpr) || force_tc();
-    int64_t cap_main = cap;
+    int64_t cap_main = cap, cap_shared = cap;
+    if (p.cascade && !p.main.tc && concurrent_cascade()) {
+        // The shared-prefix tiles (K3: tensor / MUFU bound, ~35 MB of K/V)
+        // and the private remainders (K1: HBM bound) run side by side on
+        // disjoint SMs; the SMs are split in proportion to their estimated
+        // times (per 64-key block: K3 128-row tile ~0.70 us beside K1, K1
+        // ~0.80 us — per-CTA trace, tools/trace_k3.py; an SM-count sweep on
+        // config 5 puts the optimum at 24-25 of 148 SMs for the shared pass).
+        int64_t sb = 0, mb = 0;
+        for (const VReq& v : shared_vr)
+            for (const PageDesc& d : v.pages) sb += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+        for (const VReq& v : main_vr)
+            for (const PageDesc& d : v.pages) mb += (d.n_tok + kBlockTokens - 1) / kBlockTokens;
+        const double ts = 0.70 * double(sb), tm = 0.80 * double(mb);
+        cap_shared = std::max<int64_t>(1, std::min<int64_t>(cap - 1, int64_t(double(cap) * ts / (ts + tm) + 0.5)));
+        static const int64_t env_sh = [] {
+            const char* e = std::getenv("EP_CASCADE_SHARED_CTAS");
+            return e ? std::atoll(e) : int64_t(0);
+        }();
+        if (env_sh > 0 && env_sh < cap) cap_shared = env_sh;
+        cap_main = cap - cap_shared;
+        p.concurrent = true;
+    } else {
+        p.concurrent = false;
+    }
     if (!p.main.tc) {
         static const int64_t env = [] {
             const char* e = std::getenv("EP_K1_CTAS");
@@ -323,7 +363,7 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
     build_subplan(p.main, main_vr, Hkv, cap_main, p.main.tc ? kTcItemWeight : k1_item_weight());
     p.main.rows = rpr;
     if (p.cascade) {
-        build_subplan(p.shared, shared_vr, Hkv, cap, tc_item_weight(group_cap * rpr));
+        build_subplan(p.shared, shared_vr, Hkv, cap_shared, tc_item_weight(group_cap * rpr));
         p.shared.rows = group_cap * rpr;
         p.shared.tc = true;
     }
@@ -669,9 +709,25 @@ int ep_spliced_attention(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t
     float* po = static_cast<float*>(p->d_parts_o.ptr);
     float* pl = static_cast<float*>(p->d_parts_lse.ptr);
     DecodeArgs as = make_args(*p, p->shared, pool, q_dtype, q, EP_F32, po, pl, o_dtype);
-    if (int rc = launch_subplan(*p, p->shared, pool, as, s)) return rc;
     DecodeArgs am = make_args(*p, p->main, pool, q_dtype, q, EP_F32, po + rows * p->d_head, pl + rows, o_dtype);
-    if (int rc = launch_subplan(*p, p->main, pool, am, s)) return rc;
+    if (p->concurrent) {
+        // fork: the shared pass on the side stream, the private pass here;
+        // each kernel's grid is its SM share, so they run side by side
+        if (!p->side) {
+            EP_CUDA_TRY(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "cascade stream");
+            EP_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "cascade event");
+            EP_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "cascade event");
+        }
+        EP_CUDA_TRY(cudaEventRecord(p->ev_fork, s), "cascade fork");
+        EP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0), "cascade fork");
+        if (int rc = launch_subplan(*p, p->shared, pool, as, p->side)) return rc;
+        if (int rc = launch_subplan(*p, p->main, pool, am, s)) return rc;
+        EP_CUDA_TRY(cudaEventRecord(p->ev_join, p->side), "cascade join");
+        EP_CUDA_TRY(cudaStreamWaitEvent(s, p->ev_join, 0), "cascade join");
+    } else {
+        if (int rc = launch_subplan(*p, p->shared, pool, as, s)) return rc;
+        if (int rc = launch_subplan(*p, p->main, pool, am, s)) return rc;
+    }
     EP_CUDA_TRY(launch_cascade_merge(int(rows), p->d_head, p->n_q * p->n_q_heads, po, pl,
                                      static_cast<const uint8_t*>(p->d_has_shared.ptr), o, o_dtype, lse, s),
                 "cascade merge launch");
