@@ -9,7 +9,8 @@ import os
 import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_lib", "libep_b200.so")
+# EP_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("EP_LIB") or os.path.join(PKG, "_lib", "libep_b200.so")
 HEADER = os.path.join(os.path.dirname(PKG), "include", "ep", "ep_attn.h")
 HEADERS = [HEADER, os.path.join(os.path.dirname(PKG), "include", "ep", "ep_model.h")]
 
