@@ -19,6 +19,9 @@
 //   * accept: per request, decode g_j and apply the acceptance rule.
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "ep_common.cuh"
 #include "ep_internal.h"
@@ -33,7 +36,7 @@ constexpr int kABytes = kTM * kTK * 2;  // 16 KB
 constexpr int kBBytes = kTN * kTK * 2;  // 32 KB
 constexpr int kStage = kABytes + kBBytes;
 constexpr int kScoreThreads = 192;  // warps 0-3 epilogue, 4 TMA, 5 MMA
-constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256;
+constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256 + kTN * 4;  // stages, barriers, colsum slice
 constexpr uint32_t kIdescScore = umma::idesc_bf16_f32(kTM, kTN, false, false);
 
 __device__ __forceinline__ uint64_t order_key(float z, uint32_t idx) {
@@ -114,7 +117,14 @@ struct ScoreArgs {
     const float* colsum;
     unsigned long long* best;  // [rows] packed (z, ~idx), zero-initialised
     float* logits;             // optional [rows][vocab]: rstd * z (= LN(x) @ W)
+    unsigned long long* trace; // debug (EP_TRACE=1): per CTA [start, first stage, mma done, end] ns
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(kScoreThreads, 1)
     score_argmax_kernel(const ScoreArgs sa, const __grid_constant__ CUtensorMap tmap_a,
@@ -129,6 +139,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * kTM, n0 = blockIdx.y * kTN;
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta] = gtimer();
     const int nkw = sa.width / kTK;         // k-blocks of W per pass
     const int nk = nkw * sa.a_passes;        // A is [hi | lo] when a_passes == 2
 
@@ -166,6 +178,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             for (int kb = 0; kb < nk; ++kb) {
                 const int s = kb % kStagesS;
                 mbar_wait(&full[s], (kb / kStagesS) & 1);
+                if (kb == 0 && sa.trace) sa.trace[4 * cta + 1] = gtimer();
                 umma::fence_after_sync();
                 const uint32_t a_addr = base + s * kStage, b_addr = a_addr + kABytes;
 #pragma unroll
@@ -179,31 +192,38 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             umma::mma_commit(acc_full);
         }
     } else {
-        // epilogue: thread = row (TMEM lane), 256 vocab columns
+        // epilogue: thread = row (TMEM lane), 256 vocab columns. The tile's
+        // colsum slice and the row's mean are fetched while the MMAs run; TMEM
+        // is read 64 columns per wait.
         const int row = warp * 32 + lane;
         const int grow = m0 + row;
-        mbar_wait(acc_full, 0);
-        umma::fence_after_sync();
+        float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTN] colsum of this tile
+        for (int i = threadIdx.x; i < kTN; i += 128) s_cs[i] = sa.colsum[n0 + i];
         const bool valid = grow < sa.rows;
         const float mu = valid ? sa.mean[grow] : 0.f;
         const float rs = valid ? sa.rstd[grow] : 0.f;
+        named_bar_sync(1, 128);
+        mbar_wait(acc_full, 0);
+        if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 2] = gtimer();
+        umma::fence_after_sync();
         float best = -INFINITY;
         uint32_t best_i = 0;
 #pragma unroll 1
-        for (int c = 0; c < kTN / 32; ++c) {
-            uint32_t r[32];
-            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32, r);
+        for (int c = 0; c < kTN / 32; c += 2) {
+            uint32_t r[64];
+            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r));
+            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32 + 32,
+                            *reinterpret_cast<uint32_t(*)[32]>(r + 32));
             umma::tmem_wait_ld();
             if (valid) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int n = n0 + c * 32 + j;
-                    const float z = __uint_as_float(r[j]) - mu * sa.colsum[n];
-                    if (z > best) {  // strict: ties keep the lowest id
-                        best = z;
-                        best_i = uint32_t(n);
-                    }
-                    if (sa.logits) sa.logits[size_t(grow) * sa.vocab + n] = z * rs;
+                for (int j = 0; j < 64; ++j) {
+                    const int nl = c * 32 + j;
+                    const float z = fmaf(-mu, s_cs[nl], __uint_as_float(r[j]));
+                    const bool up = z > best;  // strict: ties keep the lowest id
+                    best = up ? z : best;
+                    best_i = up ? uint32_t(n0 + nl) : best_i;
+                    if (sa.logits) sa.logits[size_t(grow) * sa.vocab + n0 + nl] = z * rs;
                 }
             }
         }
@@ -215,6 +235,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         umma::fence_after_sync();
         umma::tmem_dealloc(tmem, 256);
     }
+    if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 3] = gtimer();
 }
 
 // g_j from the packed keys; n = longest draft prefix reproduced by the target.
@@ -268,9 +289,26 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
             static_cast<const __nv_bfloat16*>(attn_out), width, mean, rstd, nullptr);
     cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
     if (e != cudaSuccess) return e;
-    ScoreArgs sa{rows, width, vocab, split ? 2 : 1, mean, rstd, colsum, best, logits};
+    static unsigned long long* trace = [] {
+        unsigned long long* b = nullptr;
+        const char* e = std::getenv("EP_TRACE");
+        if (e && e[0] == '1' && cudaMalloc(&b, 4096 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 4096 * sizeof(unsigned long long));
+        return b;
+    }();
+    ScoreArgs sa{rows, width, vocab, split ? 2 : 1, mean, rstd, colsum, best, logits, trace};
     dim3 grid((rows + kTM - 1) / kTM, vocab / kTN);
     score_argmax_kernel<<<grid, kScoreThreads, kScoreSmem, s>>>(sa, tmap_a, tmap_w);
+    if (trace) {  // debug: dump the per-CTA timeline of this launch
+        std::vector<unsigned long long> host(4096);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(host.data(), trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        const char* f = std::getenv("EP_TRACE_SCORE_FILE");
+        if (FILE* fp = std::fopen(f ? f : "ep_trace_score.bin", "wb")) {
+            std::fwrite(host.data(), sizeof(unsigned long long), host.size(), fp);
+            std::fclose(fp);
+        }
+    }
     accept_kernel<<<(batch + 127) / 128, 128, 0, s>>>(best, batch, n_q, drafts, target, n_accepted);
     return cudaGetLastError();
 }
