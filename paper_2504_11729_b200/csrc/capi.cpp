@@ -315,7 +315,7 @@ struct ep_verifier_s {
     int32_t width = 0, vocab = 0;
     const void* w_t = nullptr;
     CUtensorMap tmap_w{};
-    DeviceBuffer colsum, mean, rstd, best, split;
+    DeviceBuffer colsum, mean, rstd, best, split, wmax2, ebound, cand_cnt, cand_n, cand_z;
     CUtensorMap tmap_a{};
     const void* a_ptr = nullptr;
     int32_t a_rows = -1, a_dtype = -1;
@@ -336,9 +336,11 @@ int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_verifier_create");
     if (int rc = encode_bf16_2d(&v->tmap_w, w_score_t, uint64_t(width), uint64_t(vocab), 64, 256)) return rc;
     EP_CUDA_TRY(v->colsum.reserve(size_t(vocab) * sizeof(float)), "ep_verifier_create colsum");
-    EP_CUDA_TRY(launch_colsum(w_score_t, width, vocab, static_cast<float*>(v->colsum.ptr), h->stream),
+    EP_CUDA_TRY(v->wmax2.reserve(sizeof(float)), "ep_verifier_create colnorm");
+    EP_CUDA_TRY(launch_colsum(w_score_t, width, vocab, static_cast<float*>(v->colsum.ptr),
+                              static_cast<float*>(v->wmax2.ptr), h->stream),
                 "colsum launch");
-    h->launches++;
+    h->launches += 2;
     EP_CUDA_TRY(cudaStreamSynchronize(h->stream), "ep_verifier_create sync");
     *out = v.release();
     return EP_OK;
@@ -364,11 +366,25 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
     void* split = nullptr;
     const void* a_src = attn_out;
     uint64_t a_inner = uint64_t(v->width);
+    RefineArgs rf;
+    if (attn_dtype == EP_F32 && v->width > 4096)
+        return fail(EP_EUNSUPPORTED, "ep_verify_greedy: fp32 attention rows wider than 4096");
     if (attn_dtype == EP_F32) {
-        EP_CUDA_TRY(v->split.reserve(size_t(rows) * 2 * v->width * 2), "ep_verify_greedy ws");
+        // the bf16 hi part of the rows is the GEMM's A operand
+        EP_CUDA_TRY(v->split.reserve(size_t(rows) * v->width * 2), "ep_verify_greedy ws");
+        EP_CUDA_TRY(v->ebound.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
+        const size_t slots = size_t(v->vocab) / 256 * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
+        EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * (v->vocab / 256) * sizeof(int32_t)), "ep_verify_greedy ws");
+        EP_CUDA_TRY(v->cand_n.reserve(size_t(rows) * slots * sizeof(int32_t)), "ep_verify_greedy ws");
+        EP_CUDA_TRY(v->cand_z.reserve(size_t(rows) * slots * sizeof(float)), "ep_verify_greedy ws");
         split = v->split.ptr;
         a_src = split;
-        a_inner = 2 * uint64_t(v->width);
+        rf.wt = v->w_t;
+        rf.wmax2 = static_cast<const float*>(v->wmax2.ptr);
+        rf.ebound = static_cast<float*>(v->ebound.ptr);
+        rf.cand_cnt = static_cast<int32_t*>(v->cand_cnt.ptr);
+        rf.cand_n = static_cast<int32_t*>(v->cand_n.ptr);
+        rf.cand_z = static_cast<float*>(v->cand_z.ptr);
     }
     if (v->a_ptr != a_src || v->a_rows != rows || v->a_dtype != attn_dtype) {
         if (int rc = encode_bf16_2d(&v->tmap_a, a_src, a_inner, uint64_t(rows), 64, 128)) return rc;
@@ -380,9 +396,9 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
                                     static_cast<const float*>(v->colsum.ptr),
                                     static_cast<float*>(v->mean.ptr), static_cast<float*>(v->rstd.ptr),
                                     static_cast<unsigned long long*>(v->best.ptr), logits, batch, n_q,
-                                    drafts, target_ids, n_accepted, static_cast<cudaStream_t>(stream)),
+                                    drafts, target_ids, n_accepted, rf, static_cast<cudaStream_t>(stream)),
                 "score/accept launch");
-    h->launches += 3;
+    h->launches += split ? 4 : 3;
     return EP_OK;
 }
 

@@ -155,12 +155,23 @@ cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUten
                                     const CUtensorMap& tv, int rows, cudaStream_t s);
 
 // K4: score GEMM (tcgen05) + LN-folded argmax + greedy accept.
-cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, cudaStream_t s);
+cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, float* wmax2, cudaStream_t s);
+// fp32 attention rows: hi-only GEMM + exact refinement of the candidates
+// within the per-row error bound (kern_score.cu).
+constexpr int kScoreCandPerTile = 16;  // candidate slots per (row, 256-wide vocab tile)
+struct RefineArgs {
+    const void* wt = nullptr;      // W^T bf16 [vocab][width]
+    const float* wmax2 = nullptr;  // max_n ||W^T[n]||_2
+    float* ebound = nullptr;       // [rows]
+    int32_t* cand_cnt = nullptr;   // [rows][vocab / 256]
+    int32_t* cand_n = nullptr;     // [rows][vocab / 256][kScoreCandPerTile]
+    float* cand_z = nullptr;       // [rows][vocab / 256][kScoreCandPerTile]
+};
 cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
                                 const float* colsum, float* mean, float* rstd,
                                 unsigned long long* best, float* logits, int batch, int n_q,
                                 const int32_t* drafts, int32_t* target, int32_t* n_accepted,
-                                cudaStream_t s);
+                                const RefineArgs& rf, cudaStream_t s);
 
 }  // namespace ep

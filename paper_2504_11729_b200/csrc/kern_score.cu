@@ -16,6 +16,17 @@
 //     argmax, so the epilogue ranks z = x.w - mean * colsum(w) and reduces
 //     (z, lowest index) across the vocab tiles with one 64-bit atomicMax per
 //     row per CTA on an order-preserving key.
+//   * fp32 attention rows (the verify default) are scored in two steps
+//     rather than one bf16 hi+lo GEMM of twice the K: the GEMM runs on the
+//     bf16 hi part of the centred row xc = x - mean (LN(x).w = rstd * xc.w
+//     ranks like xc.w); since xc = hi + lo exactly, every logit satisfies
+//     |z - z_hi| <= E_row = max_n ||w_n||_2 * (||lo||_2 + 2^-12 ||xc||_2)
+//     (Cauchy-Schwarz on the lo term + the fp32 accumulation bound), so only
+//     vocab entries within 2 E_row of the row's best z_hi can be its argmax.
+//     The GEMM epilogue emits those candidates per tile; refine_kernel
+//     computes their logits exactly (fp32 dot of the centred fp32 row with
+//     the bf16 W row) and picks the first maximum — the ids of the
+//     full-precision product at half the tensor work.
 //   * accept: per request, decode g_j and apply the acceptance rule.
 #include <cmath>
 #include <cstdint>
@@ -36,7 +47,7 @@ constexpr int kABytes = kTM * kTK * 2;  // 16 KB
 constexpr int kBBytes = kTN * kTK * 2;  // 32 KB
 constexpr int kStage = kABytes + kBBytes;
 constexpr int kScoreThreads = 192;  // warps 0-3 epilogue, 4 TMA, 5 MMA
-constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256 + kTN * 4;  // stages, barriers, colsum slice
+constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256 + kTN * 4 + 24 * 128 * 5;  // stages, barriers, colsum slice, stash
 constexpr uint32_t kIdescScore = umma::idesc_bf16_f32(kTM, kTN, false, false);
 
 __device__ __forceinline__ uint64_t order_key(float z, uint32_t idx) {
@@ -99,6 +110,99 @@ __global__ void row_stats_kernel(const T* __restrict__ x, int width, float* __re
     }
 }
 
+// fp32 rows: mean, 1/sqrt(var + 1e-5) (two-pass, from registers), the bf16 hi
+// part (the GEMM's A operand) and the refinement bound E_row. 128 threads per
+// row, 8 float4 per thread (width <= 4096).
+constexpr int kStatThreads = 128;
+constexpr int kStatVec = 8;
+__global__ void __launch_bounds__(kStatThreads)
+    row_stats_split_kernel(const float* __restrict__ x, int width, float* __restrict__ mean,
+                           float* __restrict__ rstd, __nv_bfloat16* __restrict__ hi_out,
+                           const float* __restrict__ wmax2, float* __restrict__ ebound) {
+    const int row = blockIdx.x, tid = threadIdx.x;
+    const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * width);
+    const int nv = width / 4;
+    __shared__ float red[3][kStatThreads / 32];
+    float4 v[kStatVec];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kStatVec; ++i) {
+        const int c = tid + i * kStatThreads;
+        v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) red[0][tid >> 5] = s;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < kStatThreads / 32; ++w) tot += red[0][w];
+    const float mu = tot / float(width);
+    // the centred row xc = x - mean is what gets scored: LN(x).w = rstd *
+    // xc.w ranks like xc.w, and the hi / lo split of xc (not of x) keeps the
+    // refinement bound proportional to the logit spread
+    float q = 0.f, lo2 = 0.f;
+    uint2* ho = reinterpret_cast<uint2*>(hi_out + size_t(row) * width);
+#pragma unroll
+    for (int i = 0; i < kStatVec; ++i) {
+        const int c = tid + i * kStatThreads;
+        if (c < nv) {
+            const float e[4] = {v[i].x - mu, v[i].y - mu, v[i].z - mu, v[i].w - mu};
+            uint32_t hp[2];
+#pragma unroll
+            for (int k = 0; k < 4; k += 2) {
+                const __nv_bfloat162 h = __floats2bfloat162_rn(e[k], e[k + 1]);
+                hp[k / 2] = *reinterpret_cast<const uint32_t*>(&h);
+                const float2 hf = __bfloat1622float2(h);
+                const float l0 = e[k] - hf.x, l1 = e[k + 1] - hf.y;  // exact
+                lo2 += l0 * l0 + l1 * l1;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) q += e[k] * e[k];
+            ho[c] = make_uint2(hp[0], hp[1]);
+        }
+    }
+    float x2 = q;
+    q = warp_sum(q);
+    lo2 = warp_sum(lo2);
+    x2 = warp_sum(x2);
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = q;
+        red[1][tid >> 5] = lo2;
+        red[2][tid >> 5] = x2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float tq = 0.f, tl = 0.f, tx = 0.f;
+#pragma unroll
+        for (int w = 0; w < kStatThreads / 32; ++w) {
+            tq += red[0][w];
+            tl += red[1][w];
+            tx += red[2][w];
+        }
+        mean[row] = mu;
+        rstd[row] = rsqrtf(tq / float(width) + 1e-5f);
+        // |xc.w - hi.w| <= ||lo|| ||w||; fp32 accumulation of hi.w <= 2^-12 ||xc|| ||w||
+        // (<= 4096 terms); 1 % slack for the rounding of the bound itself
+        ebound[row] = 1.01f * (*wmax2) * (sqrtf(tl) + 0x1.0p-12f * sqrtf(tx));
+    }
+}
+
+// max_n ||W^T[n]||_2 (once per W), as float bits (non-negative: integer order).
+__global__ void colnorm_max_kernel(const __nv_bfloat16* __restrict__ wt, int width, int vocab,
+                                   float* __restrict__ wmax2) {
+    const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (n >= vocab) return;
+    float s = 0.f;
+    for (int c = threadIdx.x & 31; c < width; c += 32) {
+        const float w = __bfloat162float(wt[size_t(n) * width + c]);
+        s += w * w;
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0)
+        atomicMax(reinterpret_cast<unsigned int*>(wmax2), __float_as_uint(sqrtf(s) * 1.0001f));
+}
+
 // colsum[n] = sum_k W^T[n][k] (once per W).
 __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ wt, int width, int vocab,
                               float* __restrict__ colsum) {
@@ -110,6 +214,9 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ wt, int width, i
     if ((threadIdx.x & 31) == 0) colsum[n] = s;
 }
 
+constexpr int kPerTile = kScoreCandPerTile;  // candidates kept per (row, vocab tile) (overflow -> every n exactly)
+constexpr int kStash = 24;  // per-thread candidate stash of the epilogue (smem)
+
 struct ScoreArgs {
     int rows, width, vocab, a_passes;
     const float* mean;
@@ -118,6 +225,12 @@ struct ScoreArgs {
     unsigned long long* best;  // [rows] packed (z, ~idx), zero-initialised
     float* logits;             // optional [rows][vocab]: rstd * z (= LN(x) @ W)
     unsigned long long* trace; // debug (EP_TRACE=1): per CTA [start, first stage, mma done, end] ns
+    // hi-only pass (fp32 rows): per-(row, vocab tile) candidates for refine_kernel
+    const float* ebound;       // [rows] |z - z_hi| bound
+    int32_t* cand_cnt;         // [rows][n_tiles]
+    int32_t* cand_n;           // [rows][n_tiles][kPerTile]
+    float* cand_z;             // [rows][n_tiles][kPerTile]
+    int n_tiles;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -200,7 +313,8 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTN] colsum of this tile
         for (int i = threadIdx.x; i < kTN; i += 128) s_cs[i] = sa.colsum[n0 + i];
         const bool valid = grow < sa.rows;
-        const float mu = valid ? sa.mean[grow] : 0.f;
+        // (rows already centred for the hi-only pass: no mean * colsum term)
+        const float mu = valid && !sa.cand_n ? sa.mean[grow] : 0.f;
         const float rs = valid ? sa.rstd[grow] : 0.f;
         named_bar_sync(1, 128);
         mbar_wait(acc_full, 0);
@@ -208,6 +322,17 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         umma::fence_after_sync();
         float best = -INFINITY;
         uint32_t best_i = 0;
+        // hi-only pass: every n of the tile that can still be the row's
+        // argmax has z_hi >= tile max - 2 E_row (the row max is >= the tile
+        // max). One TMEM pass: after each 64-column chunk, the chunk's values
+        // within 2 E_row of the running max go to a per-thread smem stash (a
+        // superset: the max only grows), filtered by the final max at the end.
+        const bool emit = sa.cand_n != nullptr;
+        const float eb2 = emit && valid ? 2.f * sa.ebound[grow] : 0.f;
+        float* st_z = reinterpret_cast<float*>(s_cs + kTN);                 // [kStash][128]
+        uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * 128);    // [kStash][128]
+        const int me = threadIdx.x;
+        int n_st = 0;
 #pragma unroll 1
         for (int c = 0; c < kTN / 32; c += 2) {
             uint32_t r[64];
@@ -220,14 +345,49 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
                 for (int j = 0; j < 64; ++j) {
                     const int nl = c * 32 + j;
                     const float z = fmaf(-mu, s_cs[nl], __uint_as_float(r[j]));
+                    r[j] = __float_as_uint(z);
                     const bool up = z > best;  // strict: ties keep the lowest id
                     best = up ? z : best;
                     best_i = up ? uint32_t(n0 + nl) : best_i;
                     if (sa.logits) sa.logits[size_t(grow) * sa.vocab + n0 + nl] = z * rs;
                 }
+                if (emit) {
+                    const float thr = best - eb2;
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) {
+                        const float z = __uint_as_float(r[j]);
+                        if (z >= thr) {
+                            if (n_st < kStash) {
+                                st_z[n_st * 128 + me] = z;
+                                st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
+                            }
+                            ++n_st;
+                        }
+                    }
+                }
             }
         }
         if (valid) atomicMax(&sa.best[grow], order_key(best, best_i));
+        if (emit && valid) {
+            const float thr = best - eb2;
+            const size_t slot0 = (size_t(grow) * sa.n_tiles + blockIdx.y) * kPerTile;
+            int cnt = 0;
+            if (n_st > kStash) {
+                cnt = kPerTile + 1;  // stash overflow: refine scores the whole row
+            } else {
+                for (int i = 0; i < n_st; ++i) {
+                    const float z = st_z[i * 128 + me];
+                    if (z >= thr) {
+                        if (cnt < kPerTile) {
+                            sa.cand_n[slot0 + cnt] = n0 + st_n[i * 128 + me];
+                            sa.cand_z[slot0 + cnt] = z;
+                        }
+                        ++cnt;
+                    }
+                }
+            }
+            sa.cand_cnt[size_t(grow) * sa.n_tiles + blockIdx.y] = cnt;
+        }
     }
     umma::fence_before_sync();
     __syncthreads();
@@ -236,6 +396,90 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         umma::tmem_dealloc(tmem, 256);
     }
     if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 3] = gtimer();
+}
+
+__device__ __forceinline__ float key_value(unsigned long long k) {
+    uint32_t b = uint32_t(k >> 32);
+    b = (b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b;
+    return __uint_as_float(b);
+}
+
+constexpr int kRefineThreads = 256;
+constexpr int kMaxList = 512;  // candidate list of one row (n_tiles * kPerTile)
+
+// Per row: of the candidates the GEMM epilogue kept, those with z_hi >= row
+// max z_hi - 2 E_row get their exact logit z = (x - mean) . w_n (the centred
+// fp32 row staged in smem, one block-wide dot per candidate); the first
+// maximum -> best[row]. With `logits` every logit is computed exactly and
+// written scaled by rstd (diagnostics); a candidate overflow does the same.
+__global__ void __launch_bounds__(kRefineThreads)
+    refine_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ wt, int width, int vocab,
+                  int n_tiles, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_n,
+                  const float* __restrict__ cand_z, const float* __restrict__ mean, const float* __restrict__ rstd,
+                  const float* __restrict__ colsum, const float* __restrict__ ebound,
+                  unsigned long long* __restrict__ best, float* __restrict__ logits) {
+    const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    extern __shared__ float4 s_x4[];  // [width / 4]
+    __shared__ int s_list[kMaxList];
+    __shared__ int s_n;
+    __shared__ bool s_all;
+    __shared__ float s_red[kRefineThreads / 32];
+    const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * width);
+    const float mu = mean[row];
+    for (int i = tid; i < width / 4; i += kRefineThreads) {  // the centred row
+        const float4 v = xr[i];
+        s_x4[i] = make_float4(v.x - mu, v.y - mu, v.z - mu, v.w - mu);
+    }
+    // gather (all threads): the per-tile counts, then one slot per thread
+    if (tid == 0) {
+        s_all = logits != nullptr || n_tiles * kPerTile > kMaxList || n_tiles > kRefineThreads;
+        s_n = 0;
+    }
+    __syncthreads();
+    if (tid < n_tiles && cand_cnt[size_t(row) * n_tiles + tid] > kPerTile) s_all = true;
+    const float thresh = key_value(best[row]) - 2.f * ebound[row];
+    __syncthreads();
+    if (!s_all) {
+        for (int sl = tid; sl < n_tiles * kPerTile; sl += kRefineThreads) {
+            const int t = sl / kPerTile, i = sl % kPerTile;
+            const size_t b = (size_t(row) * n_tiles + t) * kPerTile + i;
+            if (i < cand_cnt[size_t(row) * n_tiles + t] && cand_z[b] >= thresh)
+                s_list[atomicAdd(&s_n, 1)] = cand_n[b];
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && s_all) s_n = vocab;
+    __syncthreads();
+    const bool all = s_all;
+    const int count = s_n;
+    unsigned long long top = 0ull;
+    for (int i = 0; i < count; ++i) {
+        const int n = all ? i : s_list[i];
+        const uint2* wr = reinterpret_cast<const uint2*>(wt + size_t(n) * width);
+        float acc = 0.f;
+        for (int c = tid; c < width / 4; c += kRefineThreads) {
+            const float4 xv = s_x4[c];
+            const uint2 w = wr[c];
+            const float2 w01 = bf16x2_to_float2(w.x), w23 = bf16x2_to_float2(w.y);
+            acc = fmaf(xv.x, w01.x, acc);
+            acc = fmaf(xv.y, w01.y, acc);
+            acc = fmaf(xv.z, w23.x, acc);
+            acc = fmaf(xv.w, w23.y, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) s_red[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            float z = 0.f;
+#pragma unroll
+            for (int w = 0; w < kRefineThreads / 32; ++w) z += s_red[w];
+            const unsigned long long k = order_key(z, uint32_t(n));
+            top = k > top ? k : top;
+            if (logits) logits[size_t(row) * vocab + n] = z * rstd[row];
+        }
+        __syncthreads();
+    }
+    if (tid == 0) best[row] = top;
 }
 
 // g_j from the packed keys; n = longest draft prefix reproduced by the target.
@@ -262,9 +506,13 @@ __global__ void accept_kernel(const unsigned long long* __restrict__ best, int b
 
 }  // namespace
 
-cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, cudaStream_t s) {
+cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, float* wmax2, cudaStream_t s) {
     colsum_kernel<<<(vocab + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(wt), width,
                                                   vocab, colsum);
+    cudaError_t e = cudaMemsetAsync(wmax2, 0, sizeof(float), s);
+    if (e != cudaSuccess) return e;
+    colnorm_max_kernel<<<(vocab + 7) / 8, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(wt), width,
+                                                       vocab, wmax2);
     return cudaGetLastError();
 }
 
@@ -273,7 +521,7 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
                                 const float* colsum, float* mean, float* rstd,
                                 unsigned long long* best, float* logits, int batch, int n_q,
                                 const int32_t* drafts, int32_t* target, int32_t* n_accepted,
-                                cudaStream_t s) {
+                                const RefineArgs& rf, cudaStream_t s) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(score_argmax_kernel,
@@ -282,13 +530,15 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
         configured = true;
     }
     if (split)
-        row_stats_kernel<float><<<rows, 256, 0, s>>>(static_cast<const float*>(attn_out), width,
-                                                     mean, rstd, static_cast<__nv_bfloat16*>(split));
+        row_stats_split_kernel<<<rows, kStatThreads, 0, s>>>(static_cast<const float*>(attn_out), width, mean,
+                                                             rstd, static_cast<__nv_bfloat16*>(split), rf.wmax2,
+                                                             rf.ebound);
     else
         row_stats_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(attn_out), width, mean, rstd, nullptr);
     cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
     if (e != cudaSuccess) return e;
+
     static unsigned long long* trace = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
@@ -296,7 +546,10 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
             cudaMemset(b, 0, 4096 * sizeof(unsigned long long));
         return b;
     }();
-    ScoreArgs sa{rows, width, vocab, split ? 2 : 1, mean, rstd, colsum, best, logits, trace};
+    // fp32 rows: the GEMM on the bf16 hi part only, then the exact refinement
+    ScoreArgs sa{rows, width, vocab, 1, mean, rstd, colsum, best, split ? nullptr : logits, trace,
+                 split ? rf.ebound : nullptr, split ? rf.cand_cnt : nullptr, split ? rf.cand_n : nullptr,
+                 split ? rf.cand_z : nullptr, vocab / kTN};
     dim3 grid((rows + kTM - 1) / kTM, vocab / kTN);
     score_argmax_kernel<<<grid, kScoreThreads, kScoreSmem, s>>>(sa, tmap_a, tmap_w);
     if (trace) {  // debug: dump the per-CTA timeline of this launch
@@ -309,6 +562,10 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
             std::fclose(fp);
         }
     }
+    if (split)
+        refine_kernel<<<rows, kRefineThreads, size_t(width) * 4, s>>>(
+            static_cast<const float*>(attn_out), static_cast<const __nv_bfloat16*>(rf.wt), width, vocab,
+            vocab / kTN, rf.cand_cnt, rf.cand_n, rf.cand_z, mean, rstd, colsum, rf.ebound, best, logits);
     accept_kernel<<<(batch + 127) / 128, 128, 0, s>>>(best, batch, n_q, drafts, target, n_accepted);
     return cudaGetLastError();
 }
