@@ -112,3 +112,46 @@ def test_verify_greedy_accept_bit_exact(cuda_handle, k):
         if not guarded[b, :min(nacc_ref[b] + 1, k)].any():
             assert nacc[b] == nacc_ref[b], (b, nacc[b], nacc_ref[b])
     assert sorted(set(nacc_ref.tolist())) == list(range(min(B, k + 1)))
+
+
+def _oracle_argmax(x, W64):
+    """argmax_token(LN(x) @ W) in fp64, first index of the maximum."""
+    xn = (x - x.mean(axis=-1, keepdims=True)) / np.sqrt(x.var(axis=-1, keepdims=True) + 1e-5)
+    return np.argmax(xn @ W64, axis=-1)
+
+
+@pytest.mark.parametrize("case", ["tie_pair", "all_equal", "random"])
+def test_score_refinement_edge_cases(cuda_handle, case):
+    """K4's hi-only GEMM + exact refinement against the fp64 argmax on crafted
+    rows: exact ties between two vocab entries (argmax_token keeps the lower
+    id), a W whose columns are all identical (every logit ties: the candidate
+    overflow path must still return id 0), and random rows."""
+    import torch
+    from paper_2504_11729_b200.verify import VerifyGreedy
+    from tests.gpu_util import torch_from_raw
+    B, n_q, width, V = 4, 3, 4096, 4096
+    rng = np.random.default_rng({"tie_pair": 1, "all_equal": 2, "random": 3}[case])
+    W = O.fill_uniform(O.DT_BF16, width * V, 77).reshape(width, V)  # raw bf16 [width][vocab]
+    x = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32) * 0.01
+    if case == "tie_pair":
+        # columns 17 and 1000: the same bf16 vector, aligned with the rows'
+        # shared direction u, so they tie for the maximum in every row
+        u = rng.uniform(-1.0, 1.0, size=width).astype(np.float32)
+        x = x + 0.05 * u
+        col = O.f64_to_bf16(0.5 * u.astype(np.float64))
+        W[:, 17] = col
+        W[:, 1000] = col
+    elif case == "all_equal":
+        W[:, :] = W[:, :1]
+    w_t = torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16)
+    ver = VerifyGreedy(w_t, handle=cuda_handle)
+    xt = torch.from_numpy(x).cuda().view(B, n_q, 32, 128)
+    drafts = torch.zeros((B, n_q - 1), dtype=torch.int32, device="cuda")
+    tgt, _, _ = ver(xt, drafts)
+    want = _oracle_argmax(x.astype(np.float64), O.bf16_to_f64(W))
+    got = tgt.cpu().numpy()
+    if case == "tie_pair":
+        assert (want == 17).all()
+    if case == "all_equal":
+        assert (want == 0).all()
+    assert np.array_equal(got, want), (got, want)
