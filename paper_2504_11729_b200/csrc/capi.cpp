@@ -315,7 +315,8 @@ struct ep_verifier_s {
     int32_t width = 0, vocab = 0;
     const void* w_t = nullptr;
     CUtensorMap tmap_w{};
-    DeviceBuffer colsum, mean, rstd, best, split, wmax2, ebound, cand_cnt, cand_n, cand_z;
+    DeviceBuffer colsum, mean, rstd, best, split, wmax2, ebound, cand_cnt, cand_n, cand_z, req_count;
+    size_t req_count_n = 0;
     CUtensorMap tmap_a{};
     const void* a_ptr = nullptr;
     int32_t a_rows = -1, a_dtype = -1;
@@ -385,6 +386,12 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         rf.cand_cnt = static_cast<int32_t*>(v->cand_cnt.ptr);
         rf.cand_n = static_cast<int32_t*>(v->cand_n.ptr);
         rf.cand_z = static_cast<float*>(v->cand_z.ptr);
+        if (size_t(batch) > v->req_count_n) {  // arrival counters start at zero; the kernel re-zeroes them
+            EP_CUDA_TRY(v->req_count.reserve(size_t(batch) * sizeof(int32_t)), "ep_verify_greedy ws");
+            EP_CUDA_TRY(cudaMemset(v->req_count.ptr, 0, size_t(batch) * sizeof(int32_t)), "ep_verify_greedy ws");
+            v->req_count_n = size_t(batch);
+        }
+        rf.req_count = static_cast<int32_t*>(v->req_count.ptr);
     }
     if (v->a_ptr != a_src || v->a_rows != rows || v->a_dtype != attn_dtype) {
         if (int rc = encode_bf16_2d(&v->tmap_a, a_src, a_inner, uint64_t(rows), 64, 128)) return rc;
@@ -398,7 +405,7 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
                                     static_cast<unsigned long long*>(v->best.ptr), logits, batch, n_q,
                                     drafts, target_ids, n_accepted, rf, static_cast<cudaStream_t>(stream)),
                 "score/accept launch");
-    h->launches += split ? 4 : 3;
+    h->launches += 3;
     return EP_OK;
 }
 

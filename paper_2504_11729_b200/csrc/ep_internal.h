@@ -166,6 +166,7 @@ struct RefineArgs {
     int32_t* cand_cnt = nullptr;   // [rows][vocab / 256]
     int32_t* cand_n = nullptr;     // [rows][vocab / 256][kScoreCandPerTile]
     float* cand_z = nullptr;       // [rows][vocab / 256][kScoreCandPerTile]
+    int32_t* req_count = nullptr;  // [batch] row arrivals of the fused accept, zero between launches
 };
 cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,

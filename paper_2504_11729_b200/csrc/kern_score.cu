@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "ep_common.cuh"
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(kStatThreads)
     const int row = blockIdx.x, tid = threadIdx.x;
     const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * width);
     const int nv = width / 4;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the attention output is complete
     __shared__ float red[3][kStatThreads / 32];
     float4 v[kStatVec];
     float s = 0.f;
@@ -270,6 +272,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // A (row stats output) is complete
 
     if (warp == 4) {
         if (lane == 0) {
@@ -407,23 +410,48 @@ __device__ __forceinline__ float key_value(unsigned long long k) {
 constexpr int kRefineThreads = 256;
 constexpr int kMaxList = 512;  // candidate list of one row (n_tiles * kPerTile)
 
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// The acceptance rule of request b from the packed argmax keys of its rows.
+__device__ __forceinline__ void accept_request(const unsigned long long* best, int b, int n_q,
+                                               const int32_t* drafts, int32_t* target, int32_t* n_accepted) {
+    const int k = n_q - 1;
+    int n = 0;
+    bool run = true;
+    for (int j = 0; j < n_q; ++j) {
+        const int32_t g = int32_t(0xFFFFFFFFu - uint32_t(__ldcg(&best[size_t(b) * n_q + j]) & 0xFFFFFFFFull));
+        target[size_t(b) * n_q + j] = g;
+        if (j < k && run) {
+            if (drafts[size_t(b) * k + j] == g)
+                ++n;
+            else
+                run = false;
+        }
+    }
+    n_accepted[b] = n;
+}
+
 // Per row: of the candidates the GEMM epilogue kept, those with z_hi >= row
 // max z_hi - 2 E_row get their exact logit z = (x - mean) . w_n (the centred
-// fp32 row staged in smem, one block-wide dot per candidate); the first
+// fp32 row staged in smem; one warp per candidate, all in flight); the first
 // maximum -> best[row]. With `logits` every logit is computed exactly and
 // written scaled by rstd (diagnostics); a candidate overflow does the same.
+// The last row of a request to finish applies the acceptance rule (fused
+// accept: a per-request arrival counter, reset by that row).
 __global__ void __launch_bounds__(kRefineThreads)
     refine_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ wt, int width, int vocab,
                   int n_tiles, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_n,
                   const float* __restrict__ cand_z, const float* __restrict__ mean, const float* __restrict__ rstd,
-                  const float* __restrict__ colsum, const float* __restrict__ ebound,
-                  unsigned long long* __restrict__ best, float* __restrict__ logits) {
+                  const float* __restrict__ ebound, unsigned long long* __restrict__ best,
+                  float* __restrict__ logits, int n_q, int32_t* __restrict__ req_count,
+                  const int32_t* __restrict__ drafts, int32_t* __restrict__ target, int32_t* __restrict__ n_accepted) {
     const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     extern __shared__ float4 s_x4[];  // [width / 4]
     __shared__ int s_list[kMaxList];
     __shared__ int s_n;
     __shared__ bool s_all;
-    __shared__ float s_red[kRefineThreads / 32];
+    __shared__ unsigned long long s_top;
+    pdl_wait();
     const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * width);
     const float mu = mean[row];
     for (int i = tid; i < width / 4; i += kRefineThreads) {  // the centred row
@@ -434,6 +462,7 @@ __global__ void __launch_bounds__(kRefineThreads)
     if (tid == 0) {
         s_all = logits != nullptr || n_tiles * kPerTile > kMaxList || n_tiles > kRefineThreads;
         s_n = 0;
+        s_top = 0ull;
     }
     __syncthreads();
     if (tid < n_tiles && cand_cnt[size_t(row) * n_tiles + tid] > kPerTile) s_all = true;
@@ -448,16 +477,15 @@ __global__ void __launch_bounds__(kRefineThreads)
         }
     }
     __syncthreads();
-    if (tid == 0 && s_all) s_n = vocab;
-    __syncthreads();
     const bool all = s_all;
-    const int count = s_n;
+    const int count = all ? vocab : s_n;
     unsigned long long top = 0ull;
-    for (int i = 0; i < count; ++i) {
+    for (int i = warp; i < count; i += kRefineThreads / 32) {
         const int n = all ? i : s_list[i];
         const uint2* wr = reinterpret_cast<const uint2*>(wt + size_t(n) * width);
         float acc = 0.f;
-        for (int c = tid; c < width / 4; c += kRefineThreads) {
+#pragma unroll 8
+        for (int c = lane; c < width / 4; c += 32) {
             const float4 xv = s_x4[c];
             const uint2 w = wr[c];
             const float2 w01 = bf16x2_to_float2(w.x), w23 = bf16x2_to_float2(w.y);
@@ -466,20 +494,25 @@ __global__ void __launch_bounds__(kRefineThreads)
             acc = fmaf(xv.z, w23.x, acc);
             acc = fmaf(xv.w, w23.y, acc);
         }
-        acc = warp_sum(acc);
-        if (lane == 0) s_red[warp] = acc;
-        __syncthreads();
-        if (tid == 0) {
-            float z = 0.f;
-#pragma unroll
-            for (int w = 0; w < kRefineThreads / 32; ++w) z += s_red[w];
-            const unsigned long long k = order_key(z, uint32_t(n));
-            top = k > top ? k : top;
-            if (logits) logits[size_t(row) * vocab + n] = z * rstd[row];
-        }
-        __syncthreads();
+        const float z = warp_sum(acc);
+        const unsigned long long k = order_key(z, uint32_t(n));
+        top = k > top ? k : top;
+        if (logits && lane == 0) logits[size_t(row) * vocab + n] = z * rstd[row];
     }
-    if (tid == 0) best[row] = top;
+    if (lane == 0 && top) atomicMax(&s_top, top);
+    __syncthreads();
+    if (tid == 0) {
+        best[row] = s_top;
+        if (req_count) {
+            const int b = row / n_q;
+            __threadfence();
+            if (atomicAdd(&req_count[b], 1) == n_q - 1) {
+                __threadfence();
+                accept_request(best, b, n_q, drafts, target, n_accepted);
+                req_count[b] = 0;  // ready for the next launch
+            }
+        }
+    }
 }
 
 // g_j from the packed keys; n = longest draft prefix reproduced by the target.
@@ -487,21 +520,25 @@ __global__ void accept_kernel(const unsigned long long* __restrict__ best, int b
                               const int32_t* __restrict__ drafts, int32_t* __restrict__ target,
                               int32_t* __restrict__ n_accepted) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= batch) return;
-    const int k = n_q - 1;
-    int n = 0;
-    bool run = true;
-    for (int j = 0; j < n_q; ++j) {
-        const int32_t g = int32_t(0xFFFFFFFFu - uint32_t(best[size_t(b) * n_q + j] & 0xFFFFFFFFull));
-        target[size_t(b) * n_q + j] = g;
-        if (j < k && run) {
-            if (drafts[size_t(b) * k + j] == g)
-                ++n;
-            else
-                run = false;
-        }
-    }
-    n_accepted[b] = n;
+    if (b < batch) accept_request(best, b, n_q, drafts, target, n_accepted);
+}
+
+// Launch with programmatic dependent launch: the kernel may start while its
+// predecessor drains; it calls griddepcontrol.wait before reading its inputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace
@@ -529,14 +566,17 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
         if (e != cudaSuccess) return e;
         configured = true;
     }
+    // (the argmax keys are cleared first so row stats -> GEMM -> refine stay
+    // adjacent kernels for programmatic dependent launch)
+    cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
+    if (e != cudaSuccess) return e;
     if (split)
-        row_stats_split_kernel<<<rows, kStatThreads, 0, s>>>(static_cast<const float*>(attn_out), width, mean,
-                                                             rstd, static_cast<__nv_bfloat16*>(split), rf.wmax2,
-                                                             rf.ebound);
+        e = launch_pdl(row_stats_split_kernel, dim3(rows), dim3(kStatThreads), 0, s,
+                       static_cast<const float*>(attn_out), width, mean, rstd,
+                       static_cast<__nv_bfloat16*>(split), static_cast<const float*>(rf.wmax2), rf.ebound);
     else
         row_stats_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(
             static_cast<const __nv_bfloat16*>(attn_out), width, mean, rstd, nullptr);
-    cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
     if (e != cudaSuccess) return e;
 
     static unsigned long long* trace = [] {
@@ -551,7 +591,8 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
                  split ? rf.ebound : nullptr, split ? rf.cand_cnt : nullptr, split ? rf.cand_n : nullptr,
                  split ? rf.cand_z : nullptr, vocab / kTN};
     dim3 grid((rows + kTM - 1) / kTM, vocab / kTN);
-    score_argmax_kernel<<<grid, kScoreThreads, kScoreSmem, s>>>(sa, tmap_a, tmap_w);
+    e = launch_pdl(score_argmax_kernel, grid, dim3(kScoreThreads), kScoreSmem, s, sa, tmap_a, tmap_w);
+    if (e != cudaSuccess) return e;
     if (trace) {  // debug: dump the per-CTA timeline of this launch
         std::vector<unsigned long long> host(4096);
         cudaStreamSynchronize(s);
@@ -563,10 +604,15 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
         }
     }
     if (split)
-        refine_kernel<<<rows, kRefineThreads, size_t(width) * 4, s>>>(
-            static_cast<const float*>(attn_out), static_cast<const __nv_bfloat16*>(rf.wt), width, vocab,
-            vocab / kTN, rf.cand_cnt, rf.cand_n, rf.cand_z, mean, rstd, colsum, rf.ebound, best, logits);
-    accept_kernel<<<(batch + 127) / 128, 128, 0, s>>>(best, batch, n_q, drafts, target, n_accepted);
+        e = launch_pdl(refine_kernel, dim3(rows), dim3(kRefineThreads), size_t(width) * 4, s,
+                       static_cast<const float*>(attn_out), static_cast<const __nv_bfloat16*>(rf.wt), width, vocab,
+                       vocab / kTN, static_cast<const int32_t*>(rf.cand_cnt), static_cast<const int32_t*>(rf.cand_n),
+                       static_cast<const float*>(rf.cand_z), static_cast<const float*>(mean),
+                       static_cast<const float*>(rstd), static_cast<const float*>(rf.ebound), best, logits, n_q,
+                       rf.req_count, drafts, target, n_accepted);
+    else
+        accept_kernel<<<(batch + 127) / 128, 128, 0, s>>>(best, batch, n_q, drafts, target, n_accepted);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
