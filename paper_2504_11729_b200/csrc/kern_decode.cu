@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     using L = RowLoader<KV, E>;
 
     extern __shared__ __align__(128) uint8_t smem[];
+    // programmatic dependent launch: nothing global is read before the
+    // predecessor (e.g. the Q/K/V projection writing q and the new K/V rows,
+    // or the previous step) has completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     uint8_t* sK = smem;
     uint8_t* sV = smem + C::OFF_V;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -509,7 +513,19 @@ cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (n_ctas > 0) kern<<<n_ctas, C::THREADS, C::SMEM, s>>>(a);
+    if (n_ctas > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n_ctas);
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, kern, a);
+    }
     return cudaGetLastError();
 }
 

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     verify_attention_kernel(const DecodeArgs a, const __grid_constant__ CUtensorMap tmap_k,
                             const __grid_constant__ CUtensorMap tmap_v, int rows) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the predecessor has completed
     uint8_t* smem = smem_raw;
     if (threadIdx.x == 0 && (smem_u32(smem) & 1023u) != 0) __trap();  // SW128 atoms need 1 KB alignment
     uint8_t* sStage = smem + OFF_STAGE;
@@ -665,7 +666,19 @@ cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUten
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (n_ctas > 0) verify_attention_kernel<<<n_ctas, kThreads, kSmem, s>>>(a, tk, tv, rows);
+    if (n_ctas > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n_ctas);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, verify_attention_kernel, a, tk, tv, rows);
+    }
     return cudaGetLastError();
 }
 
