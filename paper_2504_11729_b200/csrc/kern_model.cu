@@ -63,6 +63,18 @@ __device__ __forceinline__ void store_kv(void* pages, int kv_dtype, size_t idx, 
         static_cast<__nv_bfloat16*>(pages)[idx] = __float2bfloat16_rn(float(v));
 }
 
+// Rollout rows: step 0 embeds tokens[r], step s > 0 the previous step's
+// greedy token prev[(s - 1) * n + r]; positions are pos[s * n + r].
+__device__ __forceinline__ int embed_token(const int32_t* tokens, const int32_t* prev, const int32_t* step, int n,
+                                           int r) {
+    const int st = step ? *step : 0;
+    return st == 0 ? tokens[r] : prev[size_t(st - 1) * n + r];
+}
+
+__device__ __forceinline__ int embed_pos(const int32_t* pos, const int32_t* step, int n, int r) {
+    return pos[size_t(step ? *step : 0) * n + r];
+}
+
 template <typename T, int EPI>
 __device__ __forceinline__ void dense_epilogue(const DenseArgs& a, int row, int col, T v) {
     if constexpr (EPI == kEpiStore) {
@@ -210,16 +222,21 @@ cudaError_t launch_dense_t(const DenseArgs& a, cudaStream_t s) {
 template <typename T, int EPI, bool LN>
 cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s);
 
+bool gemv_ok(const DenseArgs& a, bool ln) {
+    const int nb = a.N / a.n_wblk;
+    bool aligned = nb % 4 == 0 && (!ln || a.K <= kGvMaxK);
+    for (int i = 0; i < a.n_wblk; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(a.w[i]) % 16 == 0;
+    return aligned;
+}
+
 template <typename T, int EPI, bool LN>
 cudaError_t dispatch_rows(const DenseArgs& a, cudaStream_t s) {
     // the cluster split-K GEMV (8-row blocks) wherever 16-byte weight loads
     // are aligned (every column block a multiple of 4 wide, 16-byte bases);
     // else the scalar kernel: every CTA streams its weight columns once for up
     // to 8 rows (decode) or 32 rows (prefill).
-    const int nb = a.N / a.n_wblk;
-    bool aligned = nb % 4 == 0 && (!LN || a.K <= kGvMaxK);
-    for (int i = 0; i < a.n_wblk; ++i) aligned = aligned && reinterpret_cast<uintptr_t>(a.w[i]) % 16 == 0;
-    if (aligned) return launch_gemv_t<T, EPI, LN>(a, s);
+    if (gemv_ok(a, LN)) return launch_gemv_t<T, EPI, LN>(a, s);
+    if (a.emb || a.next) return cudaErrorInvalidValue;  // fused work exists only in the GEMV
     if (a.n <= 8) return launch_dense_t<T, 8, EPI, LN>(a, s);
     return launch_dense_t<T, 32, EPI, LN>(a, s);
 }
@@ -314,11 +331,27 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
             constexpr int NV = kGvMaxK / 32;
             T v[NV];
             T sm = 0;
+            if (a.emb) {
+                // fused embedding of the first layer: embedding[token] + pe[pos]
+                const int n_rows = a.n;
+                const T* e = static_cast<const T*>(a.emb) +
+                             size_t(embed_token(a.tok, a.tok_prev, a.step, n_rows, grow)) * a.K;
+                const double* pr = a.pe + size_t(embed_pos(a.pos, a.step, n_rows, grow)) * a.K;
+                T* xs = (blockIdx.x == 0 && crank == 0) ? static_cast<T*>(a.x_store) + size_t(grow) * a.K : nullptr;
 #pragma unroll
-            for (int i = 0; i < NV; ++i) {
-                const int c = lane + 32 * i;
-                v[i] = c < a.K ? xr[c] : T(0);
-                sm += v[i];
+                for (int i = 0; i < NV; ++i) {
+                    const int c = lane + 32 * i;
+                    v[i] = c < a.K ? T(double(e[c]) + pr[c]) : T(0);
+                    if (xs && c < a.K) xs[c] = v[i];
+                    sm += v[i];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < NV; ++i) {
+                    const int c = lane + 32 * i;
+                    v[i] = c < a.K ? xr[c] : T(0);
+                    sm += v[i];
+                }
             }
             const T mean = warp_sum(sm) / T(a.K);
             T q = 0;
@@ -395,6 +428,51 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
         }
     }
     cluster.sync();  // peers' partials stay mapped until rank 0 has read them
+    if constexpr (EPI == kEpiStore) {
+        if (a.next && crank == 0) {
+            // fused argmax_token (model.cpp:248-255): the last CTA to store its
+            // logits takes the first maximum of every row, then advances the
+            // rollout step
+            __shared__ int s_last;
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = atomicAdd(a.arrive, 1) == int(gridDim.x * gridDim.z) - 1;
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                const T* lg = static_cast<const T*>(a.out);
+                const size_t so = a.step ? size_t(*a.step) * a.n : 0;
+                for (int r = warp; r < a.n; r += kDenseThreads / 32) {
+                    T bv = T(0);
+                    int bi = a.N;
+                    for (int c = lane; c < a.N; c += 32) {
+                        const T v = __ldcg(lg + size_t(r) * a.N + c);
+                        if (bi == a.N || v > bv) {
+                            bv = v;
+                            bi = c;
+                        }
+                    }
+#pragma unroll
+                    for (int m = 16; m > 0; m >>= 1) {
+                        const T ov = __shfl_xor_sync(0xffffffffu, bv, m);
+                        const int oi = __shfl_xor_sync(0xffffffffu, bi, m);
+                        if (oi < a.N && (bi == a.N || ov > bv || (ov == bv && oi < bi))) {
+                            bv = ov;
+                            bi = oi;
+                        }
+                    }
+                    if (lane == 0) a.next[so + r] = bi == a.N ? 0 : bi;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    *a.arrive = 0;  // ready for the next launch
+                    if (a.adv_step) *a.adv_step += 1;
+                }
+                if (a.adv_qpos)
+                    for (int b = tid; b < a.n; b += kDenseThreads) a.adv_qpos[b] += 1;
+            }
+        }
+    }
 }
 
 template <typename T, int EPI, bool LN>
@@ -430,21 +508,24 @@ cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s) {
 
 // With a rollout step counter, step 0 embeds tokens[r] and step s > 0 the
 // previous step's greedy token prev[(s - 1) * n + r]; positions are pos[s * n + r].
+// out = T(embedding (as fp64) + pe): model.cpp:121-126 adds in double.
 template <typename T>
-__global__ void embed_kernel(const T* emb, const int32_t* tokens, const int32_t* prev,
+__global__ void embed_kernel(const T* emb, const double* pe, const int32_t* tokens, const int32_t* prev,
                              const int32_t* step, const int32_t* pos, int D, T* out) {
     const int r = blockIdx.x, n = gridDim.x;
-    const int st = step ? *step : 0;
-    const int tok = st == 0 ? tokens[r] : prev[size_t(st - 1) * n + r];
-    const T* e = emb + size_t(tok) * D;
-    const double p = double(pos[size_t(st) * n + r]);
+    const T* e = emb + size_t(embed_token(tokens, prev, step, n, r)) * D;
+    const double* pr = pe + size_t(embed_pos(pos, step, n, r)) * D;
+    for (int c = threadIdx.x; c < D; c += blockDim.x) out[size_t(r) * D + c] = T(double(e[c]) + pr[c]);
+}
+
+__global__ void posenc_kernel(double* pe, int D) {
+    const int p = blockIdx.x;
     for (int c = threadIdx.x; c < D; c += blockDim.x) {
         // model.cpp:121-126: pair = c - c % 2, freq = 10000^(-pair / d)
         const int pair = c - (c % 2);
         const double freq = pow(10000.0, -double(pair) / double(D));
-        const double angle = p * freq;
-        const double add = (c % 2 == 0) ? sin(angle) : cos(angle);
-        out[size_t(r) * D + c] = T(double(e[c]) + add);
+        const double angle = double(p) * freq;
+        pe[size_t(p) * D + c] = (c % 2 == 0) ? sin(angle) : cos(angle);
     }
 }
 
@@ -638,22 +719,30 @@ __global__ void fill_at_kernel(int dt, void* dst, size_t n, uint64_t seed, uint6
 
 }  // namespace
 
+bool dense_uses_gemv(const DenseArgs& a, bool ln) { return a.n > 0 && a.N > 0 && gemv_ok(a, ln); }
+
 cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStream_t s) {
     if (a.n <= 0 || a.N <= 0) return cudaSuccess;
     return dt == EP_F64 ? dispatch_epi<double>(epi, ln, a, s) : dispatch_epi<float>(epi, ln, a, s);
 }
 
-cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* prev,
+cudaError_t launch_embed(int dt, const void* emb, const double* pe, const int32_t* tokens, const int32_t* prev,
                          const int32_t* step, const int32_t* pos, int n, int D, void* out,
                          cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int threads = D >= 256 ? 256 : ((D + 31) / 32) * 32;
     if (dt == EP_F64)
-        embed_kernel<double><<<n, threads, 0, s>>>(static_cast<const double*>(emb), tokens, prev,
-                                                   step, pos, D, static_cast<double*>(out));
+        embed_kernel<double><<<n, threads, 0, s>>>(static_cast<const double*>(emb), pe, tokens, prev, step, pos,
+                                                   D, static_cast<double*>(out));
     else
-        embed_kernel<float><<<n, threads, 0, s>>>(static_cast<const float*>(emb), tokens, prev,
-                                                  step, pos, D, static_cast<float*>(out));
+        embed_kernel<float><<<n, threads, 0, s>>>(static_cast<const float*>(emb), pe, tokens, prev, step, pos, D,
+                                                  static_cast<float*>(out));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_posenc(double* pe, int max_positions, int D, cudaStream_t s) {
+    if (max_positions <= 0) return cudaSuccess;
+    posenc_kernel<<<max_positions, D >= 256 ? 256 : ((D + 31) / 32) * 32, 0, s>>>(pe, D);
     return cudaGetLastError();
 }
 

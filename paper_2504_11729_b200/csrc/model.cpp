@@ -46,6 +46,8 @@ struct ep_model_s {
     size_t n_weights = 0, off_unembed = 0;
     std::vector<LayerOffsets> lw;
     DeviceBuffer weights;
+    DeviceBuffer pe;      // sinusoid table [max_positions][d_model] fp64 (model.cpp:121-126)
+    DeviceBuffer arrive;  // fused-argmax arrival counter (zero between launches)
     std::vector<std::unique_ptr<DeviceBuffer>> kpages, vpages;
     // per-forward workspace
     DeviceBuffer hid, xbuf, qbuf, attn, h1, logits_ws, next_ws, meta;
@@ -178,6 +180,8 @@ struct Pass {
     ep_plan plan = nullptr;
     void* logits = nullptr;
     int32_t* next = nullptr;
+    bool advance = false;       // rollout: step += 1, adv_qpos[0..batch) += 1 after the argmax
+    int64_t* adv_qpos = nullptr;
 };
 
 // Metadata upload: one pinned staging buffer, one async copy; fills the
@@ -216,9 +220,7 @@ int upload_meta(ep_model m, const Meta& md, Pass& ps, cudaStream_t s) {
 int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
     ep_handle h = m->h;
     const int dt = m->dt, n = ps.n;
-    EP_CUDA_TRY(launch_embed(dt, m->wptr(0), ps.tok, ps.prev, ps.step, ps.pos, n, m->D, m->hid.ptr, s),
-                "embed launch");
-    h->launches++;
+    bool embed_fused = false;
     for (int l = 0; l < m->L; ++l) {
         const LayerOffsets& o = m->lw[l];
         const ep_kv_pool pool = m->pool(l);
@@ -242,6 +244,24 @@ int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
         a.dst_page = ps.dst_page;
         a.dst_slot = ps.dst_slot;
         a.step = ps.step;
+        if (l == 0) {
+            // embed (model.cpp:104-129) fused into the first projection's
+            // LayerNorm prologue, which also stores the embedded rows
+            embed_fused = dense_uses_gemv(a, true);
+            if (embed_fused) {
+                a.emb = m->wptr(0);
+                a.pe = static_cast<const double*>(m->pe.ptr);
+                a.tok = ps.tok;
+                a.tok_prev = ps.prev;
+                a.pos = ps.pos;
+                a.x_store = m->hid.ptr;
+            } else {
+                EP_CUDA_TRY(launch_embed(dt, m->wptr(0), static_cast<const double*>(m->pe.ptr), ps.tok, ps.prev,
+                                         ps.step, ps.pos, n, m->D, m->hid.ptr, s),
+                            "embed launch");
+                h->launches++;
+            }
+        }
         EP_CUDA_TRY(launch_dense(dt, kEpiQKV, true, a, s), "qkv launch");
         h->launches++;
         // spliced causal attention over the request's pages
@@ -304,10 +324,27 @@ int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
     u.w[0] = m->wptr(m->off_unembed);
     u.n_wblk = 1;
     u.out = ps.logits;
+    u.step = ps.step;
+    if (dense_uses_gemv(u, true)) {
+        // argmax_token (+ the rollout's position advance) in the last CTA
+        u.next = ps.next;
+        u.arrive = static_cast<int32_t*>(m->arrive.ptr);
+        if (ps.advance) {
+            u.adv_step = const_cast<int32_t*>(ps.step);
+            u.adv_qpos = ps.adv_qpos;
+        }
+        EP_CUDA_TRY(launch_dense(dt, kEpiStore, true, u, s), "unembed launch");
+        h->launches++;
+        return EP_OK;
+    }
     EP_CUDA_TRY(launch_dense(dt, kEpiStore, true, u, s), "unembed launch");
     h->launches++;
     EP_CUDA_TRY(launch_argmax_rows(dt, ps.logits, ps.batch, m->V, ps.step, ps.next, s), "argmax launch");
     h->launches++;
+    if (ps.advance) {
+        EP_CUDA_TRY(launch_advance(const_cast<int32_t*>(ps.step), ps.adv_qpos, ps.batch, s), "advance launch");
+        h->launches++;
+    }
     return EP_OK;
 }
 
@@ -388,6 +425,11 @@ int ep_model_create(ep_handle h, const ep_model_config* cfg, int32_t kv_dtype, i
                     "ep_model_create init");
         h->launches++;
     }
+    EP_CUDA_TRY(m->pe.reserve(size_t(c.max_positions) * D * sizeof(double)), "ep_model_create pe");
+    EP_CUDA_TRY(launch_posenc(static_cast<double*>(m->pe.ptr), c.max_positions, m->D, nullptr), "posenc launch");
+    h->launches++;
+    EP_CUDA_TRY(m->arrive.reserve(sizeof(int32_t)), "ep_model_create");
+    EP_CUDA_TRY(cudaMemset(m->arrive.ptr, 0, sizeof(int32_t)), "ep_model_create");
     const size_t pool_bytes = size_t(num_pages) * m->H * size_t(page_tokens) * m->dh * kv_elem_bytes(kv_dtype);
     for (int l = 0; l < m->L; ++l) {
         m->kpages.emplace_back(new DeviceBuffer());
@@ -624,8 +666,10 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_model_generate");  // metadata + plan uploads landed
     const int64_t launches0 = m->h->launches.load();
     EP_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "ep_model_generate capture");
+    ps.advance = true;
+    ps.adv_qpos = qpos_dev;
     int rc = enqueue_pass(m, ps, cap);
-    cudaError_t e = rc ? cudaSuccess : launch_advance(const_cast<int32_t*>(ps.step), qpos_dev, batch, cap);
+    cudaError_t e = cudaSuccess;
     cudaGraph_t graph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
     if (rc) {
@@ -634,7 +678,7 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     }
     EP_CUDA_TRY(e, "ep_model_generate advance");
     EP_CUDA_TRY(e2, "ep_model_generate end capture");
-    const int64_t per_step = m->h->launches.load() - launches0 + 1;
+    const int64_t per_step = m->h->launches.load() - launches0;
     cudaGraphExec_t exec = nullptr;
     e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
@@ -646,7 +690,7 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaGraphExecDestroy(exec);
     EP_CUDA_TRY(e, "ep_model_generate replay");
-    m->h->launches += per_step * n_steps - (per_step - 1);  // replays run; the capture counted per_step - 1
+    m->h->launches += per_step * (n_steps - 1);  // replays run; the capture counted one step
     for (int b = 0; b < batch; ++b)
         for (int t = 0; t < n_steps; ++t) out_tokens[size_t(b) * n_steps + t] = host[size_t(t) * batch + b];
     return EP_OK;

@@ -40,7 +40,27 @@ struct DenseArgs {
     // rollout: device step counter; dst_page / dst_slot are [steps][n] and
     // row r of step s is entry s * n + r (null = a single forward)
     const int32_t* step;
+    // fused embedding (LN kernels only): row r = embedding[token] + pe[pos],
+    // token = tok[r] (step 0) or tok_prev[(step - 1) * n + r], pos = pos[step * n + r];
+    // the embedded rows are also stored to x_store (the layer's residual input)
+    const void* emb;
+    const double* pe;
+    const int32_t* tok;
+    const int32_t* tok_prev;
+    const int32_t* pos;
+    void* x_store;
+    // fused argmax (kEpiStore): the last CTA writes the first maximum of
+    // every row of `out` to next[step * n + r], then advances the rollout
+    // (*adv_step += 1, adv_qpos[0..n) += 1; either may be null)
+    int32_t* next;
+    int32_t* arrive;  // zero between launches
+    int64_t* adv_qpos;
+    int32_t* adv_step;
 };
+
+// Whether launch_dense runs the cluster GEMV for these arguments (the only
+// kernel with the fused embedding / argmax).
+bool dense_uses_gemv(const DenseArgs& a, bool ln);
 
 // dt: EP_F64 or EP_F32 (x, W, bias, resid, out, q_out share it).
 cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStream_t s);
@@ -48,9 +68,12 @@ cudaError_t launch_dense(int dt, int epi, bool ln, const DenseArgs& a, cudaStrea
 // embed (model.cpp:104-129): out[r] = embedding[token] + sinusoid(pos). With
 // a rollout step counter (step != null): token = tokens[r] at step 0, else
 // prev[(step - 1) * n + r]; position pos[step * n + r].
-cudaError_t launch_embed(int dt, const void* emb, const int32_t* tokens, const int32_t* prev,
+cudaError_t launch_embed(int dt, const void* emb, const double* pe, const int32_t* tokens, const int32_t* prev,
                          const int32_t* step, const int32_t* pos, int n, int D, void* out,
                          cudaStream_t s);
+
+// pe[p][c] = sin / cos(p * 10000^(-(c - c % 2) / D)) in fp64 (model.cpp:121-126).
+cudaError_t launch_posenc(double* pe, int max_positions, int D, cudaStream_t s);
 
 // Generic paged causal attention: one CTA per (query row, head); row r of
 // request row_req[r] at position row_pos[r] (row_pos[step * n + r] in a
