@@ -506,13 +506,7 @@ cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
     using C = DecodeCfg<KV, D, R, J, S>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     auto kern = spliced_decode_kernel<KV, D, R, J, S>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e =
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    if (cudaError_t e = ensure_smem<spliced_decode_kernel<KV, D, R, J, S>>(C::SMEM)) return e;
     if (n_ctas > 0) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(n_ctas);

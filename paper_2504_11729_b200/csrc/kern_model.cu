@@ -209,11 +209,8 @@ __global__ void __launch_bounds__(kDenseThreads) dense_kernel(const DenseArgs a)
 template <typename T, int MR, int EPI, bool LN>
 cudaError_t launch_dense_t(const DenseArgs& a, cudaStream_t s) {
     const size_t smem = dense_smem<T, MR>();
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dense_kernel<T, MR, EPI, LN>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-    }
+    if (smem > 48 * 1024)
+        if (cudaError_t e = ensure_smem<dense_kernel<T, MR, EPI, LN>>(int(smem))) return e;
     dim3 grid((a.N + kBN - 1) / kBN, (a.n + MR - 1) / MR);
     dense_kernel<T, MR, EPI, LN><<<grid, kDenseThreads, smem, s>>>(a);
     return cudaGetLastError();
@@ -482,11 +479,10 @@ cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s) {
     const int KR = (((a.K + cs - 1) / cs) + 15) / 16 * 16;
     cs = (a.K + KR - 1) / KR;
     const size_t smem = sizeof(T) * (size_t(kGvRows) * KR + size_t(kGvKS + 1) * kGvRows * kGvCols);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(gemv_cluster_kernel<T, EPI, LN>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-    }
+    // (KR depends on K: the opt-in is the per-CTA maximum, the launch uses smem)
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    if (smem > 48 * 1024)
+        if (cudaError_t e = ensure_smem<gemv_cluster_kernel<T, EPI, LN>>(227 * 1024)) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((a.N + kGvCols - 1) / kGvCols, cs, (a.n + kGvRows - 1) / kGvRows);
     cfg.blockDim = dim3(kDenseThreads, 1, 1);

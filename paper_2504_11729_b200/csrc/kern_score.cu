@@ -559,13 +559,7 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
                                 unsigned long long* best, float* logits, int batch, int n_q,
                                 const int32_t* drafts, int32_t* target, int32_t* n_accepted,
                                 const RefineArgs& rf, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(score_argmax_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kScoreSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    if (cudaError_t e = ensure_smem<score_argmax_kernel>(kScoreSmem)) return e;
     // (the argmax keys are cleared first so row stats -> GEMM -> refine stay
     // adjacent kernels for programmatic dependent launch)
     cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);

@@ -659,13 +659,7 @@ bool verify_supported(int kv_dtype, int d_head, int rows) {
 
 cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUtensorMap& tk,
                                     const CUtensorMap& tv, int rows, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(verify_attention_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    if (cudaError_t e = ensure_smem<verify_attention_kernel>(kSmem)) return e;
     if (n_ctas > 0) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(n_ctas);
