@@ -9,18 +9,23 @@
 
 namespace ep {
 
-// Opts kernel Kern into `bytes` of dynamic shared memory once per device
-// (the attribute is per device context; a process may drive several GPUs).
+// Opts kernel Kern into at least `bytes` of dynamic shared memory on the
+// current device (the attribute is per device context and a process may
+// drive several GPUs); raised only when a launch needs more than before.
 template <auto Kern>
 inline cudaError_t ensure_smem(int bytes) {
-    static std::atomic<uint64_t> done{0};
+    static std::atomic<int> done[64] = {};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    const uint64_t bit = 1ull << (dev & 63);
-    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    std::atomic<int>& d = done[dev & 63];
+    if (d.load(std::memory_order_acquire) >= bytes) return cudaSuccess;
     e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    if (e == cudaSuccess) {
+        int cur = d.load(std::memory_order_relaxed);
+        while (cur < bytes && !d.compare_exchange_weak(cur, bytes, std::memory_order_release)) {
+        }
+    }
     return e;
 }
 

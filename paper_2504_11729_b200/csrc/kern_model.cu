@@ -479,10 +479,8 @@ cudaError_t launch_gemv_t(const DenseArgs& a, cudaStream_t s) {
     const int KR = (((a.K + cs - 1) / cs) + 15) / 16 * 16;
     cs = (a.K + KR - 1) / KR;
     const size_t smem = sizeof(T) * (size_t(kGvRows) * KR + size_t(kGvKS + 1) * kGvRows * kGvCols);
-    // (KR depends on K: the opt-in is the per-CTA maximum, the launch uses smem)
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
     if (smem > 48 * 1024)
-        if (cudaError_t e = ensure_smem<gemv_cluster_kernel<T, EPI, LN>>(227 * 1024)) return e;
+        if (cudaError_t e = ensure_smem<gemv_cluster_kernel<T, EPI, LN>>(int(smem))) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((a.N + kGvCols - 1) / kGvCols, cs, (a.n + kGvRows - 1) / kGvRows);
     cfg.blockDim = dim3(kDenseThreads, 1, 1);
