@@ -477,8 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (two_part) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
-                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
+                        const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[2 * j]), __uint_as_float(sr[2 * j + 1])),
+                                                     make_float2(scale, scale), make_float2(-mu, -mu));
+                        const float p0 = fast_exp2(x2.x);
+                        const float p1 = fast_exp2(x2.y);
                         const float2 p2 = make_float2(p0, p1);
                         rsa[j & 3] = __fadd2_rn(rsa[j & 3], p2);
                         pk[j] = pack_bf16(p0, p1);
@@ -492,8 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // of P is unbiased, so the output scale error averages out
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const float p0 = fast_exp2(fmaf(__uint_as_float(sr[2 * j]), scale, -mu));
-                        const float p1 = fast_exp2(fmaf(__uint_as_float(sr[2 * j + 1]), scale, -mu));
+                        const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[2 * j]), __uint_as_float(sr[2 * j + 1])),
+                                                     make_float2(scale, scale), make_float2(-mu, -mu));
+                        const float p0 = fast_exp2(x2.x);
+                        const float p1 = fast_exp2(x2.y);
                         pk[j] = pack_bf16(p0, p1);
                         rsa[j & 3] = __fadd2_rn(rsa[j & 3], make_float2(p0, p1));
                     }
