@@ -63,6 +63,35 @@ __device__ __forceinline__ void merge_unit_rows(const DecodeArgs& a, int u0, int
                 L[k] += wt[k];
             }
             const int cnt = min(32, n - base);
+            if (!ok[1]) {
+                // one row in this warp's batch (a K1 unit has 4 rows for 8
+                // warps): its items 8 at a time, all in flight (a long unit is
+                // split into ~20 items at batch 1 — config 4)
+                for (int j = 0; j < cnt; j += 8) {
+                    float x[8][E];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const bool live = j + q < cnt;
+                        const float* src = a.o_part + (size_t(u0 + base + (live ? j + q : j)) * stride + rr[0]) * D + lane * E;
+                        if constexpr (E == 4) {
+                            const float4 v = live ? __ldcg(reinterpret_cast<const float4*>(src)) : make_float4(0, 0, 0, 0);
+                            x[q][0] = v.x; x[q][1] = v.y; x[q][2] = v.z; x[q][3] = v.w;
+                        } else {
+                            const float2 v = live ? __ldcg(reinterpret_cast<const float2*>(src)) : make_float2(0, 0);
+                            x[q][0] = v.x; x[q][1] = v.y;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float w = __shfl_sync(0xffffffffu, wt[0], min(j + q, cnt - 1));
+                        if (j + q < cnt) {
+#pragma unroll
+                            for (int e = 0; e < E; ++e) acc[0][e] += w * x[q][e];
+                        }
+                    }
+                }
+                continue;
+            }
             for (int j = 0; j < cnt; j += 2) {
                 const bool two = j + 1 < cnt;
                 float x0[kRB][E], x1[kRB][E];

@@ -69,7 +69,7 @@ def build_local(batch, world, rank, h, cloud=CLOUD, edge=EDGE, seed=41):
     return pool, table, attn, q, n_loc
 
 
-def run(batch, steps, warmup, check=False, combine="peer", graph=False):
+def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CLOUD):
     """combine: "peer" = one ep_splitkv_combine_dev kernel over NVLink peer
     memory; "nccl" = NCCL all-gather + K5 merge. graph: replay the step
     (attention + combine) as one CUDA graph (removes host launch overhead)."""
@@ -80,7 +80,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False):
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     h = Handle(torch.cuda.current_device())
-    pool, table, attn, q, n_loc = build_local(batch, world, rank, h)
+    pool, table, attn, q, n_loc = build_local(batch, world, rank, h, cloud=cloud)
     rows = batch * HQ
     comb = None
     if world > 1:
@@ -160,7 +160,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False):
     loc_bytes = batch * n_loc * 2 * HKV * D * 2
     gather_bytes = (world - 1) * rows * (D + 1) * 4  # received per rank
     res = {
-        "workload": f"cfg4 split-KV: {CLOUD} cloud + {EDGE} edge keys, Hq=32 Hkv=8 d=128 bf16, "
+        "workload": f"cfg4 split-KV: {cloud} cloud + {EDGE} edge keys, Hq=32 Hkv=8 d=128 bf16, "
                     f"batch {batch}, {world} GPU(s)",
         "batch": batch, "gpus": world, "combine": combine if world > 1 else None, "step_ms": t_step, "local_attention_ms": t_attn,
         "combine_ms": t_step - t_attn if world > 1 else 0.0,
@@ -201,6 +201,8 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--combine", choices=["peer", "nccl"], nargs="+", default=["peer"])
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--cloud", type=int, default=CLOUD,
+                    help="cloud tokens (e.g. 131072 / P on one GPU = one rank's local pass)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -212,7 +214,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     for cmb in args.combine:
         for b in args.batch:
-            r = run(b, args.steps, args.warmup, check=args.check, combine=cmb, graph=args.graph)
+            r = run(b, args.steps, args.warmup, check=args.check, combine=cmb, graph=args.graph,
+                    cloud=args.cloud)
             if int(os.environ.get("RANK", "0")) == 0:
                 print(json.dumps(r), flush=True)
     if world > 1:
