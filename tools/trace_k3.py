@@ -70,6 +70,9 @@ if __name__ == "__main__":
         sys.argv = [sys.argv[0], "--steps", "3"]
         import decode_only
         decode_only.main()
+    elif kind == "skv":  # K1, one rank's config-4 local pass (cloud tokens = argv[2])
+        import splitkv_bench
+        print(splitkv_bench.run(1, 3, 2, cloud=int(sys.argv[2])))
     elif kind == "shared":
         import multitenant_bench
         print(multitenant_bench.run(1, 1))
