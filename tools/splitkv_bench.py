@@ -167,6 +167,14 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
         "tokens_per_s": batch / (t_step / 1e3),
         "local_hbm_gbs": loc_bytes / (t_attn / 1e3) / 1e9,
         "allgather_bytes_per_rank": gather_bytes,
+        # NVLink roofline of the exchange: bytes each rank receives over the
+        # combine time vs 900 GB/s per direction (NVLink 5) — tiny messages,
+        # so the combine is latency-bound and this fraction is small
+        "combine_nvlink_gbs": (gather_bytes / ((t_step - t_attn) / 1e3) / 1e9
+                               if world > 1 and t_step > t_attn else None),
+        "combine_nvlink_frac": (gather_bytes / ((t_step - t_attn) / 1e3) / 900e9
+                                if world > 1 and t_step > t_attn else None),
+        "local_hbm_frac": loc_bytes / (t_attn / 1e3) / 6549.1e9,
         "graph": graph, "host_launch_us_per_step": host_us,
     }
     if per_rank is not None:
