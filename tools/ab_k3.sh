@@ -1,5 +1,5 @@
 # Same-box A/B of two library builds on the K3 128-row tile workloads.
-for v in A B A B; do
+for v in ${AB_VARIANTS:-A B A B}; do
   echo v=$v
   L=paper_2504_11729_b200/_lib/ab/lib$v.so
   EP_LIB=$L python tools/prefill_bench.py --steps 10 2>&1 | python -c "
