@@ -100,7 +100,8 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
 
 /* Which attention kernel the last ep_model_forward / ep_model_generate used: 1 = spliced decode /
  * prefill plans (K1/K3 of ep_attn.h), 2 = the generic paged kernel (fp64, or
- * d_head outside {64, 128}). */
+ * d_head outside {64, 128}), 3 = the persistent rollout kernel (fp32 models of
+ * <= 8 rows in ep_model_generate: all steps in one cooperative launch). */
 int ep_model_last_attention_path(ep_model m);
 
 #ifdef __cplusplus

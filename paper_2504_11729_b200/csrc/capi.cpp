@@ -388,7 +388,9 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         rf.cand_z = static_cast<float*>(v->cand_z.ptr);
         if (size_t(batch) > v->req_count_n) {  // arrival counters start at zero; the kernel re-zeroes them
             EP_CUDA_TRY(v->req_count.reserve(size_t(batch) * sizeof(int32_t)), "ep_verify_greedy ws");
-            EP_CUDA_TRY(cudaMemset(v->req_count.ptr, 0, size_t(batch) * sizeof(int32_t)), "ep_verify_greedy ws");
+            EP_CUDA_TRY(cudaMemsetAsync(v->req_count.ptr, 0, size_t(batch) * sizeof(int32_t),
+                                        static_cast<cudaStream_t>(stream)),
+                        "ep_verify_greedy ws");
             v->req_count_n = size_t(batch);
         }
         rf.req_count = static_cast<int32_t*>(v->req_count.ptr);

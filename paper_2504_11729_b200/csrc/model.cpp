@@ -18,6 +18,8 @@
 //     each request's last row and argmax.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -47,6 +49,8 @@ struct ep_model_s {
     std::vector<LayerOffsets> lw;
     DeviceBuffer weights;
     DeviceBuffer pe;      // sinusoid table [max_positions][d_model] fp64 (model.cpp:121-126)
+    DeviceBuffer persist_layers, persist_scratch, persist_counters;  // K9 persistent rollout (fp32 models)
+    size_t persist_counters_n = 0;
     DeviceBuffer arrive;  // fused-argmax arrival counter (zero between launches)
     std::vector<std::unique_ptr<DeviceBuffer>> kpages, vpages;
     // per-forward workspace
@@ -642,6 +646,104 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     ps.prev = static_cast<const int32_t*>(out_dev.ptr);
     ps.next = static_cast<int32_t*>(out_dev.ptr);
     ps.logits = m->logits_ws.ptr;
+
+    // K9 (opt-in, EP_MODEL_PERSIST=1): small fp32 models roll out in one
+    // persistent cooperative kernel instead of the CUDA-graph path below
+    const char* persist_e = std::getenv("EP_MODEL_PERSIST");
+    const bool persist_env = persist_e && persist_e[0] == '1';
+    if (persist_env && m->dt == EP_F32 && m->kv_dtype == EP_F32 &&
+        persist_supported(batch, m->D, m->H, m->F, m->V, m->P)) {
+        if (!m->persist_layers.ptr) {
+            std::vector<PersistLayer> tab(m->L);
+            for (int l = 0; l < m->L; ++l) {
+                const LayerOffsets& o = m->lw[l];
+                tab[l] = {reinterpret_cast<const float*>(m->wptr(o.wq)), reinterpret_cast<const float*>(m->wptr(o.wk)),
+                          reinterpret_cast<const float*>(m->wptr(o.wv)), reinterpret_cast<const float*>(m->wptr(o.wo)),
+                          reinterpret_cast<const float*>(m->wptr(o.w1)), reinterpret_cast<const float*>(m->wptr(o.b1)),
+                          reinterpret_cast<const float*>(m->wptr(o.w2)), reinterpret_cast<const float*>(m->wptr(o.b2)),
+                          static_cast<float*>(m->kpages[l]->ptr), static_cast<float*>(m->vpages[l]->ptr)};
+            }
+            EP_CUDA_TRY(m->persist_layers.reserve(tab.size() * sizeof(PersistLayer)), "ep_model_generate");
+            EP_CUDA_TRY(cudaMemcpy(m->persist_layers.ptr, tab.data(), tab.size() * sizeof(PersistLayer),
+                                   cudaMemcpyHostToDevice),
+                        "ep_model_generate");
+        }
+        int max_chunks = 1;
+        for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
+        const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
+        const size_t part = B * m->H * size_t(max_chunks) * (m->dh + 2);
+        const size_t gpart = persist_gpart_floats(batch, m->D, m->F, m->V);
+        const size_t n_cnt = (std::max(std::max(3 * D, F), V) + 31) / 32;
+        const size_t floats = 3 * B * D + B * F + B * V + part + gpart;
+        EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
+        if (m->persist_counters_n < n_cnt) {  // arrival counters start at zero; the kernel re-zeroes them
+            EP_CUDA_TRY(m->persist_counters.reserve(n_cnt * sizeof(int32_t)), "ep_model_generate counters");
+            // on the launch stream: a (non-blocking) stream does not wait for a
+            // legacy-stream memset, and reused memory is not zero
+            EP_CUDA_TRY(cudaMemsetAsync(m->persist_counters.ptr, 0, n_cnt * sizeof(int32_t), s),
+                        "ep_model_generate counters");
+            m->persist_counters_n = n_cnt;
+        }
+        float* f0 = static_cast<float*>(m->persist_scratch.ptr);
+        PersistArgs pa{};
+        pa.layers = static_cast<const PersistLayer*>(m->persist_layers.ptr);
+        pa.L = m->L;
+        pa.B = batch;
+        pa.D = m->D;
+        pa.H = m->H;
+        pa.dh = m->dh;
+        pa.F = m->F;
+        pa.V = m->V;
+        pa.P = m->P;
+        pa.n_steps = n_steps;
+        pa.max_chunks = max_chunks;
+        pa.emb = reinterpret_cast<const float*>(m->wptr(0));
+        pa.pe = static_cast<const double*>(m->pe.ptr);
+        pa.unembed = reinterpret_cast<const float*>(m->wptr(m->off_unembed));
+        pa.first = ps.tok;
+        pa.pos = ps.pos;
+        pa.dst_page = ps.dst_page;
+        pa.dst_slot = ps.dst_slot;
+        pa.pdesc = ps.pdesc;
+        pa.req_page_off = ps.req_page_off;
+        pa.x = f0;
+        pa.x2 = f0 + B * D;
+        pa.q = f0 + 2 * B * D;
+        pa.h1 = f0 + 3 * B * D;
+        pa.logits = pa.h1 + B * F;
+        pa.part = pa.logits + B * V;
+        pa.gpart = pa.part + part;
+        pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
+        pa.out = static_cast<int32_t*>(out_dev.ptr);
+        static unsigned long long* trace = [] {
+            unsigned long long* b = nullptr;
+            const char* e = std::getenv("EP_TRACE");
+            if (e && e[0] == '1' && cudaMalloc(&b, 256 * sizeof(unsigned long long)) == cudaSuccess)
+                cudaMemset(b, 0, 256 * sizeof(unsigned long long));
+            return b;
+        }();
+        pa.trace = trace;
+        EP_CUDA_TRY(launch_decode_persist(pa, m->h->n_sms, s), "ep_model_generate persistent launch");
+        if (trace) {  // debug: EP_TRACE=1 dumps the barrier timestamps to EP_TRACE_FILE
+            std::vector<unsigned long long> hb(256);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(hb.data(), trace, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+            const char* f = std::getenv("EP_TRACE_FILE");
+            if (FILE* fp = std::fopen(f ? f : "ep_trace_persist.bin", "wb")) {
+                std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), fp);
+                std::fclose(fp);
+            }
+        }
+        m->h->launches++;
+        m->last_path = 3;
+        std::vector<int32_t> host(size_t(n_steps) * batch);
+        EP_CUDA_TRY(cudaMemcpyAsync(host.data(), out_dev.ptr, host.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                    "ep_model_generate tokens");
+        EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_model_generate");
+        for (int b = 0; b < batch; ++b)
+            for (int t = 0; t < n_steps; ++t) out_tokens[size_t(b) * n_steps + t] = host[size_t(t) * batch + b];
+        return EP_OK;
+    }
 
     // the decode plan is built once for the FINAL table; the causal rule
     // masks the keys past each step's query position, which advances on the

@@ -94,6 +94,35 @@ cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, cons
 // Rollout step end: *step += 1, q_pos[0..batch) += 1 (q_pos may be null).
 cudaError_t launch_advance(int32_t* step, int64_t* q_pos, int batch, cudaStream_t s);
 
+// K9: whole greedy rollout of a small fp32 decoder in one persistent
+// cooperative kernel (kern_model_persist.cu).
+struct PersistLayer {
+    const float *wq, *wk, *wv, *wo, *w1, *b1, *w2, *b2;
+    float *kp, *vp;  // this layer's K / V pages [page][H][P][dh]
+};
+struct PersistArgs {
+    const PersistLayer* layers;  // device [L]
+    int L, B, D, H, dh, F, V, P, n_steps, max_chunks;
+    const float* emb;
+    const double* pe;
+    const float* unembed;
+    const int32_t* first;      // [B] token of step 0
+    const int32_t* pos;        // [n_steps][B]
+    const int32_t* dst_page;   // [n_steps][B]
+    const int32_t* dst_slot;   // [n_steps][B]
+    const PageDesc* pdesc;     // every request's pages (final table)
+    const int64_t* req_page_off;
+    float *x, *x2, *q, *h1, *logits, *part;  // scratch
+    float* gpart;              // GEMV k-chunk partial sums [K/32][B][N]
+    int32_t* counters;         // per column block arrivals, zero between stages
+    int32_t* out;              // [n_steps][B] greedy tokens
+    unsigned long long* trace; // debug: [8 steps][32] barrier timestamps of CTA 0 (may be null)
+};
+bool persist_supported(int B, int D, int H, int F, int V, int P);
+size_t persist_smem_bytes(int B, int D, int F, int H, int max_chunks);
+size_t persist_gpart_floats(int B, int D, int F, int V);
+cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s);
+
 // dst[i] = uniform(lo, hi) of SplitMix64(seed) draw first + i (fp64 draw,
 // stored in dt = EP_F64 / EP_F32 / EP_BF16).
 cudaError_t launch_fill_uniform_at(int dt, void* dst, size_t n, uint64_t seed, uint64_t first,

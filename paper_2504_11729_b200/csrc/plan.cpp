@@ -424,7 +424,7 @@ int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const
     return EP_OK;
 }
 
-int upload_subplan(SubPlan& sp, int d_head, std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>>& parts) {
+int upload_subplan(SubPlan& sp, int d_head, cudaStream_t s, std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>>& parts) {
     parts.push_back({&sp.d_pdesc, {sp.pdesc.data(), bytes_of(sp.pdesc)}});
     parts.push_back({&sp.d_req_off, {sp.req_page_off.data(), bytes_of(sp.req_page_off)}});
     parts.push_back({&sp.d_items, {sp.items.data(), bytes_of(sp.items)}});
@@ -436,7 +436,8 @@ int upload_subplan(SubPlan& sp, int d_head, std::vector<std::pair<DeviceBuffer*,
     const size_t units = size_t(std::max<int64_t>(1, sp.n_units));
     if (units > sp.counter_units) {
         EP_CUDA_TRY(sp.d_counter.reserve(units * sizeof(int32_t)), "ep_plan counters");
-        EP_CUDA_TRY(cudaMemset(sp.d_counter.ptr, 0, units * sizeof(int32_t)), "ep_plan counters");
+        // on the launch stream (a non-blocking stream does not wait for the legacy one)
+        EP_CUDA_TRY(cudaMemsetAsync(sp.d_counter.ptr, 0, units * sizeof(int32_t), s), "ep_plan counters");
         sp.counter_units = units;
     }
     return EP_OK;
@@ -447,9 +448,9 @@ int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
     parts.push_back({&p.d_qpos, {p.q_pos.data(), bytes_of(p.q_pos)}});
     parts.push_back({&p.d_has_shared, {p.has_shared.data(), bytes_of(p.has_shared)}});
     if (p.prefill) parts.push_back({&p.d_qrow0, {p.q_row0.data(), bytes_of(p.q_row0)}});
-    if (int rc = upload_subplan(p.main, p.d_head, parts)) return rc;
+    if (int rc = upload_subplan(p.main, p.d_head, s, parts)) return rc;
     if (p.cascade) {
-        if (int rc = upload_subplan(p.shared, p.d_head, parts)) return rc;
+        if (int rc = upload_subplan(p.shared, p.d_head, s, parts)) return rc;
         const size_t rows = size_t(p.batch) * p.n_q * p.n_q_heads;
         EP_CUDA_TRY(p.d_parts_o.reserve(2 * rows * p.d_head * sizeof(float)), "ep_plan cascade ws");
         EP_CUDA_TRY(p.d_parts_lse.reserve(2 * rows * sizeof(float)), "ep_plan cascade ws");

@@ -123,7 +123,8 @@ class Model:
         return p.value, n.value
 
     def last_attention_path(self) -> str:
-        return {1: "spliced", 2: "generic"}.get(lib().ep_model_last_attention_path(self._m), "none")
+        return {1: "spliced", 2: "generic", 3: "persistent"}.get(
+            lib().ep_model_last_attention_path(self._m), "none")
 
     def forward(self, tables, n_new, tokens, *, want_logits=True, want_hidden=False,
                 stream=None):

@@ -256,13 +256,16 @@ def test_errors_mirror_the_reference(cuda_handle):
         M.ModelConfig(2, 3, 8, 32).validate()
 
 
-@pytest.mark.parametrize("dtype,kv", [("f64", "f64"), ("f32", "f32"), ("f32", "bf16")])
-def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv):
+@pytest.mark.parametrize("dtype,kv,persist", [("f64", "f64", "0"), ("f32", "f32", "0"), ("f32", "bf16", "0"),
+                                               ("f32", "f32", "1")])
+def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv, persist, monkeypatch):
     """generate_batch (one CUDA graph per step, positions advanced on the
-    device, K1 plan built for the final length) = decode_step per token, for
-    3 sessions sharing a cloud prompt; the cached K/V are the same too."""
+    device, K1 plan built for the final length; or, persist=1, the K9
+    persistent kernel) = decode_step per token, for 3 sessions sharing a
+    cloud prompt; the cached K/V are the same too."""
     import torch
     M = _mod()
+    monkeypatch.setenv("EP_MODEL_PERSIST", persist)
     rng = O.SplitMix64(5)
     cloud = [rng.next_u64() % 256 for _ in range(100)]
     edges = [[rng.next_u64() % 256 for _ in range(n)] for n in (3, 40, 70)]
@@ -283,6 +286,7 @@ def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv):
     m1 = make(CFG1, dtype, kv, num_pages=64)
     s1 = sessions(m1)
     got = M.generate_batch(m1, [c for c, _ in s1], [t for _, t in s1], n_steps)
+    assert (m1.last_attention_path() == "persistent") == (persist == "1")
     m2 = make(CFG1, dtype, kv, num_pages=64)
     s2 = sessions(m2)
     for b, (c, t) in enumerate(s2):
