@@ -50,7 +50,6 @@ struct ep_model_s {
     DeviceBuffer weights;
     DeviceBuffer pe;      // sinusoid table [max_positions][d_model] fp64 (model.cpp:121-126)
     DeviceBuffer persist_layers, persist_scratch, persist_counters;  // K9 persistent rollout (fp32 models)
-    size_t persist_counters_n = 0;
     DeviceBuffer arrive;  // fused-argmax arrival counter (zero between launches)
     std::vector<std::unique_ptr<DeviceBuffer>> kpages, vpages;
     // per-forward workspace
@@ -651,8 +650,11 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     // persistent cooperative kernel instead of the CUDA-graph path below
     const char* persist_e = std::getenv("EP_MODEL_PERSIST");
     const bool persist_env = persist_e && persist_e[0] == '1';
+    int persist_ctas = m->h->n_sms;  // one CTA per SM (EP_PERSIST_CTAS: fewer)
+    if (const char* e = std::getenv("EP_PERSIST_CTAS"))
+        persist_ctas = std::max(1, std::min(m->h->n_sms, std::atoi(e)));
     if (persist_env && m->dt == EP_F32 && m->kv_dtype == EP_F32 &&
-        persist_supported(batch, m->D, m->H, m->F, m->V, m->P)) {
+        persist_supported(m->L, batch, m->D, m->H, m->F, m->V, m->P, persist_ctas)) {
         if (!m->persist_layers.ptr) {
             std::vector<PersistLayer> tab(m->L);
             for (int l = 0; l < m->L; ++l) {
@@ -672,18 +674,9 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
         for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
         const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
         const size_t part = B * m->H * size_t(max_chunks) * (m->dh + 2);
-        const size_t gpart = persist_gpart_floats(batch, m->D, m->F, m->V);
-        const size_t n_cnt = (std::max(std::max(3 * D, F), V) + 31) / 32;
-        const size_t floats = 3 * B * D + B * F + B * V + part + gpart;
+        const size_t floats = 3 * B * D + B * F + B * V + part;
         EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
-        if (m->persist_counters_n < n_cnt) {  // arrival counters start at zero; the kernel re-zeroes them
-            EP_CUDA_TRY(m->persist_counters.reserve(n_cnt * sizeof(int32_t)), "ep_model_generate counters");
-            // on the launch stream: a (non-blocking) stream does not wait for a
-            // legacy-stream memset, and reused memory is not zero
-            EP_CUDA_TRY(cudaMemsetAsync(m->persist_counters.ptr, 0, n_cnt * sizeof(int32_t), s),
-                        "ep_model_generate counters");
-            m->persist_counters_n = n_cnt;
-        }
+        EP_CUDA_TRY(m->persist_counters.reserve(2 * sizeof(int32_t)), "ep_model_generate counters");
         float* f0 = static_cast<float*>(m->persist_scratch.ptr);
         PersistArgs pa{};
         pa.layers = static_cast<const PersistLayer*>(m->persist_layers.ptr);
@@ -712,7 +705,6 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
         pa.h1 = f0 + 3 * B * D;
         pa.logits = pa.h1 + B * F;
         pa.part = pa.logits + B * V;
-        pa.gpart = pa.part + part;
         pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
         pa.out = static_cast<int32_t*>(out_dev.ptr);
         static unsigned long long* trace = [] {
@@ -723,7 +715,7 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
             return b;
         }();
         pa.trace = trace;
-        EP_CUDA_TRY(launch_decode_persist(pa, m->h->n_sms, s), "ep_model_generate persistent launch");
+        EP_CUDA_TRY(launch_decode_persist(pa, persist_ctas, s), "ep_model_generate persistent launch");
         if (trace) {  // debug: EP_TRACE=1 dumps the barrier timestamps to EP_TRACE_FILE
             std::vector<unsigned long long> hb(256);
             cudaStreamSynchronize(s);

@@ -113,14 +113,13 @@ struct PersistArgs {
     const PageDesc* pdesc;     // every request's pages (final table)
     const int64_t* req_page_off;
     float *x, *x2, *q, *h1, *logits, *part;  // scratch
-    float* gpart;              // GEMV k-chunk partial sums [K/32][B][N]
-    int32_t* counters;         // per column block arrivals, zero between stages
+    int32_t* counters;         // [2]: grid barrier arrivals, unembedding arrivals (zeroed per launch)
     int32_t* out;              // [n_steps][B] greedy tokens
     unsigned long long* trace; // debug: [8 steps][32] barrier timestamps of CTA 0 (may be null)
 };
-bool persist_supported(int B, int D, int H, int F, int V, int P);
-size_t persist_smem_bytes(int B, int D, int F, int H, int max_chunks);
-size_t persist_gpart_floats(int B, int D, int F, int V);
+// n_ctas = n_sms: one CTA per SM; weights stay resident in shared memory
+bool persist_supported(int L, int B, int D, int H, int F, int V, int P, int n_sms);
+size_t persist_smem_bytes(int L, int B, int D, int F, int H, int V, int max_chunks, int n_sms);
 cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s);
 
 // dst[i] = uniform(lo, hi) of SplitMix64(seed) draw first + i (fp64 draw,
