@@ -122,6 +122,7 @@ bool persist_supported(int L, int B, int D, int H, int F, int V, int P, int n_sm
 size_t persist_smem_bytes(int L, int B, int D, int F, int H, int V, int max_chunks, int n_sms);
 cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s);
 
+
 // dst[i] = uniform(lo, hi) of SplitMix64(seed) draw first + i (fp64 draw,
 // stored in dt = EP_F64 / EP_F32 / EP_BF16).
 cudaError_t launch_fill_uniform_at(int dt, void* dst, size_t n, uint64_t seed, uint64_t first,

@@ -155,11 +155,16 @@ def test_cfg1_fp32_spliced_kernels(cuda_handle):
     assert err <= 1e-4
 
 
-def test_cfg1_fp32_rollout_matches_golden(cuda_handle):
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_cfg1_fp32_rollout_matches_golden(cuda_handle, persist, monkeypatch):
+    # fp32 serving path (CUDA-graph rollout, or the K9 persistent kernel that a
+    # batch-1 rollout takes by default) = the reference's fp64 greedy tokens
     M = _mod()
+    monkeypatch.setenv("EP_MODEL_PERSIST", persist)
     m = make(CFG1, "f32", "f32")
     got = M.generate_split(m, GOLD["cfg1_cloud"], GOLD["cfg1_edge"], 64)
     assert got == GOLD["cfg1_rollout64"]
+    assert (m.last_attention_path() == "persistent") == (persist == "1")
 
 
 def test_cfg1_bf16_kv(cuda_handle):
@@ -286,7 +291,7 @@ def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv, persist, mon
     m1 = make(CFG1, dtype, kv, num_pages=64)
     s1 = sessions(m1)
     got = M.generate_batch(m1, [c for c, _ in s1], [t for _, t in s1], n_steps)
-    assert (m1.last_attention_path() == "persistent") == (persist == "1")
+    assert (m1.last_attention_path() == "persistent") == (persist != "0")
     m2 = make(CFG1, dtype, kv, num_pages=64)
     s2 = sessions(m2)
     for b, (c, t) in enumerate(s2):

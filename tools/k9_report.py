@@ -10,5 +10,6 @@ for f in sorted(glob.glob("gpurun_out/mb_*.json")):
 for f in sorted(glob.glob("gpurun_out/trace_persist_*.bin")):
     t = np.fromfile(f, dtype=np.uint64).reshape(8, 32).astype(np.int64)
     for s in (1, 2):
-        r = t[s]; st = r[31]; n = [int(x - st) for x in r[:31] if x]
-        print(f, s, "stage ends (ns):", n, "gaps:", np.diff([0] + n).tolist())
+        r = t[s]; st = r[31]
+        n = [int(x - st) for x in r[:31] if x]
+        print(f, s, "barriers (ns):", n, "gaps:", np.diff([0] + n).tolist())
