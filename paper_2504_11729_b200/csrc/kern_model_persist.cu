@@ -59,16 +59,8 @@ __host__ __device__ inline size_t resident_floats(int L, int D, int F, int V, in
     return L * layer + pad4(size_t(D) * stage_ncp(V, G));
 }
 
-// Attention / GEMV reduction scratch floats.
-__host__ __device__ inline size_t scratch_floats(int B, int H, int max_chunks) {
-    size_t v = size_t(B) * H * max_chunks + 16;
-    if (v < size_t(kPThreads / 32) * kMaxB * kMaxNcp) v = size_t(kPThreads / 32) * kMaxB * kMaxNcp;
-    return pad4(v);
-}
-
-// Attention page buffers: kNBuf x (K, V) of one (page, head), P x dh floats each.
-constexpr int kNBuf = 2;
-__host__ __device__ inline size_t att_buf_floats(int P, int dh) { return size_t(kNBuf) * 2 * P * dh; }
+// GEMV reduction / attention q scratch floats ([8 warps][kMaxB][kMaxNcp] >= [8 warps][128]).
+__host__ __device__ inline size_t scratch_floats() { return size_t(kPThreads / 32) * kMaxB * kMaxNcp; }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
@@ -184,15 +176,71 @@ __device__ void load_bias(const Stage& st, const float* b) {
     for (int j = threadIdx.x; j < st.ncp; j += kPThreads) st.bias[j] = j < st.nc ? __ldg(b + st.c0 + j) : 0.f;
 }
 
-// Copy this CTA's columns of W (row-major [K][ld], columns via col_of) into ws.
+// Copy this CTA's columns of W (column pointer col_ptr(c, k)) into ws: eight
+// loads per thread in flight (a launch for one decode step spends most of its
+// time here otherwise).
 template <typename ColPtr>
 __device__ void load_stage(const Stage& st, ColPtr col_ptr) {
-    for (int i = threadIdx.x; i < st.K * st.ncp; i += kPThreads) {
-        const int k = i / st.ncp, j = i - k * st.ncp;
-        float v = 0.f;
-        if (j < st.nc) v = __ldg(col_ptr(st.c0 + j, k));
-        st.ws[i] = v;
+    const int total = st.K * st.ncp;
+    for (int i0 = threadIdx.x; i0 < total; i0 += 8 * kPThreads) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * kPThreads, k = i / st.ncp, j = i - k * st.ncp;
+            v[u] = (i < total && j < st.nc) ? __ldg(col_ptr(st.c0 + j, k)) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * kPThreads < total) st.ws[i0 + u * kPThreads] = v[u];
     }
+}
+
+// One warp: partial attention (attention.cpp:80-114) of q over nk <= 32
+// consecutive keys (rows of kt / vt, DH floats each) -> part = {max, sum,
+// o[DH]}.
+template <int DH>
+__device__ __forceinline__ void attn_task(const float* kt, const float* vt, const float* q, int nk, float scale,
+                                          float* part) {
+    constexpr int KV4 = DH / 4, VPL = DH / 32;
+    const int lane = threadIdx.x & 31;
+    float4 kv[KV4];
+    float vv[32][VPL];
+    const float4* kr = reinterpret_cast<const float4*>(kt + size_t(lane) * DH);
+#pragma unroll
+    for (int i = 0; i < KV4; ++i) kv[i] = lane < nk ? __ldcg(kr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) vv[j][v] = j < nk ? __ldcg(vt + size_t(j) * DH + lane * VPL + v) : 0.f;
+    // the dot product of this lane's key; q is a shared-memory broadcast
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < KV4; i += 2) {
+        const float4 a0 = q4[i], b0 = kv[i];
+        s0 = fmaf(a0.x, b0.x, fmaf(a0.y, b0.y, fmaf(a0.z, b0.z, fmaf(a0.w, b0.w, s0))));
+        const float4 a1 = q4[i + 1], b1 = kv[i + 1];
+        s1 = fmaf(a1.x, b1.x, fmaf(a1.y, b1.y, fmaf(a1.z, b1.z, fmaf(a1.w, b1.w, s1))));
+    }
+    const float sc = lane < nk ? (s0 + s1) * scale : -INFINITY;
+    const float m = warp_max(sc);
+    const float p = lane < nk ? __expf(sc - m) : 0.f;
+    const float l = warp_sum(p);
+    float o[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) o[v] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, p, j);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) o[v] = fmaf(pj, vv[j][v], o[v]);
+    }
+    if (lane == 0) {
+        part[0] = m;
+        part[1] = l;
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) part[2 + lane * VPL + v] = o[v];
 }
 
 __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const PersistArgs a) {
@@ -232,13 +280,7 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
     float* res = xs + size_t(B) * Kmax;        // [B][ncp_d] residual stream of this CTA's columns
     float* s_att = res + pad4(size_t(B) * ncp_d);  // attention / reduction scratch
     float* red = s_att;                        // [8 warps][kMaxB][kMaxNcp]
-    float* kvbuf = s_att + scratch_floats(B, H, a.max_chunks);  // [kNBuf][K | V][P][dh]
-    __shared__ __align__(8) uint64_t mbar[kNBuf];
-    if (tid == 0) {
-        for (int i = 0; i < kNBuf; ++i) mbar_init(&mbar[i], 1);
-        fence_mbar_init();
-    }
-    unsigned mb_phase = 0;  // parity bit per buffer
+    const int MC = 2 * a.max_chunks;            // partials per (row, head): 32-key halves
     __syncthreads();
 
     unsigned n_bar = 0;
@@ -298,163 +340,83 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
             });
             sync(t);
 
-            // ---- attention partials: one (row, head, page) task per CTA ----
-            // the task's K and V rows (nk x dh, contiguous in the page) arrive by
-            // bulk async copy into a double buffer: the next task's copy is in
-            // flight while this one computes
+            // ---- attention partials: (row, head, page, 32-key half) warp tasks ----
+            // spread one per CTA first (task u: CTA u % G, warp u / G); a task's
+            // K and V rows are loaded in one L2 round trip (attn_task)
             {
                 int total = 0;
-                for (int b = 0; b < B; ++b) total += H * int(a.req_page_off[b + 1] - a.req_page_off[b]);
-                float* qh = s_att;        // [128]
-                float* ps = s_att + 128;  // [64] scores, then probabilities
-                float* po = s_att + 192;  // [8][128] PV partials of the key groups
-                float* rr = s_att + 1216; // [2] max, sum
-                struct Task {
-                    int b, h, c, nk, page;
-                };
-                auto task_of = [&](int u) {
-                    Task tk;
+                for (int b = 0; b < B; ++b) total += H * 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
+                for (int u = warp * gridDim.x + blockIdx.x; u < total; u += gridDim.x * kPWarps) {
                     int b = 0, rem = u;
-                    while (rem >= H * int(a.req_page_off[b + 1] - a.req_page_off[b])) {
-                        rem -= H * int(a.req_page_off[b + 1] - a.req_page_off[b]);
+                    while (rem >= H * 2 * int(a.req_page_off[b + 1] - a.req_page_off[b])) {
+                        rem -= H * 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
                         ++b;
                     }
-                    const int npg = int(a.req_page_off[b + 1] - a.req_page_off[b]);
-                    tk.b = b;
-                    tk.h = rem / npg;
-                    tk.c = rem - tk.h * npg;
-                    const PageDesc d = a.pdesc[a.req_page_off[b] + tk.c];
+                    const int n2 = 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
+                    const int h = rem / n2, c2 = rem - h * n2;
+                    const PageDesc d = a.pdesc[a.req_page_off[b] + c2 / 2];
                     const int64_t vis = int64_t(a.pos[size_t(t) * B + b]) - d.pos + 1;
-                    tk.nk = vis <= 0 ? 0 : (vis < d.n_tok ? int(vis) : d.n_tok);
-                    tk.page = d.page;
-                    return tk;
-                };
-                auto issue = [&](int i) {  // thread 0: copy task i of this CTA into buffer i % kNBuf
-                    const int u = blockIdx.x + i * gridDim.x;
-                    if (u >= total) return;
-                    const Task tk = task_of(u);
-                    if (tk.nk == 0) return;
-                    const int slot = i % kNBuf;
-                    const uint32_t bytes = uint32_t(tk.nk) * dh * 4;
-                    float* kb = kvbuf + size_t(slot) * 2 * P * dh;
-                    const size_t off = (size_t(tk.page) * H + tk.h) * P * dh;
-                    mbar_arrive_expect_tx(&mbar[slot], 2 * bytes);
-                    bulk_g2s(kb, Lw.kp + off, bytes, &mbar[slot]);
-                    bulk_g2s(kb + size_t(P) * dh, Lw.vp + off, bytes, &mbar[slot]);
-                };
-                if (tid == 0) {
-                    // K/V rows were written by generic stores of other CTAs
-                    // (ordered by the grid barrier); the copies read them
-                    // through the async proxy
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
-                    for (int i = 0; i < kNBuf; ++i) issue(i);
-                }
-                const int chunk = dh / 4;
-                for (int i = 0, u = blockIdx.x; u < total; ++i, u += gridDim.x) {
-                    const Task tk = task_of(u);
-                    const int slot = i % kNBuf, nk = tk.nk;
-                    float* part = a.part + (size_t(tk.b * H + tk.h) * a.max_chunks + tk.c) * (dh + 2);
-                    if (nk == 0) {
-                        if (tid == 0) {
+                    const int nk_page = vis <= 0 ? 0 : (vis < d.n_tok ? int(vis) : d.n_tok);
+                    const int k0 = (c2 & 1) * 32;
+                    const int nk = nk_page - k0 < 0 ? 0 : (nk_page - k0 > 32 ? 32 : nk_page - k0);
+                    float* part = a.part + (size_t(b * H + h) * MC + c2) * (dh + 2);
+                    if (nk == 0) {  // no visible key: an empty partial (weight 0, zero output)
+                        if (lane == 0) {
                             part[0] = -INFINITY;
                             part[1] = 0.f;
-                            issue(i + kNBuf);
                         }
+                        for (int e = lane; e < dh; e += 32) part[2 + e] = 0.f;
                         continue;
                     }
-                    for (int e = tid; e < dh; e += kPThreads) qh[e] = __ldcg(a.q + size_t(tk.b) * D + tk.h * dh + e);
-                    mbar_wait(&mbar[slot], (mb_phase >> slot) & 1u);
-                    mb_phase ^= 1u << slot;
-                    __syncthreads();
-                    const float* ks = kvbuf + size_t(slot) * 2 * P * dh;
-                    const float* vs = ks + size_t(P) * dh;
-                    // scores: thread = (key tid / 4, quarter of d_head); the
-                    // quarter's dimensions are rotated by the key (bank spread)
-                    {
-                        const int j = tid >> 2, qq = tid & 3;
-                        float dot = 0.f;
-                        if (j < nk) {
-                            const float* kr = ks + size_t(j) * dh + qq * chunk;
-                            const float* qr = qh + qq * chunk;
-                            for (int d0 = 0; d0 < chunk; ++d0) {
-                                const int dd = (d0 + j) & (chunk - 1);
-                                dot = fmaf(qr[dd], kr[dd], dot);
-                            }
-                        }
-                        dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-                        dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-                        if (qq == 0 && j < 64) ps[j] = j < nk ? dot * scale : -INFINITY;
-                    }
-                    __syncthreads();
-                    if (warp == 0) {
-                        const float s0 = ps[lane], s1v = ps[lane + 32];
-                        const float m = warp_max(fmaxf(s0, s1v));
-                        const float p0 = lane < nk ? __expf(s0 - m) : 0.f;
-                        const float p1 = lane + 32 < nk ? __expf(s1v - m) : 0.f;
-                        ps[lane] = p0;
-                        ps[lane + 32] = p1;
-                        const float lsum = warp_sum(p0 + p1);
-                        if (lane == 0) {
-                            rr[0] = m;
-                            rr[1] = lsum;
-                        }
-                    }
-                    __syncthreads();
-                    // PV: thread = (dimension e, key group g); groups added in order
-                    const int ng = kPThreads / dh;
-                    {
-                        const int e = tid % dh, g = tid / dh;
-                        float o = 0.f;
-                        for (int j = g; j < nk; j += ng) o = fmaf(ps[j], vs[size_t(j) * dh + e], o);
-                        po[g * 128 + e] = o;
-                    }
-                    __syncthreads();
-                    for (int e = tid; e < dh; e += kPThreads) {
-                        float o = 0.f;
-                        for (int gg = 0; gg < ng; ++gg) o += po[gg * 128 + e];
-                        part[2 + e] = o;
-                    }
-                    if (tid == 0) {
-                        part[0] = rr[0];
-                        part[1] = rr[1];
-                        issue(i + kNBuf);  // the buffer is free again (all reads done above)
-                    }
+                    // q of (b, h) straight from L2 (written before the barrier)
+                    float* qs = s_att + warp * 128;
+                    for (int e = lane; e < dh; e += 32) qs[e] = __ldcg(a.q + size_t(b) * D + h * dh + e);
+                    __syncwarp();
+                    const size_t off = ((size_t(d.page) * H + h) * P + k0) * dh;
+                    if (dh == 64)
+                        attn_task<64>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
+                    else
+                        attn_task<32>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
+                    __syncwarp();
                 }
-                __syncthreads();
             }
             sync(t);
 
             // ---- LSE merge of the partials (every CTA, all rows) + Wo + residual ----
-            {
-                float* wts = s_att;  // [B * H][max_chunks]
-                for (int bh = warp; bh < B * H; bh += kPWarps) {
-                    const int b = bh / H;
-                    const int npg = int(a.req_page_off[b + 1] - a.req_page_off[b]);
-                    const float* base = a.part + size_t(bh) * a.max_chunks * (dh + 2);
-                    float M = -INFINITY;
-                    for (int c = lane; c < npg; c += 32) M = fmaxf(M, __ldcg(base + size_t(c) * (dh + 2)));
-                    M = warp_max(M);
-                    float Ls = 0.f;
-                    for (int c = lane; c < npg; c += 32) {  // L1 hits: the maxima were just read
-                        const float m = base[size_t(c) * (dh + 2)];
-                        const float wgt = m == -INFINITY ? 0.f : __expf(m - M);
-                        wts[bh * a.max_chunks + c] = wgt;
-                        Ls += wgt * base[size_t(c) * (dh + 2) + 1];
+            // a thread's (row, dimension): the maxima, sums and outputs of all
+            // of the row's partials are loaded in one L2 round trip and merged
+            // online (attention.cpp:116-145)
+            for (int i = tid; i < B * D; i += kPThreads) {
+                const int b = i / D, cc = i - b * D, h = cc / dh, e = cc - h * dh;
+                const int n2 = 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
+                const float* base = a.part + size_t(b * H + h) * MC * (dh + 2);
+                float o = 0.f, Ls = 0.f, M = -INFINITY;
+                for (int c0 = 0; c0 < n2; c0 += 32) {
+                    float mv[32], lv[32], ov[32];
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        const bool ok = c0 + u < n2;
+                        const float* pc = base + size_t(c0 + u) * (dh + 2);
+                        mv[u] = ok ? __ldcg(pc) : -INFINITY;
+                        lv[u] = ok ? __ldcg(pc + 1) : 0.f;
+                        ov[u] = ok ? __ldcg(pc + 2 + e) : 0.f;
                     }
-                    Ls = warp_sum(Ls);
-                    for (int c = lane; c < npg; c += 32) wts[bh * a.max_chunks + c] /= Ls;
+                    float Mb = M;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) Mb = fmaxf(Mb, mv[u]);
+                    const float sc = M == -INFINITY ? 0.f : __expf(M - Mb);
+                    o *= sc;
+                    Ls *= sc;
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) {
+                        if (mv[u] == -INFINITY) continue;  // empty partial: never touch its output
+                        const float wgt = __expf(mv[u] - Mb);
+                        Ls = fmaf(wgt, lv[u], Ls);
+                        o = fmaf(wgt, ov[u], o);
+                    }
+                    M = Mb;
                 }
-                __syncthreads();
-                for (int i = tid; i < B * D; i += kPThreads) {
-                    const int b = i / D, cc = i - b * D, h = cc / dh, e = cc - h * dh;
-                    const int npg = int(a.req_page_off[b + 1] - a.req_page_off[b]);
-                    const float* base = a.part + size_t(b * H + h) * a.max_chunks * (dh + 2) + 2 + e;
-                    const float* wr = wts + (b * H + h) * a.max_chunks;
-                    float o = 0.f;
-#pragma unroll 8
-                    for (int c = 0; c < npg; ++c) o = fmaf(wr[c], __ldcg(base + size_t(c) * (dh + 2)), o);
-                    xs[i] = o;
-                }
+                xs[i] = o / Ls;
             }
             __syncthreads();
             gemv_cols(xs, so[l].ws, B, D, so[l].ncp, so[l].c0, so[l].nc, red, [&](int b, int c, float v) {
@@ -536,17 +498,17 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
 bool persist_supported(int L, int B, int D, int H, int F, int V, int P, int n_sms) {
     const int dh = D / H;
     if (L < 1 || L > 8 || B < 1 || B > kMaxB || D % 4 || F % 4 || P > 64 || n_sms < 1) return false;
-    if (dh != 32 && dh != 64 && dh != 128) return false;  // power-of-two quarters, 256 / dh key groups
+    if (dh != 32 && dh != 64) return false;  // attn_task: a lane's K row and V columns in registers
     if (stage_ncp(std::max(std::max(3 * D, F), V), n_sms) > kMaxNcp) return false;
     return persist_smem_bytes(L, B, D, F, H, V, 1, n_sms) <= 200 * 1024;
 }
 
 size_t persist_smem_bytes(int L, int B, int D, int F, int H, int V, int max_chunks, int n_sms) {
     const int Kmax = F > D ? F : D;
-    const int dh = D / H, P = 64;
+    (void)H;
+    (void)max_chunks;
     return sizeof(float) * (resident_floats(L, D, F, V, n_sms) + size_t(B) * Kmax +
-                            pad4(size_t(B) * stage_ncp(D, n_sms)) + scratch_floats(B, H, max_chunks) +
-                            att_buf_floats(P, dh));
+                            pad4(size_t(B) * stage_ncp(D, n_sms)) + scratch_floats());
 }
 
 cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s) {

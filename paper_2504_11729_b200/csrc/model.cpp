@@ -516,6 +516,104 @@ int ep_model_weight(ep_model m, const char* name, int32_t layer, void** ptr, siz
 
 int ep_model_last_attention_path(ep_model m) { return m ? m->last_path : 0; }
 
+// K9: whether decode rows of this batch run in the persistent cooperative
+// kernel — a single-session decode of a small fp32 model by default (config
+// 1: 45 vs 64 us / token for the CUDA-graph rollout; slower from batch 8 on).
+// EP_MODEL_PERSIST=0 disables it, =1 forces it for every supported batch.
+bool use_persist(ep_model m, int batch, int* n_ctas) {
+    const char* e = std::getenv("EP_MODEL_PERSIST");
+    if (!(e ? e[0] == '1' : batch == 1)) return false;
+    if (m->dt != EP_F32 || m->kv_dtype != EP_F32) return false;
+    int c = m->h->n_sms;  // one CTA per SM (EP_PERSIST_CTAS: fewer)
+    if (const char* ec = std::getenv("EP_PERSIST_CTAS")) c = std::max(1, std::min(m->h->n_sms, std::atoi(ec)));
+    *n_ctas = c;
+    return persist_supported(m->L, batch, m->D, m->H, m->F, m->V, m->P, c);
+}
+
+// n_steps greedy steps of `batch` decode rows in one K9 launch: ps holds the
+// uploaded step-major metadata (token of step 0, pos / dst_page / dst_slot
+// [n_steps][batch]) and every request's final page table; tokens -> out
+// [n_steps][batch] (device), the last step's logits -> logits_out (device
+// fp32 [batch][V], may be null).
+int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int batch, int n_steps,
+                int persist_ctas, int32_t* out, void* logits_out, cudaStream_t s) {
+    if (!m->persist_layers.ptr) {
+        std::vector<PersistLayer> tab(m->L);
+        for (int l = 0; l < m->L; ++l) {
+            const LayerOffsets& o = m->lw[l];
+            tab[l] = {reinterpret_cast<const float*>(m->wptr(o.wq)), reinterpret_cast<const float*>(m->wptr(o.wk)),
+                      reinterpret_cast<const float*>(m->wptr(o.wv)), reinterpret_cast<const float*>(m->wptr(o.wo)),
+                      reinterpret_cast<const float*>(m->wptr(o.w1)), reinterpret_cast<const float*>(m->wptr(o.b1)),
+                      reinterpret_cast<const float*>(m->wptr(o.w2)), reinterpret_cast<const float*>(m->wptr(o.b2)),
+                      static_cast<float*>(m->kpages[l]->ptr), static_cast<float*>(m->vpages[l]->ptr)};
+        }
+        EP_CUDA_TRY(m->persist_layers.reserve(tab.size() * sizeof(PersistLayer)), "ep_model_generate");
+        EP_CUDA_TRY(cudaMemcpy(m->persist_layers.ptr, tab.data(), tab.size() * sizeof(PersistLayer),
+                               cudaMemcpyHostToDevice),
+                    "ep_model_generate");
+    }
+    int max_chunks = 1;
+    for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
+    const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
+    const size_t part = B * m->H * size_t(2 * max_chunks) * (m->dh + 2);  // 32-key halves
+    const size_t floats = 3 * B * D + B * F + B * V + part;
+    EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
+    EP_CUDA_TRY(m->persist_counters.reserve(2 * sizeof(int32_t)), "ep_model_generate counters");
+    float* f0 = static_cast<float*>(m->persist_scratch.ptr);
+    PersistArgs pa{};
+    pa.layers = static_cast<const PersistLayer*>(m->persist_layers.ptr);
+    pa.L = m->L;
+    pa.B = batch;
+    pa.D = m->D;
+    pa.H = m->H;
+    pa.dh = m->dh;
+    pa.F = m->F;
+    pa.V = m->V;
+    pa.P = m->P;
+    pa.n_steps = n_steps;
+    pa.max_chunks = max_chunks;
+    pa.emb = reinterpret_cast<const float*>(m->wptr(0));
+    pa.pe = static_cast<const double*>(m->pe.ptr);
+    pa.unembed = reinterpret_cast<const float*>(m->wptr(m->off_unembed));
+    pa.first = ps.tok;
+    pa.pos = ps.pos;
+    pa.dst_page = ps.dst_page;
+    pa.dst_slot = ps.dst_slot;
+    pa.pdesc = ps.pdesc;
+    pa.req_page_off = ps.req_page_off;
+    pa.x = f0;
+    pa.x2 = f0 + B * D;
+    pa.q = f0 + 2 * B * D;
+    pa.h1 = f0 + 3 * B * D;
+    float* logits_ws = pa.h1 + B * F;
+    pa.logits = logits_out ? static_cast<float*>(logits_out) : logits_ws;
+    pa.part = logits_ws + B * V;
+    pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
+    pa.out = out;
+    static unsigned long long* trace = [] {
+        unsigned long long* b = nullptr;
+        const char* e = std::getenv("EP_TRACE");
+        if (e && e[0] == '1' && cudaMalloc(&b, 256 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 256 * sizeof(unsigned long long));
+        return b;
+    }();
+    pa.trace = trace;
+    EP_CUDA_TRY(launch_decode_persist(pa, persist_ctas, s), "ep_model_generate persistent launch");
+    if (trace) {  // debug: EP_TRACE=1 dumps the barrier timestamps to EP_TRACE_FILE
+        std::vector<unsigned long long> hb(256);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(hb.data(), trace, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        const char* f = std::getenv("EP_TRACE_FILE");
+        if (FILE* fp = std::fopen(f ? f : "ep_trace_persist.bin", "wb")) {
+            std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), fp);
+            std::fclose(fp);
+        }
+    }
+    m->h->launches++;
+    m->last_path = 3;
+    return EP_OK;
+}
+
 int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
                      const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* hidden,
                      void* logits, int32_t* next, ep_stream stream) {
@@ -554,6 +652,13 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
     if (int rc = upload_meta(m, md, ps, s)) return rc;
     ps.n = n;
     ps.batch = batch;
+
+    // decode_step of one session of a small fp32 model: the K9 persistent
+    // kernel (one launch for the whole forward)
+    int persist_ctas = 0;
+    if (all_decode && !hidden && use_persist(m, batch, &persist_ctas))
+        return run_persist(m, reqs, ps, batch, 1, persist_ctas,
+                           next ? next : static_cast<int32_t*>(m->next_ws.ptr), logits, s);
 
     // attention: the spliced decode / prefill plans where a kernel instance
     // exists, otherwise the generic paged kernel
@@ -646,90 +751,11 @@ int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, cons
     ps.next = static_cast<int32_t*>(out_dev.ptr);
     ps.logits = m->logits_ws.ptr;
 
-    // K9: a single-session rollout of a small fp32 model runs in one
-    // persistent cooperative kernel instead of the CUDA-graph path below
-    // (faster at batch 1: 50 vs 64 us / token on config 1; slower from batch
-    // 4 on). EP_MODEL_PERSIST=0 disables it, =1 forces it for every batch.
-    const char* persist_e = std::getenv("EP_MODEL_PERSIST");
-    const bool persist_env = persist_e ? persist_e[0] == '1' : batch == 1;
-    int persist_ctas = m->h->n_sms;  // one CTA per SM (EP_PERSIST_CTAS: fewer)
-    if (const char* e = std::getenv("EP_PERSIST_CTAS"))
-        persist_ctas = std::max(1, std::min(m->h->n_sms, std::atoi(e)));
-    if (persist_env && m->dt == EP_F32 && m->kv_dtype == EP_F32 &&
-        persist_supported(m->L, batch, m->D, m->H, m->F, m->V, m->P, persist_ctas)) {
-        if (!m->persist_layers.ptr) {
-            std::vector<PersistLayer> tab(m->L);
-            for (int l = 0; l < m->L; ++l) {
-                const LayerOffsets& o = m->lw[l];
-                tab[l] = {reinterpret_cast<const float*>(m->wptr(o.wq)), reinterpret_cast<const float*>(m->wptr(o.wk)),
-                          reinterpret_cast<const float*>(m->wptr(o.wv)), reinterpret_cast<const float*>(m->wptr(o.wo)),
-                          reinterpret_cast<const float*>(m->wptr(o.w1)), reinterpret_cast<const float*>(m->wptr(o.b1)),
-                          reinterpret_cast<const float*>(m->wptr(o.w2)), reinterpret_cast<const float*>(m->wptr(o.b2)),
-                          static_cast<float*>(m->kpages[l]->ptr), static_cast<float*>(m->vpages[l]->ptr)};
-            }
-            EP_CUDA_TRY(m->persist_layers.reserve(tab.size() * sizeof(PersistLayer)), "ep_model_generate");
-            EP_CUDA_TRY(cudaMemcpy(m->persist_layers.ptr, tab.data(), tab.size() * sizeof(PersistLayer),
-                                   cudaMemcpyHostToDevice),
-                        "ep_model_generate");
-        }
-        int max_chunks = 1;
-        for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
-        const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
-        const size_t part = B * m->H * size_t(max_chunks) * (m->dh + 2);
-        const size_t floats = 3 * B * D + B * F + B * V + part;
-        EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
-        EP_CUDA_TRY(m->persist_counters.reserve(2 * sizeof(int32_t)), "ep_model_generate counters");
-        float* f0 = static_cast<float*>(m->persist_scratch.ptr);
-        PersistArgs pa{};
-        pa.layers = static_cast<const PersistLayer*>(m->persist_layers.ptr);
-        pa.L = m->L;
-        pa.B = batch;
-        pa.D = m->D;
-        pa.H = m->H;
-        pa.dh = m->dh;
-        pa.F = m->F;
-        pa.V = m->V;
-        pa.P = m->P;
-        pa.n_steps = n_steps;
-        pa.max_chunks = max_chunks;
-        pa.emb = reinterpret_cast<const float*>(m->wptr(0));
-        pa.pe = static_cast<const double*>(m->pe.ptr);
-        pa.unembed = reinterpret_cast<const float*>(m->wptr(m->off_unembed));
-        pa.first = ps.tok;
-        pa.pos = ps.pos;
-        pa.dst_page = ps.dst_page;
-        pa.dst_slot = ps.dst_slot;
-        pa.pdesc = ps.pdesc;
-        pa.req_page_off = ps.req_page_off;
-        pa.x = f0;
-        pa.x2 = f0 + B * D;
-        pa.q = f0 + 2 * B * D;
-        pa.h1 = f0 + 3 * B * D;
-        pa.logits = pa.h1 + B * F;
-        pa.part = pa.logits + B * V;
-        pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
-        pa.out = static_cast<int32_t*>(out_dev.ptr);
-        static unsigned long long* trace = [] {
-            unsigned long long* b = nullptr;
-            const char* e = std::getenv("EP_TRACE");
-            if (e && e[0] == '1' && cudaMalloc(&b, 256 * sizeof(unsigned long long)) == cudaSuccess)
-                cudaMemset(b, 0, 256 * sizeof(unsigned long long));
-            return b;
-        }();
-        pa.trace = trace;
-        EP_CUDA_TRY(launch_decode_persist(pa, persist_ctas, s), "ep_model_generate persistent launch");
-        if (trace) {  // debug: EP_TRACE=1 dumps the barrier timestamps to EP_TRACE_FILE
-            std::vector<unsigned long long> hb(256);
-            cudaStreamSynchronize(s);
-            cudaMemcpy(hb.data(), trace, hb.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-            const char* f = std::getenv("EP_TRACE_FILE");
-            if (FILE* fp = std::fopen(f ? f : "ep_trace_persist.bin", "wb")) {
-                std::fwrite(hb.data(), sizeof(unsigned long long), hb.size(), fp);
-                std::fclose(fp);
-            }
-        }
-        m->h->launches++;
-        m->last_path = 3;
+    int persist_ctas = 0;
+    if (use_persist(m, batch, &persist_ctas)) {
+        if (int rc = run_persist(m, reqs, ps, batch, n_steps, persist_ctas, static_cast<int32_t*>(out_dev.ptr),
+                                 nullptr, s))
+            return rc;
         std::vector<int32_t> host(size_t(n_steps) * batch);
         EP_CUDA_TRY(cudaMemcpyAsync(host.data(), out_dev.ptr, host.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
                     "ep_model_generate tokens");

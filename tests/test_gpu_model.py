@@ -148,10 +148,15 @@ def _teacher_forced(m, cfg, n_steps, tol):
     return max(errs)
 
 
-def test_cfg1_fp32_spliced_kernels(cuda_handle):
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_cfg1_fp32_spliced_kernels(cuda_handle, persist, monkeypatch):
+    # decode_step logits of the fp32 serving path against the fp64 reference:
+    # K1 spliced decode inside the layer-by-layer forward, or (persist=1, the
+    # batch-1 default) the K9 persistent kernel
+    monkeypatch.setenv("EP_MODEL_PERSIST", persist)
     m = make(CFG1, "f32", "f32")
     err = _teacher_forced(m, CFG1, 24, 1e-3)
-    assert m.last_attention_path() == "spliced"  # K1 decode (fp32, d_head 64)
+    assert m.last_attention_path() == ("persistent" if persist == "1" else "spliced")  # d_head 64
     assert err <= 1e-4
 
 
@@ -168,7 +173,7 @@ def test_cfg1_fp32_rollout_matches_golden(cuda_handle, persist, monkeypatch):
 
 
 def test_cfg1_bf16_kv(cuda_handle):
-    m = make(CFG1, "f32", "bf16")
+    m = make(CFG1, "f32", "bf16")  # bf16 pages: never the K9 kernel
     _teacher_forced(m, CFG1, 8, 2e-2)
     assert m.last_attention_path() == "spliced"
 
