@@ -243,25 +243,31 @@ __device__ __forceinline__ void attn_task(const float* kt, const float* vt, cons
     for (int v = 0; v < VPL; ++v) part[2 + lane * VPL + v] = o[v];
 }
 
-__global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const PersistArgs a) {
-    extern __shared__ __align__(16) float smem_f[];
-    const int B = a.B, D = a.D, H = a.H, dh = a.dh, F = a.F, V = a.V, P = a.P, L = a.L;
-    const int Kmax = F > D ? F : D;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const float scale = 1.f / sqrtf(float(dh));
-    unsigned* bar = reinterpret_cast<unsigned*>(a.counters);
-    unsigned* arrive = bar + 1;
+// The shared-memory layout of one CTA's resident weights from `base`: per
+// layer the Q|K|V, Wo, W1 (+ b1) and W2 (+ b2) column slices, then the
+// unembedding's; base is advanced past them.
+__device__ void resident_layout(int L, int D, int F, int V, float*& base, Stage* sq, Stage* so, Stage* s1,
+                                Stage* s2, Stage& su) {
+    for (int l = 0; l < L; ++l) {
+        sq[l] = make_stage(D, 3 * D, false, base);
+        so[l] = make_stage(D, D, false, base);
+        s1[l] = make_stage(D, F, true, base);
+        s2[l] = make_stage(F, D, true, base);
+    }
+    su = make_stage(D, V, false, base);
+}
 
-    // ---- resident weights: this CTA's columns of every stage ----
-    float* wcur = smem_f;
+// CTA i of a G-CTA grid writes CTA i's resident image (the same bytes the
+// rollout kernel keeps in shared memory) to image + i * resident_floats.
+__global__ void __launch_bounds__(kPThreads) persist_image_kernel(const PersistArgs a) {
+    const int L = a.L, D = a.D, F = a.F, V = a.V;
+    float* base = a.image_out + size_t(blockIdx.x) * resident_floats(L, D, F, V, gridDim.x);
     constexpr int kMaxL = 8;
     Stage sq[kMaxL], so[kMaxL], s1[kMaxL], s2[kMaxL];
+    Stage su;
+    resident_layout(L, D, F, V, base, sq, so, s1, s2, su);
     for (int l = 0; l < L; ++l) {
         const PersistLayer& Lw = a.layers[l];
-        sq[l] = make_stage(D, 3 * D, false, wcur);
-        so[l] = make_stage(D, D, false, wcur);
-        s1[l] = make_stage(D, F, true, wcur);
-        s2[l] = make_stage(F, D, true, wcur);
         load_bias(s1[l], Lw.b1);
         load_bias(s2[l], Lw.b2);
         load_stage(sq[l], [&](int c, int k) {
@@ -273,8 +279,38 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
         load_stage(s1[l], [&](int c, int k) { return Lw.w1 + size_t(k) * F + c; });
         load_stage(s2[l], [&](int c, int k) { return Lw.w2 + size_t(k) * D + c; });
     }
-    const Stage su = make_stage(D, V, false, wcur);
     load_stage(su, [&](int c, int k) { return a.unembed + size_t(k) * V + c; });
+}
+
+__global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const PersistArgs a) {
+    extern __shared__ __align__(16) float smem_f[];
+    const int B = a.B, D = a.D, H = a.H, dh = a.dh, F = a.F, V = a.V, P = a.P, L = a.L;
+    const int Kmax = F > D ? F : D;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const float scale = 1.f / sqrtf(float(dh));
+    unsigned* bar = reinterpret_cast<unsigned*>(a.counters);
+    unsigned* arrive = bar + 1;
+
+    // ---- resident weights: this CTA's columns of every stage ----
+    // a.image (built once per model by persist_image_kernel) holds every
+    // CTA's shared-memory image contiguously: one bulk async copy
+    float* wcur = smem_f;
+    constexpr int kMaxL = 8;
+    Stage sq[kMaxL], so[kMaxL], s1[kMaxL], s2[kMaxL];
+    Stage su;
+    resident_layout(L, D, F, V, wcur, sq, so, s1, s2, su);
+    {
+        __shared__ __align__(8) uint64_t img_bar;
+        if (tid == 0) {
+            mbar_init(&img_bar, 1);
+            fence_mbar_init();
+            const uint32_t bytes = uint32_t((wcur - smem_f) * sizeof(float));
+            mbar_arrive_expect_tx(&img_bar, bytes);
+            bulk_g2s(smem_f, a.image + size_t(blockIdx.x) * (wcur - smem_f), bytes, &img_bar);
+        }
+        __syncthreads();
+        mbar_wait(&img_bar, 0);
+    }
     float* xs = wcur;                          // [B][Kmax] stage input rows
     const int ncp_d = so[0].ncp;               // Wo and W2 share the column split (N = D)
     float* res = xs + size_t(B) * Kmax;        // [B][ncp_d] residual stream of this CTA's columns
@@ -509,6 +545,15 @@ size_t persist_smem_bytes(int L, int B, int D, int F, int H, int V, int max_chun
     (void)max_chunks;
     return sizeof(float) * (resident_floats(L, D, F, V, n_sms) + size_t(B) * Kmax +
                             pad4(size_t(B) * stage_ncp(D, n_sms)) + scratch_floats());
+}
+
+size_t persist_image_floats(int L, int D, int F, int V, int n_ctas) {
+    return size_t(n_ctas) * resident_floats(L, D, F, V, n_ctas);
+}
+
+cudaError_t launch_persist_image(const PersistArgs& a, int n_ctas, cudaStream_t s) {
+    persist_image_kernel<<<n_ctas, kPThreads, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s) {

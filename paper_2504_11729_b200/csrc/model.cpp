@@ -50,6 +50,8 @@ struct ep_model_s {
     DeviceBuffer weights;
     DeviceBuffer pe;      // sinusoid table [max_positions][d_model] fp64 (model.cpp:121-126)
     DeviceBuffer persist_layers, persist_scratch, persist_counters;  // K9 persistent rollout (fp32 models)
+    DeviceBuffer persist_image;  // K9 resident weight images (persist_image_ctas CTAs)
+    int persist_image_ctas = 0;
     DeviceBuffer arrive;  // fused-argmax arrival counter (zero between launches)
     std::vector<std::unique_ptr<DeviceBuffer>> kpages, vpages;
     // per-forward workspace
@@ -598,6 +600,14 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
         return b;
     }();
     pa.trace = trace;
+    if (m->persist_image_ctas != persist_ctas) {  // weight images, once per model and grid size
+        EP_CUDA_TRY(m->persist_image.reserve(persist_image_floats(m->L, m->D, m->F, m->V, persist_ctas) * sizeof(float)),
+                    "ep_model persist image");
+        pa.image_out = static_cast<float*>(m->persist_image.ptr);
+        EP_CUDA_TRY(launch_persist_image(pa, persist_ctas, s), "ep_model persist image");
+        m->persist_image_ctas = persist_ctas;
+    }
+    pa.image = static_cast<const float*>(m->persist_image.ptr);
     EP_CUDA_TRY(launch_decode_persist(pa, persist_ctas, s), "ep_model_generate persistent launch");
     if (trace) {  // debug: EP_TRACE=1 dumps the barrier timestamps to EP_TRACE_FILE
         std::vector<unsigned long long> hb(256);

@@ -116,10 +116,16 @@ struct PersistArgs {
     int32_t* counters;         // [2]: grid barrier arrivals, unembedding arrivals (zeroed per launch)
     int32_t* out;              // [n_steps][B] greedy tokens
     unsigned long long* trace; // debug: [8 steps][32] barrier timestamps of CTA 0 (may be null)
+    const float* image;        // every CTA's resident weight image (persist_image_floats, from launch_persist_image)
+    float* image_out;          // launch_persist_image: where to build it
 };
 // n_ctas = n_sms: one CTA per SM; weights stay resident in shared memory
 bool persist_supported(int L, int B, int D, int H, int F, int V, int P, int n_sms);
 size_t persist_smem_bytes(int L, int B, int D, int F, int H, int V, int max_chunks, int n_sms);
+// The resident weight images of n_ctas CTAs (layers / weights of a), built
+// once per model and grid size; the rollout kernel bulk-copies its slice.
+size_t persist_image_floats(int L, int D, int F, int V, int n_ctas);
+cudaError_t launch_persist_image(const PersistArgs& a, int n_ctas, cudaStream_t s);
 cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t s);
 
 
