@@ -320,3 +320,38 @@ def test_device_rollout_equals_decode_steps(cuda_handle, dtype, kv, persist, mon
             np.testing.assert_array_equal(a, b2)
         else:
             assert rel_err(a, b2) <= (1e-5 if kv == "f32" else 1e-2)
+
+
+def test_persistent_rollout_batch8_equals_graph_rollout(cuda_handle, monkeypatch):
+    """K9 at its largest batch (8 sessions with ragged edges sharing a cloud
+    prompt, EP_MODEL_PERSIST=1) = the CUDA-graph rollout, token for token;
+    the logits of a following decode_batch agree within fp32 rounding."""
+    M = _mod()
+    rng = O.SplitMix64(23)
+    cloud = [rng.next_u64() % 256 for _ in range(150)]
+    edges = [[rng.next_u64() % 256 for _ in range(n)] for n in (1, 5, 31, 32, 33, 64, 65, 120)]
+    n_steps = 40
+
+    def run(persist):
+        monkeypatch.setenv("EP_MODEL_PERSIST", persist)
+        m = make(CFG1, "f32", "f32", num_pages=96)
+        pf = M.prefill(m, cloud, M.ORIGIN_CLOUD, 0, M.SegmentedCache(m))
+        caches, firsts = [], []
+        for edge in edges:
+            c = M.SegmentedCache(m)
+            m.pages.retain(pf.segment.pages)
+            c.append(pf.segments)
+            e = M.prefill(m, edge, M.ORIGIN_EDGE, len(cloud), c)
+            c.append(e.segments)
+            caches.append(c)
+            firsts.append(e.next_token)
+        toks = M.generate_batch(m, caches, firsts, n_steps)
+        path = m.last_attention_path()
+        _, lg = M.decode_batch(m, caches, [t[-1] for t in toks], want_logits=True)
+        return toks, path, lg
+
+    t1, p1, l1 = run("1")
+    t0, p0, l0 = run("0")
+    assert (p1, p0) == ("persistent", "spliced")
+    assert t1 == t0
+    assert rel_err(l1, l0) <= 1e-5
