@@ -243,6 +243,45 @@ __device__ __forceinline__ void attn_task(const float* kt, const float* vt, cons
     for (int v = 0; v < VPL; ++v) part[2 + lane * VPL + v] = o[v];
 }
 
+// One warp: merge the n2 partials {max, sum, o[dh]} at part (row stride dh + 2)
+// into out[dh], online in chunks of 32 (attention.cpp:116-145); empty
+// partials (max = -inf) have weight 0 and are never multiplied.
+__device__ void merge_head(const float* part, int n2, int dh, float* out) {
+    const int lane = threadIdx.x & 31;
+    const int S = dh + 2, vpl = dh / 32;
+    float M = -INFINITY, Ls = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int c0 = 0; c0 < n2; c0 += 32) {
+        const int c = c0 + lane;
+        const float mv = c < n2 ? __ldcg(part + size_t(c) * S) : -INFINITY;
+        const float lv = c < n2 ? __ldcg(part + size_t(c) * S + 1) : 0.f;
+        const float Mb = fmaxf(M, warp_max(mv));
+        const float sc = M == -INFINITY ? 0.f : __expf(M - Mb);
+        Ls *= sc;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) o[r] *= sc;
+        const float w = mv == -INFINITY ? 0.f : __expf(mv - Mb);
+        Ls += warp_sum(w * lv);
+        const int cnt = min(32, n2 - c0);
+        for (int j0 = 0; j0 < cnt; j0 += 8) {
+            float v[8][4];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    v[j][r] = (j0 + j < cnt && r < vpl) ? __ldcg(part + size_t(c0 + j0 + j) * S + 2 + lane + 32 * r) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float wj = __shfl_sync(0xffffffffu, w, (j0 + j) & 31);
+                if (j0 + j < cnt && wj != 0.f)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) o[r] = fmaf(wj, v[j][r], o[r]);
+            }
+        }
+        M = Mb;
+    }
+    for (int r = 0; r < vpl; ++r) out[lane + 32 * r] = o[r] / Ls;
+}
+
 // The shared-memory layout of one CTA's resident weights from `base`: per
 // layer the Q|K|V, Wo, W1 (+ b1) and W2 (+ b2) column slices, then the
 // unembedding's; base is advanced past them.
@@ -290,6 +329,7 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
     const float scale = 1.f / sqrtf(float(dh));
     unsigned* bar = reinterpret_cast<unsigned*>(a.counters);
     unsigned* arrive = bar + 1;
+    int* bh_arrive = a.counters + 2;  // [B][H] attention tasks finished per (row, head)
 
     // ---- resident weights: this CTA's columns of every stage ----
     // a.image (built once per model by persist_image_kernel) holds every
@@ -317,6 +357,9 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
     float* s_att = res + pad4(size_t(B) * ncp_d);  // attention / reduction scratch
     float* red = s_att;                        // [8 warps][kMaxB][kMaxNcp]
     const int MC = 2 * a.max_chunks;            // partials per (row, head): 32-key halves
+    // batch > 1: the last task of each (row, head) merges it once (fewer L2
+    // reads than every CTA merging every row); batch 1: every CTA merges
+    const bool fuse_merge = B > 1;
     __syncthreads();
 
     unsigned n_bar = 0;
@@ -402,59 +445,81 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
                             part[1] = 0.f;
                         }
                         for (int e = lane; e < dh; e += 32) part[2 + e] = 0.f;
+                    } else {
+                        // q of (b, h) straight from L2 (written before the barrier)
+                        float* qs = s_att + warp * 128;
+                        for (int e = lane; e < dh; e += 32) qs[e] = __ldcg(a.q + size_t(b) * D + h * dh + e);
+                        __syncwarp();
+                        const size_t off = ((size_t(d.page) * H + h) * P + k0) * dh;
+                        if (dh == 64)
+                            attn_task<64>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
+                        else
+                            attn_task<32>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
+                    }
+                    if (!fuse_merge) {
+                        __syncwarp();
                         continue;
                     }
-                    // q of (b, h) straight from L2 (written before the barrier)
-                    float* qs = s_att + warp * 128;
-                    for (int e = lane; e < dh; e += 32) qs[e] = __ldcg(a.q + size_t(b) * D + h * dh + e);
+                    // the last of the (row, head)'s n2 tasks to finish merges them
+                    // (attention.cpp:116-145) into att[b][h dh, (h + 1) dh)
+                    __threadfence();
                     __syncwarp();
-                    const size_t off = ((size_t(d.page) * H + h) * P + k0) * dh;
-                    if (dh == 64)
-                        attn_task<64>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
-                    else
-                        attn_task<32>(Lw.kp + off, Lw.vp + off, qs, nk, scale, part);
+                    int last = 0;
+                    if (lane == 0) last = atomicAdd(&bh_arrive[b * H + h], 1) == n2 - 1;
+                    last = __shfl_sync(0xffffffffu, last, 0);
+                    if (last) {
+                        __threadfence();
+                        merge_head(a.part + size_t(b * H + h) * MC * (dh + 2), n2, dh, a.att + size_t(b) * D + h * dh);
+                        if (lane == 0) bh_arrive[b * H + h] = 0;
+                    }
                     __syncwarp();
                 }
             }
             sync(t);
 
-            // ---- LSE merge of the partials (every CTA, all rows) + Wo + residual ----
-            // a thread's (row, dimension): the maxima, sums and outputs of all
-            // of the row's partials are loaded in one L2 round trip and merged
-            // online (attention.cpp:116-145)
-            for (int i = tid; i < B * D; i += kPThreads) {
-                const int b = i / D, cc = i - b * D, h = cc / dh, e = cc - h * dh;
-                const int n2 = 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
-                const float* base = a.part + size_t(b * H + h) * MC * (dh + 2);
-                float o = 0.f, Ls = 0.f, M = -INFINITY;
-                for (int c0 = 0; c0 < n2; c0 += 32) {
-                    float mv[32], lv[32], ov[32];
+            // ---- merged attention rows + Wo + residual ----
+            if (fuse_merge) {
+                load_rows(a.att, B * D, xs);
+                __syncthreads();
+            } else {
+                // batch 1: every CTA merges the row itself — a thread's (row,
+                // dimension) loads the maxima, sums and outputs of all of the
+                // row's partials in one L2 round trip and merges them online
+                // (attention.cpp:116-145); cheaper than the last-arriver chain
+                for (int i = tid; i < B * D; i += kPThreads) {
+                    const int b = i / D, cc = i - b * D, h = cc / dh, e = cc - h * dh;
+                    const int n2 = 2 * int(a.req_page_off[b + 1] - a.req_page_off[b]);
+                    const float* base = a.part + size_t(b * H + h) * MC * (dh + 2);
+                    float o = 0.f, Ls = 0.f, M = -INFINITY;
+                    for (int c0 = 0; c0 < n2; c0 += 32) {
+                        float mv[32], lv[32], ov[32];
 #pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        const bool ok = c0 + u < n2;
-                        const float* pc = base + size_t(c0 + u) * (dh + 2);
-                        mv[u] = ok ? __ldcg(pc) : -INFINITY;
-                        lv[u] = ok ? __ldcg(pc + 1) : 0.f;
-                        ov[u] = ok ? __ldcg(pc + 2 + e) : 0.f;
+                        for (int u = 0; u < 32; ++u) {
+                            const bool ok = c0 + u < n2;
+                            const float* pc = base + size_t(c0 + u) * (dh + 2);
+                            mv[u] = ok ? __ldcg(pc) : -INFINITY;
+                            lv[u] = ok ? __ldcg(pc + 1) : 0.f;
+                            ov[u] = ok ? __ldcg(pc + 2 + e) : 0.f;
+                        }
+                        float Mb = M;
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) Mb = fmaxf(Mb, mv[u]);
+                        const float sc = M == -INFINITY ? 0.f : __expf(M - Mb);
+                        o *= sc;
+                        Ls *= sc;
+#pragma unroll
+                        for (int u = 0; u < 32; ++u) {
+                            if (mv[u] == -INFINITY) continue;  // empty partial: never touch its output
+                            const float wgt = __expf(mv[u] - Mb);
+                            Ls = fmaf(wgt, lv[u], Ls);
+                            o = fmaf(wgt, ov[u], o);
+                        }
+                        M = Mb;
                     }
-                    float Mb = M;
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) Mb = fmaxf(Mb, mv[u]);
-                    const float sc = M == -INFINITY ? 0.f : __expf(M - Mb);
-                    o *= sc;
-                    Ls *= sc;
-#pragma unroll
-                    for (int u = 0; u < 32; ++u) {
-                        if (mv[u] == -INFINITY) continue;  // empty partial: never touch its output
-                        const float wgt = __expf(mv[u] - Mb);
-                        Ls = fmaf(wgt, lv[u], Ls);
-                        o = fmaf(wgt, ov[u], o);
-                    }
-                    M = Mb;
+                    xs[i] = o / Ls;
                 }
-                xs[i] = o / Ls;
+                __syncthreads();
             }
-            __syncthreads();
             gemv_cols(xs, so[l].ws, B, D, so[l].ncp, so[l].c0, so[l].nc, red, [&](int b, int c, float v) {
                 float& r = res[b * ncp_d + (c - so[l].c0)];
                 r = r + v;  // model.cpp:184-185
@@ -560,7 +625,7 @@ cudaError_t launch_decode_persist(const PersistArgs& a, int n_ctas, cudaStream_t
     const size_t smem = persist_smem_bytes(a.L, a.B, a.D, a.F, a.H, a.V, a.max_chunks, n_ctas);
     if (smem > 48 * 1024)
         if (cudaError_t e = ensure_smem<decode_persist_kernel>(int(smem))) return e;
-    if (cudaError_t e = cudaMemsetAsync(a.counters, 0, 2 * sizeof(int32_t), s)) return e;
+    if (cudaError_t e = cudaMemsetAsync(a.counters, 0, size_t(2 + a.B * a.H) * sizeof(int32_t), s)) return e;
     void* args[] = {const_cast<PersistArgs*>(&a)};
     return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(decode_persist_kernel), dim3(n_ctas),
                                        dim3(kPThreads), args, smem, s);

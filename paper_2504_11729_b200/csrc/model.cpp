@@ -519,12 +519,12 @@ int ep_model_weight(ep_model m, const char* name, int32_t layer, void** ptr, siz
 int ep_model_last_attention_path(ep_model m) { return m ? m->last_path : 0; }
 
 // K9: whether decode rows of this batch run in the persistent cooperative
-// kernel — a single-session decode of a small fp32 model by default (config
-// 1: 45 vs 64 us / token for the CUDA-graph rollout; slower from batch 8 on).
-// EP_MODEL_PERSIST=0 disables it, =1 forces it for every supported batch.
+// kernel — every decode of up to 8 sessions of a small fp32 model (config 1
+// rollout: 47 / 55 / 64 us per step at batch 1 / 4 / 8 vs 64 / 64 / 70 on the
+// CUDA-graph path). EP_MODEL_PERSIST=0 keeps the layer-by-layer path.
 bool use_persist(ep_model m, int batch, int* n_ctas) {
     const char* e = std::getenv("EP_MODEL_PERSIST");
-    if (!(e ? e[0] == '1' : batch == 1)) return false;
+    if (e && e[0] == '0') return false;
     if (m->dt != EP_F32 || m->kv_dtype != EP_F32) return false;
     int c = m->h->n_sms;  // one CTA per SM (EP_PERSIST_CTAS: fewer)
     if (const char* ec = std::getenv("EP_PERSIST_CTAS")) c = std::max(1, std::min(m->h->n_sms, std::atoi(ec)));
@@ -558,9 +558,9 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
     const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
     const size_t part = B * m->H * size_t(2 * max_chunks) * (m->dh + 2);  // 32-key halves
-    const size_t floats = 3 * B * D + B * F + B * V + part;
+    const size_t floats = 4 * B * D + B * F + B * V + part;
     EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
-    EP_CUDA_TRY(m->persist_counters.reserve(2 * sizeof(int32_t)), "ep_model_generate counters");
+    EP_CUDA_TRY(m->persist_counters.reserve((2 + B * m->H) * sizeof(int32_t)), "ep_model_generate counters");
     float* f0 = static_cast<float*>(m->persist_scratch.ptr);
     PersistArgs pa{};
     pa.layers = static_cast<const PersistLayer*>(m->persist_layers.ptr);
@@ -590,6 +590,7 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     float* logits_ws = pa.h1 + B * F;
     pa.logits = logits_out ? static_cast<float*>(logits_out) : logits_ws;
     pa.part = logits_ws + B * V;
+    pa.att = pa.part + part;
     pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
     pa.out = out;
     static unsigned long long* trace = [] {

@@ -112,8 +112,8 @@ struct PersistArgs {
     const int32_t* dst_slot;   // [n_steps][B]
     const PageDesc* pdesc;     // every request's pages (final table)
     const int64_t* req_page_off;
-    float *x, *x2, *q, *h1, *logits, *part;  // scratch
-    int32_t* counters;         // [2]: grid barrier arrivals, unembedding arrivals (zeroed per launch)
+    float *x, *x2, *q, *h1, *logits, *part, *att;  // scratch (att: merged attention rows [B][D])
+    int32_t* counters;         // [2 + B H]: grid barrier, unembedding, per-(row, head) attention arrivals (zeroed per launch)
     int32_t* out;              // [n_steps][B] greedy tokens
     unsigned long long* trace; // debug: [8 steps][32] barrier timestamps of CTA 0 (may be null)
     const float* image;        // every CTA's resident weight image (persist_image_floats, from launch_persist_image)
