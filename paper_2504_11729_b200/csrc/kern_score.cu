@@ -60,10 +60,6 @@ __device__ __forceinline__ uint64_t order_key(float z, uint32_t idx) {
 template <typename T>
 __device__ __forceinline__ float ldf(const T* p);
 template <>
-__device__ __forceinline__ float ldf<float>(const float* p) {
-    return *p;
-}
-template <>
 __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
     return __bfloat162float(*p);
 }

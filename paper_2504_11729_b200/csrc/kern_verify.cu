@@ -55,7 +55,6 @@ constexpr int kThreads = 384;
 constexpr int kMaxRows = 128;     // valid query rows per tile (one M = 128 MMA tile)
 constexpr float kLazy = 8.0f;     // log2 headroom before the max is moved
 
-constexpr int kQHalf = kM * 128;           // 16 KB: 128 rows x 64 bf16
 constexpr int kKVHalf = kBT * 128;         // 8 KB: 64 rows x 64 bf16
 constexpr int kBlkBytes = 2 * kKVHalf;     // one K (or V) block: two 64-column halves
 constexpr int OFF_STAGE = 0;
@@ -118,10 +117,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
-}
-
-__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-    return row * 128 + ((chunk ^ (row & 7)) << 4);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
