@@ -558,7 +558,12 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     for (const Req& r : reqs) max_chunks = std::max<int>(max_chunks, int(r.pages.size()));
     const size_t B = size_t(batch), D = size_t(m->D), F = size_t(m->F), V = size_t(m->V);
     const size_t part = B * m->H * size_t(2 * max_chunks) * (m->dh + 2);  // 32-key halves
-    const size_t floats = 4 * B * D + B * F + B * V + part;
+    // scratch blocks x | x2 | q | h1 | logits | part | att, each 256-byte
+    // aligned (the kernel reads rows with 16-byte loads)
+    auto al = [](size_t n) { return (n + 63) & ~size_t(63); };
+    const size_t o_x2 = al(B * D), o_q = o_x2 + al(B * D), o_h1 = o_q + al(B * D), o_lg = o_h1 + al(B * F),
+                 o_part = o_lg + al(B * V), o_att = o_part + al(part);
+    const size_t floats = o_att + al(B * D);
     EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
     EP_CUDA_TRY(m->persist_counters.reserve((2 + B * m->H) * sizeof(int32_t)), "ep_model_generate counters");
     float* f0 = static_cast<float*>(m->persist_scratch.ptr);
@@ -584,13 +589,12 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     pa.pdesc = ps.pdesc;
     pa.req_page_off = ps.req_page_off;
     pa.x = f0;
-    pa.x2 = f0 + B * D;
-    pa.q = f0 + 2 * B * D;
-    pa.h1 = f0 + 3 * B * D;
-    float* logits_ws = pa.h1 + B * F;
-    pa.logits = logits_out ? static_cast<float*>(logits_out) : logits_ws;
-    pa.part = logits_ws + B * V;
-    pa.att = pa.part + part;
+    pa.x2 = f0 + o_x2;
+    pa.q = f0 + o_q;
+    pa.h1 = f0 + o_h1;
+    pa.logits = logits_out ? static_cast<float*>(logits_out) : f0 + o_lg;
+    pa.part = f0 + o_part;
+    pa.att = f0 + o_att;
     pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
     pa.out = out;
     static unsigned long long* trace = [] {

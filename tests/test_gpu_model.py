@@ -355,3 +355,40 @@ def test_persistent_rollout_batch8_equals_graph_rollout(cuda_handle, monkeypatch
     assert (p1, p0) == ("persistent", "spliced")
     assert t1 == t0
     assert rel_err(l1, l0) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", [(3, 8, 256, 300, 1024, 7),   # d_head 32, vocab not a multiple of 32
+                                 (1, 2, 128, 250, 1024, 9)])  # d_head 64, one layer
+def test_persistent_rollout_other_shapes(cuda_handle, cfg, monkeypatch):
+    """K9 on shapes other than config 1 (the d_head 32 attention task, ragged
+    column splits) = the layer-by-layer path: same greedy tokens, logits
+    within fp32 rounding."""
+    M = _mod()
+    rng = O.SplitMix64(31)
+    V = cfg[3]
+    cloud = [rng.next_u64() % V for _ in range(70)]
+    edges = [[rng.next_u64() % V for _ in range(n)] for n in (2, 40, 95)]
+
+    def run(persist):
+        monkeypatch.setenv("EP_MODEL_PERSIST", persist)
+        m = make(cfg, "f32", "f32", num_pages=48)
+        pf = M.prefill(m, cloud, M.ORIGIN_CLOUD, 0, M.SegmentedCache(m))
+        caches, firsts = [], []
+        for edge in edges:
+            c = M.SegmentedCache(m)
+            m.pages.retain(pf.segment.pages)
+            c.append(pf.segments)
+            e = M.prefill(m, edge, M.ORIGIN_EDGE, len(cloud), c)
+            c.append(e.segments)
+            caches.append(c)
+            firsts.append(e.next_token)
+        toks = M.generate_batch(m, caches, firsts, 24)
+        path = m.last_attention_path()
+        _, lg = M.decode_batch(m, caches, [t[-1] for t in toks], want_logits=True)
+        return toks, path, lg
+
+    t1, p1, l1 = run("1")
+    t0, p0, l0 = run("0")
+    assert p1 == "persistent" and p0 != "persistent"
+    assert t1 == t0
+    assert rel_err(l1, l0) <= 1e-5
