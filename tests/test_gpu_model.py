@@ -357,21 +357,22 @@ def test_persistent_rollout_batch8_equals_graph_rollout(cuda_handle, monkeypatch
     assert rel_err(l1, l0) <= 1e-5
 
 
-@pytest.mark.parametrize("cfg", [(3, 8, 256, 300, 1024, 7),   # d_head 32, vocab not a multiple of 32
-                                 (1, 2, 128, 250, 1024, 9)])  # d_head 64, one layer
-def test_persistent_rollout_other_shapes(cuda_handle, cfg, monkeypatch):
+@pytest.mark.parametrize("cfg,n_cloud", [((3, 8, 256, 300, 1024, 7), 70),     # d_head 32, vocab not a multiple of 32
+                                         ((1, 2, 128, 250, 1024, 9), 70),     # d_head 64, one layer
+                                         ((2, 2, 128, 256, 4096, 5), 2200)])  # > 32 partials per (row, head)
+def test_persistent_rollout_other_shapes(cuda_handle, cfg, n_cloud, monkeypatch):
     """K9 on shapes other than config 1 (the d_head 32 attention task, ragged
-    column splits) = the layer-by-layer path: same greedy tokens, logits
-    within fp32 rounding."""
+    column splits, more than 32 key halves per row) = the layer-by-layer
+    path: same greedy tokens, logits within fp32 rounding."""
     M = _mod()
     rng = O.SplitMix64(31)
     V = cfg[3]
-    cloud = [rng.next_u64() % V for _ in range(70)]
+    cloud = [rng.next_u64() % V for _ in range(n_cloud)]
     edges = [[rng.next_u64() % V for _ in range(n)] for n in (2, 40, 95)]
 
     def run(persist):
         monkeypatch.setenv("EP_MODEL_PERSIST", persist)
-        m = make(cfg, "f32", "f32", num_pages=48)
+        m = make(cfg, "f32", "f32", num_pages=96)
         pf = M.prefill(m, cloud, M.ORIGIN_CLOUD, 0, M.SegmentedCache(m))
         caches, firsts = [], []
         for edge in edges:
@@ -385,10 +386,12 @@ def test_persistent_rollout_other_shapes(cuda_handle, cfg, monkeypatch):
         toks = M.generate_batch(m, caches, firsts, 24)
         path = m.last_attention_path()
         _, lg = M.decode_batch(m, caches, [t[-1] for t in toks], want_logits=True)
-        return toks, path, lg
+        one = M.decode_step(m, caches[2], 1)  # batch 1: every CTA merges the row itself
+        return toks, path, lg, one
 
-    t1, p1, l1 = run("1")
-    t0, p0, l0 = run("0")
+    t1, p1, l1, o1 = run("1")
+    t0, p0, l0, o0 = run("0")
     assert p1 == "persistent" and p0 != "persistent"
     assert t1 == t0
     assert rel_err(l1, l0) <= 1e-5
+    assert o1.next_token == o0.next_token and rel_err(o1.logits, o0.logits) <= 1e-5
