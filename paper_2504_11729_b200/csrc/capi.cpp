@@ -335,7 +335,7 @@ int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_
     v->vocab = vocab;
     v->w_t = w_score_t;
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_verifier_create");
-    if (int rc = encode_bf16_2d(&v->tmap_w, w_score_t, uint64_t(width), uint64_t(vocab), 64, 256)) return rc;
+    if (int rc = encode_bf16_2d(&v->tmap_w, w_score_t, uint64_t(width), uint64_t(vocab), 64, kScoreTileN)) return rc;
     EP_CUDA_TRY(v->colsum.reserve(size_t(vocab) * sizeof(float)), "ep_verifier_create colsum");
     EP_CUDA_TRY(v->wmax2.reserve(sizeof(float)), "ep_verifier_create colnorm");
     EP_CUDA_TRY(launch_colsum(w_score_t, width, vocab, static_cast<float*>(v->colsum.ptr),
@@ -374,8 +374,8 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         // the bf16 hi part of the rows is the GEMM's A operand
         EP_CUDA_TRY(v->split.reserve(size_t(rows) * v->width * 2), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->ebound.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
-        const size_t slots = size_t(v->vocab) / 256 * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
-        EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * (v->vocab / 256) * sizeof(int32_t)), "ep_verify_greedy ws");
+        const size_t slots = size_t(v->vocab) / kScoreTileN * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
+        EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * (v->vocab / kScoreTileN) * sizeof(int32_t)), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->cand_n.reserve(size_t(rows) * slots * sizeof(int32_t)), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->cand_z.reserve(size_t(rows) * slots * sizeof(float)), "ep_verify_greedy ws");
         split = v->split.ptr;

@@ -9,7 +9,7 @@
 //
 // B200 mapping:
 //   * row_stats: mean and 1/std of each attention-output row (4096 wide).
-//   * score GEMM on tcgen05: Z[128 rows x 256 vocab] (TMEM fp32) over K = 4096
+//   * score GEMM on tcgen05: Z[128 rows x 128 vocab] (TMEM fp32) over K = 4096
 //     in 64-wide TMA-fed stages (A = attention rows, B = W^T, both bf16,
 //     128B-swizzled K-major). LayerNorm is folded into the epilogue:
 //     LN(x).w = rstd * (x.w - mean * colsum(w)); rstd > 0 does not move the
@@ -42,10 +42,10 @@
 namespace ep {
 namespace {
 
-constexpr int kTM = 128, kTN = 256, kTK = 64;
-constexpr int kStagesS = 4;
+constexpr int kTM = 128, kTN = kScoreTileN, kTK = 64;
+constexpr int kStagesS = 3;  // 3 x 32 KB: two CTAs per SM (config 3 at k = 8 has 160 tiles)
 constexpr int kABytes = kTM * kTK * 2;  // 16 KB
-constexpr int kBBytes = kTN * kTK * 2;  // 32 KB
+constexpr int kBBytes = kTN * kTK * 2;  // 16 KB
 constexpr int kStage = kABytes + kBBytes;
 constexpr int kScoreThreads = 192;  // warps 0-3 epilogue, 4 TMA, 5 MMA
 constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256 + kTN * 4 + 24 * 128 * 5;  // stages, barriers, colsum slice, stash
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         mbar_init(acc_full, 1);
         fence_mbar_init();
     }
-    if (warp == 5) umma::tmem_alloc(tmem_slot, 256);
+    if (warp == 5) umma::tmem_alloc(tmem_slot, kTN);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             umma::mma_commit(acc_full);
         }
     } else {
-        // epilogue: thread = row (TMEM lane), 256 vocab columns. The tile's
+        // epilogue: thread = row (TMEM lane), kTN vocab columns. The tile's
         // colsum slice and the row's mean are fetched while the MMAs run; TMEM
         // is read 64 columns per wait.
         const int row = warp * 32 + lane;
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
     __syncthreads();
     if (warp == 5) {
         umma::fence_after_sync();
-        umma::tmem_dealloc(tmem, 256);
+        umma::tmem_dealloc(tmem, kTN);
     }
     if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 3] = gtimer();
 }
@@ -404,7 +404,7 @@ __device__ __forceinline__ float key_value(unsigned long long k) {
 }
 
 constexpr int kRefineThreads = 256;
-constexpr int kMaxList = 512;  // candidate list of one row (n_tiles * kPerTile)
+constexpr int kMaxList = 1024;  // candidate list of one row (n_tiles * kPerTile)
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
