@@ -444,6 +444,7 @@ __global__ void __launch_bounds__(kRefineThreads)
     const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     extern __shared__ float4 s_x4[];  // [width / 4]
     __shared__ int s_list[kMaxList];
+    __shared__ int s_cnt[kRefineThreads];
     __shared__ int s_n;
     __shared__ bool s_all;
     __shared__ unsigned long long s_top;
@@ -461,15 +462,22 @@ __global__ void __launch_bounds__(kRefineThreads)
         s_top = 0ull;
     }
     __syncthreads();
-    if (tid < n_tiles && cand_cnt[size_t(row) * n_tiles + tid] > kPerTile) s_all = true;
+    if (tid < n_tiles && tid < kRefineThreads) {
+        const int c = cand_cnt[size_t(row) * n_tiles + tid];
+        s_cnt[tid] = c;
+        if (c > kPerTile) s_all = true;
+    }
     const float thresh = key_value(best[row]) - 2.f * ebound[row];
     __syncthreads();
-    if (!s_all) {
-        for (int sl = tid; sl < n_tiles * kPerTile; sl += kRefineThreads) {
-            const int t = sl / kPerTile, i = sl % kPerTile;
-            const size_t b = (size_t(row) * n_tiles + t) * kPerTile + i;
-            if (i < cand_cnt[size_t(row) * n_tiles + t] && cand_z[b] >= thresh)
-                s_list[atomicAdd(&s_n, 1)] = cand_n[b];
+    if (!s_all && tid < n_tiles) {
+        // the thread that read tile tid's count gathers its slots: value and
+        // index in one round trip
+        const int c = s_cnt[tid];
+        const size_t b0 = (size_t(row) * n_tiles + tid) * kPerTile;
+        for (int i = 0; i < c; ++i) {
+            const float z = cand_z[b0 + i];
+            const int n = cand_n[b0 + i];
+            if (z >= thresh) s_list[atomicAdd(&s_n, 1)] = n;
         }
     }
     __syncthreads();
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kRefineThreads)
         const int n = all ? i : s_list[i];
         const uint2* wr = reinterpret_cast<const uint2*>(wt + size_t(n) * width);
         float acc = 0.f;
-#pragma unroll 8
+#pragma unroll 16
         for (int c = lane; c < width / 4; c += 32) {
             const float4 xv = s_x4[c];
             const uint2 w = wr[c];
