@@ -127,10 +127,11 @@ class Model:
             lib().ep_model_last_attention_path(self._m), "none")
 
     def forward(self, tables, n_new, tokens, *, want_logits=True, want_hidden=False,
-                stream=None):
+                stream=None, out=None):
         """ep_model_forward over a batch of splice tables (one per request):
         the last n_new[b] tokens of request b are new. Returns (next token ids
-        [B] int32 cuda tensor, logits [B][V] or None, hidden or None)."""
+        [B] int32 cuda tensor, logits [B][V] or None, hidden or None).
+        out: optional (next, logits) device tensors to write into."""
         torch = _torch()
         B = len(tables)
         indptr, segs, pt = _batch_arrays(tables)
@@ -139,9 +140,12 @@ class Model:
         if tok.size != int(nn.sum()):
             raise InvalidArgument("forward: len(tokens) != sum(n_new)")
         dev = f"cuda:{self.device}"
-        nxt = torch.empty(B, dtype=torch.int32, device=dev)
-        logits = (torch.empty((B, self.config.vocab_size), dtype=self.tdtype, device=dev)
-                  if want_logits else None)
+        if out is not None:
+            nxt, logits = out
+        else:
+            nxt = torch.empty(B, dtype=torch.int32, device=dev)
+            logits = (torch.empty((B, self.config.vocab_size), dtype=self.tdtype, device=dev)
+                      if want_logits else None)
         hidden = (torch.empty((int(nn.sum()), self.config.d_model), dtype=self.tdtype,
                               device=dev) if want_hidden else None)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -356,13 +360,23 @@ def decode_batch(model: Model, caches, last_tokens, *, want_logits: bool = False
     _check_tokens(model, last_tokens)
     for c in caches:
         c._grow_generated(1)
+    out, buf = None, None
+    if want_logits and model.tdtype == _torch().float32:
+        # logits and next ids in one device buffer: one device->host copy
+        torch = _torch()
+        B, V = len(caches), model.config.vocab_size
+        buf = torch.empty(B * V + B, dtype=torch.float32, device=f"cuda:{model.device}")
+        out = (buf[B * V:].view(torch.int32), buf[:B * V].view(B, V))
     try:
         nxt, logits, _ = model.forward([c.segments for c in caches], [1] * len(caches),
-                                       list(last_tokens), want_logits=want_logits)
+                                       list(last_tokens), want_logits=want_logits, out=out)
     except Exception:
         for c in caches:
             c._shrink_generated(1)
         raise
+    if buf is not None:
+        host = buf.cpu().numpy()
+        return host[B * V:].view(np.int32).copy(), host[:B * V].reshape(B, V)
     return nxt.cpu().numpy(), (logits.cpu().numpy() if logits is not None else None)
 
 
