@@ -41,6 +41,14 @@ constexpr int kMaxB = 8;
 constexpr int kMaxNcp = 32;    // output columns of one stage per CTA (power of two)
 constexpr float kEps = 1e-5f;  // model.cpp:14
 
+// Order-preserving 64-bit key of (logit, id): larger logit first, then the
+// lower id (argmax_token's strict '>' keeps the first maximum).
+__device__ __forceinline__ unsigned long long order_key(float z, uint32_t idx) {
+    uint32_t b = __float_as_uint(z);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (uint64_t(b) << 32) | uint64_t(0xFFFFFFFFu - idx);
+}
+
 __host__ __device__ inline int pow2ceil(int v) {
     int p = 1;
     while (p < v) p <<= 1;
@@ -328,7 +336,6 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const float scale = 1.f / sqrtf(float(dh));
     unsigned* bar = reinterpret_cast<unsigned*>(a.counters);
-    unsigned* arrive = bar + 1;
     int* bh_arrive = a.counters + 2;  // [B][H] attention tasks finished per (row, head)
 
     // ---- resident weights: this CTA's columns of every stage ----
@@ -360,6 +367,30 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
     // batch > 1: the last task of each (row, head) merges it once (fewer L2
     // reads than every CTA merging every row); batch 1: every CTA merges
     const bool fuse_merge = B > 1;
+    __shared__ unsigned long long s_key[kMaxB];
+    __shared__ int tok_s[kMaxB];
+    // argmax_token (model.cpp:248-255) of step s: the maximum over every
+    // CTA's candidate key (first maximum: ties go to the lowest id) -> tok_s;
+    // CTA 0 also writes it to out[s]
+    auto next_tokens = [&](int s) {
+        for (int b = warp; b < B; b += kPWarps) {
+            unsigned long long k = 0ull;
+            for (int g = lane; g < int(gridDim.x); g += 32) {
+                const unsigned long long o = __ldcg(a.keys + size_t(g) * B + b);
+                k = o > k ? o : k;
+            }
+#pragma unroll
+            for (int m = 16; m > 0; m >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, k, m);
+                k = o > k ? o : k;
+            }
+            if (lane == 0) {
+                const int tok = k ? int(0xFFFFFFFFu - uint32_t(k & 0xFFFFFFFFull)) : 0;
+                tok_s[b] = tok;
+                if (blockIdx.x == 0) a.out[size_t(s) * B + b] = tok;
+            }
+        }
+    };
     __syncthreads();
 
     unsigned n_bar = 0;
@@ -388,9 +419,15 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
             if (l == 0) {
                 // model.cpp:104-129 with the fp64 sinusoid table; CTA 0 stores
                 // the embedded rows (the residual input)
+                if (t == 0) {
+                    if (tid < B) tok_s[tid] = a.first[tid];
+                } else {
+                    next_tokens(t - 1);
+                }
+                __syncthreads();
                 for (int i = tid; i < B * D; i += kPThreads) {
                     const int b = i / D, c = i - b * D;
-                    const int tok = t == 0 ? a.first[b] : __ldcg(a.out + size_t(t - 1) * B + b);
+                    const int tok = tok_s[b];
                     const int pos = a.pos[size_t(t) * B + b];
                     const float v = float(double(a.emb[size_t(tok) * D + c]) + a.pe[size_t(pos) * D + c]);
                     xs[i] = v;
@@ -550,48 +587,22 @@ __global__ void __launch_bounds__(kPThreads, 1) decode_persist_kernel(const Pers
             sync(t);
         }
 
-        // ---- unembed_logits (model.cpp:238-246) ----
+        // ---- unembed_logits (model.cpp:238-246) + this CTA's argmax candidates ----
+        if (tid < B) s_key[tid] = 0ull;
         load_rows(a.x, B * D, xs);
         __syncthreads();
         ln_smem(xs, B, D);
         __syncthreads();
-        gemv_cols(xs, su.ws, B, D, su.ncp, su.c0, su.nc, red,
-                  [&](int b, int c, float v) { a.logits[size_t(b) * V + c] = v; });
-
-        // ---- argmax_token (model.cpp:248-255) by the last CTA to finish ----
-        __shared__ int s_last;
-        if (tid == 0) {
-            __threadfence();
-            s_last = atomicAdd(arrive, 1u) == gridDim.x - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            for (int b = warp; b < B; b += kPWarps) {
-                float bv = 0.f;
-                int bi = V;
-                for (int c = lane; c < V; c += 32) {
-                    const float v = __ldcg(a.logits + size_t(b) * V + c);
-                    if (bi == V || v > bv) {
-                        bv = v;
-                        bi = c;
-                    }
-                }
-#pragma unroll
-                for (int msk = 16; msk > 0; msk >>= 1) {
-                    const float ov = __shfl_xor_sync(0xffffffffu, bv, msk);
-                    const int oi = __shfl_xor_sync(0xffffffffu, bi, msk);
-                    if (oi < V && (bi == V || ov > bv || (ov == bv && oi < bi))) {
-                        bv = ov;
-                        bi = oi;
-                    }
-                }
-                if (lane == 0) a.out[size_t(t) * B + b] = bi == V ? 0 : bi;
-            }
-            if (tid == 0) *arrive = 0;
-        }
+        gemv_cols(xs, su.ws, B, D, su.ncp, su.c0, su.nc, red, [&](int b, int c, float v) {
+            a.logits[size_t(b) * V + c] = v;
+            atomicMax(&s_key[b], order_key(v, uint32_t(c)));
+        });
+        // the first maximum of each row among this CTA's columns; the next
+        // step (or the end of the rollout) reduces the candidates of all CTAs
+        if (tid < B) a.keys[size_t(blockIdx.x) * B + tid] = s_key[tid];
         sync(t);
     }
+    if (blockIdx.x == 0) next_tokens(a.n_steps - 1);
 }
 
 }  // namespace

@@ -563,7 +563,8 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     auto al = [](size_t n) { return (n + 63) & ~size_t(63); };
     const size_t o_x2 = al(B * D), o_q = o_x2 + al(B * D), o_h1 = o_q + al(B * D), o_lg = o_h1 + al(B * F),
                  o_part = o_lg + al(B * V), o_att = o_part + al(part);
-    const size_t floats = o_att + al(B * D);
+    const size_t o_keys = o_att + al(B * D);
+    const size_t floats = o_keys + al(2 * B * size_t(persist_ctas));
     EP_CUDA_TRY(m->persist_scratch.reserve(floats * sizeof(float)), "ep_model_generate scratch");
     EP_CUDA_TRY(m->persist_counters.reserve((2 + B * m->H) * sizeof(int32_t)), "ep_model_generate counters");
     float* f0 = static_cast<float*>(m->persist_scratch.ptr);
@@ -595,6 +596,7 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     pa.logits = logits_out ? static_cast<float*>(logits_out) : f0 + o_lg;
     pa.part = f0 + o_part;
     pa.att = f0 + o_att;
+    pa.keys = reinterpret_cast<unsigned long long*>(f0 + o_keys);
     pa.counters = static_cast<int32_t*>(m->persist_counters.ptr);
     pa.out = out;
     static unsigned long long* trace = [] {

@@ -113,6 +113,7 @@ struct PersistArgs {
     const PageDesc* pdesc;     // every request's pages (final table)
     const int64_t* req_page_off;
     float *x, *x2, *q, *h1, *logits, *part, *att;  // scratch (att: merged attention rows [B][D])
+    unsigned long long* keys;  // [n_ctas][B] per-CTA argmax candidates of the last unembedding
     int32_t* counters;         // [2 + B H]: grid barrier, unembedding, per-(row, head) attention arrivals (zeroed per launch)
     int32_t* out;              // [n_steps][B] greedy tokens
     unsigned long long* trace; // debug: [8 steps][32] barrier timestamps of CTA 0 (may be null)
