@@ -79,6 +79,60 @@ __global__ void __launch_bounds__(256) kv_ingest_kernel(const uint8_t* __restric
     }
 }
 
+// d_head % 4 == 0: one CTA per frame row (token t of K or of V; the V rows
+// follow the K rows, so row r of 2*seq is contiguous at r * H*d values) and
+// one thread per 4-value quad of it (32 wire bytes -> one 8-byte bf16 / 16-byte
+// fp32 store). Page and slot are row-uniform; the head split is one division
+// per quad. MIS8: the payload starts 8 bytes past a 16-byte boundary (it is at
+// frame+24, so a 256-aligned device frame lands here): every lane reads the
+// two aligned double2 (v[4j-1], v[4j]) and (v[4j+1], v[4j+2]) and takes v[4j+3]
+// from the next lane's first load; the last lane of the warp, or of the row,
+// reads it itself. Loops are warp-uniform so the full-mask shuffle is valid.
+template <bool BF16, bool MIS8>
+__global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __restrict__ src, uint32_t rows,
+                                                             uint32_t seq, uint32_t row_quads, uint32_t d_quads,
+                                                             uint32_t P, uint32_t H,
+                                                             const int32_t* __restrict__ page_table,
+                                                             void* __restrict__ kp, void* __restrict__ vp) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t span = (row_quads + 31) & ~31u;
+    for (uint32_t row = blockIdx.x; row < rows; row += gridDim.x) {
+        const bool is_v = row >= seq;
+        const uint32_t t = is_v ? row - seq : row;
+        const size_t page = size_t(page_table[t / P]), slot = t % P;
+        const uint8_t* rp = src + size_t(row) * row_quads * 32;
+        for (uint32_t j0 = threadIdx.x & ~31u; j0 < span; j0 += blockDim.x) {
+            const uint32_t j = j0 + lane;
+            const bool live = j < row_quads;
+            double v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+            if (MIS8) {
+                const double2* a = reinterpret_cast<const double2*>(rp + size_t(j) * 32 - 8);
+                double2 lo = make_double2(0, 0), hi = make_double2(0, 0);
+                if (live) { lo = __ldg(a); hi = __ldg(a + 1); }
+                double nx = __shfl_down_sync(0xffffffffu, lo.x, 1);
+                if (live && (lane == 31 || j + 1 >= row_quads))
+                    nx = __ldg(reinterpret_cast<const double*>(rp + size_t(j) * 32 + 24));
+                v0 = lo.y; v1 = hi.x; v2 = hi.y; v3 = nx;
+            } else if (live) {
+                const double2* a = reinterpret_cast<const double2*>(rp + size_t(j) * 32);
+                const double2 lo = __ldg(a), hi = __ldg(a + 1);
+                v0 = lo.x; v1 = lo.y; v2 = hi.x; v3 = hi.y;
+            }
+            if (!live) continue;
+            const uint32_t h = j / d_quads, cq = j - h * d_quads;
+            const size_t dst = ((page * H + h) * P + slot) * d_quads + cq;  // in quads
+            if (BF16) {
+                const uint2 w = make_uint2(uint32_t(f64_to_bf16(v0)) | (uint32_t(f64_to_bf16(v1)) << 16),
+                                           uint32_t(f64_to_bf16(v2)) | (uint32_t(f64_to_bf16(v3)) << 16));
+                static_cast<uint2*>(is_v ? vp : kp)[dst] = w;
+            } else {
+                static_cast<float4*>(is_v ? vp : kp)[dst] = make_float4(
+                    __double2float_rn(v0), __double2float_rn(v1), __double2float_rn(v2), __double2float_rn(v3));
+            }
+        }
+    }
+}
+
 uint32_t rd_u32(const uint8_t* b) {
     return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
 }
@@ -182,7 +236,29 @@ extern "C" int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const voi
     }
     const uint32_t n_pairs = uint32_t(vals / 2), d_pairs = uint32_t(f.d_head / 2);
     const uint32_t row_pairs = uint32_t(f.n_heads) * d_pairs;
-    const bool a16 = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(src) & 15;
+    const bool pool_al = (reinterpret_cast<uintptr_t>(pool->k_pages) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(pool->v_pages) & 15) == 0;
+    if (f.d_head % 4 == 0 && (mis == 0 || mis == 8) && pool_al) {
+        const uint32_t rows = 2 * f.seq_len, d_quads = uint32_t(f.d_head / 4);
+        const uint32_t row_quads = uint32_t(f.n_heads) * d_quads;
+        const uint32_t tpb = row_quads >= 256 ? 256 : ((row_quads + 31) & ~31u);
+        const uint32_t grid = std::min<uint32_t>(rows, uint32_t(h->n_sms) * (2048 / tpb));
+        const uint32_t P = uint32_t(pool->page_tokens), H = uint32_t(f.n_heads);
+#define EP_INGEST_ROWS(BF, M8)                                                                                \
+    ep::kv_ingest_rows_kernel<BF, M8><<<grid, tpb, 0, s>>>(src, rows, f.seq_len, row_quads, d_quads, P, H,  \
+                                                           page_table, pool->k_pages, pool->v_pages)
+        if (pool->dtype == EP_BF16) {
+            if (mis) EP_INGEST_ROWS(true, true); else EP_INGEST_ROWS(true, false);
+        } else {
+            if (mis) EP_INGEST_ROWS(false, true); else EP_INGEST_ROWS(false, false);
+        }
+#undef EP_INGEST_ROWS
+        EP_CUDA_TRY(cudaGetLastError(), "ep_kv_ingest_frame launch");
+        h->launches++;
+        return EP_OK;
+    }
+    const bool a16 = mis == 0;
     const uint32_t total = 2 * n_pairs;
     const uint32_t blocks = std::min<uint32_t>((total + 1023) / 1024, uint32_t(h->n_sms) * 8);
     const uint32_t P = uint32_t(pool->page_tokens), H = uint32_t(f.n_heads);

@@ -58,7 +58,7 @@ def test_ingest_bit_exact(cuda_handle, dtype, where):
 
 
 def test_ingest_unaligned_device_frame(cuda_handle):
-    """A device frame at an odd 8-byte offset takes the 8-byte-load path."""
+    """A device frame at an odd 8-byte offset (payload 16-byte aligned)."""
     import torch
     fr = _frame(64, 4, 64, seed=4)
     buf = torch.zeros(fr.size + 8, dtype=torch.uint8, device="cuda")
@@ -68,6 +68,37 @@ def test_ingest_unaligned_device_frame(cuda_handle):
     _, _, want_k, _ = O.kv_ingest(fr, O.DT_BF16, 64, [1], 2)
     got = pool.k.view(torch.int16).cpu().numpy().view(np.uint16)
     assert np.array_equal(got[1], want_k[1])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("shape", [(3, 20), (8, 128), (5, 36), (2, 6)])
+@pytest.mark.parametrize("offset", [0, 8])
+def test_ingest_row_shapes_and_offsets(cuda_handle, dtype, shape, offset):
+    """Rows whose quad count is not a multiple of 32 (the last lane of a row
+    reads its own fourth value), rows wider than one CTA (8 x 128), d_head % 4
+    != 0 (2 x 6, the pair kernel), with the payload 16-byte aligned (offset 8:
+    frame+24 lands on a 16-byte boundary) or at +8 (offset 0)."""
+    import torch
+    H, d = shape
+    seq = 131
+    fr = _frame(seq, H, d, seed=11 + H, specials=d >= 8)
+    buf = torch.zeros(fr.size + 16, dtype=torch.uint8, device="cuda")
+    buf[offset:offset + fr.size].copy_(torch.from_numpy(fr))
+    pages = np.array([2, 0, 3], dtype=np.int32)
+    pool = _pool(H, d, dtype, 4)
+    pool.ingest_frame(buf[offset:offset + fr.size], pages, handle=cuda_handle)
+    torch.cuda.synchronize()
+    kv_dt = O.DT_BF16 if dtype == "bf16" else O.DT_F32
+    code, _, want_k, want_v = O.kv_ingest(fr, kv_dt, 64, pages, 4)
+    assert code == O.WIRE_OK
+    if dtype == "bf16":
+        got_k = pool.k.view(torch.int16).cpu().numpy().view(np.uint16)
+        got_v = pool.v.view(torch.int16).cpu().numpy().view(np.uint16)
+    else:
+        got_k, got_v = pool.k.cpu().numpy(), pool.v.cpu().numpy()
+    for p in pages:
+        assert np.array_equal(got_k[p].view(np.uint8), want_k[p].view(np.uint8)), p
+        assert np.array_equal(got_v[p].view(np.uint8), want_v[p].view(np.uint8)), p
 
 
 def test_ingest_errors_match_reference(cuda_handle):
