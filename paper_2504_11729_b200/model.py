@@ -375,9 +375,27 @@ def decode_batch(model: Model, caches, last_tokens, *, want_logits: bool = False
             c._shrink_generated(1)
         raise
     if buf is not None:
-        host = buf.cpu().numpy()
-        return host[B * V:].view(np.int32).copy(), host[:B * V].reshape(B, V)
-    return nxt.cpu().numpy(), (logits.cpu().numpy() if logits is not None else None)
+        host = _to_host(model, buf)
+        return host[B * V:].view(np.int32).copy(), host[:B * V].reshape(B, V).copy()
+    if logits is None:
+        return _to_host(model, nxt).copy(), None
+    return nxt.cpu().numpy(), logits.cpu().numpy()
+
+
+def _to_host(model: Model, t):
+    """Device tensor -> numpy view of a per-model pinned landing buffer that
+    is reused across steps (a direct DMA instead of a staged pageable copy);
+    callers copy out what they keep."""
+    torch = _torch()
+    nbytes = t.numel() * t.element_size()
+    pin = getattr(model, "_pinned_out", None)
+    if pin is None or pin.numel() < nbytes:
+        pin = torch.empty(max(nbytes, 4096), dtype=torch.uint8, pin_memory=True)
+        model._pinned_out = pin
+    dst = pin[:nbytes].view(t.dtype)
+    dst.copy_(t.reshape(-1), non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return dst.numpy()
 
 
 def generate_batch(model: Model, caches, first_tokens, n_steps: int):
