@@ -139,6 +139,7 @@ int ep_destroy(ep_handle h) {
     if (!h) return EP_OK;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->hdr_pinned) cudaFreeHost(h->hdr_pinned);
     delete h;
     return EP_OK;
 }

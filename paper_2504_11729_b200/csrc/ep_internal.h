@@ -41,6 +41,7 @@ struct ep_context {
     ep::DeviceBuffer scratch;       // staging for host-buffer calls
     ep::DeviceBuffer zero_rows;     // 64 zero rows of the widest KV row (page-tail fill)
     ep::DeviceBuffer ingest_stage;  // pageable kv frames staged for ep_kv_ingest_frame
+    uint8_t* hdr_pinned = nullptr;  // pinned landing slot for a device kv frame's 24-byte header
     std::atomic<int64_t> launches{0};
 };
 

@@ -201,8 +201,14 @@ extern "C" int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const voi
     uint8_t hdr[24] = {};
     const size_t nh = frame_bytes < 24 ? frame_bytes : 24;
     if (on_device) {
-        EP_CUDA_TRY(cudaMemcpyAsync(hdr, frame, nh, cudaMemcpyDeviceToHost, s), "ep_kv_ingest_frame header");
+        // the header is checked on the host before launch (decode_frame's
+        // errors stay synchronous): one small DMA into a pinned slot
+        if (!h->hdr_pinned)
+            EP_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->hdr_pinned), 64, cudaHostAllocDefault),
+                        "ep_kv_ingest_frame header slot");
+        EP_CUDA_TRY(cudaMemcpyAsync(h->hdr_pinned, frame, nh, cudaMemcpyDeviceToHost, s), "ep_kv_ingest_frame header");
         EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_kv_ingest_frame header");
+        std::memcpy(hdr, h->hdr_pinned, nh);
     } else {
         std::memcpy(hdr, frame, nh);
     }
