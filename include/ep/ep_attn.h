@@ -247,6 +247,19 @@ int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const void* frame, s
                        const int32_t* page_table, int32_t n_pages, ep_kv_frame_info* info,
                        ep_stream stream);
 
+/* Deferred-check form of ep_kv_ingest_frame for device-resident frames
+ * (GPUDirect receive buffers): no host synchronisation. The host derives
+ * seq_len from frame_bytes and the pool's head shape and launches at once;
+ * the kernel re-parses the 24-byte header (the same decode_frame rules) and,
+ * when it disagrees, writes nothing and records the first failure in a
+ * per-handle status word. ep_kv_ingest_poll synchronises `stream`, returns
+ * that failure (EP_EWIRE with info->wire_error, or EP_EINVAL for the pool
+ * checks) and clears it. Host frames, and device frames whose length does not
+ * fit the pool's head shape, take the synchronous path (immediate errors). */
+int ep_kv_ingest_frame_async(ep_handle h, const ep_kv_pool* pool, const void* frame, size_t frame_bytes,
+                             const int32_t* page_table, int32_t n_pages, ep_stream stream);
+int ep_kv_ingest_poll(ep_handle h, ep_stream stream, ep_kv_frame_info* info);
+
 /* ==================================================================== */
 /* 3b. Cross-GPU split-KV combine over NVLink peer memory (config 4).   */
 /* ==================================================================== */

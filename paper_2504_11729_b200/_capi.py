@@ -134,6 +134,9 @@ _SIGS = {
     "ep_kv_append": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "ep_kv_ingest_frame": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, _sz, _vp, C.c_int32,
                                      C.POINTER(KVFrameInfo), _vp]),
+    "ep_kv_ingest_frame_async": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, _sz, _vp, C.c_int32,
+                                           _vp]),
+    "ep_kv_ingest_poll": (C.c_int, [_vp, _vp, C.POINTER(KVFrameInfo)]),
 }
 
 _SIGS.update({

@@ -140,6 +140,11 @@ int ep_destroy(ep_handle h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->hdr_pinned) cudaFreeHost(h->hdr_pinned);
+    if (h->ingest_status) cudaFreeHost(h->ingest_status);
+    if (h->ingest_done) {
+        cudaEventSynchronize(h->ingest_done);
+        cudaEventDestroy(h->ingest_done);
+    }
     delete h;
     return EP_OK;
 }

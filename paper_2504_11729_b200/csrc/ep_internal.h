@@ -40,8 +40,16 @@ struct ep_context {
     cudaStream_t stream = nullptr;  // used by the synchronous host-buffer entry points
     ep::DeviceBuffer scratch;       // staging for host-buffer calls
     ep::DeviceBuffer zero_rows;     // 64 zero rows of the widest KV row (page-tail fill)
-    ep::DeviceBuffer ingest_stage;  // pageable kv frames staged for ep_kv_ingest_frame
+    ep::DeviceBuffer ingest_stage;  // pageable / misaligned kv frames staged for ep_kv_ingest_frame
+    cudaEvent_t ingest_done = nullptr;  // recorded after each launch that reads ingest_stage
+    bool ingest_pending = false;        // ingest_done has been recorded at least once
     uint8_t* hdr_pinned = nullptr;  // pinned landing slot for a device kv frame's 24-byte header
+    // deferred kv frame check (ep_kv_ingest_frame_async): device words
+    // [0] = first failing kind (0 = none), [1..6] = that frame's header fields,
+    // written by the kernels; ep_kv_ingest_poll reads them into the pinned copy
+    int32_t* ingest_status = nullptr;
+    int32_t* ingest_status_dev = nullptr;
+    ep::DeviceBuffer scratch_status;  // backs ingest_status_dev
     std::atomic<int64_t> launches{0};
 };
 

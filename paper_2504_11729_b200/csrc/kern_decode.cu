@@ -170,6 +170,9 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
         for (int it = it0; it < it1; ++it) nb += a.items[it].nblk;
         a.trace[20 * 1024 + 2 * blockIdx.x] = it1 - it0;
         a.trace[20 * 1024 + 2 * blockIdx.x + 1] = nb;
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        a.trace[30 * 1024 + blockIdx.x] = sm;
     }
 
     uint8_t* sq = smem + C::OFF_Q;
@@ -383,6 +386,11 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             }
         }
 
+        if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && it - it0 < 4) {  // debug: item's last block done
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (it - it0)] = t;
+        }
         // ---- combine the two halves, then the NCW warps, by LSE ----
 #pragma unroll
         for (int r = 0; r < R; ++r)
@@ -458,6 +466,11 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             }
         }
         named_bar_sync(1, NCW * 32);
+        if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && it - it0 < 4) {  // debug: item end done
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (it - it0) + 1] = t;
+        }
     }
     if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // debug: per-CTA end (ns)
         unsigned long long t;

@@ -34,12 +34,133 @@ __device__ __forceinline__ uint16_t f64_to_bf16(double x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
+__host__ __device__ inline uint32_t rd_u32(const uint8_t* b) {
+    return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+}
+__host__ __device__ inline uint16_t rd_u16(const uint8_t* b) { return uint16_t(b[0] | (b[1] << 8)); }
+
+const char* kWireKind[] = {"ok", "bad_magic", "bad_version", "truncated", "length_overflow", "malformed",
+                           "not a kv frame"};
+
+// Why a frame fails (selects the message; the kind is what the reference throws).
+enum WhyCode : int {
+    kWhyNone, kWhyShort, kWhyMagic, kWhyVersion, kWhyType, kWhyLenLimit, kWhyLenMismatch, kWhyOtherPayload,
+    kWhyNotKv, kWhyKvTruncated, kWhyKvShape
+};
+
+// decode_header + decode_frame + the kv_frame payload header (wire.cpp:138-221)
+// on min(24, n) leading bytes of an n-byte frame: returns the WireError kind
+// + 1 (0 = a valid kv frame, 6 = a valid frame of another type) and the
+// reason; fills f. Host (synchronous check) and device (deferred check).
+__host__ __device__ inline int parse_kv_core(const uint8_t* hdr, size_t n, ep_kv_frame_info* f, int* why) {
+    *why = kWhyNone;
+    if (n < 10) { *why = kWhyShort; return 3; }
+    if (hdr[0] != 'E' || hdr[1] != 'P' || hdr[2] != 'K' || hdr[3] != 'V') { *why = kWhyMagic; return 1; }
+    if (hdr[4] != 0x01) { *why = kWhyVersion; return 2; }
+    if (hdr[5] > 4) { *why = kWhyType; return 5; }
+    const uint32_t len = rd_u32(hdr + 6);
+    if (len > (1u << 30)) { *why = kWhyLenLimit; return 4; }
+    if (n != 10 + size_t(len)) { *why = kWhyLenMismatch; return 3; }
+    // the other message types decode (or fail) as decode_payload would
+    // (wire.cpp:165-184, :202-208); a valid one is "not a kv frame"
+    const uint32_t need = hdr[5] == 0 ? 20u : hdr[5] == 1 ? 6u : 0u;
+    if ((hdr[5] == 0 || hdr[5] == 1) && len != need) { *why = kWhyOtherPayload; return len < need ? 3 : 5; }
+    if (hdr[5] == 3 && len != 0) { *why = kWhyOtherPayload; return 5; }
+    if (hdr[5] == 4 && len < 4) { *why = kWhyOtherPayload; return 3; }
+    if (hdr[5] != 2) { *why = kWhyNotKv; return 6; }
+    if (len < 14) { *why = kWhyKvTruncated; return 3; }
+    const uint8_t* p = hdr + 10;
+    f->session_id = rd_u32(p);
+    f->layer = rd_u16(p + 4);
+    f->seq_len = rd_u32(p + 6);
+    f->n_heads = rd_u16(p + 10);
+    f->d_head = rd_u16(p + 12);
+    const uint64_t vals = uint64_t(f->seq_len) * f->n_heads * f->d_head;
+    if (uint64_t(len) - 14 != 16 * vals) { *why = kWhyKvShape; return 5; }
+    return 0;
+}
+
+int parse_kv_header(const uint8_t* hdr, size_t n, ep_kv_frame_info* f, std::string* why) {
+    int w = 0;
+    const int kind = parse_kv_core(hdr, n, f, &w);
+    const uint32_t len = n >= 10 ? rd_u32(hdr + 6) : 0;
+    switch (w) {
+    case kWhyNone: break;
+    case kWhyShort: *why = "frame header shorter than 10 bytes"; break;
+    case kWhyMagic: *why = "frame magic is not EPKV"; break;
+    case kWhyVersion: *why = "unsupported protocol version " + std::to_string(hdr[4]); break;
+    case kWhyType: *why = "unknown message type " + std::to_string(hdr[5]); break;
+    case kWhyLenLimit: *why = "declared payload length " + std::to_string(len) + " exceeds limit"; break;
+    case kWhyLenMismatch:
+        *why = "frame buffer holds " + std::to_string(n) + " bytes, header declares " + std::to_string(10 + size_t(len));
+        break;
+    case kWhyOtherPayload:
+        *why = kind == 3 ? "frame payload truncated"
+               : hdr[5] == 0 ? "session init payload has trailing bytes"
+               : hdr[5] == 1 ? "ack payload has trailing bytes"
+                             : "end-of-prefill payload must be empty";
+        break;
+    case kWhyNotKv: *why = "message type " + std::to_string(hdr[5]) + " is not a kv frame"; break;
+    case kWhyKvTruncated: *why = "frame payload truncated"; break;
+    case kWhyKvShape: {
+        const uint64_t vals = uint64_t(f->seq_len) * f->n_heads * f->d_head;
+        *why = "kv frame payload length " + std::to_string(len) + " does not match shape (expected " +
+               std::to_string(14 + 16 * vals) + ")";
+        break;
+    }
+    }
+    return kind;
+}
+
+// Deferred header check of ep_kv_ingest_frame_async: every CTA re-parses the
+// frame's 24 leading bytes (an L2 hit after the first) against the shape the
+// host derived from the frame length and the pool; on any difference the CTA
+// writes nothing and CTA 0 records the first failing kind in status[0] and
+// the header fields in status[1..6] (read back by ep_kv_ingest_poll).
+struct HdrCheck {
+    const uint8_t* frame;  // null: checked on the host already
+    uint64_t frame_bytes;
+    uint32_t seq_len, n_pages, page_tokens;
+    uint16_t n_heads, d_head;
+    int32_t* status;  // device words
+};
+
+__device__ __forceinline__ bool header_ok(const HdrCheck& c) {
+    if (!c.frame) return true;
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        uint8_t hb[24];
+        for (int i = 0; i < 24; ++i) hb[i] = i < int(c.frame_bytes) ? c.frame[i] : 0;
+        ep_kv_frame_info f{};
+        int why = 0;
+        int kind = parse_kv_core(hb, c.frame_bytes, &f, &why);
+        // the pool-side checks of the synchronous path (EP_EINVAL there)
+        if (!kind && (f.n_heads != c.n_heads || f.d_head != c.d_head)) kind = 7;
+        if (!kind && f.seq_len == 0) kind = 8;
+        if (!kind && (uint64_t(f.seq_len) + c.page_tokens - 1) / c.page_tokens > c.n_pages) kind = 9;
+        if (!kind && f.seq_len != c.seq_len) kind = 5;
+        s_ok = kind == 0;
+        if (kind && blockIdx.x == 0 && atomicCAS(c.status, 0, kind) == 0) {
+            c.status[1] = int32_t(f.session_id);
+            c.status[2] = int32_t(f.seq_len);
+            c.status[3] = f.layer;
+            c.status[4] = f.n_heads;
+            c.status[5] = f.d_head;
+            c.status[6] = why;
+        }
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
 template <bool BF16, bool A16>
 __global__ void __launch_bounds__(256) kv_ingest_kernel(const uint8_t* __restrict__ src,
                                                         uint32_t n_pairs, uint32_t row_pairs,
                                                         uint32_t d_pairs, uint32_t P, uint32_t H,
                                                         const int32_t* __restrict__ page_table,
-                                                        void* __restrict__ kp, void* __restrict__ vp) {
+                                                        void* __restrict__ kp, void* __restrict__ vp,
+                                                        const HdrCheck chk) {
+    if (!header_ok(chk)) return;
     constexpr int U = 4;  // pairs in flight per thread
     const uint32_t total = 2 * n_pairs;
     const uint32_t stride = gridDim.x * blockDim.x;
@@ -93,7 +214,9 @@ __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __re
                                                              uint32_t seq, uint32_t row_quads, uint32_t d_quads,
                                                              uint32_t P, uint32_t H,
                                                              const int32_t* __restrict__ page_table,
-                                                             void* __restrict__ kp, void* __restrict__ vp) {
+                                                             void* __restrict__ kp, void* __restrict__ vp,
+                                                             const HdrCheck chk) {
+    if (!header_ok(chk)) return;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t span = (row_quads + 31) & ~31u;
     for (uint32_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -133,64 +256,90 @@ __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __re
     }
 }
 
-uint32_t rd_u32(const uint8_t* b) {
-    return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
-}
-uint16_t rd_u16(const uint8_t* b) { return uint16_t(b[0] | (b[1] << 8)); }
-
-const char* kWireKind[] = {"ok", "bad_magic", "bad_version", "truncated", "length_overflow", "malformed",
-                           "not a kv frame"};
-
-// decode_header + decode_frame + the kv_frame payload header (wire.cpp:138-221).
-// hdr holds min(24, n) leading bytes of the frame.
-int parse_kv_header(const uint8_t* hdr, size_t n, ep_kv_frame_info* f, std::string* why) {
-    if (n < 10) { *why = "frame header shorter than 10 bytes"; return 3; }
-    if (hdr[0] != 'E' || hdr[1] != 'P' || hdr[2] != 'K' || hdr[3] != 'V') { *why = "frame magic is not EPKV"; return 1; }
-    if (hdr[4] != 0x01) { *why = "unsupported protocol version " + std::to_string(hdr[4]); return 2; }
-    if (hdr[5] > 4) { *why = "unknown message type " + std::to_string(hdr[5]); return 5; }
-    const uint32_t len = rd_u32(hdr + 6);
-    if (len > (1u << 30)) { *why = "declared payload length " + std::to_string(len) + " exceeds limit"; return 4; }
-    if (n != 10 + size_t(len)) {
-        *why = "frame buffer holds " + std::to_string(n) + " bytes, header declares " + std::to_string(10 + size_t(len));
-        return 3;
-    }
-    // the other message types decode (or fail) as decode_payload would
-    // (wire.cpp:165-184, :202-208); a valid one is "not a kv frame"
-    switch (hdr[5]) {
-    case 0: if (len != 20) { *why = len < 20 ? "frame payload truncated" : "session init payload has trailing bytes"; return len < 20 ? 3 : 5; } break;
-    case 1: if (len != 6) { *why = len < 6 ? "frame payload truncated" : "ack payload has trailing bytes"; return len < 6 ? 3 : 5; } break;
-    case 3: if (len != 0) { *why = "end-of-prefill payload must be empty"; return 5; } break;
-    case 4: if (len < 4) { *why = "frame payload truncated"; return 3; } break;
-    default: break;
-    }
-    if (hdr[5] != 2) { *why = "message type " + std::to_string(hdr[5]) + " is not a kv frame"; return 6; }
-    if (len < 14) { *why = "frame payload truncated"; return 3; }
-    const uint8_t* p = hdr + 10;
-    f->session_id = rd_u32(p);
-    f->layer = rd_u16(p + 4);
-    f->seq_len = rd_u32(p + 6);
-    f->n_heads = rd_u16(p + 10);
-    f->d_head = rd_u16(p + 12);
-    const uint64_t vals = uint64_t(f->seq_len) * f->n_heads * f->d_head;
-    if (uint64_t(len) - 14 != 16 * vals) {
-        *why = "kv frame payload length " + std::to_string(len) + " does not match shape (expected " +
-               std::to_string(14 + 16 * vals) + ")";
-        return 5;
-    }
-    return 0;
-}
-
 }  // namespace
 }  // namespace ep
 
+
 using ep::fail;
+
+namespace {
+
+// Copies a frame payload into the per-handle staging buffer, ordered after the
+// previous launch that read it (which may be on another stream).
+int stage_payload(ep_context* h, const void* src, size_t bytes, cudaStream_t s, const uint8_t** out) {
+    if (h->ingest_pending && bytes > h->ingest_stage.bytes)
+        EP_CUDA_TRY(cudaEventSynchronize(h->ingest_done), "ep_kv_ingest_frame staging");
+    EP_CUDA_TRY(h->ingest_stage.reserve(bytes), "ep_kv_ingest_frame staging");
+    if (h->ingest_pending) EP_CUDA_TRY(cudaStreamWaitEvent(s, h->ingest_done, 0), "ep_kv_ingest_frame staging");
+    EP_CUDA_TRY(cudaMemcpyAsync(h->ingest_stage.ptr, src, bytes, cudaMemcpyDefault, s),
+                "ep_kv_ingest_frame staging copy");
+    *out = static_cast<const uint8_t*>(h->ingest_stage.ptr);
+    return EP_OK;
+}
+
+// One decode + convert + scatter launch over the payload at src (8-byte aligned).
+int launch_ingest(ep_context* h, const ep_kv_pool* pool, uint32_t seq_len, uint32_t n_heads, uint32_t d_head,
+                  const uint8_t* src, bool staged, const int32_t* page_table, const ep::HdrCheck& chk,
+                  cudaStream_t s) {
+    const uint64_t vals = uint64_t(seq_len) * n_heads * d_head;
+    const uint32_t n_pairs = uint32_t(vals / 2), d_pairs = d_head / 2;
+    const uint32_t row_pairs = n_heads * d_pairs;
+    const uintptr_t mis = reinterpret_cast<uintptr_t>(src) & 15;
+    const bool pool_al = (reinterpret_cast<uintptr_t>(pool->k_pages) & 15) == 0 &&
+                         (reinterpret_cast<uintptr_t>(pool->v_pages) & 15) == 0;
+    const uint32_t P = uint32_t(pool->page_tokens), H = n_heads;
+    if (d_head % 4 == 0 && pool_al) {
+        const uint32_t rows = 2 * seq_len, d_quads = d_head / 4;
+        const uint32_t row_quads = n_heads * d_quads;
+        const uint32_t tpb = row_quads >= 256 ? 256 : ((row_quads + 31) & ~31u);
+        const uint32_t grid = std::min<uint32_t>(rows, uint32_t(h->n_sms) * (2048 / tpb));
+#define EP_INGEST_ROWS(BF, M8)                                                                           \
+    ep::kv_ingest_rows_kernel<BF, M8><<<grid, tpb, 0, s>>>(src, rows, seq_len, row_quads, d_quads, P, H, \
+                                                           page_table, pool->k_pages, pool->v_pages, chk)
+        if (pool->dtype == EP_BF16) {
+            if (mis) EP_INGEST_ROWS(true, true); else EP_INGEST_ROWS(true, false);
+        } else {
+            if (mis) EP_INGEST_ROWS(false, true); else EP_INGEST_ROWS(false, false);
+        }
+#undef EP_INGEST_ROWS
+    } else {
+        const uint32_t total = 2 * n_pairs;
+        const uint32_t blocks = std::min<uint32_t>((total + 1023) / 1024, uint32_t(h->n_sms) * 8);
+#define EP_INGEST(BF, AL)                                                                              \
+    ep::kv_ingest_kernel<BF, AL><<<blocks, 256, 0, s>>>(src, n_pairs, row_pairs, d_pairs, P, H, page_table, \
+                                                       pool->k_pages, pool->v_pages, chk)
+        if (pool->dtype == EP_BF16) {
+            if (mis == 0) EP_INGEST(true, true); else EP_INGEST(true, false);
+        } else {
+            if (mis == 0) EP_INGEST(false, true); else EP_INGEST(false, false);
+        }
+#undef EP_INGEST
+    }
+    EP_CUDA_TRY(cudaGetLastError(), "ep_kv_ingest_frame launch");
+    if (staged) {
+        if (!h->ingest_done)
+            EP_CUDA_TRY(cudaEventCreateWithFlags(&h->ingest_done, cudaEventDisableTiming), "ep_kv_ingest_frame");
+        EP_CUDA_TRY(cudaEventRecord(h->ingest_done, s), "ep_kv_ingest_frame");
+        h->ingest_pending = true;
+    }
+    h->launches++;
+    return EP_OK;
+}
+
+int check_pool(const ep_kv_pool* pool, const char* where) {
+    if (pool->dtype != EP_F32 && pool->dtype != EP_BF16)
+        return fail(EP_EUNSUPPORTED, std::string(where) + ": pool dtype must be f32 or bf16");
+    if (pool->d_head % 2) return fail(EP_EUNSUPPORTED, std::string(where) + ": odd d_head");
+    return EP_OK;
+}
+
+}  // namespace
 
 extern "C" int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const void* frame,
                                   size_t frame_bytes, const int32_t* page_table, int32_t n_pages,
                                   ep_kv_frame_info* info, ep_stream stream) {
     if (!h || !pool || !frame || !page_table) return fail(EP_EINVAL, "ep_kv_ingest_frame: null argument");
-    if (pool->dtype != EP_F32 && pool->dtype != EP_BF16)
-        return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: pool dtype must be f32 or bf16");
+    if (int rc = check_pool(pool, "ep_kv_ingest_frame")) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ep_kv_frame_info f{};
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_kv_ingest_frame");
@@ -225,59 +374,86 @@ extern "C" int ep_kv_ingest_frame(ep_handle h, const ep_kv_pool* pool, const voi
     if (n_pages < need)
         return fail(EP_EINVAL, "ep_kv_ingest_frame: " + std::to_string(f.seq_len) + " tokens need " +
                                    std::to_string(need) + " pages, got " + std::to_string(n_pages));
-    if (f.d_head % 2) return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: odd d_head");
     const uint64_t vals = uint64_t(f.seq_len) * f.n_heads * f.d_head;
     if (vals / 2 > 0x7FFFFFFFull) return fail(EP_EUNSUPPORTED, "ep_kv_ingest_frame: frame too large");
-    const uint8_t* src;
-    if (on_device) {
-        src = static_cast<const uint8_t*>(frame) + 24;
-    } else if (pinned) {
-        src = static_cast<const uint8_t*>(at.devicePointer ? at.devicePointer : frame) + 24;
-    } else {
-        EP_CUDA_TRY(h->ingest_stage.reserve(16 * vals), "ep_kv_ingest_frame staging");
-        EP_CUDA_TRY(cudaMemcpyAsync(h->ingest_stage.ptr, static_cast<const uint8_t*>(frame) + 24, 16 * vals,
-                                    cudaMemcpyHostToDevice, s),
-                    "ep_kv_ingest_frame staging copy");
-        src = static_cast<const uint8_t*>(h->ingest_stage.ptr);
+    const uint8_t* src = static_cast<const uint8_t*>(on_device || !pinned || !at.devicePointer ? frame
+                                                                                             : at.devicePointer) + 24;
+    bool staged = false;
+    // pageable frames, and device / pinned payloads that are not 8-byte
+    // aligned (a kv frame following a 30-byte session_init frame in one
+    // receive buffer), are copied into the aligned per-handle staging buffer
+    if ((!on_device && !pinned) || (reinterpret_cast<uintptr_t>(src) & 7)) {
+        if (int rc = stage_payload(h, static_cast<const uint8_t*>(frame) + 24, 16 * vals, s, &src)) return rc;
+        staged = true;
     }
-    const uint32_t n_pairs = uint32_t(vals / 2), d_pairs = uint32_t(f.d_head / 2);
-    const uint32_t row_pairs = uint32_t(f.n_heads) * d_pairs;
-    const uintptr_t mis = reinterpret_cast<uintptr_t>(src) & 15;
-    const bool pool_al = (reinterpret_cast<uintptr_t>(pool->k_pages) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(pool->v_pages) & 15) == 0;
-    if (f.d_head % 4 == 0 && (mis == 0 || mis == 8) && pool_al) {
-        const uint32_t rows = 2 * f.seq_len, d_quads = uint32_t(f.d_head / 4);
-        const uint32_t row_quads = uint32_t(f.n_heads) * d_quads;
-        const uint32_t tpb = row_quads >= 256 ? 256 : ((row_quads + 31) & ~31u);
-        const uint32_t grid = std::min<uint32_t>(rows, uint32_t(h->n_sms) * (2048 / tpb));
-        const uint32_t P = uint32_t(pool->page_tokens), H = uint32_t(f.n_heads);
-#define EP_INGEST_ROWS(BF, M8)                                                                                \
-    ep::kv_ingest_rows_kernel<BF, M8><<<grid, tpb, 0, s>>>(src, rows, f.seq_len, row_quads, d_quads, P, H,  \
-                                                           page_table, pool->k_pages, pool->v_pages)
-        if (pool->dtype == EP_BF16) {
-            if (mis) EP_INGEST_ROWS(true, true); else EP_INGEST_ROWS(true, false);
-        } else {
-            if (mis) EP_INGEST_ROWS(false, true); else EP_INGEST_ROWS(false, false);
-        }
-#undef EP_INGEST_ROWS
-        EP_CUDA_TRY(cudaGetLastError(), "ep_kv_ingest_frame launch");
-        h->launches++;
-        return EP_OK;
+    return launch_ingest(h, pool, f.seq_len, f.n_heads, f.d_head, src, staged, page_table, ep::HdrCheck{}, s);
+}
+
+extern "C" int ep_kv_ingest_frame_async(ep_handle h, const ep_kv_pool* pool, const void* frame,
+                                        size_t frame_bytes, const int32_t* page_table, int32_t n_pages,
+                                        ep_stream stream) {
+    if (!h || !pool || !frame || !page_table) return fail(EP_EINVAL, "ep_kv_ingest_frame_async: null argument");
+    if (int rc = check_pool(pool, "ep_kv_ingest_frame_async")) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_kv_ingest_frame_async");
+    cudaPointerAttributes at{};
+    EP_CUDA_TRY(cudaPointerGetAttributes(&at, frame), "ep_kv_ingest_frame_async pointer attributes");
+    const bool on_device = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+    // host frames: the header is readable without a sync, so the check stays immediate
+    const uint64_t row = 16ull * uint64_t(pool->n_kv_heads) * uint64_t(pool->d_head);
+    if (!on_device || frame_bytes < 24 || row == 0 || (frame_bytes - 24) % row != 0 ||
+        (frame_bytes - 24) / row == 0 || (frame_bytes - 24) / row > 0xFFFFFFFFull ||
+        (uint64_t(frame_bytes - 24) / 16) / 2 > 0x7FFFFFFFull)
+        return ep_kv_ingest_frame(h, pool, frame, frame_bytes, page_table, n_pages, nullptr, stream);
+    // device frame whose length fits the pool's head shape: launch at once,
+    // the kernels check the header against the shape derived here
+    if (!h->ingest_status) {
+        EP_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&h->ingest_status), 64, cudaHostAllocDefault),
+                    "ep_kv_ingest_frame_async status");
+        std::memset(h->ingest_status, 0, 64);
+        EP_CUDA_TRY(h->scratch_status.reserve(64), "ep_kv_ingest_frame_async status");
+        h->ingest_status_dev = static_cast<int32_t*>(h->scratch_status.ptr);
+        EP_CUDA_TRY(cudaMemsetAsync(h->ingest_status_dev, 0, 64, s), "ep_kv_ingest_frame_async status");
     }
-    const bool a16 = mis == 0;
-    const uint32_t total = 2 * n_pairs;
-    const uint32_t blocks = std::min<uint32_t>((total + 1023) / 1024, uint32_t(h->n_sms) * 8);
-    const uint32_t P = uint32_t(pool->page_tokens), H = uint32_t(f.n_heads);
-#define EP_INGEST(BF, AL)                                                                              \
-    ep::kv_ingest_kernel<BF, AL><<<blocks, 256, 0, s>>>(src, n_pairs, row_pairs, d_pairs, P, H, page_table, \
-                                                       pool->k_pages, pool->v_pages)
-    if (pool->dtype == EP_BF16) {
-        if (a16) EP_INGEST(true, true); else EP_INGEST(true, false);
-    } else {
-        if (a16) EP_INGEST(false, true); else EP_INGEST(false, false);
+    const uint32_t seq = uint32_t((frame_bytes - 24) / row);
+    ep::HdrCheck chk{static_cast<const uint8_t*>(frame), uint64_t(frame_bytes), seq, uint32_t(n_pages > 0 ? n_pages : 0),
+                     uint32_t(pool->page_tokens), uint16_t(pool->n_kv_heads), uint16_t(pool->d_head),
+                     h->ingest_status_dev};
+    const uint8_t* src = static_cast<const uint8_t*>(frame) + 24;
+    bool staged = false;
+    if (reinterpret_cast<uintptr_t>(src) & 7) {
+        if (int rc = stage_payload(h, src, frame_bytes - 24, s, &src)) return rc;
+        staged = true;
     }
-#undef EP_INGEST
-    EP_CUDA_TRY(cudaGetLastError(), "ep_kv_ingest_frame launch");
-    h->launches++;
-    return EP_OK;
+    return launch_ingest(h, pool, seq, uint32_t(pool->n_kv_heads), uint32_t(pool->d_head), src, staged, page_table,
+                         chk, s);
+}
+
+extern "C" int ep_kv_ingest_poll(ep_handle h, ep_stream stream, ep_kv_frame_info* info) {
+    if (!h) return fail(EP_EINVAL, "ep_kv_ingest_poll: null handle");
+    if (!h->ingest_status) return EP_OK;  // no deferred ingest issued yet
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    EP_CUDA_TRY(cudaSetDevice(h->device), "ep_kv_ingest_poll");
+    EP_CUDA_TRY(cudaMemcpyAsync(h->ingest_status, h->ingest_status_dev, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                "ep_kv_ingest_poll");
+    EP_CUDA_TRY(cudaStreamSynchronize(s), "ep_kv_ingest_poll");
+    const int32_t* st = h->ingest_status;
+    const int kind = st[0];
+    if (!kind) return EP_OK;
+    ep_kv_frame_info f{};
+    f.session_id = uint32_t(st[1]);
+    f.seq_len = uint32_t(st[2]);
+    f.layer = uint16_t(st[3]);
+    f.n_heads = uint16_t(st[4]);
+    f.d_head = uint16_t(st[5]);
+    f.wire_error = kind <= 6 ? kind : 0;
+    if (info) *info = f;
+    EP_CUDA_TRY(cudaMemsetAsync(h->ingest_status_dev, 0, 64, s), "ep_kv_ingest_poll");
+    if (kind <= 6)
+        return fail(EP_EWIRE, std::string("wire: ") + ep::kWireKind[kind] + ": deferred kv frame check failed");
+    return fail(EP_EINVAL, kind == 7   ? "ep_kv_ingest_frame_async: kv frame head shape (" + std::to_string(f.n_heads) +
+                                             " x " + std::to_string(f.d_head) + ") does not match the pool"
+                           : kind == 8 ? std::string("ep_kv_ingest_frame_async: kv frame with empty sequence")
+                                       : "ep_kv_ingest_frame_async: " + std::to_string(f.seq_len) +
+                                             " tokens need more pages than given");
 }

@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
                     int bi = a.N;
                     for (int c = lane; c < a.N; c += 32) {
                         const T v = __ldcg(lg + size_t(r) * a.N + c);
-                        if (bi == a.N || v > bv) {
+                        if (v == v && (bi == a.N || v > bv)) {  // NaN: see argmax_rows_kernel
                             bv = v;
                             bi = c;
                         }
@@ -458,7 +458,10 @@ __global__ void __launch_bounds__(kDenseThreads) gemv_cluster_kernel(const Dense
                             bi = oi;
                         }
                     }
-                    if (lane == 0) a.next[so + r] = bi == a.N ? 0 : bi;
+                    if (lane == 0) {
+                        const T x0 = __ldcg(lg + size_t(r) * a.N);
+                        a.next[so + r] = (bi == a.N || x0 != x0) ? 0 : bi;
+                    }
                 }
                 __syncthreads();
                 if (tid == 0) {
@@ -662,7 +665,7 @@ __global__ void argmax_rows_kernel(const T* logits, int V, const int32_t* step, 
     int bi = V;
     for (int i = tid; i < V; i += blockDim.x) {
         const T v = x[i];
-        if (bi == V || v > bv) {
+        if (v == v && (bi == V || v > bv)) {  // a NaN is never taken (x[0] below)
             bv = v;
             bi = i;
         }
@@ -683,7 +686,8 @@ __global__ void argmax_rows_kernel(const T* logits, int V, const int32_t* step, 
         }
         __syncthreads();
     }
-    if (tid == 0) next[r] = si[0] == V ? 0 : si[0];
+    // argmax_token starts at id 0: a NaN there is never replaced
+    if (tid == 0) next[r] = (si[0] == V || x[0] != x[0]) ? 0 : si[0];
 }
 
 // ------------------------------------------------------------- init draws --

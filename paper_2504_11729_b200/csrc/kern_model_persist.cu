@@ -44,7 +44,11 @@ constexpr float kEps = 1e-5f;  // model.cpp:14
 // Order-preserving 64-bit key of (logit, id): larger logit first, then the
 // lower id (argmax_token's strict '>' keeps the first maximum).
 __device__ __forceinline__ unsigned long long order_key(float z, uint32_t idx) {
-    uint32_t b = __float_as_uint(z);
+    // argmax_token compares with '>': -0 == +0 (canonicalised so the lower
+    // id wins the tie), and a NaN is never taken over a number — except at
+    // id 0, where the scan starts and nothing compares greater than it
+    if (z != z) return idx == 0 ? ~0ull : 0ull;
+    uint32_t b = __float_as_uint(z == 0.f ? 0.f : z);
     b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
     return (uint64_t(b) << 32) | uint64_t(0xFFFFFFFFu - idx);
 }

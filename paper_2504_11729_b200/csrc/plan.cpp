@@ -528,8 +528,8 @@ unsigned long long* trace_buffer() {
     static unsigned long long* t = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&b, 22 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(b, 0, 22 * 1024 * sizeof(unsigned long long));
+        if (e && e[0] == '1' && cudaMalloc(&b, 31 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 31 * 1024 * sizeof(unsigned long long));
         return b;
     }();
     return t;
@@ -538,7 +538,7 @@ unsigned long long* trace_buffer() {
 // debug: EP_TRACE=1 dumps the trace buffer (CTA 0 event clocks, per-CTA
 // start / end / work) of the last launch to EP_TRACE_FILE
 void dump_trace(unsigned long long* trace, cudaStream_t s) {
-    std::vector<unsigned long long> host(22 * 1024);
+    std::vector<unsigned long long> host(31 * 1024);
     cudaStreamSynchronize(s);
     cudaMemcpy(host.data(), trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     const char* f = std::getenv("EP_TRACE_FILE");

@@ -50,7 +50,7 @@ class PromptKVCache:
         self.pools = list(pools or [])
         self.allocator = allocator
         self.page_tokens = page_tokens
-        self._mu = threading.Lock()
+        self._mu = threading.RLock()
         self._entries: OrderedDict[int, CachedPrompt] = OrderedDict()  # LRU order
         self._sessions: dict[int, int] = {}
 
@@ -118,6 +118,13 @@ class PromptKVCache:
                 raise OutOfMemory(f"PromptKVCache: {n_pages} pages needed, "
                                   f"{self.allocator.free_pages} free after eviction")
 
+    def reserve(self, n_pages: int) -> np.ndarray:
+        """make_room + alloc under one lock: no other thread can take the
+        pages that eviction freed before this caller allocates them."""
+        with self._mu:
+            self.make_room(n_pages)
+            return self.allocator.alloc(n_pages)
+
     def ingest(self, prompt_id: int, frames, handle=None, stream=None) -> CachedPrompt:
         """Stores a prompt whose per-layer KV arrives as EPKV kv frames (one
         per layer pool, layer order — the cloud's serve_stream output,
@@ -133,13 +140,12 @@ class PromptKVCache:
             return hit
         pages = None
         seq_len = None
+        kept = False  # our pages became the stored entry
         try:
             for layer, (pool, frame) in enumerate(zip(self.pools, frames)):
                 if pages is None:
                     seq_len = _frame_seq_len(frame)
-                    n = -(-seq_len // self.page_tokens)
-                    self.make_room(n)
-                    pages = self.allocator.alloc(n)
+                    pages = self.reserve(-(-seq_len // self.page_tokens))
                 info = pool.ingest_frame(frame, pages, handle=handle, stream=stream)
                 if info.seq_len != seq_len:
                     raise InvalidArgument("PromptKVCache.ingest: sequence length changed between "
@@ -147,9 +153,15 @@ class PromptKVCache:
                 if info.layer != layer:
                     raise InvalidArgument(f"PromptKVCache.ingest: frame for layer {info.layer} "
                                           f"arrived out of order, expected {layer}")
-            return self.store(prompt_id, seq_len, pages)
+            e = self.store(prompt_id, seq_len, pages)
+            kept = e.pages is not pages and np.array_equal(e.pages, pages)
+            return e
         finally:
             if pages is not None:
+                if not kept:
+                    # the pages go back to the free list while ingest kernels
+                    # may still be writing them: wait for the stream first
+                    _sync(stream)
                 self.allocator.release(pages)  # the entry (if stored) holds its own reference
 
     def __contains__(self, prompt_id: int) -> bool:
@@ -159,6 +171,16 @@ class PromptKVCache:
     def __len__(self) -> int:
         with self._mu:
             return len(self._entries)
+
+
+def _sync(stream) -> None:
+    import torch
+    if stream is None:
+        torch.cuda.current_stream().synchronize()
+    elif hasattr(stream, "synchronize"):
+        stream.synchronize()
+    else:
+        torch.cuda.synchronize()
 
 
 def _frame_seq_len(frame) -> int:

@@ -169,6 +169,41 @@ class KVPool:
         check(rc, "ep_kv_ingest_frame")
         return info
 
+    def ingest_frame_async(self, frame, pages, handle: Handle | None = None, stream=None):
+        """ingest_frame for a device-resident frame without a host sync
+        (ep_kv_ingest_frame_async): the header is checked by the kernel and a
+        failure surfaces at the next ``ingest_poll``. Host frames and frames
+        whose length does not fit the pool's head shape fail immediately."""
+        torch = _torch()
+        handle = handle or default_handle(self.k.device.index or 0)
+        assert isinstance(frame, torch.Tensor) and frame.dtype == torch.uint8 and frame.is_contiguous()
+        if isinstance(pages, torch.Tensor) and pages.is_cuda:
+            pt = pages.to(torch.int32).contiguous()
+        else:
+            pt = torch.as_tensor(np.asarray(pages, dtype=np.int32), device=self.k.device)
+        self._ingest_keep = (frame, pt)
+        pd = self.desc()
+        rc = lib().ep_kv_ingest_frame_async(handle.ptr, C.byref(pd), frame.data_ptr(), frame.numel(),
+                                            pt.data_ptr(), int(pt.numel()), _stream(stream))
+        if rc == _capi.EP_EWIRE:
+            raise _capi.WireError("ep_kv_ingest_frame_async: " + lib().ep_last_error().decode())
+        check(rc, "ep_kv_ingest_frame_async")
+
+    @staticmethod
+    def ingest_poll(handle: Handle | None = None, stream=None):
+        """Synchronises ``stream`` and raises the first deferred kv frame
+        failure since the last poll (WireError with ``.kind`` and ``.info``,
+        or InvalidArgument); returns None when every frame was valid."""
+        handle = handle or default_handle()
+        info = _capi.KVFrameInfo()
+        rc = lib().ep_kv_ingest_poll(handle.ptr, _stream(stream), C.byref(info))
+        if rc == _capi.EP_EWIRE:
+            err = _capi.WireError("ep_kv_ingest_poll: " + lib().ep_last_error().decode())
+            err.kind = int(info.wire_error)
+            err.info = info
+            raise err
+        check(rc, "ep_kv_ingest_poll")
+
     def desc(self) -> KVPoolDesc:
         return KVPoolDesc(self.code, self.n_kv_heads, self.d_head, self.page_tokens,
                           self.num_pages, self.k.data_ptr(), self.v.data_ptr())

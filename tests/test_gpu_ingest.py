@@ -151,3 +151,110 @@ def test_ingested_kv_attends_like_oracle(cuda_handle):
                            q=np.ascontiguousarray(q_raw), n_q=1)
     want_o, _ = O.spliced_attention(sb)
     assert rel_err(o.cpu().numpy(), want_o) < 1e-4
+
+
+def _read_pool(pool, dtype):
+    import torch
+    if dtype == "bf16":
+        return (pool.k.view(torch.int16).cpu().numpy().view(np.uint16),
+                pool.v.view(torch.int16).cpu().numpy().view(np.uint16))
+    return pool.k.cpu().numpy(), pool.v.cpu().numpy()
+
+
+@pytest.mark.parametrize("where", ["device", "pinned"])
+@pytest.mark.parametrize("offset", [1, 2, 4, 6, 30])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_ingest_misaligned_payload(cuda_handle, where, offset, dtype):
+    """A kv frame at any byte offset of a receive buffer (e.g. right after a
+    30-byte session_init frame): payloads that are not 8-byte aligned are
+    staged into an aligned buffer instead of faulting (the reference's
+    decode_frame reads bytes and accepts any alignment)."""
+    import torch
+    seq, H, d = 131, 4, 64
+    fr = _frame(seq, H, d, seed=40 + offset, specials=True)
+    buf = torch.zeros(fr.size + 64, dtype=torch.uint8)
+    buf[offset:offset + fr.size].copy_(torch.from_numpy(fr))
+    buf = buf.cuda() if where == "device" else buf.pin_memory()
+    pages = np.array([2, 0, 3], dtype=np.int32)
+    pool = _pool(H, d, dtype, 4)
+    pool.ingest_frame(buf[offset:offset + fr.size], pages, handle=cuda_handle)
+    torch.cuda.synchronize()
+    kv_dt = O.DT_BF16 if dtype == "bf16" else O.DT_F32
+    _, _, want_k, want_v = O.kv_ingest(fr, kv_dt, 64, pages, 4)
+    got_k, got_v = _read_pool(pool, dtype)
+    for p in pages:
+        assert np.array_equal(got_k[p].view(np.uint8), want_k[p].view(np.uint8)), p
+        assert np.array_equal(got_v[p].view(np.uint8), want_v[p].view(np.uint8)), p
+
+
+def test_ingest_staging_ordered_across_streams(cuda_handle):
+    """Pageable frames share one staging buffer per handle: a second frame
+    staged on another stream must not overwrite the first frame's bytes before
+    the first ingest kernel has read them."""
+    import torch
+    seq, H, d = 4096, 8, 128
+    frs = [_frame(seq, H, d, seed=60 + i) for i in range(2)]
+    pools = [_pool(H, d, "bf16", 64) for _ in range(2)]
+    pages = np.arange(64, dtype=np.int32)
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    # a long kernel ahead of the first ingest on s0 keeps its read pending
+    with torch.cuda.stream(s0):
+        torch.cuda._sleep(20_000_000)
+    pools[0].ingest_frame(frs[0], pages, handle=cuda_handle, stream=s0)
+    pools[1].ingest_frame(frs[1], pages, handle=cuda_handle, stream=s1)
+    torch.cuda.synchronize()
+    for fr, pool in zip(frs, pools):
+        _, _, want_k, want_v = O.kv_ingest(fr, O.DT_BF16, 64, pages, 64)
+        got_k, got_v = _read_pool(pool, "bf16")
+        assert np.array_equal(got_k, want_k) and np.array_equal(got_v, want_v)
+
+
+@pytest.mark.parametrize("offset", [0, 8, 3])
+def test_ingest_async_device_frames(cuda_handle, offset):
+    """ep_kv_ingest_frame_async: a valid device frame is ingested with no host
+    sync and the pages equal the synchronous path's; a corrupted header is
+    caught by the kernel (nothing written) and reported at the next poll with
+    the reference's WireError kind; the status clears after the poll."""
+    import torch
+    from paper_2504_11729_b200._capi import InvalidArgument, WireError
+    from paper_2504_11729_b200.splice import KVPool
+    seq, H, d = 200, 8, 128
+    fr = _frame(seq, H, d, seed=70, specials=True)
+    pages = np.array([6, 2, 0, 4], dtype=np.int32)
+
+    def dev(b):
+        buf = torch.zeros(b.size + 16, dtype=torch.uint8, device="cuda")
+        buf[offset:offset + b.size].copy_(torch.from_numpy(b))
+        return buf[offset:offset + b.size]
+
+    pool = _pool(H, d, "bf16", 7)
+    pool.ingest_frame_async(dev(fr), pages, handle=cuda_handle)
+    KVPool.ingest_poll(cuda_handle)
+    _, _, want_k, want_v = O.kv_ingest(fr, O.DT_BF16, 64, pages, 7)
+    got_k, got_v = _read_pool(pool, "bf16")
+    for p in pages:
+        assert np.array_equal(got_k[p], want_k[p]) and np.array_equal(got_v[p], want_v[p])
+
+    bad = {}
+    b = fr.copy(); b[0] = ord("Q"); bad["bad_magic"] = b
+    b = fr.copy(); b[4] = 7; bad["bad_version"] = b
+    b = fr.copy(); b[5] = 3; bad["end_of_prefill_type"] = b
+    b = fr.copy(); b[16:20] = np.frombuffer(np.uint32(seq - 1).tobytes(), np.uint8); bad["seq"] = b
+    for name, b in bad.items():
+        want = O.kv_frame_decode(b, "ref")[0]
+        p2 = _pool(H, d, "bf16", 7)
+        p2.ingest_frame_async(dev(b), pages, handle=cuda_handle)
+        with pytest.raises(WireError) as ei:
+            KVPool.ingest_poll(cuda_handle)
+        assert ei.value.kind == want, (name, ei.value.kind, want)
+        assert not p2.k.view(torch.int16).any().item(), name   # nothing written
+        KVPool.ingest_poll(cuda_handle)                        # cleared
+    # frame whose head shape differs from the pool's (same byte length: 4 x 256)
+    fr2 = _frame(seq, 4, 256, seed=71)
+    p3 = _pool(H, d, "bf16", 7)
+    p3.ingest_frame_async(dev(fr2), pages, handle=cuda_handle)
+    with pytest.raises(InvalidArgument):
+        KVPool.ingest_poll(cuda_handle)
+    # a length that does not fit the pool shape fails immediately
+    with pytest.raises(WireError):
+        pool.ingest_frame_async(dev(fr[:-1].copy()), pages, handle=cuda_handle)

@@ -120,17 +120,22 @@ def _oracle_argmax(x, W64):
     return np.argmax(xn @ W64, axis=-1)
 
 
-@pytest.mark.parametrize("case", ["tie_pair", "all_equal", "random"])
-def test_score_refinement_edge_cases(cuda_handle, case):
+@pytest.mark.parametrize("case,B,n_q", [
+    ("tie_pair", 4, 3), ("all_equal", 4, 3), ("random", 4, 3), ("zero_max", 4, 3),
+    ("random", 43, 3), ("random", 64, 5), ("random", 64, 9), ("tie_pair", 64, 9),
+    ("zero_max", 64, 5)])
+def test_score_refinement_edge_cases(cuda_handle, case, B, n_q):
     """K4's hi-only GEMM + exact refinement against the fp64 argmax on crafted
     rows: exact ties between two vocab entries (argmax_token keeps the lower
     id), a W whose columns are all identical (every logit ties: the candidate
-    overflow path must still return id 0), and random rows."""
+    overflow path must still return id 0), a maximum of exactly zero shared
+    by two all-zero vocab columns, and random rows — at 12 rows (one M tile)
+    and at 129 / 320 / 576 rows (2 / 3 / 5 M tiles, partial last tile)."""
     import torch
     from paper_2504_11729_b200.verify import VerifyGreedy
     from tests.gpu_util import torch_from_raw
-    B, n_q, width, V = 4, 3, 4096, 4096
-    rng = np.random.default_rng({"tie_pair": 1, "all_equal": 2, "random": 3}[case])
+    width, V = 4096, 4096
+    rng = np.random.default_rng({"tie_pair": 1, "all_equal": 2, "random": 3, "zero_max": 4}[case] + B)
     W = O.fill_uniform(O.DT_BF16, width * V, 77).reshape(width, V)  # raw bf16 [width][vocab]
     x = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32) * 0.01
     if case == "tie_pair":
@@ -143,6 +148,17 @@ def test_score_refinement_edge_cases(cuda_handle, case):
         W[:, 1000] = col
     elif case == "all_equal":
         W[:, :] = W[:, :1]
+    elif case == "zero_max":
+        # every column anti-aligned with the rows' shared direction (logits
+        # < 0) except columns 40 and 41, which are zero: the maximum is an
+        # exact 0 tie and argmax_token keeps id 40
+        u = rng.uniform(-1.0, 1.0, size=width).astype(np.float32)
+        x = x + 0.05 * u
+        scale = rng.uniform(0.2, 1.0, size=V)
+        wf = (-np.outer(u.astype(np.float64) - u.mean(), scale)).astype(np.float32).view(np.uint32)
+        W[:, :] = ((wf + 0x7FFF + ((wf >> 16) & 1)) >> 16).astype(np.uint16)   # RNE to bf16
+        W[:, 40] = 0
+        W[:, 41] = 0
     w_t = torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16)
     ver = VerifyGreedy(w_t, handle=cuda_handle)
     xt = torch.from_numpy(x).cuda().view(B, n_q, 32, 128)
@@ -154,4 +170,93 @@ def test_score_refinement_edge_cases(cuda_handle, case):
         assert (want == 17).all()
     if case == "all_equal":
         assert (want == 0).all()
+    if case == "zero_max":
+        assert (want == 40).all()
     assert np.array_equal(got, want), (got, want)
+
+
+def _cfg3_setup(k, h):
+    """BASELINE config 3 at full size, built like the bench (tools/verify_bench.py):
+    B = 64 requests, private KV, cloud 14336 + edge 1536 + generated 512 =
+    16384 keys, Hq 32 / Hkv 8 / d 128 bf16, W_score 4096 x 4096 bf16; pool, q
+    and W drawn on the device by ep_fill_uniform (the SplitMix64 stream of
+    oracle.fill_uniform, so the host can regenerate any slice)."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import verify_bench as VB
+    return VB, VB.setup(k, h)
+
+
+@pytest.mark.parametrize("k", [4, 8])
+def test_config3_verify_production_path(cuda_handle, k):
+    """The path the bench times (K3 attention -> K4 hi-only GEMM + candidate
+    refinement + fused accept, logits=None) at config 3's full shape: 64 x
+    (k+1) = 320 / 576 score rows, i.e. 3 / 5 M tiles of 128 with a partial
+    last tile. Attention is checked against the fp64 oracle on sampled
+    requests (all their units); every target id against argmax_token(LN(x) @
+    W) in fp64 over the GPU's own fp32 attention rows (model.cpp:238-255),
+    outside the margin guard; every accepted count against the acceptance rule
+    on the oracle ids (drafts force every acceptance length 0..k)."""
+    import torch
+    from tests.cases import rel_err
+    VB, st = _cfg3_setup(k, cuda_handle)
+    B, HQ, HKV, D, V, P = VB.B, VB.HQ, VB.HKV, VB.D, VB.V, VB.P
+    n_q = k + 1
+    attn, q, ver, o, lse = st["attn"], st["q"], st["ver"], st["o"], st["lse"]
+    attn(q, o=o, lse=lse)
+    torch.cuda.synchronize()
+    x = o.cpu().numpy().astype(np.float64).reshape(B, n_q, HQ * D)
+
+    # (1) attention of sampled requests vs the oracle on the same pages
+    ppr = VB.S // P
+    pool = st["pool"]
+    for b in (0, 37, 63):
+        pages = np.arange(b * ppr, (b + 1) * ppr)
+        kp = pool.k[torch.from_numpy(pages).cuda()].view(torch.int16).cpu().numpy().view(np.uint16)
+        vp = pool.v[torch.from_numpy(pages).cuda()].view(torch.int16).cpu().numpy().view(np.uint16)
+        segs = np.array([(0, VB.CLOUD, 0, 0), (1, VB.EDGE, VB.CLOUD, VB.CLOUD // P),
+                         (2, VB.GEN, VB.CLOUD + VB.EDGE, (VB.CLOUD + VB.EDGE) // P)],
+                        dtype=O.SEGMENT_DTYPE)
+        qb = q[b:b + 1].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        sb = O.HostSpliceBatch(kv_dtype=O.DT_BF16, n_kv_heads=HKV, n_q_heads=HQ, d_head=D,
+                               page_tokens=P, k_pages=np.ascontiguousarray(kp),
+                               v_pages=np.ascontiguousarray(vp),
+                               seg_indptr=np.array([0, 3], np.int64), segs=segs,
+                               page_table=np.arange(ppr, dtype=np.int32),
+                               q_pos=np.array([VB.S - n_q], np.int64), q_dtype=O.DT_BF16,
+                               q=np.ascontiguousarray(qb), n_q=n_q)
+        want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4)
+        e_o = rel_err(o[b:b + 1].cpu().numpy(), want_o)
+        e_l = rel_err(lse[b:b + 1].cpu().numpy(), want_l)
+        print(f"cfg3 k={k} request {b}: attention rel err {e_o:.2e}, lse {e_l:.2e}")
+        assert e_o <= 1e-3 and e_l <= 1e-4   # fp32 output of bf16 KV: far inside 2e-2
+
+    # (2) target ids over all B * n_q rows, fp64 oracle on the GPU's rows
+    W = O.fill_uniform(O.DT_BF16, V * HQ * D, 33).reshape(V, HQ * D)   # W^T as on the device
+    W64 = np.ascontiguousarray(O.bf16_to_f64(W).T)                     # [width][vocab]
+    g_ref, _, gap = O.verify_greedy(x, W64, np.zeros((B, k), np.int32))
+    drafts = g_ref[:, :k].copy()
+    for b in range(B):
+        a = b % (k + 1)
+        if a < k:
+            drafts[b, a] = (g_ref[b, a] + 1) % V
+            drafts[b, a + 1:] = (g_ref[b, a + 1:k] + 7) % V
+    g_ref, nacc_ref, gap = O.verify_greedy(x, W64, drafts)
+    dr = torch.from_numpy(drafts.astype(np.int32)).cuda()
+    tgt, nacc, _ = ver(o, dr)                      # the timed path: logits=None
+    torch.cuda.synchronize()
+    tgt, nacc = tgt.cpu().numpy(), nacc.cpu().numpy()
+    # margin guard from the exact-logits path (a separate call)
+    _, _, lg = ver(o, dr, logits=True)
+    xn = (x - x.mean(-1, keepdims=True)) / np.sqrt(x.var(-1, keepdims=True) + 1e-5)
+    err = float(np.max(np.abs(lg.cpu().numpy().astype(np.float64) - xn @ W64)))
+    guarded = gap < 8 * err
+    print(f"cfg3 k={k}: {B * n_q} rows, max |logit err| {err:.2e}, guarded {int(guarded.sum())}")
+    assert guarded.mean() < 0.1
+    assert np.array_equal(tgt[~guarded], g_ref[~guarded])
+    checked = 0
+    for b in range(B):
+        if not guarded[b, :min(nacc_ref[b] + 1, k)].any():
+            assert nacc[b] == nacc_ref[b], (b, nacc[b], nacc_ref[b])
+            checked += 1
+    assert checked >= B - 4
+    assert sorted(set(nacc_ref.tolist())) == list(range(k + 1))
