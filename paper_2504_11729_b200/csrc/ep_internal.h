@@ -102,6 +102,7 @@ struct DecodeArgs {
     const int64_t* req_page_off;   // [batch+1]
     const WorkItem* items;
     const int32_t* cta_item_ptr;   // [n_ctas+1]
+    const int32_t* cta_item_idx;   // K1: processing order of a CTA's items (split units first), null = in order
     const int32_t* unit_item_ptr;  // [batch*Hkv+1]
     const int64_t* q_pos;          // [batch]
     const void* q;

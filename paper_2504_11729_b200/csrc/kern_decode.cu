@@ -23,11 +23,14 @@
 //     reduce-scatter (each lane ends with one (row, key) score), warp-shuffle
 //     row max, exp2 online softmax, rescale + PV with FMUL2/FFMA2. The
 //     R = group * n_q rows of one kv-head share every K/V element (GQA reuse).
-//   * end of a work item: the warps' states combine by LSE in shared memory.
-//     An item that covers its whole (request, kv-head) writes the output
-//     directly; otherwise it writes an fp32 partial, and the LAST CTA to
-//     finish a unit (per-unit arrival counter) merges the unit's partials in
-//     page = segment order (attention.cpp:116-145) — no second launch.
+//   * end of a work item: the consumer warps hand their (m, l, o) states to
+//     the epilogue warp through shared memory (an mbarrier pair) and go on
+//     with the next item at once, so the ring never stalls on an item end.
+//     The epilogue warp combines the states by LSE; an item that covers its
+//     whole (request, kv-head) writes the output directly; otherwise it
+//     writes an fp32 partial, and the LAST CTA to finish a unit (per-unit
+//     arrival counter) merges the unit's partials in page = segment order
+//     (attention.cpp:116-145) — no second launch.
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -47,7 +50,7 @@ struct DecodeCfg {
     static constexpr int E = D / 16;       // d-elements per lane
     static constexpr int KPW = 2 * J;      // keys per warp per block
     static constexpr int NCW = BT / KPW;   // consumer warps
-    static constexpr int THREADS = (NCW + 1) * 32;
+    static constexpr int THREADS = (NCW + 2) * 32;  // + producer warp + epilogue warp
     static constexpr int NV = R * J;       // partial scores per half-warp
     static constexpr int LOGN = kLog2(NV);
     static constexpr int DUP = 4 - LOGN;   // low lane bits holding duplicate slots
@@ -64,8 +67,8 @@ struct DecodeCfg {
     static constexpr int OFF_FLAG = OFF_CL + NCW * R * 4;
     static constexpr int Q_BYTES = R * D * 4;               // one item's q rows (fp32 worst case)
     static constexpr int OFF_Q = (OFF_FLAG + 16 + 127) / 128 * 128;  // [2] q slots (bulk-prefetched)
-    static constexpr int OFF_QBAR = OFF_Q + 2 * Q_BYTES;      // q_full[2], q_empty[2]
-    static constexpr int SMEM = OFF_QBAR + 4 * 8;
+    static constexpr int OFF_QBAR = OFF_Q + 2 * Q_BYTES;      // q_full[2], q_empty[2], ep_full, ep_empty
+    static constexpr int SMEM = OFF_QBAR + 6 * 8;
     static_assert((1 << LOGN) == NV && NV <= 16, "R*J must be a power of two <= 16");
     static_assert(E % 4 == 0, "vector width");
     static_assert(NCW * 32 <= 1024 - 32, "block size");
@@ -136,6 +139,101 @@ __device__ __forceinline__ void store_o(void* o, int dtype, size_t idx, float v)
         static_cast<float*>(o)[idx] = v;
 }
 
+__device__ __forceinline__ int item_at(const DecodeArgs& a, int j) {
+    return a.cta_item_idx ? a.cta_item_idx[j] : j;
+}
+
+// End of work item `it`: combines the NCW consumer warps' (m, l, o) states in
+// c_m / c_l / c_o by LSE (row r: weights 2^(m_w - M)); an item covering its
+// whole (request, kv-head) stores the output, otherwise an fp32 partial, and
+// the last CTA to finish an item of the unit (arrival counter) merges the
+// unit's partials in page = segment order (attention.cpp:116-145). Run by a
+// group of n_grp warps (gw = this warp's index in it): the epilogue warp
+// (kOneWarp) or the consumer warps. ep_empty (may be null) is arrived at once
+// the states are read.
+template <int D, int R, int NCW, bool kOneWarp>
+__device__ __forceinline__ void item_end(const DecodeArgs& a, int it, int gw, int n_grp, const float* c_o,
+                                         const float* c_m, const float* c_l, int* s_flag, uint64_t* ep_empty) {
+    constexpr int EL = D / 32;  // columns per lane
+    const int lane = threadIdx.x & 31;
+    const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv;
+    const WorkItem w = a.items[it];
+    const int unit = w.b * Hkv + w.g;
+    const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
+    const bool direct = n_items == 1;
+#pragma unroll 1
+    for (int r = gw; r < R; r += n_grp) {
+        float M = -INFINITY;
+#pragma unroll
+        for (int ww = 0; ww < NCW; ++ww) M = fmaxf(M, c_m[ww * R + r]);
+        float acc[EL];
+#pragma unroll
+        for (int e = 0; e < EL; ++e) acc[e] = 0.f;
+        float Lsum = 0.f;
+        if (M != -INFINITY) {
+#pragma unroll
+            for (int ww = 0; ww < NCW; ++ww) {
+                const float wt = fast_exp2(c_m[ww * R + r] - M);
+                Lsum += wt * c_l[ww * R + r];
+                const float* src = c_o + (ww * R + r) * D + lane * EL;
+                if constexpr (EL == 4) {
+                    const float4 v = *reinterpret_cast<const float4*>(src);
+                    acc[0] += wt * v.x; acc[1] += wt * v.y; acc[2] += wt * v.z; acc[3] += wt * v.w;
+                } else {
+                    const float2 v = *reinterpret_cast<const float2*>(src);
+                    acc[0] += wt * v.x; acc[1] += wt * v.y;
+                }
+            }
+        }
+        const bool empty_row = !(Lsum > 0.f);
+        const float inv = empty_row ? 0.f : 1.f / Lsum;
+        const float lse2 = empty_row ? -INFINITY : M + fast_log2(Lsum);
+        if (direct) {
+            if (r < w.pad) {
+                const int qi = r / G, h = w.g * G + r % G;
+                const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
+#pragma unroll
+                for (int e = 0; e < EL; ++e) store_o(a.o, a.o_dtype, orow * D + lane * EL + e, acc[e] * inv);
+                if (lane == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+            }
+        } else {
+            float* dst = a.o_part + (size_t(it) * R + r) * D + lane * EL;
+            if constexpr (EL == 4)
+                *reinterpret_cast<float4*>(dst) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+            else
+                *reinterpret_cast<float2*>(dst) = make_float2(acc[0] * inv, acc[1] * inv);
+            if (lane == 0) a.lse_part[size_t(it) * R + r] = lse2;
+        }
+    }
+    if (kOneWarp) {
+        __syncwarp();
+        if (lane == 0 && ep_empty) mbar_arrive(ep_empty);  // the consumers may overwrite c_o
+    }
+    if (direct) return;
+    // Fused K2: the last CTA to finish one of this unit's items merges them
+    // all, in page (= segment) order (attention.cpp:128-144).
+    __threadfence();
+    int last = 0;
+    if (kOneWarp) {
+        __syncwarp();
+        if (lane == 0) last = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+    } else {
+        named_bar_sync(1, n_grp * 32);
+        if (gw == 0 && lane == 0) *s_flag = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
+        named_bar_sync(1, n_grp * 32);
+        last = *s_flag;
+    }
+    if (last) {
+        __threadfence();
+        merge_unit_rows<D>(a, u0, n_items, R, w.pad, gw, n_grp, [&](int r) {
+            const int qi = r / G, h = w.g * G + r % G;
+            return (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
+        });
+        if (gw == 0 && lane == 0) a.unit_counter[unit] = 0;  // ready for the next launch
+    }
+}
+
 template <typename KV, int D, int R, int J, int S>
 __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     spliced_decode_kernel(const DecodeArgs a) {
@@ -158,7 +256,6 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     float* c_o = reinterpret_cast<float*>(smem + C::OFF_CO);
     float* c_m = reinterpret_cast<float*>(smem + C::OFF_CM);
     float* c_l = reinterpret_cast<float*>(smem + C::OFF_CL);
-    int* s_flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int it0 = a.cta_item_ptr[blockIdx.x], it1 = a.cta_item_ptr[blockIdx.x + 1];
@@ -178,6 +275,9 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     uint8_t* sq = smem + C::OFF_Q;
     uint64_t* q_full = reinterpret_cast<uint64_t*>(smem + C::OFF_QBAR);
     uint64_t* q_empty = q_full + 2;
+    uint64_t* ep_full = q_full + 4;   // consumer warps -> epilogue warp: c_o / c_m / c_l written
+    uint64_t* ep_empty = q_full + 5;  // epilogue warp -> consumers: c_o read
+    int* s_flag = reinterpret_cast<int*>(smem + C::OFF_FLAG);
     const int qsz = a.q_dtype == EP_BF16 ? 2 : 4;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -188,6 +288,8 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             mbar_init(&q_full[s], 1);
             mbar_init(&q_empty[s], NCW);
         }
+        mbar_init(ep_full, NCW);
+        mbar_init(ep_empty, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -201,12 +303,13 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const uint8_t* vp = static_cast<const uint8_t*>(a.v_pages);
             const uint8_t* zp = static_cast<const uint8_t*>(a.zero_rows);
             const int G = a.n_q_heads / Hkv;
-            for (int it = it0; it < it1; ++it) {
+            for (int j = it0; j < it1; ++j) {
+                const int it = item_at(a, j);
                 const WorkItem w = a.items[it];
                 const PageDesc* pd = a.pdesc + a.req_page_off[w.b];
                 {
                     // the item's R query rows: n_q runs of G consecutive heads
-                    const int n = it - it0, slot = n & 1;
+                    const int n = j - it0, slot = n & 1;
                     // (a prefill chunk's last item may hold fewer than n_q query tokens:
                     // w.pad = its valid rows; only those are loaded and stored)
                     const uint32_t run = uint32_t(G) * D * qsz;
@@ -243,6 +346,32 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                     }
                 }
             }
+            // every load is issued: the next kernel in the stream may be
+            // scheduled (programmatic dependent launch; it still waits for
+            // this grid's completion before reading anything it writes)
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        }
+        return;
+    }
+
+    if (warp == NCW + 1) {
+        // ============================ epilogue ============================
+        // the item ends of every item but the CTA's last (that one the
+        // consumer warps do together: nothing is left to stream behind it)
+        for (int j = it0; j < it1 - 1; ++j) {
+            const int n = j - it0, it = item_at(a, j);
+            mbar_wait(ep_full, n & 1);
+            item_end<D, R, NCW, true>(a, it, 0, 1, c_o, c_m, c_l, s_flag, ep_empty);
+            if (a.trace && lane == 0 && blockIdx.x < 1024 && n < 4) {  // debug: item end done
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                a.trace[22 * 1024 + 8 * blockIdx.x + 2 * n + 1] = t;
+            }
+        }
+        if (a.trace && lane == 0 && blockIdx.x < 1024) {  // debug: epilogue warp end (ns)
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[31 * 1024 + blockIdx.x] = t;
         }
         return;
     }
@@ -257,17 +386,18 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
 
-    for (int it = it0; it < it1; ++it) {
+    for (int j = it0; j < it1; ++j) {
+        const int it = item_at(a, j);
         const WorkItem w = a.items[it];
         const int64_t q0 = a.q_pos[w.b];
 
         // q rows of this kv-head, pre-scaled by log2(e)/sqrt(d): logical row r
         // is (query row r / G, head g*G + r % G). Physical slot rp holds
         // logical row rp ^ my_r (see the reduce-scatter below).
-        // (prefetched by the producer into q slot (it - it0) & 1; row r sits at r * D)
+        // (prefetched by the producer into q slot (j - it0) & 1; row r sits at r * D)
         float2 q2[R][E / 2];
         {
-            const int n = it - it0, slot = n & 1;
+            const int n = j - it0, slot = n & 1;
             mbar_wait(&q_full[slot], (n >> 1) & 1);
             const uint8_t* qs = sq + slot * C::Q_BYTES;
 #pragma unroll
@@ -386,12 +516,12 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             }
         }
 
-        if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && it - it0 < 4) {  // debug: item's last block done
+        if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && j - it0 < 4) {  // debug: item's last block done
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (it - it0)] = t;
+            a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (j - it0)] = t;
         }
-        // ---- combine the two halves, then the NCW warps, by LSE ----
+        // ---- combine the two halves, then hand the warp's state to the epilogue warp ----
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -404,6 +534,8 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
         for (int msk = 1 << DUP; msk < (J << DUP); msk <<= 1)
             l_row += __shfl_xor_sync(0xffffffffu, l_row, msk);
         l_row += __shfl_xor_sync(0xffffffffu, l_row, 16);
+        mbar_wait(ep_empty, ((j - it0) & 1) ^ 1);  // the epilogue warp has read the previous item's states
+        const bool last_item = j == it1 - 1;
         if (lane < 16) {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -415,61 +547,18 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                 c_l[warp * R + my_r] = l_row;
             }
         }
-        named_bar_sync(1, NCW * 32);
-
-        const int unit = w.b * Hkv + w.g;
-        const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
-        const bool direct = n_items == 1;
-        for (int idx = threadIdx.x; idx < R * D; idx += NCW * 32) {
-            const int r = idx / D, c = idx % D;
-            float M = -INFINITY;
-#pragma unroll
-            for (int ww = 0; ww < NCW; ++ww) M = fmaxf(M, c_m[ww * R + r]);
-            float Lsum = 0.f, acc = 0.f;
-            if (M != -INFINITY) {
-#pragma unroll
-                for (int ww = 0; ww < NCW; ++ww) {
-                    const float wt = fast_exp2(c_m[ww * R + r] - M);
-                    Lsum += wt * c_l[ww * R + r];
-                    acc += wt * c_o[(ww * R + r) * D + c];
-                }
-            }
-            const bool empty_row = !(Lsum > 0.f);
-            const float val = empty_row ? 0.f : acc / Lsum;
-            const float lse2 = empty_row ? -INFINITY : M + fast_log2(Lsum);
-            if (direct) {
-                if (r < w.pad) {
-                    const int qi = r / G, h = w.g * G + r % G;
-                    const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
-                    store_o(a.o, a.o_dtype, orow * D + c, val);
-                    if (c == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
-                }
-            } else {
-                a.o_part[(size_t(it) * R + r) * D + c] = val;
-                if (c == 0) a.lse_part[size_t(it) * R + r] = lse2;
-            }
-        }
-        if (!direct) {
-            // Fused K2: the last CTA to finish one of this unit's items merges
-            // them all, in page (= segment) order (attention.cpp:128-144).
-            __threadfence();
+        if (last_item) {
+            // nothing left to stream: all consumer warps do this item end
             named_bar_sync(1, NCW * 32);
-            if (threadIdx.x == 0) *s_flag = atomicAdd(&a.unit_counter[unit], 1) == n_items - 1;
-            named_bar_sync(1, NCW * 32);
-            if (*s_flag) {
-                __threadfence();
-                merge_unit_rows<D>(a, u0, n_items, R, w.pad, warp, NCW, [&](int r) {
-                    const int qi = r / G, h = w.g * G + r % G;
-                    return (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
-                });
-                if (threadIdx.x == 0) a.unit_counter[unit] = 0;  // ready for the next launch
+            item_end<D, R, NCW, false>(a, it, warp, NCW, c_o, c_m, c_l, s_flag, nullptr);
+            if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && j - it0 < 4) {  // debug: item end done
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (j - it0) + 1] = t;
             }
-        }
-        named_bar_sync(1, NCW * 32);
-        if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024 && it - it0 < 4) {  // debug: item end done
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            a.trace[22 * 1024 + 8 * blockIdx.x + 2 * (it - it0) + 1] = t;
+        } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ep_full);
         }
     }
     if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // debug: per-CTA end (ns)

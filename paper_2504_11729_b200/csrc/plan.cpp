@@ -90,14 +90,15 @@ int64_t tc_item_weight(int rows) {
     if (env >= 0) return env;
     return rows > 64 ? 14 : kTcItemWeight;
 }
-// K1 (CUDA-core decode) item overhead in blocks: q rows, the 8-warp LSE
-// combine and, for a split unit, the partial store + arrival + merge. The
-// per-CTA trace puts a third item at ~8 us on cfg2; sweeping 0-12 blocks:
-// cfg5's ragged private pass 0.321 -> 0.296 ms at 4, cfg2 unchanged.
+// K1 (CUDA-core decode) item overhead in blocks. Item ends run on K1's
+// epilogue warp behind the streaming, so an item costs the consumers little:
+// sweeping 0/1/2/4 blocks on config 2 gave 101.7 / 102.0 / 102.1 / 103.6 us
+// (config 5 flat at 0.265 ms). (Before the epilogue warp the 8-warp item end
+// stalled the ring and 4 was best: cfg5 0.321 -> 0.296 ms.)
 int64_t k1_item_weight() {
     static const int64_t w = [] {
         const char* e = std::getenv("EP_K1_ITEM_WEIGHT");
-        return e ? std::atoll(e) : int64_t(4);
+        return e ? std::atoll(e) : int64_t(0);
     }();
     return w;
 }
@@ -118,8 +119,8 @@ struct SubPlan {
     std::vector<PageDesc> pdesc;
     std::vector<int64_t> req_page_off;
     std::vector<WorkItem> items;
-    std::vector<int32_t> cta_item_ptr, unit_item_ptr;
-    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_opart, d_lsepart, d_counter;
+    std::vector<int32_t> cta_item_ptr, unit_item_ptr, cta_item_idx;
+    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_opart, d_lsepart, d_counter, d_cta_idx;
     size_t counter_units = 0;
 };
 
@@ -193,6 +194,20 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
     for (int64_t u = 0; u < sp.n_units; ++u) {
         if (sp.unit_item_ptr[u + 1] == 0) sp.has_empty_unit = true;
         sp.unit_item_ptr[u + 1] += sp.unit_item_ptr[u];
+    }
+    // K1 order within a CTA: items of split units first, whole units last.
+    // A split item's end (partial store, arrival, maybe the merge) then runs
+    // on the epilogue warp while the CTA streams on, and the CTA's final item
+    // end — the one nothing overlaps — is a plain output store where possible.
+    sp.cta_item_idx.resize(sp.items.size());
+    for (int64_t c = 0; c < sp.n_ctas; ++c) {
+        int32_t o = sp.cta_item_ptr[c];
+        for (int pass = 0; pass < 2; ++pass)
+            for (int32_t it = sp.cta_item_ptr[c]; it < sp.cta_item_ptr[c + 1]; ++it) {
+                const int64_t unit = int64_t(sp.items[it].b) * Hkv + sp.items[it].g;
+                const bool split = sp.unit_item_ptr[unit + 1] - sp.unit_item_ptr[unit] > 1;
+                if (split == (pass == 0)) sp.cta_item_idx[o++] = it;
+            }
     }
 }
 
@@ -430,6 +445,7 @@ int upload_subplan(SubPlan& sp, int d_head, cudaStream_t s, std::vector<std::pai
     parts.push_back({&sp.d_items, {sp.items.data(), bytes_of(sp.items)}});
     parts.push_back({&sp.d_cta_ptr, {sp.cta_item_ptr.data(), bytes_of(sp.cta_item_ptr)}});
     parts.push_back({&sp.d_unit_ptr, {sp.unit_item_ptr.data(), bytes_of(sp.unit_item_ptr)}});
+    parts.push_back({&sp.d_cta_idx, {sp.cta_item_idx.data(), bytes_of(sp.cta_item_idx)}});
     const size_t ws = size_t(std::max<int64_t>(sp.n_items, 1)) * sp.rows;
     EP_CUDA_TRY(sp.d_opart.reserve(ws * d_head * sizeof(float)), "ep_plan workspace");
     EP_CUDA_TRY(sp.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
@@ -504,6 +520,7 @@ DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* po
     a.req_page_off = static_cast<const int64_t*>(sp.d_req_off.ptr);
     a.items = static_cast<const WorkItem*>(sp.d_items.ptr);
     a.cta_item_ptr = static_cast<const int32_t*>(sp.d_cta_ptr.ptr);
+    a.cta_item_idx = sp.tc ? nullptr : static_cast<const int32_t*>(sp.d_cta_idx.ptr);
     a.unit_item_ptr = static_cast<const int32_t*>(sp.d_unit_ptr.ptr);
     a.q_pos = static_cast<const int64_t*>(p.d_qpos.ptr);
     a.q = q;
@@ -528,8 +545,8 @@ unsigned long long* trace_buffer() {
     static unsigned long long* t = [] {
         unsigned long long* b = nullptr;
         const char* e = std::getenv("EP_TRACE");
-        if (e && e[0] == '1' && cudaMalloc(&b, 31 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
-            cudaMemset(b, 0, 31 * 1024 * sizeof(unsigned long long));
+        if (e && e[0] == '1' && cudaMalloc(&b, 32 * 1024 * sizeof(unsigned long long)) == cudaSuccess)
+            cudaMemset(b, 0, 32 * 1024 * sizeof(unsigned long long));
         return b;
     }();
     return t;
@@ -538,7 +555,7 @@ unsigned long long* trace_buffer() {
 // debug: EP_TRACE=1 dumps the trace buffer (CTA 0 event clocks, per-CTA
 // start / end / work) of the last launch to EP_TRACE_FILE
 void dump_trace(unsigned long long* trace, cudaStream_t s) {
-    std::vector<unsigned long long> host(31 * 1024);
+    std::vector<unsigned long long> host(32 * 1024);
     cudaStreamSynchronize(s);
     cudaMemcpy(host.data(), trace, host.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     const char* f = std::getenv("EP_TRACE_FILE");

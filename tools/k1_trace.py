@@ -21,6 +21,10 @@ def main(path):
     wk = raw[20 * NB:22 * NB].reshape(NB, 2)[:n]
     ev = raw[22 * NB:30 * NB].reshape(NB, 4, 2)[:n]
     sm = raw[30 * NB:31 * NB][:n] if raw.size >= 31 * NB else np.zeros(n, np.int64)
+    if raw.size >= 32 * NB:  # the epilogue warp may finish after the consumers
+        ep_end = raw[31 * NB:32 * NB][:n]
+        se = se.copy()
+        se[:, 1] = np.maximum(se[:, 1], ep_end)
     t0 = se[:, 0].min()
     start = (se[:, 0] - t0) / 1e3
     end = (se[:, 1] - t0) / 1e3
