@@ -83,6 +83,23 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
                      const int32_t* page_table, const int32_t* n_new, const int32_t* tokens,
                      void* hidden, void* logits, int32_t* next, ep_stream stream);
 
+/* Greedy speculative verify on the decoder: per request
+ * b, tokens [sum n_new] holds [last, d1..dk] (k = n_new[b] - 1) at the LAST
+ * n_new[b] positions of its splice table — the reference's construction,
+ * prefill(model, [last, d1..dk], generated, end_position, cache)
+ * (model.cpp:211-236) — and every new row is unembedded and argmaxed
+ * (unembed_logits + argmax_token, model.cpp:238-255):
+ *   targets:    device int32 [sum n_new], g_j of row j (ties -> lowest id)
+ *   n_accepted: device int32 [batch], the largest n <= k with d_i == g_{i-1}
+ *               for all i <= n (emit d1..dn, then the bonus token g_n)
+ *   logits:     NULL or device [sum n_new][vocab] (model dtype)
+ * The K/V of all k+1 rows are written into their slots; a caller that keeps
+ * n accepted drafts keeps positions up to last + n (the rest are rewritten by
+ * later steps). Errors as ep_model_forward. */
+int ep_model_verify(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                    const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* logits,
+                    int32_t* targets, int32_t* n_accepted, ep_stream stream);
+
 /* decode_greedy (model.cpp:285-297) resident on the device: for every request
  * b, the LAST n_steps positions of its splice table (a trailing generated
  * segment the caller has reserved) are decoded autoregressively — the first

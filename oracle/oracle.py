@@ -146,6 +146,8 @@ def _load(impl: str) -> C.CDLL:
         lib.epref_session_first_token.argtypes = [C.c_void_p, C.POINTER(C.c_uint32)]
         lib.epref_session_decode_step.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p,
                                                   C.POINTER(C.c_uint32)]
+        lib.epref_session_verify.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p,
+                                             C.c_void_p]
         if hasattr(lib, "epref_kv_frame_encode"):
             lib.epref_kv_frame_encode.restype = C.c_size_t
             lib.epref_kv_frame_encode.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -515,6 +517,20 @@ class RefSession:
         t = C.c_uint32()
         _raise(self.lib.epref_session_first_token(self.h, C.byref(t)), "first_token", self.lib)
         return t.value
+
+    def verify(self, tokens):
+        """(targets [n], logits [n][V]): the reference's prefill of ``tokens``
+        ([last, d1..dk]) as a generated segment at the cache end, then
+        unembed_logits + argmax_token per row. The session's
+        cache is unchanged."""
+        t = np.ascontiguousarray(tokens, dtype=np.uint32)
+        V = self.m.cfg["vocab"]
+        logits = np.zeros((t.size, V))
+        tg = np.zeros(t.size, dtype=np.uint32)
+        rc = self.lib.epref_session_verify(self.h, t.ctypes.data, t.size, logits.ctypes.data,
+                                           tg.ctypes.data)
+        _raise(rc, "verify", self.lib)
+        return tg.astype(np.int64), logits
 
     def decode_step(self, last: int):
         logits = np.zeros(self.m.cfg["vocab"])

@@ -390,6 +390,25 @@ int epref_session_decode_step(void* s, std::uint32_t last, double* logits, std::
     });
 }
 
+// Speculative verify as SURVEY §8a a16 constructs it from the reference's own
+// functions: prefill (model.cpp:211-236) of [last, d1..dk] as a generated
+// segment at the cache end, then unembed_logits + argmax_token per row
+// (model.cpp:238-255). The session's cache is left unchanged (prefill returns
+// its segment; it is dropped here).
+int epref_session_verify(const void* s, const std::uint32_t* toks, std::size_t n, double* logits,
+                         std::uint32_t* targets) {
+    return guarded([&] {
+        const Session* ss = static_cast<const Session*>(s);
+        PrefillResult r = prefill(*ss->model, std::vector<TokenId>(toks, toks + n), SegmentOrigin::generated,
+                                  ss->cache.end_position(), ss->cache);
+        const std::size_t V = ss->model->config.vocab_size;
+        for (std::size_t i = 0; i < n; ++i) {
+            auto lg = unembed_logits(*ss->model, r.hidden.row(i));
+            if (logits) std::copy(lg.begin(), lg.end(), logits + i * V);
+            targets[i] = argmax_token(lg);
+        }
+    });
+}
 
 // ---------------------------------------------------------------- wire --
 // The reference's own EPKV codec (wire.cpp): encode a kv frame, decode any

@@ -157,6 +157,7 @@ _SIGS.update({
     "ep_model_forward": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                    _vp]),
     "ep_model_generate": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, C.c_int32, _vp, _vp, _vp]),
+    "ep_model_verify": (C.c_int, [_vp, C.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "ep_model_last_attention_path": (C.c_int, [_vp]),
 })
 

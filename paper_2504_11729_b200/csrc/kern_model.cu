@@ -765,6 +765,23 @@ cudaError_t launch_attention_generic(int dt, int kv_dtype, const void* q, int n,
     return cudaErrorInvalidValue;
 }
 
+__global__ void accept_rows_kernel(const int32_t* tokens, const int32_t* targets, const int32_t* last_row,
+                                   int batch, int32_t* n_accepted) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    const int r0 = b == 0 ? 0 : last_row[b - 1] + 1, r1 = last_row[b];
+    int n = 0;
+    while (r0 + n + 1 <= r1 && tokens[r0 + n + 1] == targets[r0 + n]) ++n;
+    n_accepted[b] = n;
+}
+
+cudaError_t launch_accept_rows(const int32_t* tokens, const int32_t* targets, const int32_t* last_row, int batch,
+                               int32_t* n_accepted, cudaStream_t s) {
+    if (batch <= 0) return cudaSuccess;
+    accept_rows_kernel<<<(batch + 127) / 128, 128, 0, s>>>(tokens, targets, last_row, batch, n_accepted);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, const int32_t* step,
                                int32_t* next, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;

@@ -163,8 +163,9 @@ int reserve_ws(ep_model m, int n, int batch) {
     EP_CUDA_TRY(m->qbuf.reserve(size_t(n) * m->D * es), "ep_model ws");
     EP_CUDA_TRY(m->attn.reserve(size_t(n) * m->D * es), "ep_model ws");
     EP_CUDA_TRY(m->h1.reserve(size_t(n) * m->F * es), "ep_model ws");
-    EP_CUDA_TRY(m->logits_ws.reserve(size_t(batch) * m->V * es), "ep_model ws");
-    EP_CUDA_TRY(m->next_ws.reserve(size_t(batch) * sizeof(int32_t)), "ep_model ws");
+    // (verify unembeds every row: n >= batch rows of logits / next ids)
+    EP_CUDA_TRY(m->logits_ws.reserve(size_t(std::max(n, batch)) * m->V * es), "ep_model ws");
+    EP_CUDA_TRY(m->next_ws.reserve(size_t(std::max(n, batch)) * sizeof(int32_t)), "ep_model ws");
     return EP_OK;
 }
 
@@ -187,6 +188,7 @@ struct Pass {
     int32_t* next = nullptr;
     bool advance = false;       // rollout: step += 1, adv_qpos[0..batch) += 1 after the argmax
     int64_t* adv_qpos = nullptr;
+    bool all_rows = false;      // verify: unembed + argmax every new row (logits [n][V], next [n])
 };
 
 // Metadata upload: one pinned staging buffer, one async copy; fills the
@@ -322,8 +324,8 @@ int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
     // unembed_logits of each request's last row (model.cpp:238-246) + argmax
     DenseArgs u{};
     u.x = m->hid.ptr;
-    u.row_map = ps.last_row;
-    u.n = ps.batch;
+    u.row_map = ps.all_rows ? nullptr : ps.last_row;
+    u.n = ps.all_rows ? ps.n : ps.batch;
     u.K = m->D;
     u.N = m->V;
     u.w[0] = m->wptr(m->off_unembed);
@@ -344,7 +346,7 @@ int enqueue_pass(ep_model m, const Pass& ps, cudaStream_t s) {
     }
     EP_CUDA_TRY(launch_dense(dt, kEpiStore, true, u, s), "unembed launch");
     h->launches++;
-    EP_CUDA_TRY(launch_argmax_rows(dt, ps.logits, ps.batch, m->V, ps.step, ps.next, s), "argmax launch");
+    EP_CUDA_TRY(launch_argmax_rows(dt, ps.logits, u.n, m->V, ps.step, ps.next, s), "argmax launch");
     h->launches++;
     if (ps.advance) {
         EP_CUDA_TRY(launch_advance(const_cast<int32_t*>(ps.step), ps.adv_qpos, ps.batch, s), "advance launch");
@@ -631,13 +633,15 @@ int run_persist(ep_model m, const std::vector<Req>& reqs, const Pass& ps, int ba
     return EP_OK;
 }
 
-int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
-                     const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* hidden,
-                     void* logits, int32_t* next, ep_stream stream) {
-    if (!m || !seg_indptr || !n_new || !tokens || (batch > 0 && (!segs || !page_table)))
-        return fail(EP_EINVAL, "ep_model_forward: null argument");
-    if (batch < 0) return fail(EP_EINVAL, "ep_model_forward: batch");
-    if (batch == 0) return EP_OK;
+}  // extern "C"
+
+namespace {
+
+// ep_model_forward, and with all_rows the verify pass of ep_model_verify
+// (every new row unembedded, the acceptance rule per request).
+int forward_impl(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                 const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* hidden,
+                 void* logits, int32_t* next, bool all_rows, int32_t* n_accepted, ep_stream stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     EP_CUDA_TRY(cudaSetDevice(m->h->device), "ep_model_forward");
 
@@ -673,7 +677,7 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
     // decode_step of one session of a small fp32 model: the K9 persistent
     // kernel (one launch for the whole forward)
     int persist_ctas = 0;
-    if (all_decode && !hidden && use_persist(m, batch, &persist_ctas))
+    if (all_decode && !hidden && !all_rows && use_persist(m, batch, &persist_ctas))
         return run_persist(m, reqs, ps, batch, 1, persist_ctas,
                            next ? next : static_cast<int32_t*>(m->next_ws.ptr), logits, s);
 
@@ -712,11 +716,45 @@ int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const
     m->last_path = ps.plan ? 1 : 2;
     ps.logits = logits ? logits : m->logits_ws.ptr;
     ps.next = next ? next : static_cast<int32_t*>(m->next_ws.ptr);
+    ps.all_rows = all_rows;
     if (int rc = enqueue_pass(m, ps, s)) return rc;
+    if (all_rows) {
+        // the acceptance rule per request over its rows' targets (fused
+        // accept of speculative verify)
+        EP_CUDA_TRY(launch_accept_rows(ps.tok, ps.next, ps.last_row, batch, n_accepted, s), "accept launch");
+        m->h->launches++;
+    }
     if (hidden)
         EP_CUDA_TRY(cudaMemcpyAsync(hidden, m->hid.ptr, size_t(n) * m->D * m->esz(), cudaMemcpyDeviceToDevice, s),
                     "ep_model_forward hidden copy");
     return EP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ep_model_forward(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                     const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* hidden,
+                     void* logits, int32_t* next, ep_stream stream) {
+    if (!m || !seg_indptr || !n_new || !tokens || (batch > 0 && (!segs || !page_table)))
+        return fail(EP_EINVAL, "ep_model_forward: null argument");
+    if (batch < 0) return fail(EP_EINVAL, "ep_model_forward: batch");
+    if (batch == 0) return EP_OK;
+    return forward_impl(m, batch, seg_indptr, segs, page_table, n_new, tokens, hidden, logits, next, false,
+                        nullptr, stream);
+}
+
+int ep_model_verify(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,
+                    const int32_t* page_table, const int32_t* n_new, const int32_t* tokens, void* logits,
+                    int32_t* targets, int32_t* n_accepted, ep_stream stream) {
+    if (!m || !seg_indptr || !n_new || !tokens || !targets || !n_accepted ||
+        (batch > 0 && (!segs || !page_table)))
+        return fail(EP_EINVAL, "ep_model_verify: null argument");
+    if (batch < 0) return fail(EP_EINVAL, "ep_model_verify: batch");
+    if (batch == 0) return EP_OK;
+    return forward_impl(m, batch, seg_indptr, segs, page_table, n_new, tokens, nullptr, logits, targets, true,
+                        n_accepted, stream);
 }
 
 int ep_model_generate(ep_model m, int32_t batch, const int64_t* seg_indptr, const ep_segment* segs,

@@ -88,6 +88,11 @@ cudaError_t launch_attention_generic(int dt, int kv_dtype, const void* q, int n,
 
 // argmax_token (model.cpp:248-255) per row of logits [rows][V]: the first
 // index of the maximum, into next[rows] (next[step * rows + r] in a rollout).
+// Speculative verify's acceptance rule per request (model.cpp-built a16): the
+// request's rows are [prev_last + 1, last_row[b]] (tokens [last, d1..dk]);
+// n_accepted[b] = longest n with d_i == target[row_{i-1}] for all i <= n.
+cudaError_t launch_accept_rows(const int32_t* tokens, const int32_t* targets, const int32_t* last_row, int batch,
+                               int32_t* n_accepted, cudaStream_t s);
 cudaError_t launch_argmax_rows(int dt, const void* logits, int rows, int V, const int32_t* step,
                                int32_t* next, cudaStream_t s);
 

@@ -156,6 +156,30 @@ class Model:
                                      nxt.data_ptr(), s.cuda_stream), "forward")
         return nxt, logits, hidden
 
+    def verify(self, tables, n_new, tokens, *, want_logits=False, stream=None):
+        """ep_model_verify: per request the last n_new[b] positions hold
+        [last, d1..dk] (tokens, request-major). Returns (targets [sum n_new]
+        int32, n_accepted [B] int32, logits [sum n_new][V] or None) as cuda
+        tensors."""
+        torch = _torch()
+        B = len(tables)
+        indptr, segs, pt = _batch_arrays(tables)
+        nn = np.ascontiguousarray(n_new, dtype=np.int32)
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.size != int(nn.sum()):
+            raise InvalidArgument("verify: len(tokens) != sum(n_new)")
+        dev = f"cuda:{self.device}"
+        tgt = torch.empty(int(nn.sum()), dtype=torch.int32, device=dev)
+        nacc = torch.empty(B, dtype=torch.int32, device=dev)
+        logits = (torch.empty((int(nn.sum()), self.config.vocab_size), dtype=self.tdtype, device=dev)
+                  if want_logits else None)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().ep_model_verify(self._m, B, indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
+                                    nn.ctypes.data, tok.ctypes.data,
+                                    logits.data_ptr() if logits is not None else None,
+                                    tgt.data_ptr(), nacc.data_ptr(), s.cuda_stream), "verify")
+        return tgt, nacc, logits
+
     def generate(self, tables, n_steps: int, first_tokens, *, stream=None):
         """ep_model_generate: the last n_steps positions of every table are
         decoded on the device (one CUDA graph per step, replayed). Returns
@@ -380,6 +404,48 @@ def decode_batch(model: Model, caches, last_tokens, *, want_logits: bool = False
     if logits is None:
         return _to_host(model, nxt).copy(), None
     return nxt.cpu().numpy(), logits.cpu().numpy()
+
+
+@dataclass
+class VerifyResult:
+    """Greedy speculative verify of one session: the accepted drafts
+    d1..dn, the bonus token g_n (the next ``last`` token), every row's target
+    g_0..g_k and, if asked, the rows' logits."""
+    accepted: list
+    next_token: int
+    targets: np.ndarray
+    logits: object = None
+
+
+def verify_greedy(model: Model, cache: SegmentedCache, last_token: int, drafts, *,
+                  want_logits: bool = False) -> VerifyResult:
+    """Speculative verify as SURVEY §8a a16 builds it from the reference:
+    prefill(model, [last, d1..dk], generated, end_position, cache)
+    (model.cpp:211-236), then unembed_logits + argmax_token per row
+    (model.cpp:238-255); n = the longest draft prefix the targets reproduce.
+    The cache keeps the K/V of last, d1..dn — as n + 1 decode_step calls
+    would — and the bonus token g_n is returned as the next token."""
+    drafts = [int(d) for d in drafts]
+    toks = [int(last_token)] + drafts
+    if cache.empty():
+        raise InvalidArgument("verify: empty cache")
+    issue = cache.check_consistent()
+    if issue:
+        raise InvalidArgument(f"verify: inconsistent cache: {issue}")
+    if cache.end_position() + len(toks) > model.config.max_positions:
+        raise InvalidArgument("embed: positions overflow max_positions")
+    _check_tokens(model, toks)
+    cache._grow_generated(len(toks))
+    try:
+        tgt, nacc, logits = model.verify([cache.segments], [len(toks)], toks, want_logits=want_logits)
+        tgt = tgt.cpu().numpy()
+        n = int(nacc.cpu().numpy()[0])
+    except Exception:
+        cache._shrink_generated(len(toks))
+        raise
+    cache._shrink_generated(len(drafts) - n)   # keep last, d1..dn
+    return VerifyResult(drafts[:n], int(tgt[n]), tgt,
+                        logits.cpu().numpy() if logits is not None else None)
 
 
 def _to_host(model: Model, t):

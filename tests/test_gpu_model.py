@@ -395,3 +395,73 @@ def test_persistent_rollout_other_shapes(cuda_handle, cfg, n_cloud, monkeypatch)
     assert t1 == t0
     assert rel_err(l1, l0) <= 1e-5
     assert o1.next_token == o0.next_token and rel_err(o1.logits, o0.logits) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype,kv", [("f64", "f64"), ("f32", "f32")])
+def test_verify_matches_reference_prefill(cuda_handle, dtype, kv):
+    """Greedy speculative verify on config 1's decoder (the
+    rest of it): per round, [last, d1..dk] (k = 4 / 8, drafts from the
+    reference's own rollout with a forced mismatch at a varying place) go
+    through ep_model_verify; every row's target must equal the reference's
+    own construction — prefill(model, [last, d1..dk], generated, end, cache)
+    + unembed_logits + argmax_token per row (oracle/_ref, unmodified
+    sources) — and the accepted count its acceptance rule. fp64: bit-exact
+    everywhere; fp32: logits within 1e-3 and ids bit-exact outside the
+    margin guard. The cache then keeps last, d1..dn, so the rounds stay in
+    step with a reference session advanced by n + 1 decode_steps."""
+    M = _mod()
+    if not O.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    m = make(CFG1, dtype, kv, num_pages=64)
+    cloud, edge = GOLD["cfg1_cloud"], GOLD["cfg1_edge"]
+    ref = O.RefModel(*CFG1[:4], max_positions=CFG1[4], seed=CFG1[5])
+    ses = ref.session(cloud, edge)
+    cache = M.SegmentedCache(m)
+    pf = M.prefill(m, cloud, M.ORIGIN_CLOUD, 0, cache, want_hidden=False)
+    cache.append(pf.segments)
+    pf = M.prefill(m, edge, M.ORIGIN_EDGE, len(cloud), cache, want_hidden=False)
+    cache.append(pf.segments)
+    last = ses.first_token()
+    assert pf.next_token == last
+    roll = list(GOLD["cfg1_rollout64"])  # the reference's greedy continuation (roll[0] == last)
+    assert roll[0] == last
+    pos = 0                                 # index of `last` in roll
+    checked, guarded = 0, 0
+    for rnd, (k, a) in enumerate([(4, 4), (4, 1), (8, 0), (8, 5), (4, 2), (8, 8), (4, 3)]):
+        drafts = list(roll[pos + 1:pos + 1 + k])
+        if a < k:                           # force the first mismatch at draft a+1
+            drafts[a] = (drafts[a] + 1) % CFG1[3]
+        want_t, want_lg = ses.verify([last] + drafts)
+        want_n = 0
+        while want_n < k and drafts[want_n] == want_t[want_n]:
+            want_n += 1
+        r = M.verify_greedy(m, cache, last, drafts, want_logits=True)
+        err = rel_err(r.logits, want_lg)
+        if dtype == "f64":
+            assert err <= 1e-9
+            assert np.array_equal(r.targets, want_t), (rnd, r.targets, want_t)
+            assert len(r.accepted) == want_n
+        else:
+            assert err <= 1e-3, err
+            top2 = np.sort(want_lg, axis=1)[:, -2:]
+            safe = (top2[:, 1] - top2[:, 0]) > 4 * err * np.maximum(1.0, np.abs(top2[:, 1]))
+            guarded += int((~safe).sum())
+            assert np.array_equal(r.targets[safe], want_t[safe]), (rnd, r.targets, want_t)
+            if safe[:want_n + 1].all():
+                assert len(r.accepted) == want_n
+        assert r.next_token == want_t[len(r.accepted)]
+        checked += k + 1
+        # the reference session takes last, d1..dn as n + 1 decode steps
+        n = len(r.accepted)
+        for t in [last] + drafts[:n]:
+            ses.decode_step(t)
+        assert cache.end_position() == ses.end_position
+        last = r.next_token
+        pos += n + 1
+        assert roll[pos] == last            # accepted + bonus = the greedy rollout
+    # a decode step after the verify rounds still matches the reference
+    d = M.decode_step(m, cache, last)
+    nt, _ = ses.decode_step(last)
+    assert d.next_token == nt
+    cache.release()
+    assert guarded <= checked // 10
