@@ -118,7 +118,9 @@ struct DecodeArgs {
     int32_t* unit_counter;    // [batch*Hkv], zero between launches (fused K2)
     unsigned long long* trace;  // optional clock64 event trace of CTA 0 (debug, may be null)
     int32_t reqs_per_unit;    // K3: consecutive requests whose rows share one tile (cascade), else 1
-    const int32_t* q_row0;    // per (virtual) request: first q/o token row; null = b * n_q
+    const int32_t* q_row0;    // per (virtual) request: first q/o token row; null = b * n_q (or chunks below)
+    int32_t chunks;           // decode plans with more rows than K1 takes: each request's nq_total query
+    int32_t nq_total;         // tokens cut into `chunks` virtual requests of n_q tokens (1 = not cut)
     int32_t pv_parts;         // K3: P as bf16 hi+lo (2) or bf16 (1)
 };
 
@@ -137,7 +139,19 @@ int64_t* plan_qpos_dev(ep_plan p);
 // First q/o token row of (virtual) request b: prefill plans cut one request's
 // queries into chunks that are separate virtual requests.
 __host__ __device__ inline size_t q_row_base(const DecodeArgs& a, int b) {
-    return a.q_row0 ? size_t(a.q_row0[b]) : size_t(b) * a.n_q;
+    if (a.q_row0) return size_t(a.q_row0[b]);
+    if (a.chunks > 1) return size_t(b / a.chunks) * a.nq_total + size_t(b % a.chunks) * a.n_q;
+    return size_t(b) * a.n_q;
+}
+
+// Valid query rows (group * tokens) of (virtual) request b of a decode plan.
+__host__ __device__ inline int valid_rows(const DecodeArgs& a, int b) {
+    const int G = a.n_q_heads / a.n_kv_heads;
+    if (a.chunks > 1) {
+        const int left = a.nq_total - (b % a.chunks) * a.n_q;
+        return G * (left < a.n_q ? left : a.n_q);
+    }
+    return G * a.n_q;
 }
 
 // TMA tensor maps over bf16 row-major matrices (capi.cpp).
@@ -152,8 +166,12 @@ cudaError_t launch_cascade_merge(int rows, int d, int row_per_req, const float* 
                                  const float* lse_parts, const uint8_t* has_shared, void* o,
                                  int o_dtype, float* lse, cudaStream_t s);
 
-// R = rows per (request, kv-head) = group * n_q.
+// R = rows per (request, kv-head) = group * n_q; K1 pads it to a power of two.
 bool decode_supported(int kv_dtype, int d_head, int rows);
+// Any f32 / bf16 shape with d_head <= 256 (the generic kernel behind K1 / K3).
+bool generic_supported(int kv_dtype, int d_head);
+cudaError_t launch_generic_decode(int kv_dtype, int d_head, int batch, int n_q, const DecodeArgs& a,
+                                  cudaStream_t s);
 int decode_ctas_per_sm(int kv_dtype, int d_head, int rows);
 cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas,
                                   const DecodeArgs& a, cudaStream_t s);

@@ -575,6 +575,7 @@ __global__ void empty_units_kernel(const DecodeArgs a, int D, int R) {
     if (a.unit_item_ptr[unit + 1] != a.unit_item_ptr[unit]) return;
     const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv;
     const int b = unit / Hkv, g = unit % Hkv;
+    if (!a.q_row0) R = min(R, valid_rows(a, b));  // K1 pads R to a power of two
     for (int idx = threadIdx.x; idx < R * D; idx += blockDim.x) {
         const int r = idx / D, c = idx % D;
         const int qi = r / G, h = g * G + r % G;
@@ -625,6 +626,8 @@ cudaError_t launch_decode_t(int n_ctas, const DecodeArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// rows: the plan's row stride (a power of two; the valid rows of a unit
+// are its items' pad, the rest are zero-q rows that are never stored)
 template <typename KV, int D>
 cudaError_t dispatch_rows(int rows, int n_ctas, const DecodeArgs& a, cudaStream_t s) {
     switch (rows) {
@@ -636,17 +639,137 @@ cudaError_t dispatch_rows(int rows, int n_ctas, const DecodeArgs& a, cudaStream_
     }
 }
 
+// ------------------------------------------------------------ generic ----
+// Shapes outside K1 / K3 (d_head not 64 / 128, or more than 8 query heads per
+// kv head outside K3): one CTA per (request, query token, query head) row,
+// its four warps taking the request's pages round-robin with one online
+// softmax each (lane = key for q.k, lane = columns for p.v), merged by LSE
+// at the end — partial_attention + merge_partials (attention.cpp:80-145)
+// with GQA as kv-head indexing. Correct for every shape; not tuned.
+constexpr int kGenWarps = 4;
+constexpr int kGenPerLane = 8;  // d_head <= 256
+
+template <typename KV>
+__device__ __forceinline__ float kvf(const KV* p, size_t i) {
+    if constexpr (sizeof(KV) == 2)
+        return __bfloat162float(p[i]);
+    else
+        return p[i];
+}
+
+template <typename KV>
+__global__ void __launch_bounds__(kGenWarps * 32) generic_decode_kernel(const DecodeArgs a, int D) {
+    const int b = blockIdx.x, qi = blockIdx.y, h = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv, g = h / G, P = a.page_tokens;
+    extern __shared__ __align__(16) float gsm[];
+    float* qs = gsm;            // [D], pre-scaled by log2(e) / sqrt(d)
+    float* wo = qs + D;         // [warps][D]
+    __shared__ float wm[kGenWarps], wl[kGenWarps];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const size_t row = (q_row_base(a, b) + qi) * a.n_q_heads + h;
+    for (int c = tid; c < D; c += blockDim.x)
+        qs[c] = (a.q_dtype == EP_BF16 ? __bfloat162float(static_cast<const __nv_bfloat16*>(a.q)[row * D + c])
+                                      : static_cast<const float*>(a.q)[row * D + c]) *
+                a.q_scale;
+    __syncthreads();
+    const int64_t qpos = a.q_pos[b] + qi;
+    const int64_t p0 = a.req_page_off[b], np = a.req_page_off[b + 1] - p0;
+    const KV* kp = static_cast<const KV*>(a.k_pages);
+    const KV* vp = static_cast<const KV*>(a.v_pages);
+    float m = -INFINITY, l = 0.f, o[kGenPerLane];
+#pragma unroll
+    for (int i = 0; i < kGenPerLane; ++i) o[i] = 0.f;
+    for (int64_t pi = warp; pi < np; pi += kGenWarps) {
+        const PageDesc d = a.pdesc[p0 + pi];
+        const int64_t vis = qpos - d.pos + 1;  // visible prefix of the page (attention.cpp:29-33)
+        const int nk = vis <= 0 ? 0 : (vis < d.n_tok ? int(vis) : d.n_tok);
+        const size_t tile = (size_t(d.page) * Hkv + g) * size_t(P);
+        for (int j0 = 0; j0 < nk; j0 += 32) {
+            const int j = j0 + lane;
+            float sc = -INFINITY;
+            if (j < nk) {
+                const KV* kr = kp + (tile + j) * D;
+                float dot = 0.f;
+                for (int c = 0; c < D; ++c) dot = fmaf(qs[c], kvf(kr, c), dot);
+                sc = dot;
+            }
+            float cm = sc;
+#pragma unroll
+            for (int msk = 16; msk > 0; msk >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, msk));
+            const float nm = fmaxf(m, cm);
+            const float corr = m == -INFINITY ? 0.f : exp2f(m - nm);
+            const float pj_own = j < nk ? exp2f(sc - nm) : 0.f;
+            l = l * corr + warp_sum(pj_own);
+#pragma unroll
+            for (int i = 0; i < kGenPerLane; ++i) o[i] *= corr;
+            const int cnt = min(32, nk - j0);
+            for (int jj = 0; jj < cnt; ++jj) {
+                const float pj = __shfl_sync(0xffffffffu, pj_own, jj);
+                const KV* vr = vp + (tile + j0 + jj) * D;
+#pragma unroll
+                for (int i = 0; i < kGenPerLane; ++i) {
+                    const int c = lane + 32 * i;
+                    if (c < D) o[i] = fmaf(pj, kvf(vr, c), o[i]);
+                }
+            }
+            m = nm;
+        }
+    }
+    if (lane == 0) {
+        wm[warp] = m;
+        wl[warp] = l;
+    }
+#pragma unroll
+    for (int i = 0; i < kGenPerLane; ++i) {
+        const int c = lane + 32 * i;
+        if (c < D) wo[warp * D + c] = o[i];
+    }
+    __syncthreads();
+    float M = -INFINITY;
+    for (int w = 0; w < kGenWarps; ++w) M = fmaxf(M, wm[w]);
+    float L = 0.f, wt[kGenWarps];
+    for (int w = 0; w < kGenWarps; ++w) {
+        wt[w] = wm[w] == -INFINITY ? 0.f : exp2f(wm[w] - M);
+        L += wt[w] * wl[w];
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;  // no visible key: the identity (o = 0, lse = -inf)
+    for (int c = tid; c < D; c += blockDim.x) {
+        float acc = 0.f;
+        for (int w = 0; w < kGenWarps; ++w) acc += wt[w] * wo[w * D + c];
+        store_o(a.o, a.o_dtype, row * D + c, acc * inv);
+    }
+    if (tid == 0 && a.lse) a.lse[row] = L > 0.f ? (M + log2f(L)) * kLn2 : -INFINITY;
+}
+
 }  // namespace
 
 bool decode_supported(int kv_dtype, int d_head, int rows) {
-    return (kv_dtype == EP_F32 || kv_dtype == EP_BF16) && (d_head == 64 || d_head == 128) &&
-           (rows == 1 || rows == 2 || rows == 4 || rows == 8);
+    return (kv_dtype == EP_F32 || kv_dtype == EP_BF16) && (d_head == 64 || d_head == 128) && rows >= 1 &&
+           rows <= 8;
+}
+
+bool generic_supported(int kv_dtype, int d_head) {
+    return (kv_dtype == EP_F32 || kv_dtype == EP_BF16) && d_head >= 1 && d_head <= 32 * kGenPerLane;
+}
+
+cudaError_t launch_generic_decode(int kv_dtype, int d_head, int batch, int n_q, const DecodeArgs& a,
+                                  cudaStream_t s) {
+    if (batch <= 0 || n_q <= 0) return cudaSuccess;
+    const dim3 grid(batch, n_q, a.n_q_heads);
+    const size_t smem = sizeof(float) * size_t(d_head) * (1 + kGenWarps);
+    if (kv_dtype == EP_BF16)
+        generic_decode_kernel<__nv_bfloat16><<<grid, kGenWarps * 32, smem, s>>>(a, d_head);
+    else
+        generic_decode_kernel<float><<<grid, kGenWarps * 32, smem, s>>>(a, d_head);
+    return cudaGetLastError();
 }
 
 int decode_ctas_per_sm(int, int, int) { return 1; }
 
 cudaError_t launch_spliced_decode(int kv_dtype, int d_head, int rows, int n_ctas,
                                   const DecodeArgs& a, cudaStream_t s) {
+    rows = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : rows;
     if (kv_dtype == EP_BF16) {
         return d_head == 128 ? dispatch_rows<__nv_bfloat16, 128>(rows, n_ctas, a, s)
                              : dispatch_rows<__nv_bfloat16, 64>(rows, n_ctas, a, s);

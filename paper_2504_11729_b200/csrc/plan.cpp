@@ -228,6 +228,9 @@ struct ep_plan_s {
     cudaStream_t side = nullptr;      // the shared-prefix pass's stream (concurrent cascade)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool prefill = false;             // prefill plan: virtual requests = query chunks
+    int32_t chunks = 1;               // decode plan cut into query chunks (K1 takes <= 8 rows): per request
+    int32_t chunk_q = 0;              //   `chunks` virtual requests of chunk_q tokens
+    bool generic = false;             // no K1 / K3 instance: the generic kernel (any d_head <= 256, any group)
     std::vector<int32_t> q_row0;      // prefill: first q/o token row per virtual request
     SubPlan main;    // whole table (non-cascade) or the private remainders (cascade)
     SubPlan shared;  // cascade: shared prefixes, row-group tiles on K3
@@ -280,10 +283,12 @@ int collect_pages(const ep_plan_s& p, int b, const int64_t* seg_indptr, const ep
                                  first_pages);
 }
 
+int pow2ceil_rows(int r) { return r <= 1 ? 1 : r <= 2 ? 2 : r <= 4 ? 4 : 8; }
+
 int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs,
                     const int32_t* page_table, const int64_t* q_pos) {
-    const int B = p.batch, Hkv = p.n_kv_heads;
-    const int rpr = (p.n_q_heads / Hkv) * p.n_q;
+    const int B = p.batch, Hkv = p.n_kv_heads, G = p.n_q_heads / Hkv;
+    const int rpr = G * p.n_q;
     p.q_pos.assign(q_pos, q_pos + B);
     if (seg_indptr[0] != 0) return fail(EP_EINVAL, "ep_plan: seg_indptr[0] must be 0");
     // per request: page descriptors, and where its first segment's pages end
@@ -295,6 +300,65 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
             return rc;
     }
     const int64_t cap = int64_t(p.h->n_sms);
+
+    // ---- kernel choice: K1 (CUDA cores, <= 8 rows per unit, padded to a
+    // power of two), K3 (tcgen05, bf16 d 128, <= 64 rows), K1 on query
+    // chunks of 8 / G tokens (more rows, G <= 8), else the generic kernel ----
+    const bool k1_direct = decode_supported(p.kv_dtype, p.d_head, rpr);
+    const bool k3 = verify_supported(p.kv_dtype, p.d_head, rpr) && rpr <= 64;
+    const bool k1_chunk = !k1_direct && !k3 && G <= 8 && decode_supported(p.kv_dtype, p.d_head, G);
+    p.generic = !k1_direct && !k3 && !k1_chunk;
+    p.chunks = 1;
+    p.chunk_q = p.n_q;
+    if (p.generic) {
+        std::vector<VReq> vr(B);
+        for (int b = 0; b < B; ++b) {
+            vr[b].pages = std::move(req_pages[b]);
+            vr[b].rq0 = b;
+            vr[b].q0min = q_pos[b];
+            vr[b].n_rows = rpr;
+        }
+        p.cascade = false;
+        p.has_shared.assign(B, 0);
+        p.main.tc = false;
+        build_subplan(p.main, vr, Hkv, cap, 0);  // page descriptors only
+        p.main.rows = rpr;
+        return EP_OK;
+    }
+    if (k1_chunk) {
+        // virtual request v = b * chunks + c holds query tokens [c C, (c+1) C)
+        // of request b at positions q_pos[b] + c C ..; its pages stop at its
+        // last query (later keys are masked anyway)
+        const int C = std::max(1, 8 / G);
+        p.chunk_q = C;
+        p.chunks = (p.n_q + C - 1) / C;
+        std::vector<VReq> vr;
+        std::vector<int64_t> vq;
+        for (int b = 0; b < B; ++b)
+            for (int c = 0; c < p.chunks; ++c) {
+                const int nq = std::min(C, p.n_q - c * C);
+                const int64_t q0 = q_pos[b] + int64_t(c) * C, vis = q0 + nq;
+                VReq v;
+                for (const PageDesc& d : req_pages[b]) {
+                    if (d.pos >= vis) break;
+                    PageDesc t = d;
+                    t.n_tok = int32_t(std::min<int64_t>(d.n_tok, vis - d.pos));
+                    v.pages.push_back(t);
+                }
+                v.rq0 = int32_t(vr.size());
+                v.q0min = q0;
+                v.n_rows = G * nq;
+                vq.push_back(q0);
+                vr.push_back(std::move(v));
+            }
+        p.q_pos = vq;
+        p.cascade = false;
+        p.has_shared.assign(B, 0);
+        p.main.tc = false;
+        build_subplan(p.main, vr, Hkv, cap, k1_item_weight());
+        p.main.rows = pow2ceil_rows(G * C);
+        return EP_OK;
+    }
 
     // ---- cascade detection: runs of consecutive requests whose first segment
     // is the same page list (a shared cloud prompt) ----
@@ -342,7 +406,7 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         main_vr[b].q0min = q_pos[b];
         main_vr[b].n_rows = rpr;
     }
-    p.main.tc = !decode_supported(p.kv_dtype, p.d_head, rpr) || force_tc();
+    p.main.tc = !k1_direct || (force_tc() && k3);
     int64_t cap_main = cap, cap_shared = cap;
     if (p.cascade && !p.main.tc && concurrent_cascade()) {
         // The shared-prefix tiles (K3: tensor / MUFU bound, ~35 MB of K/V)
@@ -376,7 +440,7 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         if (env > 0) cap_main = env;
     }
     build_subplan(p.main, main_vr, Hkv, cap_main, p.main.tc ? kTcItemWeight : k1_item_weight());
-    p.main.rows = rpr;
+    p.main.rows = p.main.tc ? rpr : pow2ceil_rows(rpr);
     if (p.cascade) {
         build_subplan(p.shared, shared_vr, Hkv, cap_shared, tc_item_weight(group_cap * rpr));
         p.shared.rows = group_cap * rpr;
@@ -515,7 +579,9 @@ DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* po
     a.n_kv_heads = p.n_kv_heads;
     a.n_q_heads = p.n_q_heads;
     a.page_tokens = p.page_tokens;
-    a.n_q = p.n_q;
+    a.n_q = p.chunks > 1 ? p.chunk_q : p.n_q;
+    a.chunks = p.chunks;
+    a.nq_total = p.n_q;
     a.pdesc = static_cast<const PageDesc*>(sp.d_pdesc.ptr);
     a.req_page_off = static_cast<const int64_t*>(sp.d_req_off.ptr);
     a.items = static_cast<const WorkItem*>(sp.d_items.ptr);
@@ -581,6 +647,10 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
                     "verify attention launch");
         h->launches++;
         if (a.trace) dump_trace(a.trace, s);
+    } else if (p.generic) {
+        EP_CUDA_TRY(launch_generic_decode(p.kv_dtype, p.d_head, p.batch, p.n_q, a, s), "generic decode launch");
+        h->launches++;
+        return EP_OK;
     } else if (sp.n_items > 0) {
         a.trace = trace_buffer();
         EP_CUDA_TRY(launch_spliced_decode(p.kv_dtype, p.d_head, sp.rows, int(sp.n_ctas), a, s),
@@ -616,13 +686,9 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
         return fail(EP_EUNSUPPORTED, "ep_plan_create: page_tokens must be a multiple of 64");
     if (batch < 0 || n_q <= 0) return fail(EP_EINVAL, "ep_plan_create: batch/n_q");
     const int rows = (n_q_heads / pool->n_kv_heads) * n_q;
-    const bool k1 = decode_supported(pool->dtype, pool->d_head, rows);
-    const bool k3 = verify_supported(pool->dtype, pool->d_head, rows) && rows <= 64;
-    if (!k1 && !k3)
+    if (!generic_supported(pool->dtype, pool->d_head))
         return fail(EP_EUNSUPPORTED, "ep_plan_create: no kernel for kv dtype " + std::to_string(pool->dtype) +
-                                         ", d_head=" + std::to_string(pool->d_head) + ", rows=group*n_q=" +
-                                         std::to_string(rows) +
-                                         " (CUDA-core decode: rows 1/2/4/8; tcgen05 verify: bf16, d 128, rows <= 64)");
+                                         ", d_head=" + std::to_string(pool->d_head) + " (d_head must be 1..256)");
     std::unique_ptr<ep_plan_s> p(new (std::nothrow) ep_plan_s());
     if (!p) return fail(EP_ENOMEM, "ep_plan_create");
     p->h = h;

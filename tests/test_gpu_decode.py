@@ -178,7 +178,52 @@ def test_plan_rejects_bad_tables(cuda_handle):
                                     indptr.ctypes.data, segs.ctypes.data, pt_bad.ctypes.data,
                                     table.q_pos.ctypes.data, 0, C.byref(plan))
     assert rc == _capi.EP_EINVAL
+    # rows = 4 * 17 = 68 > 64: past K3, K1 takes it in query chunks
     rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd), 8, 17, table.batch,
                                     indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
                                     table.q_pos.ctypes.data, 0, C.byref(plan))
-    assert rc == _capi.EP_EUNSUPPORTED  # rows = 4*17 = 68 > 64: no kernel instance
+    assert rc == _capi.EP_OK
+    _capi.lib().ep_plan_destroy(plan)
+    pd_wide = pool.desc()
+    pd_wide.d_head = 512   # the only shape without a kernel: d_head > 256
+    rc = _capi.lib().ep_plan_create(cuda_handle.ptr, C.byref(pd_wide), 8, 1, table.batch,
+                                    indptr.ctypes.data, segs.ctypes.data, pt.ctypes.data,
+                                    table.q_pos.ctypes.data, 0, C.byref(plan))
+    assert rc == _capi.EP_EUNSUPPORTED
+
+
+# Every head shape the reference accepts (any n_heads, any d_head,
+# attention.cpp:80-114, model.hpp:15-25) runs on the device: K1 with its row
+# stride padded to a power of two (group 3 / 5 / 6, n_q*group = 5), K1 over
+# query chunks of 8 / group tokens when a unit has more than 8 rows and K3
+# does not apply (fp32 verify: 20 rows; config 1's k = 8 verify on MHA d 64:
+# 9 rows), and the generic kernel for the rest (d_head 96 / 256 / 80, group
+# 16 on fp32). Ragged segments, a shared cloud prompt, a request of only its
+# own query tokens.
+@pytest.mark.parametrize("kv,Hq,Hkv,d,n_q", [
+    (O.DT_BF16, 12, 4, 128, 1),   # G 3 -> R 4
+    (O.DT_F32, 10, 2, 64, 1),     # G 5 -> R 8
+    (O.DT_BF16, 24, 4, 128, 1),   # G 6 -> R 8
+    (O.DT_F32, 4, 4, 64, 5),      # MHA verify k = 4: 5 rows -> R 8
+    (O.DT_F32, 4, 4, 64, 9),      # MHA verify k = 8: 9 rows -> chunks of 8 + 1 tokens
+    (O.DT_F32, 16, 4, 128, 5),    # fp32 GQA verify: 20 rows -> chunks of 2 tokens
+    (O.DT_BF16, 12, 4, 64, 7),    # bf16 d 64, 21 rows -> chunks of 2 tokens (K3 needs d 128)
+    (O.DT_BF16, 8, 2, 96, 1),     # generic: d 96
+    (O.DT_BF16, 4, 2, 256, 3),    # generic: d 256, multi-row
+    (O.DT_F32, 32, 2, 64, 1),     # generic: group 16
+    (O.DT_F32, 6, 3, 80, 2),      # generic: d 80
+])
+def test_any_head_shape(cuda_handle, kv, Hq, Hkv, d, n_q):
+    import torch
+    reqs = [[(SC.CLOUD, 300, "c"), (SC.EDGE, 37, None), (SC.GEN, 9, None)],
+            [(SC.CLOUD, 300, "c"), (SC.EDGE, 130, None), (SC.GEN, 12, None)],
+            [(SC.EDGE, 64, None)],
+            [(SC.GEN, n_q, None)],
+            [(SC.CLOUD, 70, None), (SC.EDGE, 1, None), (SC.GEN, n_q, None)]]
+    sb = SC.make_case(kv, Hq, Hkv, d, reqs, n_q=n_q, seed=17 + d + Hq)
+    _, _, attn, q = to_device(sb, cuda_handle)
+    want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4)
+    for o_dtype in (torch.float32, q.dtype):
+        o, lse = attn(q, o_dtype=o_dtype)
+        err = _check(o, lse, want_o, want_l, sb.kv_dtype)
+        print(Hq, Hkv, d, n_q, o_dtype, err)
