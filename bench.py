@@ -11,11 +11,17 @@ K 22, V 23), no checkpoint.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 is launched by torchrun: every rank serves its own batch of 32
-requests (replicas, weak scaling — config 2 does not shard). Prints one JSON
-line on rank 0. `--impl reference` times the reference's own CPU
-implementation (oracle/_ref: the unmodified reference sources) of the same
-workload on the host cores.
+N > 1 is launched by torchrun and measures the path that shards: BASELINE
+config 4 (long-context split-KV) — 32 requests of 131072 cloud + 512 edge
+keys, the cloud KV cut into N contiguous shards (one per GPU), every rank
+running K1 over its shard and the peer-memory (o, lse) combine over NVLink;
+`value` = tokens/s of the whole job (strong scaling: the total work is
+fixed), with the same workload unsharded on one GPU measured in the same run
+(`value_1gpu`). Config 2 does not shard (independent requests); its
+N-replica throughput is reported beside it. Prints one JSON line on rank 0.
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref: the unmodified reference sources) of the same workload on the
+host cores.
 """
 from __future__ import annotations
 
@@ -44,6 +50,14 @@ SEED_Q, SEED_K, SEED_V = 21, 22, 23
 
 WORKLOAD = ("cfg2: 7B-shaped spliced decode, Hq=32 Hkv=8 d=128 bf16, 4096 cloud + 512 edge "
             "+ 1 self KV per request (private pages), batch 32, n_q=1")
+# Config 4 (the sharded path, N > 1)
+SKV_B, SKV_CLOUD, SKV_EDGE = 32, 131072, 512
+
+
+def skv_workload(world):
+    return (f"cfg4: long-context split-KV, Hq=32 Hkv=8 d=128 bf16, {SKV_CLOUD} cloud + {SKV_EDGE} "
+            f"edge KV per request (private pages), batch {SKV_B}, n_q=1, cloud KV in {world} "
+            "contiguous shards (one per GPU), edge on the last rank")
 
 
 def peaks():
@@ -151,6 +165,48 @@ def cpu_reference_rate(sb, threads, min_seconds=10.0, max_seconds=30.0):
     return tokens / el, el, passes * units_per_pass
 
 
+def run_reference_skv(args, world):
+    """--impl reference at N > 1: the reference attention block on config 4's
+    workload (one request of 131072 + 512 keys x 32 heads per step: every
+    partial_attention over the request's segments + merge_partials, fp64,
+    oracle/_ref) on all host threads."""
+    import numpy as np
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    ppr = SKV_CLOUD // P + SKV_EDGE // P
+    per_pool = ppr * HKV * P * D
+    k_host = O.fill_uniform(O.DT_BF16, per_pool, SEED_K).reshape(-1, HKV, P, D)
+    v_host = O.fill_uniform(O.DT_BF16, per_pool, SEED_V).reshape(-1, HKV, P, D)
+    q_host = O.fill_uniform(O.DT_BF16, HQ * D, SEED_Q).reshape(1, 1, HQ, D)
+    segs = np.array([(0, SKV_CLOUD, 0, 0), (1, SKV_EDGE, SKV_CLOUD, SKV_CLOUD // P)], dtype=O.SEGMENT_DTYPE)
+    sb = O.HostSpliceBatch(O.DT_BF16, HKV, HQ, D, P, np.ascontiguousarray(k_host), np.ascontiguousarray(v_host),
+                           np.array([0, 2], np.int64), segs, np.arange(ppr, dtype=np.int32),
+                           np.array([SKV_CLOUD + SKV_EDGE - 1], np.int64), O.DT_BF16, np.ascontiguousarray(q_host), 1)
+    cache = O.RefBatchCache(sb)
+    for _ in range(args.warmup):
+        cache.attention(n_threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        cache.attention(n_threads=threads)
+        times.append(time.perf_counter() - t0)
+    step_s = sum(times) / len(times)
+    value = 1.0 / step_s  # one token (query row of one request through one layer) per step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": skv_workload(world), "sample_requests_per_step": 1},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                         "sample": f"1 of {SKV_B} requests x 32 heads per step ({SKV_CLOUD + SKV_EDGE} keys), "
+                                   "reference attention block (partial_attention per segment + merge) "
+                                   "in fp64 from oracle/_ref"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU implementation of the same
     workload on the host cores (rank 0 only)."""
@@ -208,7 +264,10 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args)
+            if world > 1:
+                run_reference_skv(args, world)
+            else:
+                run_reference(args)
         return
 
     import numpy as np
@@ -223,6 +282,11 @@ def main():
     from paper_2504_11729_b200 import _capi
     from paper_2504_11729_b200.attention import Handle
     from paper_2504_11729_b200.splice import KVPool, SpliceTable, SplicedAttention
+
+    if world > 1:
+        run_sharded(args, world, rank, local_rank)
+        dist.destroy_process_group()
+        return
 
     h = Handle(local_rank)
     stream = torch.cuda.current_stream()
@@ -401,6 +465,203 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_sharded(args, world, rank, local_rank):
+    """N > 1: config 4 split-KV over the N GPUs as the measured step (local
+    K1 over this rank's cloud shard + ONE peer-memory combine kernel pushing
+    (o, lse) over NVLink and merging in rank order), the same workload
+    unsharded on rank 0's GPU for the scaling reference, the e2e through the
+    public API with host buffers, and config 2 replicas beside it."""
+    import gc
+
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import splitkv_bench as SB
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splitkv import PeerSplitKVCombine
+
+    h = Handle(local_rank)
+    stream = torch.cuda.current_stream()
+    pool, table, attn, q, n_loc = SB.build_local(SKV_B, world, rank, h, cloud=SKV_CLOUD, edge=SKV_EDGE)
+    rows = SKV_B * HQ
+    comb = PeerSplitKVCombine(world, rank, rows, D, h)
+    o_part = torch.empty((SKV_B, 1, HQ, D), dtype=torch.float32, device="cuda")
+    lse_part = torch.empty((SKV_B, 1, HQ), dtype=torch.float32, device="cuda")
+    out = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
+    out_lse = torch.empty((rows,), dtype=torch.float32, device="cuda")
+
+    def step(qq=q):
+        attn(qq, o=o_part, lse=lse_part, stream=stream)
+        comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    steps = args.steps
+
+    def timed(fn, n):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / n], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with ClockSampler(local_rank) as clocks:
+        l0 = h.launch_count()
+        ms = timed(step, steps)
+        launches = h.launch_count() - l0
+    # inside the step: the local pass (the HBM-bound kernel) and the combine
+    # (incl. waiting for the slowest peer), per-step events, max over ranks
+    n_split = max(5, min(steps, 200))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_split + 1)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for i in range(n_split):
+        attn(q, o=o_part, lse=lse_part, stream=stream)
+        ev[2 * i + 1].record(stream)
+        comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=stream)
+        ev[2 * i + 2].record(stream)
+    torch.cuda.synchronize()
+    split = torch.tensor([sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(n_split)) / n_split,
+                          sum(ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(n_split)) / n_split],
+                         device="cuda")
+    dist.all_reduce(split, op=dist.ReduceOp.MAX)
+    ms_local, combine_ms = float(split[0]), float(split[1])
+
+    # e2e through the public API with host buffers: every step copies the
+    # batch's query rows from pinned host memory and reads the merged output
+    # rows back (every rank holds the same merged rows; each reads its own)
+    q_host = q.cpu().pin_memory()
+    o_host = torch.empty((rows, D), dtype=torch.bfloat16).pin_memory()
+    q_dev = torch.empty_like(q)
+
+    def e2e_step():
+        q_dev.copy_(q_host, non_blocking=True)
+        step(q_dev)
+        o_host.copy_(out, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    ms_e2e = timed(e2e_step, steps)
+    ok = bool(torch.equal(o_host.to("cuda"), out))
+
+    # the same workload unsharded on one GPU (rank 0), for the scaling reference
+    ms_1 = None
+    if rank == 0:
+        _, _, attn1, q1, _ = SB.build_local(SKV_B, 1, 0, h, cloud=SKV_CLOUD, edge=SKV_EDGE)
+        o1 = torch.empty((SKV_B, 1, HQ, D), dtype=torch.bfloat16, device="cuda")
+        for _ in range(args.warmup):
+            attn1(q1, o=o1, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            attn1(q1, o=o1, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_1 = e0.elapsed_time(e1) / steps
+        del attn1, q1, o1
+        gc.collect()
+        torch.cuda.empty_cache()
+    dist.barrier()
+
+    peak, peak_kind = peaks()
+    loc_bytes = SKV_B * n_loc * 2 * HKV * D * 2
+    t_loc = torch.tensor([float(loc_bytes)], device="cuda")
+    dist.all_reduce(t_loc, op=dist.ReduceOp.MAX)
+    achieved = float(t_loc.item()) / (ms_local / 1e3) / 1e9
+    gather_bytes = (world - 1) * rows * (D + 1) * 4
+    value = SKV_B / (ms / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": skv_workload(world), "global_batch": SKV_B, "seq_len": SKV_CLOUD + SKV_EDGE,
+                   "parallelism": f"split-KV x{world}: contiguous cloud-KV shards, one per GPU; "
+                                  "(o, lse) combine = one peer-memory kernel over NVLink",
+                   "l2": f"inputs larger than L2 ({loc_bytes / 1e9:.1f} GB of KV per rank per step), no flush"},
+        "value_1gpu": (SKV_B / (ms_1 / 1e3)) if ms_1 else None,
+        "ms_per_step_1gpu": ms_1,
+        "hbm_gbs_per_gpu": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "note": "per GPU: the largest rank's shard bytes (2*Hkv*d*2 B per key x keys x 32 "
+                             "requests) / the local K1 time inside the step (per-step CUDA events, "
+                             "max over ranks)"},
+        "combine": {"ms": combine_ms, "bytes_received_per_rank": gather_bytes,
+                    "nvlink_gbs": gather_bytes / (combine_ms / 1e3) / 1e9,
+                    "nvlink_frac": gather_bytes / (combine_ms / 1e3) / 900e9,
+                    "note": "per-step events around the combine kernel, max over ranks (includes "
+                            "waiting for the slowest peer); latency-bound (tiny messages)"},
+        "e2e": {"value": SKV_B / (ms_e2e / 1e3), "unit": "tokens/s",
+                "h2d_bytes_per_step": q.numel() * 2, "d2h_bytes_per_step": rows * D * 2,
+                "ms_per_step": ms_e2e, "result_check": ok,
+                "path": "SplicedAttention + PeerSplitKVCombine (the C-ABI calls) with pinned host q / output"},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    comb.close()
+    del attn, pool, table, q, o_part, lse_part, out, out_lse, comb
+    gc.collect()
+    torch.cuda.empty_cache()
+    if not args.no_extras:
+        extras = {}
+        # config 4 at batch 1 (latency): both combines
+        skv = {}
+        for cmb in ("peer", "nccl"):
+            skv[f"batch1_{cmb}"] = SB.run(1, max(5, min(steps, 30)), 3, combine=cmb)
+            gc.collect()
+            torch.cuda.empty_cache()
+        extras["splitkv"] = skv
+        extras["cfg2_replicas"] = cfg2_replicas(args, world, rank, local_rank, h)
+        line.update(extras)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cfg2_replicas(args, world, rank, local_rank, h):
+    """Config 2 (does not shard): every rank runs its own batch of 32."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_11729_b200 import _capi
+    from paper_2504_11729_b200.splice import KVPool, SpliceTable, SplicedAttention
+    stream = torch.cuda.current_stream()
+    pool = KVPool(B * PAGES_PER_REQ, HKV, D, P, dtype="bf16", device=local_rank)
+    lib = _capi.lib()
+    sp = stream.cuda_stream
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, pool.k.data_ptr(), pool.k.numel(), SEED_K, -1.0, 1.0, sp))
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, pool.v.data_ptr(), pool.v.numel(), SEED_V, -1.0, 1.0, sp))
+    q = torch.empty((B, 1, HQ, D), dtype=torch.bfloat16, device="cuda")
+    _capi.check(lib.ep_fill_uniform(h.ptr, _capi.EP_BF16, q.data_ptr(), q.numel(), SEED_Q, -1.0, 1.0, sp))
+    attn = SplicedAttention(pool, build_requests_table(SpliceTable, pool, B), HQ, 1, handle=h)
+    o = torch.empty_like(q)
+    for _ in range(args.warmup):
+        attn(q, o=o, stream=stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(20, min(args.steps, 500))
+    e0.record(stream)
+    for _ in range(n):
+        attn(q, o=o, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / n], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": WORKLOAD + f", one batch per GPU (x{world})", "ms_per_step": ms,
+            "tokens_per_s": B * world / (ms / 1e3), "scaling": "weak"}
 
 
 def run_extras(args, world, rank, h):

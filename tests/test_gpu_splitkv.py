@@ -103,14 +103,21 @@ def test_peer_combine_emulated_ranks(cuda_handle, world):
         g.close()
 
 
-def test_torchrun_nccl_two_ranks():
+@pytest.mark.parametrize("batch", [1, 32])
+def test_torchrun_config4_two_ranks(batch):
+    """Config 4 at its own shape on 2 GPUs: 131072 cloud + 512 edge keys per
+    request sharded over two processes, both combines (peer-memory kernel
+    over NVLink, NCCL all-gather + K5); rank 0 checks the merged output
+    against an unsharded single-GPU run of the same batch and against the
+    fp64 oracle on sampled units (tools/splitkv_bench.py --check)."""
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29533",
-           os.path.join(ROOT, "tools", "splitkv_bench.py"), "--batch", "2", "--steps", "3",
+           "--master-addr", "127.0.0.1", "--master-port", str(29533 + batch),
+           os.path.join(ROOT, "tools", "splitkv_bench.py"), "--batch", str(batch), "--steps", "3",
            "--check", "--combine", "peer", "nccl"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
+    print(r.stdout)
     assert r.stdout.count('"check_ok": true') == 2, r.stdout

@@ -69,6 +69,35 @@ def build_local(batch, world, rank, h, cloud=CLOUD, edge=EDGE, seed=41):
     return pool, table, attn, q, n_loc
 
 
+def oracle_check(pool1, q1, b, heads, out, out_lse, cloud=CLOUD, edge=EDGE):
+    """fp64 oracle (oracle/ep_oracle.c) on units (b, h) of the unsharded
+    layout of build_local(batch, 1, ...), against the merged rows out /
+    out_lse [rows]; returns (max rel err of o, of lse) with the reference's
+    metric |got - want| / max(1, |want|)."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    ppr = -(-cloud // P) + -(-edge // P)
+    pages = torch.arange(b * ppr, (b + 1) * ppr, device=pool1.k.device)
+    kp = pool1.k[pages].view(torch.int16).cpu().numpy().view(np.uint16)
+    vp = pool1.v[pages].view(torch.int16).cpu().numpy().view(np.uint16)
+    segs = np.array([(0, cloud, 0, 0), (1, edge, cloud, -(-cloud // P))], dtype=O.SEGMENT_DTYPE)
+    qb = q1[b:b + 1].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+    sb = O.HostSpliceBatch(kv_dtype=O.DT_BF16, n_kv_heads=HKV, n_q_heads=HQ, d_head=D, page_tokens=P,
+                           k_pages=np.ascontiguousarray(kp), v_pages=np.ascontiguousarray(vp),
+                           seg_indptr=np.array([0, 2], np.int64), segs=segs,
+                           page_table=np.arange(ppr, dtype=np.int32),
+                           q_pos=np.array([cloud + edge - 1], np.int64), q_dtype=O.DT_BF16,
+                           q=np.ascontiguousarray(qb), n_q=1)
+    want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4, units=heads)
+    got_o = out.float().cpu().numpy().reshape(-1, HQ, D)[b]
+    got_l = out_lse.cpu().numpy().reshape(-1, HQ)[b]
+    e_o = max(float(np.max(np.abs(got_o[h] - want_o[0, 0, h]) / np.maximum(1.0, np.abs(want_o[0, 0, h]))))
+              for h in heads)
+    e_l = max(float(abs(got_l[h] - want_l[0, 0, h]) / max(1.0, abs(want_l[0, 0, h]))) for h in heads)
+    return e_o, e_l
+
+
 def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CLOUD):
     """combine: "peer" = one ep_splitkv_combine_dev kernel over NVLink peer
     memory; "nccl" = NCCL all-gather + K5 merge. graph: replay the step
@@ -188,9 +217,11 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     if check:
         ok = True
         if world > 1:
-            # rank 0 recomputes the unsharded batch on its own GPU
+            # rank 0 recomputes the unsharded batch on its own GPU, and the
+            # fp64 oracle recomputes sampled units of the last request from
+            # the same pages (merge in rank = segment order, attention.cpp:116-145)
             if rank == 0:
-                _, _, attn1, q1, _ = build_local(batch, 1, 0, h)
+                pool1, table1, attn1, q1, _ = build_local(batch, 1, 0, h)
                 o1, l1 = attn1(q1, o_dtype=torch.float32)
                 torch.cuda.synchronize()
                 err = (out.float() - o1.reshape(rows, D)).abs().max().item()
@@ -198,6 +229,10 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
                 res["check_max_abs_err"] = err
                 res["check_lse_max_abs_err"] = lerr
                 ok = err < 2e-2 and lerr < 1e-3
+                e_o, e_l = oracle_check(pool1, q1, batch - 1, [0, 13, 31], out, out_lse, cloud)
+                res["check_oracle_rel_err"] = e_o
+                res["check_oracle_lse_rel_err"] = e_l
+                ok = ok and e_o <= 2e-2 and e_l <= 1e-4
         res["check_ok"] = ok
     if world > 1:
         torch.cuda.synchronize()
