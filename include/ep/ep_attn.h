@@ -297,6 +297,22 @@ int ep_splitkv_combine_dev(ep_handle h, ep_peer_group g, int32_t rows, const flo
                            ep_stream stream);
 int ep_peer_group_destroy(ep_peer_group g);
 
+/* Split-KV attention with the cross-GPU combine fused into the decode
+ * kernel (config 4): plan p covers this rank's KV shard of every request
+ * (every rank the same requests, the same query rows); the K1 pass over the
+ * shard pushes each (request, kv-head) unit's merged fp32 (o, lse) rows into
+ * every rank's receive buffer of group g over NVLink peer memory as soon as
+ * the unit is done, and at the end of the kernel each unit's owner CTA
+ * merges the W rank partials in rank (= segment) order (attention.cpp:
+ * 116-145) into o / lse — one launch per rank, no separate combine. Every
+ * rank ends with identical rows. Collective: every rank calls it once per
+ * step with the same plan structure. A group serves either this call or
+ * ep_splitkv_combine_dev, not both. EP_EUNSUPPORTED for plans not on K1
+ * (shared-prefix cascade, tcgen05 tiles, the generic kernel, query chunks). */
+int ep_spliced_attention_splitkv(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype,
+                                 const void* q, ep_peer_group g, int32_t o_dtype, void* o, float* lse,
+                                 ep_stream stream);
+
 /* ==================================================================== */
 /* 4. Utilities                                                         */
 /* ==================================================================== */

@@ -118,6 +118,8 @@ _SIGS = {
     "ep_peer_group_connect_ptrs": (C.c_int, [_vp, C.POINTER(_vp)]),
     "ep_splitkv_combine_dev": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp, _vp]),
     "ep_peer_group_destroy": (C.c_int, [_vp]),
+    "ep_spliced_attention_splitkv": (C.c_int, [_vp, _vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp,
+                                               C.c_int32, _vp, _vp, _vp]),
     "ep_plan_create_prefill": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, C.c_int32, _vp,
                                          _vp, _vp, _vp, C.POINTER(_vp)]),
     "ep_plan_create": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, C.c_int32, C.c_int32, _vp,

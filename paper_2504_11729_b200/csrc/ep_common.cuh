@@ -174,6 +174,40 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// ------------------------------------- NVLink low-latency {value, flag} --
+// A 16-byte word {v0, flag, v1, flag} written with one vector store over
+// peer memory carries its own flag: the reader polls until both flags equal
+// the step epoch (no fence, no separate flag round trip). Used by the split-KV
+// combine (kern_peer.cu) and the fused split-KV decode (K1 + merge.cuh).
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void st_ll(uint4* p, float v0, float v1, uint32_t flag) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "r"(__float_as_uint(v0)), "r"(flag), "r"(__float_as_uint(v1)), "r"(flag)
+                 : "memory");
+}
+
+// Poll one LL word until both halves carry `flag`; trap after 20 s.
+__device__ __forceinline__ float2 ld_ll(const uint4* p, uint32_t flag) {
+    uint4 w;
+    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
+    if (w.y != flag || w.w != flag) {
+        const uint64_t t0 = globaltimer();
+        do {
+            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
+            if (globaltimer() - t0 > 20000000000ull) __trap();
+        } while (w.y != flag || w.w != flag);
+    }
+    return make_float2(__uint_as_float(w.x), __uint_as_float(w.z));
+}
+
 // ----------------------------------------------------------- dtype I/O --
 
 template <typename T>

@@ -94,6 +94,19 @@ struct WorkItem {
     int32_t pad;
 };
 
+// Fused split-KV combine (config 4): K1 on this rank's KV shard pushes every
+// unit's merged (o, lse) rows into every rank's receive buffer over NVLink
+// peer memory (kern_peer.cu's {value, flag} words), and each unit's owner CTA
+// merges the W rank partials in rank order at the end of the kernel.
+constexpr int kPeerMaxWorld = 8;
+struct PeerLink {
+    int32_t world = 0, rank = 0;        // world == 0: no exchange (plain decode)
+    int64_t src_units = 0;              // 16-byte words per source slot: rows_max * (d/2 + 1)
+    uint4* recv[kPeerMaxWorld] = {};    // rank p's receive area [2][world][src_units] (mapped here)
+    uint32_t* epoch = nullptr;          // own per-unit step epochs
+    const int32_t* cta_unit_ptr = nullptr;  // [n_ctas+1]: units whose final merge CTA c owns
+};
+
 struct DecodeArgs {
     const void* k_pages;
     const void* v_pages;
@@ -122,7 +135,13 @@ struct DecodeArgs {
     int32_t chunks;           // decode plans with more rows than K1 takes: each request's nq_total query
     int32_t nq_total;         // tokens cut into `chunks` virtual requests of n_q tokens (1 = not cut)
     int32_t pv_parts;         // K3: P as bf16 hi+lo (2) or bf16 (1)
+    PeerLink peer;            // K1 fused split-KV combine (world 0 = off)
 };
+
+// The fused split-KV link of a peer group for a plan of n_units units and
+// `rows` output rows of width d (kern_peer.cu); cta_unit_ptr is the plan's.
+int peer_link_fill(ep_peer_group g, int64_t n_units, int64_t rows, int d, const int32_t* cta_unit_ptr,
+                   PeerLink* out);
 
 // Validates request b's segments of a host splice table with the
 // SegmentedCache invariants (cache.cpp:25-53: gapless positions, origin

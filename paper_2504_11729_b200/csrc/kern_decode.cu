@@ -192,9 +192,16 @@ __device__ __forceinline__ void item_end(const DecodeArgs& a, int it, int gw, in
             if (r < w.pad) {
                 const int qi = r / G, h = w.g * G + r % G;
                 const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
+                if (a.peer.world) {  // fused split-KV: the row goes to every rank
+                    float v[EL];
 #pragma unroll
-                for (int e = 0; e < EL; ++e) store_o(a.o, a.o_dtype, orow * D + lane * EL + e, acc[e] * inv);
-                if (lane == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+                    for (int e = 0; e < EL; ++e) v[e] = acc[e] * inv;
+                    peer_push_row<D>(a, unit, orow, v, lse2);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < EL; ++e) store_o(a.o, a.o_dtype, orow * D + lane * EL + e, acc[e] * inv);
+                    if (lane == 0 && a.lse) a.lse[orow] = lse2 * kLn2;
+                }
             }
         } else {
             float* dst = a.o_part + (size_t(it) * R + r) * D + lane * EL;
@@ -229,7 +236,7 @@ __device__ __forceinline__ void item_end(const DecodeArgs& a, int it, int gw, in
         merge_unit_rows<D>(a, u0, n_items, R, w.pad, gw, n_grp, [&](int r) {
             const int qi = r / G, h = w.g * G + r % G;
             return (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
-        });
+        }, unit);
         if (gw == 0 && lane == 0) a.unit_counter[unit] = 0;  // ready for the next launch
     }
 }
@@ -560,6 +567,16 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(ep_full);
         }
+    }
+    if (a.peer.world) {
+        // fused split-KV: merge the rank partials of the units this CTA owns
+        // (every push of this rank is issued without waiting, so these polls
+        // cannot deadlock), then advance their epochs
+        peer_merge_owned<D>(a, warp, NCW);
+        named_bar_sync(1, NCW * 32);
+        if (threadIdx.x == 0)
+            for (int u = a.peer.cta_unit_ptr[blockIdx.x]; u < a.peer.cta_unit_ptr[blockIdx.x + 1]; ++u)
+                a.peer.epoch[u] += 1u;
     }
     if (a.trace && threadIdx.x == 0 && blockIdx.x < 1024) {  // debug: per-CTA end (ns)
         unsigned long long t;

@@ -57,34 +57,6 @@ struct PeerArgs {
     unsigned long long* trace;  // debug (EP_PEER_TRACE): CTA 0 phase timestamps, [64][8]
 };
 
-__device__ __forceinline__ uint64_t globaltimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-__device__ __forceinline__ void st_ll(uint4* p, float v0, float v1, uint32_t flag) {
-    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p),
-                 "r"(__float_as_uint(v0)), "r"(flag), "r"(__float_as_uint(v1)), "r"(flag)
-                 : "memory");
-}
-
-// Poll one LL word until both halves carry `flag`; trap after 20 s.
-__device__ __forceinline__ float2 ld_ll(const uint4* p, uint32_t flag) {
-    uint4 w;
-    asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
-    if (w.y != flag || w.w != flag) {
-        const uint64_t t0 = globaltimer();
-        do {
-            asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w) : "l"(p) : "memory");
-            if (globaltimer() - t0 > 20000000000ull) __trap();
-        } while (w.y != flag || w.w != flag);
-    }
-    return make_float2(__uint_as_float(w.x), __uint_as_float(w.z));
-}
-
 __global__ void __launch_bounds__(kPeerThreads) splitkv_combine_kernel(const PeerArgs a) {
     const int c = blockIdx.x;
     const int tid = threadIdx.x;
@@ -178,10 +150,13 @@ struct ep_peer_group_s {
     bool peer_is_ipc[ep::kMaxWorld] = {};
     bool connected = false;
     unsigned long long* trace = nullptr;  // EP_PEER_TRACE=1: [64][8] device timestamps
+    int mode = 0;  // 0 unused, 1 combine kernel (ep_splitkv_combine_dev), 2 fused K1 (ep_spliced_attention_splitkv)
     // per source rank: rows_max rows of d/2 {value, flag} data words + 1 lse word
     size_t src_units() const { return size_t(rows_max) * (d / 2 + 1); }
     size_t recv_bytes() const { return size_t(2) * world * src_units() * 16; }
     size_t epoch_off() const { return (recv_bytes() + 255) & ~size_t(255); }
+    // fused mode: one epoch per (request, kv-head) unit (<= rows_max units)
+    size_t unit_epoch_off() const { return (epoch_off() + size_t(nslices) * sizeof(uint32_t) + 255) & ~size_t(255); }
     ~ep_peer_group_s() {
         if (h) cudaSetDevice(h->device);
         for (int p = 0; p < world; ++p)
@@ -205,6 +180,30 @@ struct ep_peer_group_s {
 
 using ep::fail;
 
+namespace ep {
+int peer_link_fill(ep_peer_group g, int64_t n_units, int64_t rows, int d, const int32_t* cta_unit_ptr,
+                   PeerLink* out) {
+    if (!g->connected && g->world > 1) return fail(EP_EINVAL, "ep_spliced_attention_splitkv: group not connected");
+    if (g->mode == 1)
+        return fail(EP_EINVAL, "ep_spliced_attention_splitkv: group is used by ep_splitkv_combine_dev "
+                               "(one combine protocol per group)");
+    if (d != g->d) return fail(EP_EINVAL, "ep_spliced_attention_splitkv: group d != the plan's d_head");
+    if (rows > g->rows_max || n_units > g->rows_max)
+        return fail(EP_EINVAL, "ep_spliced_attention_splitkv: plan rows " + std::to_string(rows) +
+                                   " exceed the group's rows_max " + std::to_string(g->rows_max));
+    g->mode = 2;
+    PeerLink l{};
+    l.world = g->world;
+    l.rank = g->rank;
+    l.src_units = int64_t(g->src_units());
+    for (int p = 0; p < g->world; ++p) l.recv[p] = static_cast<uint4*>(g->peer[p]);
+    l.epoch = reinterpret_cast<uint32_t*>(static_cast<char*>(g->base) + g->unit_epoch_off());
+    l.cta_unit_ptr = cta_unit_ptr;
+    *out = l;
+    return EP_OK;
+}
+}  // namespace ep
+
 extern "C" {
 
 int ep_peer_group_create(ep_handle h, int32_t world, int32_t rank, int32_t rows_max, int32_t d,
@@ -223,7 +222,7 @@ int ep_peer_group_create(ep_handle h, int32_t world, int32_t rank, int32_t rows_
     g->rows_max = rows_max;
     g->d = d;
     g->nslices = rows_max < ep::kMaxSlices ? rows_max : ep::kMaxSlices;
-    g->bytes = g->epoch_off() + size_t(g->nslices) * sizeof(uint32_t);
+    g->bytes = g->unit_epoch_off() + size_t(rows_max) * sizeof(uint32_t);
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_peer_group_create");
     EP_CUDA_TRY(cudaMalloc(&g->base, g->bytes), "ep_peer_group_create alloc");
     EP_CUDA_TRY(cudaMemset(g->base, 0, g->bytes), "ep_peer_group_create memset");
@@ -301,6 +300,10 @@ int ep_splitkv_combine_dev(ep_handle h, ep_peer_group g, int32_t rows, const flo
         return fail(EP_EINVAL, "ep_splitkv_combine_dev: null argument");
     if (!g->connected && g->world > 1) return fail(EP_EINVAL, "ep_splitkv_combine_dev: group not connected");
     if (rows < 0 || rows > g->rows_max) return fail(EP_EINVAL, "ep_splitkv_combine_dev: rows > rows_max");
+    if (g->mode == 2)
+        return fail(EP_EINVAL, "ep_splitkv_combine_dev: group is used by ep_spliced_attention_splitkv "
+                               "(one combine protocol per group)");
+    g->mode = 1;
     if (out_dtype != EP_F32 && out_dtype != EP_BF16)
         return fail(EP_EUNSUPPORTED, "ep_splitkv_combine_dev: out dtype");
     if ((reinterpret_cast<uintptr_t>(o_part) & 7) != 0 || (reinterpret_cast<uintptr_t>(out) & 7) != 0)
@@ -329,6 +332,7 @@ int ep_splitkv_combine_dev(ep_handle h, ep_peer_group g, int32_t rows, const flo
 }
 
 int ep_peer_group_destroy(ep_peer_group g) {
+    // (the plan / kernels using g must have completed)
     delete g;
     return EP_OK;
 }

@@ -13,15 +13,94 @@
 
 namespace ep {
 
+// ---- fused split-KV combine (config 4, K1 with a PeerLink) ----
+// A unit's merged local row (this rank's KV shard) goes to slot [rank] of
+// every rank's receive buffer (own included) as {value, flag} words of the
+// step epoch; a lane holds columns [lane*E, lane*E + E). Never waits.
+template <int D>
+__device__ __forceinline__ void peer_push_row(const DecodeArgs& a, int unit, size_t orow, const float* v,
+                                              float lse2) {
+    constexpr int E = D / 32, H = D / 2;
+    const int lane = threadIdx.x & 31;
+    const uint32_t ep = __ldcg(a.peer.epoch + unit) + 1u;
+    const size_t off = size_t(ep & 1u) * a.peer.world * a.peer.src_units +
+                       size_t(a.peer.rank) * a.peer.src_units + orow * (H + 1);
+    const float lse = lse2 == -INFINITY ? -INFINITY : lse2 * kLn2;  // natural log, as the combine
+    for (int p = 0; p < a.peer.world; ++p) {
+        uint4* dst = a.peer.recv[p] + off;
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) st_ll(dst + lane * (E / 2) + j, v[2 * j], v[2 * j + 1], ep);
+        if (lane == 0) st_ll(dst + H, lse, 0.f, ep);
+    }
+}
+
+// At the end of K1: the units this CTA owns (the CTA of each unit's last
+// work item) — one warp per row polls the W ranks' words of the row and
+// folds them in rank (= KV segment) order (attention.cpp:116-145): the same
+// arithmetic on every rank, so every rank ends with identical rows. Called
+// by n_grp warps (this one is gw); the caller advances the units' epochs
+// once every warp is done.
+template <int D>
+__device__ __forceinline__ void peer_merge_owned(const DecodeArgs& a, int gw, int n_grp) {
+    constexpr int E = D / 32, H = D / 2;
+    const int lane = threadIdx.x & 31;
+    const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv, W = a.peer.world;
+    const int u0 = a.peer.cta_unit_ptr[blockIdx.x], u1 = a.peer.cta_unit_ptr[blockIdx.x + 1];
+    const uint4* mine = a.peer.recv[a.peer.rank];
+    for (int u = u0; u < u1; ++u) {
+        const uint32_t ep = __ldcg(a.peer.epoch + u) + 1u;
+        const size_t par = size_t(ep & 1u) * W * a.peer.src_units;
+        const int b = u / Hkv, g = u % Hkv, nrows = valid_rows(a, b);
+        for (int r = gw; r < nrows; r += n_grp) {
+            const size_t orow = (q_row_base(a, b) + r / G) * a.n_q_heads + size_t(g) * G + r % G;
+            float lse_p[kPeerMaxWorld];
+            float M = -INFINITY;
+            for (int p = 0; p < W; ++p) {
+                float2 x = make_float2(0.f, 0.f);
+                if (lane == 0) x = ld_ll(mine + par + size_t(p) * a.peer.src_units + orow * (H + 1) + H, ep);
+                lse_p[p] = __shfl_sync(0xffffffffu, x.x, 0);
+                M = fmaxf(M, lse_p[p]);
+            }
+            float acc[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = 0.f;
+            float L = 0.f;
+            for (int p = 0; p < W; ++p) {
+                const float wt = (M == -INFINITY || lse_p[p] == -INFINITY) ? 0.f : expf(lse_p[p] - M);
+                L += wt;
+                const uint4* src = mine + par + size_t(p) * a.peer.src_units + orow * (H + 1) + lane * (E / 2);
+#pragma unroll
+                for (int j = 0; j < E / 2; ++j) {  // every word is consumed (it carries the flag)
+                    const float2 x = ld_ll(src + j, ep);
+                    acc[2 * j] += wt * x.x;
+                    acc[2 * j + 1] += wt * x.y;
+                }
+            }
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            if (a.o_dtype == EP_BF16) {
+                __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(a.o) + orow * D + lane * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e] = __float2bfloat16_rn(acc[e] * inv);
+            } else {
+                float* dst = static_cast<float*>(a.o) + orow * D + lane * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) dst[e] = acc[e] * inv;
+            }
+            if (lane == 0 && a.lse) a.lse[orow] = L > 0.f ? M + logf(L) : -INFINITY;
+        }
+    }
+}
+
 // o_part[(item * stride + r) * D + c], lse_part[item * stride + r] (log2);
-// rows r = r0, r0 + r_step, ... < nrows; orow(r) = output row index.
+// rows r = r0, r0 + r_step, ... < nrows; orow(r) = output row index; with a
+// PeerLink the merged rows of `unit` are pushed to every rank instead.
 // Latency-bound by construction (a few rows x a few items of L2 reads), so a
 // warp works on kRB rows at once: their lse loads, then their partial rows of
 // two items at a time, all in flight together (a K3 shared-prefix tile merges
 // 128 rows x 2-3 items; serial per-row loads made that the CTA's tail).
 template <int D, typename RowMap>
 __device__ __forceinline__ void merge_unit_rows(const DecodeArgs& a, int u0, int n, int stride,
-                                                int nrows, int r0, int r_step, RowMap orow_of) {
+                                                int nrows, int r0, int r_step, RowMap orow_of, int unit = -1) {
     constexpr int E = D / 32;
     constexpr int kRB = 4;
     static_assert(E == 2 || E == 4, "D must be 64 or 128");
@@ -133,6 +212,13 @@ __device__ __forceinline__ void merge_unit_rows(const DecodeArgs& a, int u0, int
             if (!ok[k]) continue;
             const bool er = !(L[k] > 0.f);
             const size_t orow = orow_of(rr[k]);
+            if (a.peer.world) {  // fused split-KV: this rank's merged row goes to every rank
+                float v[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = acc[k][e] * inv[k];
+                peer_push_row<D>(a, unit, orow, v, er ? -INFINITY : M[k] + fast_log2(L[k]));
+                continue;
+            }
             if (a.o_dtype == EP_BF16) {
                 __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(a.o) + orow * D + lane * E;
 #pragma unroll

@@ -120,7 +120,9 @@ struct SubPlan {
     std::vector<int64_t> req_page_off;
     std::vector<WorkItem> items;
     std::vector<int32_t> cta_item_ptr, unit_item_ptr, cta_item_idx;
-    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_opart, d_lsepart, d_counter, d_cta_idx;
+    std::vector<int32_t> cta_unit_ptr;  // fused split-KV: units whose final merge CTA c owns (its last item's CTA)
+    DeviceBuffer d_pdesc, d_req_off, d_items, d_cta_ptr, d_unit_ptr, d_opart, d_lsepart, d_counter, d_cta_idx,
+        d_cta_unit;
     size_t counter_units = 0;
 };
 
@@ -195,6 +197,11 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
         if (sp.unit_item_ptr[u + 1] == 0) sp.has_empty_unit = true;
         sp.unit_item_ptr[u + 1] += sp.unit_item_ptr[u];
     }
+    // owner of each unit = the CTA of its last item (monotonic in the unit)
+    sp.cta_unit_ptr.assign(sp.n_ctas + 1, 0);
+    for (int64_t u = 0; u < sp.n_units; ++u)
+        if (sp.unit_item_ptr[u + 1] > sp.unit_item_ptr[u]) sp.cta_unit_ptr[item_cta[sp.unit_item_ptr[u + 1] - 1] + 1]++;
+    for (int64_t c = 0; c < sp.n_ctas; ++c) sp.cta_unit_ptr[c + 1] += sp.cta_unit_ptr[c];
     // K1 order within a CTA: items of split units first, whole units last.
     // A split item's end (partial store, arrival, maybe the merge) then runs
     // on the epilogue warp while the CTA streams on, and the CTA's final item
@@ -510,6 +517,7 @@ int upload_subplan(SubPlan& sp, int d_head, cudaStream_t s, std::vector<std::pai
     parts.push_back({&sp.d_cta_ptr, {sp.cta_item_ptr.data(), bytes_of(sp.cta_item_ptr)}});
     parts.push_back({&sp.d_unit_ptr, {sp.unit_item_ptr.data(), bytes_of(sp.unit_item_ptr)}});
     parts.push_back({&sp.d_cta_idx, {sp.cta_item_idx.data(), bytes_of(sp.cta_item_idx)}});
+    parts.push_back({&sp.d_cta_unit, {sp.cta_unit_ptr.data(), bytes_of(sp.cta_unit_ptr)}});
     const size_t ws = size_t(std::max<int64_t>(sp.n_items, 1)) * sp.rows;
     EP_CUDA_TRY(sp.d_opart.reserve(ws * d_head * sizeof(float)), "ep_plan workspace");
     EP_CUDA_TRY(sp.d_lsepart.reserve(ws * sizeof(float)), "ep_plan workspace");
@@ -763,6 +771,27 @@ int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
 int ep_plan_destroy(ep_plan p) {
     delete p;
     return EP_OK;
+}
+
+int ep_spliced_attention_splitkv(ep_handle h, ep_plan p, const ep_kv_pool* pool, int32_t q_dtype, const void* q,
+                                 ep_peer_group g, int32_t o_dtype, void* o, float* lse, ep_stream stream) {
+    if (!h || !p || !pool || !q || !g || !o) return fail(EP_EINVAL, "ep_spliced_attention_splitkv: null argument");
+    if (pool->dtype != p->kv_dtype || pool->n_kv_heads != p->n_kv_heads || pool->d_head != p->d_head ||
+        pool->page_tokens != p->page_tokens || pool->num_pages < p->num_pages)
+        return fail(EP_EINVAL, "ep_spliced_attention_splitkv: pool does not match the plan");
+    if (!valid_dt(q_dtype) || !valid_dt(o_dtype))
+        return fail(EP_EUNSUPPORTED, "ep_spliced_attention_splitkv: q/o dtype must be f32 or bf16");
+    if (p->cascade || p->main.tc || p->generic || p->prefill || p->chunks > 1)
+        return fail(EP_EUNSUPPORTED, "ep_spliced_attention_splitkv: the fused combine runs on the K1 decode "
+                                     "plans (f32/bf16 KV, d_head 64/128, <= 8 rows per unit, no shared prefix)");
+    if (p->main.has_empty_unit)
+        return fail(EP_EINVAL, "ep_spliced_attention_splitkv: every (request, kv-head) needs keys on every rank");
+    const int64_t rows = int64_t(p->batch) * p->n_q * p->n_q_heads;
+    DecodeArgs a = make_args(*p, p->main, pool, q_dtype, q, o_dtype, o, lse, o_dtype);
+    if (int rc = peer_link_fill(g, p->main.n_units, rows, p->d_head,
+                                static_cast<const int32_t*>(p->main.d_cta_unit.ptr), &a.peer))
+        return rc;
+    return launch_subplan(*p, p->main, pool, a, static_cast<cudaStream_t>(stream));
 }
 
 int ep_plan_info(ep_plan p, int64_t* n_ctas, int64_t* n_items, int64_t* n_pages) {

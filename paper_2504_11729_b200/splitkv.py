@@ -126,6 +126,28 @@ class PeerSplitKVCombine:
               "ep_splitkv_combine_dev")
         return out, out_lse
 
+    def attend(self, attn, q, out=None, out_lse=None, stream=None):
+        """Split-KV attention with the combine fused into the decode kernel
+        (ep_spliced_attention_splitkv): ``attn`` is this rank's
+        SplicedAttention over its KV shard; one launch computes the shard's
+        partials, exchanges them over NVLink and merges them in rank order.
+        Returns (out [B][n_q][Hq][d], out_lse [B][n_q][Hq]) — identical on every
+        rank. A group serves either this or __call__ (the separate combine
+        kernel), not both."""
+        import torch
+        from .splice import _stream, dtype_code
+        if out is None:
+            out = torch.empty(q.shape, dtype=q.dtype, device=q.device)
+        if out_lse is None:
+            out_lse = torch.empty(tuple(q.shape[:3]), dtype=torch.float32, device=q.device)
+        pd = attn.pool.desc()
+        check(self._lib.ep_spliced_attention_splitkv(self.handle.ptr, attn.plan, C.byref(pd), dtype_code(q.dtype),
+                                                     q.data_ptr(), self._g, dtype_code(out.dtype), out.data_ptr(),
+                                                     out_lse.data_ptr() if out_lse is not False else None,
+                                                     _stream(stream)),
+              "ep_spliced_attention_splitkv")
+        return out, out_lse
+
     def close(self):
         if self._g is not None and self._g.value:
             self._lib.ep_peer_group_destroy(self._g)

@@ -106,18 +106,72 @@ def test_peer_combine_emulated_ranks(cuda_handle, world):
 @pytest.mark.parametrize("batch", [1, 32])
 def test_torchrun_config4_two_ranks(batch):
     """Config 4 at its own shape on 2 GPUs: 131072 cloud + 512 edge keys per
-    request sharded over two processes, both combines (peer-memory kernel
-    over NVLink, NCCL all-gather + K5); rank 0 checks the merged output
+    request sharded over two processes, all three combines (peer-memory
+    kernel over NVLink, NCCL all-gather + K5, fused into K1); rank 0 checks the merged output
     against an unsharded single-GPU run of the same batch and against the
-    fp64 oracle on sampled units (tools/splitkv_bench.py --check)."""
+    fp64 oracle on sampled units (tools/splitkv_bench.py --check); and the
+    combine fused into the decode kernel (ep_spliced_attention_splitkv)."""
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(29533 + batch),
            os.path.join(ROOT, "tools", "splitkv_bench.py"), "--batch", str(batch), "--steps", "3",
-           "--check", "--combine", "peer", "nccl"]
+           "--check", "--combine", "peer", "nccl", "fused"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     print(r.stdout)
-    assert r.stdout.count('"check_ok": true') == 2, r.stdout
+    assert r.stdout.count('"check_ok": true') == 3, r.stdout
+
+
+_FUSED_EMULATED = r"""
+import os, sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, os.path.join({root!r}, "tools"))
+import torch
+import splitkv_bench as SB
+from paper_2504_11729_b200.attention import Handle
+from paper_2504_11729_b200.splitkv import PeerSplitKVCombine
+world, batch, cloud, edge = {world}, 3, 8192, 200
+rows, D, HQ = batch * SB.HQ, SB.D, SB.HQ
+handles = [Handle(0) for _ in range(world)]
+groups = PeerSplitKVCombine.local_group(world, rows, D, handles)
+ranks = [SB.build_local(batch, world, r, handles[r], cloud=cloud, edge=edge) for r in range(world)]
+_, _, attn1, q1, _ = SB.build_local(batch, 1, 0, handles[0], cloud=cloud, edge=edge)
+want_o, want_l = attn1(q1, o_dtype=torch.float32)
+streams = [torch.cuda.Stream() for _ in range(world)]
+torch.cuda.synchronize()
+for step in range(4):
+    outs = []
+    for r in range(world):
+        _, _, attn, q, _ = ranks[r]
+        dt = torch.bfloat16 if step == 3 else torch.float32
+        o = torch.full(q.shape, float("nan"), dtype=dt, device="cuda")
+        l = torch.full(tuple(q.shape[:3]), float("nan"), device="cuda")
+        groups[r].attend(attn, q, out=o, out_lse=l, stream=streams[r])
+        outs.append((o, l))
+    torch.cuda.synchronize()
+    for r, (o, l) in enumerate(outs):
+        tol = 2e-2 if step == 3 else 1e-4
+        err = (o.float() - want_o).abs().max().item()
+        lerr = (l - want_l).abs().max().item()
+        assert err < tol and lerr < 1e-4, (step, r, err, lerr)
+        assert torch.equal(o, outs[0][0]) and torch.equal(l, outs[0][1]), (step, r)  # identical on every rank
+    print("step", step, "ok", err, lerr)
+for g in groups:
+    g.close()
+print("FUSED_OK")
+"""
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_splitkv_emulated_ranks(world):
+    """ep_spliced_attention_splitkv (K1 with the cross-rank exchange fused in)
+    with `world` ranks emulated on one GPU — each rank's plan on 148 / world
+    SMs (EP_K1_CTAS) so all ranks' kernels run side by side, one stream each:
+    every rank's merged rows equal the unsharded run (and each other,
+    bit-identically), over 4 steps (epoch parity, buffer reuse, bf16 out)."""
+    env = dict(os.environ, EP_K1_CTAS=str(148 // world))
+    code = _FUSED_EMULATED.format(root=ROOT, world=world)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0 and "FUSED_OK" in r.stdout, r.stdout + r.stderr[-3000:]

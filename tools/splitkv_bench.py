@@ -100,7 +100,8 @@ def oracle_check(pool1, q1, b, heads, out, out_lse, cloud=CLOUD, edge=EDGE):
 
 def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CLOUD):
     """combine: "peer" = one ep_splitkv_combine_dev kernel over NVLink peer
-    memory; "nccl" = NCCL all-gather + K5 merge. graph: replay the step
+    memory; "nccl" = NCCL all-gather + K5 merge; "fused" = the combine inside
+    the decode kernel (ep_spliced_attention_splitkv). graph: replay the step
     (attention + combine) as one CUDA graph (removes host launch overhead)."""
     import torch
     import torch.distributed as dist
@@ -113,8 +114,9 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     rows = batch * HQ
     comb = None
     if world > 1:
-        comb = (PeerSplitKVCombine(world, rank, rows, D, h) if combine == "peer" else
+        comb = (PeerSplitKVCombine(world, rank, rows, D, h) if combine in ("peer", "fused") else
                 SplitKVCombine(world, rows, D, handle=h, device="cuda"))
+    fused = world > 1 and combine == "fused"
     o_part = torch.empty((batch, 1, HQ, D), dtype=torch.float32, device="cuda")
     lse_part = torch.empty((batch, 1, HQ), dtype=torch.float32, device="cuda")
     out = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
@@ -122,6 +124,9 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     stream = torch.cuda.current_stream()
 
     def step(st=stream):
+        if fused:  # one kernel: local pass + NVLink exchange + rank-order merge
+            comb.attend(attn, q, out=out.view(batch, 1, HQ, D), out_lse=out_lse.view(batch, 1, HQ), stream=st)
+            return
         attn(q, o=o_part, lse=lse_part, stream=st)
         if comb is not None:
             comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=st)
@@ -168,7 +173,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_attn, t_step = float(t[0]), float(t[1])
     per_rank = None
-    if world > 1:
+    if world > 1 and not fused:
         # where the step goes on each rank: attention vs combine (incl. waiting for peers)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps + 1)]
         torch.cuda.synchronize()
@@ -248,7 +253,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--check", action="store_true")
-    ap.add_argument("--combine", choices=["peer", "nccl"], nargs="+", default=["peer"])
+    ap.add_argument("--combine", choices=["peer", "nccl", "fused"], nargs="+", default=["peer"])
     ap.add_argument("--graph", action="store_true")
     ap.add_argument("--cloud", type=int, default=CLOUD,
                     help="cloud tokens (e.g. 131072 / P on one GPU = one rank's local pass)")
