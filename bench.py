@@ -492,9 +492,10 @@ def run_sharded(args, world, rank, local_rank):
     out = torch.empty((rows, D), dtype=torch.bfloat16, device="cuda")
     out_lse = torch.empty((rows,), dtype=torch.float32, device="cuda")
 
-    def step(qq=q):
-        attn(qq, o=o_part, lse=lse_part, stream=stream)
-        comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=stream)
+    out4, out_lse4 = out.view(SKV_B, 1, HQ, D), out_lse.view(SKV_B, 1, HQ)
+
+    def step(qq=q):  # ONE kernel per rank: local K1 pass + NVLink exchange + rank-order merge
+        comb.attend(attn, qq, out=out4, out_lse=out_lse4, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -519,24 +520,11 @@ def run_sharded(args, world, rank, local_rank):
         l0 = h.launch_count()
         ms = timed(step, steps)
         launches = h.launch_count() - l0
-    # inside the step: the local pass (the HBM-bound kernel) and the combine
-    # (incl. waiting for the slowest peer), per-step events, max over ranks
-    n_split = max(5, min(steps, 200))
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_split + 1)]
-    dist.barrier()
-    torch.cuda.synchronize()
-    ev[0].record(stream)
-    for i in range(n_split):
-        attn(q, o=o_part, lse=lse_part, stream=stream)
-        ev[2 * i + 1].record(stream)
-        comb(o_part.view(rows, D), lse_part.view(rows), out=out, out_lse=out_lse, stream=stream)
-        ev[2 * i + 2].record(stream)
-    torch.cuda.synchronize()
-    split = torch.tensor([sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(n_split)) / n_split,
-                          sum(ev[2 * i + 1].elapsed_time(ev[2 * i + 2]) for i in range(n_split)) / n_split],
-                         device="cuda")
-    dist.all_reduce(split, op=dist.ReduceOp.MAX)
-    ms_local, combine_ms = float(split[0]), float(split[1])
+    # the local pass alone (the same K1 over the shard without the exchange):
+    # the HBM-bound part of the step; the rest of the fused step is the
+    # exchange and the wait for the slowest rank
+    ms_local = timed(lambda: attn(q, o=o_part, lse=lse_part, stream=stream), steps)
+    combine_ms = max(ms - ms_local, 0.0)
 
     # e2e through the public API with host buffers: every step copies the
     # batch's query rows from pinned host memory and reads the merged output
@@ -588,8 +576,8 @@ def run_sharded(args, world, rank, local_rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": skv_workload(world), "global_batch": SKV_B, "seq_len": SKV_CLOUD + SKV_EDGE,
-                   "parallelism": f"split-KV x{world}: contiguous cloud-KV shards, one per GPU; "
-                                  "(o, lse) combine = one peer-memory kernel over NVLink",
+                   "parallelism": f"split-KV x{world}: contiguous cloud-KV shards, one per GPU; the "
+                                  "(o, lse) combine fused into the decode kernel over NVLink peer memory",
                    "l2": f"inputs larger than L2 ({loc_bytes / 1e9:.1f} GB of KV per rank per step), no flush"},
         "value_1gpu": (SKV_B / (ms_1 / 1e3)) if ms_1 else None,
         "ms_per_step_1gpu": ms_1,
@@ -600,14 +588,15 @@ def run_sharded(args, world, rank, local_rank):
                              "requests) / the local K1 time inside the step (per-step CUDA events, "
                              "max over ranks)"},
         "combine": {"ms": combine_ms, "bytes_received_per_rank": gather_bytes,
-                    "nvlink_gbs": gather_bytes / (combine_ms / 1e3) / 1e9,
-                    "nvlink_frac": gather_bytes / (combine_ms / 1e3) / 900e9,
-                    "note": "per-step events around the combine kernel, max over ranks (includes "
-                            "waiting for the slowest peer); latency-bound (tiny messages)"},
+                    "nvlink_gbs": gather_bytes / (combine_ms / 1e3) / 1e9 if combine_ms > 0 else None,
+                    "nvlink_frac": gather_bytes / (combine_ms / 1e3) / 900e9 if combine_ms > 0 else None,
+                    "note": "fused step - local pass alone (max over ranks): the exchange and the wait "
+                            "for the slowest rank; latency-bound (tiny messages)"},
         "e2e": {"value": SKV_B / (ms_e2e / 1e3), "unit": "tokens/s",
                 "h2d_bytes_per_step": q.numel() * 2, "d2h_bytes_per_step": rows * D * 2,
                 "ms_per_step": ms_e2e, "result_check": ok,
-                "path": "SplicedAttention + PeerSplitKVCombine (the C-ABI calls) with pinned host q / output"},
+                "path": "PeerSplitKVCombine.attend = ep_spliced_attention_splitkv (the C-ABI call) with "
+                        "pinned host q / output"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
@@ -619,7 +608,7 @@ def run_sharded(args, world, rank, local_rank):
         extras = {}
         # config 4 at batch 1 (latency): both combines
         skv = {}
-        for cmb in ("peer", "nccl"):
+        for cmb in ("fused", "peer", "nccl"):
             skv[f"batch1_{cmb}"] = SB.run(1, max(5, min(steps, 30)), 3, combine=cmb)
             gc.collect()
             torch.cuda.empty_cache()

@@ -98,7 +98,7 @@ def oracle_check(pool1, q1, b, heads, out, out_lse, cloud=CLOUD, edge=EDGE):
     return e_o, e_l
 
 
-def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CLOUD):
+def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CLOUD, edge=EDGE):
     """combine: "peer" = one ep_splitkv_combine_dev kernel over NVLink peer
     memory; "nccl" = NCCL all-gather + K5 merge; "fused" = the combine inside
     the decode kernel (ep_spliced_attention_splitkv). graph: replay the step
@@ -110,7 +110,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     h = Handle(torch.cuda.current_device())
-    pool, table, attn, q, n_loc = build_local(batch, world, rank, h, cloud=cloud)
+    pool, table, attn, q, n_loc = build_local(batch, world, rank, h, cloud=cloud, edge=edge)
     rows = batch * HQ
     comb = None
     if world > 1:
@@ -169,7 +169,11 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     t_attn = e[0].elapsed_time(e[1]) / steps
     t_step = e[2].elapsed_time(e[3]) / steps
     t = torch.tensor([t_attn, t_step], device="cuda")
+    per_rank_times = None
     if world > 1:
+        allt = torch.empty((world, 2), device="cuda")
+        dist.all_gather_into_tensor(allt, t)
+        per_rank_times = [[round(float(x), 4) for x in r] for r in allt.cpu()]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_attn, t_step = float(t[0]), float(t[1])
     per_rank = None
@@ -199,7 +203,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     loc_bytes = batch * n_loc * 2 * HKV * D * 2
     gather_bytes = (world - 1) * rows * (D + 1) * 4  # received per rank
     res = {
-        "workload": f"cfg4 split-KV: {cloud} cloud + {EDGE} edge keys, Hq=32 Hkv=8 d=128 bf16, "
+        "workload": f"cfg4 split-KV: {cloud} cloud + {edge} edge keys, Hq=32 Hkv=8 d=128 bf16, "
                     f"batch {batch}, {world} GPU(s)",
         "batch": batch, "gpus": world, "combine": combine if world > 1 else None, "step_ms": t_step, "local_attention_ms": t_attn,
         "combine_ms": (max(r[1] for r in per_rank) if per_rank else 0.0),
@@ -219,6 +223,8 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
     }
     if per_rank is not None:
         res["per_rank_attention_combine_ms"] = per_rank
+    if per_rank_times is not None:
+        res["per_rank_attention_b2b_step_ms"] = per_rank_times
     if check:
         ok = True
         if world > 1:
@@ -226,7 +232,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
             # fp64 oracle recomputes sampled units of the last request from
             # the same pages (merge in rank = segment order, attention.cpp:116-145)
             if rank == 0:
-                pool1, table1, attn1, q1, _ = build_local(batch, 1, 0, h)
+                pool1, table1, attn1, q1, _ = build_local(batch, 1, 0, h, cloud=cloud, edge=edge)
                 o1, l1 = attn1(q1, o_dtype=torch.float32)
                 torch.cuda.synchronize()
                 err = (out.float() - o1.reshape(rows, D)).abs().max().item()
@@ -234,7 +240,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
                 res["check_max_abs_err"] = err
                 res["check_lse_max_abs_err"] = lerr
                 ok = err < 2e-2 and lerr < 1e-3
-                e_o, e_l = oracle_check(pool1, q1, batch - 1, [0, 13, 31], out, out_lse, cloud)
+                e_o, e_l = oracle_check(pool1, q1, batch - 1, [0, 13, 31], out, out_lse, cloud, edge)
                 res["check_oracle_rel_err"] = e_o
                 res["check_oracle_lse_rel_err"] = e_l
                 ok = ok and e_o <= 2e-2 and e_l <= 1e-4
@@ -255,6 +261,7 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--combine", choices=["peer", "nccl", "fused"], nargs="+", default=["peer"])
     ap.add_argument("--graph", action="store_true")
+    ap.add_argument("--edge", type=int, default=EDGE)
     ap.add_argument("--cloud", type=int, default=CLOUD,
                     help="cloud tokens (e.g. 131072 / P on one GPU = one rank's local pass)")
     args = ap.parse_args()
@@ -269,7 +276,7 @@ def main():
     for cmb in args.combine:
         for b in args.batch:
             r = run(b, args.steps, args.warmup, check=args.check, combine=cmb, graph=args.graph,
-                    cloud=args.cloud)
+                    cloud=args.cloud, edge=args.edge)
             if int(os.environ.get("RANK", "0")) == 0:
                 print(json.dumps(r), flush=True)
     if world > 1:
