@@ -152,6 +152,56 @@ int ep_plan_create(ep_handle h, const ep_kv_pool* pool, int32_t n_q_heads, int32
  * reused when large enough, so captured CUDA graphs stay valid. */
 int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
                    const int32_t* page_table, const int64_t* q_pos, ep_stream stream);
+/* ==================================================================== */
+/* 2b. Splice state: SegmentedCache (cache.hpp:30-61) as a C-ABI object.  */
+/* ==================================================================== */
+
+/* Per layer and request, an ordered list of segments {origin, pos_offset,
+ * len, pages} over the layer's page pool — the reference's per-layer
+ * KVSegment lists with the K/V living in device pages. Host-only (no CUDA
+ * calls); not thread-safe (one mutator per cache). */
+typedef struct ep_cache_s* ep_cache;
+int ep_cache_create(int32_t n_layers, int32_t batch, int32_t page_tokens, ep_cache* out);
+int ep_cache_destroy(ep_cache c);
+/* SegmentedCache::end_position (cache.cpp:21-24): layer 0's end; -1 for a bad request. */
+int64_t ep_cache_end_position(ep_cache c, int32_t b);
+/* SegmentedCache::append (cache.cpp:25-53) for request b: layer = -1 appends
+ * the segment to every layer (the common case: page ids shared by the layers'
+ * pools), layer >= 0 to that layer only (K/V arriving layer by layer). Every
+ * invariant is checked for every affected layer before anything changes
+ * (atomic): contiguous with the end, non-empty, origin order cloud -> edge ->
+ * generated; EP_EINVAL with the reference's messages. */
+int ep_cache_append(ep_cache c, int32_t layer, int32_t b, int32_t origin, int64_t pos_offset, int32_t len,
+                    const int32_t* pages, int32_t n_pages);
+/* append_generated_token (cache.cpp:55-80) for the whole batch, every layer:
+ * request b's trailing generated segment grows by n_tokens[b] (created at the
+ * end if absent), no copy — the new tokens take the last page's free slots,
+ * then pages new_pages[b * max_new ..] (pages_used[b] of them). dst_page /
+ * dst_slot [sum n_tokens] receive where each new token's K/V row goes (for
+ * ep_kv_append or a projection epilogue). */
+int ep_cache_append_generated(ep_cache c, const int32_t* n_tokens, const int32_t* new_pages, int32_t max_new,
+                              int32_t* dst_page, int32_t* dst_slot, int32_t* pages_used);
+/* Drops the last n_tokens of request b's generated segment in every layer
+ * (rejected speculative drafts); pages no longer used are written to
+ * released (may be NULL) and counted in n_released. */
+int ep_cache_truncate(ep_cache c, int32_t b, int32_t n_tokens, int32_t* released, int32_t* n_released);
+/* SegmentedCache::check_consistent (cache.cpp:82-103): gapless coverage,
+ * origin order and identical position ranges across layers, per request;
+ * EP_EINVAL with the reference's description ("gap in position coverage",
+ * "origin order violated", "layers cover different position ranges", ...). */
+int ep_cache_check_consistent(ep_cache c);
+/* One layer's table in the ep_plan_create layout (seg_indptr [batch+1],
+ * segs, page_table); seg_indptr = NULL only reports the sizes. */
+int ep_cache_layer_arrays(ep_cache c, int32_t layer, int64_t* seg_indptr, ep_segment* segs, int64_t segs_cap,
+                          int32_t* page_table, int64_t pages_cap, int64_t* n_segs, int64_t* n_pages);
+/* Plans straight from the cache: request b's queries are its last n_q
+ * positions (decode_step: n_q = 1; verify: k + 1). ep_plan_update_cache
+ * re-plans after the cache grew (per-token growth: a host rebuild of a few
+ * microseconds plus one async upload). */
+int ep_plan_create_cache(ep_handle h, const ep_kv_pool* pool, ep_cache c, int32_t layer, int32_t n_q_heads,
+                         int32_t n_q, ep_plan* out);
+int ep_plan_update_cache(ep_plan p, ep_cache c, int32_t layer, int32_t n_q, ep_stream stream);
+
 /* Prefill plan — the cloud-prompt / edge prefill attention tiles (prefill,
  * model.cpp:211-236 -> transformer_layer's attention block, model.cpp:161-182;
  * CloudServer::serve_stream, cloud.cpp:160-172). The LAST n_new[b] tokens of

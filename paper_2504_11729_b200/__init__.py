@@ -22,7 +22,7 @@ __all__ = [
 def __getattr__(name):
     # torch-dependent modules load on first use so the CPU test suite and
     # `import paper_2504_11729_b200` stay torch-free.
-    if name in ("KVPool", "SpliceTable", "SplicedAttention", "SegmentRef"):
+    if name in ("KVPool", "SpliceTable", "SplicedAttention", "SegmentRef", "SpliceCache"):
         from . import splice
         return getattr(splice, name)
     if name in ("VerifyGreedy",):

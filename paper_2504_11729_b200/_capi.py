@@ -136,6 +136,18 @@ _SIGS = {
     "ep_kv_append": (C.c_int, [_vp, C.POINTER(KVPoolDesc), C.c_int32, _vp, _vp, _vp, _vp, _vp]),
     "ep_kv_ingest_frame": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, _sz, _vp, C.c_int32,
                                      C.POINTER(KVFrameInfo), _vp]),
+    "ep_cache_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "ep_cache_destroy": (C.c_int, [_vp]),
+    "ep_cache_end_position": (C.c_int64, [_vp, C.c_int32]),
+    "ep_cache_append": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32, _vp, C.c_int32]),
+    "ep_cache_append_generated": (C.c_int, [_vp, _vp, _vp, C.c_int32, _vp, _vp, _vp]),
+    "ep_cache_truncate": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.POINTER(C.c_int32)]),
+    "ep_cache_check_consistent": (C.c_int, [_vp]),
+    "ep_cache_layer_arrays": (C.c_int, [_vp, C.c_int32, _vp, _vp, C.c_int64, _vp, C.c_int64,
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ep_plan_create_cache": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, C.c_int32, C.c_int32, C.c_int32,
+                                       C.POINTER(_vp)]),
+    "ep_plan_update_cache": (C.c_int, [_vp, _vp, C.c_int32, C.c_int32, _vp]),
     "ep_kv_ingest_frame_async": (C.c_int, [_vp, C.POINTER(KVPoolDesc), _vp, _sz, _vp, C.c_int32,
                                            _vp]),
     "ep_kv_ingest_poll": (C.c_int, [_vp, _vp, C.POINTER(KVFrameInfo)]),

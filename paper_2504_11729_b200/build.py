@@ -29,7 +29,8 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", f"-I{INCL
 CU_FLAGS = ARCH + COMMON + ["--expt-relaxed-constexpr", "-Xptxas", "-O3"]
 
 SOURCES = ["kern_reference.cu", "kern_decode.cu", "kern_verify.cu", "kern_score.cu", "kern_peer.cu",
-           "kern_ingest.cu", "kern_model.cu", "kern_model_persist.cu", "capi.cpp", "plan.cpp", "model.cpp"]
+           "kern_ingest.cu", "kern_model.cu", "kern_model_persist.cu", "capi.cpp", "plan.cpp", "model.cpp",
+           "cache.cpp"]
 HEADERS = ["ep_common.cuh", "ep_internal.h", "umma.cuh", "merge.cuh", "model_internal.h"]
 PUBLIC_HEADERS = ["ep_attn.h", "ep_model.h"]
 

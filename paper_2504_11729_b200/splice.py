@@ -321,6 +321,88 @@ class SpliceTable:
         return indptr, segs_arr, np.ascontiguousarray(pt)
 
 
+class SpliceCache:
+    """ep_cache — SegmentedCache (cache.hpp:30-61, cache.cpp:16-103) as the
+    library's own host object for a batch of sessions over paged KV: per
+    layer and request an ordered segment list {origin, pos_offset, len,
+    pages}. Plans read it directly (SplicedAttention.from_cache), so growing
+    every session by one token per step costs a C++ rebuild, not Python."""
+
+    def __init__(self, n_layers: int, batch: int, page_tokens: int = 64):
+        c = C.c_void_p()
+        check(lib().ep_cache_create(n_layers, batch, page_tokens, C.byref(c)), "ep_cache_create")
+        self._c = c
+        self.n_layers, self.batch, self.page_tokens = n_layers, batch, page_tokens
+
+    @property
+    def ptr(self):
+        return self._c
+
+    def end_position(self, b: int) -> int:
+        return int(lib().ep_cache_end_position(self._c, b))
+
+    def append(self, b: int, origin: int, pos_offset: int, length: int, pages, layer: int = -1) -> None:
+        """SegmentedCache::append (cache.cpp:25-53), validated then applied;
+        layer = -1: every layer (shared page ids)."""
+        pg = np.ascontiguousarray(pages, dtype=np.int32)
+        check(lib().ep_cache_append(self._c, layer, b, origin, pos_offset, length,
+                                    pg.ctypes.data if pg.size else None, int(pg.size)), "ep_cache_append")
+
+    def append_generated(self, n_tokens, new_pages=None):
+        """append_generated_token (cache.cpp:55-80) for the batch: request b
+        grows by n_tokens[b]; new_pages [B][max_new] supplies pages when the
+        last page is full. Returns (dst_page, dst_slot, pages_used)."""
+        n = np.ascontiguousarray(n_tokens, dtype=np.int32)
+        assert n.size == self.batch
+        npg = (np.ascontiguousarray(new_pages, dtype=np.int32).reshape(self.batch, -1)
+               if new_pages is not None else np.zeros((self.batch, 0), np.int32))
+        dst_page = np.zeros(max(1, int(n.sum())), np.int32)
+        dst_slot = np.zeros_like(dst_page)
+        used = np.zeros(self.batch, np.int32)
+        check(lib().ep_cache_append_generated(self._c, n.ctypes.data, npg.ctypes.data if npg.size else None,
+                                              int(npg.shape[1]), dst_page.ctypes.data, dst_slot.ctypes.data,
+                                              used.ctypes.data), "ep_cache_append_generated")
+        k = int(n.sum())
+        return dst_page[:k], dst_slot[:k], used
+
+    def truncate(self, b: int, n_tokens: int) -> np.ndarray:
+        """Drops the last n_tokens generated tokens of request b (rejected
+        drafts); returns the pages no longer used."""
+        rel = np.zeros(max(1, -(-n_tokens // self.page_tokens) + 1), np.int32)
+        nr = C.c_int32()
+        check(lib().ep_cache_truncate(self._c, b, n_tokens, rel.ctypes.data, C.byref(nr)), "ep_cache_truncate")
+        return rel[:nr.value].copy()
+
+    def check_consistent(self) -> str:
+        """cache.cpp:82-103: '' when consistent, else the reason."""
+        rc = lib().ep_cache_check_consistent(self._c)
+        return "" if rc == 0 else lib().ep_last_error().decode()
+
+    def arrays(self, layer: int = 0):
+        """(seg_indptr, segs, page_table) of one layer (ep_plan_create layout)."""
+        ns, npg = C.c_int64(), C.c_int64()
+        check(lib().ep_cache_layer_arrays(self._c, layer, None, None, 0, None, 0, C.byref(ns), C.byref(npg)),
+              "ep_cache_layer_arrays")
+        indptr = np.zeros(self.batch + 1, np.int64)
+        segs = np.zeros(max(1, ns.value), SEGMENT_DTYPE)
+        pt = np.zeros(max(1, npg.value), np.int32)
+        check(lib().ep_cache_layer_arrays(self._c, layer, indptr.ctypes.data, segs.ctypes.data, segs.size,
+                                          pt.ctypes.data, pt.size, C.byref(ns), C.byref(npg)),
+              "ep_cache_layer_arrays")
+        return indptr, segs[:ns.value], pt[:npg.value]
+
+    def close(self):
+        if getattr(self, "_c", None) is not None and self._c.value:
+            lib().ep_cache_destroy(self._c)
+        self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class SplicedAttention:
     """ep_plan over (pool, table): spliced attention for every request."""
 
@@ -340,6 +422,32 @@ class SplicedAttention:
               "ep_plan_create")
         self.plan = plan
 
+    @classmethod
+    def from_cache(cls, pool: KVPool, cache: SpliceCache, n_q_heads: int, n_q: int = 1, layer: int = 0,
+                   handle: Handle | None = None) -> "SplicedAttention":
+        """Plan straight from an ep_cache (ep_plan_create_cache): request b's
+        queries are its last n_q positions. update_from_cache() re-plans after
+        the cache grew (one C++ rebuild + an async upload per step)."""
+        self = cls.__new__(cls)
+        self.pool, self.table, self.cache, self.layer = pool, None, cache, layer
+        self.n_q_heads, self.n_q = n_q_heads, n_q
+        self.handle = handle or default_handle(pool.k.device.index or 0)
+        self._keep = None
+        plan = C.c_void_p()
+        pd = pool.desc()
+        check(lib().ep_plan_create_cache(self.handle.ptr, C.byref(pd), cache.ptr, layer, n_q_heads, n_q,
+                                         C.byref(plan)), "ep_plan_create_cache")
+        self.plan = plan
+        return self
+
+    def update_from_cache(self, stream=None) -> None:
+        check(lib().ep_plan_update_cache(self.plan, self.cache.ptr, self.layer, self.n_q, _stream(stream)),
+              "ep_plan_update_cache")
+
+    @property
+    def batch(self) -> int:
+        return self.table.batch if self.table is not None else self.cache.batch
+
     def update(self, stream=None) -> None:
         """Re-plan after the table changed (ep_plan_update, stream-ordered)."""
         indptr, segs, pt = self.table.arrays()
@@ -356,7 +464,7 @@ class SplicedAttention:
     def __call__(self, q, o=None, lse=None, o_dtype=None, stream=None):
         """q [B][n_q][Hq][d] (bf16/fp32 CUDA tensor) -> (o, lse)."""
         torch = _torch()
-        B, d = self.table.batch, self.pool.d_head
+        B, d = self.batch, self.pool.d_head
         if tuple(q.shape) != (B, self.n_q, self.n_q_heads, d) or not q.is_contiguous():
             raise InvalidArgument(f"SplicedAttention: q must be contiguous "
                                   f"[{B}][{self.n_q}][{self.n_q_heads}][{d}]")
