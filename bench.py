@@ -336,55 +336,100 @@ def main():
         ms = float(t.item())
 
     # ----------------------------------------------------- end-to-end (host) --
-    # Per step, through the public C-ABI: H2D of the step's query rows and the
-    # new (self) token's K/V rows from pinned host memory, ep_kv_append into
-    # the generated page slot, ep_spliced_attention, D2H of the output rows.
-    # The copies run on a copy stream, double-buffered, so step i+1's inputs
-    # arrive and step i-1's output leaves while step i computes (what a
-    # serving loop does); every step still moves its own bytes both ways.
-    q_host = q.cpu().pin_memory()
+    # A decode step as a serving loop runs it, through the public C-ABI, with
+    # the cache GROWING by one token per request per step: the splice state
+    # (ep_cache) gives every request's new token its page slot
+    # (ep_cache_append_generated), the step's query rows and new K/V rows
+    # arrive from pinned host memory together with those slots, ep_kv_append
+    # writes the rows, ep_plan_update_cache re-plans from the grown cache
+    # (host rebuild + async upload), ep_spliced_attention runs, and the
+    # output rows go back to pinned host memory. Copies run on a copy stream,
+    # double-buffered (step i+1's inputs arrive and step i-1's output leaves
+    # while step i computes). The generated segment grows from 1 to 64 tokens
+    # within its page, then is truncated back to 1 (ep_cache_truncate, as a
+    # rejected draft would be), so the workload stays at 4609-4672 keys.
+    from paper_2504_11729_b200.splice import SpliceCache
+    cache = SpliceCache(1, B, P)
+    for b in range(B):
+        for sg in table.requests[b]:
+            cache.append(b, sg.origin, sg.pos_offset, sg.length, sg.pages)
+    attn_e = SplicedAttention.from_cache(pool, cache, HQ, 1, handle=h)
+    # one pinned input blob per buffer j: [q | new K rows | new V rows | page | slot],
+    # one H2D copy per step; copies and events through the CUDA runtime
+    # directly (cuda.bindings), the library through its C-ABI (ctypes)
+    from cuda.bindings import runtime as rt
+    import ctypes as C
+    qb, kvb, slb = q.numel() * 2, 2 * B * HKV * D * 2, 2 * B * 4
+    in_bytes = qb + kvb + slb
+    host_in = [torch.empty(in_bytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    dev_in = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
     kv_rows = torch.empty((2, B, HKV, D), dtype=torch.bfloat16)
     kv_rows[0] = pool.k[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
     kv_rows[1] = pool.v[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
-    kv_host = kv_rows.pin_memory()
+    for j in range(2):
+        host_in[j][:qb].copy_(q.cpu().view(-1).view(torch.uint8))
+        host_in[j][qb:qb + kvb].copy_(kv_rows.view(-1).view(torch.uint8))
+    slots_np = [host_in[j][qb + kvb:].numpy().view(np.int32).reshape(2, B) for j in range(2)]
     o_host = [torch.empty_like(o, device="cpu").pin_memory() for _ in range(2)]
-    q_dev = [torch.empty_like(q) for _ in range(2)]
-    kv_dev = [torch.empty_like(kv_host, device="cuda") for _ in range(2)]
     o_dev = [torch.empty_like(o) for _ in range(2)]
-    dst_page = torch.tensor([b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)],
-                            dtype=torch.int32, device="cuda")
-    dst_slot = torch.zeros(B, dtype=torch.int32, device="cuda")
+    ones = np.ones(B, np.int32)
     pd = pool.desc()
-    import ctypes as C
+    pd_ref = C.byref(pd)
+    in_ptr = [(host_in[j].data_ptr(), dev_in[j].data_ptr()) for j in range(2)]
+    q_ptr = [dev_in[j].data_ptr() for j in range(2)]
+    append_ptrs = [(dev_in[j].data_ptr() + qb + kvb, dev_in[j].data_ptr() + qb + kvb + 4 * B,
+                    dev_in[j].data_ptr() + qb, dev_in[j].data_ptr() + qb + kvb // 2) for j in range(2)]
+    o_ptr = [(o_dev[j].data_ptr(), o_host[j].data_ptr()) for j in range(2)]
+    ob = o.numel() * 2
     copy = torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]    # inputs of buffer j landed
-    ev_done = [torch.cuda.Event() for _ in range(2)]  # attention on buffer j finished
-    ev_out = [torch.cuda.Event() for _ in range(2)]   # output of buffer j read back
+    cs = copy.cuda_stream
+    H2D, D2H = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
+
+    def mkev():
+        err, ev = rt.cudaEventCreateWithFlags(rt.cudaEventDisableTiming)
+        assert err == rt.cudaError_t.cudaSuccess
+        return ev
+
+    ev_in = [mkev() for _ in range(2)]    # inputs of buffer j landed
+    ev_done = [mkev() for _ in range(2)]  # attention on buffer j finished
+    ev_out = [mkev() for _ in range(2)]   # output of buffer j read back
+    gen = {"len": 1}
+    plan, cptr = attn_e.plan, cache.ptr
+
+    def grow(j):
+        """This step's token per request: a slot in the cache (host) -> pinned blob j."""
+        if gen["len"] == P:
+            for b in range(B):
+                cache.truncate(b, P - 1)
+            gen["len"] = 1
+        rt.cudaEventSynchronize(ev_in[j])  # the pinned blob j is free again
+        sl = slots_np[j]
+        cache.append_generated(ones, out=(sl[0], sl[1]))
+        gen["len"] += 1
 
     def h2d(j):
-        with torch.cuda.stream(copy):
-            copy.wait_event(ev_done[j])  # buffer j's previous attention is done
-            q_dev[j].copy_(q_host, non_blocking=True)
-            kv_dev[j].copy_(kv_host, non_blocking=True)
-            ev_in[j].record(copy)
+        rt.cudaStreamWaitEvent(cs, ev_done[j], 0)  # buffer j's previous attention is done
+        rt.cudaMemcpyAsync(in_ptr[j][1], in_ptr[j][0], in_bytes, H2D, cs)
+        rt.cudaEventRecord(ev_in[j], cs)
 
     def e2e_run(n):
+        grow(0)
         h2d(0)
         for i in range(n):
             j = i & 1
+            _capi.check(lib.ep_plan_update_cache(plan, cptr, 0, 1, sp))  # the plan of the grown cache
             if i + 1 < n:
+                grow(j ^ 1)
                 h2d(j ^ 1)
-            stream.wait_event(ev_in[j])
-            stream.wait_event(ev_out[j])  # o_dev[j] of step i-2 has been read back
-            _capi.check(lib.ep_kv_append(h.ptr, C.byref(pd), B, dst_page.data_ptr(),
-                                         dst_slot.data_ptr(), kv_dev[j][0].data_ptr(),
-                                         kv_dev[j][1].data_ptr(), sp))
-            attn(q_dev[j], o=o_dev[j], lse=lse, stream=stream)
-            ev_done[j].record(stream)
-            with torch.cuda.stream(copy):
-                copy.wait_event(ev_done[j])
-                o_host[j].copy_(o_dev[j], non_blocking=True)
-                ev_out[j].record(copy)
+            rt.cudaStreamWaitEvent(sp, ev_in[j], 0)
+            rt.cudaStreamWaitEvent(sp, ev_out[j], 0)  # o_dev[j] of step i-2 has been read back
+            _capi.check(lib.ep_kv_append(h.ptr, pd_ref, B, *append_ptrs[j], sp))
+            _capi.check(lib.ep_spliced_attention(h.ptr, plan, pd_ref, _capi.EP_BF16, q_ptr[j], _capi.EP_BF16,
+                                                 o_ptr[j][0], lse.data_ptr(), sp))
+            rt.cudaEventRecord(ev_done[j], sp)
+            rt.cudaStreamWaitEvent(cs, ev_done[j], 0)
+            rt.cudaMemcpyAsync(o_ptr[j][1], o_ptr[j][0], ob, D2H, cs)
+            rt.cudaEventRecord(ev_out[j], cs)
         stream.wait_stream(copy)
 
     e2e_run(args.warmup)
@@ -396,15 +441,35 @@ def main():
     e0.record(stream)
     stream.wait_event(e0)
     copy.wait_stream(stream)
-    e2e_run(args.steps)
+    h0 = time.perf_counter()
+    if os.environ.get("EP_E2E_PROFILE"):
+        import cProfile
+        import pstats
+        pr = cProfile.Profile()
+        pr.enable()
+        e2e_run(args.steps)
+        pr.disable()
+        pstats.Stats(pr, stream=sys.stderr).sort_stats("tottime").print_stats(18)
+    else:
+        e2e_run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
+    host_us_e2e = (time.perf_counter() - h0) / args.steps * 1e6
     ms_e2e = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms_e2e], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
-    ok = bool(torch.equal(o_host[(args.steps - 1) & 1].to("cuda"), o))
+    # the last step's output equals a device-side recomputation on the same cache
+    o_chk = torch.empty_like(o)
+    attn_e(q, o=o_chk, lse=lse, stream=stream)
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(o_host[(args.steps - 1) & 1].to("cuda"), o_chk))
+    keys_e2e = [cache.end_position(b) for b in range(B)]
+    attn_e.close()
+    cache.close()
+    for ev in ev_in + ev_done + ev_out:
+        rt.cudaEventDestroy(ev)
 
     tokens_per_step = B * world
     value = tokens_per_step / (ms / 1e3)
@@ -436,9 +501,14 @@ def main():
                              "step; time = K1 decode + K2 merge per step (CUDA events)",
                      "frac_of_8tbs_nominal": achieved / 8000.0},
         "e2e": {"value": tokens_per_step / (ms_e2e / 1e3), "unit": "tokens/s",
-                "h2d_bytes_per_step": q.numel() * 2 + kv_host.numel() * 2,
+                "h2d_bytes_per_step": in_bytes,
                 "d2h_bytes_per_step": o.numel() * 2, "ms_per_step": ms_e2e,
+                "host_us_per_step": host_us_e2e,
                 "result_check": ok,
+                "cache_growth": "one token per request per step into the generated segment "
+                                "(ep_cache_append_generated -> ep_kv_append -> ep_plan_update_cache), "
+                                f"truncated back every {P - 1} steps; keys per request 4609..4672 "
+                                f"(last step {min(keys_e2e)}..{max(keys_e2e)})",
                 "overlap": "H2D of step i+1 and D2H of step i-1 on a copy stream "
                            "(double-buffered) while step i computes"},
         "gpu_launches": int(launches),

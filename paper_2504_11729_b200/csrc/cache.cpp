@@ -34,6 +34,10 @@ struct Seg {
 
 struct ep_cache_s {
     int32_t n_layers = 0, batch = 0, page_tokens = 0;
+    // bumped by every change other than tokens landing in already-listed
+    // pages (append, a new page, truncation): a plan built at this version
+    // can follow pure in-page growth without re-planning
+    uint64_t structure_version = 1;
     std::vector<std::vector<std::vector<Seg>>> seg;  // [layer][request] -> segments
     // flattened arrays of one layer (rebuilt on demand for the plan builders)
     std::vector<int64_t> indptr;
@@ -141,6 +145,7 @@ int ep_cache_append(ep_cache c, int32_t layer, int32_t b, int32_t origin, int64_
     for (int l = l0; l < l1; ++l)
         c->seg[l][b].push_back(Seg{origin, pos_offset, len,
                                    std::vector<int32_t>(pages, pages + pages_for(len, c->page_tokens))});
+    c->structure_version++;
     return EP_OK;
 }
 
@@ -175,10 +180,14 @@ int ep_cache_append_generated(ep_cache c, const int32_t* n_tokens, const int32_t
             const int64_t pos = c->end_position(0, b);
             for (int l = 0; l < c->n_layers; ++l) {
                 auto& segs = c->seg[l][b];
-                if (segs.empty() || segs.back().origin != 2) segs.push_back(Seg{2, pos, 0, {}});
+                if (segs.empty() || segs.back().origin != 2) {
+                    segs.push_back(Seg{2, pos, 0, {}});
+                    c->structure_version++;
+                }
                 Seg& g = segs.back();
                 int32_t u = 0;
                 while (int64_t(g.pages.size()) * P < g.len + n) g.pages.push_back(new_pages[size_t(b) * max_new + u++]);
+                if (u) c->structure_version++;
                 used = u;
                 if (l == 0)
                     for (int32_t i = 0; i < n; ++i) {
@@ -219,6 +228,7 @@ int ep_cache_truncate(ep_cache c, int32_t b, int32_t n_tokens, int32_t* released
         g.pages.resize(keep);
         if (g.len == 0) segs.pop_back();
     }
+    c->structure_version++;
     if (n_released) *n_released = nr;
     return EP_OK;
 }
@@ -258,16 +268,29 @@ int ep_plan_create_cache(ep_handle h, const ep_kv_pool* pool, ep_cache c, int32_
     c->flatten(layer);
     std::vector<int64_t> qp(c->batch);
     for (int b = 0; b < c->batch; ++b) qp[b] = std::max<int64_t>(0, c->end_position(layer, b) - n_q);
-    return ep_plan_create(h, pool, n_q_heads, n_q, c->batch, c->indptr.data(), c->flat.data(), c->pt.data(),
-                          qp.data(), 0, out);
+    if (int rc = ep_plan_create(h, pool, n_q_heads, n_q, c->batch, c->indptr.data(), c->flat.data(), c->pt.data(),
+                                qp.data(), 0, out))
+        return rc;
+    ep::plan_mark_built(*out, c, c->structure_version, layer);
+    return EP_OK;
 }
 
 int ep_plan_update_cache(ep_plan p, ep_cache c, int32_t layer, int32_t n_q, ep_stream stream) {
     if (!c || layer < 0 || layer >= c->n_layers) return fail(EP_EINVAL, "ep_plan_update_cache: bad cache / layer");
+    std::vector<int64_t> ends(c->batch);
+    for (int b = 0; b < c->batch; ++b) ends[b] = c->end_position(layer, b);
+    // pure in-page growth since the plan's last full build from this cache:
+    // O(batch) page-descriptor refresh, no re-plan
+    const int fast = ep::plan_grow_in_place(p, c, c->structure_version, layer, ends.data(), n_q,
+                                            static_cast<cudaStream_t>(stream));
+    if (fast < 0) return -fast;
+    if (fast == 1) return EP_OK;
     c->flatten(layer);
     std::vector<int64_t> qp(c->batch);
-    for (int b = 0; b < c->batch; ++b) qp[b] = std::max<int64_t>(0, c->end_position(layer, b) - n_q);
-    return ep_plan_update(p, c->indptr.data(), c->flat.data(), c->pt.data(), qp.data(), stream);
+    for (int b = 0; b < c->batch; ++b) qp[b] = std::max<int64_t>(0, ends[b] - n_q);
+    if (int rc = ep_plan_update(p, c->indptr.data(), c->flat.data(), c->pt.data(), qp.data(), stream)) return rc;
+    ep::plan_mark_built(p, c, c->structure_version, layer);
+    return EP_OK;
 }
 
 }  // extern "C"

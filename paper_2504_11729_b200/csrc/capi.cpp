@@ -31,11 +31,12 @@ int cuda_fail(cudaError_t e, const char* where) {
 }
 
 DeviceBuffer::~DeviceBuffer() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && !view) cudaFree(ptr);
 }
 
 cudaError_t DeviceBuffer::reserve(size_t n) {
     if (n <= bytes) return cudaSuccess;
+    if (view) return cudaErrorInvalidValue;  // views are sized by their owner
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     bytes = 0;

@@ -28,6 +28,7 @@ int cuda_fail(cudaError_t e, const char* where);
 struct DeviceBuffer {
     void* ptr = nullptr;
     size_t bytes = 0;
+    bool view = false;  // a slice of another buffer (a plan's arena): not freed here
     ~DeviceBuffer();
     cudaError_t reserve(size_t n);
 };
@@ -150,6 +151,15 @@ int peer_link_fill(ep_peer_group g, int64_t n_units, int64_t rows, int d, const 
 int collect_request_pages(int page_tokens, int64_t num_pages, int b, const int64_t* seg_indptr,
                           const ep_segment* segs, const int32_t* page_table, std::vector<PageDesc>& out,
                           int64_t* first_pages);
+
+// ep_cache <-> plan: the plan remembers which cache (and structure version,
+// layer) it was last fully built from; plan_grow_in_place then follows pure
+// in-page growth of every request to ends[b] (query rows end - n_q) with an
+// O(batch) page-descriptor refresh and one staged upload. Returns 1 applied,
+// 0 a full rebuild is needed, < 0 an error (negated status).
+void plan_mark_built(ep_plan p, const void* cache, uint64_t version, int layer);
+int plan_grow_in_place(ep_plan p, const void* cache, uint64_t version, int layer, const int64_t* ends, int n_q,
+                       cudaStream_t s);
 
 // Device copy of a plan's per-request query positions (a device-resident
 // rollout advances them in place, one token per step).

@@ -244,17 +244,37 @@ struct ep_plan_s {
     std::vector<int64_t> q_pos;
     std::vector<uint8_t> has_shared;  // per request (cascade)
     DeviceBuffer d_qpos, d_has_shared, d_parts_o, d_parts_lse, d_qrow0;
-    // staging for stream-ordered updates
-    void* h_stage = nullptr;
-    size_t h_stage_bytes = 0;
-    cudaEvent_t staged = nullptr;
+    // every uploaded plan array lives in ONE device arena (views above and in
+    // the sub-plans), each part with some capacity slack: an update is one
+    // pinned-staged H2D copy, and the views stay put (captured CUDA graphs
+    // stay valid) until a part outgrows its capacity
+    DeviceBuffer arena;
+    std::vector<size_t> arena_cap;
+    // ep_cache the plan was last fully built from (ep_plan_create_cache / a
+    // full ep_plan_update_cache): identity, structure version, layer
+    const void* built_cache = nullptr;
+    uint64_t built_version = 0;
+    int built_layer = -1;
+    // staging for stream-ordered updates: a ring of pinned buffers, so an
+    // update waits only for the upload kStageRing updates back (the host
+    // stays ahead of the GPU in a serving loop)
+    static constexpr int kStageRing = 4;
+    void* h_stage[kStageRing] = {};
+    size_t h_stage_bytes[kStageRing] = {};
+    cudaEvent_t staged[kStageRing] = {};
+    int stage_idx = 0;
     CUtensorMap tmap_k{}, tmap_v{};
     const void* tm_k = nullptr;
     const void* tm_v = nullptr;
     int64_t tm_pages = -1;
     ~ep_plan_s() {
-        if (h_stage) cudaFreeHost(h_stage);
-        if (staged) cudaEventDestroy(staged);
+        for (int i = 0; i < kStageRing; ++i) {
+            if (staged[i]) {
+                cudaEventSynchronize(staged[i]);
+                cudaEventDestroy(staged[i]);
+            }
+            if (h_stage[i]) cudaFreeHost(h_stage[i]);
+        }
         if (side) cudaStreamDestroy(side);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
@@ -531,6 +551,112 @@ int upload_subplan(SubPlan& sp, int d_head, cudaStream_t s, std::vector<std::pai
     return EP_OK;
 }
 
+using Parts = std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>>;
+
+// Stream-ordered upload of the plan arrays: (re)lays out the arena when a
+// part does not fit its capacity, stages every part at its arena offset in
+// one pinned slot of the ring and copies the used extent with ONE H2D copy
+// (async), or synchronously at plan creation.
+int stage_and_copy(ep_plan_s& p, const Parts& parts, cudaStream_t s, bool async) {
+    bool relayout = p.arena_cap.size() != parts.size() || !p.arena.ptr;
+    for (size_t i = 0; !relayout && i < parts.size(); ++i) relayout = parts[i].second.second > p.arena_cap[i];
+    if (relayout) {
+        p.arena_cap.resize(parts.size());
+        size_t total = 0;
+        for (size_t i = 0; i < parts.size(); ++i) {
+            const size_t b = parts[i].second.second;
+            p.arena_cap[i] = (std::max<size_t>(b + b / 4, 256) + 255) & ~size_t(255);
+            total += p.arena_cap[i];
+        }
+        // (cudaFree of the old arena waits for kernels still reading it)
+        if (p.arena.ptr) {
+            cudaFree(p.arena.ptr);
+            p.arena.ptr = nullptr;
+            p.arena.bytes = 0;
+        }
+        EP_CUDA_TRY(p.arena.reserve(total), "ep_plan arena");
+        size_t off = 0;
+        for (size_t i = 0; i < parts.size(); ++i) {
+            DeviceBuffer* v = parts[i].first;
+            if (v->ptr && !v->view) cudaFree(v->ptr);
+            v->ptr = static_cast<char*>(p.arena.ptr) + off;
+            v->bytes = p.arena_cap[i];
+            v->view = true;
+            off += p.arena_cap[i];
+        }
+    }
+    size_t extent = 0, off = 0;
+    for (size_t i = 0; i < parts.size(); ++i) {
+        if (parts[i].second.second) extent = off + parts[i].second.second;
+        off += p.arena_cap[i];
+    }
+    if (!extent) return EP_OK;
+    if (!async) {
+        std::vector<char> blob(extent);
+        off = 0;
+        for (size_t i = 0; i < parts.size() && off < extent; ++i) {
+            if (parts[i].second.second) std::memcpy(blob.data() + off, parts[i].second.first, parts[i].second.second);
+            off += p.arena_cap[i];
+        }
+        EP_CUDA_TRY(cudaMemcpy(p.arena.ptr, blob.data(), extent, cudaMemcpyHostToDevice), "ep_plan upload");
+        return EP_OK;
+    }
+    const int k = p.stage_idx;
+    p.stage_idx = (p.stage_idx + 1) % ep_plan_s::kStageRing;
+    if (p.staged[k]) EP_CUDA_TRY(cudaEventSynchronize(p.staged[k]), "ep_plan_update wait");
+    if (extent > p.h_stage_bytes[k]) {
+        if (p.h_stage[k]) cudaFreeHost(p.h_stage[k]);
+        p.h_stage[k] = nullptr;
+        EP_CUDA_TRY(cudaMallocHost(&p.h_stage[k], p.arena.bytes), "ep_plan_update pinned");
+        p.h_stage_bytes[k] = p.arena.bytes;
+    }
+    if (!p.staged[k]) EP_CUDA_TRY(cudaEventCreateWithFlags(&p.staged[k], cudaEventDisableTiming), "event");
+    off = 0;
+    for (size_t i = 0; i < parts.size() && off < extent; ++i) {
+        if (parts[i].second.second)
+            std::memcpy(static_cast<char*>(p.h_stage[k]) + off, parts[i].second.first, parts[i].second.second);
+        off += p.arena_cap[i];
+    }
+    EP_CUDA_TRY(cudaMemcpyAsync(p.arena.ptr, p.h_stage[k], extent, cudaMemcpyHostToDevice, s), "ep_plan_update copy");
+    EP_CUDA_TRY(cudaEventRecord(p.staged[k], s), "ep_plan_update event");
+    return EP_OK;
+}
+
+int upload_plan(ep_plan_s& p, cudaStream_t s, bool async);
+
+// Per-token growth fast path of ep_plan_update: when every request keeps the
+// same pages, in the same 64-token blocks, and only the token counts of its
+// pages and its query position moved (a decode step appending into the last
+// page's free slots), the work partition stays valid: the page descriptors
+// and query positions are refreshed and re-uploaded, nothing is re-planned.
+// Returns 1 when it applied, 0 when a full rebuild is needed, <0 on error.
+int try_grow_in_place(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* segs, const int32_t* page_table,
+                      const int64_t* q_pos, cudaStream_t s) {
+    if (p.cascade || p.prefill || p.generic || p.chunks > 1 || p.main.tc || p.main.pdesc.empty()) return 0;
+    SubPlan& sp = p.main;
+    std::vector<PageDesc> pages;
+    pages.reserve(sp.pdesc.size());
+    for (int b = 0; b < p.batch; ++b) {
+        if (q_pos[b] < 0 || q_pos[b] > INT32_MAX) return -fail(EP_EINVAL, "ep_plan: query position out of range");
+        const size_t before = pages.size();
+        int64_t first = 0;
+        if (int rc = collect_pages(p, b, seg_indptr, segs, page_table, pages, &first)) return -rc;
+        const int64_t n = int64_t(pages.size() - before);
+        if (n != sp.req_page_off[b + 1] - sp.req_page_off[b]) return 0;
+    }
+    if (pages.size() != sp.pdesc.size()) return 0;
+    for (size_t i = 0; i < pages.size(); ++i) {
+        const PageDesc &a = pages[i], &o = sp.pdesc[i];
+        if (a.page != o.page || a.pos != o.pos ||
+            (a.n_tok + kBlockTokens - 1) / kBlockTokens != (o.n_tok + kBlockTokens - 1) / kBlockTokens)
+            return 0;
+    }
+    sp.pdesc.swap(pages);
+    p.q_pos.assign(q_pos, q_pos + p.batch);
+    if (int rc = upload_plan(p, s, true)) return -rc;  // one staged copy of the (unchanged-layout) arena
+    return 1;
+}
+
 int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
     std::vector<std::pair<DeviceBuffer*, std::pair<const void*, size_t>>> parts;
     parts.push_back({&p.d_qpos, {p.q_pos.data(), bytes_of(p.q_pos)}});
@@ -543,36 +669,7 @@ int upload_plan(ep_plan_s& p, cudaStream_t s, bool async) {
         EP_CUDA_TRY(p.d_parts_o.reserve(2 * rows * p.d_head * sizeof(float)), "ep_plan cascade ws");
         EP_CUDA_TRY(p.d_parts_lse.reserve(2 * rows * sizeof(float)), "ep_plan cascade ws");
     }
-    size_t total = 0;
-    for (auto& x : parts) total += (x.second.second + 255) & ~size_t(255);
-    for (auto& x : parts) EP_CUDA_TRY(x.first->reserve(std::max<size_t>(x.second.second, 16)), "ep_plan alloc");
-    if (!async) {
-        for (auto& x : parts)
-            if (x.second.second)
-                EP_CUDA_TRY(cudaMemcpy(x.first->ptr, x.second.first, x.second.second, cudaMemcpyHostToDevice),
-                            "ep_plan upload");
-        return EP_OK;
-    }
-    if (p.staged) EP_CUDA_TRY(cudaEventSynchronize(p.staged), "ep_plan_update wait");
-    if (total > p.h_stage_bytes) {
-        if (p.h_stage) cudaFreeHost(p.h_stage);
-        p.h_stage = nullptr;
-        EP_CUDA_TRY(cudaMallocHost(&p.h_stage, total), "ep_plan_update pinned");
-        p.h_stage_bytes = total;
-    }
-    if (!p.staged) EP_CUDA_TRY(cudaEventCreateWithFlags(&p.staged, cudaEventDisableTiming), "event");
-    size_t off = 0;
-    for (auto& x : parts) {
-        if (x.second.second) {
-            std::memcpy(static_cast<char*>(p.h_stage) + off, x.second.first, x.second.second);
-            EP_CUDA_TRY(cudaMemcpyAsync(x.first->ptr, static_cast<char*>(p.h_stage) + off, x.second.second,
-                                        cudaMemcpyHostToDevice, s),
-                        "ep_plan_update copy");
-        }
-        off += (x.second.second + 255) & ~size_t(255);
-    }
-    EP_CUDA_TRY(cudaEventRecord(p.staged, s), "ep_plan_update event");
-    return EP_OK;
+    return stage_and_copy(p, parts, s, async);
 }
 
 bool valid_dt(int dt) { return dt == EP_F32 || dt == EP_BF16; }
@@ -676,6 +773,37 @@ int launch_subplan(ep_plan_s& p, SubPlan& sp, const ep_kv_pool* pool, DecodeArgs
 }  // namespace
 
 namespace ep {
+void plan_mark_built(ep_plan p, const void* cache, uint64_t version, int layer) {
+    if (!p) return;
+    p->built_cache = cache;
+    p->built_version = version;
+    p->built_layer = layer;
+}
+
+int plan_grow_in_place(ep_plan p, const void* cache, uint64_t version, int layer, const int64_t* ends, int n_q,
+                       cudaStream_t s) {
+    if (!p || p->built_cache != cache || p->built_version != version || p->built_layer != layer) return 0;
+    if (p->cascade || p->prefill || p->generic || p->chunks > 1 || p->main.tc || n_q != p->n_q) return 0;
+    SubPlan& sp = p->main;
+    // every request's last page takes its new end; block counts must not change
+    for (int b = 0; b < p->batch; ++b) {
+        const int64_t i = sp.req_page_off[b + 1] - 1;
+        if (i < sp.req_page_off[b]) return 0;
+        const PageDesc& d = sp.pdesc[size_t(i)];
+        const int64_t n = ends[b] - d.pos;
+        if (n < 1 || n > p->page_tokens ||
+            (n + kBlockTokens - 1) / kBlockTokens != (d.n_tok + kBlockTokens - 1) / kBlockTokens)
+            return 0;
+    }
+    for (int b = 0; b < p->batch; ++b) {
+        PageDesc& d = sp.pdesc[size_t(sp.req_page_off[b + 1] - 1)];
+        d.n_tok = int32_t(ends[b] - d.pos);
+        p->q_pos[b] = std::max<int64_t>(0, ends[b] - n_q);
+    }
+    if (int rc = upload_plan(*p, s, true)) return -rc;
+    return 1;
+}
+
 int64_t* plan_qpos_dev(ep_plan p) { return p ? static_cast<int64_t*>(p->d_qpos.ptr) : nullptr; }
 }  // namespace ep
 
@@ -764,6 +892,10 @@ int ep_plan_update(ep_plan p, const int64_t* seg_indptr, const ep_segment* segs,
                    const int32_t* page_table, const int64_t* q_pos, ep_stream stream) {
     if (!p) return fail(EP_EINVAL, "ep_plan_update: null plan");
     if (p->prefill) return fail(EP_EINVAL, "ep_plan_update: prefill plans are rebuilt with ep_plan_create_prefill");
+    p->built_cache = nullptr;  // (ep_plan_update_cache re-marks after a full build)
+    const int fast = try_grow_in_place(*p, seg_indptr, segs, page_table, q_pos, static_cast<cudaStream_t>(stream));
+    if (fast < 0) return -fast;
+    if (fast == 1) return EP_OK;
     if (int rc = build_plan_host(*p, seg_indptr, segs, page_table, q_pos)) return rc;
     return upload_plan(*p, static_cast<cudaStream_t>(stream), true);
 }

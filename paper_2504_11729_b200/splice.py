@@ -348,16 +348,20 @@ class SpliceCache:
         check(lib().ep_cache_append(self._c, layer, b, origin, pos_offset, length,
                                     pg.ctypes.data if pg.size else None, int(pg.size)), "ep_cache_append")
 
-    def append_generated(self, n_tokens, new_pages=None):
+    def append_generated(self, n_tokens, new_pages=None, out=None):
         """append_generated_token (cache.cpp:55-80) for the batch: request b
         grows by n_tokens[b]; new_pages [B][max_new] supplies pages when the
-        last page is full. Returns (dst_page, dst_slot, pages_used)."""
+        last page is full. Returns (dst_page, dst_slot, pages_used); out =
+        (dst_page, dst_slot) int32 arrays to fill (e.g. pinned staging)."""
         n = np.ascontiguousarray(n_tokens, dtype=np.int32)
         assert n.size == self.batch
         npg = (np.ascontiguousarray(new_pages, dtype=np.int32).reshape(self.batch, -1)
                if new_pages is not None else np.zeros((self.batch, 0), np.int32))
-        dst_page = np.zeros(max(1, int(n.sum())), np.int32)
-        dst_slot = np.zeros_like(dst_page)
+        if out is not None:
+            dst_page, dst_slot = out
+        else:
+            dst_page = np.zeros(max(1, int(n.sum())), np.int32)
+            dst_slot = np.zeros_like(dst_page)
         used = np.zeros(self.batch, np.int32)
         check(lib().ep_cache_append_generated(self._c, n.ctypes.data, npg.ctypes.data if npg.size else None,
                                               int(npg.shape[1]), dst_page.ctypes.data, dst_slot.ctypes.data,
