@@ -448,7 +448,6 @@ __global__ void __launch_bounds__(kRefineThreads)
     const int row = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     extern __shared__ float4 s_x4[];  // [width / 4]
     __shared__ int s_list[kMaxList];
-    __shared__ int s_cnt[kRefineThreads];
     __shared__ int s_n;
     __shared__ bool s_all;
     __shared__ unsigned long long s_top;
@@ -459,29 +458,34 @@ __global__ void __launch_bounds__(kRefineThreads)
         const float4 v = xr[i];
         s_x4[i] = make_float4(v.x - mu, v.y - mu, v.z - mu, v.w - mu);
     }
-    // gather (all threads): the per-tile counts, then one slot per thread
+    // gather (all threads): thread t reads the counts of tiles t, t + 256, ...
+    // and appends their candidates within the bound to the row's list (value
+    // and index in one round trip); a tile whose slots overflowed, or a list
+    // longer than kMaxList, falls back to scoring every vocab entry
     if (tid == 0) {
-        s_all = logits != nullptr || n_tiles * kPerTile > kMaxList || n_tiles > kRefineThreads;
+        s_all = logits != nullptr;
         s_n = 0;
         s_top = 0ull;
     }
     __syncthreads();
-    if (tid < n_tiles && tid < kRefineThreads) {
-        const int c = cand_cnt[size_t(row) * n_tiles + tid];
-        s_cnt[tid] = c;
-        if (c > kPerTile) s_all = true;
-    }
     const float thresh = key_value(best[row]) - 2.f * ebound[row];
-    __syncthreads();
-    if (!s_all && tid < n_tiles) {
-        // the thread that read tile tid's count gathers its slots: value and
-        // index in one round trip
-        const int c = s_cnt[tid];
-        const size_t b0 = (size_t(row) * n_tiles + tid) * kPerTile;
-        for (int i = 0; i < c; ++i) {
-            const float z = cand_z[b0 + i];
-            const int n = cand_n[b0 + i];
-            if (z >= thresh) s_list[atomicAdd(&s_n, 1)] = n;
+    if (!s_all) {
+        for (int t = tid; t < n_tiles; t += kRefineThreads) {
+            const int c = cand_cnt[size_t(row) * n_tiles + t];
+            if (c > kPerTile) {
+                s_all = true;
+                continue;
+            }
+            const size_t b0 = (size_t(row) * n_tiles + t) * kPerTile;
+            for (int i = 0; i < c; ++i) {
+                const float z = cand_z[b0 + i];
+                const int n = cand_n[b0 + i];
+                if (z >= thresh) {
+                    const int k = atomicAdd(&s_n, 1);
+                    if (k < kMaxList) s_list[k] = n;
+                    else s_all = true;
+                }
+            }
         }
     }
     __syncthreads();

@@ -260,3 +260,23 @@ def test_config3_verify_production_path(cuda_handle, k):
             checked += 1
     assert checked >= B - 4
     assert sorted(set(nacc_ref.tolist())) == list(range(k + 1))
+
+
+@pytest.mark.parametrize("V", [16384, 40960])
+def test_score_large_vocab_candidate_path(cuda_handle, V):
+    """Vocabularies past 64 (and past 256) tiles of 128: the refinement keeps
+    using the candidate list (sized by the gathered count, tiles read in
+    strides of the block) instead of scoring every entry; ids equal the fp64
+    argmax_token(LN(x) @ W) (model.cpp:238-255)."""
+    import torch
+    from paper_2504_11729_b200.verify import VerifyGreedy
+    from tests.gpu_util import torch_from_raw
+    B, n_q, width = 4, 3, 4096
+    rng = np.random.default_rng(V)
+    W = O.fill_uniform(O.DT_BF16, width * V, 91).reshape(width, V)
+    x = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32)
+    ver = VerifyGreedy(torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16), handle=cuda_handle)
+    tgt, _, _ = ver(torch.from_numpy(x).cuda().view(B, n_q, 32, 128),
+                    torch.zeros((B, n_q - 1), dtype=torch.int32, device="cuda"))
+    want = _oracle_argmax(x.astype(np.float64), O.bf16_to_f64(W))
+    assert np.array_equal(tgt.cpu().numpy(), want)
