@@ -21,6 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_build")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libep_b200.so")
+CHECKED_LIB = os.path.join(LIB_DIR, "libep_b200_checked.so")
 INCLUDE = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", "nvcc")
@@ -47,10 +48,12 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def _compile(src: str, force: bool, ptxas_v: bool) -> str:
-    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, force: bool, ptxas_v: bool, obj_dir: str = OBJ, checked: bool = False) -> str:
+    obj = os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
     if force or _stale(obj, _deps(src)):
         flags = CU_FLAGS + (["-Xptxas", "-v"] if ptxas_v and src.endswith(".cu") else [])
+        if checked:
+            flags = flags + ["-DEP_CHECKED"]
         cmd = [NVCC] + flags + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -60,23 +63,28 @@ def _compile(src: str, force: bool, ptxas_v: bool) -> str:
     return obj
 
 
-def build(force: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, ptxas_v: bool = False, checked: bool = False) -> str:
+    """checked: the -DEP_CHECKED variant (device bounds checks, bounded spins)
+    into _build/checked/ and _lib/libep_b200_checked.so."""
+    obj_dir = os.path.join(OBJ, "checked") if checked else OBJ
+    lib = CHECKED_LIB if checked else LIB
+    os.makedirs(obj_dir, exist_ok=True)
     os.makedirs(LIB_DIR, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, ptxas_v), srcs))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-cudart", "static"]
+        objs = list(ex.map(lambda s: _compile(s, force, ptxas_v, obj_dir, checked), srcs))
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="the -DEP_CHECKED variant (bounds checks)")
     args = ap.parse_args()
-    print(build(force=args.force, ptxas_v=args.ptxas_v))
+    print(build(force=args.force, ptxas_v=args.ptxas_v, checked=args.checked))

@@ -309,7 +309,7 @@ int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int3
     if (row_bytes % 16) return fail(EP_EUNSUPPORTED, "ep_kv_append: row must be a multiple of 16 bytes");
     EP_CUDA_TRY(launch_kv_append(row_bytes, pool->n_kv_heads, pool->page_tokens, n_rows, dst_page,
                                  dst_slot, k_new, v_new, pool->k_pages, pool->v_pages,
-                                 static_cast<cudaStream_t>(stream)),
+                                 static_cast<cudaStream_t>(stream), pool->num_pages),
                 "ep_kv_append launch");
     if (n_rows > 0) h->launches++;
     return EP_OK;

@@ -7,6 +7,29 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+// Checked build (python -m paper_2504_11729_b200.build --checked ->
+// _lib/libep_b200_checked.so, -DEP_CHECKED): device-side bounds checks on
+// every index the kernels derive from plan / table data and bounded
+// mbarrier / flag spins, each trapping with the failing condition, file and
+// line. The GPU test suite runs against it (EP_LIB=...) as this repo's
+// stand-in for compute-sanitizer (closed on this GPU pool). Release builds
+// compile the checks away.
+#ifdef EP_CHECKED
+#include <cstdio>
+#define EP_DCHECK(cond)                                                                                   \
+    do {                                                                                                  \
+        if (!(cond)) {                                                                                    \
+            printf("EP_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,   \
+                   int(blockIdx.x), int(threadIdx.x));                                                   \
+            __trap();                                                                                     \
+        }                                                                                                 \
+    } while (0)
+#else
+#define EP_DCHECK(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace ep {
 
 // Opts kernel Kern into at least `bytes` of dynamic shared memory on the
@@ -71,8 +94,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef EP_CHECKED
+    // a protocol bug (an arrival that never comes) traps instead of hanging
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (!mbar_try_wait(bar, parity)) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 5000000000ull) {
+            printf("EP_DCHECK: mbarrier wait > 5 s (block %d thread %d parity %u)\n", int(blockIdx.x),
+                   int(threadIdx.x), parity);
+            __trap();
+        }
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // ------------------------------------------------- bulk async copy (TMA) --

@@ -69,7 +69,8 @@ cudaError_t launch_merge_generic(int dt, size_t n_parts, const void* outs, const
 
 cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int n_rows,
                              const int32_t* dst_page, const int32_t* dst_slot, const void* k_new,
-                             const void* v_new, void* k_pages, void* v_pages, cudaStream_t s);
+                             const void* v_new, void* k_pages, void* v_pages, cudaStream_t s,
+                             int64_t num_pages = -1);
 
 cudaError_t launch_merge_packed(int n_parts, const float* packed, int rows, int d, void* out,
                                 int out_dtype, float* lse, cudaStream_t s);
@@ -137,6 +138,9 @@ struct DecodeArgs {
     int32_t nq_total;         // tokens cut into `chunks` virtual requests of n_q tokens (1 = not cut)
     int32_t pv_parts;         // K3: P as bf16 hi+lo (2) or bf16 (1)
     PeerLink peer;            // K1 fused split-KV combine (world 0 = off)
+    int64_t num_pages;        // pool pages (checked build: page ids in range)
+    int64_t n_q_rows;         // query / output token rows of the launch (checked build)
+    int32_t n_items;          // work items of the sub-plan (checked build)
 };
 
 // The fused split-KV link of a peer group for a plan of n_units units and

@@ -159,7 +159,9 @@ __device__ __forceinline__ void item_end(const DecodeArgs& a, int it, int gw, in
     const int Hkv = a.n_kv_heads, G = a.n_q_heads / Hkv;
     const WorkItem w = a.items[it];
     const int unit = w.b * Hkv + w.g;
+    EP_DCHECK(it >= 0 && it < a.n_items && unit >= 0 && unit < a.batch * Hkv);
     const int u0 = a.unit_item_ptr[unit], n_items = a.unit_item_ptr[unit + 1] - u0;
+    EP_DCHECK(n_items >= 1 && u0 + n_items <= a.n_items && it >= u0 && it < u0 + n_items);
     const bool direct = n_items == 1;
 #pragma unroll 1
     for (int r = gw; r < R; r += n_grp) {
@@ -192,6 +194,7 @@ __device__ __forceinline__ void item_end(const DecodeArgs& a, int it, int gw, in
             if (r < w.pad) {
                 const int qi = r / G, h = w.g * G + r % G;
                 const size_t orow = (q_row_base(a, w.b) + qi) * a.n_q_heads + h;
+                EP_DCHECK(int64_t(orow) < a.n_q_rows * a.n_q_heads);
                 if (a.peer.world) {  // fused split-KV: the row goes to every rank
                     float v[EL];
 #pragma unroll
@@ -312,8 +315,10 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
             const int G = a.n_q_heads / Hkv;
             for (int j = it0; j < it1; ++j) {
                 const int it = item_at(a, j);
+                EP_DCHECK(it >= 0 && it < a.n_items);
                 const WorkItem w = a.items[it];
                 const PageDesc* pd = a.pdesc + a.req_page_off[w.b];
+                EP_DCHECK(w.lp0 < w.lp1 && w.g >= 0 && w.g < Hkv && w.pad >= 1 && w.pad <= R);
                 {
                     // the item's R query rows: n_q runs of G consecutive heads
                     const int n = j - it0, slot = n & 1;
@@ -321,6 +326,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                     // w.pad = its valid rows; only those are loaded and stored)
                     const uint32_t run = uint32_t(G) * D * qsz;
                     const int nq = min(a.n_q, (w.pad + G - 1) / G);
+                    EP_DCHECK(int64_t(q_row_base(a, w.b)) + nq <= a.n_q_rows);
                     mbar_wait(&q_empty[slot], ((n >> 1) & 1) ^ 1);
                     mbar_arrive_expect_tx(&q_full[slot], run * nq);
                     for (int qi = 0; qi < nq; ++qi)
@@ -331,6 +337,7 @@ __global__ void __launch_bounds__(DecodeCfg<KV, D, R, J, S>::THREADS, 1)
                 }
                 for (int lp = w.lp0; lp < w.lp1; ++lp) {
                     const PageDesc d = pd[lp];
+                    EP_DCHECK(d.page >= 0 && d.page < a.num_pages && d.n_tok >= 1 && d.n_tok <= P);
                     const size_t tile = (size_t(d.page) * Hkv + w.g) * size_t(P);
                     for (int t0 = 0; t0 < d.n_tok; t0 += BT) {
                         const int nv = min(BT, d.n_tok - t0);

@@ -253,8 +253,10 @@ __global__ void kv_append_kernel(int row_bytes, int n_kv_heads, int page_tokens,
                                  const int32_t* __restrict__ dst_page,
                                  const int32_t* __restrict__ dst_slot,
                                  const uint8_t* __restrict__ k_new, const uint8_t* __restrict__ v_new,
-                                 uint8_t* __restrict__ k_pages, uint8_t* __restrict__ v_pages) {
+                                 uint8_t* __restrict__ k_pages, uint8_t* __restrict__ v_pages, int64_t num_pages) {
     const int i = blockIdx.x;
+    EP_DCHECK(num_pages < 0 || (dst_page[i] >= 0 && dst_page[i] < num_pages));
+    EP_DCHECK(dst_slot[i] >= 0 && dst_slot[i] < page_tokens);
     const size_t page = size_t(dst_page[i]), slot = size_t(dst_slot[i]);
     const int chunks = row_bytes / 16;
     for (int c = threadIdx.x; c < n_kv_heads * chunks; c += blockDim.x) {
@@ -270,13 +272,14 @@ __global__ void kv_append_kernel(int row_bytes, int n_kv_heads, int page_tokens,
 
 cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int n_rows,
                              const int32_t* dst_page, const int32_t* dst_slot, const void* k_new,
-                             const void* v_new, void* k_pages, void* v_pages, cudaStream_t s) {
+                             const void* v_new, void* k_pages, void* v_pages, cudaStream_t s,
+                             int64_t num_pages) {
     if (n_rows <= 0) return cudaSuccess;
     kv_append_kernel<<<n_rows, 128, 0, s>>>(row_bytes, n_kv_heads, page_tokens, dst_page, dst_slot,
                                             static_cast<const uint8_t*>(k_new),
                                             static_cast<const uint8_t*>(v_new),
                                             static_cast<uint8_t*>(k_pages),
-                                            static_cast<uint8_t*>(v_pages));
+                                            static_cast<uint8_t*>(v_pages), num_pages);
     return cudaGetLastError();
 }
 

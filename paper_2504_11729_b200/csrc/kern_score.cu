@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(kRefineThreads)
     unsigned long long top = 0ull;
     for (int i = warp; i < count; i += kRefineThreads / 32) {
         const int n = all ? i : s_list[i];
+        EP_DCHECK(n >= 0 && n < vocab);
         const uint2* wr = reinterpret_cast<const uint2*>(wt + size_t(n) * width);
         float acc = 0.f;
 #pragma unroll 16

@@ -129,12 +129,18 @@ struct BlockWalker {
     const PageDesc* pd;
     int lp, lp1, t0;
     PageDesc cur;
-    __device__ void init(const PageDesc* p, int lp0, int lp1_) {
+    int64_t num_pages = -1;  // checked build: page ids in range
+    __device__ void load() {
+        cur = pd[lp];
+        EP_DCHECK(num_pages < 0 || (cur.page >= 0 && cur.page < num_pages && cur.n_tok >= 1));
+    }
+    __device__ void init(const PageDesc* p, int lp0, int lp1_, int64_t n_pages = -1) {
         pd = p;
         lp = lp0;
         lp1 = lp1_;
         t0 = 0;
-        if (lp < lp1) cur = pd[lp];
+        num_pages = n_pages;
+        if (lp < lp1) load();
     }
     // current block: valid rows and absolute position of its first key
     __device__ int nv() const { return min(kBT, cur.n_tok - t0); }
@@ -143,7 +149,7 @@ struct BlockWalker {
         t0 += kBT;
         if (t0 >= cur.n_tok) {
             t0 = 0;
-            if (++lp < lp1) cur = pd[lp];
+            if (++lp < lp1) load();
         }
     }
 };
@@ -229,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int it = it0; it < it1; ++it) {
                 const WorkItem w = a.items[it];
                 BlockWalker wk;
-                wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
+                wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1, a.num_pages);
                 for (int i = 0; i < w.nblk; ++i, ++gi, wk.next()) {
                     const int st = gi % ns;
                     mbar_wait(&emptyb[st], ((gi / ns) & 1) ^ 1);
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
             float m_used = -INFINITY, l = 0.f;
             BlockWalker wk;
-            wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1);
+            wk.init(a.pdesc + a.req_page_off[w.b], w.lp0, w.lp1, a.num_pages);
             if (grp == 1) wk.next();
             for (int i = grp; i < w.nblk; i += 2) {
                 const int nv = wk.nv();

@@ -212,6 +212,7 @@ __device__ __forceinline__ void merge_unit_rows(const DecodeArgs& a, int u0, int
             if (!ok[k]) continue;
             const bool er = !(L[k] > 0.f);
             const size_t orow = orow_of(rr[k]);
+            EP_DCHECK(int64_t(orow) < a.n_q_rows * a.n_q_heads);
             if (a.peer.world) {  // fused split-KV: this rank's merged row goes to every rank
                 float v[E];
 #pragma unroll

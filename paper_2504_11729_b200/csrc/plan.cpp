@@ -239,6 +239,7 @@ struct ep_plan_s {
     int32_t chunk_q = 0;              //   `chunks` virtual requests of chunk_q tokens
     bool generic = false;             // no K1 / K3 instance: the generic kernel (any d_head <= 256, any group)
     std::vector<int32_t> q_row0;      // prefill: first q/o token row per virtual request
+    int64_t n_q_rows = 0;             // prefill: query token rows (sum n_new)
     SubPlan main;    // whole table (non-cascade) or the private remainders (cascade)
     SubPlan shared;  // cascade: shared prefixes, row-group tiles on K3
     std::vector<int64_t> q_pos;
@@ -523,6 +524,7 @@ int build_prefill_host(ep_plan_s& p, int n_req, const int64_t* seg_indptr, const
         if (tok_base > INT32_MAX) return fail(EP_EINVAL, "ep_plan_create_prefill: too many query tokens");
     }
     p.batch = int32_t(vr.size());
+    p.n_q_rows = tok_base;
     p.cascade = false;
     p.has_shared.assign(vr.size(), 0);
     build_subplan(p.main, vr, Hkv, int64_t(p.h->n_sms), p.main.tc ? tc_item_weight(G * C) : 1);
@@ -685,6 +687,9 @@ DecodeArgs make_args(const ep_plan_s& p, const SubPlan& sp, const ep_kv_pool* po
     a.n_q_heads = p.n_q_heads;
     a.page_tokens = p.page_tokens;
     a.n_q = p.chunks > 1 ? p.chunk_q : p.n_q;
+    a.num_pages = pool->num_pages;
+    a.n_q_rows = p.prefill ? p.n_q_rows : int64_t(p.batch) * p.n_q;
+    a.n_items = int32_t(sp.n_items);
     a.chunks = p.chunks;
     a.nq_total = p.n_q;
     a.pdesc = static_cast<const PageDesc*>(sp.d_pdesc.ptr);
