@@ -19,7 +19,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 SEQ, H, D, P = 4096, 8, 128, 64
-HBM_PEAK_GBS = 6549.1
+def _hbm_peak():
+    """Measured HBM copy GB/s from the driver-written MEASURED_PEAKS.json."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak()
 
 
 def make_frame(seq=SEQ):

@@ -23,7 +23,17 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 HQ, HKV, D, P = 32, 8, 128, 64
-BF16_PEAK_TFLOPS = 1627.9  # MEASURED_PEAKS.json, dense bf16 burst
+def _bf16_peak():
+    """Dense bf16 burst TFLOP/s from the driver-written MEASURED_PEAKS.json
+    (this pool's B200s); the B200_PROFILING.md fallback when absent."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    except Exception:
+        return 2250.0, "fallback (nominal dense bf16)"
+
+
+BF16_PEAK_TFLOPS, BF16_PEAK_KIND = _bf16_peak()
 
 
 def setup(kind: str, batch: int, h):
@@ -91,6 +101,7 @@ def run(kind: str, batch: int, steps: int, warmup: int, h=None):
         "batch": batch, "query_tokens": int(q.shape[0]), "ms": ms,
         "query_tokens_per_s": q.shape[0] / (ms / 1e3),
         "causal_flops": flops, "tflops": tf, "frac_of_bf16_peak": tf / BF16_PEAK_TFLOPS,
+        "bf16_peak_tflops": BF16_PEAK_TFLOPS, "bf16_peak_kind": BF16_PEAK_KIND,
         "plan": dict(zip(("ctas", "items", "pages"), pre.info())),
     }
 

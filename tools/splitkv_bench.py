@@ -21,6 +21,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 HQ, HKV, D, P = 32, 8, 128, 64
+
+
+def _hbm_peak():
+    """Measured HBM copy GB/s from the driver-written MEASURED_PEAKS.json."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
 CLOUD, EDGE = 131072, 512
 
 
@@ -218,7 +227,7 @@ def run(batch, steps, warmup, check=False, combine="peer", graph=False, cloud=CL
                                if per_rank else None),
         "combine_nvlink_frac": (gather_bytes / (max(r[1] for r in per_rank) / 1e3) / 900e9
                                 if per_rank else None),
-        "local_hbm_frac": loc_bytes / (t_attn / 1e3) / 6549.1e9,
+        "local_hbm_frac": loc_bytes / (t_attn / 1e3) / (_hbm_peak() * 1e9),
         "graph": graph, "host_launch_us_per_step": host_us,
     }
     if per_rank is not None:
