@@ -156,6 +156,21 @@ int collect_request_pages(int page_tokens, int64_t num_pages, int b, const int64
                           const ep_segment* segs, const int32_t* page_table, std::vector<PageDesc>& out,
                           int64_t* first_pages);
 
+// Per-token growth of a plan in place on the device (the fast path of
+// ep_plan_update_cache): desc[idx[i]].n_tok = ntok[i], q_pos[req[i]] = qpos[i]
+// for n entries, in one small kernel launch instead of a staged H2D copy.
+constexpr int kPlanPatchMax = 128;
+struct PlanPatch {
+    PageDesc* pdesc;
+    int64_t* q_pos;
+    int32_t n;
+    int32_t idx[kPlanPatchMax];
+    int32_t ntok[kPlanPatchMax];
+    int32_t req[kPlanPatchMax];
+    int64_t qpos[kPlanPatchMax];
+};
+cudaError_t launch_plan_patch(const PlanPatch& pp, cudaStream_t s);
+
 // ep_cache <-> plan: the plan remembers which cache (and structure version,
 // layer) it was last fully built from; plan_grow_in_place then follows pure
 // in-page growth of every request to ends[b] (query rows end - n_q) with an

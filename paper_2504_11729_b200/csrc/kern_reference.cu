@@ -270,6 +270,19 @@ __global__ void kv_append_kernel(int row_bytes, int n_kv_heads, int page_tokens,
 
 }  // namespace
 
+__global__ void plan_patch_kernel(const PlanPatch pp) {
+    for (int i = threadIdx.x; i < pp.n; i += blockDim.x) {
+        pp.pdesc[pp.idx[i]].n_tok = pp.ntok[i];
+        pp.q_pos[pp.req[i]] = pp.qpos[i];
+    }
+}
+
+cudaError_t launch_plan_patch(const PlanPatch& pp, cudaStream_t s) {
+    if (pp.n <= 0) return cudaSuccess;
+    plan_patch_kernel<<<1, 128, 0, s>>>(pp);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int n_rows,
                              const int32_t* dst_page, const int32_t* dst_slot, const void* k_new,
                              const void* v_new, void* k_pages, void* v_pages, cudaStream_t s,

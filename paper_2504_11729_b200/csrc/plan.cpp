@@ -800,12 +800,29 @@ int plan_grow_in_place(ep_plan p, const void* cache, uint64_t version, int layer
             (n + kBlockTokens - 1) / kBlockTokens != (d.n_tok + kBlockTokens - 1) / kBlockTokens)
             return 0;
     }
+    // host mirror + device patch (one small kernel per 128 requests; the
+    // arena, its views and any captured graph's pointers stay as they are)
+    PlanPatch pp{};
+    pp.pdesc = static_cast<PageDesc*>(sp.d_pdesc.ptr);
+    pp.q_pos = static_cast<int64_t*>(p->d_qpos.ptr);
     for (int b = 0; b < p->batch; ++b) {
-        PageDesc& d = sp.pdesc[size_t(sp.req_page_off[b + 1] - 1)];
-        d.n_tok = int32_t(ends[b] - d.pos);
-        p->q_pos[b] = std::max<int64_t>(0, ends[b] - n_q);
+        const int32_t i = int32_t(sp.req_page_off[b + 1] - 1);
+        PageDesc& d = sp.pdesc[size_t(i)];
+        const int32_t nt = int32_t(ends[b] - d.pos);
+        const int64_t qp = std::max<int64_t>(0, ends[b] - n_q);
+        if (nt == d.n_tok && qp == p->q_pos[b]) continue;
+        d.n_tok = nt;
+        p->q_pos[b] = qp;
+        pp.idx[pp.n] = i;
+        pp.ntok[pp.n] = nt;
+        pp.req[pp.n] = b;
+        pp.qpos[pp.n] = qp;
+        if (++pp.n == kPlanPatchMax) {
+            EP_CUDA_TRY(launch_plan_patch(pp, s), "ep_plan_update_cache patch");
+            pp.n = 0;
+        }
     }
-    if (int rc = upload_plan(*p, s, true)) return -rc;
+    EP_CUDA_TRY(launch_plan_patch(pp, s), "ep_plan_update_cache patch");
     return 1;
 }
 

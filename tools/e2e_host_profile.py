@@ -85,5 +85,72 @@ def main():
     pstats.Stats(pr).sort_stats("tottime").print_stats(12)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def phases():
+    """Per-phase host time of the bench's e2e loop body (GPU kept busy)."""
+    import torch
+    import bench
+    from cuda.bindings import runtime as rt
+    from paper_2504_11729_b200 import _capi
+    from paper_2504_11729_b200.attention import Handle
+    from paper_2504_11729_b200.splice import KVPool, SpliceCache, SpliceTable, SplicedAttention
+    h = Handle(0)
+    B, P = bench.B, bench.P
+    pool = KVPool(B * bench.PAGES_PER_REQ, bench.HKV, bench.D, P, dtype="bf16")
+    table = bench.build_requests_table(SpliceTable, pool, B)
+    cache = SpliceCache(1, B, P)
+    for b in range(B):
+        for sg in table.requests[b]:
+            cache.append(b, sg.origin, sg.pos_offset, sg.length, sg.pages)
+    attn = SplicedAttention.from_cache(pool, cache, bench.HQ, 1, handle=h)
+    lib = _capi.lib()
+    pd = pool.desc()
+    pdr = C.byref(pd)
+    q = torch.zeros((B, 1, bench.HQ, bench.D), dtype=torch.bfloat16, device="cuda")
+    o = torch.empty_like(q)
+    lse = torch.empty((B, 1, bench.HQ), dtype=torch.float32, device="cuda")
+    sl = np.zeros((2, B), np.int32)
+    sd = torch.zeros((2, B), dtype=torch.int32, device="cuda")
+    kv = torch.zeros((2, B, bench.HKV, bench.D), dtype=torch.bfloat16, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+    ones = np.ones(B, np.int32)
+    ptrs = (sd[0].data_ptr(), sd[1].data_ptr(), kv[0].data_ptr(), kv[1].data_ptr())
+    acc = {k: 0.0 for k in ("grow", "update", "append", "attn")}
+    n = 300
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    st = torch.cuda.current_stream()
+    for i in range(n):
+        evs[i][0].record(st)
+        t0 = time.perf_counter()
+        if i % 60 == 59:
+            for b in range(B):
+                cache.truncate(b, 59)
+        cache.append_generated(ones, out=(sl[0], sl[1]))
+        t1 = time.perf_counter()
+        lib.ep_plan_update_cache(attn.plan, cache.ptr, 0, 1, sp)
+        evs[i][1].record(st)
+        t2 = time.perf_counter()
+        lib.ep_kv_append(h.ptr, pdr, B, *ptrs, sp)
+        evs[i][2].record(st)
+        t3 = time.perf_counter()
+        lib.ep_spliced_attention(h.ptr, attn.plan, pdr, 1, q.data_ptr(), 1, o.data_ptr(), lse.data_ptr(), sp)
+        evs[i][3].record(st)
+        t4 = time.perf_counter()
+        for k, a, b_ in (("grow", t0, t1), ("update", t1, t2), ("append", t2, t3), ("attn", t3, t4)):
+            acc[k] += (b_ - a)
+    torch.cuda.synchronize()
+    print("host us", {k: round(v / n * 1e6, 1) for k, v in acc.items()})
+    g = {"upload": 0.0, "append": 0.0, "attn": 0.0, "gap_to_next": 0.0}
+    for i in range(50, n - 1):
+        g["upload"] += evs[i][0].elapsed_time(evs[i][1])
+        g["append"] += evs[i][1].elapsed_time(evs[i][2])
+        g["attn"] += evs[i][2].elapsed_time(evs[i][3])
+        g["gap_to_next"] += evs[i][3].elapsed_time(evs[i + 1][0])
+    print("gpu us", {k: round(v / (n - 51) * 1e3, 2) for k, v in g.items()})
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "phases":
+    phases()
