@@ -327,6 +327,7 @@ struct ep_verifier_s {
     CUtensorMap tmap_a{};
     const void* a_ptr = nullptr;
     int32_t a_rows = -1, a_dtype = -1;
+    int32_t w_tn = -1;  // tile width tmap_w was encoded for (the W box is 64 x tn)
 };
 
 int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_score_t,
@@ -342,7 +343,6 @@ int ep_verifier_create(ep_handle h, int32_t width, int32_t vocab, const void* w_
     v->vocab = vocab;
     v->w_t = w_score_t;
     EP_CUDA_TRY(cudaSetDevice(h->device), "ep_verifier_create");
-    if (int rc = encode_bf16_2d(&v->tmap_w, w_score_t, uint64_t(width), uint64_t(vocab), 64, kScoreTileN)) return rc;
     EP_CUDA_TRY(v->colsum.reserve(size_t(vocab) * sizeof(float)), "ep_verifier_create colsum");
     EP_CUDA_TRY(v->wmax2.reserve(sizeof(float)), "ep_verifier_create colnorm");
     EP_CUDA_TRY(launch_colsum(w_score_t, width, vocab, static_cast<float*>(v->colsum.ptr),
@@ -368,6 +368,12 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
     if (attn_dtype != EP_F32 && attn_dtype != EP_BF16)
         return fail(EP_EUNSUPPORTED, "ep_verify_greedy: attn_out must be f32 or bf16");
     const int32_t rows = batch * n_q;
+    const int tn = score_tile_n(rows, v->vocab, h->n_sms);
+    if (v->w_tn != tn) {
+        if (int rc = encode_bf16_2d(&v->tmap_w, v->w_t, uint64_t(v->width), uint64_t(v->vocab), 64, uint32_t(tn)))
+            return rc;
+        v->w_tn = tn;
+    }
     EP_CUDA_TRY(v->mean.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
     EP_CUDA_TRY(v->rstd.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
     EP_CUDA_TRY(v->best.reserve(size_t(rows) * sizeof(unsigned long long)), "ep_verify_greedy ws");
@@ -381,8 +387,9 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         // the bf16 hi part of the rows is the GEMM's A operand
         EP_CUDA_TRY(v->split.reserve(size_t(rows) * v->width * 2), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->ebound.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
-        const size_t slots = size_t(v->vocab) / kScoreTileN * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
-        EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * (v->vocab / kScoreTileN) * sizeof(int32_t)), "ep_verify_greedy ws");
+        const size_t n_tiles = size_t((v->vocab + tn - 1) / tn);
+        const size_t slots = n_tiles * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
+        EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * n_tiles * sizeof(int32_t)), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->cand_n.reserve(size_t(rows) * slots * sizeof(int32_t)), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->cand_z.reserve(size_t(rows) * slots * sizeof(float)), "ep_verify_greedy ws");
         split = v->split.ptr;
@@ -408,7 +415,7 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         v->a_rows = rows;
         v->a_dtype = attn_dtype;
     }
-    EP_CUDA_TRY(launch_score_accept(rows, v->width, v->vocab, attn_out, split, v->tmap_a, v->tmap_w,
+    EP_CUDA_TRY(launch_score_accept(rows, v->width, v->vocab, tn, attn_out, split, v->tmap_a, v->tmap_w,
                                     static_cast<const float*>(v->colsum.ptr),
                                     static_cast<float*>(v->mean.ptr), static_cast<float*>(v->rstd.ptr),
                                     static_cast<unsigned long long*>(v->best.ptr), logits, batch, n_q,

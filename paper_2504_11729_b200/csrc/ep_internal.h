@@ -234,18 +234,20 @@ cudaError_t launch_verify_attention(int n_ctas, const DecodeArgs& a, const CUten
 cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, float* wmax2, cudaStream_t s);
 // fp32 attention rows: hi-only GEMM + exact refinement of the candidates
 // within the per-row error bound (kern_score.cu).
-constexpr int kScoreTileN = 128;       // vocabulary columns per K4 score tile (one TMEM accumulator)
+constexpr int kScoreTileNMax = 256;    // vocabulary columns per K4 score tile, at most (one TMEM accumulator)
 constexpr int kScoreCandPerTile = 16;  // candidate slots per (row, vocab tile)
+// K4 tile width for `rows` score rows: one wave of CTAs over n_sms SMs.
+int score_tile_n(int rows, int vocab, int n_sms);
 struct RefineArgs {
     const void* wt = nullptr;      // W^T bf16 [vocab][width]
     const float* wmax2 = nullptr;  // max_n ||W^T[n]||_2
     float* ebound = nullptr;       // [rows]
     int32_t* cand_cnt = nullptr;   // [rows][vocab / 256]
-    int32_t* cand_n = nullptr;     // [rows][vocab / kScoreTileN][kScoreCandPerTile]
-    float* cand_z = nullptr;       // [rows][vocab / kScoreTileN][kScoreCandPerTile]
+    int32_t* cand_n = nullptr;     // [rows][vocab tiles][kScoreCandPerTile]
+    float* cand_z = nullptr;       // [rows][vocab tiles][kScoreCandPerTile]
     int32_t* req_count = nullptr;  // [batch] row arrivals of the fused accept, zero between launches
 };
-cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn_out, void* split,
+cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
                                 const float* colsum, float* mean, float* rstd,
                                 unsigned long long* best, float* logits, int batch, int n_q,

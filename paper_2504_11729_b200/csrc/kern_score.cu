@@ -42,14 +42,23 @@
 namespace ep {
 namespace {
 
-constexpr int kTM = 128, kTN = kScoreTileN, kTK = 64;
-constexpr int kStagesS = 3;  // 3 x 32 KB: two CTAs per SM (config 3 at k = 8 has 160 tiles)
+// Tiles are kTM = 128 rows x tn vocabulary columns, tn chosen per launch so
+// that one wave of CTAs (one per SM) covers the product: tn = 32-multiple
+// of ceil(vocab / floor(SMs / M tiles)), <= 256 (config 3: 160 at k = 8, 96
+// at k = 4). One CTA per SM with as deep a ring as shared memory allows.
+constexpr int kTM = 128, kTNMax = kScoreTileNMax, kTK = 64;
+constexpr int kStagesMax = 8;
 constexpr int kABytes = kTM * kTK * 2;  // 16 KB
-constexpr int kBBytes = kTN * kTK * 2;  // 16 KB
-constexpr int kStage = kABytes + kBBytes;
-constexpr int kScoreThreads = 192;  // warps 0-3 epilogue, 4 TMA, 5 MMA
-constexpr int kScoreSmem = kStagesS * kStage + 1024 + 256 + kTN * 4 + 24 * 128 * 5;  // stages, barriers, colsum slice, stash
-constexpr uint32_t kIdescScore = umma::idesc_bf16_f32(kTM, kTN, false, false);
+constexpr int kScoreThreads = 192;      // warps 0-3 epilogue, 4 TMA, 5 MMA
+constexpr int kStash = 24;              // per-thread candidate stash of the epilogue (smem)
+constexpr int kScoreSmemFixed = 1024 + 256 + kTNMax * 4 + kStash * 128 * 5;  // align, barriers, colsum slice, stash
+constexpr int kScoreSmemBudget = 227 * 1024 - kScoreSmemFixed;
+
+__host__ __device__ inline int score_stage_bytes(int tn) { return kABytes + tn * kTK * 2; }
+__host__ __device__ inline int score_stages(int tn) {
+    const int s = kScoreSmemBudget / score_stage_bytes(tn);
+    return s < kStagesMax ? s : kStagesMax;
+}
 
 __device__ __forceinline__ uint64_t order_key(float z, uint32_t idx) {
     // argmax_token compares with '>': -0 == +0 (canonicalised so the lower
@@ -217,7 +226,6 @@ __global__ void colsum_kernel(const __nv_bfloat16* __restrict__ wt, int width, i
 }
 
 constexpr int kPerTile = kScoreCandPerTile;  // candidates kept per (row, vocab tile) (overflow -> every n exactly)
-constexpr int kStash = 24;  // per-thread candidate stash of the epilogue (smem)
 
 struct ScoreArgs {
     int rows, width, vocab, a_passes;
@@ -233,6 +241,8 @@ struct ScoreArgs {
     int32_t* cand_n;           // [rows][n_tiles][kPerTile]
     float* cand_z;             // [rows][n_tiles][kPerTile]
     int n_tiles;
+    int tn, stages;            // tile width (vocab columns, multiple of 32) and ring depth
+    uint32_t idesc;            // M = 128, N = tn
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -247,27 +257,31 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesS * kStage);
-    uint64_t* empty = full + kStagesS;
-    uint64_t* acc_full = empty + kStagesS;
+    const int TN = sa.tn, NS = sa.stages, kStage = score_stage_bytes(TN);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * kStage);
+    uint64_t* empty = full + kStagesMax;
+    uint64_t* acc_full = empty + kStagesMax;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * kTM, n0 = blockIdx.y * kTN;
+    const int m0 = blockIdx.x * kTM, n0 = blockIdx.y * TN;
     const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-    if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta] = gtimer();
+    // debug (EP_TRACE=1): per CTA [start, first stage, MMAs done, scan done, candidates done, end, first TMEM load] ns
+    unsigned long long* trc = sa.trace && cta < 512 ? sa.trace + 8 * cta : nullptr;
+    unsigned long long* tr = threadIdx.x == 0 ? trc : nullptr;
+    if (tr) tr[0] = gtimer();
     const int nkw = sa.width / kTK;         // k-blocks of W per pass
     const int nk = nkw * sa.a_passes;        // A is [hi | lo] when a_passes == 2
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStagesS; ++s) {
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
         fence_mbar_init();
     }
-    if (warp == 5) umma::tmem_alloc(tmem_slot, kTN);
+    if (warp == 5) umma::tmem_alloc(tmem_slot, kTNMax);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -279,10 +293,11 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             umma::tma_prefetch_desc(&tmap_a);
             umma::tma_prefetch_desc(&tmap_w);
             const uint64_t pol = l2_policy_evict_last();  // W tiles are shared by the M tiles
+            const uint32_t wbytes = uint32_t(TN) * kTK * 2;
             for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kStagesS;
-                mbar_wait(&empty[s], ((kb / kStagesS) & 1) ^ 1);
-                mbar_arrive_expect_tx(&full[s], kStage);
+                const int s = kb % NS;
+                mbar_wait(&empty[s], ((kb / NS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&full[s], kABytes + wbytes);
                 uint8_t* dst = smem + s * kStage;
                 umma::tma_load_2d(dst, &tmap_a, kb * kTK, m0, &full[s], pol);
                 umma::tma_load_2d(dst + kABytes, &tmap_w, (kb % nkw) * kTK, n0, &full[s], pol);
@@ -292,84 +307,98 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         if (lane == 0) {
             const uint32_t base = smem_u32(smem);
             for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % kStagesS;
-                mbar_wait(&full[s], (kb / kStagesS) & 1);
-                if (kb == 0 && sa.trace) sa.trace[4 * cta + 1] = gtimer();
+                const int s = kb % NS;
+                mbar_wait(&full[s], (kb / NS) & 1);
+                if (kb == 0 && trc) trc[1] = gtimer();
                 umma::fence_after_sync();
                 const uint32_t a_addr = base + s * kStage, b_addr = a_addr + kABytes;
 #pragma unroll
                 for (int kk = 0; kk < kTK / 16; ++kk) {
                     const uint64_t ad = umma::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
                     const uint64_t bd = umma::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
-                    umma::mma_bf16_ss(tmem, ad, bd, kIdescScore, (kb | kk) ? 1u : 0u);
+                    umma::mma_bf16_ss(tmem, ad, bd, sa.idesc, (kb | kk) ? 1u : 0u);
                 }
                 umma::mma_commit(&empty[s]);
             }
             umma::mma_commit(acc_full);
         }
     } else {
-        // epilogue: thread = row (TMEM lane), kTN vocab columns. The tile's
-        // colsum slice and the row's mean are fetched while the MMAs run; TMEM
-        // is read 64 columns per wait.
+        // epilogue: thread = row (TMEM lane), TN vocab columns (32 per TMEM
+        // load). The tile's colsum slice and the row's mean are fetched while
+        // the MMAs run; columns past the vocabulary (a partial last tile: TMA
+        // zero-filled) are skipped.
         const int row = warp * 32 + lane;
         const int grow = m0 + row;
-        float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTN] colsum of this tile
-        for (int i = threadIdx.x; i < kTN; i += 128) s_cs[i] = sa.colsum[n0 + i];
+        float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of this tile
+        const int ncols = min(TN, sa.vocab - n0);
+        for (int i = threadIdx.x; i < ncols; i += 128) s_cs[i] = sa.colsum[n0 + i];
         const bool valid = grow < sa.rows;
         // (rows already centred for the hi-only pass: no mean * colsum term)
         const float mu = valid && !sa.cand_n ? sa.mean[grow] : 0.f;
         const float rs = valid ? sa.rstd[grow] : 0.f;
         named_bar_sync(1, 128);
         mbar_wait(acc_full, 0);
-        if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 2] = gtimer();
+        if (tr) tr[2] = gtimer();
         umma::fence_after_sync();
         float best = -INFINITY;
         uint32_t best_i = 0;
         // hi-only pass: every n of the tile that can still be the row's
         // argmax has z_hi >= tile max - 2 E_row (the row max is >= the tile
-        // max). One TMEM pass: after each 64-column chunk, the chunk's values
+        // max). One TMEM pass: after each 32-column chunk, the chunk's values
         // within 2 E_row of the running max go to a per-thread smem stash (a
         // superset: the max only grows), filtered by the final max at the end.
         const bool emit = sa.cand_n != nullptr;
         const float eb2 = emit && valid ? 2.f * sa.ebound[grow] : 0.f;
-        float* st_z = reinterpret_cast<float*>(s_cs + kTN);                 // [kStash][128]
+        float* st_z = reinterpret_cast<float*>(s_cs + kTNMax);              // [kStash][128]
         uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * 128);    // [kStash][128]
         const int me = threadIdx.x;
         int n_st = 0;
-#pragma unroll 1
-        for (int c = 0; c < kTN / 32; c += 2) {
-            uint32_t r[64];
-            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r));
-            umma::tmem_ld32(tmem + (uint32_t(warp * 32) << 16) + c * 32 + 32,
-                            *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-            umma::tmem_wait_ld();
-            if (valid) {
+        const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+        auto scan = [&](uint32_t (&cur)[32], int c) {
+            if (!valid) return;
+            const int nlim = ncols - c * 32;  // valid columns of this chunk
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int nl = c * 32 + j;
-                    const float z = fmaf(-mu, s_cs[nl], __uint_as_float(r[j]));
-                    r[j] = __float_as_uint(z);
-                    const bool up = z > best;  // strict: ties keep the lowest id
-                    best = up ? z : best;
-                    best_i = up ? uint32_t(n0 + nl) : best_i;
-                    if (sa.logits) sa.logits[size_t(grow) * sa.vocab + n0 + nl] = z * rs;
-                }
-                if (emit) {
-                    const float thr = best - eb2;
+            for (int j = 0; j < 32; ++j) {
+                const int nl = c * 32 + j;
+                const float z = j < nlim ? fmaf(-mu, s_cs[nl], __uint_as_float(cur[j])) : -INFINITY;
+                cur[j] = __float_as_uint(z);
+                const bool up = z > best;  // strict: ties keep the lowest id
+                best = up ? z : best;
+                best_i = up ? uint32_t(n0 + nl) : best_i;
+                if (sa.logits && j < nlim) sa.logits[size_t(grow) * sa.vocab + n0 + nl] = z * rs;
+            }
+            if (emit) {
+                const float thr = best - eb2;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        const float z = __uint_as_float(r[j]);
-                        if (z >= thr) {
-                            if (n_st < kStash) {
-                                st_z[n_st * 128 + me] = z;
-                                st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
-                            }
-                            ++n_st;
+                for (int j = 0; j < 32; ++j) {
+                    const float z = __uint_as_float(cur[j]);
+                    if (z >= thr) {
+                        if (n_st < kStash) {
+                            st_z[n_st * 128 + me] = z;
+                            st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
                         }
+                        ++n_st;
                     }
                 }
             }
+        };
+        // two register sets: chunk c + 1 is loaded while chunk c is scanned
+        const int nch = TN / 32;
+        uint32_t ra[32], rb[32];
+        umma::tmem_ld32(trow, ra);
+#pragma unroll 1
+        for (int c = 0; c < nch; c += 2) {
+            umma::tmem_wait_ld();
+            if (c == 0 && tr) tr[6] = gtimer();
+            if (c + 1 < nch) umma::tmem_ld32(trow + (c + 1) * 32, rb);
+            scan(ra, c);
+            if (c + 1 < nch) {
+                umma::tmem_wait_ld();
+                if (c + 2 < nch) umma::tmem_ld32(trow + (c + 2) * 32, ra);
+                scan(rb, c + 1);
+            }
         }
+        if (tr) tr[3] = gtimer();
         if (valid) atomicMax(&sa.best[grow], order_key(best, best_i));
         if (emit && valid) {
             const float thr = best - eb2;
@@ -391,14 +420,15 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             }
             sa.cand_cnt[size_t(grow) * sa.n_tiles + blockIdx.y] = cnt;
         }
+        if (tr) tr[4] = gtimer();
     }
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 5) {
         umma::fence_after_sync();
-        umma::tmem_dealloc(tmem, kTN);
+        umma::tmem_dealloc(tmem, kTNMax);
     }
-    if (sa.trace && threadIdx.x == 0) sa.trace[4 * cta + 3] = gtimer();
+    if (tr) tr[5] = gtimer();
 }
 
 __device__ __forceinline__ float key_value(unsigned long long k) {
@@ -566,13 +596,20 @@ cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, f
     return cudaGetLastError();
 }
 
-cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn_out, void* split,
+int score_tile_n(int rows, int vocab, int n_sms) {
+    const int m_tiles = (rows + kTM - 1) / kTM;
+    const int n_max = n_sms / m_tiles > 0 ? n_sms / m_tiles : 1;
+    int tn = (vocab + n_max - 1) / n_max;
+    tn = (tn + 31) / 32 * 32;
+    return tn < 32 ? 32 : tn > kTNMax ? kTNMax : tn;
+}
+
+cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
                                 const float* colsum, float* mean, float* rstd,
                                 unsigned long long* best, float* logits, int batch, int n_q,
                                 const int32_t* drafts, int32_t* target, int32_t* n_accepted,
                                 const RefineArgs& rf, cudaStream_t s) {
-    if (cudaError_t e = ensure_smem<score_argmax_kernel>(kScoreSmem)) return e;
     // (the argmax keys are cleared first so row stats -> GEMM -> refine stay
     // adjacent kernels for programmatic dependent launch)
     cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
@@ -594,11 +631,15 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
         return b;
     }();
     // fp32 rows: the GEMM on the bf16 hi part only, then the exact refinement
+    const int n_tiles = (vocab + tn - 1) / tn;
     ScoreArgs sa{rows, width, vocab, 1, mean, rstd, colsum, best, split ? nullptr : logits, trace,
                  split ? rf.ebound : nullptr, split ? rf.cand_cnt : nullptr, split ? rf.cand_n : nullptr,
-                 split ? rf.cand_z : nullptr, vocab / kTN};
-    dim3 grid((rows + kTM - 1) / kTM, vocab / kTN);
-    e = launch_pdl(score_argmax_kernel, grid, dim3(kScoreThreads), kScoreSmem, s, sa, tmap_a, tmap_w);
+                 split ? rf.cand_z : nullptr, n_tiles, tn, score_stages(tn),
+                 umma::idesc_bf16_f32(kTM, tn, false, false)};
+    const int smem = score_stages(tn) * score_stage_bytes(tn) + kScoreSmemFixed;
+    if (cudaError_t e2 = ensure_smem<score_argmax_kernel>(227 * 1024)) return e2;
+    dim3 grid((rows + kTM - 1) / kTM, n_tiles);
+    e = launch_pdl(score_argmax_kernel, grid, dim3(kScoreThreads), smem, s, sa, tmap_a, tmap_w);
     if (e != cudaSuccess) return e;
     if (trace) {  // debug: dump the per-CTA timeline of this launch
         std::vector<unsigned long long> host(4096);
@@ -613,7 +654,7 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, const void* attn
     if (split)
         e = launch_pdl(refine_kernel, dim3(rows), dim3(kRefineThreads), size_t(width) * 4, s,
                        static_cast<const float*>(attn_out), static_cast<const __nv_bfloat16*>(rf.wt), width, vocab,
-                       vocab / kTN, static_cast<const int32_t*>(rf.cand_cnt), static_cast<const int32_t*>(rf.cand_n),
+                       n_tiles, static_cast<const int32_t*>(rf.cand_cnt), static_cast<const int32_t*>(rf.cand_n),
                        static_cast<const float*>(rf.cand_z), static_cast<const float*>(mean),
                        static_cast<const float*>(rstd), static_cast<const float*>(rf.ebound), best, logits, n_q,
                        rf.req_count, drafts, target, n_accepted);
