@@ -83,8 +83,11 @@ __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) {
 // product keeps fp32-level accuracy.
 template <typename T>
 __global__ void row_stats_kernel(const T* __restrict__ x, int width, float* __restrict__ mean,
-                                 float* __restrict__ rstd, __nv_bfloat16* __restrict__ split) {
+                                 float* __restrict__ rstd, __nv_bfloat16* __restrict__ split,
+                                 unsigned long long* __restrict__ best_key) {
     const int row = blockIdx.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the attention output is complete
+    if (threadIdx.x == 0) best_key[row] = 0ull;
     const T* xr = x + size_t(row) * width;
     __shared__ float red[32];
     float s = 0.f;
@@ -128,10 +131,24 @@ constexpr int kStatVec = 8;
 __global__ void __launch_bounds__(kStatThreads)
     row_stats_split_kernel(const float* __restrict__ x, int width, float* __restrict__ mean,
                            float* __restrict__ rstd, __nv_bfloat16* __restrict__ hi_out,
-                           const float* __restrict__ wmax2, float* __restrict__ ebound) {
+                           const float* __restrict__ wmax2, float* __restrict__ ebound,
+                           const uint8_t* __restrict__ w_bytes, size_t w_size,
+                           unsigned long long* __restrict__ best_key) {
     const int row = blockIdx.x, tid = threadIdx.x;
     const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * width);
     const int nv = width / 4;
+    // W_score is constant: bring this CTA's slice of it into L2 before
+    // waiting for the attention (programmatic dependent launch lets this
+    // overlap the attention's tail), so the GEMM's W tiles are L2 hits
+    // instead of first-touch DRAM reads on the critical path
+    if (w_bytes && tid < 4) {
+        const size_t per = ((w_size + gridDim.x - 1) / gridDim.x + 63) & ~size_t(63);
+        const size_t b0 = size_t(row) * per;
+        for (size_t off = b0 + size_t(tid) * 16384; off < b0 + per && off < w_size; off += 4 * 16384) {
+            const size_t n = min(min(size_t(16384), b0 + per - off), w_size - off);
+            bulk_prefetch_l2(w_bytes + off, uint32_t(n) & ~15u);
+        }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the attention output is complete
     __shared__ float red[3][kStatThreads / 32];
     float4 v[kStatVec];
@@ -184,6 +201,7 @@ __global__ void __launch_bounds__(kStatThreads)
     }
     __syncthreads();
     if (tid == 0) {
+        best_key[row] = 0ull;  // the GEMM's argmax key of this row starts empty
         float tq = 0.f, tl = 0.f, tx = 0.f;
 #pragma unroll
         for (int w = 0; w < kStatThreads / 32; ++w) {
@@ -254,9 +272,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __global__ void __launch_bounds__(kScoreThreads, 1)
     score_argmax_kernel(const ScoreArgs sa, const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_w) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    // 1 KB aligned base (SW128 atoms) derived from the __shared__ array by an
+    // offset, so every pointer below stays in the shared window (LDS / STS,
+    // not generic loads: the generic form made the epilogue scan 8.6 us)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int TN = sa.tn, NS = sa.stages, kStage = score_stage_bytes(TN);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * kStage);
     uint64_t* empty = full + kStagesMax;
@@ -354,48 +374,50 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
         const int me = threadIdx.x;
         int n_st = 0;
         const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
-        auto scan = [&](uint32_t (&cur)[32], int c) {
-            if (!valid) return;
-            const int nlim = ncols - c * 32;  // valid columns of this chunk
+        const bool fold = mu != 0.f;        // bf16 rows: LN(x).w = rstd (x.w - mean colsum(w))
+        float* logits_row = sa.logits ? sa.logits + size_t(grow) * sa.vocab + n0 : nullptr;
+        // one 32-column TMEM load per chunk, the chunk loop kept rolled: the
+        // scan is straight-line code executed once per warp, and an unrolled
+        // 8-chunk body (~40 KB of SASS) ran at instruction-fetch speed
+        const int nch = TN / 32;
+#pragma unroll 1
+        for (int c = 0; c < nch; ++c) {
+            uint32_t buf[32];
+            umma::tmem_ld32(trow + c * 32, buf);
+            umma::tmem_wait_ld();
+            if (c == 0 && tr) tr[6] = gtimer();
+            // warp-uniform (rows past the last valid one score -inf)
+            const int nlim = valid ? ncols - c * 32 : 0;  // valid columns of this chunk
+            float z[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int nl = c * 32 + j;
-                const float z = j < nlim ? fmaf(-mu, s_cs[nl], __uint_as_float(cur[j])) : -INFINITY;
-                cur[j] = __float_as_uint(z);
-                const bool up = z > best;  // strict: ties keep the lowest id
-                best = up ? z : best;
-                best_i = up ? uint32_t(n0 + nl) : best_i;
-                if (sa.logits && j < nlim) sa.logits[size_t(grow) * sa.vocab + n0 + nl] = z * rs;
+                float v = __uint_as_float(buf[j]);
+                if (fold) v = fmaf(-mu, s_cs[c * 32 + j], v);
+                z[j] = j < nlim ? v : -INFINITY;
+                const bool up = z[j] > best;  // strict: ties keep the lowest id
+                best = up ? z[j] : best;
+                best_i = up ? uint32_t(n0 + c * 32 + j) : best_i;
+            }
+            if (logits_row && valid) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < nlim) logits_row[c * 32 + j] = z[j] * rs;
             }
             if (emit) {
+                // candidates are rare after the first chunks: a warp vote
+                // skips the store path unless some lane has one
                 const float thr = best - eb2;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const float z = __uint_as_float(cur[j]);
-                    if (z >= thr) {
-                        if (n_st < kStash) {
-                            st_z[n_st * 128 + me] = z;
+                    const bool pass = valid && z[j] >= thr;
+                    if (__any_sync(0xffffffffu, pass)) {
+                        if (pass && n_st < kStash) {
+                            st_z[n_st * 128 + me] = z[j];
                             st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
                         }
-                        ++n_st;
+                        n_st += pass ? 1 : 0;
                     }
                 }
-            }
-        };
-        // two register sets: chunk c + 1 is loaded while chunk c is scanned
-        const int nch = TN / 32;
-        uint32_t ra[32], rb[32];
-        umma::tmem_ld32(trow, ra);
-#pragma unroll 1
-        for (int c = 0; c < nch; c += 2) {
-            umma::tmem_wait_ld();
-            if (c == 0 && tr) tr[6] = gtimer();
-            if (c + 1 < nch) umma::tmem_ld32(trow + (c + 1) * 32, rb);
-            scan(ra, c);
-            if (c + 1 < nch) {
-                umma::tmem_wait_ld();
-                if (c + 2 < nch) umma::tmem_ld32(trow + (c + 2) * 32, ra);
-                scan(rb, c + 1);
             }
         }
         if (tr) tr[3] = gtimer();
@@ -610,17 +632,19 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const vo
                                 unsigned long long* best, float* logits, int batch, int n_q,
                                 const int32_t* drafts, int32_t* target, int32_t* n_accepted,
                                 const RefineArgs& rf, cudaStream_t s) {
-    // (the argmax keys are cleared first so row stats -> GEMM -> refine stay
-    // adjacent kernels for programmatic dependent launch)
-    cudaError_t e = cudaMemsetAsync(best, 0, sizeof(unsigned long long) * rows, s);
-    if (e != cudaSuccess) return e;
+    // (the argmax keys are cleared by the row-stats kernel, so attention ->
+    // row stats -> GEMM -> refine are adjacent kernels for programmatic
+    // dependent launch)
+    cudaError_t e = cudaSuccess;
     if (split)
         e = launch_pdl(row_stats_split_kernel, dim3(rows), dim3(kStatThreads), 0, s,
                        static_cast<const float*>(attn_out), width, mean, rstd,
-                       static_cast<__nv_bfloat16*>(split), static_cast<const float*>(rf.wmax2), rf.ebound);
+                       static_cast<__nv_bfloat16*>(split), static_cast<const float*>(rf.wmax2), rf.ebound,
+                       static_cast<const uint8_t*>(rf.wt), size_t(width) * size_t(vocab) * 2, best);
     else
-        row_stats_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(
-            static_cast<const __nv_bfloat16*>(attn_out), width, mean, rstd, nullptr);
+        e = launch_pdl(row_stats_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, s,
+                       static_cast<const __nv_bfloat16*>(attn_out), width, mean, rstd,
+                       static_cast<__nv_bfloat16*>(nullptr), best);
     if (e != cudaSuccess) return e;
 
     static unsigned long long* trace = [] {
