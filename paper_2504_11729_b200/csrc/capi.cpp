@@ -370,7 +370,8 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
     const int32_t rows = batch * n_q;
     const int tn = score_tile_n(rows, v->vocab, h->n_sms);
     if (v->w_tn != tn) {
-        if (int rc = encode_bf16_2d(&v->tmap_w, v->w_t, uint64_t(v->width), uint64_t(v->vocab), 64, uint32_t(tn)))
+        if (int rc = encode_bf16_2d(&v->tmap_w, v->w_t, uint64_t(v->width), uint64_t(v->vocab), 64,
+                                    uint32_t(score_w_box_rows(tn))))
             return rc;
         v->w_tn = tn;
     }

@@ -236,8 +236,10 @@ cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, f
 // within the per-row error bound (kern_score.cu).
 constexpr int kScoreTileNMax = 256;    // vocabulary columns per K4 score tile, at most (one TMEM accumulator)
 constexpr int kScoreCandPerTile = 16;  // candidate slots per (row, vocab tile)
-// K4 tile width for `rows` score rows: one wave of CTAs over n_sms SMs.
+// K4 tile width for `rows` score rows: one wave of CTAs (or CTA pairs) over
+// n_sms SMs; rows of the W tensor-map box for that width.
 int score_tile_n(int rows, int vocab, int n_sms);
+int score_w_box_rows(int tn);
 struct RefineArgs {
     const void* wt = nullptr;      // W^T bf16 [vocab][width]
     const float* wmax2 = nullptr;  // max_n ||W^T[n]||_2

@@ -269,6 +269,116 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// Epilogue of a score tile: the 4 epilogue warps, thread = accumulator row
+// (TMEM lane) of this CTA's 128 rows [m0, m0 + 128), TN vocab columns from
+// n0: LN fold, tile argmax (64-bit key atomicMax per row) and, on the hi-only
+// pass, the refinement candidates of the tile.
+__device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tmem, uint64_t* acc_full,
+                                               uint32_t* tmem_slot, int m0, int n0, int TN,
+                                               unsigned long long* tr) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // epilogue: thread = row (TMEM lane), TN vocab columns (32 per TMEM
+    // load). The tile's colsum slice and the row's mean are fetched while
+    // the MMAs run; columns past the vocabulary (a partial last tile: TMA
+    // zero-filled) are skipped.
+    const int row = warp * 32 + lane;
+    const int grow = m0 + row;
+    float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of this tile
+    const int ncols = min(TN, sa.vocab - n0);
+    for (int i = threadIdx.x; i < ncols; i += 128) s_cs[i] = sa.colsum[n0 + i];
+    const bool valid = grow < sa.rows;
+    // (rows already centred for the hi-only pass: no mean * colsum term)
+    const float mu = valid && !sa.cand_n ? sa.mean[grow] : 0.f;
+    const float rs = valid ? sa.rstd[grow] : 0.f;
+    named_bar_sync(1, 128);
+    mbar_wait(acc_full, 0);
+    if (tr) tr[2] = gtimer();
+    umma::fence_after_sync();
+    float best = -INFINITY;
+    uint32_t best_i = 0;
+    // hi-only pass: every n of the tile that can still be the row's
+    // argmax has z_hi >= tile max - 2 E_row (the row max is >= the tile
+    // max). One TMEM pass: after each 32-column chunk, the chunk's values
+    // within 2 E_row of the running max go to a per-thread smem stash (a
+    // superset: the max only grows), filtered by the final max at the end.
+    const bool emit = sa.cand_n != nullptr;
+    const float eb2 = emit && valid ? 2.f * sa.ebound[grow] : 0.f;
+    float* st_z = reinterpret_cast<float*>(s_cs + kTNMax);              // [kStash][128]
+    uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * 128);    // [kStash][128]
+    const int me = threadIdx.x;
+    int n_st = 0;
+    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
+    const bool fold = mu != 0.f;        // bf16 rows: LN(x).w = rstd (x.w - mean colsum(w))
+    float* logits_row = sa.logits ? sa.logits + size_t(grow) * sa.vocab + n0 : nullptr;
+    // one 32-column TMEM load per chunk, the chunk loop kept rolled: the
+    // scan is straight-line code executed once per warp, and an unrolled
+    // 8-chunk body (~40 KB of SASS) ran at instruction-fetch speed
+    const int nch = TN / 32;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c) {
+        uint32_t buf[32];
+        umma::tmem_ld32(trow + c * 32, buf);
+        umma::tmem_wait_ld();
+        if (c == 0 && tr) tr[6] = gtimer();
+        // warp-uniform (rows past the last valid one score -inf)
+        const int nlim = valid ? ncols - c * 32 : 0;  // valid columns of this chunk
+        float z[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float v = __uint_as_float(buf[j]);
+            if (fold) v = fmaf(-mu, s_cs[c * 32 + j], v);
+            z[j] = j < nlim ? v : -INFINITY;
+            const bool up = z[j] > best;  // strict: ties keep the lowest id
+            best = up ? z[j] : best;
+            best_i = up ? uint32_t(n0 + c * 32 + j) : best_i;
+        }
+        if (logits_row && valid) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nlim) logits_row[c * 32 + j] = z[j] * rs;
+        }
+        if (emit) {
+            // candidates are rare after the first chunks: a warp vote
+            // skips the store path unless some lane has one
+            const float thr = best - eb2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const bool pass = valid && z[j] >= thr;
+                if (__any_sync(0xffffffffu, pass)) {
+                    if (pass && n_st < kStash) {
+                        st_z[n_st * 128 + me] = z[j];
+                        st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
+                    }
+                    n_st += pass ? 1 : 0;
+                }
+            }
+        }
+    }
+    if (tr) tr[3] = gtimer();
+    if (valid) atomicMax(&sa.best[grow], order_key(best, best_i));
+    if (emit && valid) {
+        const float thr = best - eb2;
+        const size_t slot0 = (size_t(grow) * sa.n_tiles + blockIdx.y) * kPerTile;
+        int cnt = 0;
+        if (n_st > kStash) {
+            cnt = kPerTile + 1;  // stash overflow: refine scores the whole row
+        } else {
+            for (int i = 0; i < n_st; ++i) {
+                const float z = st_z[i * 128 + me];
+                if (z >= thr) {
+                    if (cnt < kPerTile) {
+                        sa.cand_n[slot0 + cnt] = n0 + st_n[i * 128 + me];
+                        sa.cand_z[slot0 + cnt] = z;
+                    }
+                    ++cnt;
+                }
+            }
+        }
+        sa.cand_cnt[size_t(grow) * sa.n_tiles + blockIdx.y] = cnt;
+    }
+    if (tr) tr[4] = gtimer();
+}
+
 __global__ void __launch_bounds__(kScoreThreads, 1)
     score_argmax_kernel(const ScoreArgs sa, const __grid_constant__ CUtensorMap tmap_a,
                         const __grid_constant__ CUtensorMap tmap_w) {
@@ -343,112 +453,104 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
             umma::mma_commit(acc_full);
         }
     } else {
-        // epilogue: thread = row (TMEM lane), TN vocab columns (32 per TMEM
-        // load). The tile's colsum slice and the row's mean are fetched while
-        // the MMAs run; columns past the vocabulary (a partial last tile: TMA
-        // zero-filled) are skipped.
-        const int row = warp * 32 + lane;
-        const int grow = m0 + row;
-        float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of this tile
-        const int ncols = min(TN, sa.vocab - n0);
-        for (int i = threadIdx.x; i < ncols; i += 128) s_cs[i] = sa.colsum[n0 + i];
-        const bool valid = grow < sa.rows;
-        // (rows already centred for the hi-only pass: no mean * colsum term)
-        const float mu = valid && !sa.cand_n ? sa.mean[grow] : 0.f;
-        const float rs = valid ? sa.rstd[grow] : 0.f;
-        named_bar_sync(1, 128);
-        mbar_wait(acc_full, 0);
-        if (tr) tr[2] = gtimer();
-        umma::fence_after_sync();
-        float best = -INFINITY;
-        uint32_t best_i = 0;
-        // hi-only pass: every n of the tile that can still be the row's
-        // argmax has z_hi >= tile max - 2 E_row (the row max is >= the tile
-        // max). One TMEM pass: after each 32-column chunk, the chunk's values
-        // within 2 E_row of the running max go to a per-thread smem stash (a
-        // superset: the max only grows), filtered by the final max at the end.
-        const bool emit = sa.cand_n != nullptr;
-        const float eb2 = emit && valid ? 2.f * sa.ebound[grow] : 0.f;
-        float* st_z = reinterpret_cast<float*>(s_cs + kTNMax);              // [kStash][128]
-        uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * 128);    // [kStash][128]
-        const int me = threadIdx.x;
-        int n_st = 0;
-        const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
-        const bool fold = mu != 0.f;        // bf16 rows: LN(x).w = rstd (x.w - mean colsum(w))
-        float* logits_row = sa.logits ? sa.logits + size_t(grow) * sa.vocab + n0 : nullptr;
-        // one 32-column TMEM load per chunk, the chunk loop kept rolled: the
-        // scan is straight-line code executed once per warp, and an unrolled
-        // 8-chunk body (~40 KB of SASS) ran at instruction-fetch speed
-        const int nch = TN / 32;
-#pragma unroll 1
-        for (int c = 0; c < nch; ++c) {
-            uint32_t buf[32];
-            umma::tmem_ld32(trow + c * 32, buf);
-            umma::tmem_wait_ld();
-            if (c == 0 && tr) tr[6] = gtimer();
-            // warp-uniform (rows past the last valid one score -inf)
-            const int nlim = valid ? ncols - c * 32 : 0;  // valid columns of this chunk
-            float z[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                float v = __uint_as_float(buf[j]);
-                if (fold) v = fmaf(-mu, s_cs[c * 32 + j], v);
-                z[j] = j < nlim ? v : -INFINITY;
-                const bool up = z[j] > best;  // strict: ties keep the lowest id
-                best = up ? z[j] : best;
-                best_i = up ? uint32_t(n0 + c * 32 + j) : best_i;
-            }
-            if (logits_row && valid) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (j < nlim) logits_row[c * 32 + j] = z[j] * rs;
-            }
-            if (emit) {
-                // candidates are rare after the first chunks: a warp vote
-                // skips the store path unless some lane has one
-                const float thr = best - eb2;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const bool pass = valid && z[j] >= thr;
-                    if (__any_sync(0xffffffffu, pass)) {
-                        if (pass && n_st < kStash) {
-                            st_z[n_st * 128 + me] = z[j];
-                            st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
-                        }
-                        n_st += pass ? 1 : 0;
-                    }
-                }
-            }
-        }
-        if (tr) tr[3] = gtimer();
-        if (valid) atomicMax(&sa.best[grow], order_key(best, best_i));
-        if (emit && valid) {
-            const float thr = best - eb2;
-            const size_t slot0 = (size_t(grow) * sa.n_tiles + blockIdx.y) * kPerTile;
-            int cnt = 0;
-            if (n_st > kStash) {
-                cnt = kPerTile + 1;  // stash overflow: refine scores the whole row
-            } else {
-                for (int i = 0; i < n_st; ++i) {
-                    const float z = st_z[i * 128 + me];
-                    if (z >= thr) {
-                        if (cnt < kPerTile) {
-                            sa.cand_n[slot0 + cnt] = n0 + st_n[i * 128 + me];
-                            sa.cand_z[slot0 + cnt] = z;
-                        }
-                        ++cnt;
-                    }
-                }
-            }
-            sa.cand_cnt[size_t(grow) * sa.n_tiles + blockIdx.y] = cnt;
-        }
-        if (tr) tr[4] = gtimer();
+        score_epilogue(sa, tmem, acc_full, tmem_slot, m0, n0, TN, tr);
     }
     umma::fence_before_sync();
     __syncthreads();
     if (warp == 5) {
         umma::fence_after_sync();
         umma::tmem_dealloc(tmem, kTNMax);
+    }
+    if (tr) tr[5] = gtimer();
+}
+
+// The same GEMM on CTA pairs (cta_group::2): a cluster of two CTAs on one TPC
+// computes a 256-row x tn tile with M = 256 MMAs issued by the even CTA. Each
+// CTA streams its 128 rows of A and half of the tile's W rows (tn / 2) into
+// the same shared-memory offsets; the tensor cores read A from each CTA and B
+// from both, so the shared-memory bytes per FLOP halve against the 1-SM form
+// (whose mainloop is shared-memory-bandwidth bound: operand reads + TMA writes
+// of ~230 B/clk per SM against the 128 B/clk port). Stage fills complete on
+// the even CTA's mbarriers; each MMA commit frees the stage in both CTAs.
+__global__ void __launch_bounds__(kScoreThreads, 1)
+    score_argmax_pair_kernel(const ScoreArgs sa, const __grid_constant__ CUtensorMap tmap_a,
+                             const __grid_constant__ CUtensorMap tmap_w) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int TN = sa.tn, NS = sa.stages, kStage = kABytes + (TN / 2) * kTK * 2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * kStage);
+    uint64_t* empty = full + kStagesMax;
+    uint64_t* acc_full = empty + kStagesMax;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = umma::cluster_ctarank();
+    const int m0 = (blockIdx.x >> 1) * (2 * kTM) + int(rank) * kTM, n0 = blockIdx.y * TN;
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    unsigned long long* trc = sa.trace && cta < 512 ? sa.trace + 8 * cta : nullptr;
+    unsigned long long* tr = threadIdx.x == 0 ? trc : nullptr;
+    if (tr) tr[0] = gtimer();
+    const int nkw = sa.width / kTK;
+    const int nk = nkw * sa.a_passes;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 5) umma::tmem_alloc_pair(tmem_slot, kTNMax);
+    umma::fence_before_sync();
+    umma::cluster_sync();  // both CTAs' barriers initialised and TMEM allocated
+    umma::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // A (row stats output) is complete
+
+    if (warp == 4) {
+        if (lane == 0) {
+            umma::tma_prefetch_desc(&tmap_a);
+            umma::tma_prefetch_desc(&tmap_w);
+            const uint64_t pol = l2_policy_evict_last();
+            const int nb = n0 + int(rank) * (TN / 2);  // this CTA's half of the tile's W rows
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % NS;
+                mbar_wait(&empty[s], ((kb / NS) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&full[s], 2u * uint32_t(kStage));
+                const uint32_t bar0 = umma::mapa_shared(&full[s], 0);
+                uint8_t* dst = smem + s * kStage;
+                umma::tma_load_2d_pair(dst, &tmap_a, kb * kTK, m0, bar0, pol);
+                umma::tma_load_2d_pair(dst + kABytes, &tmap_w, (kb % nkw) * kTK, nb, bar0, pol);
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0 && rank == 0) {
+            const uint32_t base = smem_u32(smem);
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % NS;
+                mbar_wait(&full[s], (kb / NS) & 1);
+                if (kb == 0 && trc) trc[1] = gtimer();
+                umma::fence_after_sync();
+                const uint32_t a_addr = base + s * kStage, b_addr = a_addr + kABytes;
+#pragma unroll
+                for (int kk = 0; kk < kTK / 16; ++kk) {
+                    const uint64_t ad = umma::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+                    const uint64_t bd = umma::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                    umma::mma_bf16_ss_pair(tmem, ad, bd, sa.idesc, (kb | kk) ? 1u : 0u);
+                }
+                umma::mma_commit_pair(&empty[s], 0x3);
+            }
+            umma::mma_commit_pair(acc_full, 0x3);
+        }
+    } else {
+        score_epilogue(sa, tmem, acc_full, tmem_slot, m0, n0, TN, tr);
+    }
+    umma::fence_before_sync();
+    umma::cluster_sync();  // no CTA leaves while its peer may still signal or read it
+    if (warp == 5) {
+        umma::fence_after_sync();
+        umma::tmem_dealloc_pair(tmem, kTNMax);
     }
     if (tr) tr[5] = gtimer();
 }
@@ -618,13 +720,28 @@ cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, f
     return cudaGetLastError();
 }
 
+bool score_pairs() {
+    static const bool one_sm = [] {
+        const char* e = std::getenv("EP_K4_1SM");
+        return e && e[0] == '1';
+    }();
+    return !one_sm;
+}
+
+// Tile width for one wave: 1-SM tiles of 128 rows over n_sms CTAs, or (the
+// default) CTA-pair tiles of 256 rows over n_sms / 2 pairs; a multiple of 32
+// (epilogue chunks; for pairs also the per-CTA half of 16-row TMA boxes).
 int score_tile_n(int rows, int vocab, int n_sms) {
-    const int m_tiles = (rows + kTM - 1) / kTM;
-    const int n_max = n_sms / m_tiles > 0 ? n_sms / m_tiles : 1;
+    const bool pairs = score_pairs();
+    const int m_tiles = pairs ? (rows + 2 * kTM - 1) / (2 * kTM) : (rows + kTM - 1) / kTM;
+    const int slots = pairs ? n_sms / 2 : n_sms;
+    const int n_max = slots / m_tiles > 0 ? slots / m_tiles : 1;
     int tn = (vocab + n_max - 1) / n_max;
     tn = (tn + 31) / 32 * 32;
     return tn < 32 ? 32 : tn > kTNMax ? kTNMax : tn;
 }
+
+int score_w_box_rows(int tn) { return score_pairs() ? tn / 2 : tn; }
 
 cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
@@ -660,10 +777,34 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const vo
                  split ? rf.ebound : nullptr, split ? rf.cand_cnt : nullptr, split ? rf.cand_n : nullptr,
                  split ? rf.cand_z : nullptr, n_tiles, tn, score_stages(tn),
                  umma::idesc_bf16_f32(kTM, tn, false, false)};
-    const int smem = score_stages(tn) * score_stage_bytes(tn) + kScoreSmemFixed;
-    if (cudaError_t e2 = ensure_smem<score_argmax_kernel>(227 * 1024)) return e2;
-    dim3 grid((rows + kTM - 1) / kTM, n_tiles);
-    e = launch_pdl(score_argmax_kernel, grid, dim3(kScoreThreads), smem, s, sa, tmap_a, tmap_w);
+    if (score_pairs()) {
+        // CTA pairs: stage = A 16 KB + half of the W rows
+        const int stage = kABytes + (tn / 2) * kTK * 2;
+        sa.stages = std::min(kStagesMax, kScoreSmemBudget / stage);
+        sa.idesc = umma::idesc_bf16_f32(2 * kTM, tn, false, false);
+        const int smem = sa.stages * stage + kScoreSmemFixed;
+        if (cudaError_t e2 = ensure_smem<score_argmax_pair_kernel>(227 * 1024)) return e2;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2 * ((rows + 2 * kTM - 1) / (2 * kTM)), n_tiles);
+        cfg.blockDim = dim3(kScoreThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 2;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        e = cudaLaunchKernelEx(&cfg, score_argmax_pair_kernel, sa, tmap_a, tmap_w);
+    } else {
+        const int smem = score_stages(tn) * score_stage_bytes(tn) + kScoreSmemFixed;
+        if (cudaError_t e2 = ensure_smem<score_argmax_kernel>(227 * 1024)) return e2;
+        dim3 grid((rows + kTM - 1) / kTM, n_tiles);
+        e = launch_pdl(score_argmax_kernel, grid, dim3(kScoreThreads), smem, s, sa, tmap_a, tmap_w);
+    }
     if (e != cudaSuccess) return e;
     if (trace) {  // debug: dump the per-CTA timeline of this launch
         std::vector<unsigned long long> host(4096);
