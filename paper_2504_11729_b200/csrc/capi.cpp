@@ -324,6 +324,8 @@ struct ep_verifier_s {
     CUtensorMap tmap_w{};
     DeviceBuffer colsum, mean, rstd, best, split, wmax2, ebound, cand_cnt, cand_n, cand_z, req_count;
     size_t req_count_n = 0;
+    DeviceBuffer sk_ws, sk_flags;  // stream-K score GEMM partial tiles and their flags
+    bool sk_ready = false;
     CUtensorMap tmap_a{};
     const void* a_ptr = nullptr;
     int32_t a_rows = -1, a_dtype = -1;
@@ -388,7 +390,7 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
         // the bf16 hi part of the rows is the GEMM's A operand
         EP_CUDA_TRY(v->split.reserve(size_t(rows) * v->width * 2), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->ebound.reserve(size_t(rows) * sizeof(float)), "ep_verify_greedy ws");
-        const size_t n_tiles = size_t((v->vocab + tn - 1) / tn);
+        const size_t n_tiles = size_t(score_cand_tiles(v->vocab, tn));
         const size_t slots = n_tiles * kScoreCandPerTile;  // [rows][vocab tiles][per tile]
         EP_CUDA_TRY(v->cand_cnt.reserve(size_t(rows) * n_tiles * sizeof(int32_t)), "ep_verify_greedy ws");
         EP_CUDA_TRY(v->cand_n.reserve(size_t(rows) * slots * sizeof(int32_t)), "ep_verify_greedy ws");
@@ -409,6 +411,19 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
             v->req_count_n = size_t(batch);
         }
         rf.req_count = static_cast<int32_t*>(v->req_count.ptr);
+    }
+    if (score_mode() == kScoreStreamK) {
+        if (!v->sk_ready) {  // flags start at zero; every launch leaves them at zero
+            EP_CUDA_TRY(v->sk_ws.reserve(score_streamk_ws_bytes(h->n_sms)), "ep_verify_greedy ws");
+            EP_CUDA_TRY(v->sk_flags.reserve(size_t(h->n_sms) * sizeof(unsigned int)), "ep_verify_greedy ws");
+            EP_CUDA_TRY(cudaMemsetAsync(v->sk_flags.ptr, 0, size_t(h->n_sms) * sizeof(unsigned int),
+                                        static_cast<cudaStream_t>(stream)),
+                        "ep_verify_greedy ws");
+            v->sk_ready = true;
+        }
+        rf.sk_ws = static_cast<float*>(v->sk_ws.ptr);
+        rf.sk_flags = static_cast<unsigned int*>(v->sk_flags.ptr);
+        rf.sk_ctas = h->n_sms;
     }
     if (v->a_ptr != a_src || v->a_rows != rows || v->a_dtype != attn_dtype) {
         if (int rc = encode_bf16_2d(&v->tmap_a, a_src, a_inner, uint64_t(rows), 64, 128)) return rc;

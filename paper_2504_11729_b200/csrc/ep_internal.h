@@ -238,8 +238,12 @@ constexpr int kScoreTileNMax = 256;    // vocabulary columns per K4 score tile, 
 constexpr int kScoreCandPerTile = 16;  // candidate slots per (row, vocab tile)
 // K4 tile width for `rows` score rows: one wave of CTAs (or CTA pairs) over
 // n_sms SMs; rows of the W tensor-map box for that width.
+constexpr int kScoreStreamK = 0, kScorePair = 1, kScoreOneSm = 2;
+int score_mode();
 int score_tile_n(int rows, int vocab, int n_sms);
 int score_w_box_rows(int tn);
+int score_cand_tiles(int vocab, int tn);
+size_t score_streamk_ws_bytes(int n_sms);
 struct RefineArgs {
     const void* wt = nullptr;      // W^T bf16 [vocab][width]
     const float* wmax2 = nullptr;  // max_n ||W^T[n]||_2
@@ -248,6 +252,9 @@ struct RefineArgs {
     int32_t* cand_n = nullptr;     // [rows][vocab tiles][kScoreCandPerTile]
     float* cand_z = nullptr;       // [rows][vocab tiles][kScoreCandPerTile]
     int32_t* req_count = nullptr;  // [batch] row arrivals of the fused accept, zero between launches
+    float* sk_ws = nullptr;        // stream-K GEMM: [sk_ctas] fp32 partial tiles (score_streamk_ws_bytes)
+    unsigned int* sk_flags = nullptr;  // [sk_ctas], zero between launches
+    int sk_ctas = 0;
 };
 cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,

@@ -53,6 +53,12 @@ constexpr int kScoreThreads = 192;      // warps 0-3 epilogue, 4 TMA, 5 MMA
 constexpr int kStash = 24;              // per-thread candidate stash of the epilogue (smem)
 constexpr int kScoreSmemFixed = 1024 + 256 + kTNMax * 4 + kStash * 128 * 5;  // align, barriers, colsum slice, stash
 constexpr int kScoreSmemBudget = 227 * 1024 - kScoreSmemFixed;
+// stream-K kernel: 8 epilogue warps (two per TMEM lane quarter, each taking
+// half of a tile's chunks), then the TMA and MMA warps
+constexpr int kSkEpiThreads = 256;
+constexpr int kSkThreads = kSkEpiThreads + 64;
+constexpr int kSkWarpTma = kSkEpiThreads / 32, kSkWarpMma = kSkWarpTma + 1;
+constexpr int kSkSmemFixed = 1024 + 256 + kTNMax * 4 + kStash * kSkEpiThreads * 5;
 
 __host__ __device__ inline int score_stage_bytes(int tn) { return kABytes + tn * kTK * 2; }
 __host__ __device__ inline int score_stages(int tn) {
@@ -261,6 +267,11 @@ struct ScoreArgs {
     int n_tiles;
     int tn, stages;            // tile width (vocab columns, multiple of 32) and ring depth
     uint32_t idesc;            // M = 128, N = tn
+    // stream-K (score_argmax_streamk_kernel): tiles_m x n_tiles tiles of nkt
+    // k-blocks, flattened M-fastest and cut into gridDim.x equal ranges
+    int tiles_m = 0, nkt = 0, n_vt = 0;  // (n_tiles counts the 128-column candidate tiles)
+    float* sk_ws = nullptr;          // [ctas][kTNMax / 32][8][128] float4 partial tiles
+    unsigned int* sk_flags = nullptr;  // [ctas] partial published (1) / consumed (0)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -269,31 +280,30 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// Epilogue of a score tile: the 4 epilogue warps, thread = accumulator row
-// (TMEM lane) of this CTA's 128 rows [m0, m0 + 128), TN vocab columns from
-// n0: LN fold, tile argmax (64-bit key atomicMax per row) and, on the hi-only
-// pass, the refinement candidates of the tile.
-__device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tmem, uint64_t* acc_full,
-                                               uint32_t* tmem_slot, int m0, int n0, int TN,
-                                               unsigned long long* tr) {
+// Scan of one finished score tile by the 4 epilogue warps, thread =
+// accumulator row (TMEM lane) of the 128 rows [m0, m0 + 128), TN vocab
+// columns from n0 (vocab tile `ntile`): LN fold, tile argmax (64-bit key
+// atomicMax per row) and, on the hi-only pass, the refinement candidates of
+// the tile. The tile's colsum slice is in s_cs. Stream-K owners add the
+// fp32 partial tiles of CTAs [cp0, cp0 + n_part) (ws: [cta][chunk][4-float group][row])
+// to each accumulator chunk before scoring it.
+//
+// Chunks [c_lo, c_hi) of the tile are scanned by this warp (the stream-K
+// kernel splits a tile's 8 chunks over two warps per TMEM lane quarter);
+// their candidates go to candidate tile `ntile` (columns [n0 + 32 c_lo,
+// n0 + 32 c_hi)); nthr = epilogue threads (the stash stride).
+__device__ __forceinline__ void score_scan(const ScoreArgs& sa, uint32_t tmem, const float* s_cs, int m0, int n0,
+                                           int ntile, int TN, int c_lo, int c_hi, int nthr,
+                                           const float* __restrict__ ws, int cp0, int n_part,
+                                           const float4* spart, uint64_t* pbar, unsigned long long* tr) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // epilogue: thread = row (TMEM lane), TN vocab columns (32 per TMEM
-    // load). The tile's colsum slice and the row's mean are fetched while
-    // the MMAs run; columns past the vocabulary (a partial last tile: TMA
-    // zero-filled) are skipped.
-    const int row = warp * 32 + lane;
+    const int row = (warp & 3) * 32 + lane;
     const int grow = m0 + row;
-    float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of this tile
     const int ncols = min(TN, sa.vocab - n0);
-    for (int i = threadIdx.x; i < ncols; i += 128) s_cs[i] = sa.colsum[n0 + i];
     const bool valid = grow < sa.rows;
     // (rows already centred for the hi-only pass: no mean * colsum term)
     const float mu = valid && !sa.cand_n ? sa.mean[grow] : 0.f;
     const float rs = valid ? sa.rstd[grow] : 0.f;
-    named_bar_sync(1, 128);
-    mbar_wait(acc_full, 0);
-    if (tr) tr[2] = gtimer();
-    umma::fence_after_sync();
     float best = -INFINITY;
     uint32_t best_i = 0;
     // hi-only pass: every n of the tile that can still be the row's
@@ -303,23 +313,77 @@ __device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tme
     // superset: the max only grows), filtered by the final max at the end.
     const bool emit = sa.cand_n != nullptr;
     const float eb2 = emit && valid ? 2.f * sa.ebound[grow] : 0.f;
-    float* st_z = reinterpret_cast<float*>(s_cs + kTNMax);              // [kStash][128]
-    uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * 128);    // [kStash][128]
+    float* st_z = const_cast<float*>(s_cs) + kTNMax;                    // [kStash][nthr]
+    uint8_t* st_n = reinterpret_cast<uint8_t*>(st_z + kStash * nthr);   // [kStash][nthr]
     const int me = threadIdx.x;
     int n_st = 0;
-    const uint32_t trow = tmem + (uint32_t(warp * 32) << 16);
-    const bool fold = mu != 0.f;        // bf16 rows: LN(x).w = rstd (x.w - mean colsum(w))
+    const uint32_t trow = tmem + (uint32_t((warp & 3) * 32) << 16);
+    // bf16 rows: LN(x).w = rstd (x.w - mean colsum(w)); warp-uniform, so the
+    // hi-only pass (rows centred already) carries no colsum loads
+    const bool fold = !emit;
     float* logits_row = sa.logits ? sa.logits + size_t(grow) * sa.vocab + n0 : nullptr;
     // one 32-column TMEM load per chunk, the chunk loop kept rolled: the
     // scan is straight-line code executed once per warp, and an unrolled
     // 8-chunk body (~40 KB of SASS) ran at instruction-fetch speed
-    const int nch = TN / 32;
+    // stream-K partials: chunk c + 1 of the first partial is loaded while
+    // chunk c is scored (the loads are L2 round trips; 4 warps alone cannot
+    // hide them one chunk at a time)
+    // (ws layout [cta][chunk][j4][row] float4: one load instruction of a
+    // warp reads 512 contiguous bytes)
+    auto part_ptr = [&](int q, int c) {
+        return reinterpret_cast<const float4*>(ws) + (size_t(cp0 + q) * (kTNMax / 32) + c) * 8 * 128 + row;
+    };
+    // (spart: the first partial already on its way into shared memory, one
+    // bulk copy per chunk completing on pbar[chunk])
+    float4 pre[8];
+    if (n_part > 0 && !spart) {
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) pre[j4] = __ldcg(part_ptr(0, c_lo) + j4 * 128);
+    }
 #pragma unroll 1
-    for (int c = 0; c < nch; ++c) {
+    for (int c = c_lo; c < c_hi; ++c) {
         uint32_t buf[32];
         umma::tmem_ld32(trow + c * 32, buf);
         umma::tmem_wait_ld();
-        if (c == 0 && tr) tr[6] = gtimer();
+        if (c == c_lo && tr) tr[6] = gtimer();
+        if (spart) {
+            const unsigned long long w0 = tr ? gtimer() : 0ull;
+            mbar_wait(&pbar[c], 0);
+            if (tr) tr[7] += gtimer() - w0;
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 v = spart[(c * 8 + j4) * 128 + row];
+                buf[4 * j4 + 0] = __float_as_uint(__uint_as_float(buf[4 * j4 + 0]) + v.x);
+                buf[4 * j4 + 1] = __float_as_uint(__uint_as_float(buf[4 * j4 + 1]) + v.y);
+                buf[4 * j4 + 2] = __float_as_uint(__uint_as_float(buf[4 * j4 + 2]) + v.z);
+                buf[4 * j4 + 3] = __float_as_uint(__uint_as_float(buf[4 * j4 + 3]) + v.w);
+            }
+        } else if (n_part > 0) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 v = pre[j4];
+                buf[4 * j4 + 0] = __float_as_uint(__uint_as_float(buf[4 * j4 + 0]) + v.x);
+                buf[4 * j4 + 1] = __float_as_uint(__uint_as_float(buf[4 * j4 + 1]) + v.y);
+                buf[4 * j4 + 2] = __float_as_uint(__uint_as_float(buf[4 * j4 + 2]) + v.z);
+                buf[4 * j4 + 3] = __float_as_uint(__uint_as_float(buf[4 * j4 + 3]) + v.w);
+            }
+            if (c + 1 < c_hi) {
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) pre[j4] = __ldcg(part_ptr(0, c + 1) + j4 * 128);
+            }
+        }
+#pragma unroll 1
+        for (int q = 1; q < n_part; ++q) {
+            const float4* pp = part_ptr(q, c);
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+                const float4 v = __ldcg(pp + j4 * 128);
+                buf[4 * j4 + 0] = __float_as_uint(__uint_as_float(buf[4 * j4 + 0]) + v.x);
+                buf[4 * j4 + 1] = __float_as_uint(__uint_as_float(buf[4 * j4 + 1]) + v.y);
+                buf[4 * j4 + 2] = __float_as_uint(__uint_as_float(buf[4 * j4 + 2]) + v.z);
+                buf[4 * j4 + 3] = __float_as_uint(__uint_as_float(buf[4 * j4 + 3]) + v.w);
+            }
+        }
         // warp-uniform (rows past the last valid one score -inf)
         const int nlim = valid ? ncols - c * 32 : 0;  // valid columns of this chunk
         float z[32];
@@ -328,9 +392,23 @@ __device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tme
             float v = __uint_as_float(buf[j]);
             if (fold) v = fmaf(-mu, s_cs[c * 32 + j], v);
             z[j] = j < nlim ? v : -INFINITY;
-            const bool up = z[j] > best;  // strict: ties keep the lowest id
-            best = up ? z[j] : best;
-            best_i = up ? uint32_t(n0 + c * 32 + j) : best_i;
+        }
+        // chunk maximum by a tree (fmaxf drops NaN, as '>' never takes
+        // one), then the first column reaching it: the same result as the
+        // sequential strict '>' scan, without its 32-long dependency chain
+        float m[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) m[j] = fmaxf(z[j], z[j + 16]);
+#pragma unroll
+        for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+            for (int j = 0; j < w; ++j) m[j] = fmaxf(m[j], m[j + w]);
+        if (m[0] > best) {  // strict: ties keep the lowest id
+            uint32_t eq = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) eq |= (z[j] == m[0] ? 1u : 0u) << j;
+            best = m[0];
+            best_i = uint32_t(n0 + c * 32 + __ffs(eq) - 1);
         }
         if (logits_row && valid) {
 #pragma unroll
@@ -338,18 +416,23 @@ __device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tme
                 if (j < nlim) logits_row[c * 32 + j] = z[j] * rs;
         }
         if (emit) {
-            // candidates are rare after the first chunks: a warp vote
-            // skips the store path unless some lane has one
+            // candidates (rare after the first chunks): a bit mask of the
+            // columns within 2 E_row of the running max, built only when
+            // the chunk maximum itself is within it for some lane of the warp
             const float thr = best - eb2;
+            if (__any_sync(0xffffffffu, valid && m[0] >= thr)) {
+                uint32_t pass = 0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const bool pass = valid && z[j] >= thr;
-                if (__any_sync(0xffffffffu, pass)) {
-                    if (pass && n_st < kStash) {
-                        st_z[n_st * 128 + me] = z[j];
-                        st_n[n_st * 128 + me] = uint8_t(c * 32 + j);
+                for (int j = 0; j < 32; ++j) pass |= (valid && z[j] >= thr ? 1u : 0u) << j;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (pass & (1u << j)) {
+                        if (n_st < kStash) {
+                            st_z[n_st * nthr + me] = z[j];
+                            st_n[n_st * nthr + me] = uint8_t(c * 32 + j);
+                        }
+                        ++n_st;
                     }
-                    n_st += pass ? 1 : 0;
                 }
             }
         }
@@ -358,25 +441,41 @@ __device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tme
     if (valid) atomicMax(&sa.best[grow], order_key(best, best_i));
     if (emit && valid) {
         const float thr = best - eb2;
-        const size_t slot0 = (size_t(grow) * sa.n_tiles + blockIdx.y) * kPerTile;
+        const size_t slot0 = (size_t(grow) * sa.n_tiles + ntile) * kPerTile;
         int cnt = 0;
         if (n_st > kStash) {
             cnt = kPerTile + 1;  // stash overflow: refine scores the whole row
         } else {
             for (int i = 0; i < n_st; ++i) {
-                const float z = st_z[i * 128 + me];
+                const float z = st_z[i * nthr + me];
                 if (z >= thr) {
                     if (cnt < kPerTile) {
-                        sa.cand_n[slot0 + cnt] = n0 + st_n[i * 128 + me];
+                        sa.cand_n[slot0 + cnt] = n0 + st_n[i * nthr + me];
                         sa.cand_z[slot0 + cnt] = z;
                     }
                     ++cnt;
                 }
             }
         }
-        sa.cand_cnt[size_t(grow) * sa.n_tiles + blockIdx.y] = cnt;
+        sa.cand_cnt[size_t(grow) * sa.n_tiles + ntile] = cnt;
     }
     if (tr) tr[4] = gtimer();
+}
+
+// Epilogue of the one-tile-per-CTA kernels: colsum slice fetched while the
+// MMAs run (columns past the vocabulary — a partial last tile, TMA
+// zero-filled — are skipped by the scan), then the scan of the accumulator.
+__device__ __forceinline__ void score_epilogue(const ScoreArgs& sa, uint32_t tmem, uint64_t* acc_full,
+                                               uint32_t* tmem_slot, int m0, int n0, int TN,
+                                               unsigned long long* tr) {
+    float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of this tile
+    const int ncols = min(TN, sa.vocab - n0);
+    for (int i = threadIdx.x; i < ncols; i += 128) s_cs[i] = sa.colsum[n0 + i];
+    named_bar_sync(1, 128);
+    mbar_wait(acc_full, 0);
+    if (tr) tr[2] = gtimer();
+    umma::fence_after_sync();
+    score_scan(sa, tmem, s_cs, m0, n0, blockIdx.y, TN, 0, TN / 32, 128, nullptr, 0, 0, nullptr, nullptr, tr);
 }
 
 __global__ void __launch_bounds__(kScoreThreads, 1)
@@ -555,6 +654,226 @@ __global__ void __launch_bounds__(kScoreThreads, 1)
     if (tr) tr[5] = gtimer();
 }
 
+// Stream-K form of the score GEMM. A tcgen05 MMA costs ~176 SM cycles
+// whatever its N (32 ... 256) or M (64 / 128) when it accumulates into the
+// same TMEM tile as the previous one (tools/gemm_probe.cu, measured), so a
+// tile's K loop is a chain of K / 16 such steps and only the number of
+// chained steps per SM sets the GEMM time: tiles are 128 x 256 (the most
+// work per step) and the flattened (tile, k-block) space is cut into
+// gridDim.x (= SMs) equal ranges, ~35 k-blocks per CTA at config 3 k = 8
+// instead of 64 per one-tile CTA. A range covers the tail of one tile and /
+// or the head of the next: the CTA holding a tile's last k-block owns it
+// (scores it); a CTA whose range ends inside a tile publishes that fp32
+// partial tile to its own workspace slot and raises its flag, and it does
+// that segment first so the owner rarely waits. TMEM holds two 256-column
+// accumulators so a segment's epilogue overlaps the next segment's MMAs.
+// The epilogue is 8 warps (two per TMEM lane quarter, 4 chunks each: the
+// scan is latency-bound per warp) and its candidates are kept per 128-column
+// half tile.
+__device__ __forceinline__ long long sk_begin(int c, int G, long long total) { return total * c / G; }
+__device__ __forceinline__ int sk_cta_of(long long x, int G, long long total) {
+    int c = int(x * G / total);
+    while (c + 1 < G && sk_begin(c + 1, G, total) <= x) ++c;
+    while (c > 0 && sk_begin(c, G, total) > x) --c;
+    return c;
+}
+struct SkSeg {
+    int tile, k0, k1;
+    bool owner;
+};
+// Segment p (processing order) of CTA c: the trailing partial segment, if
+// any, first, then the rest in k order.
+__device__ __forceinline__ SkSeg sk_segment(int p, long long b, long long e, int nkt) {
+    const long long t0 = b / nkt;
+    const int nseg = int((e - 1) / nkt - t0 + 1);
+    const bool tail_first = nseg > 1 && (e - ((e - 1) / nkt) * nkt) < nkt;
+    const int j = tail_first ? (p == 0 ? nseg - 1 : p - 1) : p;
+    SkSeg sg;
+    sg.tile = int(t0) + j;
+    const long long ts = (long long)sg.tile * nkt;
+    sg.k0 = j == 0 ? int(b - ts) : 0;
+    sg.k1 = int(min((long long)nkt, e - ts));
+    sg.owner = sg.k1 == nkt;
+    return sg;
+}
+__device__ __forceinline__ int sk_num_segments(long long b, long long e, int nkt) {
+    return b >= e ? 0 : int((e - 1) / nkt - b / nkt + 1);
+}
+
+__global__ void __launch_bounds__(kSkThreads, 1)
+    score_argmax_streamk_kernel(const ScoreArgs sa, const __grid_constant__ CUtensorMap tmap_a,
+                                const __grid_constant__ CUtensorMap tmap_w) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr int TN = kTNMax;
+    const int NS = sa.stages, kStage = score_stage_bytes(TN);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * kStage);
+    uint64_t* empty = full + kStagesMax;
+    uint64_t* acc_full = empty + kStagesMax;  // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2]
+    uint64_t* pbar = acc_empty + 2;           // [kTNMax / 32] staged partial chunks
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + kTNMax / 32);
+    float* s_cs = reinterpret_cast<float*>(tmem_slot + 4);  // [kTNMax] colsum of the tile being scored
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x, c = blockIdx.x;
+    const long long total = (long long)sa.tiles_m * sa.n_vt * sa.nkt;
+    const long long b = sk_begin(c, G, total), e = sk_begin(c + 1, G, total);
+    const int nseg = sk_num_segments(b, e, sa.nkt);
+    unsigned long long* trc = sa.trace && c < 512 ? sa.trace + 8 * c : nullptr;
+    unsigned long long* tr = threadIdx.x == 0 ? trc : nullptr;
+    if (tr) {
+        tr[0] = gtimer();
+        tr[7] = 0ull;
+    }
+    const int nkw = sa.width / kTK;  // k-blocks of W per pass
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], kSkEpiThreads);
+        }
+        for (int i = 0; i < kTNMax / 32; ++i) mbar_init(&pbar[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == kSkWarpMma) umma::tmem_alloc(tmem_slot, 2 * TN);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // A (row stats output) is complete
+
+    if (warp == kSkWarpTma) {
+        if (lane == 0) {
+            umma::tma_prefetch_desc(&tmap_a);
+            umma::tma_prefetch_desc(&tmap_w);
+            const uint64_t pol = l2_policy_evict_last();
+            const uint32_t bytes = uint32_t(kStage);
+            int kc = 0;
+            for (int p = 0; p < nseg; ++p) {
+                const SkSeg sg = sk_segment(p, b, e, sa.nkt);
+                const int m0 = (sg.tile % sa.tiles_m) * kTM, n0 = (sg.tile / sa.tiles_m) * TN;
+                for (int k = sg.k0; k < sg.k1; ++k, ++kc) {
+                    const int s = kc % NS;
+                    mbar_wait(&empty[s], ((kc / NS) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], bytes);
+                    uint8_t* dst = smem + s * kStage;
+                    umma::tma_load_2d(dst, &tmap_a, k * kTK, m0, &full[s], pol);
+                    umma::tma_load_2d(dst + kABytes, &tmap_w, (k % nkw) * kTK, n0, &full[s], pol);
+                }
+            }
+        }
+    } else if (warp == kSkWarpMma) {
+        if (lane == 0) {
+            const uint32_t base = smem_u32(smem);
+            int kc = 0;
+            for (int p = 0; p < nseg; ++p) {
+                const SkSeg sg = sk_segment(p, b, e, sa.nkt);
+                const int slot = p & 1;
+                if (p >= 2) mbar_wait(&acc_empty[slot], ((p >> 1) - 1) & 1);  // scanned / published
+                umma::fence_after_sync();
+                const uint32_t d = tmem + uint32_t(slot * TN);
+                for (int k = sg.k0; k < sg.k1; ++k, ++kc) {
+                    const int s = kc % NS;
+                    mbar_wait(&full[s], (kc / NS) & 1);
+                    if (kc == 0 && trc) trc[1] = gtimer();
+                    umma::fence_after_sync();
+                    const uint32_t a_addr = base + s * kStage, b_addr = a_addr + kABytes;
+#pragma unroll
+                    for (int kk = 0; kk < kTK / 16; ++kk) {
+                        const uint64_t ad = umma::smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+                        const uint64_t bd = umma::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        umma::mma_bf16_ss(d, ad, bd, sa.idesc, (k > sg.k0 || kk) ? 1u : 0u);
+                    }
+                    umma::mma_commit(&empty[s]);
+                }
+                umma::mma_commit(&acc_full[slot]);
+            }
+        }
+    } else {
+        const int row = (warp & 3) * 32 + lane;
+        const uint32_t trow = uint32_t((warp & 3) * 32) << 16;
+        const int half = warp >> 2;  // this warp's chunks: [4 half, 4 half + 4)
+        constexpr int kHalfCh = TN / 64;
+        for (int p = 0; p < nseg; ++p) {
+            const SkSeg sg = sk_segment(p, b, e, sa.nkt);
+            const int slot = p & 1;
+            const int m0 = (sg.tile % sa.tiles_m) * kTM, n0 = (sg.tile / sa.tiles_m) * TN;
+            const uint32_t acc = tmem + uint32_t(slot * TN);
+            if (sg.owner) {
+                // the other CTAs covering this tile: [cp0, c), each with its
+                // trailing partial segment on this tile
+                const int cp0 = sg.k0 > 0 ? sk_cta_of((long long)sg.tile * sa.nkt, G, total) : c;
+                named_bar_sync(1, kSkEpiThreads);  // the previous scan is done with s_cs
+                const int ncols = min(TN, sa.vocab - n0);
+                for (int i = threadIdx.x; i < ncols; i += kSkEpiThreads) s_cs[i] = sa.colsum[n0 + i];
+                if (threadIdx.x == 0)
+                    for (int q = cp0; q < c; ++q)
+                        while (ld_acquire_gpu(&sa.sk_flags[q]) == 0u) {
+                        }
+                named_bar_sync(1, kSkEpiThreads);
+                mbar_wait(&acc_full[slot], (p >> 1) & 1);
+                if (tr && p == nseg - 1) tr[2] = gtimer();
+                umma::fence_after_sync();
+                // the CTA's last segment: the MMAs are done with the operand
+                // ring, so the first partial tile streams into it by bulk
+                // copies (one per 32-column chunk) while the scan starts
+                const bool staged = c > cp0 && p == nseg - 1;
+                if (staged && threadIdx.x == 0) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired partial -> async proxy
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(sa.sk_ws) +
+                                         size_t(cp0) * (TN / 32) * 8 * 128 * sizeof(float4);
+                    for (int ch = 0; ch < TN / 32; ++ch) {
+                        mbar_arrive_expect_tx(&pbar[ch], 8 * 128 * sizeof(float4));
+                        bulk_g2s(smem + ch * 8 * 128 * sizeof(float4), src + ch * 8 * 128 * sizeof(float4),
+                                 8 * 128 * sizeof(float4), &pbar[ch]);
+                    }
+                }
+                score_scan(sa, acc, s_cs, m0, n0, (sg.tile / sa.tiles_m) * 2 + half, TN, half * kHalfCh,
+                           half * kHalfCh + kHalfCh, kSkEpiThreads, sa.sk_ws, cp0, c - cp0,
+                           staged ? reinterpret_cast<const float4*>(smem) : nullptr, pbar,
+                           p == nseg - 1 ? tr : nullptr);
+                named_bar_sync(1, kSkEpiThreads);
+                if (threadIdx.x == 0)
+                    for (int q = cp0; q < c; ++q) sa.sk_flags[q] = 0u;  // consumed: clear for the next launch
+            } else {
+                // publish the partial tile: [chunk][j4][row] float4, so each
+                // store instruction of a warp writes 512 contiguous bytes
+                mbar_wait(&acc_full[slot], (p >> 1) & 1);
+                umma::fence_after_sync();
+                float4* dst = reinterpret_cast<float4*>(sa.sk_ws) + size_t(c) * (TN / 32) * 8 * 128 + row;
+#pragma unroll 1
+                for (int ch = half * kHalfCh; ch < half * kHalfCh + kHalfCh; ++ch) {
+                    uint32_t r[32];
+                    umma::tmem_ld32(acc + trow + ch * 32, r);
+                    umma::tmem_wait_ld();
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4)
+                        __stcg(dst + (size_t(ch) * 8 + j4) * 128,
+                               make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
+                                           __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])));
+                }
+                __threadfence();
+                named_bar_sync(1, kSkEpiThreads);
+                if (threadIdx.x == 0) st_release_gpu(&sa.sk_flags[c], 1u);
+            }
+            umma::fence_before_sync();
+            mbar_arrive(&acc_empty[slot]);
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    if (warp == kSkWarpMma) {
+        umma::fence_after_sync();
+        umma::tmem_dealloc(tmem, 2 * TN);
+    }
+    if (tr) tr[5] = gtimer();
+}
+
 __device__ __forceinline__ float key_value(unsigned long long k) {
     uint32_t b = uint32_t(k >> 32);
     b = (b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b;
@@ -720,19 +1039,28 @@ cudaError_t launch_colsum(const void* wt, int width, int vocab, float* colsum, f
     return cudaGetLastError();
 }
 
-bool score_pairs() {
-    static const bool one_sm = [] {
-        const char* e = std::getenv("EP_K4_1SM");
-        return e && e[0] == '1';
+// GEMM form: stream-K 128 x 256 tiles over one CTA per SM (default),
+// EP_K4_PAIR=1 CTA-pair tiles (cta_group::2, 256 rows), EP_K4_1SM=1 one
+// 128 x tn tile per CTA.
+int score_mode() {
+    static const int mode = [] {
+        const char* p = std::getenv("EP_K4_PAIR");
+        const char* o = std::getenv("EP_K4_1SM");
+        if (o && o[0] == '1') return kScoreOneSm;
+        if (p && p[0] == '1') return kScorePair;
+        return kScoreStreamK;
     }();
-    return !one_sm;
+    return mode;
 }
 
-// Tile width for one wave: 1-SM tiles of 128 rows over n_sms CTAs, or (the
-// default) CTA-pair tiles of 256 rows over n_sms / 2 pairs; a multiple of 32
-// (epilogue chunks; for pairs also the per-CTA half of 16-row TMA boxes).
+// Tile width: 256 for stream-K; for the one-tile-per-CTA forms the width
+// giving one wave (1-SM tiles of 128 rows over n_sms CTAs or CTA-pair tiles
+// of 256 rows over n_sms / 2 pairs), a multiple of 32 (epilogue chunks; for
+// pairs also the per-CTA half of 16-row TMA boxes).
 int score_tile_n(int rows, int vocab, int n_sms) {
-    const bool pairs = score_pairs();
+    const int mode = score_mode();
+    if (mode == kScoreStreamK) return kTNMax;
+    const bool pairs = mode == kScorePair;
     const int m_tiles = pairs ? (rows + 2 * kTM - 1) / (2 * kTM) : (rows + kTM - 1) / kTM;
     const int slots = pairs ? n_sms / 2 : n_sms;
     const int n_max = slots / m_tiles > 0 ? slots / m_tiles : 1;
@@ -741,7 +1069,15 @@ int score_tile_n(int rows, int vocab, int n_sms) {
     return tn < 32 ? 32 : tn > kTNMax ? kTNMax : tn;
 }
 
-int score_w_box_rows(int tn) { return score_pairs() ? tn / 2 : tn; }
+int score_w_box_rows(int tn) { return score_mode() == kScorePair ? tn / 2 : tn; }
+
+// Candidate tiles of the refinement (per row): one per vocab tile, or per
+// 128-column half tile for stream-K (two epilogue warps per tile).
+int score_cand_tiles(int vocab, int tn) {
+    return score_mode() == kScoreStreamK ? (vocab + 127) / 128 : (vocab + tn - 1) / tn;
+}
+
+size_t score_streamk_ws_bytes(int n_sms) { return size_t(n_sms) * kTNMax * kTM * sizeof(float); }
 
 cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const void* attn_out, void* split,
                                 const CUtensorMap& tmap_a, const CUtensorMap& tmap_w,
@@ -772,12 +1108,25 @@ cudaError_t launch_score_accept(int rows, int width, int vocab, int tn, const vo
         return b;
     }();
     // fp32 rows: the GEMM on the bf16 hi part only, then the exact refinement
-    const int n_tiles = (vocab + tn - 1) / tn;
+    const int n_tiles = score_cand_tiles(vocab, tn);
     ScoreArgs sa{rows, width, vocab, 1, mean, rstd, colsum, best, split ? nullptr : logits, trace,
                  split ? rf.ebound : nullptr, split ? rf.cand_cnt : nullptr, split ? rf.cand_n : nullptr,
                  split ? rf.cand_z : nullptr, n_tiles, tn, score_stages(tn),
                  umma::idesc_bf16_f32(kTM, tn, false, false)};
-    if (score_pairs()) {
+    const int mode = score_mode();
+    if (mode == kScoreStreamK) {
+        sa.tiles_m = (rows + kTM - 1) / kTM;
+        sa.nkt = width / kTK;
+        sa.n_vt = (vocab + kTNMax - 1) / kTNMax;
+        sa.sk_ws = rf.sk_ws;
+        sa.sk_flags = rf.sk_flags;
+        sa.stages = std::min(kStagesMax, (227 * 1024 - kSkSmemFixed) / score_stage_bytes(kTNMax));
+        const long long total = (long long)sa.tiles_m * sa.n_vt * sa.nkt;
+        const int grid = int(std::min<long long>(total, rf.sk_ctas));
+        const int smem = sa.stages * score_stage_bytes(kTNMax) + kSkSmemFixed;
+        if (cudaError_t e2 = ensure_smem<score_argmax_streamk_kernel>(227 * 1024)) return e2;
+        e = launch_pdl(score_argmax_streamk_kernel, dim3(grid), dim3(kSkThreads), smem, s, sa, tmap_a, tmap_w);
+    } else if (mode == kScorePair) {
         // CTA pairs: stage = A 16 KB + half of the W rows
         const int stage = kABytes + (tn / 2) * kTK * 2;
         sa.stages = std::min(kStagesMax, kScoreSmemBudget / stage);
