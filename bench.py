@@ -54,6 +54,19 @@ WORKLOAD = ("cfg2: 7B-shaped spliced decode, Hq=32 Hkv=8 d=128 bf16, 4096 cloud 
 SKV_B, SKV_CLOUD, SKV_EDGE = 32, 131072, 512
 
 
+
+def cpu_model():
+    """Host CPU model name (the CPU baseline names its cores)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
 def skv_workload(world):
     return (f"cfg4: long-context split-KV, Hq=32 Hkv=8 d=128 bf16, {SKV_CLOUD} cloud + {SKV_EDGE} "
             f"edge KV per request (private pages), batch {SKV_B}, n_q=1, cloud KV in {world} "
@@ -198,7 +211,7 @@ def run_reference_skv(args, world):
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": skv_workload(world), "sample_requests_per_step": 1},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "cpu_model": cpu_model(), "kind": "reference",
                          "sample": f"1 of {SKV_B} requests x 32 heads per step ({SKV_CLOUD + SKV_EDGE} keys), "
                                    "reference attention block (partial_attention per segment + merge) "
                                    "in fp64 from oracle/_ref"},
@@ -235,7 +248,7 @@ def run_reference(args):
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample_requests_per_step": n_req},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "cpu_model": cpu_model(),
                          "kind": "reference",
                          "sample": f"{n_req} of 32 requests x 32 heads per step (all segments), "
                                    "reference attention block (partial_attention per segment + "
@@ -525,7 +538,7 @@ def main():
                             q[:n_req].view(torch.int16).cpu().numpy().view(np.uint16))
         rate, secs, units = cpu_reference_rate(sb, threads)
         line["cpu_baseline"] = {
-            "value": rate, "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "value": rate, "unit": "tokens/s", "cores": threads, "cpu_model": cpu_model(), "kind": "reference",
             "sample": f"requests 0-3 of the same workload (128 (request, head) units per pass, "
                       f"{units} units in {secs:.1f} s), reference attention block in fp64 "
                       "(oracle/_ref, unmodified reference sources)"}
@@ -768,6 +781,14 @@ def run_extras(args, world, rank, h):
         extras["model_cfg1"] = model_bench.run(64, 5, h, batch=64, cpu=not args.no_cpu_baseline)
         gc.collect()
         torch.cuda.empty_cache()
+        # the link-level drop-in (reference model code + attention_dropin.cpp)
+        # beside the same code on its own attention.cpp (config 1, 64 tokens)
+        if not args.no_cpu_baseline:
+            import dropin_bench
+            try:
+                extras["dropin_cfg1"] = dropin_bench.run(64, 2)
+            except Exception as e:  # oracle/_ref not shipped: report, do not fail the bench
+                extras["dropin_cfg1"] = {"unavailable": str(e)[:200]}
     skv = {}
     for b in (1, 32):
         skv[f"batch{b}"] = splitkv_bench.run(b, steps, 3, combine="peer")

@@ -141,6 +141,7 @@ int ep_destroy(ep_handle h) {
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->hdr_pinned) cudaFreeHost(h->hdr_pinned);
+    if (h->pin) cudaFreeHost(h->pin);
     if (h->ingest_status) cudaFreeHost(h->ingest_status);
     if (h->ingest_done) {
         cudaEventSynchronize(h->ingest_done);
@@ -160,6 +161,20 @@ int check_head(size_t d, const char* where) {
     if (d == 0) return fail(EP_EINVAL, std::string(where) + ": zero head width");
     if (d > 256) return fail(EP_EUNSUPPORTED, std::string(where) + ": head width > 256");
     return EP_OK;
+}
+
+// Pinned staging area of the synchronous host-buffer calls: the inputs are
+// packed into it and cross PCIe in one copy each way (pageable sources
+// would cost the driver a staging copy per argument).
+cudaError_t reserve_pin(ep_context* h, size_t n) {
+    if (n <= h->pin_bytes) return cudaSuccess;
+    if (h->pin) cudaFreeHost(h->pin);
+    h->pin = nullptr;
+    h->pin_bytes = 0;
+    const size_t cap = std::max(n, size_t(1) << 20);
+    cudaError_t e = cudaMallocHost(&h->pin, cap);
+    if (e == cudaSuccess) h->pin_bytes = cap;
+    return e;
 }
 
 size_t visible(size_t q_off, size_t k_off, size_t n_keys, size_t i) {
@@ -186,18 +201,24 @@ int ep_partial_attention_f64(ep_handle h, const double* q, size_t n_q, const dou
     double* dout = dv + nk;
     double* dlse = dout + nq;
     cudaStream_t s = h->stream;
-    EP_CUDA_TRY(cudaMemcpyAsync(dq, q, nq * sizeof(double), cudaMemcpyHostToDevice, s), "H2D q");
+    // q | k | v packed in pinned memory -> one H2D; out | lse (adjacent on
+    // the device) -> one D2H
+    EP_CUDA_TRY(reserve_pin(h, total), "partial_attention pinned staging");
+    double* hp = static_cast<double*>(h->pin);
+    std::memcpy(hp, q, nq * sizeof(double));
     if (nk) {
-        EP_CUDA_TRY(cudaMemcpyAsync(dk, k, nk * sizeof(double), cudaMemcpyHostToDevice, s), "H2D k");
-        EP_CUDA_TRY(cudaMemcpyAsync(dv, v, nk * sizeof(double), cudaMemcpyHostToDevice, s), "H2D v");
+        std::memcpy(hp + nq, k, nk * sizeof(double));
+        std::memcpy(hp + nq + nk, v, nk * sizeof(double));
     }
+    EP_CUDA_TRY(cudaMemcpyAsync(dq, hp, (nq + 2 * nk) * sizeof(double), cudaMemcpyHostToDevice, s), "H2D q|k|v");
     EP_CUDA_TRY(launch_partial_generic(EP_F64, dq, d, n_q, dk, d, dv, d, n_keys, d, query_offset,
                                        key_offset, dout, d, dlse, s),
                 "partial_attention launch");
     h->launches++;
-    EP_CUDA_TRY(cudaMemcpyAsync(out, dout, nq * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H out");
-    EP_CUDA_TRY(cudaMemcpyAsync(lse, dlse, n_q * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H lse");
+    EP_CUDA_TRY(cudaMemcpyAsync(hp, dout, (nq + n_q) * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H out|lse");
     EP_CUDA_TRY(cudaStreamSynchronize(s), "partial_attention sync");
+    std::memcpy(out, hp, nq * sizeof(double));
+    std::memcpy(lse, hp + nq, n_q * sizeof(double));
     return EP_OK;
 }
 
@@ -230,16 +251,23 @@ int ep_merge_partials_f64(ep_handle h, size_t n_parts, const double* const* outs
     double* d_out = d_lses + n_parts * n_q;
     double* d_lse = d_out + per;
     cudaStream_t s = h->stream;
+    // every partial (outs, then lses) packed in pinned memory -> one H2D;
+    // out | lse (adjacent on the device) -> one D2H
+    EP_CUDA_TRY(reserve_pin(h, total), "merge_partials pinned staging");
+    double* hp = static_cast<double*>(h->pin);
     for (size_t p = 0; p < n_parts; ++p) {
-        EP_CUDA_TRY(cudaMemcpyAsync(d_outs + p * per, outs[p], per * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-        EP_CUDA_TRY(cudaMemcpyAsync(d_lses + p * n_q, lses[p], n_q * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+        std::memcpy(hp + p * per, outs[p], per * sizeof(double));
+        std::memcpy(hp + n_parts * per + p * n_q, lses[p], n_q * sizeof(double));
     }
+    EP_CUDA_TRY(cudaMemcpyAsync(d_outs, hp, n_parts * (per + n_q) * sizeof(double), cudaMemcpyHostToDevice, s),
+                "H2D partials");
     EP_CUDA_TRY(launch_merge_generic(EP_F64, n_parts, d_outs, d_lses, n_q, d, d_out, d_lse, s),
                 "merge_partials launch");
     h->launches++;
-    EP_CUDA_TRY(cudaMemcpyAsync(out, d_out, per * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-    EP_CUDA_TRY(cudaMemcpyAsync(lse, d_lse, n_q * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    EP_CUDA_TRY(cudaMemcpyAsync(hp, d_out, (per + n_q) * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H out|lse");
     EP_CUDA_TRY(cudaStreamSynchronize(s), "merge_partials sync");
+    std::memcpy(out, hp, per * sizeof(double));
+    std::memcpy(lse, hp + per, n_q * sizeof(double));
     return EP_OK;
 }
 

@@ -40,6 +40,8 @@ struct ep_context {
     int n_sms = 0;
     cudaStream_t stream = nullptr;  // used by the synchronous host-buffer entry points
     ep::DeviceBuffer scratch;       // staging for host-buffer calls
+    void* pin = nullptr;            // pinned host staging of the host-buffer calls (one H2D + one D2H each)
+    size_t pin_bytes = 0;
     ep::DeviceBuffer zero_rows;     // 64 zero rows of the widest KV row (page-tail fill)
     ep::DeviceBuffer ingest_stage;  // pageable / misaligned kv frames staged for ep_kv_ingest_frame
     cudaEvent_t ingest_done = nullptr;  // recorded after each launch that reads ingest_stage
