@@ -280,3 +280,33 @@ def test_score_large_vocab_candidate_path(cuda_handle, V):
                     torch.zeros((B, n_q - 1), dtype=torch.int32, device="cuda"))
     want = _oracle_argmax(x.astype(np.float64), O.bf16_to_f64(W))
     assert np.array_equal(tgt.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("B,n_q,width,V", [
+    (64, 9, 1024, 4096),   # 5 x 16 tiles of 16 k-blocks over 148 CTAs: tiles span 2-3 CTAs (1-2 partials)
+    (7, 3, 2048, 1024),    # 1 M tile x 4 vocab tiles x 32 k-blocks: 128 k-blocks < 148 CTAs (one per CTA)
+    (1, 1, 64, 256),       # a single k-block: one CTA, no partials
+    (43, 5, 4096, 8192),   # 2 M tiles x 32 vocab tiles: partial last M tile, ~28 k-blocks per CTA
+])
+def test_score_streamk_partition_shapes(cuda_handle, B, n_q, width, V):
+    """K4's stream-K GEMM (score_argmax_streamk_kernel): ranges of the flattened
+    (tile, k-block) space that start / end inside tiles, tiles covered by 1-3
+    CTAs (owner + published partial tiles), fewer k-blocks than SMs, a single
+    k-block; target ids equal the fp64 argmax_token(LN(x) @ W)
+    (model.cpp:238-255)."""
+    import torch
+    from paper_2504_11729_b200.verify import VerifyGreedy
+    from tests.gpu_util import torch_from_raw
+    rng = np.random.default_rng(B * 7919 + width + V)
+    W = O.fill_uniform(O.DT_BF16, width * V, 1234).reshape(width, V)
+    x = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32)
+    ver = VerifyGreedy(torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16), handle=cuda_handle)
+    drafts = torch.zeros((B, max(n_q - 1, 0)), dtype=torch.int32, device="cuda")
+    tgt, _, _ = ver(torch.from_numpy(x).cuda().view(B, n_q, width), drafts)
+    want = _oracle_argmax(x.astype(np.float64), O.bf16_to_f64(W))
+    assert np.array_equal(tgt.cpu().numpy(), want)
+    # a second launch on the same verifier: the partial-tile flags were
+    # cleared by their consumers, so the owners wait for fresh partials
+    x2 = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32)
+    tgt2, _, _ = ver(torch.from_numpy(x2).cuda().view(B, n_q, width), drafts)
+    assert np.array_equal(tgt2.cpu().numpy(), _oracle_argmax(x2.astype(np.float64), O.bf16_to_f64(W)))
