@@ -460,14 +460,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 64; ++j)
                         if (!(j < nv && pos + j <= my_qpos)) sr[j] = __float_as_uint(-INFINITY);
                 }
-                // row max as a tree (8 independent chains, then 3 levels)
+                // row max: 8 independent chains of 3-input maxima (FMNMX3),
+                // then a 3-input tree
                 float mx[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) mx[c] = __uint_as_float(sr[c]);
 #pragma unroll
-                for (int j = 8; j < 64; ++j) mx[j & 7] = fmaxf(mx[j & 7], __uint_as_float(sr[j]));
-                const float hmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                         fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                for (int j = 8; j < 64; j += 16)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        mx[c] = fmax3(mx[c], __uint_as_float(sr[j + c]),
+                                      j + 8 + c < 64 ? __uint_as_float(sr[j + 8 + c]) : -INFINITY);
+                const float hmax = fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7]));
                 const float bmax = valid_row ? hmax * scale : -INFINITY;
                 // lazy max: move it only when the block exceeds it by > 2^kLazy
                 float corr = 1.f;
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             make_uint4(0, 0, 0, 0);
                     }
                 }
-                umma::fence_proxy_async_smem();
+                if (nv < kBT) umma::fence_proxy_async_smem();  // the zeroed V rows -> the MMA's proxy
                 umma::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&B.p_full[grp]);
