@@ -255,6 +255,11 @@ __global__ void kv_append_kernel(int row_bytes, int n_kv_heads, int page_tokens,
                                  const uint8_t* __restrict__ k_new, const uint8_t* __restrict__ v_new,
                                  uint8_t* __restrict__ k_pages, uint8_t* __restrict__ v_pages, int64_t num_pages) {
     const int i = blockIdx.x;
+    // PDL: let the next kernel (the attention) start its prologue now; the
+    // rows are written only after the predecessor (plan patch / previous
+    // step) has completed
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     EP_DCHECK(num_pages < 0 || (dst_page[i] >= 0 && dst_page[i] < num_pages));
     EP_DCHECK(dst_slot[i] >= 0 && dst_slot[i] < page_tokens);
     const size_t page = size_t(dst_page[i]), slot = size_t(dst_slot[i]);
@@ -271,6 +276,10 @@ __global__ void kv_append_kernel(int row_bytes, int n_kv_heads, int page_tokens,
 }  // namespace
 
 __global__ void plan_patch_kernel(const PlanPatch pp) {
+    // PDL: the descriptors change only after the previous attention (which
+    // reads them) has completed; the next kernel may be scheduled meanwhile
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int i = threadIdx.x; i < pp.n; i += blockDim.x) {
         pp.pdesc[pp.idx[i]].n_tok = pp.ntok[i];
         pp.q_pos[pp.req[i]] = pp.qpos[i];
@@ -279,8 +288,7 @@ __global__ void plan_patch_kernel(const PlanPatch pp) {
 
 cudaError_t launch_plan_patch(const PlanPatch& pp, cudaStream_t s) {
     if (pp.n <= 0) return cudaSuccess;
-    plan_patch_kernel<<<1, 128, 0, s>>>(pp);
-    return cudaGetLastError();
+    return launch_with_pdl(plan_patch_kernel, dim3(1), dim3(128), 0, s, pp);
 }
 
 cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int n_rows,
@@ -288,12 +296,10 @@ cudaError_t launch_kv_append(int row_bytes, int n_kv_heads, int page_tokens, int
                              const void* v_new, void* k_pages, void* v_pages, cudaStream_t s,
                              int64_t num_pages) {
     if (n_rows <= 0) return cudaSuccess;
-    kv_append_kernel<<<n_rows, 128, 0, s>>>(row_bytes, n_kv_heads, page_tokens, dst_page, dst_slot,
-                                            static_cast<const uint8_t*>(k_new),
-                                            static_cast<const uint8_t*>(v_new),
-                                            static_cast<uint8_t*>(k_pages),
-                                            static_cast<uint8_t*>(v_pages), num_pages);
-    return cudaGetLastError();
+    return launch_with_pdl(kv_append_kernel, dim3(n_rows), dim3(128), 0, s, row_bytes, n_kv_heads, page_tokens,
+                           dst_page, dst_slot, static_cast<const uint8_t*>(k_new),
+                           static_cast<const uint8_t*>(v_new), static_cast<uint8_t*>(k_pages),
+                           static_cast<uint8_t*>(v_pages), num_pages);
 }
 
 }  // namespace ep
