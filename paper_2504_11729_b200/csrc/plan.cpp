@@ -95,6 +95,14 @@ int64_t tc_item_weight(int rows) {
 // sweeping 0/1/2/4 blocks on config 2 gave 101.7 / 102.0 / 102.1 / 103.6 us
 // (config 5 flat at 0.265 ms). (Before the epilogue warp the 8-warp item end
 // stalled the ring and 4 was best: cfg5 0.321 -> 0.296 ms.)
+// K1 tail penalty in blocks (see build_subplan)
+int64_t k1_tail_pen() {
+    static const int64_t w = [] {
+        const char* e = std::getenv("EP_K1_TAIL_PEN");
+        return e ? std::atoll(e) : int64_t(5);  // config 2 sweep 0/3/5/8: 100.4 / 99.0 / 97.8 / 98.7 us
+    }();
+    return w;
+}
 int64_t k1_item_weight() {
     static const int64_t w = [] {
         const char* e = std::getenv("EP_K1_ITEM_WEIGHT");
@@ -130,8 +138,14 @@ struct SubPlan {
 // 64-token-block units, so CTAs that get many short units (prefill chunks near
 // the start of a prompt) are not overloaded. Measured for K3 (clock64 item
 // trace): ~12-13K cycles per item vs ~1.0-1.4K per block -> 10.
+//
+// tail_pen (K1): a CTA whose items are all pieces of split units ends with
+// one of them, and that final item end (partial store, arrival and usually
+// the unit's merge) is not overlapped by streaming (~4 us vs ~1 us for a
+// whole unit's store, per-CTA trace on config 2); such CTAs get tail_pen
+// fewer blocks and the others share them (one re-cut).
 void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t cap_ctas,
-                   int64_t item_weight = 0) {
+                   int64_t item_weight = 0, int64_t tail_pen = 0) {
     sp.pdesc.clear();
     sp.req_page_off.assign(vr.size() + 1, 0);
     std::vector<int64_t> blocks(vr.size(), 0);
@@ -150,12 +164,37 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
         total_blocks += x * Hkv;
     }
     sp.n_ctas = std::max<int64_t>(1, std::min<int64_t>(cap_ctas, total_blocks));
+    std::vector<int32_t> item_cta;
+    // cumulative capacity ends of the CTAs (equal shares first)
+    std::vector<int64_t> bnd(sp.n_ctas);
+    for (int64_t c = 0; c < sp.n_ctas; ++c) bnd[c] = (total * (c + 1) + sp.n_ctas - 1) / sp.n_ctas;
+    for (int pass = 0; pass < (tail_pen > 0 && sp.n_ctas > 1 ? 2 : 1); ++pass) {
+    if (pass == 1) {
+        // CTAs without a whole unit: shorter shares
+        std::vector<int> whole(sp.n_ctas, 0);
+        std::vector<int32_t> n_it(sp.n_units, 0);
+        for (const WorkItem& w : sp.items) n_it[int64_t(w.b) * Hkv + w.g]++;
+        for (size_t i = 0; i < sp.items.size(); ++i)
+            if (n_it[int64_t(sp.items[i].b) * Hkv + sp.items[i].g] == 1) whole[item_cta[i]] = 1;
+        int64_t n_flag = 0;
+        for (int64_t c = 0; c < sp.n_ctas; ++c) n_flag += whole[c] ? 0 : 1;
+        if (n_flag == 0 || n_flag == sp.n_ctas) break;
+        const double base = double(total) / double(sp.n_ctas);
+        const double lo = base - double(tail_pen);
+        const double hi = base + double(tail_pen) * double(n_flag) / double(sp.n_ctas - n_flag);
+        double run = 0.0;
+        for (int64_t c = 0; c < sp.n_ctas; ++c) {
+            run += whole[c] ? hi : lo;
+            bnd[c] = int64_t(run + 0.5);
+        }
+        bnd[sp.n_ctas - 1] = total;
+    }
     sp.items.clear();
+    item_cta.clear();
     sp.cta_item_ptr.assign(sp.n_ctas + 1, 0);
     sp.unit_item_ptr.assign(sp.n_units + 1, 0);
-    std::vector<int32_t> item_cta;
     int64_t acc = 0, cta = 0;
-    auto boundary = [&](int64_t c) { return (total * (c + 1) + sp.n_ctas - 1) / sp.n_ctas; };
+    auto boundary = [&](int64_t c) { return bnd[c]; };
     for (size_t b = 0; b < vr.size(); ++b) {
         const int64_t npg = sp.req_page_off[b + 1] - sp.req_page_off[b];
         for (int g = 0; g < Hkv; ++g) {
@@ -189,6 +228,7 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
             }
         }
     }
+    }  // passes
     sp.n_items = int64_t(sp.items.size());
     for (int32_t c : item_cta) sp.cta_item_ptr[c + 1]++;
     for (int64_t c = 0; c < sp.n_ctas; ++c) sp.cta_item_ptr[c + 1] += sp.cta_item_ptr[c];
@@ -383,7 +423,7 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         p.cascade = false;
         p.has_shared.assign(B, 0);
         p.main.tc = false;
-        build_subplan(p.main, vr, Hkv, cap, k1_item_weight());
+        build_subplan(p.main, vr, Hkv, cap, k1_item_weight(), k1_tail_pen());
         p.main.rows = pow2ceil_rows(G * C);
         return EP_OK;
     }
@@ -467,7 +507,8 @@ int build_plan_host(ep_plan_s& p, const int64_t* seg_indptr, const ep_segment* s
         }();
         if (env > 0) cap_main = env;
     }
-    build_subplan(p.main, main_vr, Hkv, cap_main, p.main.tc ? kTcItemWeight : k1_item_weight());
+    build_subplan(p.main, main_vr, Hkv, cap_main, p.main.tc ? kTcItemWeight : k1_item_weight(),
+                  p.main.tc ? 0 : k1_tail_pen());
     p.main.rows = p.main.tc ? rpr : pow2ceil_rows(rpr);
     if (p.cascade) {
         build_subplan(p.shared, shared_vr, Hkv, cap_shared, tc_item_weight(group_cap * rpr));
