@@ -58,9 +58,28 @@ def analyse(path):
     print("total span", (t[t > 0].max() - base))
 
 
+def items(path, n_show=24):
+    """Per-item phases of CTA 0 (clock64): start -> Q in TMEM -> last PV
+    done -> epilogue (O read) -> outputs stored -> end (merge)."""
+    raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
+    t = raw[:18 * NB].reshape(18, NB)
+    st, qd, lp, ep, out, end = (t[12 + i] for i in range(6))
+    n = int((st > 0).sum())
+    print(f"items traced: {n}")
+    print(" item  start->Q  Q->lastPV  lastPV->epi  epi->out  out->end  end->next start")
+    for i in range(min(n, n_show)):
+        nxt = st[i + 1] - end[i] if i + 1 < n else 0
+        print(f"{i:5d} {qd[i]-st[i]:9d} {lp[i]-qd[i]:10d} {ep[i]-lp[i]:12d} {out[i]-ep[i]:9d} {end[i]-out[i]:9d} {nxt:9d}")
+    tot = [np.median((b - a)[:n]) for a, b in ((st, qd), (qd, lp), (lp, ep), (ep, out), (out, end))]
+    print("medians:", [int(x) for x in tot])
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--analyse":
         analyse(sys.argv[2])
+        sys.exit(0)
+    if sys.argv[1] == "--items":
+        items(sys.argv[2])
         sys.exit(0)
     kind = sys.argv[1]
     if kind.startswith("verify"):
