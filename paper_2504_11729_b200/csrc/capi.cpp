@@ -83,8 +83,29 @@ int encode_bf16_2d(CUtensorMap* map, const void* base, uint64_t inner, uint64_t 
 // The KV pool as a 2-D tensor of 128-element bf16 rows (one row per (page,
 // head, slot)); 64 x 64 boxes with 128B swizzle are exactly the UMMA K-major
 // (K tiles) / MN-major (V tiles) canonical layouts.
+//
+// As a 3-D tensor {64 d, rows, 2 d-halves} (strides 256 B, 128 B) one box
+// {64, 64, 2} moves a whole 64-row block in the [d-half][row][64] layout K3
+// uses: one TMA instruction per K or V block instead of two.
 int encode_kv_map(CUtensorMap* map, const void* base, int64_t rows) {
-    return encode_bf16_2d(map, base, 128, uint64_t(rows), 64, 64);
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !f)
+            return fail(EP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(f);
+    }
+    const cuuint64_t dims[3] = {64, uint64_t(rows), 2};
+    const cuuint64_t strides[2] = {256, 128};
+    const cuuint32_t box[3] = {64, 64, 2};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(EP_ECUDA, "cuTensorMapEncodeTiled (KV, 3-D) failed: " + std::to_string(int(r)));
+    return EP_OK;
 }
 
 bool force_tc() {

@@ -243,8 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_arrive_expect_tx(&fullb[st], kBlkBytes);
                     const int row = int((int64_t(wk.cur.page) * Hkv + w.g) * P + wk.t0);
                     uint8_t* dst = ring + st * kBlkBytes;
-                    umma::tma_load_2d(dst, tm, 0, row, &fullb[st], pol);
-                    umma::tma_load_2d(dst + kKVHalf, tm, 64, row, &fullb[st], pol);
+                    umma::tma_load_3d(dst, tm, 0, row, 0, &fullb[st], pol);  // both d-halves
                 }
             }
         }
