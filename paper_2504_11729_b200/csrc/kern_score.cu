@@ -806,7 +806,10 @@ __global__ void __launch_bounds__(kSkThreads, 1)
             const uint32_t acc = tmem + uint32_t(slot * TN);
             if (sg.owner) {
                 // the other CTAs covering this tile: [cp0, c), each with its
-                // trailing partial segment on this tile
+                // trailing partial segment on this tile. An owner only waits
+                // for lower-indexed CTAs, which the hardware dispatches first,
+                // so the spin cannot wait on a CTA that is not resident (the
+                // grid is at most one CTA per SM).
                 const int cp0 = sg.k0 > 0 ? sk_cta_of((long long)sg.tile * sa.nkt, G, total) : c;
                 named_bar_sync(1, kSkEpiThreads);  // the previous scan is done with s_cs
                 const int ncols = min(TN, sa.vocab - n0);
