@@ -278,6 +278,8 @@ def main():
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("EP_TRACE_FILE") and world > 1:  # debug traces: one file per rank
+        os.environ["EP_TRACE_FILE"] = os.environ["EP_TRACE_FILE"] + f".r{local}"
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
