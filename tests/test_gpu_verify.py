@@ -310,3 +310,46 @@ def test_score_streamk_partition_shapes(cuda_handle, B, n_q, width, V):
     x2 = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32)
     tgt2, _, _ = ver(torch.from_numpy(x2).cuda().view(B, n_q, width), drafts)
     assert np.array_equal(tgt2.cpu().numpy(), _oracle_argmax(x2.astype(np.float64), O.bf16_to_f64(W)))
+
+
+@pytest.mark.parametrize("B,n_q", [(4, 3), (64, 9)])
+def test_score_bf16_rows_folded_ln(cuda_handle, B, n_q):
+    """bf16 attention rows (the prefill / bf16-output path of ep_verify_greedy):
+    one bf16 GEMM with LayerNorm folded into the epilogue (z = x.w - mean *
+    colsum(w)), no refinement, the acceptance rule in accept_kernel. Logits
+    (rstd * z) within a measured error of the fp64 LN(x) @ W; target ids
+    bit-exact on every row whose fp64 top-2 gap exceeds 8x that error, and
+    accepted counts bit-exact where no guarded row decides them
+    (model.cpp:238-255)."""
+    import torch
+    from paper_2504_11729_b200.verify import VerifyGreedy
+    from tests.gpu_util import torch_from_raw
+    width, V = 4096, 4096
+    rng = np.random.default_rng(B * 31 + n_q)
+    W = O.fill_uniform(O.DT_BF16, width * V, 555).reshape(width, V)
+    x = rng.uniform(-1.0, 1.0, size=(B, n_q, width)).astype(np.float32) + 0.25  # nonzero mean: the fold matters
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    x64 = xb.to(torch.float64).numpy()
+    W64 = O.bf16_to_f64(W)
+    g_ref, _, _ = O.verify_greedy(x64, W64, np.zeros((B, n_q - 1), np.int32))
+    drafts = g_ref[:, :n_q - 1].copy()
+    for b in range(B):
+        a = b % n_q
+        if a < n_q - 1:
+            drafts[b, a] = (g_ref[b, a] + 1) % V
+    g_ref, nacc_ref, _ = O.verify_greedy(x64, W64, drafts)
+    ver = VerifyGreedy(torch_from_raw(np.ascontiguousarray(W.T), O.DT_BF16), handle=cuda_handle)
+    tgt, nacc, lg = ver(xb.cuda().view(B, n_q, width), torch.from_numpy(drafts).cuda(), logits=True)
+    torch.cuda.synchronize()
+    tgt, nacc, lg = tgt.cpu().numpy(), nacc.cpu().numpy(), lg.cpu().numpy().reshape(B, n_q, V)
+    xn = (x64 - x64.mean(-1, keepdims=True)) / np.sqrt(x64.var(-1, keepdims=True) + 1e-5)
+    ref = xn @ W64
+    err = float(np.max(np.abs(lg - ref)))
+    assert err < 1e-2 * float(np.max(np.abs(ref)))
+    top2 = np.sort(ref, axis=-1)[..., -2:]
+    guarded = (top2[..., 1] - top2[..., 0]) < 8 * err
+    assert guarded.mean() < 0.2
+    assert np.array_equal(tgt[~guarded], g_ref[~guarded])
+    for b in range(B):
+        if not guarded[b, :min(nacc_ref[b] + 1, n_q - 1)].any():
+            assert nacc[b] == nacc_ref[b], (b, nacc[b], nacc_ref[b])
