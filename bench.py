@@ -366,7 +366,12 @@ def main():
     for b in range(B):
         for sg in table.requests[b]:
             cache.append(b, sg.origin, sg.pos_offset, sg.length, sg.pages)
+    # two plans of the same cache, used on alternate steps: step i's plan
+    # refresh and K/V append (side stream) then overlap step i-1's attention
+    # — the plan they patch was last read by step i-2, and the appended rows
+    # lie past every key step i-1 reads
     attn_e = SplicedAttention.from_cache(pool, cache, HQ, 1, handle=h)
+    attn_e2 = SplicedAttention.from_cache(pool, cache, HQ, 1, handle=h)
     # one pinned input blob per buffer j: [q | new K rows | new V rows | page | slot],
     # one H2D copy per step; copies and events through the CUDA runtime
     # directly (cuda.bindings), the library through its C-ABI (ctypes)
@@ -406,12 +411,17 @@ def main():
     ev_in = [mkev() for _ in range(2)]    # inputs of buffer j landed
     ev_done = [mkev() for _ in range(2)]  # attention on buffer j finished
     ev_out = [mkev() for _ in range(2)]   # output of buffer j read back
+    ev_prep = [mkev() for _ in range(2)]  # plan refresh + K/V append of buffer j done
     gen = {"len": 1}
-    plan, cptr = attn_e.plan, cache.ptr
+    trunc = [False, False]                # buffer j's token reused a truncated slot
+    plans, cptr = [attn_e.plan, attn_e2.plan], cache.ptr
+    side = torch.cuda.Stream()
+    ss = side.cuda_stream
 
     def grow(j):
         """This step's token per request: a slot in the cache (host) -> pinned blob j."""
-        if gen["len"] == P:
+        trunc[j] = gen["len"] == P
+        if trunc[j]:
             for b in range(B):
                 cache.truncate(b, P - 1)
             gen["len"] = 1
@@ -430,20 +440,28 @@ def main():
         h2d(0)
         for i in range(n):
             j = i & 1
-            _capi.check(lib.ep_plan_update_cache(plan, cptr, 0, 1, sp))  # the plan of the grown cache
+            # side stream: plans[j] (last read by step i-2's attention) follows
+            # the grown cache, then the step's K/V rows are written
+            rt.cudaStreamWaitEvent(ss, ev_done[j], 0)
+            _capi.check(lib.ep_plan_update_cache(plans[j], cptr, 0, 1, ss))
+            rt.cudaStreamWaitEvent(ss, ev_in[j], 0)
+            if trunc[j]:  # the token reuses a slot step i-1 may still read
+                rt.cudaStreamWaitEvent(ss, ev_done[j ^ 1], 0)
+            _capi.check(lib.ep_kv_append(h.ptr, pd_ref, B, *append_ptrs[j], ss))
+            rt.cudaEventRecord(ev_prep[j], ss)
             if i + 1 < n:
                 grow(j ^ 1)
                 h2d(j ^ 1)
-            rt.cudaStreamWaitEvent(sp, ev_in[j], 0)
+            rt.cudaStreamWaitEvent(sp, ev_prep[j], 0)
             rt.cudaStreamWaitEvent(sp, ev_out[j], 0)  # o_dev[j] of step i-2 has been read back
-            _capi.check(lib.ep_kv_append(h.ptr, pd_ref, B, *append_ptrs[j], sp))
-            _capi.check(lib.ep_spliced_attention(h.ptr, plan, pd_ref, _capi.EP_BF16, q_ptr[j], _capi.EP_BF16,
+            _capi.check(lib.ep_spliced_attention(h.ptr, plans[j], pd_ref, _capi.EP_BF16, q_ptr[j], _capi.EP_BF16,
                                                  o_ptr[j][0], lse.data_ptr(), sp))
             rt.cudaEventRecord(ev_done[j], sp)
             rt.cudaStreamWaitEvent(cs, ev_done[j], 0)
             rt.cudaMemcpyAsync(o_ptr[j][1], o_ptr[j][0], ob, D2H, cs)
             rt.cudaEventRecord(ev_out[j], cs)
         stream.wait_stream(copy)
+        stream.wait_stream(side)
 
     e2e_run(args.warmup)
     torch.cuda.synchronize()
@@ -475,13 +493,15 @@ def main():
         ms_e2e = float(t.item())
     # the last step's output equals a device-side recomputation on the same cache
     o_chk = torch.empty_like(o)
+    attn_e.update_from_cache(stream=stream)
     attn_e(q, o=o_chk, lse=lse, stream=stream)
     torch.cuda.synchronize()
     ok = bool(torch.equal(o_host[(args.steps - 1) & 1].to("cuda"), o_chk))
     keys_e2e = [cache.end_position(b) for b in range(B)]
     attn_e.close()
+    attn_e2.close()
     cache.close()
-    for ev in ev_in + ev_done + ev_out:
+    for ev in ev_in + ev_done + ev_out + ev_prep:
         rt.cudaEventDestroy(ev)
 
     tokens_per_step = B * world
@@ -523,7 +543,9 @@ def main():
                                 f"truncated back every {P - 1} steps; keys per request 4609..4672 "
                                 f"(last step {min(keys_e2e)}..{max(keys_e2e)})",
                 "overlap": "H2D of step i+1 and D2H of step i-1 on a copy stream "
-                           "(double-buffered) while step i computes"},
+                           "(double-buffered) while step i computes; step i's plan refresh and "
+                           "K/V append on a side stream during step i-1's attention (two plans "
+                           "of the cache, alternate steps)"},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
