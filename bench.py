@@ -379,25 +379,26 @@ def main():
     import ctypes as C
     qb, kvb, slb = q.numel() * 2, 2 * B * HKV * D * 2, 2 * B * 4
     in_bytes = qb + kvb + slb
-    host_in = [torch.empty(in_bytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
-    dev_in = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    NB = 4  # input / output buffers in flight: the host may run NB - 1 steps ahead
+    host_in = [torch.empty(in_bytes, dtype=torch.uint8).pin_memory() for _ in range(NB)]
+    dev_in = [torch.empty(in_bytes, dtype=torch.uint8, device="cuda") for _ in range(NB)]
     kv_rows = torch.empty((2, B, HKV, D), dtype=torch.bfloat16)
     kv_rows[0] = pool.k[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
     kv_rows[1] = pool.v[[b * PAGES_PER_REQ + PAGES_PER_REQ - 1 for b in range(B)], :, 0, :].cpu()
-    for j in range(2):
+    for j in range(NB):
         host_in[j][:qb].copy_(q.cpu().view(-1).view(torch.uint8))
         host_in[j][qb:qb + kvb].copy_(kv_rows.view(-1).view(torch.uint8))
-    slots_np = [host_in[j][qb + kvb:].numpy().view(np.int32).reshape(2, B) for j in range(2)]
-    o_host = [torch.empty_like(o, device="cpu").pin_memory() for _ in range(2)]
-    o_dev = [torch.empty_like(o) for _ in range(2)]
+    slots_np = [host_in[j][qb + kvb:].numpy().view(np.int32).reshape(2, B) for j in range(NB)]
+    o_host = [torch.empty_like(o, device="cpu").pin_memory() for _ in range(NB)]
+    o_dev = [torch.empty_like(o) for _ in range(NB)]
     ones = np.ones(B, np.int32)
     pd = pool.desc()
     pd_ref = C.byref(pd)
-    in_ptr = [(host_in[j].data_ptr(), dev_in[j].data_ptr()) for j in range(2)]
-    q_ptr = [dev_in[j].data_ptr() for j in range(2)]
+    in_ptr = [(host_in[j].data_ptr(), dev_in[j].data_ptr()) for j in range(NB)]
+    q_ptr = [dev_in[j].data_ptr() for j in range(NB)]
     append_ptrs = [(dev_in[j].data_ptr() + qb + kvb, dev_in[j].data_ptr() + qb + kvb + 4 * B,
-                    dev_in[j].data_ptr() + qb, dev_in[j].data_ptr() + qb + kvb // 2) for j in range(2)]
-    o_ptr = [(o_dev[j].data_ptr(), o_host[j].data_ptr()) for j in range(2)]
+                    dev_in[j].data_ptr() + qb, dev_in[j].data_ptr() + qb + kvb // 2) for j in range(NB)]
+    o_ptr = [(o_dev[j].data_ptr(), o_host[j].data_ptr()) for j in range(NB)]
     ob = o.numel() * 2
     copy = torch.cuda.Stream()
     cs = copy.cuda_stream
@@ -408,12 +409,12 @@ def main():
         assert err == rt.cudaError_t.cudaSuccess
         return ev
 
-    ev_in = [mkev() for _ in range(2)]    # inputs of buffer j landed
-    ev_done = [mkev() for _ in range(2)]  # attention on buffer j finished
-    ev_out = [mkev() for _ in range(2)]   # output of buffer j read back
-    ev_prep = [mkev() for _ in range(2)]  # plan refresh + K/V append of buffer j done
+    ev_in = [mkev() for _ in range(NB)]    # inputs of buffer j landed
+    ev_done = [mkev() for _ in range(NB)]  # attention on buffer j finished
+    ev_out = [mkev() for _ in range(NB)]   # output of buffer j read back
+    ev_prep = [mkev() for _ in range(NB)]  # plan refresh + K/V append of buffer j done
     gen = {"len": 1}
-    trunc = [False, False]                # buffer j's token reused a truncated slot
+    trunc = [False] * NB                   # buffer j's token reused a truncated slot
     plans, cptr = [attn_e.plan, attn_e2.plan], cache.ptr
     side = torch.cuda.Stream()
     ss = side.cuda_stream
@@ -435,27 +436,29 @@ def main():
         rt.cudaMemcpyAsync(in_ptr[j][1], in_ptr[j][0], in_bytes, H2D, cs)
         rt.cudaEventRecord(ev_in[j], cs)
 
+    # the cache grows in step order on the host: step i's token is appended
+    # (grow) before step i's plan refresh and after step i-1's
     def e2e_run(n):
         grow(0)
         h2d(0)
         for i in range(n):
-            j = i & 1
-            # side stream: plans[j] (last read by step i-2's attention) follows
-            # the grown cache, then the step's K/V rows are written
-            rt.cudaStreamWaitEvent(ss, ev_done[j], 0)
-            _capi.check(lib.ep_plan_update_cache(plans[j], cptr, 0, 1, ss))
+            j = i % NB
+            # side stream: plans[i % 2] (last read by step i-2's attention)
+            # follows the grown cache, then the step's K/V rows are written
+            rt.cudaStreamWaitEvent(ss, ev_done[(i - 2) % NB], 0)
+            _capi.check(lib.ep_plan_update_cache(plans[i & 1], cptr, 0, 1, ss))
             rt.cudaStreamWaitEvent(ss, ev_in[j], 0)
             if trunc[j]:  # the token reuses a slot step i-1 may still read
-                rt.cudaStreamWaitEvent(ss, ev_done[j ^ 1], 0)
+                rt.cudaStreamWaitEvent(ss, ev_done[(i - 1) % NB], 0)
             _capi.check(lib.ep_kv_append(h.ptr, pd_ref, B, *append_ptrs[j], ss))
             rt.cudaEventRecord(ev_prep[j], ss)
             if i + 1 < n:
-                grow(j ^ 1)
-                h2d(j ^ 1)
+                grow((i + 1) % NB)
+                h2d((i + 1) % NB)
             rt.cudaStreamWaitEvent(sp, ev_prep[j], 0)
-            rt.cudaStreamWaitEvent(sp, ev_out[j], 0)  # o_dev[j] of step i-2 has been read back
-            _capi.check(lib.ep_spliced_attention(h.ptr, plans[j], pd_ref, _capi.EP_BF16, q_ptr[j], _capi.EP_BF16,
-                                                 o_ptr[j][0], lse.data_ptr(), sp))
+            rt.cudaStreamWaitEvent(sp, ev_out[j], 0)  # o_dev[j] of step i-NB has been read back
+            _capi.check(lib.ep_spliced_attention(h.ptr, plans[i & 1], pd_ref, _capi.EP_BF16, q_ptr[j],
+                                                 _capi.EP_BF16, o_ptr[j][0], lse.data_ptr(), sp))
             rt.cudaEventRecord(ev_done[j], sp)
             rt.cudaStreamWaitEvent(cs, ev_done[j], 0)
             rt.cudaMemcpyAsync(o_ptr[j][1], o_ptr[j][0], ob, D2H, cs)
@@ -496,7 +499,7 @@ def main():
     attn_e.update_from_cache(stream=stream)
     attn_e(q, o=o_chk, lse=lse, stream=stream)
     torch.cuda.synchronize()
-    ok = bool(torch.equal(o_host[(args.steps - 1) & 1].to("cuda"), o_chk))
+    ok = bool(torch.equal(o_host[(args.steps - 1) % NB].to("cuda"), o_chk))
     keys_e2e = [cache.end_position(b) for b in range(B)]
     attn_e.close()
     attn_e2.close()
