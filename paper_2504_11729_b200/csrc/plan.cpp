@@ -168,7 +168,9 @@ void build_subplan(SubPlan& sp, const std::vector<VReq>& vr, int Hkv, int64_t ca
     // cumulative capacity ends of the CTAs (equal shares first)
     std::vector<int64_t> bnd(sp.n_ctas);
     for (int64_t c = 0; c < sp.n_ctas; ++c) bnd[c] = (total * (c + 1) + sp.n_ctas - 1) / sp.n_ctas;
-    for (int pass = 0; pass < (tail_pen > 0 && sp.n_ctas > 1 ? 2 : 1); ++pass) {
+    // (the re-cut only where a CTA's share is much larger than the penalty)
+    const bool recut = tail_pen > 0 && sp.n_ctas > 1 && total > 4 * tail_pen * sp.n_ctas;
+    for (int pass = 0; pass < (recut ? 2 : 1); ++pass) {
     if (pass == 1) {
         // CTAs without a whole unit: shorter shares
         std::vector<int> whole(sp.n_ctas, 0);
