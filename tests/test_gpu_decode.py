@@ -281,3 +281,57 @@ def test_cache_object_per_token_growth(cuda_handle):
             want_o, want_l = O.spliced_attention(hb, n_threads=4)
             _check(o, lse, want_o, want_l, sb.kv_dtype)
     assert cache.check_consistent() == ""
+
+
+def test_cache_two_plans_alternating(cuda_handle):
+    """The serving pattern of bench.py's e2e: two plans of one ep_cache used on
+    alternate steps, so each plan follows the cache two tokens at a time
+    (in-page growth through the device patch, a re-plan when a page fills,
+    a truncation in between); every checked step matches the oracle on the
+    cache's own pages."""
+    import ctypes as C
+    import torch
+    from paper_2504_11729_b200 import _capi
+    from paper_2504_11729_b200.splice import SpliceCache, SplicedAttention
+    sb = SC.make_case(O.DT_BF16, 8, 2, 128, [[(SC.CLOUD, 130, None), (SC.EDGE, 61, None)],
+                                              [(SC.EDGE, 7, None)]], seed=29, spare_pages=8)
+    pool, table, _, q = to_device(sb, cuda_handle)
+    cache = SpliceCache(1, table.batch, 64)
+    for b in range(table.batch):
+        for s in table.requests[b]:
+            cache.append(b, s.origin, s.pos_offset, s.length, s.pages)
+    used = set(sb.page_table.tolist())
+    free = [p for p in range(pool.num_pages) if p not in used]
+    plans = [SplicedAttention.from_cache(pool, cache, 8, 1, handle=cuda_handle) for _ in range(2)]
+    host_k, host_v = sb.k_pages.copy(), sb.v_pages.copy()
+    lib = _capi.lib()
+    pd = pool.desc()
+    for step in range(75):
+        newp = np.array([[free[0]], [free[1]]], np.int32)
+        dp, ds, nused = cache.append_generated([1, 1], newp)
+        taken = {int(newp[b, 0]) for b in range(2) if nused[b]}
+        free = [p for p in free if p not in taken]
+        kv = O.fill_uniform(O.DT_BF16, 2 * 2 * 2 * 128, 5000 + step).reshape(2, 2, 2, 128)
+        kd = torch_from_raw(np.ascontiguousarray(kv[0]), O.DT_BF16)
+        vd = torch_from_raw(np.ascontiguousarray(kv[1]), O.DT_BF16)
+        dpg = torch.from_numpy(dp.astype(np.int32)).cuda()
+        dsl = torch.from_numpy(ds.astype(np.int32)).cuda()
+        _capi.check(lib.ep_kv_append(cuda_handle.ptr, C.byref(pd), 2, dpg.data_ptr(), dsl.data_ptr(),
+                                     kd.data_ptr(), vd.data_ptr(), None), "ep_kv_append")
+        for b in range(2):
+            host_k[dp[b], :, ds[b]] = kv[0, b]
+            host_v[dp[b], :, ds[b]] = kv[1, b]
+        if step == 33:   # a rejected draft of 2 tokens on request 0
+            rel = cache.truncate(0, 2)
+            free = list(rel) + free
+        attn = plans[step & 1]
+        attn.update_from_cache()
+        o, lse = attn(q)
+        if step % 11 == 0 or step in (33, 34, 74):
+            indptr, segs, pt = cache.arrays(0)
+            qp = np.array([cache.end_position(b) - 1 for b in range(2)], np.int64)
+            hb = O.HostSpliceBatch(sb.kv_dtype, 2, 8, 128, 64, host_k, host_v, indptr, segs, pt,
+                                   qp, sb.q_dtype, sb.q, 1)
+            want_o, want_l = O.spliced_attention(hb, n_threads=4)
+            _check(o, lse, want_o, want_l, sb.kv_dtype)
+    assert cache.check_consistent() == ""
