@@ -262,7 +262,11 @@ int ep_verify_greedy(ep_handle h, ep_verifier v, int32_t batch, int32_t n_q, int
 /* Appends n_tok token rows per request into the pool (the device form of
  * SegmentedCache::append_generated_token, cache.cpp:55-80, without its
  * whole-segment copy). k_new/v_new: [n_rows][n_kv_heads][d_head] in the pool
- * dtype; row i goes to page dst_page[i], slot dst_slot[i] (device int32). */
+ * dtype; row i goes to page dst_page[i], slot dst_slot[i] (device int32).
+ * Stream-ordered; launched with programmatic dependent launch, so a caller's
+ * own PDL-launched successor kernel must execute griddepcontrol.wait before
+ * it reads the pool (ordinary launches and this library's kernels do). The
+ * same holds for the descriptor patch of ep_plan_update_cache. */
 int ep_kv_append(ep_handle h, const ep_kv_pool* pool, int32_t n_rows, const int32_t* dst_page,
                  const int32_t* dst_slot, const void* k_new, const void* v_new,
                  ep_stream stream);
