@@ -34,6 +34,20 @@ __device__ __forceinline__ uint16_t f64_to_bf16(double x) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
 }
 
+// Two values at once: fp64 -> fp32 round-to-odd each (exact double rounding,
+// as f64_to_bf16), then one packed RNE conversion; NaN -> 0x7FC0 like the
+// scalar rule (checked on the fp32 value: an fp64 NaN stays NaN).
+__device__ __forceinline__ uint32_t f64x2_to_bf16x2(double x0, double x1) {
+    float f0 = __double2float_rz(x0), f1 = __double2float_rz(x1);
+    if (double(f0) != x0) f0 = __uint_as_float(__float_as_uint(f0) | 1u);
+    if (double(f1) != x1) f1 = __uint_as_float(__float_as_uint(f1) | 1u);
+    const __nv_bfloat162 b = __floats2bfloat162_rn(f0, f1);
+    uint32_t w = *reinterpret_cast<const uint32_t*>(&b);
+    if (f0 != f0) w = (w & 0xFFFF0000u) | 0x7FC0u;
+    if (f1 != f1) w = (w & 0x0000FFFFu) | 0x7FC00000u;
+    return w;
+}
+
 __host__ __device__ inline uint32_t rd_u32(const uint8_t* b) {
     return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
 }
@@ -209,14 +223,18 @@ __global__ void __launch_bounds__(256) kv_ingest_kernel(const uint8_t* __restric
 // two aligned double2 (v[4j-1], v[4j]) and (v[4j+1], v[4j+2]) and takes v[4j+3]
 // from the next lane's first load; the last lane of the warp, or of the row,
 // reads it itself. Loops are warp-uniform so the full-mask shuffle is valid.
-template <bool BF16, bool MIS8>
+// DQ: d_head / 4 at compile time (16 / 32; 0 = a runtime d_quads), so the
+// head split of a quad is a shift and its store address one multiply-add
+// from the row's base.
+template <bool BF16, bool MIS8, int DQ>
 __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __restrict__ src, uint32_t rows,
-                                                             uint32_t seq, uint32_t row_quads, uint32_t d_quads,
+                                                             uint32_t seq, uint32_t row_quads, uint32_t d_quads_rt,
                                                              uint32_t P, uint32_t H,
                                                              const int32_t* __restrict__ page_table,
                                                              void* __restrict__ kp, void* __restrict__ vp,
                                                              const HdrCheck chk) {
     if (!header_ok(chk)) return;
+    const uint32_t d_quads = DQ > 0 ? uint32_t(DQ) : d_quads_rt;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t span = (row_quads + 31) & ~31u;
     for (uint32_t row = blockIdx.x; row < rows; row += gridDim.x) {
@@ -224,6 +242,8 @@ __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __re
         const uint32_t t = is_v ? row - seq : row;
         const size_t page = size_t(page_table[t / P]), slot = t % P;
         const uint8_t* rp = src + size_t(row) * row_quads * 32;
+        const size_t row_base = (page * H * P + slot) * d_quads;  // quad index of head 0
+        const size_t head_step = size_t(P) * d_quads;
         for (uint32_t j0 = threadIdx.x & ~31u; j0 < span; j0 += blockDim.x) {
             const uint32_t j = j0 + lane;
             const bool live = j < row_quads;
@@ -243,10 +263,9 @@ __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __re
             }
             if (!live) continue;
             const uint32_t h = j / d_quads, cq = j - h * d_quads;
-            const size_t dst = ((page * H + h) * P + slot) * d_quads + cq;  // in quads
+            const size_t dst = row_base + h * head_step + cq;  // in quads
             if (BF16) {
-                const uint2 w = make_uint2(uint32_t(f64_to_bf16(v0)) | (uint32_t(f64_to_bf16(v1)) << 16),
-                                           uint32_t(f64_to_bf16(v2)) | (uint32_t(f64_to_bf16(v3)) << 16));
+                const uint2 w = make_uint2(f64x2_to_bf16x2(v0, v1), f64x2_to_bf16x2(v2, v3));
                 static_cast<uint2*>(is_v ? vp : kp)[dst] = w;
             } else {
                 static_cast<float4*>(is_v ? vp : kp)[dst] = make_float4(
@@ -293,14 +312,21 @@ int launch_ingest(ep_context* h, const ep_kv_pool* pool, uint32_t seq_len, uint3
         const uint32_t row_quads = n_heads * d_quads;
         const uint32_t tpb = row_quads >= 256 ? 256 : ((row_quads + 31) & ~31u);
         const uint32_t grid = std::min<uint32_t>(rows, uint32_t(h->n_sms) * (2048 / tpb));
-#define EP_INGEST_ROWS(BF, M8)                                                                           \
-    ep::kv_ingest_rows_kernel<BF, M8><<<grid, tpb, 0, s>>>(src, rows, seq_len, row_quads, d_quads, P, H, \
-                                                           page_table, pool->k_pages, pool->v_pages, chk)
+#define EP_INGEST_ROWS(BF, M8, DQ)                                                                          \
+    ep::kv_ingest_rows_kernel<BF, M8, DQ><<<grid, tpb, 0, s>>>(src, rows, seq_len, row_quads, d_quads, P, H, \
+                                                               page_table, pool->k_pages, pool->v_pages, chk)
+#define EP_INGEST_ROWS_DQ(BF, M8)                                      \
+    do {                                                               \
+        if (d_quads == 32) EP_INGEST_ROWS(BF, M8, 32);                 \
+        else if (d_quads == 16) EP_INGEST_ROWS(BF, M8, 16);            \
+        else EP_INGEST_ROWS(BF, M8, 0);                                \
+    } while (0)
         if (pool->dtype == EP_BF16) {
-            if (mis) EP_INGEST_ROWS(true, true); else EP_INGEST_ROWS(true, false);
+            if (mis) EP_INGEST_ROWS_DQ(true, true); else EP_INGEST_ROWS_DQ(true, false);
         } else {
-            if (mis) EP_INGEST_ROWS(false, true); else EP_INGEST_ROWS(false, false);
+            if (mis) EP_INGEST_ROWS_DQ(false, true); else EP_INGEST_ROWS_DQ(false, false);
         }
+#undef EP_INGEST_ROWS_DQ
 #undef EP_INGEST_ROWS
     } else {
         const uint32_t total = 2 * n_pairs;
