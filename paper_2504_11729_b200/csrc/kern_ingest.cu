@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256) kv_ingest_kernel(const uint8_t* __restric
 template <bool BF16, bool MIS8, int DQ>
 __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __restrict__ src, uint32_t rows,
                                                              uint32_t seq, uint32_t row_quads, uint32_t d_quads_rt,
-                                                             uint32_t P, uint32_t H,
+                                                             uint32_t P, int p_shift, uint32_t H,
                                                              const int32_t* __restrict__ page_table,
                                                              void* __restrict__ kp, void* __restrict__ vp,
                                                              const HdrCheck chk) {
@@ -240,7 +240,9 @@ __global__ void __launch_bounds__(256) kv_ingest_rows_kernel(const uint8_t* __re
     for (uint32_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const bool is_v = row >= seq;
         const uint32_t t = is_v ? row - seq : row;
-        const size_t page = size_t(page_table[t / P]), slot = t % P;
+        // page / slot of token t (a shift for the usual power-of-two pages)
+        const uint32_t pg = p_shift >= 0 ? t >> p_shift : t / P;
+        const size_t page = size_t(page_table[pg]), slot = t - pg * P;
         const uint8_t* rp = src + size_t(row) * row_quads * 32;
         const size_t row_base = (page * H * P + slot) * d_quads;  // quad index of head 0
         const size_t head_step = size_t(P) * d_quads;
@@ -312,8 +314,12 @@ int launch_ingest(ep_context* h, const ep_kv_pool* pool, uint32_t seq_len, uint3
         const uint32_t row_quads = n_heads * d_quads;
         const uint32_t tpb = row_quads >= 256 ? 256 : ((row_quads + 31) & ~31u);
         const uint32_t grid = std::min<uint32_t>(rows, uint32_t(h->n_sms) * (2048 / tpb));
+        int p_shift = -1;
+        if ((P & (P - 1)) == 0)
+            for (p_shift = 0; (1u << p_shift) < P; ++p_shift) {
+            }
 #define EP_INGEST_ROWS(BF, M8, DQ)                                                                          \
-    ep::kv_ingest_rows_kernel<BF, M8, DQ><<<grid, tpb, 0, s>>>(src, rows, seq_len, row_quads, d_quads, P, H, \
+    ep::kv_ingest_rows_kernel<BF, M8, DQ><<<grid, tpb, 0, s>>>(src, rows, seq_len, row_quads, d_quads, P, p_shift, H, \
                                                                page_table, pool->k_pages, pool->v_pages, chk)
 #define EP_INGEST_ROWS_DQ(BF, M8)                                      \
     do {                                                               \
