@@ -455,9 +455,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
 
                 if (!(nv == kBT && pos + kBT - 1 <= q0)) {
+                    // keys j < lim are valid and visible: one 32-bit compare per key
+                    const int64_t vis = my_qpos - pos + 1;
+                    const int lim = vis < 0 ? 0 : int(vis < int64_t(nv) ? vis : int64_t(nv));
 #pragma unroll
                     for (int j = 0; j < 64; ++j)
-                        if (!(j < nv && pos + j <= my_qpos)) sr[j] = __float_as_uint(-INFINITY);
+                        if (j >= lim) sr[j] = __float_as_uint(-INFINITY);
                 }
                 // row max: 8 independent chains of 3-input maxima (FMNMX3),
                 // then a 3-input tree
