@@ -375,6 +375,33 @@ __global__ void cascade_merge_kernel(int rows, int d, int row_per_req, const flo
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
     const bool sh = has_shared[row / row_per_req] != 0;
+    if (d == 128) {
+        // one float4 of each part per lane, loaded with the lse values (one
+        // round trip); an empty part's garbage is discarded by the select
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(po + size_t(row) * d) + lane);
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(po + (size_t(rows) + row) * d) + lane);
+        const float l0 = sh ? pl[row] : -INFINITY, l1 = pl[rows + row];
+        const float M = fmaxf(l0, l1);
+        const float w0 = (M == -INFINITY || l0 == -INFINITY) ? 0.f : expf(l0 - M);
+        const float w1 = (M == -INFINITY || l1 == -INFINITY) ? 0.f : expf(l1 - M);
+        const float L = w0 + w1;
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        const float c0 = w0 * inv, c1 = w1 * inv;
+        float v[4] = {a.x, a.y, a.z, a.w}, u[4] = {b.x, b.y, b.z, b.w}, r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = (w0 > 0.f ? v[k] * c0 : 0.f) + (w1 > 0.f ? u[k] * c1 : 0.f);
+        if (o_dtype == EP_BF16) {
+            const __nv_bfloat162 p0 = __floats2bfloat162_rn(r[0], r[1]), p1 = __floats2bfloat162_rn(r[2], r[3]);
+            uint2 w;
+            w.x = *reinterpret_cast<const uint32_t*>(&p0);
+            w.y = *reinterpret_cast<const uint32_t*>(&p1);
+            reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(o) + size_t(row) * d)[lane] = w;
+        } else {
+            reinterpret_cast<float4*>(static_cast<float*>(o) + size_t(row) * d)[lane] = make_float4(r[0], r[1], r[2], r[3]);
+        }
+        if (lane == 0 && lse) lse[row] = L > 0.f ? M + logf(L) : -INFINITY;
+        return;
+    }
     const float l0 = sh ? pl[row] : -INFINITY, l1 = pl[rows + row];
     const float M = fmaxf(l0, l1);
     const float w0 = (M == -INFINITY || l0 == -INFINITY) ? 0.f : expf(l0 - M);
