@@ -568,7 +568,11 @@ def main():
                       f"{units} units in {secs:.1f} s), reference attention block in fp64 "
                       "(oracle/_ref, unmodified reference sources)"}
     if not args.no_extras:
-        line.update(run_extras(args, world, rank, h))
+        extras = run_extras(args, world, rank, h)
+        line.update(extras)
+        # the other configs' headline numbers, early in the line (a record
+        # that keeps only part of a long line still shows them)
+        line = summary_first(line, extras)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -759,6 +763,33 @@ def cfg2_replicas(args, world, rank, local_rank, h):
     ms = float(t.item())
     return {"workload": WORKLOAD + f", one batch per GPU (x{world})", "ms_per_step": ms,
             "tokens_per_s": B * world / (ms / 1e3), "scaling": "weak"}
+
+
+def summary_first(line, ex):
+    """The line with a compact `summary` of the extras placed after `config`."""
+    sm = {}
+    try:
+        if "verify_p50_ms" in ex:
+            sm["cfg3_verify_p50_ms"] = {k: round(v, 4) for k, v in ex["verify_p50_ms"].items()}
+        if "multitenant" in ex:
+            sm["cfg5_ms_per_step"] = round(ex["multitenant"]["ms_per_step"], 4)
+            sm["cfg5_unique_gbs"] = round(ex["multitenant"]["unique_gbs"])
+        if "splitkv" in ex:
+            sm["cfg4_1gpu_step_ms"] = {k: round(v["step_ms"], 4) for k, v in ex["splitkv"].items()
+                                       if isinstance(v, dict) and "step_ms" in v}
+        if "prefill" in ex:
+            sm["prefill_ms"] = {k: round(v["ms"], 4) for k, v in ex["prefill"].items()}
+            sm["prefill_tflops"] = {k: round(v["tflops"]) for k, v in ex["prefill"].items()}
+        if "ingest" in ex and "device_async" in ex["ingest"]:
+            sm["ingest_device_frame_us"] = round(ex["ingest"]["device_async"]["ms"] * 1e3, 2)
+    except (KeyError, TypeError):
+        pass
+    out = {}
+    for k, v in line.items():
+        out[k] = v
+        if k == "config":
+            out["summary"] = sm
+    return out
 
 
 def run_extras(args, world, rank, h):
