@@ -789,6 +789,7 @@ def summary_first(line, ex):
         out[k] = v
         if k == "config":
             out["summary"] = sm
+    out["summary_end"] = sm  # and at the end, for records that keep a line's tail
     return out
 
 
