@@ -335,3 +335,26 @@ def test_cache_two_plans_alternating(cuda_handle):
             want_o, want_l = O.spliced_attention(hb, n_threads=4)
             _check(o, lse, want_o, want_l, sb.kv_dtype)
     assert cache.check_consistent() == ""
+
+
+@pytest.mark.parametrize("P", [128, 192])
+@pytest.mark.parametrize("kind", ["decode", "verify", "shared"])
+def test_page_sizes_beyond_64(cuda_handle, P, kind):
+    """Pages of 128 and 192 tokens (any multiple of 64 is legal, ep_plan
+    splits them into 64-token pipeline blocks): K1 decode, K3 verify rows
+    (n_q = 5) and the config-5 cascade (a cloud segment shared by every
+    request), with ragged segment tails inside the larger pages; vs the oracle."""
+    Hq, Hkv, d = 32, 8, 128
+    n_q = 5 if kind == "verify" else 1
+    r = O.SplitMix64(P + len(kind))
+    if kind == "shared":
+        reqs = [[(SC.CLOUD, 1000, "cloud"), (SC.EDGE, 40 + r.next_u64() % 300, None), (SC.GEN, 1, None)]
+                for _ in range(40)]
+    else:
+        reqs = [[(SC.CLOUD, 300 + r.next_u64() % 700, None), (SC.EDGE, 1 + r.next_u64() % 250, None),
+                 (SC.GEN, n_q, None)] for _ in range(6)]
+    sb = SC.make_case(O.DT_BF16, Hq, Hkv, d, reqs, n_q=n_q, page_tokens=P, seed=70 + P)
+    _, _, attn, q = to_device(sb, cuda_handle)
+    o, lse = attn(q)
+    want_o, want_l = O.spliced_attention(sb, n_threads=os.cpu_count() or 4)
+    _check(o, lse, want_o, want_l, sb.kv_dtype)
