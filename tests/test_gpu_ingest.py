@@ -258,3 +258,30 @@ def test_ingest_async_device_frames(cuda_handle, offset):
     # a length that does not fit the pool shape fails immediately
     with pytest.raises(WireError):
         pool.ingest_frame_async(dev(fr[:-1].copy()), pages, handle=cuda_handle)
+
+
+@pytest.mark.parametrize("P", [64, 128, 192])
+@pytest.mark.parametrize("shape", [(8, 128), (4, 64)])
+@pytest.mark.parametrize("offset", [0, 8])
+def test_ingest_page_sizes(cuda_handle, P, shape, offset):
+    """The row kernel's compile-time quad splits (d_head 128 -> 32 quads,
+    64 -> 16) and its page index by shift (64, 128) or division (192 tokens
+    per page), bf16 pages: bit-exact vs the C oracle's decode + round + scatter."""
+    import torch
+    from paper_2504_11729_b200.splice import KVPool
+    H, d = shape
+    seq = 2 * P + 37  # a partial last page
+    fr = _frame(seq, H, d, seed=P + d, specials=True)
+    buf = torch.zeros(fr.size + 16, dtype=torch.uint8, device="cuda")
+    buf[offset:offset + fr.size].copy_(torch.from_numpy(fr))
+    pages = np.array([3, 0, 2], dtype=np.int32)
+    pool = KVPool(4, H, d, P, dtype="bf16")
+    pool.ingest_frame(buf[offset:offset + fr.size], pages, handle=cuda_handle)
+    torch.cuda.synchronize()
+    code, _, want_k, want_v = O.kv_ingest(fr, O.DT_BF16, P, pages, 4)
+    assert code == O.WIRE_OK
+    got_k = pool.k.view(torch.int16).cpu().numpy().view(np.uint16)
+    got_v = pool.v.view(torch.int16).cpu().numpy().view(np.uint16)
+    for p in pages:
+        assert np.array_equal(got_k[p].view(np.uint8), want_k[p].view(np.uint8)), p
+        assert np.array_equal(got_v[p].view(np.uint8), want_v[p].view(np.uint8)), p
