@@ -60,13 +60,14 @@ def _oracle(sb, q, n_new):
     return np.concatenate(outs), np.concatenate(lses)
 
 
+@pytest.mark.parametrize("page_tokens", [64, 192])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_prefill_matches_oracle(cuda_handle, name):
+def test_prefill_matches_oracle(cuda_handle, name, page_tokens):
     import torch
     from paper_2504_11729_b200.splice import SplicedPrefill
     cfg = CASES[name]
     sb = SC.make_case(O.DT_BF16, cfg["n_q_heads"], cfg["n_kv_heads"], 128, cfg["requests"],
-                      n_q=1, seed=11)
+                      n_q=1, page_tokens=page_tokens, seed=11)
     T = sum(cfg["n_new"])
     q_raw = O.fill_uniform(O.DT_BF16, T * cfg["n_q_heads"] * 128, 11_009).reshape(
         T, cfg["n_q_heads"], 128)
